@@ -1,0 +1,109 @@
+/* nmx.h -- C ABI of libnmx.so, the B200 (sm_100a) traffic-matrix hot path.
+ *
+ * The reference (`netmeter`, /root/reference/pkg/src/netmeter) is pure Python
+ * + numpy and has no FFI; the Python package paper_2510_14050_b200 binds these
+ * entry points with ctypes and re-exposes the reference's own function names.
+ * Each entry cites the reference interface it replaces.
+ *
+ * Conventions
+ *   - every function returns an int status: NMX_OK (0) or a negative code;
+ *     nmx_last_error() returns the calling thread's message for the last failure;
+ *   - no CUDA or torch types: device pointers are plain pointers obtained from
+ *     nmx_malloc (or any cudaMalloc'd memory of the context's device);
+ *   - addresses are uint32 (the reference's 9-byte packet record already limits
+ *     them to 32 bits, traffic.py:25,370-372); `address_space` is 1..2^32;
+ *   - a `valid` column is optional (NULL = all valid), one byte per packet,
+ *     nonzero = valid (traffic.py:43-51);
+ *   - statistics are int64 in this order (the "stats9" layout):
+ *       0 valid_packets        1 unique_links        2 max_link_packets
+ *       3 unique_sources       4 max_source_packets  5 max_fanout
+ *       6 unique_destinations  7 max_destination_packets  8 max_fanin
+ *     (analytics.py:31-40 AggregateReport + the three Graph Challenge maxima);
+ *   - one context = one device + one CUDA stream; calls on one context are
+ *     serialised by an internal lock, so a context may be shared by threads
+ *     (tests/test_analytics.py:178-194).
+ */
+#ifndef NMX_H
+#define NMX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NMX_OK 0
+#define NMX_EINVAL -1  /* maps to ValueError / TypeError in Python */
+#define NMX_ENOMEM -2  /* device or pinned-host allocation failed  */
+#define NMX_ECUDA -3   /* CUDA runtime / kernel error              */
+#define NMX_ENODEV -4  /* no CUDA device                           */
+
+#define NMX_GEN_UNIFORM 0  /* SURVEY.md 8(d) cfg3 generator */
+#define NMX_GEN_POWERLAW 1 /* SURVEY.md 8(d) cfg4 "octave" generator */
+
+#define NMX_REDUCE_SUM 0 /* analytics.py:84-86 sum_reduce (int64 wrap) */
+#define NMX_REDUCE_MAX 1 /* analytics.py:89-92 max_scan (INT64_MIN sentinel -> 0) */
+
+typedef struct nmx_ctx nmx_ctx;
+typedef struct nmx_coo nmx_coo;
+
+int nmx_version(void);
+const char* nmx_last_error(void);
+int nmx_device_count(int* count);
+
+/* Execution resource: replaces one member pool of make_group_scheduler
+ * (resources.py:139-159); resource_count == number of contexts. */
+int nmx_create(int device, nmx_ctx** out);
+void nmx_destroy(nmx_ctx* ctx);
+/* the context's cudaStream_t, as an opaque pointer (for interop only) */
+void* nmx_stream(nmx_ctx* ctx);
+int nmx_synchronize(nmx_ctx* ctx);
+
+/* device / pinned memory owned by the caller */
+int nmx_malloc(nmx_ctx* ctx, uint64_t bytes, void** dptr);
+int nmx_free(nmx_ctx* ctx, void* dptr);
+int nmx_host_alloc(uint64_t bytes, void** hptr);
+int nmx_host_free(void* hptr);
+int nmx_memcpy_h2d(nmx_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+int nmx_memcpy_d2h(nmx_ctx* ctx, void* dst, const void* src, uint64_t bytes);
+
+/* Synthetic packets i in [offset, offset+n) of stream `seed` into device
+ * columns; chunk-addressable. Same integer function as oracle/netmeter_oracle.py
+ * gen_uniform / gen_powerlaw. (Input preparation, cf. traffic.py:82-104.) */
+int nmx_generate(nmx_ctx* ctx, int kind, uint64_t seed, uint64_t offset, uint64_t n, uint64_t address_space,
+                 uint32_t* d_src, uint32_t* d_dst);
+
+/* THE HOT PATH. Nine statistics of the traffic matrix summed over all valid
+ * packets, i.e. build_matrices(stream, window_size=len(stream)) (traffic.py:221-242)
+ * -> to_flat (traffic.py:263-292) -> analyze_matrix (analytics.py:95-106)
+ * + max_scan over weights / row_sums[:,1] / col_sums[:,1] (analytics.py:89-92).
+ * Device-resident columns; n < 2^32 per call. */
+int nmx_stats9_device(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                      uint64_t address_space, int64_t out[9]);
+/* Same, from host columns (copied H2D inside the call; pinned memory is fastest). */
+int nmx_stats9_host(nmx_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                    uint64_t address_space, int64_t out[9]);
+
+/* Per-window statistics: window t = packets [t*W, (t+1)*W) by raw position,
+ * invalid packets keep their position (traffic.py:221-242); out has
+ * ceil(n/W) rows of 9 (analyze_dataset per-window reports, analytics.py:109-130). */
+int nmx_window_stats9_device(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                             uint64_t n, uint64_t address_space, uint64_t window_size, int64_t* out);
+int nmx_window_stats9_host(nmx_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                           uint64_t address_space, uint64_t window_size, int64_t* out);
+
+/* Reductions of the drop-in sum_reduce / max_scan (analytics.py:54-92) over a
+ * host int64 view: op NMX_REDUCE_SUM wraps mod 2^64; NMX_REDUCE_MAX returns
+ * INT64_MIN for an empty view (the Python layer maps it to 0). */
+int nmx_reduce_i64(nmx_ctx* ctx, const int64_t* data, uint64_t n, int op, int64_t* out);
+
+/* Timing hooks used by bench.py: CUDA-event time (ms) of the last hot-path
+ * call's whole device section, and of its dominant kernel class (the onesweep
+ * passes) summed over launches, plus the number of kernels it launched. */
+int nmx_last_timing(nmx_ctx* ctx, float* total_ms, float* sort_ms, int* sort_launches, int* kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NMX_H */

@@ -1,0 +1,304 @@
+"""ctypes binding of libnmx.so (include/nmx.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is visible, every compute entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libnmx.so"
+
+NMX_OK = 0
+NMX_EINVAL = -1
+NMX_ENOMEM = -2
+NMX_ECUDA = -3
+NMX_ENODEV = -4
+
+GEN_UNIFORM = 0
+GEN_POWERLAW = 1
+REDUCE_SUM = 0
+REDUCE_MAX = 1
+
+# Every symbol include/nmx.h declares, with its ctypes signature.
+_VP = C.c_void_p
+_U64 = C.c_uint64
+SIGNATURES = {
+    "nmx_version": (C.c_int, []),
+    "nmx_last_error": (C.c_char_p, []),
+    "nmx_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "nmx_create": (C.c_int, [C.c_int, C.POINTER(_VP)]),
+    "nmx_destroy": (None, [_VP]),
+    "nmx_stream": (_VP, [_VP]),
+    "nmx_synchronize": (C.c_int, [_VP]),
+    "nmx_malloc": (C.c_int, [_VP, _U64, C.POINTER(_VP)]),
+    "nmx_free": (C.c_int, [_VP, _VP]),
+    "nmx_host_alloc": (C.c_int, [_U64, C.POINTER(_VP)]),
+    "nmx_host_free": (C.c_int, [_VP]),
+    "nmx_memcpy_h2d": (C.c_int, [_VP, _VP, _VP, _U64]),
+    "nmx_memcpy_d2h": (C.c_int, [_VP, _VP, _VP, _U64]),
+    "nmx_generate": (C.c_int, [_VP, C.c_int, _U64, _U64, _U64, _U64, _VP, _VP]),
+    "nmx_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
+    "nmx_window_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
+    "nmx_reduce_i64": (C.c_int, [_VP, _VP, _U64, C.c_int, _VP]),
+    "nmx_last_timing": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int)]),
+}
+
+
+class NativeUnavailable(RuntimeError):
+    """libnmx.so is not built or no CUDA device is visible (there is no CPU fallback)."""
+
+
+class NmxError(RuntimeError):
+    """A CUDA or allocation failure inside libnmx.so."""
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load libnmx.so and bind every declared symbol (no device needed)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise NativeUnavailable(f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc == NMX_OK:
+        return
+    msg = (load().nmx_last_error() or b"").decode(errors="replace")
+    if rc == NMX_EINVAL:
+        raise ValueError(msg)
+    if rc == NMX_ENODEV:
+        raise NativeUnavailable(msg)
+    raise NmxError(f"libnmx error {rc}: {msg}")
+
+
+class Context:
+    """One device + one CUDA stream (include/nmx.h nmx_ctx)."""
+
+    def __init__(self, device: int = 0):
+        lib = load()
+        h = C.c_void_p()
+        check(lib.nmx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = int(device)
+        self._lib = lib
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if self._h:
+            self._lib.nmx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return self._lib.nmx_stream(self._h) or 0
+
+    def last_timing(self):
+        t, s = C.c_float(), C.c_float()
+        sl, kl = C.c_int(), C.c_int()
+        check(self._lib.nmx_last_timing(self._h, C.byref(t), C.byref(s), C.byref(sl), C.byref(kl)))
+        return dict(total_ms=t.value, sort_ms=s.value, sort_launches=sl.value, kernel_launches=kl.value)
+
+
+_contexts: dict[int, Context] = {}
+_ctx_lock = threading.Lock()
+
+
+def context(device: int = 0) -> Context:
+    """Process-wide cached context per device."""
+    with _ctx_lock:
+        c = _contexts.get(device)
+        if c is None:
+            c = Context(device)
+            _contexts[device] = c
+        return c
+
+
+def device_count() -> int:
+    lib = load()
+    n = C.c_int(0)
+    rc = lib.nmx_device_count(C.byref(n))
+    return n.value if rc == NMX_OK else 0
+
+
+def _ptr(a) -> int:
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return int(a.data_ptr())  # torch tensor (device or pinned host)
+
+
+def _u32_host(a) -> np.ndarray:
+    a = np.asarray(a)
+    if a.dtype == np.uint32 and a.flags.c_contiguous:
+        return a
+    if a.size and (a.min() < 0 or a.max() > 0xFFFFFFFF):
+        raise ValueError("addresses must lie in [0, 2^32)")
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def _valid_host(v):
+    if v is None:
+        return None
+    v = np.asarray(v)
+    if v.dtype == np.bool_ or v.dtype == np.uint8:
+        return np.ascontiguousarray(v).view(np.uint8)
+    return np.ascontiguousarray(v != 0).view(np.uint8)
+
+
+def _is_device(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def stats9(src, dst, valid=None, address_space: int = 1 << 32, device: int = 0) -> tuple:
+    """Nine statistics of the summed traffic matrix (nmx_stats9_{host,device}).
+
+    ``src``/``dst``: numpy arrays (host) or CUDA uint32/int32 tensors (device).
+    """
+    ctx = context(device)
+    out = np.zeros(9, dtype=np.int64)
+    if _is_device(src):
+        n = int(src.numel())
+        check(ctx._lib.nmx_stats9_device(ctx.handle, _ptr(src), _ptr(dst), _ptr(valid), n, int(address_space),
+                                         out.ctypes.data))
+    else:
+        s, d, v = _u32_host(src), _u32_host(dst), _valid_host(valid)
+        if len(s) != len(d) or (v is not None and len(v) != len(s)):
+            raise ValueError("src, dst and valid must have equal lengths")
+        check(ctx._lib.nmx_stats9_host(ctx.handle, _ptr(s), _ptr(d), _ptr(v), len(s), int(address_space),
+                                       out.ctypes.data))
+    return tuple(int(x) for x in out)
+
+
+def window_stats9(src, dst, valid, address_space: int, window_size: int, device: int = 0) -> np.ndarray:
+    """Per-window nine statistics, shape (ceil(n/W), 9) int64."""
+    ctx = context(device)
+    if _is_device(src):
+        n = int(src.numel())
+    else:
+        src, dst, valid = _u32_host(src), _u32_host(dst), _valid_host(valid)
+        n = len(src)
+    nw = (n + window_size - 1) // window_size if window_size >= 1 else 0
+    out = np.zeros((max(nw, 0), 9), dtype=np.int64)
+    fn = ctx._lib.nmx_window_stats9_device if _is_device(src) else ctx._lib.nmx_window_stats9_host
+    check(fn(ctx.handle, _ptr(src), _ptr(dst), _ptr(valid), n, int(address_space), int(window_size),
+             out.ctypes.data if nw else 0))
+    return out
+
+
+def reduce_i64(data: np.ndarray, op: int, device: int = 0) -> int:
+    ctx = context(device)
+    a = np.ascontiguousarray(data, dtype=np.int64)
+    out = np.zeros(1, dtype=np.int64)
+    check(ctx._lib.nmx_reduce_i64(ctx.handle, _ptr(a), len(a), int(op), out.ctypes.data))
+    return int(out[0])
+
+
+def generate(kind: int, seed: int, offset: int, n: int, address_space: int, d_src, d_dst, device: int = 0) -> None:
+    ctx = context(device)
+    check(ctx._lib.nmx_generate(ctx.handle, int(kind), int(seed), int(offset), int(n), int(address_space),
+                                _ptr(d_src), _ptr(d_dst)))
+
+
+class DeviceArray:
+    """Device memory from nmx_malloc, freed on close/GC. Quacks like a CUDA
+    tensor for the entry points above (data_ptr / numel / is_cuda)."""
+
+    is_cuda = True
+
+    def __init__(self, n: int, itemsize: int = 4, device: int = 0):
+        self.ctx = context(device)
+        self.n = int(n)
+        self.itemsize = itemsize
+        p = C.c_void_p()
+        check(self.ctx._lib.nmx_malloc(self.ctx.handle, max(self.n * itemsize, 1), C.byref(p)))
+        self._p = p
+
+    def data_ptr(self) -> int:
+        return self._p.value or 0
+
+    def numel(self) -> int:
+        return self.n
+
+    def upload(self, host: np.ndarray) -> "DeviceArray":
+        host = np.ascontiguousarray(host)
+        if host.nbytes > self.n * self.itemsize:
+            raise ValueError("host array larger than device buffer")
+        check(self.ctx._lib.nmx_memcpy_h2d(self.ctx.handle, self._p, host.ctypes.data, host.nbytes))
+        return self
+
+    def download(self, dtype=np.uint32) -> np.ndarray:
+        out = np.empty(self.n * self.itemsize // np.dtype(dtype).itemsize, dtype=dtype)
+        check(self.ctx._lib.nmx_memcpy_d2h(self.ctx.handle, out.ctypes.data, self._p, out.nbytes))
+        return out
+
+    def close(self) -> None:
+        if self._p:
+            self.ctx._lib.nmx_free(self.ctx.handle, self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PinnedArray:
+    """Page-locked host buffer (nmx_host_alloc) viewed as a numpy array."""
+
+    def __init__(self, n: int, dtype=np.uint32):
+        dt = np.dtype(dtype)
+        self._lib = load()
+        p = C.c_void_p()
+        check(self._lib.nmx_host_alloc(max(n * dt.itemsize, 1), C.byref(p)))
+        self._p = p
+        buf = (C.c_char * max(n * dt.itemsize, 1)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dt, count=n)
+
+    def close(self) -> None:
+        if self._p:
+            self.array = None
+            self._lib.nmx_host_free(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,619 @@
+// nmx_api.cu -- context, workspace and the C ABI of libnmx.so (include/nmx.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/nmx.h"
+#include "nmx_kernels.cuh"
+
+using namespace nmx;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+struct CudaError {
+  cudaError_t e;
+  const char* what;
+  int line;
+};
+
+#define CK(x)                                              \
+  do {                                                     \
+    cudaError_t e_ = (x);                                  \
+    if (e_ != cudaSuccess) throw CudaError{e_, #x, __LINE__}; \
+  } while (0)
+#define CK_LAUNCH() CK(cudaGetLastError())
+
+constexpr int kIPT = 16;
+constexpr int kTile = kThreads * kIPT;  // 4096 items per tile
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  // grow (never shrinks); returns true when (re)allocated (contents undefined / zeroed by caller)
+  bool grow(size_t bytes) {
+    if (bytes <= cap) return false;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes + bytes / 8, 1 << 16);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      want = bytes;
+      CK(cudaMalloc(&p, want));
+    }
+    cap = want;
+    return true;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// small device block layout (u32 words)
+constexpr int kHist = 0;                    // 8*256 row-pass histograms
+constexpr int kBase = kHist + 8 * kRadix;   // 8*256 row-pass bin bases
+constexpr int kCHist = kBase + 8 * kRadix;  // 8*256 column-pass histograms
+constexpr int kCBase = kCHist + 8 * kRadix; // 8*256 column-pass bin bases
+constexpr int kCounters = kCBase + 8 * kRadix;  // 32 tile counters
+constexpr int kU = kCounters + 32;          // unique-link count
+constexpr int kGCount = kU + 2;             // u64 valid count (8-byte aligned)
+constexpr int kSmallWords = kGCount + 2;
+
+uint32_t ceil_log2(uint64_t x) {  // x >= 1
+  uint32_t b = 0;
+  while ((1ull << b) < x && b < 64) ++b;
+  return b;
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+}  // namespace
+
+struct nmx_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t st = nullptr;
+  std::mutex mu;
+  DevBuf keysA, keysB, ukeys, ustart, ckA, ckB, cvA, cvB, status, cstatus, small, stats, in_src, in_dst, in_valid,
+      red;
+  uint32_t epoch = 0;
+  uint32_t* h_small = nullptr;  // pinned mirror of `small`
+  unsigned long long* h_stats = nullptr;
+  size_t h_stats_cap = 0;
+  cudaEvent_t ev[40];
+  int nev = 0;
+  float last_total_ms = 0, last_sort_ms = 0;
+  int last_sort_launches = 0, last_launches = 0;
+  int launches = 0;
+
+  uint32_t next_epoch() {
+    if (++epoch >= (1u << 22)) {
+      if (status.p) CK(cudaMemsetAsync(status.p, 0, status.cap, st));
+      if (cstatus.p) CK(cudaMemsetAsync(cstatus.p, 0, cstatus.cap, st));
+      epoch = 1;
+    }
+    return epoch;
+  }
+  void grow_status(size_t tiles_x_cols) {
+    if (status.grow(tiles_x_cols * sizeof(uint64_t))) CK(cudaMemsetAsync(status.p, 0, status.cap, st));
+  }
+  void grow_cstatus(size_t tiles) {
+    if (cstatus.grow(tiles * sizeof(CarryStatus))) CK(cudaMemsetAsync(cstatus.p, 0, cstatus.cap, st));
+  }
+  void grow_hstats(size_t words) {
+    if (words <= h_stats_cap) return;
+    if (h_stats) cudaFreeHost(h_stats);
+    h_stats = nullptr;
+    CK(cudaMallocHost(&h_stats, words * sizeof(unsigned long long)));
+    h_stats_cap = words;
+  }
+  void mark() { CK(cudaEventRecord(ev[nev++], st)); }
+};
+
+namespace {
+
+uint64_t tiles_of(uint64_t items) { return (items + kTile - 1) / kTile; }
+
+template <typename Src, typename KeyT, bool HAS_VAL>
+void launch_pass(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32_t* vout, int shift,
+                 const uint32_t* binbase, uint32_t* counter) {
+  using S = PassSmem<KeyT, HAS_VAL, kIPT>;
+  auto kern = onesweep_pass<Src, KeyT, HAS_VAL, kIPT>;
+  set_smem(kern, sizeof(S));
+  const uint64_t t = tiles_of(items);
+  if (!t) return;
+  kern<<<(unsigned)t, kThreads, sizeof(S), c->st>>>(src, out, vout, shift, binbase, c->status.as<uint64_t>(),
+                                                      c->next_epoch(), counter);
+  CK_LAUNCH();
+  ++c->launches;
+}
+
+// Run a sort of `items` column keys (already written by row_kernel) with counts.
+template <typename ColKeyT>
+ColKeyT* column_phase(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small, int& sort_launches) {
+  const int colbits = b + wb;
+  const int ncolpass = (colbits + 7) / 8;
+  ColKeyT* ck = c->ckA.as<ColKeyT>();
+  uint32_t* cv = c->cvA.as<uint32_t>();
+  // column digit histograms were accumulated by row_kernel
+  bin_scan_kernel<<<1, kThreads, 0, c->st>>>(d_small + kCHist, ncolpass, d_small + kCBase);
+  CK_LAUNCH();
+  ++c->launches;
+  CK(cudaMemcpyAsync(c->h_small + kCHist, d_small + kCHist, sizeof(uint32_t) * ncolpass * kRadix,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  int idx = 0;
+  for (int p = 0; p < ncolpass; ++p) {
+    const uint32_t* hp = c->h_small + kCHist + p * kRadix;
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d)
+      if (hp[d] == u) trivial = true;
+    if (trivial) continue;
+    ColKeyT* ok = (idx & 1) ? c->ckA.as<ColKeyT>() : c->ckB.as<ColKeyT>();
+    uint32_t* ov = (idx & 1) ? c->cvA.as<uint32_t>() : c->cvB.as<uint32_t>();
+    KeySrc<ColKeyT, true> src{ck, cv, u};
+    launch_pass<KeySrc<ColKeyT, true>, ColKeyT, true>(c, src, u, ok, ov, 8 * p, d_small + kCBase + p * kRadix,
+                                                      d_small + kCounters + 16 + idx);
+    ck = ok;
+    cv = ov;
+    ++idx;
+    ++sort_launches;
+  }
+  c->mark();
+  auto kern = col_kernel<ColKeyT, kIPT>;
+  set_smem(kern, sizeof(SegSmem<kIPT>));
+  kern<<<(unsigned)tiles_of(u), kThreads, sizeof(SegSmem<kIPT>), c->st>>>(
+      ck, cv, u, b, wb, c->cstatus.as<CarryStatus>(), c->next_epoch(), d_small + kCounters + 26,
+      c->stats.as<unsigned long long>());
+  CK_LAUNCH();
+  ++c->launches;
+  return ck;
+}
+
+template <typename ColKeyT>
+void launch_row(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small) {
+  const int ncolpass = (b + wb + 7) / 8;
+  auto kern = row_kernel<ColKeyT, kIPT>;
+  set_smem(kern, sizeof(SegSmem<kIPT>));
+  kern<<<(unsigned)tiles_of(u), kThreads, sizeof(SegSmem<kIPT>), c->st>>>(
+      c->ukeys.as<uint64_t>(), c->ustart.as<uint32_t>(), u, b, wb, c->ckA.as<ColKeyT>(), c->cvA.as<uint32_t>(),
+      ncolpass, d_small + kCHist, c->cstatus.as<CarryStatus>(), c->next_epoch(), d_small + kCounters + 25,
+      c->stats.as<unsigned long long>());
+  CK_LAUNCH();
+  ++c->launches;
+}
+
+// The whole pipeline over packet columns already on the device. Writes W*9
+// statistics (u64) into c->h_stats. Windows: window_size == 0 -> one window.
+void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                  int b, uint64_t window_size, uint64_t W) {
+  const int wb = W > 1 ? (int)ceil_log2(W) : 0;
+  const int kb = 2 * b + wb;
+  const int npass = (kb + 7) / 8;
+  c->nev = 0;
+  c->launches = 0;
+  c->small.grow(kSmallWords * sizeof(uint32_t));
+  if (!c->h_small) CK(cudaMallocHost(&c->h_small, kSmallWords * sizeof(uint32_t)));
+  c->stats.grow(W * S_COUNT * sizeof(unsigned long long));
+  c->grow_hstats(W * S_COUNT);
+  uint32_t* d_small = c->small.as<uint32_t>();
+  c->mark();  // 0
+  CK(cudaMemsetAsync(d_small, 0, kSmallWords * sizeof(uint32_t), c->st));
+  CK(cudaMemsetAsync(c->stats.p, 0, W * S_COUNT * sizeof(unsigned long long), c->st));
+
+  PacketSrc ps{d_src, d_dst, d_valid, n, W > 1 ? window_size : 0, b};
+  {
+    const uint64_t want = (n + kThreads * 4 - 1) / (kThreads * 4);
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)c->sms * 8));
+    hist_kernel<PacketSrc, uint64_t><<<grid, kThreads, 0, c->st>>>(
+        ps, n, npass, d_small + kHist, reinterpret_cast<unsigned long long*>(d_small + kGCount));
+    CK_LAUNCH();
+    bin_scan_kernel<<<1, kThreads, 0, c->st>>>(d_small + kHist, npass, d_small + kBase);
+    CK_LAUNCH();
+    c->launches += 2;
+  }
+  CK(cudaMemcpyAsync(c->h_small, d_small, kSmallWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const uint64_t m = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
+  c->last_sort_launches = 0;
+  if (m == 0) {
+    CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       c->st));
+    c->mark();
+    CK(cudaStreamSynchronize(c->st));
+    c->last_sort_ms = 0;
+    CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
+    c->last_launches = c->launches;
+    return;
+  }
+  if (m >= (1ull << 32)) throw std::runtime_error("more than 2^32-1 valid packets in one call");
+
+  // ---- row sort (LSD onesweep over the packed key) ----
+  std::vector<int> active;
+  for (int p = 0; p < npass; ++p) {
+    const uint32_t* hp = c->h_small + kHist + p * kRadix;
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d)
+      if (hp[d] == m) trivial = true;
+    if (!trivial) active.push_back(p);
+  }
+  if (active.empty()) active.push_back(0);  // still need one pass to pack the keys
+  c->keysA.grow(m * 8);
+  c->keysB.grow(m * 8);
+  c->grow_status(std::max(tiles_of(n), tiles_of(m)) * kRadix);
+  c->mark();  // 1: sort start
+  uint64_t* keys = nullptr;
+  for (size_t i = 0; i < active.size(); ++i) {
+    const int p = active[i];
+    uint64_t* out = (i & 1) ? c->keysB.as<uint64_t>() : c->keysA.as<uint64_t>();
+    if (i == 0) {
+      launch_pass<PacketSrc, uint64_t, false>(c, ps, n, out, nullptr, 8 * p, d_small + kBase + p * kRadix,
+                                              d_small + kCounters + i);
+    } else {
+      KeySrc<uint64_t, false> ks{keys, nullptr, m};
+      launch_pass<KeySrc<uint64_t, false>, uint64_t, false>(c, ks, m, out, nullptr, 8 * p,
+                                                            d_small + kBase + p * kRadix, d_small + kCounters + i);
+    }
+    keys = out;
+  }
+  c->last_sort_launches = (int)active.size();
+  c->mark();  // 2: sort end
+
+  // ---- run-length encode -> unique links ----
+  c->ukeys.grow(m * 8);
+  c->ustart.grow((m + 1) * 4);
+  {
+    const size_t smem = (size_t)kTile * 12;
+    set_smem(rle_kernel<kIPT>, smem);
+    rle_kernel<kIPT><<<(unsigned)tiles_of(m), kThreads, smem, c->st>>>(
+        keys, (uint32_t)m, c->ukeys.as<uint64_t>(), c->ustart.as<uint32_t>(), c->status.as<uint64_t>(),
+        c->next_epoch(), d_small + kCounters + 24, d_small + kU);
+    CK_LAUNCH();
+    ++c->launches;
+  }
+  CK(cudaMemcpyAsync(c->h_small + kU, d_small + kU, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const uint32_t u = c->h_small[kU];
+  c->mark();  // 3
+
+  // ---- rows + links, then columns ----
+  const bool wide = b + wb > 32;
+  c->ckA.grow((size_t)u * (wide ? 8 : 4));
+  c->ckB.grow((size_t)u * (wide ? 8 : 4));
+  c->cvA.grow((size_t)u * 4);
+  c->cvB.grow((size_t)u * 4);
+  c->grow_cstatus(tiles_of(u));
+  c->grow_status(tiles_of(u) * kRadix);
+  if (wide)
+    launch_row<uint64_t>(c, u, b, wb, d_small);
+  else
+    launch_row<uint32_t>(c, u, b, wb, d_small);
+  c->mark();  // 4
+  int col_launches = 0;
+  if (wide)
+    column_phase<uint64_t>(c, u, b, wb, d_small, col_launches);
+  else
+    column_phase<uint32_t>(c, u, b, wb, d_small, col_launches);
+  CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     c->st));
+  c->mark();
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
+  CK(cudaEventElapsedTime(&c->last_sort_ms, c->ev[1], c->ev[2]));
+  c->last_launches = c->launches;
+}
+
+template <typename F>
+int guarded(nmx_ctx* c, F&& f) {
+  if (!c) return fail(NMX_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(c->mu);
+  try {
+    CK(cudaSetDevice(c->device));
+    return f();
+  } catch (const CudaError& e) {
+    cudaGetLastError();
+    return fail(NMX_ECUDA, "CUDA error %s (%s) at nmx_api.cu:%d", cudaGetErrorString(e.e), e.what, e.line);
+  } catch (const std::bad_alloc&) {
+    return fail(NMX_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(NMX_EINVAL, "%s", e.what());
+  }
+}
+
+int check_space(uint64_t address_space, int& b) {
+  if (address_space < 1 || address_space > (1ull << 32))
+    return fail(NMX_EINVAL, "address_space must lie in [1, 2^32], got %llu", (unsigned long long)address_space);
+  b = std::max<int>(1, (int)ceil_log2(address_space));
+  return NMX_OK;
+}
+
+void copy_out9(const unsigned long long* s, int64_t* out, uint64_t W) {
+  for (uint64_t i = 0; i < W * S_COUNT; ++i) out[i] = (int64_t)s[i];
+}
+
+int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                      uint64_t space, uint64_t window_size, int64_t* out) {
+  int b;
+  if (int r = check_space(space, b)) return r;
+  if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call, got %llu", (unsigned long long)n);
+  if (!out) return fail(NMX_EINVAL, "null output");
+  if (n == 0) {
+    if (window_size == 0) std::fill(out, out + S_COUNT, 0);
+    return NMX_OK;
+  }
+  if (!d_src || !d_dst) return fail(NMX_EINVAL, "null packet columns");
+  if (window_size == 0 || window_size >= n) {
+    run_pipeline(c, d_src, d_dst, d_valid, n, b, 0, 1);
+    copy_out9(c->h_stats, out, 1);
+    return NMX_OK;
+  }
+  const uint64_t W = (n + window_size - 1) / window_size;
+  const int wb = (int)ceil_log2(W);
+  if (2 * b + wb <= 64) {
+    run_pipeline(c, d_src, d_dst, d_valid, n, b, window_size, W);
+    copy_out9(c->h_stats, out, W);
+    return NMX_OK;
+  }
+  // keys too wide to carry the window id: one window per pipeline run
+  for (uint64_t t = 0; t < W; ++t) {
+    const uint64_t lo = t * window_size, len = std::min(window_size, n - lo);
+    run_pipeline(c, d_src + lo, d_dst + lo, d_valid ? d_valid + lo : nullptr, len, b, 0, 1);
+    copy_out9(c->h_stats, out + t * S_COUNT, 1);
+  }
+  return NMX_OK;
+}
+
+int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                    uint64_t space, uint64_t window_size, int64_t* out) {
+  if (n && (!src || !dst)) return fail(NMX_EINVAL, "null packet columns");
+  if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call, got %llu", (unsigned long long)n);
+  if (n) {
+    c->in_src.grow(n * 4);
+    c->in_dst.grow(n * 4);
+    CK(cudaMemcpyAsync(c->in_src.p, src, n * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->in_dst.p, dst, n * 4, cudaMemcpyHostToDevice, c->st));
+    if (valid) {
+      c->in_valid.grow(n);
+      CK(cudaMemcpyAsync(c->in_valid.p, valid, n, cudaMemcpyHostToDevice, c->st));
+    }
+  }
+  return stats_device_impl(c, c->in_src.as<uint32_t>(), c->in_dst.as<uint32_t>(),
+                           valid ? c->in_valid.as<uint8_t>() : nullptr, n, space, window_size, out);
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int nmx_version(void) { return 1; }
+
+const char* nmx_last_error(void) { return g_err.c_str(); }
+
+int nmx_device_count(int* count) {
+  if (!count) return fail(NMX_EINVAL, "null count");
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return fail(NMX_ENODEV, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  return NMX_OK;
+}
+
+int nmx_create(int device, nmx_ctx** out) {
+  if (!out) return fail(NMX_EINVAL, "null out");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(NMX_ENODEV, "no CUDA device visible");
+  }
+  if (device < 0 || device >= n) return fail(NMX_EINVAL, "device %d out of range [0,%d)", device, n);
+  nmx_ctx* c = new (std::nothrow) nmx_ctx();
+  if (!c) return fail(NMX_ENOMEM, "context allocation failed");
+  c->device = device;
+  try {
+    CK(cudaSetDevice(device));
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, device));
+    if (p.major < 10) {
+      delete c;
+      return fail(NMX_ENODEV, "device %d is sm_%d%d; libnmx.so is built for sm_100a only", device, p.major, p.minor);
+    }
+    c->sms = p.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  } catch (const CudaError& e) {
+    cudaGetLastError();
+    delete c;
+    return fail(NMX_ECUDA, "CUDA error %s (%s)", cudaGetErrorString(e.e), e.what);
+  }
+  *out = c;
+  return NMX_OK;
+}
+
+void nmx_destroy(nmx_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  for (DevBuf* b : {&c->keysA, &c->keysB, &c->ukeys, &c->ustart, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status,
+                    &c->cstatus, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
+    b->release();
+  if (c->h_small) cudaFreeHost(c->h_small);
+  if (c->h_stats) cudaFreeHost(c->h_stats);
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+void* nmx_stream(nmx_ctx* c) { return c ? (void*)c->st : nullptr; }
+
+int nmx_synchronize(nmx_ctx* c) {
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->st));
+    return NMX_OK;
+  });
+}
+
+int nmx_malloc(nmx_ctx* c, uint64_t bytes, void** dptr) {
+  if (!dptr) return fail(NMX_EINVAL, "null out");
+  return guarded(c, [&] {
+    cudaError_t e = cudaMalloc(dptr, std::max<uint64_t>(bytes, 1));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(NMX_ENOMEM, "cudaMalloc(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+    }
+    return NMX_OK;
+  });
+}
+
+int nmx_free(nmx_ctx* c, void* dptr) {
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaFree(dptr));
+    return NMX_OK;
+  });
+}
+
+int nmx_host_alloc(uint64_t bytes, void** hptr) {
+  if (!hptr) return fail(NMX_EINVAL, "null out");
+  cudaError_t e = cudaMallocHost(hptr, std::max<uint64_t>(bytes, 1));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(NMX_ENOMEM, "cudaMallocHost(%llu) failed: %s", (unsigned long long)bytes, cudaGetErrorString(e));
+  }
+  return NMX_OK;
+}
+
+int nmx_host_free(void* hptr) {
+  cudaError_t e = cudaFreeHost(hptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(NMX_ECUDA, "cudaFreeHost failed: %s", cudaGetErrorString(e));
+  }
+  return NMX_OK;
+}
+
+int nmx_memcpy_h2d(nmx_ctx* c, void* dst, const void* src, uint64_t bytes) {
+  return guarded(c, [&] {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return NMX_OK;
+  });
+}
+
+int nmx_memcpy_d2h(nmx_ctx* c, void* dst, const void* src, uint64_t bytes) {
+  return guarded(c, [&] {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return NMX_OK;
+  });
+}
+
+int nmx_generate(nmx_ctx* c, int kind, uint64_t seed, uint64_t offset, uint64_t n, uint64_t address_space,
+                 uint32_t* d_src, uint32_t* d_dst) {
+  if (kind != NMX_GEN_UNIFORM && kind != NMX_GEN_POWERLAW) return fail(NMX_EINVAL, "unknown generator %d", kind);
+  if (address_space < 1 || address_space > (1ull << 32)) return fail(NMX_EINVAL, "address_space out of range");
+  return guarded(c, [&] {
+    if (!n) return NMX_OK;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->sms * 16);
+    gen_kernel<<<grid, 256, 0, c->st>>>(kind, seed, offset, n, address_space, d_src, d_dst);
+    CK_LAUNCH();
+    CK(cudaStreamSynchronize(c->st));
+    return NMX_OK;
+  });
+}
+
+int nmx_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                      uint64_t address_space, int64_t out[9]) {
+  return guarded(c, [&] { return stats_device_impl(c, d_src, d_dst, d_valid, n, address_space, 0, out); });
+}
+
+int nmx_stats9_host(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                    uint64_t address_space, int64_t out[9]) {
+  return guarded(c, [&] { return stats_host_impl(c, src, dst, valid, n, address_space, 0, out); });
+}
+
+int nmx_window_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                             uint64_t n, uint64_t address_space, uint64_t window_size, int64_t* out) {
+  if (window_size < 1) return fail(NMX_EINVAL, "window_size must be >= 1");
+  return guarded(c, [&] {
+    if (n == 0) return NMX_OK;
+    if (window_size >= n) return stats_device_impl(c, d_src, d_dst, d_valid, n, address_space, 0, out);
+    return stats_device_impl(c, d_src, d_dst, d_valid, n, address_space, window_size, out);
+  });
+}
+
+int nmx_window_stats9_host(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                           uint64_t address_space, uint64_t window_size, int64_t* out) {
+  if (window_size < 1) return fail(NMX_EINVAL, "window_size must be >= 1");
+  return guarded(c, [&] {
+    if (n == 0) return NMX_OK;
+    return stats_host_impl(c, src, dst, valid, n, address_space, window_size >= n ? 0 : window_size, out);
+  });
+}
+
+int nmx_reduce_i64(nmx_ctx* c, const int64_t* data, uint64_t n, int op, int64_t* out) {
+  if (op != NMX_REDUCE_SUM && op != NMX_REDUCE_MAX) return fail(NMX_EINVAL, "unknown reduce op %d", op);
+  if (!out) return fail(NMX_EINVAL, "null output");
+  return guarded(c, [&] {
+    c->red.grow(n * 8 + 64);
+    unsigned long long init = op == NMX_REDUCE_SUM ? 0ull : (unsigned long long)INT64_MIN;
+    unsigned long long* d_out = reinterpret_cast<unsigned long long*>(c->red.as<int64_t>() + n);
+    CK(cudaMemcpyAsync(d_out, &init, 8, cudaMemcpyHostToDevice, c->st));
+    if (n) {
+      CK(cudaMemcpyAsync(c->red.p, data, n * 8, cudaMemcpyHostToDevice, c->st));
+      const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)c->sms * 8);
+      reduce_i64_kernel<<<grid, 256, 0, c->st>>>(c->red.as<int64_t>(), n, op, d_out);
+      CK_LAUNCH();
+    }
+    unsigned long long r;
+    CK(cudaMemcpyAsync(&r, d_out, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    *out = (int64_t)r;
+    return NMX_OK;
+  });
+}
+
+int nmx_last_timing(nmx_ctx* c, float* total_ms, float* sort_ms, int* sort_launches, int* kernel_launches) {
+  if (!c) return fail(NMX_EINVAL, "null context");
+  if (total_ms) *total_ms = c->last_total_ms;
+  if (sort_ms) *sort_ms = c->last_sort_ms;
+  if (sort_launches) *sort_launches = c->last_sort_launches;
+  if (kernel_launches) *kernel_launches = c->last_launches;
+  return NMX_OK;
+}
+
+}  // extern "C"

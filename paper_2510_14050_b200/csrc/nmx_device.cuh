@@ -1,0 +1,202 @@
+// nmx_device.cuh -- device primitives shared by the traffic-matrix kernels (sm_100a).
+//
+// Everything here is integer work: warp ballots for digit multisplit, block
+// scans, and the tile-status words of the decoupled-lookback scans.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nmx {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kThreads = 256;  // every tile kernel runs 8 warps
+constexpr int kWarps = kThreads / 32;
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 1 << kRadixBits;
+static_assert(kRadix == kThreads, "one thread per digit in the lookback/scan phases");
+
+// ---------------------------------------------------------------------------
+// synthetic packet generators; identical integer functions in
+// oracle/netmeter_oracle.py (gen_uniform / gen_powerlaw) and oracle/nmx_oracle.c
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint32_t octave32(uint64_t bits) {
+  uint32_t e = (uint32_t)(bits >> 59);
+  uint64_t rank = (1ull << e) | (bits & ((1ull << e) - 1));
+  return (uint32_t)(rank * 0x9E3779B1ull);
+}
+__host__ __device__ __forceinline__ uint32_t scale32(uint32_t v, uint64_t space) {
+  return space == (1ull << 32) ? v : (uint32_t)(((uint64_t)v * space) >> 32);
+}
+
+// ---------------------------------------------------------------------------
+// lane / memory-order helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Tile status word for single-value lookback scans:
+//   [63:42] epoch (22 bits, never 0 once written) | [41:40] flag | [39:0] value
+// The epoch tag lets one status array serve every pass without a memset: a
+// word whose epoch differs from the current launch's reads as "not ready".
+constexpr uint64_t kFlagAgg = 1, kFlagInc = 2;
+constexpr uint64_t kValueMask = (1ull << 40) - 1;
+__device__ __forceinline__ uint64_t st_pack(uint32_t epoch, uint64_t flag, uint64_t v) {
+  return ((uint64_t)epoch << 42) | (flag << 40) | (v & kValueMask);
+}
+__device__ __forceinline__ uint32_t st_epoch(uint64_t w) { return (uint32_t)(w >> 42); }
+__device__ __forceinline__ uint64_t st_flag(uint64_t w) { return (w >> 40) & 3; }
+__device__ __forceinline__ uint64_t st_value(uint64_t w) { return w & kValueMask; }
+
+// Exclusive prefix over predecessors of `tile` for one lane of a lookback
+// (status row stride `stride` words, column `col`). Spins until ready.
+__device__ __forceinline__ uint64_t lookback_exclusive(const uint64_t* status, uint32_t tile, int stride, int col,
+                                                       uint32_t epoch) {
+  uint64_t excl = 0;
+  int64_t p = (int64_t)tile - 1;
+  while (p >= 0) {
+    uint64_t w = ld_relaxed(status + (size_t)p * stride + col);
+    if (st_epoch(w) != epoch) continue;  // predecessor not published yet
+    excl += st_value(w);
+    if (st_flag(w) == kFlagInc) break;
+    --p;
+  }
+  return excl;
+}
+
+// Segmented-carry status (reduce-by-segment across tiles). The AGG and INC
+// payloads live in separate words so a reader that saw flag == AGG can never
+// pick up INC data written later (the data words are never rewritten within
+// one epoch); the flag word is stored last with release semantics.
+struct CarryStatus {
+  uint64_t agg_len, agg_sum;
+  uint64_t inc_len, inc_sum;
+  uint64_t flag;  // epoch << 2 | {1 = AGG, 2 = INC}
+  uint64_t pad[3];
+};
+
+// ---------------------------------------------------------------------------
+// block scans (256 threads)
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T x, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+// Exclusive block scan of one value per thread; returns the exclusive prefix,
+// writes the block total to *total. `wtot` is kWarps words of shared memory.
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T x, T* wtot, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = warp_incl_scan(x, lane);
+  if (lane == 31) wtot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    T v = lane < kWarps ? wtot[lane] : T(0);
+    T vi = warp_incl_scan(v, lane);
+    if (lane < kWarps) wtot[lane] = vi - v;  // exclusive warp offsets
+    if (lane == kWarps - 1) wtot[kWarps] = vi;
+  }
+  __syncthreads();
+  T res = wtot[warp] + inc - x;
+  *total = wtot[kWarps];
+  __syncthreads();
+  return res;
+}
+
+// Segmented scan element: f = a segment head occurred, (len, sum) = partial
+// since the last head (or since the start when f == 0).
+struct Seg {
+  uint32_t f;
+  uint32_t len;
+  uint64_t sum;
+};
+__device__ __forceinline__ Seg seg_combine(const Seg& a, const Seg& b) {
+  Seg r;
+  r.f = a.f | b.f;
+  r.len = b.f ? b.len : a.len + b.len;
+  r.sum = b.f ? b.sum : a.sum + b.sum;
+  return r;
+}
+
+// Exclusive segmented block scan; `sm` holds kWarps+1 Seg. Returns exclusive
+// prefix for this thread; *total = inclusive total of the block.
+__device__ __forceinline__ Seg block_excl_segscan(Seg x, Seg* sm, Seg* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Seg inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Seg y;
+    y.f = __shfl_up_sync(FULL, inc.f, o);
+    y.len = __shfl_up_sync(FULL, inc.len, o);
+    y.sum = __shfl_up_sync(FULL, inc.sum, o);
+    if (lane >= o) inc = seg_combine(y, inc);
+  }
+  Seg ex;
+  ex.f = __shfl_up_sync(FULL, inc.f, 1);
+  ex.len = __shfl_up_sync(FULL, inc.len, 1);
+  ex.sum = __shfl_up_sync(FULL, inc.sum, 1);
+  if (lane == 0) ex = Seg{0, 0, 0};
+  if (lane == 31) sm[warp] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Seg run{0, 0, 0};
+    for (int w = 0; w < kWarps; ++w) {
+      Seg t = sm[w];
+      sm[w] = run;
+      run = seg_combine(run, t);
+    }
+    sm[kWarps] = run;
+  }
+  __syncthreads();
+  Seg res = seg_combine(sm[warp], ex);
+  *total = sm[kWarps];
+  __syncthreads();
+  return res;
+}
+
+// Peers of this lane's 8-bit digit within the warp via 8 ballots (warp
+// multisplit). MATCH.ANY measured ~60 cycles/instr/SM on B200 (profiles/
+// r01_device_probe.txt), so ballots are the ranking primitive here.
+__device__ __forceinline__ uint32_t warp_digit_peers(uint32_t d, bool ok) {
+  uint32_t peers = __ballot_sync(FULL, ok);
+#pragma unroll
+  for (int b = 0; b < kRadixBits; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(FULL, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
+}  // namespace nmx
