@@ -101,6 +101,10 @@ int nmx_reduce_i64(nmx_ctx* ctx, const int64_t* data, uint64_t n, int op, int64_
  * call's whole device section, and of its dominant kernel class (the onesweep
  * passes) summed over launches, plus the number of kernels it launched. */
 int nmx_last_timing(nmx_ctx* ctx, float* total_ms, float* sort_ms, int* sort_launches, int* kernel_launches);
+/* Per-stage CUDA-event times (ms) of the last hot-path call: [0] ingest histogram
+ * (+ host pass planning), [1] row sort (onesweep passes), [2] fused link/row
+ * kernel, [3] column sort, [4] column kernel + result copy. Returns the count. */
+int nmx_last_stages(nmx_ctx* ctx, float* ms, int cap);
 
 #ifdef __cplusplus
 }

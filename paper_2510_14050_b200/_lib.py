@@ -50,6 +50,7 @@ SIGNATURES = {
     "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_window_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_reduce_i64": (C.c_int, [_VP, _VP, _U64, C.c_int, _VP]),
+    "nmx_last_stages": (C.c_int, [_VP, C.POINTER(C.c_float), C.c_int]),
     "nmx_last_timing": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_int),
                                   C.POINTER(C.c_int)]),
 }
@@ -131,7 +132,10 @@ class Context:
         t, s = C.c_float(), C.c_float()
         sl, kl = C.c_int(), C.c_int()
         check(self._lib.nmx_last_timing(self._h, C.byref(t), C.byref(s), C.byref(sl), C.byref(kl)))
-        return dict(total_ms=t.value, sort_ms=s.value, sort_launches=sl.value, kernel_launches=kl.value)
+        st = (C.c_float * 8)()
+        k = self._lib.nmx_last_stages(self._h, st, 8)
+        return dict(total_ms=t.value, sort_ms=s.value, sort_launches=sl.value, kernel_launches=kl.value,
+                    stages_ms=[round(st[i], 4) for i in range(max(k, 0))])
 
 
 _contexts: dict[int, Context] = {}

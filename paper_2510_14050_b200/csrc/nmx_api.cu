@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -104,7 +105,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf keysA, keysB, ukeys, ustart, ckA, ckB, cvA, cvB, status, cstatus, small, stats, in_src, in_dst, in_valid,
+  DevBuf keysA, keysB, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
@@ -113,22 +114,22 @@ struct nmx_ctx {
   cudaEvent_t ev[40];
   int nev = 0;
   float last_total_ms = 0, last_sort_ms = 0;
+  float last_stage_ms[8] = {0};
+  int last_nstage = 0;
   int last_sort_launches = 0, last_launches = 0;
   int launches = 0;
 
   uint32_t next_epoch() {
     if (++epoch >= (1u << 22)) {
       if (status.p) CK(cudaMemsetAsync(status.p, 0, status.cap, st));
-      if (cstatus.p) CK(cudaMemsetAsync(cstatus.p, 0, cstatus.cap, st));
+      if (lrstatus.p) CK(cudaMemsetAsync(lrstatus.p, 0, lrstatus.cap, st));
+      if (csstatus.p) CK(cudaMemsetAsync(csstatus.p, 0, csstatus.cap, st));
       epoch = 1;
     }
     return epoch;
   }
   void grow_status(size_t tiles_x_cols) {
     if (status.grow(tiles_x_cols * sizeof(uint64_t))) CK(cudaMemsetAsync(status.p, 0, status.cap, st));
-  }
-  void grow_cstatus(size_t tiles) {
-    if (cstatus.grow(tiles * sizeof(CarryStatus))) CK(cudaMemsetAsync(cstatus.p, 0, cstatus.cap, st));
   }
   void grow_hstats(size_t words) {
     if (words <= h_stats_cap) return;
@@ -142,31 +143,63 @@ struct nmx_ctx {
 
 namespace {
 
-uint64_t tiles_of(uint64_t items) { return (items + kTile - 1) / kTile; }
+uint64_t tiles_of(uint64_t items, int tile = kTile) { return (items + tile - 1) / tile; }
 
-template <typename Src, typename KeyT, bool HAS_VAL>
-void launch_pass(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32_t* vout, int shift,
-                 const uint32_t* binbase, uint32_t* counter) {
-  using S = PassSmem<KeyT, HAS_VAL, kIPT>;
-  auto kern = onesweep_pass<Src, KeyT, HAS_VAL, kIPT>;
+// onesweep pass configurations (THREADS, IPT, ranking, min blocks/SM); the
+// default was picked by the sweep in profiles/ (NMX_PASS_VARIANT overrides).
+constexpr int kDefaultVariant = 5;
+constexpr int kMinPassTile = 2048;  // smallest THREADS*IPT among the variants
+int pass_variant() {
+  static const int v = [] {
+    const char* e = getenv("NMX_PASS_VARIANT");
+    return e ? atoi(e) : kDefaultVariant;
+  }();
+  return v;
+}
+
+template <typename Src, typename KeyT, bool HAS_VAL, int THREADS, int IPT, int RANK, int MINB>
+void launch_pass_v(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32_t* vout, int shift,
+                   const uint32_t* binbase, uint32_t* counter) {
+  using S = PassSmem<KeyT, HAS_VAL, THREADS, IPT>;
+  auto kern = onesweep_pass<Src, KeyT, HAS_VAL, THREADS, IPT, RANK, MINB>;
   set_smem(kern, sizeof(S));
-  const uint64_t t = tiles_of(items);
+  const uint64_t t = tiles_of(items, THREADS * IPT);
   if (!t) return;
-  kern<<<(unsigned)t, kThreads, sizeof(S), c->st>>>(src, out, vout, shift, binbase, c->status.as<uint64_t>(),
-                                                      c->next_epoch(), counter);
+  kern<<<(unsigned)t, THREADS, sizeof(S), c->st>>>(src, out, vout, shift, binbase, c->status.as<uint64_t>(),
+                                                     c->next_epoch(), counter);
   CK_LAUNCH();
   ++c->launches;
 }
 
-// Run a sort of `items` column keys (already written by row_kernel) with counts.
+template <typename Src, typename KeyT, bool HAS_VAL>
+void launch_pass(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32_t* vout, int shift,
+                 const uint32_t* binbase, uint32_t* counter) {
+#define NMX_PV(T, I, R, M) \
+  launch_pass_v<Src, KeyT, HAS_VAL, T, I, R, M>(c, src, items, out, vout, shift, binbase, counter)
+  switch (pass_variant()) {
+    case 1: NMX_PV(256, 16, RANK_ATOMIC_OR, 1); break;
+    case 2: NMX_PV(256, 8, RANK_BALLOT, 3); break;
+    case 3: NMX_PV(256, 8, RANK_ATOMIC_OR, 3); break;
+    case 4: NMX_PV(512, 8, RANK_BALLOT, 2); break;
+    case 5: NMX_PV(512, 8, RANK_ATOMIC_OR, 2); break;
+    case 6: NMX_PV(256, 12, RANK_BALLOT, 2); break;
+    case 7: NMX_PV(256, 12, RANK_ATOMIC_OR, 2); break;
+    case 0: NMX_PV(256, 16, RANK_BALLOT, 1); break;
+    default: NMX_PV(512, 8, RANK_ATOMIC_OR, 2); break;
+  }
+#undef NMX_PV
+}
+
+constexpr int kSegIPT = 8;  // link_row / col kernels: 2048 items per tile
+constexpr int kSegTile = 256 * kSegIPT;
+
 template <typename ColKeyT>
-ColKeyT* column_phase(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small, int& sort_launches) {
-  const int colbits = b + wb;
-  const int ncolpass = (colbits + 7) / 8;
+void column_phase(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small) {
+  const int ncolpass = (b + wb + 7) / 8;
   ColKeyT* ck = c->ckA.as<ColKeyT>();
   uint32_t* cv = c->cvA.as<uint32_t>();
-  // column digit histograms were accumulated by row_kernel
-  bin_scan_kernel<<<1, kThreads, 0, c->st>>>(d_small + kCHist, ncolpass, d_small + kCBase);
+  // column digit histograms were accumulated by link_row_kernel
+  bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kCHist, ncolpass, d_small + kCBase);
   CK_LAUNCH();
   ++c->launches;
   CK(cudaMemcpyAsync(c->h_small + kCHist, d_small + kCHist, sizeof(uint32_t) * ncolpass * kRadix,
@@ -187,28 +220,37 @@ ColKeyT* column_phase(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small, 
     ck = ok;
     cv = ov;
     ++idx;
-    ++sort_launches;
   }
-  c->mark();
-  auto kern = col_kernel<ColKeyT, kIPT>;
-  set_smem(kern, sizeof(SegSmem<kIPT>));
-  kern<<<(unsigned)tiles_of(u), kThreads, sizeof(SegSmem<kIPT>), c->st>>>(
-      ck, cv, u, b, wb, c->cstatus.as<CarryStatus>(), c->next_epoch(), d_small + kCounters + 26,
+  c->mark();  // column sort end
+  col_kernel<ColKeyT, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
+      ck, cv, u, b, wb, c->csstatus.as<CSStatus>(), c->next_epoch(), d_small + kCounters + 26,
       c->stats.as<unsigned long long>());
   CK_LAUNCH();
   ++c->launches;
-  return ck;
 }
 
 template <typename ColKeyT>
-void launch_row(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small) {
+void launch_link_row(nmx_ctx* c, const uint64_t* keys, uint32_t m, int b, int wb, uint32_t* d_small) {
   const int ncolpass = (b + wb + 7) / 8;
-  auto kern = row_kernel<ColKeyT, kIPT>;
-  set_smem(kern, sizeof(SegSmem<kIPT>));
-  kern<<<(unsigned)tiles_of(u), kThreads, sizeof(SegSmem<kIPT>), c->st>>>(
-      c->ukeys.as<uint64_t>(), c->ustart.as<uint32_t>(), u, b, wb, c->ckA.as<ColKeyT>(), c->cvA.as<uint32_t>(),
-      ncolpass, d_small + kCHist, c->cstatus.as<CarryStatus>(), c->next_epoch(), d_small + kCounters + 25,
-      c->stats.as<unsigned long long>());
+  link_row_kernel<ColKeyT, kSegIPT><<<(unsigned)tiles_of(m, kSegTile), 256, 0, c->st>>>(
+      keys, m, b, wb, c->ckA.as<ColKeyT>(), c->cvA.as<uint32_t>(), ncolpass, d_small + kCHist,
+      c->lrstatus.as<LRStatus>(), c->next_epoch(), d_small + kCounters + 25, c->stats.as<unsigned long long>(),
+      d_small + kU);
+  CK_LAUNCH();
+  ++c->launches;
+}
+
+void launch_hist(nmx_ctx* c, const PacketSrc& ps, int npass, uint32_t* d_small) {
+  const uint64_t want = (ps.n + 1023) / 1024;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)c->sms * 8));
+  auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
+  switch (npass) {
+#define NMX_HCASE(P) \
+  case P: hist_kernel<P><<<grid, 256, 0, c->st>>>(ps, d_small + kHist, gcount); break;
+    NMX_HCASE(1) NMX_HCASE(2) NMX_HCASE(3) NMX_HCASE(4) NMX_HCASE(5) NMX_HCASE(6) NMX_HCASE(7) NMX_HCASE(8)
+#undef NMX_HCASE
+    default: throw std::runtime_error("bad pass count");
+  }
   CK_LAUNCH();
   ++c->launches;
 }
@@ -227,31 +269,25 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
   c->stats.grow(W * S_COUNT * sizeof(unsigned long long));
   c->grow_hstats(W * S_COUNT);
   uint32_t* d_small = c->small.as<uint32_t>();
-  c->mark();  // 0
+  c->mark();  // 0: start
   CK(cudaMemsetAsync(d_small, 0, kSmallWords * sizeof(uint32_t), c->st));
   CK(cudaMemsetAsync(c->stats.p, 0, W * S_COUNT * sizeof(unsigned long long), c->st));
 
   PacketSrc ps{d_src, d_dst, d_valid, n, W > 1 ? window_size : 0, b};
-  {
-    const uint64_t want = (n + kThreads * 4 - 1) / (kThreads * 4);
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)c->sms * 8));
-    hist_kernel<PacketSrc, uint64_t><<<grid, kThreads, 0, c->st>>>(
-        ps, n, npass, d_small + kHist, reinterpret_cast<unsigned long long*>(d_small + kGCount));
-    CK_LAUNCH();
-    bin_scan_kernel<<<1, kThreads, 0, c->st>>>(d_small + kHist, npass, d_small + kBase);
-    CK_LAUNCH();
-    c->launches += 2;
-  }
+  launch_hist(c, ps, npass, d_small);
+  bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kHist, npass, d_small + kBase);
+  CK_LAUNCH();
+  ++c->launches;
   CK(cudaMemcpyAsync(c->h_small, d_small, kSmallWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   const uint64_t m = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
   c->last_sort_launches = 0;
+  c->last_sort_ms = 0;
   if (m == 0) {
     CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                        c->st));
     c->mark();
     CK(cudaStreamSynchronize(c->st));
-    c->last_sort_ms = 0;
     CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
     c->last_launches = c->launches;
     return;
@@ -270,7 +306,7 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
   if (active.empty()) active.push_back(0);  // still need one pass to pack the keys
   c->keysA.grow(m * 8);
   c->keysB.grow(m * 8);
-  c->grow_status(std::max(tiles_of(n), tiles_of(m)) * kRadix);
+  c->grow_status(tiles_of(std::max(n, m), kMinPassTile) * kRadix);
   c->mark();  // 1: sort start
   uint64_t* keys = nullptr;
   for (size_t i = 0; i < active.size(); ++i) {
@@ -289,47 +325,37 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
   c->last_sort_launches = (int)active.size();
   c->mark();  // 2: sort end
 
-  // ---- run-length encode -> unique links ----
-  c->ukeys.grow(m * 8);
-  c->ustart.grow((m + 1) * 4);
-  {
-    const size_t smem = (size_t)kTile * 12;
-    set_smem(rle_kernel<kIPT>, smem);
-    rle_kernel<kIPT><<<(unsigned)tiles_of(m), kThreads, smem, c->st>>>(
-        keys, (uint32_t)m, c->ukeys.as<uint64_t>(), c->ustart.as<uint32_t>(), c->status.as<uint64_t>(),
-        c->next_epoch(), d_small + kCounters + 24, d_small + kU);
-    CK_LAUNCH();
-    ++c->launches;
-  }
+  // ---- unique links + rows (fused), then columns ----
+  const bool wide = b + wb > 32;
+  c->ckA.grow(m * (wide ? 8 : 4));
+  c->ckB.grow(m * (wide ? 8 : 4));
+  c->cvA.grow(m * 4);
+  c->cvB.grow(m * 4);
+  if (c->lrstatus.grow(tiles_of(m, kSegTile) * sizeof(LRStatus)))
+    CK(cudaMemsetAsync(c->lrstatus.p, 0, c->lrstatus.cap, c->st));
+  if (c->csstatus.grow(tiles_of(m, kSegTile) * sizeof(CSStatus)))
+    CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+  if (wide)
+    launch_link_row<uint64_t>(c, keys, (uint32_t)m, b, wb, d_small);
+  else
+    launch_link_row<uint32_t>(c, keys, (uint32_t)m, b, wb, d_small);
+  c->mark();  // 3: link/row end
   CK(cudaMemcpyAsync(c->h_small + kU, d_small + kU, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   const uint32_t u = c->h_small[kU];
-  c->mark();  // 3
-
-  // ---- rows + links, then columns ----
-  const bool wide = b + wb > 32;
-  c->ckA.grow((size_t)u * (wide ? 8 : 4));
-  c->ckB.grow((size_t)u * (wide ? 8 : 4));
-  c->cvA.grow((size_t)u * 4);
-  c->cvB.grow((size_t)u * 4);
-  c->grow_cstatus(tiles_of(u));
-  c->grow_status(tiles_of(u) * kRadix);
+  c->grow_status(tiles_of(u, kMinPassTile) * kRadix);
   if (wide)
-    launch_row<uint64_t>(c, u, b, wb, d_small);
+    column_phase<uint64_t>(c, u, b, wb, d_small);
   else
-    launch_row<uint32_t>(c, u, b, wb, d_small);
-  c->mark();  // 4
-  int col_launches = 0;
-  if (wide)
-    column_phase<uint64_t>(c, u, b, wb, d_small, col_launches);
-  else
-    column_phase<uint32_t>(c, u, b, wb, d_small, col_launches);
+    column_phase<uint32_t>(c, u, b, wb, d_small);
   CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      c->st));
-  c->mark();
+  c->mark();  // 5: end
   CK(cudaStreamSynchronize(c->st));
   CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
   CK(cudaEventElapsedTime(&c->last_sort_ms, c->ev[1], c->ev[2]));
+  for (int i = 0; i + 1 < c->nev && i < 8; ++i) CK(cudaEventElapsedTime(&c->last_stage_ms[i], c->ev[i], c->ev[i + 1]));
+  c->last_nstage = std::min(c->nev - 1, 8);
   c->last_launches = c->launches;
 }
 
@@ -468,8 +494,8 @@ void nmx_destroy(nmx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (DevBuf* b : {&c->keysA, &c->keysB, &c->ukeys, &c->ustart, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status,
-                    &c->cstatus, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
+  for (DevBuf* b : {&c->keysA, &c->keysB, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
+                    &c->csstatus, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
     b->release();
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_stats) cudaFreeHost(c->h_stats);
@@ -605,6 +631,13 @@ int nmx_reduce_i64(nmx_ctx* c, const int64_t* data, uint64_t n, int op, int64_t*
     *out = (int64_t)r;
     return NMX_OK;
   });
+}
+
+int nmx_last_stages(nmx_ctx* c, float* ms, int cap) {
+  if (!c) return fail(NMX_EINVAL, "null context");
+  const int k = std::min(cap, c->last_nstage);
+  for (int i = 0; i < k; ++i) ms[i] = c->last_stage_ms[i];
+  return k;
 }
 
 int nmx_last_timing(nmx_ctx* c, float* total_ms, float* sort_ms, int* sort_launches, int* kernel_launches) {

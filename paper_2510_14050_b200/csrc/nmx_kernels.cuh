@@ -1,18 +1,19 @@
 // nmx_kernels.cuh -- the traffic-matrix hot path as sm_100a kernels.
 //
 // Pipeline for one call (n packets, b address bits, W windows, wb window bits):
-//   K1  hist_kernel<PacketSrc>   ingest u32 src/dst (+valid) -> digit histograms of
-//                                 every LSD pass of key = win<<2b | src<<b | dst
-//   K2  onesweep_pass<...>       one stable 8-bit LSD pass per non-trivial digit;
-//                                 the first pass packs keys straight from the packet
-//                                 columns (traffic.py:205-207 `src*dim+dst`)
-//   K3  rle_kernel               run-length encode sorted keys -> unique links
-//                                 (np.unique(return_counts), traffic.py:207)
-//   K5  row_kernel               per-link + per-source statistics (segmented over
-//                                 src runs), emits (dst, count) for the columns and
-//                                 their digit histograms (traffic.py:267-277)
-//   K6  onesweep_pass<u32|u64,+count> then col_kernel: per-destination statistics
-//                                 (traffic.py:279-283 bincount / add.at)
+//   K1  hist_kernel          ingest u32 src/dst (+valid) -> digit histograms of every
+//                            LSD pass of key = win<<2b | src<<b | dst (one read)
+//   K2  onesweep_pass        one stable 8-bit LSD pass per non-trivial digit; the
+//                            first pass packs keys straight from the packet columns
+//                            (traffic.py:205-207 `src*dim+dst`)
+//   K3+K5 link_row_kernel    run-length encode the sorted keys into unique links
+//                            (np.unique(return_counts), traffic.py:207) fused with the
+//                            per-link and per-source statistics (traffic.py:267-277);
+//                            emits compacted (win<<b|dst, count) column entries and
+//                            their digit histograms
+//   K6  onesweep_pass<+count> over the column entries, then col_kernel: per-destination
+//                            statistics (traffic.py:279-283 bincount / add.at)
+// Every cross-tile dependency is a decoupled lookback over tile-status words.
 // Statistics land in a per-window u64[9] array (analytics.py:95-130 + the three
 // Graph Challenge maxima).
 #pragma once
@@ -34,11 +35,15 @@ enum : int {
   S_COUNT = 9
 };
 
+// padded index for blocked (thread-contiguous) shared-memory access: 16
+// consecutive items per thread would otherwise put a warp on one bank
+__device__ __forceinline__ uint32_t pad16(uint32_t i) { return i + (i >> 4); }
+
 // ---------------------------------------------------------------------------
 // item sources
 // ---------------------------------------------------------------------------
 // Raw packet columns -> packed key. Invalid packets are dropped here
-// (traffic.py:238-240), their positions still define the windows.
+// (traffic.py:238-240); their positions still define the windows.
 struct PacketSrc {
   const uint32_t* src;
   const uint32_t* dst;
@@ -73,58 +78,50 @@ struct KeySrc {
 // ---------------------------------------------------------------------------
 // K1: digit histograms for every pass, plus the valid-item count
 // ---------------------------------------------------------------------------
-template <typename Src, typename KeyT>
-__global__ void __launch_bounds__(kThreads) hist_kernel(Src src, uint64_t n, int npass, uint32_t* __restrict__ ghist,
-                                                       unsigned long long* __restrict__ gcount) {
-  __shared__ uint32_t h[8][kRadix];
-  for (int i = threadIdx.x; i < 8 * kRadix; i += kThreads) (&h[0][0])[i] = 0;
+template <int NPASS>
+__global__ void __launch_bounds__(256) hist_kernel(PacketSrc src, uint32_t* __restrict__ ghist,
+                                                  unsigned long long* __restrict__ gcount) {
+  __shared__ uint32_t h[NPASS][kRadix];
+  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) (&h[0][0])[i] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   uint32_t cnt = 0;
   constexpr int U = 4;
-  const uint64_t stride = (uint64_t)gridDim.x * kThreads * U;
-  for (uint64_t base = (uint64_t)blockIdx.x * kThreads * U; base < n; base += stride) {
-    KeyT k[U];
+  const uint64_t n = src.n;
+  const uint64_t stride = (uint64_t)gridDim.x * 256 * U;
+  for (uint64_t base = (uint64_t)blockIdx.x * 256 * U; base < n; base += stride) {
+    uint64_t k[U];
     bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       uint32_t v;
-      uint64_t kk = 0;
-      ok[u] = src.load(base + (uint64_t)u * kThreads + threadIdx.x, *reinterpret_cast<KeyT*>(&kk), v);
-      k[u] = *reinterpret_cast<KeyT*>(&kk);
+      ok[u] = src.load(base + (uint64_t)u * 256 + threadIdx.x, k[u], v);
       cnt += ok[u];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      for (int p = 0; p < npass; ++p) {
-        const uint32_t d = (uint32_t)(k[u] >> (8 * p)) & 0xFFu;
-        const uint32_t d0 = __shfl_sync(FULL, d, 0);
-        if (__all_sync(FULL, ok[u] && d == d0)) {
-          if (lane == 0) atomicAdd(&h[p][d0], 32u);
-        } else if (ok[u]) {
-          atomicAdd(&h[p][d], 1u);
-        }
+      if (ok[u]) {
+#pragma unroll
+        for (int p = 0; p < NPASS; ++p) atomicAdd(&h[p][(uint32_t)(k[u] >> (8 * p)) & 0xFFu], 1u);
       }
     }
   }
-  // warp-reduce the valid count
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
-  if (lane == 0 && cnt) atomicAdd(gcount, (unsigned long long)cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(gcount, (unsigned long long)cnt);
   __syncthreads();
-  for (int i = threadIdx.x; i < npass * kRadix; i += kThreads) {
-    uint32_t v = (&h[0][0])[i];
+  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) {
+    const uint32_t v = (&h[0][0])[i];
     if (v) atomicAdd(ghist + i, v);
   }
 }
 
 // exclusive scan of each pass's 256-bin histogram -> global bin base offsets
-__global__ void __launch_bounds__(kThreads) bin_scan_kernel(const uint32_t* __restrict__ ghist, int npass,
-                                                           uint32_t* __restrict__ gbase) {
+__global__ void __launch_bounds__(256) bin_scan_kernel(const uint32_t* __restrict__ ghist, int npass,
+                                                      uint32_t* __restrict__ gbase) {
   __shared__ uint32_t wt[kWarps + 1];
   for (int p = 0; p < npass; ++p) {
     uint32_t tot;
-    uint32_t ex = block_excl_scan<uint32_t>(ghist[p * kRadix + threadIdx.x], wt, &tot);
+    const uint32_t ex = block_excl_scan<uint32_t>(ghist[p * kRadix + threadIdx.x], wt, &tot);
     gbase[p * kRadix + threadIdx.x] = ex;
   }
 }
@@ -132,108 +129,157 @@ __global__ void __launch_bounds__(kThreads) bin_scan_kernel(const uint32_t* __re
 // ---------------------------------------------------------------------------
 // K2: one onesweep LSD pass (8-bit digit at `shift`), stable.
 //   * tile id from an atomic counter (forward progress for the lookback)
-//   * warp multisplit ranking with ballots into per-warp smem counters
+//   * warp-level stable ranking into per-warp smem counters; peers of a digit
+//     found either with 8 ballots (RANK_BALLOT) or one smem atomicOr of the
+//     lane bit (RANK_ATOMIC_OR)
 //   * decoupled lookback per digit over epoch-tagged u64 status words
 //   * keys staged in smem in digit order -> near-coalesced scatter
 // ---------------------------------------------------------------------------
-template <typename KeyT, bool HAS_VAL, int IPT>
+enum { RANK_BALLOT = 0, RANK_ATOMIC_OR = 1 };
+
+template <typename KeyT, bool HAS_VAL, int THREADS, int IPT>
 struct PassSmem {
-  KeyT keys[kThreads * IPT];
-  uint32_t vals[HAS_VAL ? kThreads * IPT : 1];
-  uint32_t whist[kWarps][kRadix];
+  static constexpr int W = THREADS / 32;
+  KeyT keys[THREADS * IPT];
+  uint32_t vals[HAS_VAL ? THREADS * IPT : 1];
+  uint32_t whist[W][kRadix];
+  uint32_t mm[W][kRadix];
   uint32_t tstart[kRadix];
   uint32_t gbase[kRadix];
-  uint32_t wt[kWarps + 1];
+  uint32_t wt[W + 1];
   uint32_t tile;
 };
 
-template <typename Src, typename KeyT, bool HAS_VAL, int IPT>
-__global__ void __launch_bounds__(kThreads) onesweep_pass(Src src, KeyT* __restrict__ keys_out,
-                                                         uint32_t* __restrict__ vals_out, int shift,
-                                                         const uint32_t* __restrict__ bin_base,
-                                                         uint64_t* __restrict__ status, uint32_t epoch,
-                                                         uint32_t* __restrict__ tile_counter) {
-  constexpr int TILE = kThreads * IPT;
+template <int THREADS>
+__device__ __forceinline__ uint32_t block_excl_scan_n(uint32_t x, uint32_t* wt, uint32_t* total) {
+  constexpr int W = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = warp_incl_scan(x, lane);
+  if (lane == 31) wt[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < W ? wt[lane] : 0u;
+    const uint32_t vi = warp_incl_scan(v, lane);
+    if (lane < W) wt[lane] = vi - v;
+    if (lane == W - 1) wt[W] = vi;
+  }
+  __syncthreads();
+  const uint32_t res = wt[warp] + inc - x;
+  *total = wt[W];
+  __syncthreads();
+  return res;
+}
+
+template <typename Src, typename KeyT, bool HAS_VAL, int THREADS, int IPT, int RANK, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    onesweep_pass(Src src, KeyT* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int shift,
+                  const uint32_t* __restrict__ bin_base, uint64_t* __restrict__ status, uint32_t epoch,
+                  uint32_t* __restrict__ tile_counter) {
+  constexpr int TILE = THREADS * IPT;
+  constexpr int W = THREADS / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& s = *reinterpret_cast<PassSmem<KeyT, HAS_VAL, IPT>*>(smem_raw);
+  auto& s = *reinterpret_cast<PassSmem<KeyT, HAS_VAL, THREADS, IPT>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   if (tid == 0) s.tile = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&s.whist[0][0])[i] = 0;
+  for (int i = tid; i < W * kRadix; i += THREADS) {
+    (&s.whist[0][0])[i] = 0;
+    if (RANK == RANK_ATOMIC_OR) (&s.mm[0][0])[i] = 0;
+  }
   __syncthreads();
   const uint32_t tile = s.tile;
   const uint64_t base = (uint64_t)tile * TILE + (uint64_t)warp * 32 * IPT;
 
   KeyT k[IPT];
-  uint32_t v[IPT];
+  uint32_t v[HAS_VAL ? IPT : 1];
   uint32_t okmask = 0;
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
-    uint64_t kk = 0;
     uint32_t vv = 0;
-    bool ok = src.load(base + (uint64_t)i * 32 + lane, *reinterpret_cast<KeyT*>(&kk), vv);
-    k[i] = *reinterpret_cast<KeyT*>(&kk);
-    v[i] = vv;
+    const bool ok = src.load(base + (uint64_t)i * 32 + lane, k[i], vv);
+    if (HAS_VAL) v[HAS_VAL ? i : 0] = vv;
     okmask |= (uint32_t)ok << i;
   }
 
-  // rank within the warp (stable: item order is (i, lane))
-  uint32_t rk[IPT];
+  // stable rank within the warp: item order is (i, lane)
+  uint32_t rk[(IPT + 1) / 2];  // two 16-bit ranks per register
   const uint32_t lt = lanemask_lt();
+  const uint32_t lanebit = 1u << lane;
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const bool ok = (okmask >> i) & 1u;
     const uint32_t d = (uint32_t)(k[i] >> shift) & 0xFFu;
-    const uint32_t peers = warp_digit_peers(d, ok);
+    uint32_t peers;
+    if (RANK == RANK_BALLOT) {
+      peers = warp_digit_peers(d, ok);
+    } else {
+      volatile uint32_t* mp = &s.mm[warp][d];
+      if (ok) atomicOr((uint32_t*)mp, lanebit);
+      __syncwarp();
+      peers = ok ? *mp : 0u;
+      __syncwarp();
+    }
     const int leader = ok ? __ffs(peers) - 1 : lane;
     uint32_t b = 0;
     if (ok && lane == leader) {
       b = s.whist[warp][d];
       s.whist[warp][d] = b + __popc(peers);
+      if (RANK == RANK_ATOMIC_OR) s.mm[warp][d] = 0;
     }
     b = __shfl_sync(FULL, b, leader);
-    rk[i] = b + __popc(peers & lt);
+    const uint32_t r = b + __popc(peers & lt);
+    if (i & 1)
+      rk[i >> 1] |= r << 16;
+    else
+      rk[i >> 1] = r;
     __syncwarp();
   }
   __syncthreads();
 
-  // per-digit: exclusive over warps, tile count
+  // per digit (threads < 256): exclusive over warps, tile count
   uint32_t cnt = 0;
+  if (tid < kRadix) {
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    uint32_t c = s.whist[w][tid];
-    s.whist[w][tid] = cnt;
-    cnt += c;
+    for (int w = 0; w < W; ++w) {
+      const uint32_t c = s.whist[w][tid];
+      s.whist[w][tid] = cnt;
+      cnt += c;
+    }
   }
   // publish + decoupled lookback (thread tid owns digit tid)
-  uint64_t* my = status + (size_t)tile * kRadix + tid;
   uint64_t excl = 0;
-  if (tile == 0) {
-    st_relaxed(my, st_pack(epoch, kFlagInc, cnt));
-  } else {
-    st_relaxed(my, st_pack(epoch, kFlagAgg, cnt));
-    excl = lookback_exclusive(status, tile, kRadix, tid, epoch);
-    st_relaxed(my, st_pack(epoch, kFlagInc, excl + cnt));
+  if (tid < kRadix) {
+    uint64_t* my = status + (size_t)tile * kRadix + tid;
+    if (tile == 0) {
+      st_relaxed(my, st_pack(epoch, kFlagInc, cnt));
+    } else {
+      st_relaxed(my, st_pack(epoch, kFlagAgg, cnt));
+      excl = lookback_exclusive(status, tile, kRadix, tid, epoch);
+      st_relaxed(my, st_pack(epoch, kFlagInc, excl + cnt));
+    }
   }
   uint32_t total;
-  const uint32_t tstart = block_excl_scan<uint32_t>(cnt, s.wt, &total);
-  s.tstart[tid] = tstart;
-  s.gbase[tid] = bin_base[tid] + (uint32_t)excl - tstart;
+  const uint32_t tstart = block_excl_scan_n<THREADS>(cnt, s.wt, &total);
+  if (tid < kRadix) {
+    s.tstart[tid] = tstart;
+    s.gbase[tid] = bin_base[tid] + (uint32_t)excl - tstart;
+  }
   __syncthreads();
 
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     if ((okmask >> i) & 1u) {
       const uint32_t d = (uint32_t)(k[i] >> shift) & 0xFFu;
-      const uint32_t lp = s.tstart[d] + s.whist[warp][d] + rk[i];
+      const uint32_t r = (i & 1) ? (rk[i >> 1] >> 16) : (rk[i >> 1] & 0xFFFFu);
+      const uint32_t lp = s.tstart[d] + s.whist[warp][d] + r;
       s.keys[lp] = k[i];
-      if (HAS_VAL) s.vals[lp] = v[i];
+      if (HAS_VAL) s.vals[lp] = v[HAS_VAL ? i : 0];
     }
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
-    const uint32_t idx = j * kThreads + tid;
+    const uint32_t idx = j * THREADS + tid;
     if (idx < total) {
       const KeyT key = s.keys[idx];
       const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
@@ -245,372 +291,439 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(Src src, KeyT* __restr
 }
 
 // ---------------------------------------------------------------------------
-// K3: run-length encode sorted keys -> ukeys[u], ustart[u+1] (ustart[u] = m)
+// Composite scan element of the fused link/row kernel (all counts < 2^32):
+//   nh        number of link heads (-> output index of each unique link)
+//   link seg  (llen)         run of equal keys: llen = packets on the link
+//   src  seg  (slen, ssum)   run of equal sources: slen = packets of the
+//                             source, ssum = link heads = fan-out
+//   fl        bit0: a link head occurred, bit1: a source head occurred
 // ---------------------------------------------------------------------------
-template <int IPT>
-__global__ void __launch_bounds__(kThreads) rle_kernel(const uint64_t* __restrict__ keys, uint32_t m,
-                                                      uint64_t* __restrict__ ukeys, uint32_t* __restrict__ ustart,
-                                                      uint64_t* __restrict__ status, uint32_t epoch,
-                                                      uint32_t* __restrict__ tile_counter,
+struct LR {
+  uint32_t nh, fl, llen, slen, ssum;
+  __device__ __forceinline__ static LR identity() { return LR{0, 0, 0, 0, 0}; }
+};
+__device__ __forceinline__ LR lr_combine(const LR& a, const LR& b) {
+  LR r;
+  r.nh = a.nh + b.nh;
+  r.fl = a.fl | b.fl;
+  r.llen = (b.fl & 1) ? b.llen : a.llen + b.llen;
+  r.slen = (b.fl & 2) ? b.slen : a.slen + b.slen;
+  r.ssum = (b.fl & 2) ? b.ssum : a.ssum + b.ssum;
+  return r;
+}
+__device__ __forceinline__ LR lr_shfl_up(const LR& x, int o) {
+  LR y;
+  y.nh = __shfl_up_sync(FULL, x.nh, o);
+  y.fl = __shfl_up_sync(FULL, x.fl, o);
+  y.llen = __shfl_up_sync(FULL, x.llen, o);
+  y.slen = __shfl_up_sync(FULL, x.slen, o);
+  y.ssum = __shfl_up_sync(FULL, x.ssum, o);
+  return y;
+}
+
+// column segment (run of equal destinations): len = fan-in, sum = packets
+struct CS {
+  uint32_t f, len, sum;
+  __device__ __forceinline__ static CS identity() { return CS{0, 0, 0}; }
+};
+__device__ __forceinline__ CS cs_combine(const CS& a, const CS& b) {
+  return CS{a.f | b.f, b.f ? b.len : a.len + b.len, b.f ? b.sum : a.sum + b.sum};
+}
+__device__ __forceinline__ CS cs_shfl_up(const CS& x, int o) {
+  return CS{__shfl_up_sync(FULL, x.f, o), __shfl_up_sync(FULL, x.len, o), __shfl_up_sync(FULL, x.sum, o)};
+}
+
+// generic exclusive block scan (256 threads) for LR / CS
+template <typename T, T (*COMB)(const T&, const T&), T (*SHFL)(const T&, int)>
+__device__ __forceinline__ T block_excl_scan_op(T x, T* sm, T* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = SHFL(inc, o);
+    if (lane >= o) inc = COMB(y, inc);
+  }
+  T ex = SHFL(inc, 1);
+  if (lane == 0) ex = T::identity();
+  if (lane == 31) sm[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const T w = lane < kWarps ? sm[lane] : T::identity();
+    T wi = w;
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1) {
+      T y = SHFL(wi, o);
+      if (lane >= o) wi = COMB(y, wi);
+    }
+    T we = SHFL(wi, 1);
+    if (lane == 0) we = T::identity();
+    __syncwarp();
+    if (lane < kWarps) sm[lane] = we;
+    if (lane == kWarps - 1) sm[kWarps] = wi;
+  }
+  __syncthreads();
+  const T res = COMB(sm[warp], ex);
+  *total = sm[kWarps];
+  __syncthreads();
+  return res;
+}
+
+// Multi-word tile status for composite lookbacks: AGG and INC payloads in
+// separate words (never rewritten within an epoch), flag stored last (release).
+template <int NW>
+struct TileStatus {
+  uint32_t agg[NW];
+  uint32_t inc[NW];
+  uint64_t flag;  // epoch << 2 | {1 = AGG, 2 = INC}
+};
+
+__device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T, int NW>
+__device__ __forceinline__ void publish(TileStatus<NW>* st, const T& x, uint32_t epoch, bool inclusive) {
+  static_assert(sizeof(T) == 4 * NW, "status payload size");
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
+  uint32_t* dst = inclusive ? st->inc : st->agg;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) st_u32(dst + i, w[i]);
+  st_release(&st->flag, ((uint64_t)epoch << 2) | (inclusive ? kFlagInc : kFlagAgg));
+}
+
+// exclusive prefix of tile `tile` (single thread)
+template <typename T, int NW, T (*COMB)(const T&, const T&)>
+__device__ __forceinline__ T lookback_op(TileStatus<NW>* status, uint32_t tile, uint32_t epoch) {
+  T acc = T::identity();
+  for (int64_t p = (int64_t)tile - 1; p >= 0;) {
+    const uint64_t f = ld_acquire(&status[p].flag);
+    if ((uint32_t)(f >> 2) != epoch) continue;
+    T x;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+    const bool inc = (f & 3) == kFlagInc;
+    const uint32_t* srcw = inc ? status[p].inc : status[p].agg;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) w[i] = ld_u32(srcw + i);
+    acc = COMB(x, acc);
+    if (inc) break;
+    --p;
+  }
+  return acc;
+}
+
+using LRStatus = TileStatus<5>;
+using CSStatus = TileStatus<3>;
+
+// ---------------------------------------------------------------------------
+// K3+K5: links + rows, fused. Items are the sorted keys [0, m).
+// ---------------------------------------------------------------------------
+template <typename ColKeyT, int IPT>
+__global__ void __launch_bounds__(256) link_row_kernel(const uint64_t* __restrict__ keys, uint32_t m, int b,
+                                                      int wb, ColKeyT* __restrict__ ckeys,
+                                                      uint32_t* __restrict__ ccounts, int ncolpass,
+                                                      uint32_t* __restrict__ colhist, LRStatus* status,
+                                                      uint32_t epoch, uint32_t* __restrict__ tile_counter,
+                                                      unsigned long long* __restrict__ stats,
                                                       uint32_t* __restrict__ d_u) {
-  constexpr int TILE = kThreads * IPT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* sk = reinterpret_cast<uint64_t*>(smem_raw);
-  uint32_t* ss = reinterpret_cast<uint32_t*>(sk + TILE);
-  __shared__ uint32_t wt[kWarps + 1];
+  constexpr int TILE = 256 * IPT;
+  // staging: keys (padded, blocked reads), then reused for the column outputs
+  __shared__ __align__(16) uint64_t sk[TILE + TILE / 16];
+  __shared__ uint32_t sc[TILE];
+  __shared__ uint32_t h[8][kRadix];
+  __shared__ LR sm_lr[kWarps + 1];
+  __shared__ LR s_excl;
+  __shared__ unsigned long long sm_red[kWarps][6];
   __shared__ uint32_t s_tile;
-  __shared__ uint64_t s_prev, s_excl;
-  const int tid = threadIdx.x;
+  __shared__ uint64_t s_prev, s_next;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  for (int i = tid; i < ncolpass * kRadix; i += 256) (&h[0][0])[i] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint64_t t0 = (uint64_t)tile * TILE;
   const uint32_t cnt = (uint32_t)umin64(TILE, m - t0);
+  const bool last_tile = t0 + cnt == m;
   for (int j = 0; j < IPT; ++j) {
-    uint32_t i = j * kThreads + tid;
-    if (i < cnt) sk[i] = keys[t0 + i];
+    const uint32_t i = j * 256 + tid;
+    if (i < cnt) sk[pad16(i)] = keys[t0 + i];
   }
-  if (tid == 0) s_prev = t0 ? keys[t0 - 1] : ~keys[0];
+  if (tid == 0) {
+    s_prev = t0 ? keys[t0 - 1] : ~keys[0];
+    s_next = last_tile ? 0 : keys[t0 + cnt];
+  }
   __syncthreads();
+  const uint64_t first_key = sk[0], last_key = sk[pad16(cnt - 1)];
+  const int b2 = 2 * b;
+  const bool uniform = wb == 0 || (first_key >> b2) == (last_key >> b2);
+  const uint64_t wfirst = wb ? (first_key >> b2) : 0;
+  const uint64_t sprev = s_prev, snext = s_next;
+
+  // pass 1: thread aggregate over its IPT consecutive keys
   uint64_t k[IPT];
-  uint32_t hmask = 0, nh = 0;
-  uint64_t prev = tid ? (tid * IPT - 1 < cnt ? sk[tid * IPT - 1] : 0) : s_prev;
+  const uint32_t i0 = tid * IPT;
+  uint64_t prev = i0 == 0 ? sprev : (i0 < cnt ? sk[pad16(i0 - 1)] : 0);
+  const uint64_t prev0 = prev;
+  LR agg = LR::identity();
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
-    const uint32_t i = tid * IPT + q;
+    const uint32_t i = i0 + q;
     if (i < cnt) {
-      k[q] = sk[i];
-      const bool h = k[q] != prev;
-      hmask |= (uint32_t)h << q;
-      nh += h;
+      k[q] = sk[pad16(i)];
+      const uint32_t hl = k[q] != prev, hs = (k[q] >> b) != (prev >> b);
+      agg = lr_combine(agg, LR{hl, hl | (hs << 1), 1, 1, hl});
       prev = k[q];
     }
   }
-  uint32_t total;
-  uint32_t off = block_excl_scan<uint32_t>(nh, wt, &total);
+  LR total;
+  const LR pre = block_excl_scan_op<LR, lr_combine, lr_shfl_up>(agg, sm_lr, &total);
   if (tid == 0) {
-    uint64_t* my = status + tile;
-    uint64_t ex = 0;
+    LRStatus* my = status + tile;
+    LR ex = LR::identity();
     if (tile == 0) {
-      st_relaxed(my, st_pack(epoch, kFlagInc, total));
+      publish<LR, 5>(my, total, epoch, true);
     } else {
-      st_relaxed(my, st_pack(epoch, kFlagAgg, total));
-      ex = lookback_exclusive(status, tile, 1, 0, epoch);
-      st_relaxed(my, st_pack(epoch, kFlagInc, ex + total));
+      publish<LR, 5>(my, total, epoch, false);
+      ex = lookback_op<LR, 5, lr_combine>(status, tile, epoch);
+      publish<LR, 5>(my, lr_combine(ex, total), epoch, true);
+    }
+    s_excl = ex;
+    if (last_tile) *d_u = ex.nh + total.nh;
+  }
+  __syncthreads();  // sk is no longer read: reused as column staging below
+  const LR ex = s_excl;
+  // index of the link run containing the tile's first key
+  const uint32_t jbase = ex.nh + (first_key != sprev ? 1u : 0u) - 1u;
+  LR run = lr_combine(ex, pre);
+  ColKeyT* sck = reinterpret_cast<ColKeyT*>(sk);
+  const uint64_t dmask = (1ull << b) - 1;
+  // local accumulators (uniform tile): valid, links, srcs, maxlink, maxsrcpk, maxfanout
+  unsigned long long a_valid = 0, a_links = 0, a_srcs = 0, a_mlink = 0, a_msrc = 0, a_mfan = 0;
+  auto win = [&](uint64_t key) -> uint64_t { return wb ? (key >> b2) : 0; };
+  auto emit_link = [&](uint64_t key, uint32_t j, uint32_t count) {
+    const uint32_t slot = j - jbase;
+    sck[slot] = (ColKeyT)((win(key) << b) | (key & dmask));
+    sc[slot] = count;
+    if (uniform)
+      a_mlink = max(a_mlink, (unsigned long long)count);
+    else
+      atomicMax(stats + win(key) * S_COUNT + S_MAXLINK, (unsigned long long)count);
+  };
+  auto close_src = [&](uint64_t key, uint32_t slen, uint32_t ssum) {
+    if (uniform) {
+      a_msrc = max(a_msrc, (unsigned long long)slen);
+      a_mfan = max(a_mfan, (unsigned long long)ssum);
+    } else {
+      unsigned long long* st = stats + win(key) * S_COUNT;
+      atomicMax(st + S_MAXSRCPK, (unsigned long long)slen);
+      atomicMax(st + S_MAXFANOUT, (unsigned long long)ssum);
+    }
+  };
+  prev = prev0;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const uint32_t i = i0 + q;
+    if (i < cnt) {
+      const uint64_t key = k[q];
+      const uint32_t hl = key != prev, hs = (key >> b) != (prev >> b);
+      if (hl && i != 0) emit_link(prev, run.nh - 1, run.llen);
+      if (hs && i != 0) close_src(prev, run.slen, run.ssum);
+      run = lr_combine(run, LR{hl, hl | (hs << 1), 1, 1, hl});
+      if (uniform) {
+        a_valid += 1;
+        a_links += hl;
+        a_srcs += hs;
+      } else {
+        unsigned long long* st = stats + win(key) * S_COUNT;
+        atomicAdd(st + S_VALID, 1ull);
+        if (hl) atomicAdd(st + S_LINKS, 1ull);
+        if (hs) atomicAdd(st + S_SRCS, 1ull);
+      }
+      if (i == cnt - 1) {  // tile tail: close what ends at the tile boundary
+        if (last_tile || snext != key) emit_link(key, run.nh - 1, run.llen);
+        if (last_tile || (snext >> b) != (key >> b)) close_src(key, run.slen, run.ssum);
+      }
+      prev = key;
+    }
+  }
+  if (uniform) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a_valid += __shfl_xor_sync(FULL, a_valid, o);
+      a_links += __shfl_xor_sync(FULL, a_links, o);
+      a_srcs += __shfl_xor_sync(FULL, a_srcs, o);
+      a_mlink = max(a_mlink, __shfl_xor_sync(FULL, a_mlink, o));
+      a_msrc = max(a_msrc, __shfl_xor_sync(FULL, a_msrc, o));
+      a_mfan = max(a_mfan, __shfl_xor_sync(FULL, a_mfan, o));
+    }
+    if (lane == 0) {
+      sm_red[warp][0] = a_valid;
+      sm_red[warp][1] = a_links;
+      sm_red[warp][2] = a_srcs;
+      sm_red[warp][3] = a_mlink;
+      sm_red[warp][4] = a_msrc;
+      sm_red[warp][5] = a_mfan;
+    }
+  }
+  __syncthreads();
+  if (uniform && tid == 0) {
+    unsigned long long r[6] = {0, 0, 0, 0, 0, 0};
+    for (int w = 0; w < kWarps; ++w) {
+      for (int x = 0; x < 3; ++x) r[x] += sm_red[w][x];
+      for (int x = 3; x < 6; ++x) r[x] = max(r[x], sm_red[w][x]);
+    }
+    unsigned long long* st = stats + wfirst * S_COUNT;
+    atomicAdd(st + S_VALID, r[0]);
+    if (r[1]) atomicAdd(st + S_LINKS, r[1]);
+    if (r[2]) atomicAdd(st + S_SRCS, r[2]);
+    if (r[3]) atomicMax(st + S_MAXLINK, r[3]);
+    if (r[4]) atomicMax(st + S_MAXSRCPK, r[4]);
+    if (r[5]) atomicMax(st + S_MAXFANOUT, r[5]);
+  }
+  // column entries of the links closed in this tile: [jbase, jbase + nclosed)
+  const uint32_t nclosed = (ex.nh + total.nh) - jbase - ((last_tile || snext != last_key) ? 0u : 1u);
+  for (uint32_t j = tid; j < nclosed; j += 256) {
+    const ColKeyT ck = sck[j];
+    ckeys[jbase + j] = ck;
+    ccounts[jbase + j] = sc[j];
+    for (int p = 0; p < ncolpass; ++p) atomicAdd(&h[p][(uint32_t)((uint64_t)ck >> (8 * p)) & 0xFFu], 1u);
+  }
+  __syncthreads();
+  for (int i = tid; i < ncolpass * kRadix; i += 256) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(colhist + i, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K6 (tail): destinations, segmented over the sorted column entries.
+// ---------------------------------------------------------------------------
+template <typename ColKeyT, int IPT>
+__global__ void __launch_bounds__(256) col_kernel(const ColKeyT* __restrict__ ckeys,
+                                                 const uint32_t* __restrict__ ccounts, uint32_t u, int b, int wb,
+                                                 CSStatus* status, uint32_t epoch,
+                                                 uint32_t* __restrict__ tile_counter,
+                                                 unsigned long long* __restrict__ stats) {
+  constexpr int TILE = 256 * IPT;
+  __shared__ __align__(16) uint64_t sk[TILE + TILE / 16];
+  __shared__ uint32_t sw[TILE + TILE / 16];
+  __shared__ CS sm_cs[kWarps + 1];
+  __shared__ CS s_excl;
+  __shared__ unsigned long long sm_red[kWarps][3];
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_prev, s_next;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t t0 = (uint64_t)tile * TILE;
+  const uint32_t cnt = (uint32_t)umin64(TILE, (uint64_t)u - t0);
+  const bool last_tile = t0 + cnt == u;
+  for (int j = 0; j < IPT; ++j) {
+    const uint32_t i = j * 256 + tid;
+    if (i < cnt) {
+      sk[pad16(i)] = (uint64_t)ckeys[t0 + i];
+      sw[pad16(i)] = ccounts[t0 + i];
+    }
+  }
+  if (tid == 0) {
+    s_prev = t0 ? (uint64_t)ckeys[t0 - 1] : ~(uint64_t)ckeys[0];
+    s_next = last_tile ? 0 : (uint64_t)ckeys[t0 + cnt];
+  }
+  __syncthreads();
+  const uint64_t first_key = sk[0], last_key = sk[pad16(cnt - 1)];
+  const bool uniform = wb == 0 || (first_key >> b) == (last_key >> b);
+  const uint64_t wfirst = wb ? (first_key >> b) : 0;
+  const uint64_t snext = s_next;
+  auto win = [&](uint64_t key) -> uint64_t { return wb ? (key >> b) : 0; };
+
+  const uint32_t i0 = tid * IPT;
+  uint64_t prev = i0 == 0 ? s_prev : (i0 < cnt ? sk[pad16(i0 - 1)] : 0);
+  const uint64_t prev0 = prev;
+  CS agg = CS::identity();
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const uint32_t i = i0 + q;
+    if (i < cnt) {
+      const uint64_t key = sk[pad16(i)];
+      agg = cs_combine(agg, CS{key != prev, 1, sw[pad16(i)]});
+      prev = key;
+    }
+  }
+  CS total;
+  const CS pre = block_excl_scan_op<CS, cs_combine, cs_shfl_up>(agg, sm_cs, &total);
+  if (tid == 0) {
+    CSStatus* my = status + tile;
+    CS ex = CS::identity();
+    if (tile == 0) {
+      publish<CS, 3>(my, total, epoch, true);
+    } else {
+      publish<CS, 3>(my, total, epoch, false);
+      ex = lookback_op<CS, 3, cs_combine>(status, tile, epoch);
+      publish<CS, 3>(my, cs_combine(ex, total), epoch, true);
     }
     s_excl = ex;
   }
-  __syncthreads();  // everyone done reading sk (k[] in registers)
-#pragma unroll
-  for (int q = 0; q < IPT; ++q) {
-    if ((hmask >> q) & 1u) {
-      sk[off] = k[q];
-      ss[off] = (uint32_t)(t0 + tid * IPT + q);
-      ++off;
-    }
-  }
   __syncthreads();
-  const uint64_t ex = s_excl;
-  for (int j = 0; j < IPT; ++j) {
-    uint32_t i = j * kThreads + tid;
-    if (i < total) {
-      ukeys[ex + i] = sk[i];
-      ustart[ex + i] = ss[i];
-    }
-  }
-  if (tid == 0 && t0 + cnt == m) {
-    *d_u = (uint32_t)(ex + total);
-    ustart[ex + total] = m;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// segmented reduction over one tile of sorted segment keys with weights.
-// Shared by the row (segment = src) and column (segment = dst) kernels.
-// Emits, per window: #segments, max segment length, max segment weight.
-// Segments crossing tiles are stitched by a carry lookback (CarryStatus).
-// ---------------------------------------------------------------------------
-struct SegOut {
-  int s_count, s_maxlen, s_maxsum;  // stat slots
-  int wshift;                        // window = seg >> wshift (wshift >= 64 -> window 0)
-};
-
-__device__ __forceinline__ uint64_t window_of(uint64_t seg, int wshift) { return wshift >= 64 ? 0 : (seg >> wshift); }
-
-template <int IPT>
-struct SegSmem {
-  uint64_t seg[kThreads * IPT];
-  uint32_t w[kThreads * IPT];
-};
-
-template <int IPT>
-__device__ void seg_tile(const SegSmem<IPT>& s, uint32_t cnt, uint32_t tile, bool head0, bool tail_closes,
-                         CarryStatus* __restrict__ cstatus, uint32_t epoch, unsigned long long* __restrict__ stats,
-                         SegOut o, Seg* sm_seg, uint64_t* sm_carry, unsigned long long* sm_red) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  const uint64_t win_first = window_of(s.seg[0], o.wshift);
-  const uint64_t win_last = window_of(s.seg[cnt - 1], o.wshift);
-  const bool uniform = win_first == win_last;
-
-  // pass 1: thread aggregate
-  Seg agg{0, 0, 0};
-  uint32_t nheads = 0;
-  for (int q = 0; q < IPT; ++q) {
-    const uint32_t i = tid * IPT + q;
-    if (i >= cnt) break;
-    const bool h = i == 0 ? head0 : (s.seg[i] != s.seg[i - 1]);
-    const uint32_t w = s.w[i];
-    if (h) {
-      agg = Seg{1, 1, w};
-      ++nheads;
-    } else {
-      agg.len += 1;
-      agg.sum += w;
-    }
-  }
-  Seg total;
-  Seg pre = block_excl_segscan(agg, sm_seg, &total);
-
-  // carry-in for the tile's first segment (if it started in an earlier tile).
-  // A tile with a head publishes its last segment's partial as final (INC)
-  // at once; a tile without one publishes AGG, looks back, then INC.
-  if (tid == 0) {
-    CarryStatus* my = cstatus + tile;
-    if (total.f) {
-      st_relaxed(&my->inc_len, total.len);
-      st_relaxed(&my->inc_sum, total.sum);
-      st_release(&my->flag, ((uint64_t)epoch << 2) | kFlagInc);
-    } else {
-      st_relaxed(&my->agg_len, total.len);
-      st_relaxed(&my->agg_sum, total.sum);
-      st_release(&my->flag, ((uint64_t)epoch << 2) | kFlagAgg);
-    }
-    uint64_t clen = 0, csum = 0;
-    if (!head0) {  // implies tile > 0
-      for (int64_t p = (int64_t)tile - 1; p >= 0;) {
-        const uint64_t f = ld_acquire(&cstatus[p].flag);
-        if ((uint32_t)(f >> 2) != epoch) continue;
-        if ((f & 3) == kFlagInc) {
-          clen += ld_relaxed(&cstatus[p].inc_len);
-          csum += ld_relaxed(&cstatus[p].inc_sum);
-          break;
-        }
-        clen += ld_relaxed(&cstatus[p].agg_len);
-        csum += ld_relaxed(&cstatus[p].agg_sum);
-        --p;
-      }
-    }
-    if (!total.f) {
-      st_relaxed(&my->inc_len, clen + total.len);
-      st_relaxed(&my->inc_sum, csum + total.sum);
-      st_release(&my->flag, ((uint64_t)epoch << 2) | kFlagInc);
-    }
-    sm_carry[0] = clen;
-    sm_carry[1] = csum;
-  }
-  __syncthreads();
-  if (!pre.f) {  // still inside the tile's first segment: add the carry
-    pre.len += (uint32_t)sm_carry[0];
-    pre.sum += sm_carry[1];
-  }
-
-  // pass 2: close segments (segment lengths < 2^32: the API bounds m < 2^32)
-  unsigned long long lmaxlen = 0, lmaxsum = 0;
-  auto close_seg = [&](uint64_t seg, uint64_t len, uint64_t sum) {
+  CS run = cs_combine(s_excl, pre);
+  unsigned long long a_cnt = 0, a_len = 0, a_sum = 0;
+  auto close = [&](uint64_t key, uint32_t len, uint32_t sum) {
     if (uniform) {
-      lmaxlen = max(lmaxlen, (unsigned long long)len);
-      lmaxsum = max(lmaxsum, (unsigned long long)sum);
+      a_len = max(a_len, (unsigned long long)len);
+      a_sum = max(a_sum, (unsigned long long)sum);
     } else {
-      const uint64_t wdw = window_of(seg, o.wshift);
-      atomicMax(stats + wdw * S_COUNT + o.s_maxlen, (unsigned long long)len);
-      atomicMax(stats + wdw * S_COUNT + o.s_maxsum, (unsigned long long)sum);
+      unsigned long long* st = stats + win(key) * S_COUNT;
+      atomicMax(st + S_MAXFANIN, (unsigned long long)len);
+      atomicMax(st + S_MAXDSTPK, (unsigned long long)sum);
     }
   };
-  Seg run = pre;
+  prev = prev0;
+#pragma unroll
   for (int q = 0; q < IPT; ++q) {
-    const uint32_t i = tid * IPT + q;
-    if (i >= cnt) break;
-    const bool h = i == 0 ? head0 : (s.seg[i] != s.seg[i - 1]);
-    const uint32_t w = s.w[i];
-    if (h) {
-      if (i > 0) close_seg(s.seg[i - 1], run.len, run.sum);
-      if (!uniform) atomicAdd(stats + window_of(s.seg[i], o.wshift) * S_COUNT + o.s_count, 1ull);
-      run = Seg{1, 1, w};
-    } else {
-      run.len += 1;
-      run.sum += w;
+    const uint32_t i = i0 + q;
+    if (i < cnt) {
+      const uint64_t key = sk[pad16(i)];
+      const uint32_t h = key != prev;
+      if (h && i != 0) close(prev, run.len, run.sum);
+      run = cs_combine(run, CS{h, 1, sw[pad16(i)]});
+      if (uniform)
+        a_cnt += h;
+      else if (h)
+        atomicAdd(stats + win(key) * S_COUNT + S_DSTS, 1ull);
+      if (i == cnt - 1 && (last_tile || snext != key)) close(key, run.len, run.sum);
+      prev = key;
     }
-    if (i == cnt - 1 && tail_closes) close_seg(s.seg[i], run.len, run.sum);
   }
   if (uniform) {
-    // block reduce: count (sum), maxlen, maxsum
-    unsigned long long c = nheads;
 #pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      c += __shfl_xor_sync(FULL, c, off);
-      lmaxlen = max(lmaxlen, __shfl_xor_sync(FULL, lmaxlen, off));
-      lmaxsum = max(lmaxsum, __shfl_xor_sync(FULL, lmaxsum, off));
+    for (int o = 16; o; o >>= 1) {
+      a_cnt += __shfl_xor_sync(FULL, a_cnt, o);
+      a_len = max(a_len, __shfl_xor_sync(FULL, a_len, o));
+      a_sum = max(a_sum, __shfl_xor_sync(FULL, a_sum, o));
     }
-    const int warp = tid >> 5;
     if (lane == 0) {
-      sm_red[warp * 3 + 0] = c;
-      sm_red[warp * 3 + 1] = lmaxlen;
-      sm_red[warp * 3 + 2] = lmaxsum;
+      sm_red[warp][0] = a_cnt;
+      sm_red[warp][1] = a_len;
+      sm_red[warp][2] = a_sum;
     }
     __syncthreads();
     if (tid == 0) {
-      unsigned long long a = 0, b2 = 0, c2 = 0;
+      unsigned long long r0 = 0, r1 = 0, r2 = 0;
       for (int w = 0; w < kWarps; ++w) {
-        a += sm_red[w * 3];
-        b2 = max(b2, sm_red[w * 3 + 1]);
-        c2 = max(c2, sm_red[w * 3 + 2]);
+        r0 += sm_red[w][0];
+        r1 = max(r1, sm_red[w][1]);
+        r2 = max(r2, sm_red[w][2]);
       }
-      unsigned long long* st = stats + win_first * S_COUNT;
-      if (a) atomicAdd(st + o.s_count, a);
-      if (b2) atomicMax(st + o.s_maxlen, b2);
-      if (c2) atomicMax(st + o.s_maxsum, c2);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K5: links + rows. Items are unique links j in [0,u): key, count = ustart[j+1]-ustart[j].
-// Writes the column keys (win<<b | dst) and counts, plus their digit histograms.
-// ---------------------------------------------------------------------------
-template <typename ColKeyT, int IPT>
-__global__ void __launch_bounds__(kThreads) row_kernel(const uint64_t* __restrict__ ukeys,
-                                                      const uint32_t* __restrict__ ustart, uint32_t u, int b,
-                                                      int wb, ColKeyT* __restrict__ ckeys,
-                                                      uint32_t* __restrict__ ccounts, int ncolpass,
-                                                      uint32_t* __restrict__ colhist, CarryStatus* cstatus,
-                                                      uint32_t epoch, uint32_t* __restrict__ tile_counter,
-                                                      unsigned long long* __restrict__ stats) {
-  constexpr int TILE = kThreads * IPT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& s = *reinterpret_cast<SegSmem<IPT>*>(smem_raw);
-  __shared__ uint32_t h[4][kRadix];  // <= 4 column passes when ColKeyT is u32; u64 uses up to 5 -> see host
-  __shared__ uint32_t h5[kRadix * 4];
-  __shared__ Seg sm_seg[kWarps + 1];
-  __shared__ uint64_t sm_carry[2];
-  __shared__ unsigned long long sm_red[kWarps * 3];
-  __shared__ uint32_t s_tile;
-  __shared__ uint64_t s_prevseg;
-  __shared__ int s_head0, s_tailc;
-  const int tid = threadIdx.x;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < 4 * kRadix; i += kThreads) {
-    (&h[0][0])[i] = 0;
-    h5[i] = 0;
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t t0 = (uint64_t)tile * TILE;
-  const uint32_t cnt = (uint32_t)umin64(TILE, (uint64_t)u - t0);
-  const uint64_t dmask = (b >= 64) ? ~0ull : ((1ull << b) - 1);
-  const bool uniform_w = (wb == 0) || ((ukeys[t0] >> (2 * b)) == (ukeys[t0 + cnt - 1] >> (2 * b)));
-  const uint64_t wfirst = wb ? (ukeys[t0] >> (2 * b)) : 0;
-
-  unsigned long long links = 0, valid = 0, maxlink = 0;
-  for (int j = 0; j < IPT; ++j) {
-    const uint32_t i = j * kThreads + tid;
-    if (i < cnt) {
-      const uint64_t key = ukeys[t0 + i];
-      const uint32_t c = ustart[t0 + i + 1] - ustart[t0 + i];
-      const uint64_t wdw = wb ? (key >> (2 * b)) : 0;
-      const ColKeyT ck = (ColKeyT)((wdw << b) | (key & dmask));
-      ckeys[t0 + i] = ck;
-      ccounts[t0 + i] = c;
-      for (int p = 0; p < ncolpass; ++p) {
-        const uint32_t d = (uint32_t)((uint64_t)ck >> (8 * p)) & 0xFFu;
-        if (p < 4)
-          atomicAdd(&h[p][d], 1u);
-        else
-          atomicAdd(&h5[(p - 4) * kRadix + d], 1u);
-      }
-      s.seg[i] = key >> b;
-      s.w[i] = c;
-      if (uniform_w) {
-        links += 1;
-        valid += c;
-        maxlink = max(maxlink, (unsigned long long)c);
-      } else {
-        unsigned long long* st = stats + wdw * S_COUNT;
-        atomicAdd(st + S_LINKS, 1ull);
-        atomicAdd(st + S_VALID, (unsigned long long)c);
-        atomicMax(st + S_MAXLINK, (unsigned long long)c);
-      }
-    }
-  }
-  if (tid == 0) {
-    s_prevseg = t0 ? (ukeys[t0 - 1] >> b) : 0;
-    s_head0 = t0 == 0 ? 1 : 0;
-    const bool last = t0 + cnt == u;
-    s_tailc = last ? 1 : ((ukeys[t0 + cnt] >> b) != (ukeys[t0 + cnt - 1] >> b));
-  }
-  __syncthreads();
-  if (tid == 0 && t0) s_head0 = s.seg[0] != s_prevseg;
-  if (uniform_w) {
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      links += __shfl_xor_sync(FULL, links, off);
-      valid += __shfl_xor_sync(FULL, valid, off);
-      maxlink = max(maxlink, __shfl_xor_sync(FULL, maxlink, off));
-    }
-    if ((tid & 31) == 0) {
       unsigned long long* st = stats + wfirst * S_COUNT;
-      atomicAdd(st + S_LINKS, links);
-      atomicAdd(st + S_VALID, valid);
-      atomicMax(st + S_MAXLINK, maxlink);
+      if (r0) atomicAdd(st + S_DSTS, r0);
+      if (r1) atomicMax(st + S_MAXFANIN, r1);
+      if (r2) atomicMax(st + S_MAXDSTPK, r2);
     }
   }
-  __syncthreads();
-  for (int i = tid; i < ncolpass * kRadix; i += kThreads) {
-    const int p = i / kRadix, d = i % kRadix;
-    const uint32_t v = p < 4 ? h[p][d] : h5[(p - 4) * kRadix + d];
-    if (v) atomicAdd(colhist + i, v);
-  }
-  seg_tile<IPT>(s, cnt, tile, s_head0 != 0, s_tailc != 0, cstatus, epoch, stats,
-                SegOut{S_SRCS, S_MAXFANOUT, S_MAXSRCPK, wb ? b : 64}, sm_seg, sm_carry, sm_red);
-}
-
-// ---------------------------------------------------------------------------
-// K6 (tail): destinations, segmented over sorted column keys.
-// ---------------------------------------------------------------------------
-template <typename ColKeyT, int IPT>
-__global__ void __launch_bounds__(kThreads) col_kernel(const ColKeyT* __restrict__ ckeys,
-                                                      const uint32_t* __restrict__ ccounts, uint32_t u, int b,
-                                                      int wb, CarryStatus* cstatus, uint32_t epoch,
-                                                      uint32_t* __restrict__ tile_counter,
-                                                      unsigned long long* __restrict__ stats) {
-  constexpr int TILE = kThreads * IPT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& s = *reinterpret_cast<SegSmem<IPT>*>(smem_raw);
-  __shared__ Seg sm_seg[kWarps + 1];
-  __shared__ uint64_t sm_carry[2];
-  __shared__ unsigned long long sm_red[kWarps * 3];
-  __shared__ uint32_t s_tile;
-  __shared__ int s_head0, s_tailc;
-  const int tid = threadIdx.x;
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t t0 = (uint64_t)tile * TILE;
-  const uint32_t cnt = (uint32_t)umin64(TILE, (uint64_t)u - t0);
-  for (int j = 0; j < IPT; ++j) {
-    const uint32_t i = j * kThreads + tid;
-    if (i < cnt) {
-      s.seg[i] = (uint64_t)ckeys[t0 + i];
-      s.w[i] = ccounts[t0 + i];
-    }
-  }
-  if (tid == 0) {
-    s_head0 = t0 == 0 ? 1 : ((uint64_t)ckeys[t0 - 1] != (uint64_t)ckeys[t0]);
-    const bool last = t0 + cnt == u;
-    s_tailc = last ? 1 : ((uint64_t)ckeys[t0 + cnt] != (uint64_t)ckeys[t0 + cnt - 1]);
-  }
-  __syncthreads();
-  seg_tile<IPT>(s, cnt, tile, s_head0 != 0, s_tailc != 0, cstatus, epoch, stats,
-                SegOut{S_DSTS, S_MAXFANIN, S_MAXDSTPK, wb ? b : 64}, sm_seg, sm_carry, sm_red);
 }
 
 // ---------------------------------------------------------------------------
