@@ -1,0 +1,337 @@
+"""Benchmark: packets/s for traffic-matrix build + 9 statistics (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 3 -- 2^30 packets uniform over the 2^32 address
+space (splitmix64 generator), summed into one hypersparse
+traffic matrix, nine Graph Challenge statistics. One step = one full pass of
+the hot path (ingest -> onesweep sort -> unique links/rows -> column sort ->
+columns -> 9 int64 to host) over the whole batch.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nmx|reference]
+                  [--config cfg3|cfg4|cfg2|cfg1] [--log2n L]
+
+N > 1 is launched by torchrun (one rank per GPU): the 2^30 packets are sharded
+across ranks and exchanged by owner(src) / owner(dst) over NCCL
+(paper_2510_14050_b200/distributed.py), total work fixed -> "scaling": "strong".
+
+`--impl reference` times the reference's CPU path (the numpy port in
+oracle/netmeter_oracle.py of build_matrices -> to_flat -> analyze_matrix, the
+reference is pure Python and cannot travel to the GPU box) on the host cores,
+rank 0 only, on a bounded sample of the same workload per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "packets/sec for traffic-matrix build + 9 stats at 1/2/4/8 B200; % HBM roofline"
+CONFIGS = {
+    # name: (log2 n, address space, generator)
+    "cfg3": (30, 1 << 32, "uniform"),
+    "cfg4": (30, 1 << 32, "powerlaw"),
+    "cfg2": (23, 1 << 24, "uniform"),
+    "cfg1": (17, 1 << 18, "uniform"),
+}
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_port_rate(log2n: int, space: int, gen: str, reps: int = 1):
+    """The reference's CPU path (numpy port) on a bounded sample: packets/s."""
+    import numpy as np
+
+    from oracle import netmeter_oracle as orc
+
+    g = orc.gen_uniform if gen == "uniform" else orc.gen_powerlaw
+    s, d = g(7, 0, 1 << log2n, space)
+    cs, cd, dim = orc.compact_ids(s, d)  # excluded from timing
+    valid = np.ones(len(cs), dtype=bool)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.ref_stats9(cs, cd, valid, dim)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return (1 << log2n) / best, best
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    log2n, space, gen = CONFIGS[args.config]
+    sample = min(log2n, args.ref_log2n)
+    for _ in range(args.warmup):
+        cpu_port_rate(sample, space, gen)
+    rates = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, _ = cpu_port_rate(sample, space, gen)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    value = statistics.median(rates)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: 2^{log2n} packets {gen} over {space} addresses, summed matrix, 9 stats",
+                   "sample": f"2^{sample} packets of the same generator per step (ids compacted outside the timed region)"},
+        "cpu_baseline": {"value": value, "unit": "packets/s", "cores": 1, "kind": "port",
+                         "sample": f"2^{sample} packets/step; oracle/netmeter_oracle.py ref_stats9 = numpy port of "
+                                   "traffic.py:197-292 + analytics.py:95-106 (numpy build is single-threaded)"},
+        "e2e": {"value": value, "unit": "packets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_nmx(args) -> None:
+    import torch
+
+    from paper_2510_14050_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    log2n, space, gen = CONFIGS[args.config]
+    if args.log2n:
+        log2n = args.log2n
+    n_total = 1 << log2n
+    kind = _lib.GEN_UNIFORM if gen == "uniform" else _lib.GEN_POWERLAW
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = _lib.context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    # this rank's contiguous shard of the packet stream (partition_even rule)
+    base, rem = divmod(n_total, world)
+    n = base + (1 if rank < rem else 0)
+    off = rank * base + min(rank, rem)
+    ds, dd = _lib.DeviceArray(n, device=local), _lib.DeviceArray(n, device=local)
+    _lib.generate(kind, 7, off, n, space, ds, dd, device=local)  # this rank's shard, chunk-addressable
+
+    if world > 1:
+        from paper_2510_14050_b200 import distributed as nd
+
+        def step():
+            return nd.sharded_stats9_device(ds, dd, space, device=local)
+    else:
+        def step():
+            return _lib.stats9(ds, dd, None, space, device=local)
+
+    for _ in range(args.warmup):
+        stats = step()
+    timing_last = ctx.last_timing()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(local)
+
+    # ---- device-resident timed region (value) ----
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sort_ms, sort_launch, launches, totals = 0.0, 0, 0, []
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            stats = step()
+            t = ctx.last_timing()
+            sort_ms += t["sort_ms"]
+            sort_launch += t["sort_launches"]
+            launches += t["kernel_launches"]
+            totals.append(t)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        mt = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        ms = float(mt.item())
+    ms_per_step = ms / args.steps
+    value = n_total / (ms_per_step / 1e3)
+
+    # ---- end-to-end through the public C-ABI host entry (pinned host buffers) ----
+    e2e = None
+    if not args.no_e2e:
+        hs, hd = _lib.PinnedArray(n), _lib.PinnedArray(n)
+        hs.array[:] = ds.download()
+        hd.array[:] = dd.download()
+        if world > 1:
+            from paper_2510_14050_b200 import distributed as nd
+
+            def hstep():
+                return nd.sharded_stats9_host(hs.array, hd.array, space, device=local)
+        else:
+            def hstep():
+                return _lib.stats9(hs.array, hd.array, None, space, device=local)
+        hstats = hstep()
+        assert hstats == stats, (hstats, stats)
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            hstep()
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1) / args.e2e_steps
+        if dist is not None:
+            mt = torch.tensor([ems], device=f"cuda:{local}")
+            dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+            ems = float(mt.item())
+        e2e = {"value": n_total / (ems / 1e3), "unit": "packets/s", "h2d_bytes_per_step": 8 * n_total,
+               "d2h_bytes_per_step": 72 * world, "ms_per_step": ems, "steps": args.e2e_steps,
+               "api": "nmx_stats9_host (include/nmx.h) via paper_2510_14050_b200._lib.stats9, pinned host buffers"}
+        hs.close()
+        hd.close()
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_kind = _peaks()
+    # dominant kernel: the onesweep LSD pass (16 B of key traffic per packet per launch)
+    pass_ms = sort_ms / max(sort_launch, 1)
+    bytes_per_launch = 16 * n
+    achieved = bytes_per_launch / (pass_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "onesweep_pass (row sort, u64 keys)", "achieved": round(achieved, 1),
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+            "peak_kind": peak_kind, "traffic": None,
+            "bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(pass_ms, 4),
+            "note": "algorithmic bytes = 8 B read + 8 B write per key per pass (SURVEY.md 8(d)); traffic: see "
+                    "profiles/ (ncu dram__bytes per launch)"}
+    # whole-step algorithmic bytes: n(16+16P) + u(36+16Pc), P = 2*ceil(b/8), Pc = ceil(b/8)
+    b = 32 if space == 1 << 32 else max(1, (space - 1).bit_length())
+    P, Pc = 2 * ((b + 7) // 8), (b + 7) // 8
+    u = stats[1]
+    b_alg = n_total * (16 + 16 * P) + u * (36 + 16 * Pc)
+    whole = b_alg / (ms_per_step / 1e3) / 1e9
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        sample = min(log2n, args.cpu_log2n)
+        rate, secs = cpu_port_rate(sample, space, gen, reps=2)
+        cpu = {"value": rate, "unit": "packets/s", "cores": 1, "kind": "port",
+               "sample": f"2^{sample} packets of the {args.config} generator, best of 2 ({secs:.2f} s each); "
+                         "oracle/netmeter_oracle.py ref_stats9 (numpy port of traffic.py:197-292 + "
+                         "analytics.py:95-106; ids compacted outside the timed region)"}
+    stage_ms = timing_last.get("stages_ms", [])
+    line = {
+        "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: 2^{log2n} packets {gen} over {space} addresses (splitmix64, "
+                               "SURVEY.md 8(d)) summed into one traffic matrix, 9 statistics",
+                   "packets": n_total, "address_space": space, "parallelism": f"shards{world}",
+                   "l2": "inputs (8 GiB) and sort buffers larger than L2; no flush needed"},
+        "stats9": list(stats),
+        "roofline": roof,
+        "whole_step": {"b_alg_bytes": b_alg, "achieved_gbs": round(whole, 1),
+                       "frac": round(whole / peaks["hbm_gbs"], 4), "stages_ms": stage_ms,
+                       "stages": ["hist+plan", "row sort", "link/row", "col sort", "col+d2h"]},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="nmx", choices=["nmx", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--log2n", type=int, default=0)
+    ap.add_argument("--ref-log2n", type=int, default=22, help="reference-arm sample per step")
+    ap.add_argument("--cpu-log2n", type=int, default=24, help="cpu_baseline sample (about 10-30 s of CPU work)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_nmx(args)
+
+
+if __name__ == "__main__":
+    main()

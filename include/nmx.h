@@ -97,6 +97,23 @@ int nmx_window_stats9_host(nmx_ctx* ctx, const uint32_t* src, const uint32_t* ds
  * INT64_MIN for an empty view (the Python layer maps it to 0). */
 int nmx_reduce_i64(nmx_ctx* ctx, const int64_t* data, uint64_t n, int op, int64_t* out);
 
+/* Multi-GPU building blocks (one process per GPU; the exchange itself is NCCL
+ * all-to-all driven by paper_2510_14050_b200/distributed.py). owner(x) =
+ * (fmix32(x) * nparts) >> 32, nparts <= 64. Counts are written to host arrays.
+ *  - nmx_partition_packets: route valid packets by owner(src) into
+ *    part-contiguous output columns (capacity n each);
+ *  - nmx_shard_rows: link + row statistics of packets whose sources this rank
+ *    owns (fields 0-5 of stats9 exact; 6-8 zero) and its unique links' (dst,
+ *    count) column entries routed by owner(dst) (capacity n each);
+ *  - nmx_shard_cols: column statistics (fields 6-8) of received column entries.
+ * No reference counterpart: the reference is single-process. */
+int nmx_partition_packets(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                          uint64_t n, int nparts, uint32_t* d_out_src, uint32_t* d_out_dst, uint64_t* counts);
+int nmx_shard_rows(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, uint64_t address_space,
+                   int nparts, uint32_t* d_out_dst, uint32_t* d_out_count, uint64_t* counts, int64_t out[9]);
+int nmx_shard_cols(nmx_ctx* ctx, const uint32_t* d_dst, const uint32_t* d_count, uint64_t u, uint64_t address_space,
+                   int64_t out[9]);
+
 /* Timing hooks used by bench.py: CUDA-event time (ms) of the last hot-path
  * call's whole device section, and of its dominant kernel class (the onesweep
  * passes) summed over launches, plus the number of kernels it launched. */

@@ -50,6 +50,9 @@ SIGNATURES = {
     "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_window_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_reduce_i64": (C.c_int, [_VP, _VP, _U64, C.c_int, _VP]),
+    "nmx_partition_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.c_int, _VP, _VP, _VP]),
+    "nmx_shard_rows": (C.c_int, [_VP, _VP, _VP, _U64, _U64, C.c_int, _VP, _VP, _VP, _VP]),
+    "nmx_shard_cols": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_last_stages": (C.c_int, [_VP, C.POINTER(C.c_float), C.c_int]),
     "nmx_last_timing": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_int),
                                   C.POINTER(C.c_int)]),

@@ -105,7 +105,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf keysA, keysB, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, stats, in_src, in_dst, in_valid,
+  DevBuf keysA, keysB, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
@@ -118,6 +118,7 @@ struct nmx_ctx {
   int last_nstage = 0;
   int last_sort_launches = 0, last_launches = 0;
   int launches = 0;
+  uint64_t* sorted_keys = nullptr;  // last row sort output (materialisation)
 
   uint32_t next_epoch() {
     if (++epoch >= (1u << 22)) {
@@ -255,25 +256,47 @@ void launch_hist(nmx_ctx* c, const PacketSrc& ps, int npass, uint32_t* d_small) 
   ++c->launches;
 }
 
-// The whole pipeline over packet columns already on the device. Writes W*9
-// statistics (u64) into c->h_stats. Windows: window_size == 0 -> one window.
-void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
-                  int b, uint64_t window_size, uint64_t W) {
-  const int wb = W > 1 ? (int)ceil_log2(W) : 0;
-  const int kb = 2 * b + wb;
-  const int npass = (kb + 7) / 8;
+// ---- pipeline stages -------------------------------------------------------
+void stage_begin(nmx_ctx* c, uint64_t W) {
   c->nev = 0;
   c->launches = 0;
+  c->last_sort_launches = 0;
+  c->last_sort_ms = 0;
   c->small.grow(kSmallWords * sizeof(uint32_t));
   if (!c->h_small) CK(cudaMallocHost(&c->h_small, kSmallWords * sizeof(uint32_t)));
   c->stats.grow(W * S_COUNT * sizeof(unsigned long long));
   c->grow_hstats(W * S_COUNT);
-  uint32_t* d_small = c->small.as<uint32_t>();
   c->mark();  // 0: start
-  CK(cudaMemsetAsync(d_small, 0, kSmallWords * sizeof(uint32_t), c->st));
+  CK(cudaMemsetAsync(c->small.p, 0, kSmallWords * sizeof(uint32_t), c->st));
   CK(cudaMemsetAsync(c->stats.p, 0, W * S_COUNT * sizeof(unsigned long long), c->st));
+}
 
-  PacketSrc ps{d_src, d_dst, d_valid, n, W > 1 ? window_size : 0, b};
+void stage_finish(nmx_ctx* c, uint64_t W) {
+  CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     c->st));
+  c->mark();  // end
+  CK(cudaStreamSynchronize(c->st));
+  CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
+  if (c->nev >= 3 && c->last_sort_launches) CK(cudaEventElapsedTime(&c->last_sort_ms, c->ev[1], c->ev[2]));
+  c->last_nstage = 0;
+  for (int i = 0; i + 1 < c->nev && i < 8; ++i) CK(cudaEventElapsedTime(&c->last_stage_ms[i], c->ev[i], c->ev[i + 1]));
+  c->last_nstage = std::min(c->nev - 1, 8);
+  c->last_launches = c->launches;
+}
+
+struct RowsOut {
+  uint64_t m;  // valid packets
+  uint32_t u;  // unique links (column entries in ckA/cvA, link order)
+  bool wide;   // column keys are u64
+};
+
+// hist -> onesweep row sort -> fused link/row kernel. Link + row statistics
+// accumulate into c->stats; the column entries are left in c->ckA / c->cvA.
+RowsOut stage_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb) {
+  const uint64_t n = ps.n;
+  const int kb = 2 * b + wb;
+  const int npass = (kb + 7) / 8;
+  uint32_t* d_small = c->small.as<uint32_t>();
   launch_hist(c, ps, npass, d_small);
   bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kHist, npass, d_small + kBase);
   CK_LAUNCH();
@@ -281,20 +304,10 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
   CK(cudaMemcpyAsync(c->h_small, d_small, kSmallWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   const uint64_t m = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
-  c->last_sort_launches = 0;
-  c->last_sort_ms = 0;
-  if (m == 0) {
-    CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                       c->st));
-    c->mark();
-    CK(cudaStreamSynchronize(c->st));
-    CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
-    c->last_launches = c->launches;
-    return;
-  }
+  const bool wide = b + wb > 32;
+  if (m == 0) return RowsOut{0, 0, wide};
   if (m >= (1ull << 32)) throw std::runtime_error("more than 2^32-1 valid packets in one call");
 
-  // ---- row sort (LSD onesweep over the packed key) ----
   std::vector<int> active;
   for (int p = 0; p < npass; ++p) {
     const uint32_t* hp = c->h_small + kHist + p * kRadix;
@@ -324,9 +337,8 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
   }
   c->last_sort_launches = (int)active.size();
   c->mark();  // 2: sort end
+  c->sorted_keys = keys;
 
-  // ---- unique links + rows (fused), then columns ----
-  const bool wide = b + wb > 32;
   c->ckA.grow(m * (wide ? 8 : 4));
   c->ckB.grow(m * (wide ? 8 : 4));
   c->cvA.grow(m * 4);
@@ -342,21 +354,59 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
   c->mark();  // 3: link/row end
   CK(cudaMemcpyAsync(c->h_small + kU, d_small + kU, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  const uint32_t u = c->h_small[kU];
+  return RowsOut{m, c->h_small[kU], wide};
+}
+
+// column sort + column kernel over the u entries in c->ckA / c->cvA (whose
+// digit histograms are in small[kCHist]).
+void stage_cols(nmx_ctx* c, uint32_t u, int b, int wb, bool wide) {
+  if (!u) return;
+  uint32_t* d_small = c->small.as<uint32_t>();
   c->grow_status(tiles_of(u, kMinPassTile) * kRadix);
   if (wide)
     column_phase<uint64_t>(c, u, b, wb, d_small);
   else
     column_phase<uint32_t>(c, u, b, wb, d_small);
-  CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                     c->st));
-  c->mark();  // 5: end
+}
+
+// The whole pipeline over packet columns already on the device. Writes W*9
+// statistics (u64) into c->h_stats. Windows: window_size == 0 -> one window.
+void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                  int b, uint64_t window_size, uint64_t W) {
+  const int wb = W > 1 ? (int)ceil_log2(W) : 0;
+  stage_begin(c, W);
+  PacketSrc ps{d_src, d_dst, d_valid, n, W > 1 ? window_size : 0, b};
+  const RowsOut r = stage_rows(c, ps, b, wb);
+  stage_cols(c, r.u, b, wb, r.wide);
+  stage_finish(c, W);
+}
+
+// ---- owner partitions for the multi-GPU exchange ----------
+// returns per-part counts on the host; items scattered part-contiguously
+template <typename Item>
+void partition_items(nmx_ctx* c, const Item& it, uint64_t n, int nparts, uint64_t* counts_host) {
+  c->part.grow(2 * kMaxParts * sizeof(unsigned long long));
+  auto* d_counts = c->part.as<unsigned long long>();
+  auto* d_cursor = d_counts + kMaxParts;
+  CK(cudaMemsetAsync(d_counts, 0, kMaxParts * sizeof(unsigned long long), c->st));
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, (uint64_t)c->sms * 4));
+  part_count_kernel<Item><<<grid, 256, 0, c->st>>>(it, n, nparts, d_counts);
+  CK_LAUNCH();
+  unsigned long long hc[kMaxParts];
+  CK(cudaMemcpyAsync(hc, d_counts, sizeof(hc), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
-  CK(cudaEventElapsedTime(&c->last_sort_ms, c->ev[1], c->ev[2]));
-  for (int i = 0; i + 1 < c->nev && i < 8; ++i) CK(cudaEventElapsedTime(&c->last_stage_ms[i], c->ev[i], c->ev[i + 1]));
-  c->last_nstage = std::min(c->nev - 1, 8);
-  c->last_launches = c->launches;
+  unsigned long long base[kMaxParts], acc = 0;
+  for (int p = 0; p < nparts; ++p) {
+    base[p] = acc;
+    acc += hc[p];
+    counts_host[p] = hc[p];
+  }
+  CK(cudaMemcpyAsync(d_cursor, base, sizeof(unsigned long long) * nparts, cudaMemcpyHostToDevice, c->st));
+  const uint64_t chunk = (n + grid - 1) / grid;
+  part_scatter_kernel<Item><<<grid, 256, 0, c->st>>>(it, n, chunk, nparts, d_cursor);
+  CK_LAUNCH();
+  c->launches += 2;
+  CK(cudaStreamSynchronize(c->st));
 }
 
 template <typename F>
@@ -495,7 +545,7 @@ void nmx_destroy(nmx_ctx* c) {
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   for (DevBuf* b : {&c->keysA, &c->keysB, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
-                    &c->csstatus, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
+                    &c->csstatus, &c->part, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
     b->release();
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_stats) cudaFreeHost(c->h_stats);
@@ -629,6 +679,81 @@ int nmx_reduce_i64(nmx_ctx* c, const int64_t* data, uint64_t n, int op, int64_t*
     CK(cudaMemcpyAsync(&r, d_out, 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     *out = (int64_t)r;
+    return NMX_OK;
+  });
+}
+
+int nmx_partition_packets(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                          uint64_t n, int nparts, uint32_t* d_out_src, uint32_t* d_out_dst, uint64_t* counts) {
+  if (nparts < 1 || nparts > kMaxParts) return fail(NMX_EINVAL, "nparts must lie in [1, %d]", kMaxParts);
+  if (!counts) return fail(NMX_EINVAL, "null counts");
+  return guarded(c, [&] {
+    if (!n) {
+      std::fill(counts, counts + nparts, 0);
+      return NMX_OK;
+    }
+    PacketPart it{d_src, d_dst, d_valid, d_out_src, d_out_dst};
+    partition_items(c, it, n, nparts, counts);
+    return NMX_OK;
+  });
+}
+
+int nmx_shard_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, uint64_t address_space,
+                   int nparts, uint32_t* d_out_dst, uint32_t* d_out_count, uint64_t* counts, int64_t out[9]) {
+  if (nparts < 1 || nparts > kMaxParts) return fail(NMX_EINVAL, "nparts must lie in [1, %d]", kMaxParts);
+  if (!counts || !out) return fail(NMX_EINVAL, "null output");
+  int b;
+  if (int r = check_space(address_space, b)) return r;
+  if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call");
+  return guarded(c, [&] {
+    std::fill(out, out + S_COUNT, 0);
+    std::fill(counts, counts + nparts, 0);
+    if (!n) return NMX_OK;
+    stage_begin(c, 1);
+    PacketSrc ps{d_src, d_dst, nullptr, n, 0, b};
+    const RowsOut r = stage_rows(c, ps, b, 0);
+    if (r.u) {
+      ColPart it{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), d_out_dst, d_out_count};
+      partition_items(c, it, r.u, nparts, counts);
+    }
+    stage_finish(c, 1);
+    copy_out9(c->h_stats, out, 1);
+    return NMX_OK;
+  });
+}
+
+int nmx_shard_cols(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, uint64_t u, uint64_t address_space,
+                   int64_t out[9]) {
+  if (!out) return fail(NMX_EINVAL, "null output");
+  int b;
+  if (int r = check_space(address_space, b)) return r;
+  if (u >= (1ull << 32)) return fail(NMX_EINVAL, "u must be < 2^32 per call");
+  return guarded(c, [&] {
+    std::fill(out, out + S_COUNT, 0);
+    if (!u) return NMX_OK;
+    stage_begin(c, 1);
+    c->ckA.grow(u * 4);
+    c->ckB.grow(u * 4);
+    c->cvA.grow(u * 4);
+    c->cvB.grow(u * 4);
+    if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
+      CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+    CK(cudaMemcpyAsync(c->ckA.p, d_dst, u * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->cvA.p, d_count, u * 4, cudaMemcpyDeviceToDevice, c->st));
+    const int ncolpass = (b + 7) / 8;
+    uint32_t* d_small = c->small.as<uint32_t>();
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((u + 1023) / 1024, (uint64_t)c->sms * 8));
+    switch (ncolpass) {
+      case 1: hist_u32_kernel<1><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+      case 2: hist_u32_kernel<2><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+      case 3: hist_u32_kernel<3><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+      default: hist_u32_kernel<4><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+    }
+    CK_LAUNCH();
+    ++c->launches;
+    stage_cols(c, (uint32_t)u, b, 0, false);
+    stage_finish(c, 1);
+    copy_out9(c->h_stats, out, 1);
     return NMX_OK;
   });
 }

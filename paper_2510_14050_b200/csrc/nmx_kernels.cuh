@@ -769,4 +769,136 @@ __global__ void reduce_i64_kernel(const int64_t* __restrict__ x, uint64_t n, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// owner partitions for the multi-GPU exchange:
+// owner(x) = (fmix32(x) * G) >> 32 (murmur3 finaliser; oracle: distributed.owner)
+// ---------------------------------------------------------------------------
+constexpr int kMaxParts = 64;
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+__host__ __device__ __forceinline__ int owner_of(uint32_t x, int parts) {
+  return (int)(((uint64_t)fmix32(x) * (uint64_t)parts) >> 32);
+}
+
+// packets routed by owner(src); invalid packets are dropped
+struct PacketPart {
+  const uint32_t* src;
+  const uint32_t* dst;
+  const uint8_t* valid;
+  uint32_t* out_src;
+  uint32_t* out_dst;
+  __device__ __forceinline__ bool key(uint64_t i, uint32_t& k) const {
+    if (valid && !valid[i]) return false;
+    k = src[i];
+    return true;
+  }
+  __device__ __forceinline__ void store(uint64_t i, uint64_t pos) const {
+    out_src[pos] = src[i];
+    out_dst[pos] = dst[i];
+  }
+};
+// column entries (dst, count) routed by owner(dst)
+struct ColPart {
+  const uint32_t* ck;
+  const uint32_t* cv;
+  uint32_t* out_ck;
+  uint32_t* out_cv;
+  __device__ __forceinline__ bool key(uint64_t i, uint32_t& k) const {
+    k = ck[i];
+    return true;
+  }
+  __device__ __forceinline__ void store(uint64_t i, uint64_t pos) const {
+    out_ck[pos] = ck[i];
+    out_cv[pos] = cv[i];
+  }
+};
+
+template <typename Item>
+__device__ __forceinline__ void part_count_range(const Item& it, uint64_t lo, uint64_t hi, uint64_t step, int parts,
+                                                 uint32_t* sc) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = lo; base < hi; base += step) {
+    const uint64_t i = base + threadIdx.x;
+    uint32_t k = 0;
+    const bool ok = i < hi && it.key(i, k);
+    const int o = ok ? owner_of(k, parts) : -1;
+    for (int p = 0; p < parts; ++p) {
+      const uint32_t mask = __ballot_sync(FULL, o == p);
+      if (lane == 0 && mask) atomicAdd(&sc[p], (uint32_t)__popc(mask));
+    }
+  }
+}
+
+template <typename Item>
+__global__ void __launch_bounds__(256) part_count_kernel(Item it, uint64_t n, int parts,
+                                                        unsigned long long* __restrict__ counts) {
+  __shared__ uint32_t sc[kMaxParts];
+  if (threadIdx.x < kMaxParts) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk, hi = umin64(n, lo + chunk);
+  part_count_range(it, lo, hi, 256, parts, sc);
+  __syncthreads();
+  if (threadIdx.x < parts && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
+}
+
+template <typename Item>
+__global__ void __launch_bounds__(256) part_scatter_kernel(Item it, uint64_t n, uint64_t chunk, int parts,
+                                                          unsigned long long* __restrict__ cursor) {
+  __shared__ uint32_t sc[kMaxParts];
+  __shared__ unsigned long long sbase[kMaxParts];
+  if (threadIdx.x < kMaxParts) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk, hi = umin64(n, lo + chunk);
+  part_count_range(it, lo, hi, 256, parts, sc);
+  __syncthreads();
+  if (threadIdx.x < parts) {
+    sbase[threadIdx.x] = sc[threadIdx.x] ? atomicAdd(cursor + threadIdx.x, (unsigned long long)sc[threadIdx.x]) : 0;
+    sc[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  for (uint64_t base = lo; base < hi; base += 256) {
+    const uint64_t i = base + threadIdx.x;
+    uint32_t k = 0;
+    const bool ok = i < hi && it.key(i, k);
+    const int o = ok ? owner_of(k, parts) : -1;
+    for (int p = 0; p < parts; ++p) {
+      const uint32_t mask = __ballot_sync(FULL, o == p);
+      if (!mask) continue;
+      const int leader = __ffs(mask) - 1;
+      uint32_t w = 0;
+      if (lane == leader) w = atomicAdd(&sc[p], (uint32_t)__popc(mask));
+      w = __shfl_sync(FULL, w, leader);
+      if (o == p) it.store(i, sbase[p] + w + __popc(mask & lt));
+    }
+  }
+}
+
+// digit histograms of received u32 column keys (multi-GPU column stage)
+template <int NPASS>
+__global__ void __launch_bounds__(256) hist_u32_kernel(const uint32_t* __restrict__ keys, uint64_t n,
+                                                      uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[NPASS][kRadix];
+  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (uint64_t)gridDim.x * 256) {
+    const uint32_t k = keys[i];
+#pragma unroll
+    for (int p = 0; p < NPASS; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFFu], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(ghist + i, v);
+  }
+}
+
 }  // namespace nmx

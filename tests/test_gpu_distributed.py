@@ -1,0 +1,99 @@
+"""Device stages of the multi-GPU path on one B200.
+
+G ranks are simulated in one process (each 'rank' runs nmx_partition_packets /
+nmx_shard_rows / nmx_shard_cols; the all-to-all is done by slicing), and the
+real NCCL orchestration runs as a world-size-1 process group."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import netmeter_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2510_14050_b200.distributed import CudaShardOps
+
+    return CudaShardOps(0)
+
+
+def _t(ops, a):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).to("cuda:0")
+
+
+def _simulate(ops, s, d, valid, space, G):
+    from paper_2510_14050_b200 import distributed as nd
+    from paper_2510_14050_b200.partitioning import partition_even
+
+    import torch
+
+    spans = partition_even(len(s), G).spans
+    # exchange 1
+    inbox = [[[], []] for _ in range(G)]
+    for off, ln in spans:
+        v = None if valid is None else torch.from_numpy(valid[off:off + ln].astype(np.uint8)).to("cuda:0")
+        ps, pd, c = ops.partition_packets(_t(ops, s[off:off + ln]), _t(ops, d[off:off + ln]), v, G)
+        at = 0
+        for o in range(G):
+            inbox[o][0].append(ps[at:at + c[o]])
+            inbox[o][1].append(pd[at:at + c[o]])
+            at += c[o]
+    # rows + exchange 2
+    rows, inbox2 = [], [[[], []] for _ in range(G)]
+    for o in range(G):
+        rs, rd = torch.cat(inbox[o][0]), torch.cat(inbox[o][1])
+        st, cd, cc, c = ops.rows(rs, rd, space, G)
+        rows.append(st)
+        at = 0
+        for q in range(G):
+            inbox2[q][0].append(cd[at:at + c[q]])
+            inbox2[q][1].append(cc[at:at + c[q]])
+            at += c[q]
+    cols = [ops.cols(torch.cat(inbox2[q][0]), torch.cat(inbox2[q][1]), space) for q in range(G)]
+    out = [0] * 9
+    for i in nd.SUM_FIELDS:
+        out[i] = int(sum((rows[r] if i < 6 else cols[r])[i] for r in range(G)))
+    for i in nd.MAX_FIELDS:
+        out[i] = int(max((rows[r] if i < 6 else cols[r])[i] for r in range(G)))
+    return tuple(out)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
+def test_simulated_ranks_match_oracle(ops, G, kind):
+    gen = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
+    for lg, space, frac in ((18, 1 << 32, 0.0), (16, 5000, 0.25)):
+        s, d = gen(21, 0, 1 << lg, space)
+        valid = None if not frac else np.random.default_rng(2).random(len(s)) >= frac
+        assert _simulate(ops, s, d, valid, space, G) == orc.stats9_packed(s, d, valid), (G, kind, lg)
+
+
+def test_nccl_world_of_one():
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_14050_b200 import _lib
+    from paper_2510_14050_b200 import distributed as nd
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n = 1 << 20
+        ds, dd = _lib.DeviceArray(n), _lib.DeviceArray(n)
+        _lib.generate(_lib.GEN_POWERLAW, 4, 0, n, 1 << 32, ds, dd)
+        got = nd.sharded_stats9_device(ds, dd, 1 << 32)
+        assert got == orc.stats9_packed(ds.download(), dd.download())
+        hs, hd = ds.download(), dd.download()
+        assert nd.sharded_stats9_host(hs, hd, 1 << 32) == got
+    finally:
+        dist.destroy_process_group()
