@@ -97,6 +97,28 @@ int nmx_window_stats9_host(nmx_ctx* ctx, const uint32_t* src, const uint32_t* ds
  * INT64_MIN for an empty view (the Python layer maps it to 0). */
 int nmx_reduce_i64(nmx_ctx* ctx, const int64_t* data, uint64_t n, int op, int64_t* out);
 
+/* Materialisation for the drop-in containers:
+ *  - nmx_coo_build: sorted unique links of host packets with counts, i.e.
+ *    np.unique(src*dim+dst, return_counts=True) (traffic.py:207), per window
+ *    when window_size > 0 (build_matrices, traffic.py:221-242). Keys are
+ *    packed as window<<2b | src<<b | dst with b = ceil(log2(address_space));
+ *    requires 2b + window bits <= 64. Kept in the context until the next call;
+ *  - nmx_coo_fetch: copy keys / counts of the last nmx_coo_build to the host;
+ *  - nmx_coo_rowptr: dense row_ptr[dim+1] of the COO slice [lo, hi) of one
+ *    window (traffic.py:210-211);
+ *  - nmx_flat_build / nmx_flat_fetch: to_flat (traffic.py:263-292) of a CSR
+ *    matrix: per-nonzero row ids (edges[:,0]), occupied rows with nnz (fan-out)
+ *    and value sums, occupied columns with nnz (fan-in) and value sums. Values
+ *    must lie in [1, 2^32) (packet counts); nnz, dim < 2^32. */
+int nmx_coo_build(nmx_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                  uint64_t address_space, uint64_t window_size, uint64_t* nnz);
+int nmx_coo_fetch(nmx_ctx* ctx, uint64_t* keys, int64_t* counts);
+int nmx_coo_rowptr(nmx_ctx* ctx, uint64_t lo, uint64_t hi, uint64_t window, uint64_t dim, int64_t* row_ptr);
+int nmx_flat_build(nmx_ctx* ctx, const int64_t* row_ptr, uint64_t dim, const int64_t* col_idx, const int64_t* values,
+                   uint64_t nnz, uint64_t* rows_out, uint64_t* cols_out);
+int nmx_flat_fetch(nmx_ctx* ctx, int64_t* edge_src, int64_t* row_ids, int64_t* row_nnz, int64_t* row_sum,
+                   int64_t* col_ids, int64_t* col_nnz, int64_t* col_sum);
+
 /* Multi-GPU building blocks (one process per GPU; the exchange itself is NCCL
  * all-to-all driven by paper_2510_14050_b200/distributed.py). owner(x) =
  * (fmix32(x) * nparts) >> 32, nparts <= 64. Counts are written to host arrays.

@@ -50,6 +50,11 @@ SIGNATURES = {
     "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_window_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_reduce_i64": (C.c_int, [_VP, _VP, _U64, C.c_int, _VP]),
+    "nmx_coo_build": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, C.POINTER(_U64)]),
+    "nmx_coo_fetch": (C.c_int, [_VP, _VP, _VP]),
+    "nmx_coo_rowptr": (C.c_int, [_VP, _U64, _U64, _U64, _U64, _VP]),
+    "nmx_flat_build": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _U64, C.POINTER(_U64), C.POINTER(_U64)]),
+    "nmx_flat_fetch": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "nmx_partition_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.c_int, _VP, _VP, _VP]),
     "nmx_shard_rows": (C.c_int, [_VP, _VP, _VP, _U64, _U64, C.c_int, _VP, _VP, _VP, _VP]),
     "nmx_shard_cols": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),

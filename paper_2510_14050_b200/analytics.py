@@ -1,0 +1,195 @@
+"""Aggregate traffic measures on the B200 (mirrors netmeter.analytics, analytics.py:1-157).
+
+Reference-compatible entry points (same names, argument meaning and errors):
+``sum_reduce``, ``max_scan``, ``analyze_matrix``, ``analyze_dataset``,
+``oracle_analyze``, ``AggregateReport``. Their reductions run in libnmx.so
+(``nmx_reduce_i64``); the scheduler argument only contributes its
+``resource_count`` / ``batch_count`` validation because a device reduction has
+no per-resource partial slots to fill.
+
+The hot path (BASELINE.json north star) is ``stats9`` / ``analyze_summed``:
+packets -> summed traffic matrix -> the nine Graph Challenge statistics, with
+no host-side containers at all (``nmx_stats9_*``), and ``analyze_windows`` for
+the per-window (analyze_dataset) semantics (``nmx_window_stats9_*``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import asdict, dataclass
+
+import numpy as np
+
+from . import _lib
+from .traffic import FlatContainers, PacketStream, TrafficMatrix, to_flat
+
+_INT64_MIN = np.iinfo(np.int64).min
+
+
+@dataclass(frozen=True)
+class AggregateReport:
+    """The six aggregate measures (analytics.py:31-51); key order pinned by the reference tests."""
+
+    valid_packets: int
+    unique_links: int
+    unique_sources: int
+    max_fanout: int
+    unique_destinations: int
+    max_fanin: int
+
+    def to_dict(self) -> dict[str, int]:
+        return asdict(self)
+
+    @classmethod
+    def from_dict(cls, data: dict[str, int]) -> "AggregateReport":
+        return cls(**{f: int(data[f]) for f in cls.__dataclass_fields__})
+
+    @classmethod
+    def zero(cls) -> "AggregateReport":
+        return cls(0, 0, 0, 0, 0, 0)
+
+
+@dataclass(frozen=True)
+class Stats9:
+    """The nine Graph Challenge statistics of one traffic matrix."""
+
+    valid_packets: int
+    unique_links: int
+    max_link_packets: int
+    unique_sources: int
+    max_source_packets: int
+    max_fanout: int
+    unique_destinations: int
+    max_destination_packets: int
+    max_fanin: int
+
+    def to_dict(self) -> dict[str, int]:
+        return asdict(self)
+
+    def astuple(self) -> tuple:
+        return tuple(getattr(self, f) for f in self.__dataclass_fields__)
+
+    def report(self) -> AggregateReport:
+        return AggregateReport(self.valid_packets, self.unique_links, self.unique_sources, self.max_fanout,
+                               self.unique_destinations, self.max_fanin)
+
+    @classmethod
+    def zero(cls) -> "Stats9":
+        return cls(0, 0, 0, 0, 0, 0, 0, 0, 0)
+
+
+def _check_view(data, batch_count: int) -> np.ndarray:
+    """analytics.py:68-75 argument rules."""
+    if batch_count < 1:
+        raise ValueError("batch_count must be >= 1")
+    data = np.asarray(data)
+    if data.size and data.dtype.kind not in "iub":
+        raise TypeError(f"expected an integer view, got dtype {data.dtype}")
+    return np.ascontiguousarray(data, dtype=np.int64).reshape(-1)
+
+
+def _device_of(scheduler) -> int:
+    return int(getattr(scheduler, "device", 0) or 0)
+
+
+def sum_reduce(data, scheduler, batch_count: int = 1) -> int:
+    """Sum of an integer view (int64 wrap-around, analytics.py:84-86); empty -> 0."""
+    a = _check_view(data, batch_count)
+    return _lib.reduce_i64(a, _lib.REDUCE_SUM, device=_device_of(scheduler))
+
+
+def max_scan(data, scheduler, batch_count: int = 1) -> int:
+    """Maximum of an integer view; empty view (and INT64_MIN) -> 0 (analytics.py:89-92)."""
+    a = _check_view(data, batch_count)
+    peak = _lib.reduce_i64(a, _lib.REDUCE_MAX, device=_device_of(scheduler))
+    return 0 if peak == _INT64_MIN else peak
+
+
+def analyze_matrix(flat: FlatContainers, scheduler, batch_count: int = 1) -> AggregateReport:
+    """The six measures of one matrix from its flat containers (analytics.py:95-106)."""
+    return AggregateReport(
+        valid_packets=sum_reduce(flat.weights, scheduler, batch_count),
+        unique_links=len(flat.edges),
+        unique_sources=len(flat.row_sums),
+        max_fanout=max_scan(flat.out_degrees, scheduler, batch_count),
+        unique_destinations=len(flat.col_sums),
+        max_fanin=max_scan(flat.in_degrees, scheduler, batch_count),
+    )
+
+
+def _totals6(reports) -> AggregateReport:
+    return AggregateReport(
+        valid_packets=sum(r.valid_packets for r in reports),
+        unique_links=sum(r.unique_links for r in reports),
+        unique_sources=sum(r.unique_sources for r in reports),
+        max_fanout=max((r.max_fanout for r in reports), default=0),
+        unique_destinations=sum(r.unique_destinations for r in reports),
+        max_fanin=max((r.max_fanin for r in reports), default=0),
+    )
+
+
+def analyze_dataset(matrices, scheduler, batch_count: int = 1) -> tuple[list[AggregateReport], AggregateReport]:
+    """Per-matrix reports plus dataset totals (analytics.py:109-130)."""
+    reports = []
+    for item in matrices:
+        flat = to_flat(item, device=_device_of(scheduler)) if isinstance(item, TrafficMatrix) else item
+        reports.append(analyze_matrix(flat, scheduler, batch_count))
+    return reports, _totals6(reports)
+
+
+def _pairs_of(window):
+    if isinstance(window, PacketStream):
+        return window.src[window.valid], window.dst[window.valid], None
+    arr = np.asarray([(int(s), int(d)) for s, d in window], dtype=np.int64).reshape(-1, 2)
+    return arr[:, 0], arr[:, 1], None
+
+
+def oracle_analyze(window) -> AggregateReport:
+    """Measures straight from raw pairs, no matrix (analytics.py:133-157), computed by the
+    device hot path (use oracle/ for an independent CPU cross-check)."""
+    s, d, _ = _pairs_of(window)
+    if len(s) == 0:
+        return AggregateReport.zero()
+    space = int(max(s.max(), d.max())) + 1
+    if min(s.min(), d.min()) < 0 or space > 1 << 32:
+        raise ValueError("addresses must lie in [0, 2^32)")
+    return Stats9(*_lib.stats9(s, d, None, space)).report()
+
+
+# ---------------------------------------------------------------------------
+# the north-star hot path
+# ---------------------------------------------------------------------------
+def stats9(stream: PacketStream, device: int = 0) -> Stats9:
+    """Nine statistics of the matrix summed over all valid packets of ``stream``
+    (= build_matrices(stream, len(stream)) -> to_flat -> analyze_matrix + 3 max_scan)."""
+    if len(stream) == 0:
+        return Stats9.zero()
+    s, d, v = stream.wire()
+    return Stats9(*_lib.stats9(s, d, None if stream.valid.all() else v, stream.address_space, device=device))
+
+
+def analyze_summed(streams, device: int = 0) -> Stats9:
+    """Statistics of sum_t A_t over several streams (windows) of one address space:
+    the element-wise sum of count matrices is the count matrix of the concatenated
+    packets, so one device pass over all of them is exact."""
+    streams = [streams] if isinstance(streams, PacketStream) else list(streams)
+    if not streams:
+        return Stats9.zero()
+    space = max(s.address_space for s in streams)
+    cat = PacketStream(np.concatenate([s.src for s in streams]), np.concatenate([s.dst for s in streams]),
+                       np.concatenate([s.valid for s in streams]), space)
+    return stats9(cat, device=device)
+
+
+def analyze_windows(stream: PacketStream, window_size: int, device: int = 0) -> tuple[list[Stats9], Stats9]:
+    """Per-window nine statistics with analyze_dataset totals (sums of the counting
+    measures, maxima of the max measures; analytics.py:122-129)."""
+    if window_size < 1:
+        raise ValueError("window_size must be >= 1")
+    if len(stream) == 0:
+        return [], Stats9.zero()
+    s, d, v = stream.wire()
+    rows = _lib.window_stats9(s, d, v, stream.address_space, window_size, device=device)
+    per = [Stats9(*map(int, r)) for r in rows]
+    sums = {0, 1, 3, 6}
+    tot = [sum(r.astuple()[k] for r in per) if k in sums else max(r.astuple()[k] for r in per) for k in range(9)]
+    return per, Stats9(*tot)

@@ -105,7 +105,8 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf keysA, keysB, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, stats, in_src, in_dst, in_valid,
+  DevBuf keysA, keysB, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
+      ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
@@ -118,7 +119,9 @@ struct nmx_ctx {
   int last_nstage = 0;
   int last_sort_launches = 0, last_launches = 0;
   int launches = 0;
-  uint64_t* sorted_keys = nullptr;  // last row sort output (materialisation)
+  // materialised outputs (drop-in TrafficMatrix / FlatContainers)
+  uint64_t coo_nnz = 0, flat_nnz = 0, flat_r = 0, flat_c = 0;
+  int coo_b = 0;
 
   uint32_t next_epoch() {
     if (++epoch >= (1u << 22)) {
@@ -194,18 +197,20 @@ void launch_pass(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32_t
 constexpr int kSegIPT = 8;  // link_row / col kernels: 2048 items per tile
 constexpr int kSegTile = 256 * kSegIPT;
 
+// LSD onesweep sort of u entries (ColKeyT keys in ckA, u32 values in cvA; their
+// digit histograms already in small[kCHist]) -> sorted pointers.
 template <typename ColKeyT>
-void column_phase(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small) {
-  const int ncolpass = (b + wb + 7) / 8;
+std::pair<ColKeyT*, uint32_t*> sort_col_entries(nmx_ctx* c, uint32_t u, int nbits, uint32_t* d_small) {
+  const int ncolpass = (nbits + 7) / 8;
   ColKeyT* ck = c->ckA.as<ColKeyT>();
   uint32_t* cv = c->cvA.as<uint32_t>();
-  // column digit histograms were accumulated by link_row_kernel
   bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kCHist, ncolpass, d_small + kCBase);
   CK_LAUNCH();
   ++c->launches;
   CK(cudaMemcpyAsync(c->h_small + kCHist, d_small + kCHist, sizeof(uint32_t) * ncolpass * kRadix,
                      cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  c->grow_status(tiles_of(u, kMinPassTile) * kRadix);
   int idx = 0;
   for (int p = 0; p < ncolpass; ++p) {
     const uint32_t* hp = c->h_small + kCHist + p * kRadix;
@@ -222,9 +227,15 @@ void column_phase(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small) {
     cv = ov;
     ++idx;
   }
+  return {ck, cv};
+}
+
+template <typename ColKeyT>
+void column_phase(nmx_ctx* c, uint32_t u, int b, int wb, uint32_t* d_small) {
+  auto sorted = sort_col_entries<ColKeyT>(c, u, b + wb, d_small);
   c->mark();  // column sort end
   col_kernel<ColKeyT, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
-      ck, cv, u, b, wb, c->csstatus.as<CSStatus>(), c->next_epoch(), d_small + kCounters + 26,
+      sorted.first, sorted.second, u, b, wb, c->csstatus.as<CSStatus>(), c->next_epoch(), d_small + kCounters + 26,
       c->stats.as<unsigned long long>());
   CK_LAUNCH();
   ++c->launches;
@@ -292,7 +303,8 @@ struct RowsOut {
 
 // hist -> onesweep row sort -> fused link/row kernel. Link + row statistics
 // accumulate into c->stats; the column entries are left in c->ckA / c->cvA.
-RowsOut stage_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb) {
+// hist -> onesweep LSD sort of the packed keys; returns the sorted keys (m valid)
+uint64_t* sort_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb, uint64_t* m_out) {
   const uint64_t n = ps.n;
   const int kb = 2 * b + wb;
   const int npass = (kb + 7) / 8;
@@ -304,8 +316,8 @@ RowsOut stage_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb) {
   CK(cudaMemcpyAsync(c->h_small, d_small, kSmallWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   const uint64_t m = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
-  const bool wide = b + wb > 32;
-  if (m == 0) return RowsOut{0, 0, wide};
+  *m_out = m;
+  if (m == 0) return nullptr;
   if (m >= (1ull << 32)) throw std::runtime_error("more than 2^32-1 valid packets in one call");
 
   std::vector<int> active;
@@ -337,8 +349,15 @@ RowsOut stage_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb) {
   }
   c->last_sort_launches = (int)active.size();
   c->mark();  // 2: sort end
-  c->sorted_keys = keys;
+  return keys;
+}
 
+RowsOut stage_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb) {
+  uint64_t m = 0;
+  uint64_t* keys = sort_rows(c, ps, b, wb, &m);
+  const bool wide = b + wb > 32;
+  if (m == 0) return RowsOut{0, 0, wide};
+  uint32_t* d_small = c->small.as<uint32_t>();
   c->ckA.grow(m * (wide ? 8 : 4));
   c->ckB.grow(m * (wide ? 8 : 4));
   c->cvA.grow(m * 4);
@@ -367,6 +386,25 @@ void stage_cols(nmx_ctx* c, uint32_t u, int b, int wb, bool wide) {
     column_phase<uint64_t>(c, u, b, wb, d_small);
   else
     column_phase<uint32_t>(c, u, b, wb, d_small);
+}
+
+// reduce-by-key launch; returns the number of segments (host sync)
+template <typename KeyT>
+uint32_t run_rbk(nmx_ctx* c, const KeyT* keys, const uint32_t* w, uint32_t n, int shift, unsigned long long* okeys,
+                 uint32_t* olen, unsigned long long* osum, int counter) {
+  if (!n) return 0;
+  uint32_t* d_small = c->small.as<uint32_t>();
+  if (c->rbstatus.grow(tiles_of(n, kSegTile) * sizeof(RBStatus)))
+    CK(cudaMemsetAsync(c->rbstatus.p, 0, c->rbstatus.cap, c->st));
+  rbk_kernel<KeyT, kSegIPT><<<(unsigned)tiles_of(n, kSegTile), 256, 0, c->st>>>(
+      keys, w, n, shift, okeys, olen, osum, c->rbstatus.as<RBStatus>(), c->next_epoch(), d_small + kCounters + counter,
+      d_small + kU);
+  CK_LAUNCH();
+  ++c->launches;
+  uint32_t r = 0;
+  CK(cudaMemcpyAsync(&r, d_small + kU, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return r;
 }
 
 // The whole pipeline over packet columns already on the device. Writes W*9
@@ -545,7 +583,8 @@ void nmx_destroy(nmx_ctx* c) {
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   for (DevBuf* b : {&c->keysA, &c->keysB, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
-                    &c->csstatus, &c->part, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
+                    &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
+                    &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
     b->release();
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_stats) cudaFreeHost(c->h_stats);
@@ -754,6 +793,174 @@ int nmx_shard_cols(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, u
     stage_cols(c, (uint32_t)u, b, 0, false);
     stage_finish(c, 1);
     copy_out9(c->h_stats, out, 1);
+    return NMX_OK;
+  });
+}
+
+int nmx_coo_build(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                  uint64_t address_space, uint64_t window_size, uint64_t* nnz) {
+  if (!nnz) return fail(NMX_EINVAL, "null output");
+  int b;
+  if (int r = check_space(address_space, b)) return r;
+  if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call");
+  return guarded(c, [&] {
+    *nnz = 0;
+    c->coo_nnz = 0;
+    c->coo_b = b;
+    if (!n) return NMX_OK;
+    const uint64_t W = (window_size && window_size < n) ? (n + window_size - 1) / window_size : 1;
+    const int wb = W > 1 ? (int)ceil_log2(W) : 0;
+    if (2 * b + wb > 64) return fail(NMX_EINVAL, "2*bits + window bits exceed 64; build windows separately");
+    c->in_src.grow(n * 4);
+    c->in_dst.grow(n * 4);
+    CK(cudaMemcpyAsync(c->in_src.p, src, n * 4, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->in_dst.p, dst, n * 4, cudaMemcpyHostToDevice, c->st));
+    if (valid) {
+      c->in_valid.grow(n);
+      CK(cudaMemcpyAsync(c->in_valid.p, valid, n, cudaMemcpyHostToDevice, c->st));
+    }
+    stage_begin(c, 1);
+    PacketSrc ps{c->in_src.as<uint32_t>(), c->in_dst.as<uint32_t>(), valid ? c->in_valid.as<uint8_t>() : nullptr, n,
+                 W > 1 ? window_size : 0, b};
+    uint64_t m = 0;
+    uint64_t* keys = sort_rows(c, ps, b, wb, &m);
+    if (m) {
+      c->mkeys.grow(m * 8);
+      c->mlen.grow(m * 4);
+      c->coo_nnz = run_rbk<uint64_t>(c, keys, nullptr, (uint32_t)m, 0, c->mkeys.as<unsigned long long>(),
+                                     c->mlen.as<uint32_t>(), nullptr, 27);
+    }
+    stage_finish(c, 1);
+    *nnz = c->coo_nnz;
+    return NMX_OK;
+  });
+}
+
+int nmx_coo_fetch(nmx_ctx* c, uint64_t* keys, int64_t* counts) {
+  return guarded(c, [&] {
+    const uint64_t u = c->coo_nnz;
+    if (!u) return NMX_OK;
+    if (keys) CK(cudaMemcpyAsync(keys, c->mkeys.p, u * 8, cudaMemcpyDeviceToHost, c->st));
+    std::vector<uint32_t> tmp(counts ? u : 0);
+    if (counts) CK(cudaMemcpyAsync(tmp.data(), c->mlen.p, u * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (uint64_t i = 0; counts && i < u; ++i) counts[i] = tmp[i];
+    return NMX_OK;
+  });
+}
+
+int nmx_coo_rowptr(nmx_ctx* c, uint64_t lo, uint64_t hi, uint64_t window, uint64_t dim, int64_t* row_ptr) {
+  if (!row_ptr) return fail(NMX_EINVAL, "null output");
+  return guarded(c, [&] {
+    if (hi < lo || hi > c->coo_nnz) return fail(NMX_EINVAL, "slice [%llu,%llu) outside the COO", (unsigned long long)lo,
+                                                 (unsigned long long)hi);
+    const int b = c->coo_b;
+    if (dim > (1ull << b)) return fail(NMX_EINVAL, "dim exceeds the address space of the COO");
+    DevBuf& out = c->frows;
+    out.grow((dim + 1) * 8);
+    const uint64_t wbase = 2 * b < 64 ? (window << (2 * b)) : 0;
+    const unsigned grid = (unsigned)std::min<uint64_t>((dim + 256) / 256, (uint64_t)c->sms * 16);
+    coo_rowptr_kernel<<<grid, 256, 0, c->st>>>(c->mkeys.as<uint64_t>(), lo, hi, wbase, b, dim,
+                                               out.as<long long>());
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(row_ptr, out.p, (dim + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return NMX_OK;
+  });
+}
+
+int nmx_flat_build(nmx_ctx* c, const int64_t* row_ptr, uint64_t dim, const int64_t* col_idx, const int64_t* values,
+                   uint64_t nnz, uint64_t* r_out, uint64_t* c_out) {
+  if (!r_out || !c_out) return fail(NMX_EINVAL, "null output");
+  if (nnz >= (1ull << 32) || dim >= (1ull << 32)) return fail(NMX_EINVAL, "nnz and dim must be < 2^32");
+  for (uint64_t k = 0; k < nnz; ++k)
+    if (values[k] < 1 || values[k] > 0xFFFFFFFFll) return fail(NMX_EINVAL, "values must lie in [1, 2^32)");
+  return guarded(c, [&] {
+    *r_out = *c_out = 0;
+    c->flat_nnz = nnz;
+    c->flat_r = c->flat_c = 0;
+    if (!nnz) return NMX_OK;
+    stage_begin(c, 1);
+    uint32_t* d_small = c->small.as<uint32_t>();
+    // upload CSR
+    c->in_src.grow((dim + 1) * 8);
+    c->in_dst.grow(nnz * 16);
+    long long* d_rp = c->in_src.as<long long>();
+    long long* d_col = c->in_dst.as<long long>();
+    long long* d_val = d_col + nnz;
+    CK(cudaMemcpyAsync(d_rp, row_ptr, (dim + 1) * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(d_col, col_idx, nnz * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(d_val, values, nnz * 8, cudaMemcpyHostToDevice, c->st));
+    c->frows.grow(nnz * 4);
+    c->ckA.grow(nnz * 4);
+    c->ckB.grow(nnz * 4);
+    c->cvA.grow(nnz * 4);
+    c->cvB.grow(nnz * 4);
+    const unsigned grid = (unsigned)std::min<uint64_t>((nnz + 255) / 256, (uint64_t)c->sms * 16);
+    csr_expand_kernel<<<grid, 256, 0, c->st>>>(d_rp, dim, d_col, d_val, nnz, c->frows.as<uint32_t>(),
+                                                c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>());
+    CK_LAUNCH();
+    // rows: CSR order is row-sorted -> reduce by row (np.add.reduceat, traffic.py:271-277)
+    c->mkeys.grow(nnz * 8);
+    c->mlen.grow(nnz * 4);
+    c->msum.grow(nnz * 8);
+    c->flat_r = run_rbk<uint32_t>(c, c->frows.as<uint32_t>(), c->cvA.as<uint32_t>(), (uint32_t)nnz, 0,
+                                  c->mkeys.as<unsigned long long>(), c->mlen.as<uint32_t>(),
+                                  c->msum.as<unsigned long long>(), 28);
+    // columns: sort (col, value) then reduce by column (bincount / np.add.at, traffic.py:279-283)
+    const int cb = std::max<int>(1, (int)ceil_log2(std::max<uint64_t>(dim, 2)));
+    const int ncolpass = (cb + 7) / 8;
+    const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nnz + 1023) / 1024, (uint64_t)c->sms * 8));
+    switch (ncolpass) {
+      case 1: hist_u32_kernel<1><<<hgrid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), nnz, d_small + kCHist); break;
+      case 2: hist_u32_kernel<2><<<hgrid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), nnz, d_small + kCHist); break;
+      case 3: hist_u32_kernel<3><<<hgrid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), nnz, d_small + kCHist); break;
+      default: hist_u32_kernel<4><<<hgrid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), nnz, d_small + kCHist); break;
+    }
+    CK_LAUNCH();
+    auto sorted = sort_col_entries<uint32_t>(c, (uint32_t)nnz, cb, d_small);
+    c->ckeys2.grow(nnz * 8);
+    c->clen2.grow(nnz * 4);
+    c->csum2.grow(nnz * 8);
+    c->flat_c = run_rbk<uint32_t>(c, sorted.first, sorted.second, (uint32_t)nnz, 0,
+                                  c->ckeys2.as<unsigned long long>(), c->clen2.as<uint32_t>(),
+                                  c->csum2.as<unsigned long long>(), 29);
+    stage_finish(c, 1);
+    *r_out = c->flat_r;
+    *c_out = c->flat_c;
+    return NMX_OK;
+  });
+}
+
+int nmx_flat_fetch(nmx_ctx* c, int64_t* edge_src, int64_t* row_ids, int64_t* row_nnz, int64_t* row_sum,
+                   int64_t* col_ids, int64_t* col_nnz, int64_t* col_sum) {
+  return guarded(c, [&] {
+    const uint64_t nnz = c->flat_nnz, r = c->flat_r, cc = c->flat_c;
+    std::vector<uint32_t> rows(nnz), rl(r), cl(cc);
+    std::vector<unsigned long long> rk(r), rs(r), ck(cc), cs(cc);
+    if (nnz) CK(cudaMemcpyAsync(rows.data(), c->frows.p, nnz * 4, cudaMemcpyDeviceToHost, c->st));
+    if (r) {
+      CK(cudaMemcpyAsync(rk.data(), c->mkeys.p, r * 8, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(rl.data(), c->mlen.p, r * 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(rs.data(), c->msum.p, r * 8, cudaMemcpyDeviceToHost, c->st));
+    }
+    if (cc) {
+      CK(cudaMemcpyAsync(ck.data(), c->ckeys2.p, cc * 8, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(cl.data(), c->clen2.p, cc * 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(cs.data(), c->csum2.p, cc * 8, cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    for (uint64_t i = 0; edge_src && i < nnz; ++i) edge_src[i] = rows[i];
+    for (uint64_t i = 0; i < r; ++i) {
+      if (row_ids) row_ids[i] = (int64_t)rk[i];
+      if (row_nnz) row_nnz[i] = rl[i];
+      if (row_sum) row_sum[i] = (int64_t)rs[i];
+    }
+    for (uint64_t i = 0; i < cc; ++i) {
+      if (col_ids) col_ids[i] = (int64_t)ck[i];
+      if (col_nnz) col_nnz[i] = cl[i];
+      if (col_sum) col_sum[i] = (int64_t)cs[i];
+    }
     return NMX_OK;
   });
 }

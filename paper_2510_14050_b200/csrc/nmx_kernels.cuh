@@ -901,4 +901,144 @@ __global__ void __launch_bounds__(256) hist_u32_kernel(const uint32_t* __restric
   }
 }
 
+// ---------------------------------------------------------------------------
+// Materialisation (drop-in TrafficMatrix / FlatContainers)
+// ---------------------------------------------------------------------------
+// reduce-by-key with compacted outputs: for every run of equal (key >> shift)
+// in a sorted array emit (segment key, length, sum of weights). This is
+// np.unique(return_counts) (traffic.py:207), np.add.reduceat over rows
+// (traffic.py:271-277) and bincount / np.add.at over columns (traffic.py:279-283).
+struct RB {
+  uint32_t nh, f, len, pad;
+  unsigned long long sum;
+  __device__ __forceinline__ static RB identity() { return RB{0, 0, 0, 0, 0ull}; }
+};
+__device__ __forceinline__ RB rb_combine(const RB& a, const RB& b) {
+  return RB{a.nh + b.nh, a.f | b.f, b.f ? b.len : a.len + b.len, 0u, b.f ? b.sum : a.sum + b.sum};
+}
+__device__ __forceinline__ RB rb_shfl_up(const RB& x, int o) {
+  return RB{__shfl_up_sync(FULL, x.nh, o), __shfl_up_sync(FULL, x.f, o), __shfl_up_sync(FULL, x.len, o), 0u,
+            __shfl_up_sync(FULL, x.sum, o)};
+}
+using RBStatus = TileStatus<6>;
+
+template <typename KeyT, int IPT>
+__global__ void __launch_bounds__(256) rbk_kernel(const KeyT* __restrict__ keys, const uint32_t* __restrict__ w,
+                                                 uint32_t n, int shift, unsigned long long* __restrict__ okeys,
+                                                 uint32_t* __restrict__ olen, unsigned long long* __restrict__ osum,
+                                                 RBStatus* status, uint32_t epoch, uint32_t* __restrict__ tile_counter,
+                                                 uint32_t* __restrict__ d_count) {
+  constexpr int TILE = 256 * IPT;
+  __shared__ __align__(16) uint64_t sk[TILE + TILE / 16];
+  __shared__ RB sm[kWarps + 1];
+  __shared__ RB s_excl;
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_prev, s_next;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t t0 = (uint64_t)tile * TILE;
+  const uint32_t cnt = (uint32_t)umin64(TILE, (uint64_t)n - t0);
+  const bool last_tile = t0 + cnt == n;
+  for (int j = 0; j < IPT; ++j) {
+    const uint32_t i = j * 256 + tid;
+    if (i < cnt) sk[pad16(i)] = (uint64_t)keys[t0 + i] >> shift;
+  }
+  if (tid == 0) {
+    const uint64_t k0 = (uint64_t)keys[t0] >> shift;
+    s_prev = t0 ? ((uint64_t)keys[t0 - 1] >> shift) : ~k0;
+    s_next = last_tile ? 0 : ((uint64_t)keys[t0 + cnt] >> shift);
+  }
+  __syncthreads();
+  const uint32_t i0 = tid * IPT;
+  uint64_t prev = i0 == 0 ? s_prev : (i0 < cnt ? sk[pad16(i0 - 1)] : 0);
+  const uint64_t prev0 = prev;
+  RB agg = RB::identity();
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const uint32_t i = i0 + q;
+    if (i < cnt) {
+      const uint64_t k = sk[pad16(i)];
+      const uint32_t h = k != prev;
+      agg = rb_combine(agg, RB{h, h, 1u, 0u, w ? (unsigned long long)w[t0 + i] : 1ull});
+      prev = k;
+    }
+  }
+  RB total;
+  const RB pre = block_excl_scan_op<RB, rb_combine, rb_shfl_up>(agg, sm, &total);
+  if (tid == 0) {
+    RBStatus* my = status + tile;
+    RB ex = RB::identity();
+    if (tile == 0) {
+      publish<RB, 6>(my, total, epoch, true);
+    } else {
+      publish<RB, 6>(my, total, epoch, false);
+      ex = lookback_op<RB, 6, rb_combine>(status, tile, epoch);
+      publish<RB, 6>(my, rb_combine(ex, total), epoch, true);
+    }
+    s_excl = ex;
+    if (last_tile) *d_count = ex.nh + total.nh;
+  }
+  __syncthreads();
+  RB run = rb_combine(s_excl, pre);
+  const uint64_t snext = s_next;
+  prev = prev0;
+  auto emit = [&](uint64_t key, const RB& r) {
+    const uint32_t j = r.nh - 1;
+    okeys[j] = key;
+    if (olen) olen[j] = r.len;
+    if (osum) osum[j] = r.sum;
+  };
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    const uint32_t i = i0 + q;
+    if (i < cnt) {
+      const uint64_t k = sk[pad16(i)];
+      const uint32_t h = k != prev;
+      if (h && i != 0) emit(prev, run);
+      run = rb_combine(run, RB{h, h, 1u, 0u, w ? (unsigned long long)w[t0 + i] : 1ull});
+      if (i == cnt - 1 && (last_tile || snext != k)) emit(k, run);
+      prev = k;
+    }
+  }
+}
+
+// CSR -> per-nonzero row ids (np.repeat(arange(dim), diff(row_ptr)), traffic.py:268)
+// plus u32 column/value columns for the column grouping
+__global__ void csr_expand_kernel(const long long* __restrict__ row_ptr, uint64_t dim, const long long* __restrict__ col,
+                                  const long long* __restrict__ val, uint64_t nnz, uint32_t* __restrict__ rows,
+                                  uint32_t* __restrict__ ck, uint32_t* __restrict__ cv) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = dim;  // last r with row_ptr[r] <= k
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if ((uint64_t)row_ptr[mid] <= k)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    rows[k] = (uint32_t)lo;
+    ck[k] = (uint32_t)col[k];
+    cv[k] = (uint32_t)val[k];
+  }
+}
+
+// dense row_ptr of one window's slice of the packed COO (traffic.py:210-211)
+__global__ void coo_rowptr_kernel(const uint64_t* __restrict__ keys, uint64_t lo, uint64_t hi, uint64_t wbase,
+                                  int b, uint64_t dim, long long* __restrict__ row_ptr) {
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= dim; r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t target = wbase | (r << b);
+    uint64_t a = lo, z = hi;  // first index with key >= target
+    while (a < z) {
+      const uint64_t mid = (a + z) >> 1;
+      if (keys[mid] < target)
+        a = mid + 1;
+      else
+        z = mid;
+    }
+    row_ptr[r] = (long long)(a - lo);
+  }
+}
+
 }  // namespace nmx

@@ -1,0 +1,290 @@
+"""Packet streams and traffic matrices -- the reference's data layer on the B200.
+
+Mirrors ``netmeter.traffic`` (/root/reference/pkg/src/netmeter/traffic.py)
+name for name; every aggregation runs in libnmx.so:
+
+* ``matrix_from_pairs`` / ``build_matrices`` (traffic.py:197-242): packed-key
+  onesweep sort + reduce-by-key on the GPU (``nmx_coo_build``), dense CSR
+  ``row_ptr`` per window by a GPU binary-search kernel (``nmx_coo_rowptr``);
+* ``to_flat`` (traffic.py:263-292): row and column grouping on the GPU
+  (``nmx_flat_build``).
+
+The containers keep the reference layout (int64 CSR, dense in ``dim``) so the
+reference's own tests and callers work unchanged. The hot path itself
+(``analytics.stats9`` / ``analyze_summed``) never materialises them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterator
+
+import numpy as np
+
+from . import _lib
+
+_PACKET_DTYPE = np.dtype([("src", "<u4"), ("dst", "<u4"), ("valid", "u1")])
+
+
+class MatrixFormatError(ValueError):
+    """A matrix violates the CSR invariants (traffic.py:28-29)."""
+
+
+class MatrixFileError(ValueError):
+    """A matrix file cannot be parsed; the message carries path and line (traffic.py:32-33)."""
+
+
+@dataclass(frozen=True)
+class PacketRecord:
+    src: int
+    dst: int
+    valid: bool = True
+
+
+@dataclass
+class PacketStream:
+    """Columnar packets (traffic.py:43-71): int64 src/dst, bool valid, address_space."""
+
+    src: np.ndarray
+    dst: np.ndarray
+    valid: np.ndarray
+    address_space: int
+
+    def __post_init__(self):
+        self.src = np.ascontiguousarray(self.src, dtype=np.int64)
+        self.dst = np.ascontiguousarray(self.dst, dtype=np.int64)
+        self.valid = np.ascontiguousarray(self.valid, dtype=bool)
+        if not (len(self.src) == len(self.dst) == len(self.valid)):
+            raise ValueError("src, dst and valid must have equal lengths")
+        if self.address_space < 1:
+            raise ValueError("address_space must be >= 1")
+        if len(self.src):
+            lo = min(self.src.min(), self.dst.min())
+            hi = max(self.src.max(), self.dst.max())
+            if lo < 0 or hi >= self.address_space:
+                raise ValueError("addresses must lie in [0, address_space)")
+
+    def __len__(self) -> int:
+        return len(self.src)
+
+    def records(self) -> Iterator[PacketRecord]:
+        for s, d, v in zip(self.src.tolist(), self.dst.tolist(), self.valid.tolist()):
+            yield PacketRecord(s, d, v)
+
+    def wire(self):
+        """The device wire format: u32 src / dst columns + u8 valid (8-9 B/packet)."""
+        if self.address_space > 1 << 32:
+            raise ValueError("address_space above 2^32 does not fit the 32-bit packet format")
+        return (self.src.astype(np.uint32), self.dst.astype(np.uint32), self.valid.view(np.uint8))
+
+
+@dataclass(frozen=True)
+class AnonymizationMap:
+    key: int
+    mapping: dict = field(repr=False)
+
+
+def generate_packets(n: int, address_space: int, seed: int, invalid_fraction: float = 0.0) -> PacketStream:
+    """Uniform packets from PCG64, identical to traffic.py:82-104 for identical arguments
+    (host input preparation; bulk synthetic inputs come from nmx_generate instead)."""
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    if address_space < 1:
+        raise ValueError("address_space must be >= 1")
+    if not 0.0 <= invalid_fraction <= 1.0:
+        raise ValueError("invalid_fraction must be in [0, 1]")
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, address_space, size=n, dtype=np.int64)
+    dst = rng.integers(0, address_space, size=n, dtype=np.int64)
+    valid = rng.random(n) >= invalid_fraction if invalid_fraction > 0.0 else np.ones(n, dtype=bool)
+    return PacketStream(src=src, dst=dst, valid=valid, address_space=address_space)
+
+
+def anonymize(stream: PacketStream, key: int) -> tuple[PacketStream, AnonymizationMap]:
+    """Keyed first-seen dense relabel (traffic.py:107-137; host input preparation,
+    SURVEY.md 8(f) f3 lists the GPU version as a next step)."""
+    both = np.empty(2 * len(stream), dtype=np.int64)
+    both[0::2], both[1::2] = stream.src, stream.dst
+    distinct, first, inverse = np.unique(both, return_index=True, return_inverse=True)
+    rank = np.empty(len(distinct), dtype=np.int64)
+    rank[np.argsort(first, kind="stable")] = np.arange(len(distinct), dtype=np.int64)
+    code = np.random.default_rng(key).permutation(len(distinct)).astype(np.int64)[rank]
+    relabeled = code[inverse]
+    anon = PacketStream(src=relabeled[0::2].copy(), dst=relabeled[1::2].copy(), valid=stream.valid.copy(),
+                        address_space=max(1, len(distinct)))
+    return anon, AnonymizationMap(key=key, mapping=dict(zip(distinct.tolist(), code.tolist())))
+
+
+@dataclass(eq=False)
+class TrafficMatrix:
+    """One window's packet-count matrix in CSR form (traffic.py:140-194)."""
+
+    window_id: int
+    dim: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int64)
+        self.values = np.ascontiguousarray(self.values, dtype=np.int64)
+
+    @property
+    def nnz(self) -> int:
+        return len(self.col_idx)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, TrafficMatrix):
+            return NotImplemented
+        return (self.window_id == other.window_id and self.dim == other.dim
+                and np.array_equal(self.row_ptr, other.row_ptr) and np.array_equal(self.col_idx, other.col_idx)
+                and np.array_equal(self.values, other.values))
+
+    def validate(self) -> None:
+        """Raise MatrixFormatError unless the CSR invariants hold (traffic.py:170-188)."""
+        if self.dim < 1:
+            raise MatrixFormatError("dim must be >= 1")
+        rp = self.row_ptr
+        if len(rp) != self.dim + 1:
+            raise MatrixFormatError("row_ptr must have dim + 1 entries")
+        if rp[0] != 0 or np.any(rp[1:] < rp[:-1]):
+            raise MatrixFormatError("row_ptr must start at 0 and be nondecreasing")
+        if rp[-1] != len(self.col_idx) or len(self.col_idx) != len(self.values):
+            raise MatrixFormatError("row_ptr[-1], col_idx and values must agree on nnz")
+        if self.nnz:
+            c = self.col_idx
+            if c.min() < 0 or c.max() >= self.dim:
+                raise MatrixFormatError("column indices must lie in [0, dim)")
+            if self.values.min() < 1:
+                raise MatrixFormatError("values must be positive packet counts")
+            # strictly increasing within rows: a decrease is only legal at a row start
+            starts = np.zeros(self.nnz, dtype=bool)
+            starts[rp[:-1][rp[:-1] < rp[1:]]] = True
+            bad = (c[1:] <= c[:-1]) & ~starts[1:]
+            if np.any(bad):
+                raise MatrixFormatError("column indices must be strictly increasing within rows")
+
+    def to_dense(self) -> np.ndarray:
+        dense = np.zeros((self.dim, self.dim), dtype=np.int64)
+        rows = np.repeat(np.arange(self.dim, dtype=np.int64), np.diff(self.row_ptr))
+        dense[rows, self.col_idx] = self.values
+        return dense
+
+
+def _bits(space: int) -> int:
+    return max(1, (int(space) - 1).bit_length())
+
+
+def _coo(src, dst, valid, space: int, window_size: int, device: int = 0):
+    """Device build of the (windowed) unique-link COO; returns keys (u64) and counts."""
+    ctx = _lib.context(device)
+    s = np.ascontiguousarray(src, dtype=np.uint32)
+    d = np.ascontiguousarray(dst, dtype=np.uint32)
+    v = None if valid is None else np.ascontiguousarray(valid, dtype=bool).view(np.uint8)
+    nnz = C.c_uint64(0)
+    _lib.check(ctx._lib.nmx_coo_build(ctx.handle, s.ctypes.data, d.ctypes.data, v.ctypes.data if v is not None else None,
+                                      len(s), int(space), int(window_size), C.byref(nnz)))
+    keys = np.empty(nnz.value, dtype=np.uint64)
+    counts = np.empty(nnz.value, dtype=np.int64)
+    _lib.check(ctx._lib.nmx_coo_fetch(ctx.handle, keys.ctypes.data, counts.ctypes.data))
+    return ctx, keys, counts
+
+
+def _matrix_from_slice(ctx, keys, counts, lo, hi, window, b, dim, window_id) -> TrafficMatrix:
+    row_ptr = np.empty(dim + 1, dtype=np.int64)
+    _lib.check(ctx._lib.nmx_coo_rowptr(ctx.handle, int(lo), int(hi), int(window), int(dim), row_ptr.ctypes.data))
+    cols = (keys[lo:hi] & np.uint64((1 << b) - 1)).astype(np.int64)
+    return TrafficMatrix(window_id=window_id, dim=dim, row_ptr=row_ptr, col_idx=cols, values=counts[lo:hi])
+
+
+def matrix_from_pairs(src, dst, dim: int, window_id: int = 0) -> TrafficMatrix:
+    """Count-aggregate (src, dst) pairs into one CSR matrix (traffic.py:197-218)."""
+    if dim < 1:
+        raise ValueError("dim must be >= 1")
+    if dim > 2**31:
+        raise ValueError("dim too large for packed pair keys")
+    src = np.asarray(src, dtype=np.int64)
+    dst = np.asarray(dst, dtype=np.int64)
+    if len(src) != len(dst):
+        raise ValueError("src and dst must have equal lengths")
+    if len(src) and (min(src.min(), dst.min()) < 0 or max(src.max(), dst.max()) >= dim):
+        raise ValueError("pairs must lie in [0, dim)")
+    if len(src) == 0:
+        return TrafficMatrix(window_id, dim, np.zeros(dim + 1, np.int64), np.empty(0, np.int64),
+                             np.empty(0, np.int64))
+    ctx, keys, counts = _coo(src, dst, None, dim, 0)
+    return _matrix_from_slice(ctx, keys, counts, 0, len(keys), 0, _bits(dim), dim, window_id)
+
+
+def build_matrices(stream: PacketStream, window_size: int, dim: int | None = None) -> list[TrafficMatrix]:
+    """One matrix per window of ``window_size`` raw positions (traffic.py:221-242)."""
+    if window_size < 1:
+        raise ValueError("window_size must be >= 1")
+    if dim is None:
+        dim = stream.address_space
+    if dim < 1:
+        raise ValueError("dim must be >= 1")
+    if dim > 2**31:
+        raise ValueError("dim too large for packed pair keys")
+    n = len(stream)
+    nw = (n + window_size - 1) // window_size
+    if nw == 0:
+        return []
+    if len(stream.src) and max(stream.src.max(), stream.dst.max()) >= dim:
+        raise ValueError("addresses must lie in [0, dim)")
+    b = _bits(dim)
+    wb = max(0, (nw - 1).bit_length()) if nw > 1 else 0
+    out = []
+    if 2 * b + wb <= 64:
+        ctx, keys, counts = _coo(stream.src, stream.dst, stream.valid, dim, window_size if nw > 1 else 0)
+        win = keys >> np.uint64(2 * b) if 2 * b < 64 else np.zeros(len(keys), np.uint64)
+        bounds = np.searchsorted(win, np.arange(nw + 1, dtype=np.uint64))
+        for t in range(nw):
+            out.append(_matrix_from_slice(ctx, keys, counts, bounds[t], bounds[t + 1], t, b, dim, t))
+        return out
+    for t in range(nw):  # keys too wide for a window field: one device build per window
+        lo, hi = t * window_size, min((t + 1) * window_size, n)
+        ctx, keys, counts = _coo(stream.src[lo:hi], stream.dst[lo:hi], stream.valid[lo:hi], dim, 0)
+        out.append(_matrix_from_slice(ctx, keys, counts, 0, len(keys), 0, b, dim, t))
+    return out
+
+
+@dataclass
+class FlatContainers:
+    """Flat per-nonzero expansion of a CSR matrix (traffic.py:245-260)."""
+
+    edges: np.ndarray
+    weights: np.ndarray
+    out_degrees: np.ndarray
+    in_degrees: np.ndarray
+    row_sums: np.ndarray
+    col_sums: np.ndarray
+
+
+def to_flat(matrix: TrafficMatrix, device: int = 0) -> FlatContainers:
+    """Expand a valid CSR matrix into its flat containers (traffic.py:263-292), on the GPU."""
+    matrix.validate()
+    nnz = matrix.nnz
+    if nnz == 0:
+        e = np.empty(0, np.int64)
+        return FlatContainers(np.empty((0, 2), np.int64), e.copy(), e.copy(), e.copy(),
+                              np.empty((0, 2), np.int64), np.empty((0, 2), np.int64))
+    ctx = _lib.context(device)
+    r, c = C.c_uint64(0), C.c_uint64(0)
+    _lib.check(ctx._lib.nmx_flat_build(ctx.handle, matrix.row_ptr.ctypes.data, matrix.dim, matrix.col_idx.ctypes.data,
+                                       matrix.values.ctypes.data, nnz, C.byref(r), C.byref(c)))
+    edge_src = np.empty(nnz, np.int64)
+    rid, rnz, rsum = (np.empty(r.value, np.int64) for _ in range(3))
+    cid, cnz, csum = (np.empty(c.value, np.int64) for _ in range(3))
+    _lib.check(ctx._lib.nmx_flat_fetch(ctx.handle, edge_src.ctypes.data, rid.ctypes.data, rnz.ctypes.data,
+                                       rsum.ctypes.data, cid.ctypes.data, cnz.ctypes.data, csum.ctypes.data))
+    return FlatContainers(
+        edges=np.column_stack([edge_src, matrix.col_idx]),
+        weights=matrix.values.copy(),
+        out_degrees=rnz,
+        in_degrees=cnz,
+        row_sums=np.column_stack([rid, rsum]),
+        col_sums=np.column_stack([cid, csum]),
+    )
