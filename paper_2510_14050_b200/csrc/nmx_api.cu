@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "../../include/nmx.h"
-#include "nmx_kernels.cuh"
+#include "nmx_msd.cuh"
 
 using namespace nmx;
 
@@ -105,7 +105,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf keysA, keysB, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
+  DevBuf keysA, keysB, keysC, keysD, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
@@ -252,13 +252,14 @@ void launch_link_row(nmx_ctx* c, const uint64_t* keys, uint32_t m, int b, int wb
   ++c->launches;
 }
 
-void launch_hist(nmx_ctx* c, const PacketSrc& ps, int npass, uint32_t* d_small) {
+template <typename Src>
+void launch_hist(nmx_ctx* c, const Src& ps, int npass, uint32_t* d_small) {
   const uint64_t want = (ps.n + 1023) / 1024;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)c->sms * 8));
   auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
   switch (npass) {
 #define NMX_HCASE(P) \
-  case P: hist_kernel<P><<<grid, 256, 0, c->st>>>(ps, d_small + kHist, gcount); break;
+  case P: hist_kernel<Src, P><<<grid, 256, 0, c->st>>>(ps, d_small + kHist, gcount); break;
     NMX_HCASE(1) NMX_HCASE(2) NMX_HCASE(3) NMX_HCASE(4) NMX_HCASE(5) NMX_HCASE(6) NMX_HCASE(7) NMX_HCASE(8)
 #undef NMX_HCASE
     default: throw std::runtime_error("bad pass count");
@@ -407,10 +408,228 @@ uint32_t run_rbk(nmx_ctx* c, const KeyT* keys, const uint32_t* w, uint32_t n, in
   return r;
 }
 
+// ---- MSD partition + shared-memory grouping (nmx_msd.cuh) -------------------
+// used for the summed matrix when 2^20 <= n <= 2^30 and the D MSD bits are all
+// source bits; NMX_PATH=lsd forces the LSD path.
+int msd_bits(uint64_t n, int b) {
+  const char* e = getenv("NMX_PATH");
+  if (e && std::string(e) == "lsd") return 0;
+  if (n < (1ull << 20) || n > (1ull << 30)) return 0;
+  const int D = std::min(21, std::max(11, (int)ceil_log2(n) - 9));
+  return D <= b ? D : 0;
+}
+
+// LSD onesweep sort of m u64 keys (kb significant bits) between two buffers
+uint64_t* sort_keys_u64(nmx_ctx* c, uint64_t* keys, uint64_t m, int kb, uint64_t* other) {
+  uint32_t* d_small = c->small.as<uint32_t>();
+  const int npass = (kb + 7) / 8;
+  CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * 8 * kRadix, c->st));
+  KeySrc<uint64_t, false> ks{keys, nullptr, m};
+  launch_hist(c, ks, npass, d_small);
+  bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kHist, npass, d_small + kBase);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(c->h_small, d_small, sizeof(uint32_t) * 8 * kRadix, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->grow_status(tiles_of(m, kMinPassTile) * kRadix);
+  uint64_t* cur = keys;
+  uint64_t* alt = other;
+  int idx = 0;
+  for (int p = 0; p < npass; ++p) {
+    const uint32_t* hp = c->h_small + kHist + p * kRadix;
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d)
+      if (hp[d] == m) trivial = true;
+    if (trivial) continue;
+    KeySrc<uint64_t, false> src{cur, nullptr, m};
+    launch_pass<KeySrc<uint64_t, false>, uint64_t, false>(c, src, m, alt, nullptr, 8 * p,
+                                                          d_small + kBase + p * kRadix, d_small + kCounters + idx);
+    std::swap(cur, alt);
+    ++idx;
+  }
+  return cur;
+}
+
+void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                      int b, int D) {
+  const int kb = 2 * b;
+  const int D1 = std::min(11, D), D2 = D - D1;
+  const uint32_t nb = 1u << D;
+  stage_begin(c, 1);
+  uint32_t* d_small = c->small.as<uint32_t>();
+  auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
+  PacketSrc ps{d_src, d_dst, d_valid, n, 0, b};
+  // L1 histogram
+  {
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 1023) / 1024, (uint64_t)c->sms * 8));
+    msd_hist1_kernel<<<grid, 256, 0, c->st>>>(ps, kb - D1, d_small + kHist, gcount);
+    CK_LAUNCH();
+    ++c->launches;
+  }
+  c->mcur.grow(((size_t)nb + 8) * 4);
+  c->moff.grow(((size_t)nb + 8) * 4);
+  c->mhist2.grow(((size_t)nb + 8) * 4);
+  uint32_t* cur = c->mcur.as<uint32_t>();
+  uint32_t* off = c->moff.as<uint32_t>();
+  big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(d_small + kHist, 1u << D1, off, cur);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(c->h_small + kGCount, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const uint64_t m = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
+  if (m == 0) {
+    stage_finish(c, 1);
+    return;
+  }
+  c->keysA.grow(m * 8);
+  c->keysB.grow(m * 8);
+  c->mark();  // 1: scatter start
+  set_smem(msd_scatter_kernel<PacketSrc, 1>, sizeof(MsdSmem));
+  msd_scatter_kernel<PacketSrc, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(MsdSmem), c->st>>>(
+      ps, n, c->keysA.as<uint64_t>(), kb - D1, D1, 0, cur);
+  CK_LAUNCH();
+  ++c->launches;
+  uint64_t* keys = c->keysA.as<uint64_t>();
+  int sort_launches = 1;
+  if (D2 > 0) {
+    uint32_t* h2 = c->mhist2.as<uint32_t>();
+    CK(cudaMemsetAsync(h2, 0, (size_t)nb * 4, c->st));
+    msd_count2_kernel<<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(keys, m, kb - D, D2, kb - D1, h2);
+    CK_LAUNCH();
+    big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(h2, nb, off, cur);
+    CK_LAUNCH();
+    KeySrc<uint64_t, false> ks{keys, nullptr, m};
+    set_smem(msd_scatter_kernel<KeySrc<uint64_t, false>, 2>, sizeof(MsdSmem));
+    msd_scatter_kernel<KeySrc<uint64_t, false>, 2>
+        <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(MsdSmem), c->st>>>(ks, m, c->keysB.as<uint64_t>(),
+                                                                                     kb - D, D2, kb - D1, cur);
+    CK_LAUNCH();
+    c->launches += 3;
+    keys = c->keysB.as<uint64_t>();
+    ++sort_launches;
+  }
+  c->last_sort_launches = sort_launches;
+  c->mark();  // 2: scatter end
+  // groups of whole buckets, shared-memory grouping
+  const uint32_t S = 1024, capb = 1024;
+  const uint32_t ngroups = (uint32_t)((m + S - 1) / S);
+  c->mgb.grow(((size_t)ngroups + 2) * 4);
+  c->mheavy.grow(((size_t)ngroups + 2) * 8);
+  c->colL_dst.grow(m * 4);
+  c->colL_cnt.grow(m * 4);
+  group_bounds_kernel<<<(unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8), 256, 0, c->st>>>(
+      off, nb, S, ngroups, c->mgb.as<uint32_t>());
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(d_small + kCounters + 30, 0, 8, c->st));
+  set_smem(local_rows_kernel, sizeof(LocSmem));
+  local_rows_kernel<<<(unsigned)(c->sms * 3), kLocThreads, sizeof(LocSmem), c->st>>>(
+      keys, off, c->mgb.as<uint32_t>(), ngroups, capb, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
+      c->mheavy.as<uint32_t>(), d_small + kCounters + 31, d_small + kCounters + 30, c->stats.as<unsigned long long>());
+  CK_LAUNCH();
+  c->launches += 2;
+  c->mark();  // 3: local end
+  uint32_t nheavy = 0;
+  CK(cudaMemcpyAsync(&nheavy, d_small + kCounters + 31, 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  uint64_t uh = 0;
+  if (nheavy) {
+    std::vector<uint32_t> hr(2 * (size_t)nheavy), dof(nheavy);
+    CK(cudaMemcpyAsync(hr.data(), c->mheavy.p, hr.size() * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    uint64_t mh = 0;
+    for (uint32_t r = 0; r < nheavy; ++r) {
+      dof[r] = (uint32_t)mh;
+      mh += hr[2 * r + 1] - hr[2 * r];
+    }
+    c->mdst.grow((size_t)nheavy * 4);
+    CK(cudaMemcpyAsync(c->mdst.p, dof.data(), (size_t)nheavy * 4, cudaMemcpyHostToDevice, c->st));
+    c->keysC.grow(mh * 8);
+    c->keysD.grow(mh * 8);
+    gather_ranges_kernel<<<(unsigned)std::min<uint32_t>(nheavy, c->sms * 8), 256, 0, c->st>>>(
+        keys, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, c->keysC.as<uint64_t>(),
+        c->colL_cnt.as<uint32_t>());
+    CK_LAUNCH();
+    uint64_t* hs = sort_keys_u64(c, c->keysC.as<uint64_t>(), mh, kb, c->keysD.as<uint64_t>());
+    c->ckA.grow(mh * 4);
+    c->cvA.grow(mh * 4);
+    if (c->lrstatus.grow(tiles_of(mh, kSegTile) * sizeof(LRStatus)))
+      CK(cudaMemsetAsync(c->lrstatus.p, 0, c->lrstatus.cap, c->st));
+    launch_link_row<uint32_t>(c, hs, (uint32_t)mh, b, 0, d_small);
+    CK(cudaMemcpyAsync(c->h_small + kU, d_small + kU, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    uh = c->h_small[kU];
+  }
+  c->mark();  // 4: heavy end
+  // columns: light slots (with holes) + heavy entries -> onesweep -> col_kernel
+  const int ncolpass = (b + 7) / 8;
+  CK(cudaMemsetAsync(d_small + kCHist, 0, sizeof(uint32_t) * 8 * kRadix, c->st));
+  CK(cudaMemsetAsync(gcount, 0, 8, c->st));
+  ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), m,
+                  c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh, m + uh};
+  {
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m + uh + 1023) / 1024, (uint64_t)c->sms * 8));
+    switch (ncolpass) {
+      case 1: hist_concat_kernel<1><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
+      case 2: hist_concat_kernel<2><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
+      case 3: hist_concat_kernel<3><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
+      default: hist_concat_kernel<4><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
+    }
+    CK_LAUNCH();
+    bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kCHist, ncolpass, d_small + kCBase);
+    CK_LAUNCH();
+    c->launches += 2;
+  }
+  CK(cudaMemcpyAsync(c->h_small, d_small, kSmallWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const uint64_t u = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
+  c->ckA.grow(std::max<uint64_t>(u, uh) * 4);
+  c->cvA.grow(std::max<uint64_t>(u, uh) * 4);
+  c->ckB.grow(u * 4);
+  c->cvB.grow(u * 4);
+  c->grow_status(tiles_of(m + uh, kMinPassTile) * kRadix);
+  std::vector<int> active;
+  for (int p = 0; p < ncolpass; ++p) {
+    const uint32_t* hp = c->h_small + kCHist + p * kRadix;
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d)
+      if (hp[d] == u) trivial = true;
+    if (!trivial) active.push_back(p);
+  }
+  if (active.empty()) active.push_back(0);
+  uint32_t* ck = nullptr;
+  uint32_t* cv = nullptr;
+  for (size_t i = 0; i < active.size(); ++i) {
+    const int p = active[i];
+    uint32_t* ok = (i & 1) ? c->ckA.as<uint32_t>() : c->ckB.as<uint32_t>();
+    uint32_t* ov = (i & 1) ? c->cvA.as<uint32_t>() : c->cvB.as<uint32_t>();
+    if (i == 0) {
+      launch_pass<ColConcatSrc, uint32_t, true>(c, cs, m + uh, ok, ov, 8 * p, d_small + kCBase + p * kRadix,
+                                                d_small + kCounters + 16 + i);
+    } else {
+      KeySrc<uint32_t, true> ks{ck, cv, u};
+      launch_pass<KeySrc<uint32_t, true>, uint32_t, true>(c, ks, u, ok, ov, 8 * p, d_small + kCBase + p * kRadix,
+                                                          d_small + kCounters + 16 + i);
+    }
+    ck = ok;
+    cv = ov;
+  }
+  c->mark();  // 5: column sort end
+  if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
+    CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+  col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
+      ck, cv, (uint32_t)u, b, 0, c->csstatus.as<CSStatus>(), c->next_epoch(), d_small + kCounters + 26,
+      c->stats.as<unsigned long long>());
+  CK_LAUNCH();
+  ++c->launches;
+  stage_finish(c, 1);
+}
+
 // The whole pipeline over packet columns already on the device. Writes W*9
 // statistics (u64) into c->h_stats. Windows: window_size == 0 -> one window.
 void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
                   int b, uint64_t window_size, uint64_t W) {
+  if (W == 1) {
+    const int D = msd_bits(n, b);
+    if (D) return run_pipeline_msd(c, d_src, d_dst, d_valid, n, b, D);
+  }
   const int wb = W > 1 ? (int)ceil_log2(W) : 0;
   stage_begin(c, W);
   PacketSrc ps{d_src, d_dst, d_valid, n, W > 1 ? window_size : 0, b};
@@ -582,7 +801,8 @@ void nmx_destroy(nmx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (DevBuf* b : {&c->keysA, &c->keysB, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
+  for (DevBuf* b : {&c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
+                    &c->mhist2, &c->mgb, &c->mheavy, &c->mdst, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
     b->release();

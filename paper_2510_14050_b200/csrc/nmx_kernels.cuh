@@ -78,8 +78,8 @@ struct KeySrc {
 // ---------------------------------------------------------------------------
 // K1: digit histograms for every pass, plus the valid-item count
 // ---------------------------------------------------------------------------
-template <int NPASS>
-__global__ void __launch_bounds__(256) hist_kernel(PacketSrc src, uint32_t* __restrict__ ghist,
+template <typename Src, int NPASS>
+__global__ void __launch_bounds__(256) hist_kernel(Src src, uint32_t* __restrict__ ghist,
                                                   unsigned long long* __restrict__ gcount) {
   __shared__ uint32_t h[NPASS][kRadix];
   for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) (&h[0][0])[i] = 0;
@@ -1028,7 +1028,7 @@ __global__ void csr_expand_kernel(const long long* __restrict__ row_ptr, uint64_
 __global__ void coo_rowptr_kernel(const uint64_t* __restrict__ keys, uint64_t lo, uint64_t hi, uint64_t wbase,
                                   int b, uint64_t dim, long long* __restrict__ row_ptr) {
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= dim; r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t target = wbase | (r << b);
+    const uint64_t target = wbase + (r << b);  // r == 2^b reaches the next window
     uint64_t a = lo, z = hi;  // first index with key >= target
     while (a < z) {
       const uint64_t mid = (a + z) >> 1;

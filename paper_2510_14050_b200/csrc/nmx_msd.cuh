@@ -1,0 +1,555 @@
+// nmx_msd.cuh -- MSD partition + shared-memory grouping path for the summed matrix.
+//
+// The LSD path sorts all 2b key bits (8 + 4 onesweep passes at b = 32). Grouping
+// only needs equal keys together, so here:
+//   L1  msd_scatter<level 1>  packets -> keys grouped by the top D1 key bits
+//   L2  msd_count2 + scan, msd_scatter<level 2>  -> grouped by the top D = D1+D2 bits
+//       (buckets of ~2^10 keys; the top D bits are source bits, so every source
+//       lies in one bucket)
+//   LOC local_rows_kernel  per group of whole buckets: hash the keys into shared
+//       memory (links with counts, sources with packets and fan-out), emit the
+//       (dst, count) column entries in place, accumulate link + row statistics
+// Buckets larger than the shared-memory capacity ("heavy", power-law hitters)
+// are gathered and finished by the LSD path (onesweep + link_row_kernel).
+// Both scatter levels are non-stable: a tile ranks keys with shared atomics and
+// reserves each digit's output range with one global atomicAdd per digit, so
+// there is no lookback chain; order inside a bucket is irrelevant to the
+// statistics.
+#pragma once
+#include "nmx_kernels.cuh"
+
+namespace nmx {
+
+constexpr int kMsdThreads = 512;
+constexpr int kMsdIPT = 8;
+constexpr int kMsdTile = kMsdThreads * kMsdIPT;  // 4096 keys
+constexpr int kMsdMaxBins = 2048;                // 2 x 2^10 (level 2 spans <= 2 level-1 buckets per bin set)
+
+// block exclusive scan of NB counters held in smem (512 threads, NB % 512 == 0 or NB <= 512)
+template <int NB>
+__device__ __forceinline__ void smem_excl_scan(uint32_t* cnt, uint32_t* out, uint32_t* wt) {
+  constexpr int PER = (NB + kMsdThreads - 1) / kMsdThreads;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t loc[PER];
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int i = tid * PER + q;
+    loc[q] = i < NB ? cnt[i] : 0u;
+    s += loc[q];
+  }
+  uint32_t inc = warp_incl_scan(s, lane);
+  if (lane == 31) wt[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < kMsdThreads / 32 ? wt[lane] : 0u;
+    const uint32_t vi = warp_incl_scan(v, lane);
+    if (lane < kMsdThreads / 32) wt[lane] = vi - v;
+  }
+  __syncthreads();
+  uint32_t run = wt[warp] + inc - s;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int i = tid * PER + q;
+    if (i < NB) out[i] = run;
+    run += loc[q];
+  }
+  __syncthreads();
+}
+
+// Level 1 (Src = PacketSrc, cursor indexed by the D1-bit digit) and level 2
+// (Src = KeySrc<u64>, cursor indexed by the D-bit bucket id; a tile lies in one
+// or two level-1 buckets, keys of further buckets take a per-key global atomic).
+struct MsdSmem {
+  uint64_t stage[kMsdTile];
+  uint32_t cnt[kMsdMaxBins];
+  uint32_t tstart[kMsdMaxBins];
+  uint32_t gbase[kMsdMaxBins];
+  uint32_t wt[kMsdThreads / 32 + 1];
+  uint64_t b1first;
+};
+
+template <typename Src, int LEVEL>
+__global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint64_t n_items,
+                                                                   uint64_t* __restrict__ out, int shift, int dbits,
+                                                                   int bshift, uint32_t* __restrict__ cursor) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MsdSmem& S = *reinterpret_cast<MsdSmem*>(smem_raw);
+  uint32_t* cnt = S.cnt;
+  uint32_t* tstart = S.tstart;
+  uint32_t* gbase = S.gbase;
+  uint32_t* wt = S.wt;
+  uint64_t* stage = S.stage;
+  uint64_t& s_b1first = S.b1first;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nbins = LEVEL == 1 ? (1 << dbits) : (2 << dbits);
+  for (int i = tid; i < kMsdMaxBins; i += kMsdThreads) cnt[i] = 0;
+  const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
+  if (LEVEL == 2 && tid == 0) {
+    uint64_t k0 = 0;
+    uint32_t v;
+    src.load(base, k0, v);
+    s_b1first = k0 >> bshift;
+  }
+  __syncthreads();
+  const uint32_t dmask = (1u << dbits) - 1;
+  uint64_t k[kMsdIPT];
+  uint32_t rank[kMsdIPT];
+  int bin[kMsdIPT];
+#pragma unroll
+  for (int i = 0; i < kMsdIPT; ++i) {
+    uint32_t v;
+    const uint64_t idx = base + (uint64_t)warp * 32 * kMsdIPT + (uint64_t)i * 32 + lane;
+    bin[i] = -1;
+    if (src.load(idx, k[i], v)) {
+      const uint32_t d = (uint32_t)(k[i] >> shift) & dmask;
+      if (LEVEL == 1) {
+        bin[i] = (int)d;
+      } else {
+        const uint64_t rel = (k[i] >> bshift) - s_b1first;
+        if (rel < 2) {
+          bin[i] = (int)((rel << dbits) | d);
+        } else {  // third+ level-1 bucket inside one tile: direct placement
+          const uint32_t g = (uint32_t)(k[i] >> shift);
+          out[atomicAdd(cursor + g, 1u)] = k[i];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMsdIPT; ++i)
+    if (bin[i] >= 0) rank[i] = atomicAdd(&cnt[bin[i]], 1u);
+  __syncthreads();
+  if (LEVEL == 1 && (1 << dbits) <= kMsdThreads)
+    smem_excl_scan<kMsdThreads>(cnt, tstart, wt);
+  else
+    smem_excl_scan<kMsdMaxBins>(cnt, tstart, wt);
+  // reserve each non-empty digit's range in the output
+  for (int i = tid; i < nbins; i += kMsdThreads) {
+    const uint32_t c = cnt[i];
+    if (c) {
+      uint32_t g;
+      if (LEVEL == 1)
+        g = (uint32_t)i;
+      else
+        g = (uint32_t)(((s_b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask));
+      gbase[i] = atomicAdd(cursor + g, c) - tstart[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMsdIPT; ++i)
+    if (bin[i] >= 0) stage[tstart[bin[i]] + rank[i]] = k[i];
+  __syncthreads();
+  uint32_t total = 0;
+  if (nbins > 0) total = tstart[nbins - 1] + cnt[nbins - 1];
+  for (uint32_t j = tid; j < total; j += kMsdThreads) {
+    const uint64_t key = stage[j];
+    int b;
+    if (LEVEL == 1)
+      b = (int)((uint32_t)(key >> shift) & dmask);
+    else
+      b = (int)((((key >> bshift) - s_b1first) << dbits) | ((key >> shift) & dmask));
+    out[gbase[b] + j] = key;
+  }
+}
+
+// level-1 histogram: top D1 bits of the packed key (+ valid count)
+__global__ void __launch_bounds__(256) msd_hist1_kernel(PacketSrc src, int shift, uint32_t* __restrict__ hist1,
+                                                       unsigned long long* __restrict__ gcount) {
+  __shared__ uint32_t h[kMsdMaxBins];
+  for (int i = threadIdx.x; i < kMsdMaxBins; i += 256) h[i] = 0;
+  __syncthreads();
+  uint32_t c = 0;
+  constexpr int U = 4;
+  const uint64_t stride = (uint64_t)gridDim.x * 256 * U;
+  for (uint64_t base = (uint64_t)blockIdx.x * 256 * U; base < src.n; base += stride) {
+    uint64_t k[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t v;
+      ok[u] = src.load(base + (uint64_t)u * 256 + threadIdx.x, k[u], v);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) {
+        ++c;
+        atomicAdd(&h[(uint32_t)(k[u] >> shift)], 1u);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(gcount, (unsigned long long)c);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMsdMaxBins; i += 256)
+    if (h[i]) atomicAdd(hist1 + i, h[i]);
+}
+
+// level-2 digit counts per level-1 bucket over the level-1 output
+__global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const uint64_t* __restrict__ keys, uint64_t m,
+                                                                  int shift, int dbits, int bshift,
+                                                                  uint32_t* __restrict__ hist2) {
+  __shared__ uint32_t cnt[kMsdMaxBins];
+  __shared__ uint64_t s_b1first;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kMsdMaxBins; i += kMsdThreads) cnt[i] = 0;
+  const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
+  if (tid == 0) s_b1first = keys[base] >> bshift;
+  __syncthreads();
+  const uint32_t dmask = (1u << dbits) - 1;
+  for (int i = 0; i < kMsdIPT; ++i) {
+    const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
+    if (idx < m) {
+      const uint64_t key = keys[idx];
+      const uint64_t rel = (key >> bshift) - s_b1first;
+      if (rel < 2)
+        atomicAdd(&cnt[(rel << dbits) | ((key >> shift) & dmask)], 1u);
+      else
+        atomicAdd(hist2 + (uint32_t)(key >> shift), 1u);
+    }
+  }
+  __syncthreads();
+  const int nbins = 2 << dbits;
+  for (int i = tid; i < nbins; i += kMsdThreads) {
+    const uint32_t c = cnt[i];
+    if (c) {
+      const uint64_t g = ((s_b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask);
+      atomicAdd(hist2 + g, c);
+    }
+  }
+}
+
+// exclusive scan of nb counters (single CTA, 1024 threads): off[0..nb], cursor = off
+__global__ void __launch_bounds__(1024) big_excl_scan_kernel(const uint32_t* __restrict__ cnt, uint32_t nb,
+                                                            uint32_t* __restrict__ off, uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t wt[33];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t per = (nb + 1023) / 1024;
+  const uint32_t lo = tid * per, hi = min(nb, lo + per);
+  uint32_t s = 0;
+  for (uint32_t i = lo; i < hi; ++i) s += cnt[i];
+  const uint32_t inc = warp_incl_scan(s, lane);
+  if (lane == 31) wt[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = wt[lane];
+    const uint32_t vi = warp_incl_scan(v, lane);
+    wt[lane] = vi - v;
+    if (lane == 31) wt[32] = vi;
+  }
+  __syncthreads();
+  uint32_t run = wt[warp] + inc - s;
+  for (uint32_t i = lo; i < hi; ++i) {
+    off[i] = run;
+    if (cursor) cursor[i] = run;
+    run += cnt[i];
+  }
+  if (tid == 0) off[nb] = wt[32];
+}
+
+// group g covers the buckets whose start lies in [g*S, (g+1)*S)
+__global__ void group_bounds_kernel(const uint32_t* __restrict__ off, uint32_t nb, uint32_t S, uint32_t ngroups,
+                                    uint32_t* __restrict__ gb) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g <= ngroups; g += gridDim.x * blockDim.x) {
+    const uint64_t target = (uint64_t)g * S;
+    uint32_t a = 0, z = nb;  // first bucket with off >= target (nb if none)
+    while (a < z) {
+      const uint32_t mid = (a + z) >> 1;
+      if (off[mid] < target)
+        a = mid + 1;
+      else
+        z = mid;
+    }
+    gb[g] = g == ngroups ? nb : a;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LOC: per group of buckets, shared-memory hash grouping
+// ---------------------------------------------------------------------------
+constexpr int kLocThreads = 512;
+constexpr int kLocMaxKeys = 2048;  // light keys per group (chunk S + one light bucket)
+constexpr int kLocT1 = 3072;       // link table slots (load <= 2/3)
+constexpr int kLocT2 = 3072;       // source table slots
+constexpr int kLocMaxHeavy = 8;
+
+struct LocSmem {
+  unsigned long long t1key[kLocT1];  // key + 1 (0 = empty)
+  uint32_t t1cnt[kLocT1];
+  uint32_t t2key[kLocT2];  // src + 1 (0 = empty)
+  uint32_t t2pk[kLocT2];
+  uint32_t t2fo[kLocT2];
+  uint32_t heavy_lo[kLocMaxHeavy], heavy_hi[kLocMaxHeavy];
+  uint32_t nheavy;
+  uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
+  uint32_t wt[kLocThreads / 32 + 1];
+  uint32_t group, blo, bhi, klo, khi;
+};
+
+__device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
+  const uint64_t h = x * 0x9E3779B97F4A7C15ull;
+  return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
+}
+
+__global__ void __launch_bounds__(kLocThreads, 3)
+    local_rows_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ off,
+                      const uint32_t* __restrict__ gb, uint32_t ngroups, uint32_t capb, int b,
+                      uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt, uint32_t* __restrict__ heavy,
+                      uint32_t* __restrict__ nheavy_out, uint32_t* __restrict__ group_counter,
+                      unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kLocT1; i += kLocThreads) {
+    s.t1key[i] = 0;
+    s.t1cnt[i] = 0;
+  }
+  for (int i = tid; i < kLocT2; i += kLocThreads) {
+    s.t2key[i] = 0;
+    s.t2pk[i] = 0;
+    s.t2fo[i] = 0;
+  }
+  if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+  const uint64_t dmask = (1ull << b) - 1;
+  unsigned long long a_valid = 0, a_links = 0, a_srcs = 0, a_mlink = 0, a_msrc = 0, a_mfan = 0;
+  for (;;) {
+    if (tid == 0) {
+      const uint32_t g = atomicAdd(group_counter, 1u);
+      s.group = g;
+      if (g < ngroups) {
+        s.blo = gb[g];
+        s.bhi = gb[g + 1];
+        s.klo = off[s.blo];
+        s.khi = off[s.bhi];
+      }
+      s.nheavy = 0;
+    }
+    __syncthreads();
+    if (s.group >= ngroups) break;
+    const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
+    // heavy buckets of this group: excluded here, finished by the LSD path
+    for (uint32_t j = blo + tid; j < bhi; j += kLocThreads) {
+      const uint32_t lo = off[j], hi = off[j + 1];
+      if (hi - lo > capb) {
+        const uint32_t q = atomicAdd(&s.nheavy, 1u);
+        if (q < kLocMaxHeavy) {
+          s.heavy_lo[q] = lo;
+          s.heavy_hi[q] = hi;
+        }
+        const uint32_t gq = atomicAdd(nheavy_out, 1u);
+        heavy[2 * gq] = lo;
+        heavy[2 * gq + 1] = hi;
+      }
+    }
+    __syncthreads();
+    const uint32_t nh = min(s.nheavy, (uint32_t)kLocMaxHeavy);
+    // light segments of [klo, khi): heavy ranges removed (their column slots are
+    // zeroed by gather_ranges_kernel). Buckets start inside a chunk of S keys and a
+    // heavy bucket has > capb >= S keys, so nh <= 1 and there are <= 2 segments.
+    uint32_t seg_lo[2], seg_hi[2];
+    uint32_t nseg = 0;
+    if (nh == 0) {
+      seg_lo[0] = klo;
+      seg_hi[0] = khi;
+      nseg = 1;
+    } else {
+      seg_lo[0] = klo;
+      seg_hi[0] = s.heavy_lo[0];
+      seg_lo[1] = s.heavy_hi[0];
+      seg_hi[1] = khi;
+      nseg = 2;
+    }
+    // insert every light key
+    for (uint32_t sg = 0; sg < nseg; ++sg) {
+      for (uint32_t i = seg_lo[sg] + tid; i < seg_hi[sg]; i += kLocThreads) {
+        const uint64_t key = keys[i];
+        bool fresh;
+        if (key == ~0ull) {
+          fresh = atomicAdd(&s.sp_link, 1u) == 0;
+        } else {
+          const unsigned long long kk = key + 1;
+          uint32_t h = hslot(kk, kLocT1);
+          for (;;) {
+            unsigned long long cur = s.t1key[h];
+            if (cur == 0) {
+              cur = atomicCAS(&s.t1key[h], 0ull, kk);
+              if (cur == 0) {
+                atomicAdd(&s.t1cnt[h], 1u);
+                fresh = true;
+                break;
+              }
+            }
+            if (cur == kk) {
+              atomicAdd(&s.t1cnt[h], 1u);
+              fresh = false;
+              break;
+            }
+            h = h + 1 == kLocT1 ? 0 : h + 1;
+          }
+        }
+        const uint32_t src = (uint32_t)(key >> b);
+        if (src == 0xFFFFFFFFu) {
+          atomicAdd(&s.sp_src_pk, 1u);
+          if (fresh) atomicAdd(&s.sp_src_fo, 1u);
+        } else {
+          const uint32_t sk = src + 1;
+          uint32_t h = hslot(sk, kLocT2);
+          for (;;) {
+            uint32_t cur = s.t2key[h];
+            if (cur == 0) {
+              cur = atomicCAS(&s.t2key[h], 0u, sk);
+              if (cur == 0) cur = sk;
+            }
+            if (cur == sk) {
+              atomicAdd(&s.t2pk[h], 1u);
+              if (fresh) atomicAdd(&s.t2fo[h], 1u);
+              break;
+            }
+            h = h + 1 == kLocT2 ? 0 : h + 1;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // links: occupied slots -> compacted (dst, count) in the light slots of this group
+    uint32_t mine = 0;
+    for (int j = tid; j < kLocT1; j += kLocThreads) mine += s.t1key[j] != 0;
+    uint32_t total;
+    uint32_t at = block_excl_scan_n<kLocThreads>(mine, s.wt, &total);
+    const uint32_t len0 = seg_hi[0] - seg_lo[0];
+    auto slot_of = [&](uint32_t j) -> uint32_t { return j < len0 ? seg_lo[0] + j : seg_lo[1] + (j - len0); };
+    const uint32_t sp = s.sp_link;
+    for (int j = tid; j < kLocT1; j += kLocThreads) {
+      const unsigned long long kk = s.t1key[j];
+      if (kk) {
+        const uint64_t key = kk - 1;
+        const uint32_t c = s.t1cnt[j];
+        const uint32_t pos = slot_of(at);
+        col_dst[pos] = (uint32_t)(key & dmask);
+        col_cnt[pos] = c;
+        ++at;
+        a_links += 1;
+        a_valid += c;
+        a_mlink = max(a_mlink, (unsigned long long)c);
+        s.t1key[j] = 0;
+        s.t1cnt[j] = 0;
+      }
+    }
+    uint32_t used = total;
+    if (sp) {
+      if (tid == 0) {
+        const uint32_t pos = slot_of(total);
+        col_dst[pos] = (uint32_t)dmask;
+        col_cnt[pos] = sp;
+        a_links += 1;
+        a_valid += sp;
+        a_mlink = max(a_mlink, (unsigned long long)sp);
+      }
+      used += 1;
+    }
+    // the remaining light slots become holes (count 0)
+    uint32_t nlight = 0;
+    for (uint32_t sg = 0; sg < nseg; ++sg) nlight += seg_hi[sg] - seg_lo[sg];
+    for (uint32_t j = used + tid; j < nlight; j += kLocThreads) col_cnt[slot_of(j)] = 0;
+    // sources
+    for (int j = tid; j < kLocT2; j += kLocThreads) {
+      if (s.t2key[j]) {
+        a_srcs += 1;
+        a_msrc = max(a_msrc, (unsigned long long)s.t2pk[j]);
+        a_mfan = max(a_mfan, (unsigned long long)s.t2fo[j]);
+        s.t2key[j] = 0;
+        s.t2pk[j] = 0;
+        s.t2fo[j] = 0;
+      }
+    }
+    if (tid == 0 && s.sp_src_pk) {
+      a_srcs += 1;
+      a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk);
+      a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo);
+    }
+    __syncthreads();
+    if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a_valid += __shfl_xor_sync(FULL, a_valid, o);
+    a_links += __shfl_xor_sync(FULL, a_links, o);
+    a_srcs += __shfl_xor_sync(FULL, a_srcs, o);
+    a_mlink = max(a_mlink, __shfl_xor_sync(FULL, a_mlink, o));
+    a_msrc = max(a_msrc, __shfl_xor_sync(FULL, a_msrc, o));
+    a_mfan = max(a_mfan, __shfl_xor_sync(FULL, a_mfan, o));
+  }
+  if (lane == 0) {
+    if (a_valid) atomicAdd(stats + S_VALID, a_valid);
+    if (a_links) atomicAdd(stats + S_LINKS, a_links);
+    if (a_srcs) atomicAdd(stats + S_SRCS, a_srcs);
+    if (a_mlink) atomicMax(stats + S_MAXLINK, a_mlink);
+    if (a_msrc) atomicMax(stats + S_MAXSRCPK, a_msrc);
+    if (a_mfan) atomicMax(stats + S_MAXFANOUT, a_mfan);
+  }
+  (void)warp;
+}
+
+// gather heavy bucket ranges into one contiguous array
+// (and turn their slots of the light column array into holes)
+__global__ void gather_ranges_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ranges,
+                                     const uint32_t* __restrict__ dstoff, uint32_t nranges,
+                                     uint64_t* __restrict__ out, uint32_t* __restrict__ col_cnt) {
+  for (uint32_t r = blockIdx.x; r < nranges; r += gridDim.x) {
+    const uint32_t lo = ranges[2 * r], hi = ranges[2 * r + 1], o = dstoff[r];
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      out[o + (i - lo)] = keys[i];
+      col_cnt[i] = 0;
+    }
+  }
+}
+
+// column entries from two arrays; entries with a zero count are holes
+struct ColConcatSrc {
+  const uint32_t* k1;
+  const uint32_t* v1;
+  uint64_t n1;
+  const uint32_t* k2;
+  const uint32_t* v2;
+  uint64_t n2;
+  uint64_t n;  // n1 + n2
+  __device__ __forceinline__ bool load(uint64_t i, uint32_t& key, uint32_t& val) const {
+    if (i >= n) return false;
+    if (i < n1) {
+      val = v1[i];
+      if (!val) return false;
+      key = k1[i];
+    } else {
+      key = k2[i - n1];
+      val = v2[i - n1];
+    }
+    return true;
+  }
+};
+
+template <int NPASS>
+__global__ void __launch_bounds__(256) hist_concat_kernel(ColConcatSrc src, uint32_t* __restrict__ ghist,
+                                                         unsigned long long* __restrict__ gcount) {
+  __shared__ uint32_t h[NPASS][kRadix];
+  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) (&h[0][0])[i] = 0;
+  __syncthreads();
+  uint32_t c = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < src.n; i += (uint64_t)gridDim.x * 256) {
+    uint32_t k, v;
+    if (src.load(i, k, v)) {
+      ++c;
+#pragma unroll
+      for (int p = 0; p < NPASS; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFFu], 1u);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(gcount, (unsigned long long)c);
+  __syncthreads();
+  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) {
+    const uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(ghist + i, v);
+  }
+}
+
+}  // namespace nmx
