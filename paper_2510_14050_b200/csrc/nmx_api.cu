@@ -105,7 +105,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf keysA, keysB, keysC, keysD, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
+  DevBuf keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
@@ -449,22 +449,58 @@ uint64_t* sort_keys_u64(nmx_ctx* c, uint64_t* keys, uint64_t m, int kb, uint64_t
   return cur;
 }
 
-void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
-                      int b, int D) {
-  const int kb = 2 * b;
+// LSD onesweep sort of n (u32 key, u32 value) pairs (nbits significant key bits)
+std::pair<uint32_t*, uint32_t*> sort_u32_pairs(nmx_ctx* c, uint32_t* k, uint32_t* v, uint64_t n, int nbits,
+                                               uint32_t* k2, uint32_t* v2) {
+  uint32_t* d_small = c->small.as<uint32_t>();
+  const int npass = (nbits + 7) / 8;
+  CK(cudaMemsetAsync(d_small + kCHist, 0, sizeof(uint32_t) * 8 * kRadix, c->st));
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 1023) / 1024, (uint64_t)c->sms * 8));
+  switch (npass) {
+    case 1: hist_u32_kernel<1><<<grid, 256, 0, c->st>>>(k, n, d_small + kCHist); break;
+    case 2: hist_u32_kernel<2><<<grid, 256, 0, c->st>>>(k, n, d_small + kCHist); break;
+    case 3: hist_u32_kernel<3><<<grid, 256, 0, c->st>>>(k, n, d_small + kCHist); break;
+    default: hist_u32_kernel<4><<<grid, 256, 0, c->st>>>(k, n, d_small + kCHist); break;
+  }
+  CK_LAUNCH();
+  bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kCHist, npass, d_small + kCBase);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(c->h_small + kCHist, d_small + kCHist, sizeof(uint32_t) * npass * kRadix, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->grow_status(tiles_of(n, kMinPassTile) * kRadix);
+  int idx = 0;
+  for (int p = 0; p < npass; ++p) {
+    const uint32_t* hp = c->h_small + kCHist + p * kRadix;
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d)
+      if (hp[d] == n) trivial = true;
+    if (trivial) continue;
+    KeySrc<uint32_t, true> src{k, v, n};
+    launch_pass<KeySrc<uint32_t, true>, uint32_t, true>(c, src, n, k2, v2, 8 * p, d_small + kCBase + p * kRadix,
+                                                        d_small + kCounters + 16 + idx);
+    std::swap(k, k2);
+    std::swap(v, v2);
+    ++idx;
+  }
+  return {k, v};
+}
+
+// Two-level non-stable MSD partition of the valid items of `src` (kb-bit keys)
+// by their top D bits. Leaves bucket offsets in c->moff (2^D + 1 entries) and
+// returns the partitioned keys / values and the number of valid items.
+template <typename Src, typename KeyT, bool HAS_VAL>
+uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, KeyT* outA, uint32_t* voutA,
+                       KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v) {
   const int D1 = std::min(11, D), D2 = D - D1;
   const uint32_t nb = 1u << D;
-  stage_begin(c, 1);
   uint32_t* d_small = c->small.as<uint32_t>();
   auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
-  PacketSrc ps{d_src, d_dst, d_valid, n, 0, b};
-  // L1 histogram
-  {
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 1023) / 1024, (uint64_t)c->sms * 8));
-    msd_hist1_kernel<<<grid, 256, 0, c->st>>>(ps, kb - D1, d_small + kHist, gcount);
-    CK_LAUNCH();
-    ++c->launches;
-  }
+  CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
+  CK(cudaMemsetAsync(gcount, 0, 8, c->st));
+  const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
+  msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - D1, d_small + kHist, gcount);
+  CK_LAUNCH();
   c->mcur.grow(((size_t)nb + 8) * 4);
   c->moff.grow(((size_t)nb + 8) * 4);
   c->mhist2.grow(((size_t)nb + 8) * 4);
@@ -472,49 +508,94 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   uint32_t* off = c->moff.as<uint32_t>();
   big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(d_small + kHist, 1u << D1, off, cur);
   CK_LAUNCH();
-  CK(cudaMemcpyAsync(c->h_small + kGCount, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+  unsigned long long m = 0;
+  CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  const uint64_t m = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
-  if (m == 0) {
-    stage_finish(c, 1);
-    return;
-  }
-  c->keysA.grow(m * 8);
-  c->keysB.grow(m * 8);
-  c->mark();  // 1: scatter start
-  set_smem(msd_scatter_kernel<PacketSrc, 1>, sizeof(MsdSmem));
-  msd_scatter_kernel<PacketSrc, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(MsdSmem), c->st>>>(
-      ps, n, c->keysA.as<uint64_t>(), kb - D1, D1, 0, cur);
+  c->launches += 2;
+  *res_k = outA;
+  *res_v = voutA;
+  if (!m) return 0;
+  using S1 = MsdSmem<KeyT, HAS_VAL>;
+  set_smem(msd_scatter_kernel<Src, KeyT, HAS_VAL, 1>, sizeof(S1));
+  msd_scatter_kernel<Src, KeyT, HAS_VAL, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
+      src, n, outA, voutA, kb - D1, D1, 0, cur);
   CK_LAUNCH();
   ++c->launches;
-  uint64_t* keys = c->keysA.as<uint64_t>();
-  int sort_launches = 1;
   if (D2 > 0) {
     uint32_t* h2 = c->mhist2.as<uint32_t>();
     CK(cudaMemsetAsync(h2, 0, (size_t)nb * 4, c->st));
-    msd_count2_kernel<<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(keys, m, kb - D, D2, kb - D1, h2);
+    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(outA, m, kb - D, D2, kb - D1,
+                                                                                         h2);
     CK_LAUNCH();
     big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(h2, nb, off, cur);
     CK_LAUNCH();
-    KeySrc<uint64_t, false> ks{keys, nullptr, m};
-    set_smem(msd_scatter_kernel<KeySrc<uint64_t, false>, 2>, sizeof(MsdSmem));
-    msd_scatter_kernel<KeySrc<uint64_t, false>, 2>
-        <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(MsdSmem), c->st>>>(ks, m, c->keysB.as<uint64_t>(),
-                                                                                     kb - D, D2, kb - D1, cur);
+    KeySrc<KeyT, HAS_VAL> ks{outA, voutA, m};
+    set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>, sizeof(S1));
+    msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>
+        <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(ks, m, outB, voutB, kb - D, D2,
+                                                                               kb - D1, cur);
     CK_LAUNCH();
     c->launches += 3;
-    keys = c->keysB.as<uint64_t>();
-    ++sort_launches;
+    *res_k = outB;
+    *res_v = voutB;
   }
-  c->last_sort_launches = sort_launches;
-  c->mark();  // 2: scatter end
-  // groups of whole buckets, shared-memory grouping
+  return m;
+}
+
+// heavy bucket list of the last local kernel -> (count, host ranges, device dst offsets)
+uint64_t fetch_heavy(nmx_ctx* c, uint32_t* d_count, uint32_t* nheavy_out) {
+  uint32_t nheavy = 0;
+  CK(cudaMemcpyAsync(&nheavy, d_count, 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  *nheavy_out = nheavy;
+  if (!nheavy) return 0;
+  std::vector<uint32_t> hr(2 * (size_t)nheavy), dof(nheavy);
+  CK(cudaMemcpyAsync(hr.data(), c->mheavy.p, hr.size() * 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  uint64_t total = 0;
+  for (uint32_t r = 0; r < nheavy; ++r) {
+    dof[r] = (uint32_t)total;
+    total += hr[2 * r + 1] - hr[2 * r];
+  }
+  c->mdst.grow((size_t)nheavy * 4);
+  CK(cudaMemcpyAsync(c->mdst.p, dof.data(), (size_t)nheavy * 4, cudaMemcpyHostToDevice, c->st));
+  return total;
+}
+
+void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                      int b, int D) {
+  const int kb = 2 * b;
   const uint32_t S = 1024, capb = 1024;
-  const uint32_t ngroups = (uint32_t)((m + S - 1) / S);
+  stage_begin(c, 1);
+  uint32_t* d_small = c->small.as<uint32_t>();
+  // every buffer the step needs is sized up front (n bounds m, u and the heavy parts)
+  c->keysA.grow(n * 8);
+  c->keysB.grow(n * 8);
+  c->colL_dst.grow(n * 4);
+  c->colL_cnt.grow(n * 4);
+  c->ckA.grow(n * 4);
+  c->cvA.grow(n * 4);
+  c->ckB.grow(n * 4);
+  c->cvB.grow(n * 4);
+
+  // ---- rows: MSD partition of the packed keys by source bits ----
+  PacketSrc ps{d_src, d_dst, d_valid, n, 0, b};
+  c->mark();  // 1: row partition start
+  uint64_t* keys = nullptr;
+  uint32_t* dummy = nullptr;
+  const uint64_t m = msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
+                                                               c->keysB.as<uint64_t>(), nullptr, &keys, &dummy);
+  c->last_sort_launches = D > 11 ? 2 : 1;
+  c->mark();  // 2: row partition end
+  if (!m) {
+    stage_finish(c, 1);
+    return;
+  }
+  const uint32_t nb = 1u << D;
+  uint32_t* off = c->moff.as<uint32_t>();
+  uint32_t ngroups = (uint32_t)((m + S - 1) / S);
   c->mgb.grow(((size_t)ngroups + 2) * 4);
   c->mheavy.grow(((size_t)ngroups + 2) * 8);
-  c->colL_dst.grow(m * 4);
-  c->colL_cnt.grow(m * 4);
   group_bounds_kernel<<<(unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8), 256, 0, c->st>>>(
       off, nb, S, ngroups, c->mgb.as<uint32_t>());
   CK_LAUNCH();
@@ -525,22 +606,11 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
       c->mheavy.as<uint32_t>(), d_small + kCounters + 31, d_small + kCounters + 30, c->stats.as<unsigned long long>());
   CK_LAUNCH();
   c->launches += 2;
-  c->mark();  // 3: local end
+  c->mark();  // 3: local rows end
   uint32_t nheavy = 0;
-  CK(cudaMemcpyAsync(&nheavy, d_small + kCounters + 31, 4, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
+  const uint64_t mh = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
   uint64_t uh = 0;
-  if (nheavy) {
-    std::vector<uint32_t> hr(2 * (size_t)nheavy), dof(nheavy);
-    CK(cudaMemcpyAsync(hr.data(), c->mheavy.p, hr.size() * 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    uint64_t mh = 0;
-    for (uint32_t r = 0; r < nheavy; ++r) {
-      dof[r] = (uint32_t)mh;
-      mh += hr[2 * r + 1] - hr[2 * r];
-    }
-    c->mdst.grow((size_t)nheavy * 4);
-    CK(cudaMemcpyAsync(c->mdst.p, dof.data(), (size_t)nheavy * 4, cudaMemcpyHostToDevice, c->st));
+  if (mh) {  // heavy row buckets: gather -> LSD sort -> fused link/row kernel
     c->keysC.grow(mh * 8);
     c->keysD.grow(mh * 8);
     gather_ranges_kernel<<<(unsigned)std::min<uint32_t>(nheavy, c->sms * 8), 256, 0, c->st>>>(
@@ -548,77 +618,60 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
         c->colL_cnt.as<uint32_t>());
     CK_LAUNCH();
     uint64_t* hs = sort_keys_u64(c, c->keysC.as<uint64_t>(), mh, kb, c->keysD.as<uint64_t>());
-    c->ckA.grow(mh * 4);
-    c->cvA.grow(mh * 4);
     if (c->lrstatus.grow(tiles_of(mh, kSegTile) * sizeof(LRStatus)))
       CK(cudaMemsetAsync(c->lrstatus.p, 0, c->lrstatus.cap, c->st));
-    launch_link_row<uint32_t>(c, hs, (uint32_t)mh, b, 0, d_small);
+    launch_link_row<uint32_t>(c, hs, (uint32_t)mh, b, 0, d_small);  // entries -> ckA / cvA
     CK(cudaMemcpyAsync(c->h_small + kU, d_small + kU, 4, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     uh = c->h_small[kU];
   }
-  c->mark();  // 4: heavy end
-  // columns: light slots (with holes) + heavy entries -> onesweep -> col_kernel
-  const int ncolpass = (b + 7) / 8;
-  CK(cudaMemsetAsync(d_small + kCHist, 0, sizeof(uint32_t) * 8 * kRadix, c->st));
-  CK(cudaMemsetAsync(gcount, 0, 8, c->st));
+  c->mark();  // 4: heavy rows end
+
+  // ---- columns: MSD partition of the (dst, count) entries by destination bits ----
   ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), m,
                   c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh, m + uh};
-  {
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m + uh + 1023) / 1024, (uint64_t)c->sms * 8));
-    switch (ncolpass) {
-      case 1: hist_concat_kernel<1><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
-      case 2: hist_concat_kernel<2><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
-      case 3: hist_concat_kernel<3><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
-      default: hist_concat_kernel<4><<<grid, 256, 0, c->st>>>(cs, d_small + kCHist, gcount); break;
-    }
-    CK_LAUNCH();
-    bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kCHist, ncolpass, d_small + kCBase);
-    CK_LAUNCH();
-    c->launches += 2;
-  }
-  CK(cudaMemcpyAsync(c->h_small, d_small, kSmallWords * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  const uint64_t u = *reinterpret_cast<unsigned long long*>(c->h_small + kGCount);
-  c->ckA.grow(std::max<uint64_t>(u, uh) * 4);
-  c->cvA.grow(std::max<uint64_t>(u, uh) * 4);
-  c->ckB.grow(u * 4);
-  c->cvB.grow(u * 4);
-  c->grow_status(tiles_of(m + uh, kMinPassTile) * kRadix);
-  std::vector<int> active;
-  for (int p = 0; p < ncolpass; ++p) {
-    const uint32_t* hp = c->h_small + kCHist + p * kRadix;
-    bool trivial = false;
-    for (int d = 0; d < kRadix; ++d)
-      if (hp[d] == u) trivial = true;
-    if (!trivial) active.push_back(p);
-  }
-  if (active.empty()) active.push_back(0);
+  const int Dc = std::min(D, b);
   uint32_t* ck = nullptr;
   uint32_t* cv = nullptr;
-  for (size_t i = 0; i < active.size(); ++i) {
-    const int p = active[i];
-    uint32_t* ok = (i & 1) ? c->ckA.as<uint32_t>() : c->ckB.as<uint32_t>();
-    uint32_t* ov = (i & 1) ? c->cvA.as<uint32_t>() : c->cvB.as<uint32_t>();
-    if (i == 0) {
-      launch_pass<ColConcatSrc, uint32_t, true>(c, cs, m + uh, ok, ov, 8 * p, d_small + kCBase + p * kRadix,
-                                                d_small + kCounters + 16 + i);
-    } else {
-      KeySrc<uint32_t, true> ks{ck, cv, u};
-      launch_pass<KeySrc<uint32_t, true>, uint32_t, true>(c, ks, u, ok, ov, 8 * p, d_small + kCBase + p * kRadix,
-                                                          d_small + kCounters + 16 + i);
-    }
-    ck = ok;
-    cv = ov;
-  }
-  c->mark();  // 5: column sort end
-  if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
-    CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
-  col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
-      ck, cv, (uint32_t)u, b, 0, c->csstatus.as<CSStatus>(), c->next_epoch(), d_small + kCounters + 26,
-      c->stats.as<unsigned long long>());
+  const uint64_t u = msd_partition<ColConcatSrc, uint32_t, true>(c, cs, m + uh, b, Dc, c->ckB.as<uint32_t>(),
+                                                                 c->cvB.as<uint32_t>(), c->ckA.as<uint32_t>(),
+                                                                 c->cvA.as<uint32_t>(), &ck, &cv);
+  c->mark();  // 5: column partition end
+  const uint32_t nbc = 1u << Dc;
+  ngroups = (uint32_t)((u + S - 1) / S);
+  c->mgb.grow(((size_t)ngroups + 2) * 4);
+  c->mheavy.grow(((size_t)ngroups + 2) * 8);
+  group_bounds_kernel<<<(unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8), 256, 0, c->st>>>(
+      off, nbc, S, ngroups, c->mgb.as<uint32_t>());
   CK_LAUNCH();
-  ++c->launches;
+  CK(cudaMemsetAsync(d_small + kCounters + 30, 0, 8, c->st));
+  set_smem(local_cols_kernel, sizeof(LocColSmem));
+  local_cols_kernel<<<(unsigned)(c->sms * 4), kLocThreads, sizeof(LocColSmem), c->st>>>(
+      ck, cv, off, c->mgb.as<uint32_t>(), ngroups, capb, c->mheavy.as<uint32_t>(), d_small + kCounters + 31,
+      d_small + kCounters + 30, c->stats.as<unsigned long long>());
+  CK_LAUNCH();
+  c->launches += 2;
+  c->mark();  // 6: local columns end
+  const uint64_t ch = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
+  if (ch) {  // heavy destination buckets: gather -> LSD sort -> column kernel
+    c->cgk.grow(ch * 4);
+    c->cgv.grow(ch * 4);
+    c->cgk2.grow(ch * 4);
+    c->cgv2.grow(ch * 4);
+    gather_pairs_kernel<<<(unsigned)std::min<uint32_t>(nheavy, c->sms * 8), 256, 0, c->st>>>(
+        ck, cv, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, c->cgk.as<uint32_t>(),
+        c->cgv.as<uint32_t>());
+    CK_LAUNCH();
+    auto sorted = sort_u32_pairs(c, c->cgk.as<uint32_t>(), c->cgv.as<uint32_t>(), ch, b, c->cgk2.as<uint32_t>(),
+                                 c->cgv2.as<uint32_t>());
+    if (c->csstatus.grow(tiles_of(ch, kSegTile) * sizeof(CSStatus)))
+      CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+    col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(ch, kSegTile), 256, 0, c->st>>>(
+        sorted.first, sorted.second, (uint32_t)ch, b, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
+        d_small + kCounters + 26, c->stats.as<unsigned long long>());
+    CK_LAUNCH();
+    ++c->launches;
+  }
   stage_finish(c, 1);
 }
 
@@ -801,7 +854,7 @@ void nmx_destroy(nmx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (DevBuf* b : {&c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
+  for (DevBuf* b : {&c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
                     &c->mhist2, &c->mgb, &c->mheavy, &c->mdst, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})

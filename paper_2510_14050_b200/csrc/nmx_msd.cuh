@@ -57,11 +57,14 @@ __device__ __forceinline__ void smem_excl_scan(uint32_t* cnt, uint32_t* out, uin
   __syncthreads();
 }
 
-// Level 1 (Src = PacketSrc, cursor indexed by the D1-bit digit) and level 2
-// (Src = KeySrc<u64>, cursor indexed by the D-bit bucket id; a tile lies in one
-// or two level-1 buckets, keys of further buckets take a per-key global atomic).
+// Level 1 (cursor indexed by the D1-bit digit) and level 2 (cursor indexed by
+// the D-bit bucket id; a tile lies in one or two level-1 buckets, keys of further
+// buckets take a per-key global atomic). KeyT u64 = packed row keys; KeyT u32
+// with a u32 payload = column entries (dst, count).
+template <typename KeyT, bool HAS_VAL>
 struct MsdSmem {
-  uint64_t stage[kMsdTile];
+  KeyT stage[kMsdTile];
+  uint32_t vstage[HAS_VAL ? kMsdTile : 1];
   uint32_t cnt[kMsdMaxBins];
   uint32_t tstart[kMsdMaxBins];
   uint32_t gbase[kMsdMaxBins];
@@ -69,112 +72,112 @@ struct MsdSmem {
   uint64_t b1first;
 };
 
-template <typename Src, int LEVEL>
-__global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint64_t n_items,
-                                                                   uint64_t* __restrict__ out, int shift, int dbits,
+template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL>
+__global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
+                                                                   uint32_t* __restrict__ vout, int shift, int dbits,
                                                                    int bshift, uint32_t* __restrict__ cursor) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  MsdSmem& S = *reinterpret_cast<MsdSmem*>(smem_raw);
-  uint32_t* cnt = S.cnt;
-  uint32_t* tstart = S.tstart;
-  uint32_t* gbase = S.gbase;
-  uint32_t* wt = S.wt;
-  uint64_t* stage = S.stage;
-  uint64_t& s_b1first = S.b1first;
+  auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbins = LEVEL == 1 ? (1 << dbits) : (2 << dbits);
-  for (int i = tid; i < kMsdMaxBins; i += kMsdThreads) cnt[i] = 0;
+  for (int i = tid; i < kMsdMaxBins; i += kMsdThreads) S.cnt[i] = 0;
   const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
   if (LEVEL == 2 && tid == 0) {
-    uint64_t k0 = 0;
+    KeyT k0 = 0;
     uint32_t v;
     src.load(base, k0, v);
-    s_b1first = k0 >> bshift;
+    S.b1first = (uint64_t)k0 >> bshift;
   }
+  // issue every load of the tile before using any (memory-level parallelism)
+  KeyT k[kMsdIPT];
+  uint32_t v[kMsdIPT];
+  bool ok[kMsdIPT];
+#pragma unroll
+  for (int i = 0; i < kMsdIPT; ++i)
+    ok[i] = src.load(base + (uint64_t)warp * 32 * kMsdIPT + (uint64_t)i * 32 + lane, k[i], v[i]);
   __syncthreads();
+  const uint64_t b1first = S.b1first;
   const uint32_t dmask = (1u << dbits) - 1;
-  uint64_t k[kMsdIPT];
   uint32_t rank[kMsdIPT];
   int bin[kMsdIPT];
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i) {
-    uint32_t v;
-    const uint64_t idx = base + (uint64_t)warp * 32 * kMsdIPT + (uint64_t)i * 32 + lane;
     bin[i] = -1;
-    if (src.load(idx, k[i], v)) {
-      const uint32_t d = (uint32_t)(k[i] >> shift) & dmask;
+    if (ok[i]) {
+      const uint32_t d = (uint32_t)((uint64_t)k[i] >> shift) & dmask;
       if (LEVEL == 1) {
         bin[i] = (int)d;
       } else {
-        const uint64_t rel = (k[i] >> bshift) - s_b1first;
+        const uint64_t rel = ((uint64_t)k[i] >> bshift) - b1first;
         if (rel < 2) {
           bin[i] = (int)((rel << dbits) | d);
         } else {  // third+ level-1 bucket inside one tile: direct placement
-          const uint32_t g = (uint32_t)(k[i] >> shift);
-          out[atomicAdd(cursor + g, 1u)] = k[i];
+          const uint32_t pos = atomicAdd(cursor + (uint32_t)((uint64_t)k[i] >> shift), 1u);
+          out[pos] = k[i];
+          if (HAS_VAL) vout[pos] = v[i];
         }
       }
     }
   }
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i)
-    if (bin[i] >= 0) rank[i] = atomicAdd(&cnt[bin[i]], 1u);
+    if (bin[i] >= 0) rank[i] = atomicAdd(&S.cnt[bin[i]], 1u);
   __syncthreads();
   if (LEVEL == 1 && (1 << dbits) <= kMsdThreads)
-    smem_excl_scan<kMsdThreads>(cnt, tstart, wt);
+    smem_excl_scan<kMsdThreads>(S.cnt, S.tstart, S.wt);
   else
-    smem_excl_scan<kMsdMaxBins>(cnt, tstart, wt);
-  // reserve each non-empty digit's range in the output
-  for (int i = tid; i < nbins; i += kMsdThreads) {
-    const uint32_t c = cnt[i];
+    smem_excl_scan<kMsdMaxBins>(S.cnt, S.tstart, S.wt);
+  for (int i = tid; i < nbins; i += kMsdThreads) {  // reserve each digit's output range
+    const uint32_t c = S.cnt[i];
     if (c) {
-      uint32_t g;
-      if (LEVEL == 1)
-        g = (uint32_t)i;
-      else
-        g = (uint32_t)(((s_b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask));
-      gbase[i] = atomicAdd(cursor + g, c) - tstart[i];
+      const uint32_t g = LEVEL == 1 ? (uint32_t)i
+                                    : (uint32_t)(((b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask));
+      S.gbase[i] = atomicAdd(cursor + g, c) - S.tstart[i];
     }
   }
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i)
-    if (bin[i] >= 0) stage[tstart[bin[i]] + rank[i]] = k[i];
+    if (bin[i] >= 0) {
+      const uint32_t at = S.tstart[bin[i]] + rank[i];
+      S.stage[at] = k[i];
+      if (HAS_VAL) S.vstage[at] = v[i];
+    }
   __syncthreads();
-  uint32_t total = 0;
-  if (nbins > 0) total = tstart[nbins - 1] + cnt[nbins - 1];
+  const uint32_t total = S.tstart[nbins - 1] + S.cnt[nbins - 1];
   for (uint32_t j = tid; j < total; j += kMsdThreads) {
-    const uint64_t key = stage[j];
+    const KeyT key = S.stage[j];
     int b;
     if (LEVEL == 1)
-      b = (int)((uint32_t)(key >> shift) & dmask);
+      b = (int)((uint32_t)((uint64_t)key >> shift) & dmask);
     else
-      b = (int)((((key >> bshift) - s_b1first) << dbits) | ((key >> shift) & dmask));
-    out[gbase[b] + j] = key;
+      b = (int)(((((uint64_t)key >> bshift) - b1first) << dbits) | (((uint64_t)key >> shift) & dmask));
+    const uint32_t pos = S.gbase[b] + j;
+    out[pos] = key;
+    if (HAS_VAL) vout[pos] = S.vstage[j];
   }
 }
 
-// level-1 histogram: top D1 bits of the packed key (+ valid count)
-__global__ void __launch_bounds__(256) msd_hist1_kernel(PacketSrc src, int shift, uint32_t* __restrict__ hist1,
+// level-1 histogram: top D1 bits of the key (+ valid count)
+template <typename Src, typename KeyT>
+__global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int shift, uint32_t* __restrict__ hist1,
                                                        unsigned long long* __restrict__ gcount) {
   __shared__ uint32_t h[kMsdMaxBins];
   for (int i = threadIdx.x; i < kMsdMaxBins; i += 256) h[i] = 0;
   __syncthreads();
   uint32_t c = 0;
-  constexpr int U = 4;
+  constexpr int U = 8;
   const uint64_t stride = (uint64_t)gridDim.x * 256 * U;
-  for (uint64_t base = (uint64_t)blockIdx.x * 256 * U; base < src.n; base += stride) {
-    uint64_t k[U];
+  for (uint64_t base = (uint64_t)blockIdx.x * 256 * U; base < n; base += stride) {
+    KeyT k[U];
+    uint32_t v[U];
     bool ok[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      uint32_t v;
-      ok[u] = src.load(base + (uint64_t)u * 256 + threadIdx.x, k[u], v);
-    }
+    for (int u = 0; u < U; ++u) ok[u] = src.load(base + (uint64_t)u * 256 + threadIdx.x, k[u], v[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (ok[u]) {
         ++c;
-        atomicAdd(&h[(uint32_t)(k[u] >> shift)], 1u);
+        atomicAdd(&h[(uint32_t)((uint64_t)k[u] >> shift)], 1u);
       }
   }
 #pragma unroll
@@ -186,22 +189,30 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(PacketSrc src, int shift
 }
 
 // level-2 digit counts per level-1 bucket over the level-1 output
-__global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const uint64_t* __restrict__ keys, uint64_t m,
-                                                                  int shift, int dbits, int bshift,
-                                                                  uint32_t* __restrict__ hist2) {
+template <typename KeyT>
+__global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __restrict__ keys, uint64_t m, int shift,
+                                                                  int dbits, int bshift, uint32_t* __restrict__ hist2) {
   __shared__ uint32_t cnt[kMsdMaxBins];
   __shared__ uint64_t s_b1first;
   const int tid = threadIdx.x;
   for (int i = tid; i < kMsdMaxBins; i += kMsdThreads) cnt[i] = 0;
   const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
-  if (tid == 0) s_b1first = keys[base] >> bshift;
+  KeyT k[kMsdIPT];
+#pragma unroll
+  for (int i = 0; i < kMsdIPT; ++i) {
+    const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
+    k[i] = idx < m ? keys[idx] : KeyT(0);
+  }
+  if (tid == 0) s_b1first = (uint64_t)keys[base] >> bshift;
   __syncthreads();
   const uint32_t dmask = (1u << dbits) - 1;
+  const uint64_t b1first = s_b1first;
+#pragma unroll
   for (int i = 0; i < kMsdIPT; ++i) {
     const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
     if (idx < m) {
-      const uint64_t key = keys[idx];
-      const uint64_t rel = (key >> bshift) - s_b1first;
+      const uint64_t key = (uint64_t)k[i];
+      const uint64_t rel = (key >> bshift) - b1first;
       if (rel < 2)
         atomicAdd(&cnt[(rel << dbits) | ((key >> shift) & dmask)], 1u);
       else
@@ -212,10 +223,7 @@ __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const uint64_t*
   const int nbins = 2 << dbits;
   for (int i = tid; i < nbins; i += kMsdThreads) {
     const uint32_t c = cnt[i];
-    if (c) {
-      const uint64_t g = ((s_b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask);
-      atomicAdd(hist2 + g, c);
-    }
+    if (c) atomicAdd(hist2 + (((b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask)), c);
   }
 }
 
@@ -549,6 +557,147 @@ __global__ void __launch_bounds__(256) hist_concat_kernel(ColConcatSrc src, uint
   for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) {
     const uint32_t v = (&h[0][0])[i];
     if (v) atomicAdd(ghist + i, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LOC (columns): per group of destination buckets, shared-memory hash of dst ->
+// (fan-in, packets); heavy buckets go to the LSD column path
+// ---------------------------------------------------------------------------
+constexpr int kLocCT = 3072;
+struct LocColSmem {
+  uint32_t key[kLocCT];  // dst + 1 (0 = empty)
+  uint32_t nnz[kLocCT];
+  uint32_t sum[kLocCT];
+  uint32_t heavy_lo[kLocMaxHeavy], heavy_hi[kLocMaxHeavy];
+  uint32_t nheavy;
+  uint32_t sp_nnz, sp_sum;  // dst == 0xFFFFFFFF
+  uint32_t group, blo, bhi, klo, khi;
+};
+
+__global__ void __launch_bounds__(kLocThreads, 4)
+    local_cols_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
+                      const uint32_t* __restrict__ off, const uint32_t* __restrict__ gb, uint32_t ngroups,
+                      uint32_t capb, uint32_t* __restrict__ heavy, uint32_t* __restrict__ nheavy_out,
+                      uint32_t* __restrict__ group_counter, unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kLocCT; i += kLocThreads) {
+    s.key[i] = 0;
+    s.nnz[i] = 0;
+    s.sum[i] = 0;
+  }
+  if (tid == 0) s.sp_nnz = s.sp_sum = 0;
+  unsigned long long a_cnt = 0, a_fanin = 0, a_pk = 0;
+  for (;;) {
+    if (tid == 0) {
+      const uint32_t g = atomicAdd(group_counter, 1u);
+      s.group = g;
+      if (g < ngroups) {
+        s.blo = gb[g];
+        s.bhi = gb[g + 1];
+        s.klo = off[s.blo];
+        s.khi = off[s.bhi];
+      }
+      s.nheavy = 0;
+    }
+    __syncthreads();
+    if (s.group >= ngroups) break;
+    const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
+    for (uint32_t j = blo + tid; j < bhi; j += kLocThreads) {
+      const uint32_t lo = off[j], hi = off[j + 1];
+      if (hi - lo > capb) {
+        const uint32_t q = atomicAdd(&s.nheavy, 1u);
+        if (q < kLocMaxHeavy) {
+          s.heavy_lo[q] = lo;
+          s.heavy_hi[q] = hi;
+        }
+        const uint32_t gq = atomicAdd(nheavy_out, 1u);
+        heavy[2 * gq] = lo;
+        heavy[2 * gq + 1] = hi;
+      }
+    }
+    __syncthreads();
+    uint32_t seg_lo[2], seg_hi[2], nseg;
+    if (s.nheavy == 0) {
+      seg_lo[0] = klo;
+      seg_hi[0] = khi;
+      nseg = 1;
+    } else {
+      seg_lo[0] = klo;
+      seg_hi[0] = s.heavy_lo[0];
+      seg_lo[1] = s.heavy_hi[0];
+      seg_hi[1] = khi;
+      nseg = 2;
+    }
+    for (uint32_t sg = 0; sg < nseg; ++sg) {
+      for (uint32_t i = seg_lo[sg] + tid; i < seg_hi[sg]; i += kLocThreads) {
+        const uint32_t d = ck[i], c = cv[i];
+        if (d == 0xFFFFFFFFu) {
+          atomicAdd(&s.sp_nnz, 1u);
+          atomicAdd(&s.sp_sum, c);
+          continue;
+        }
+        const uint32_t dk = d + 1;
+        uint32_t h = hslot(dk, kLocCT);
+        for (;;) {
+          uint32_t cur = s.key[h];
+          if (cur == 0) {
+            cur = atomicCAS(&s.key[h], 0u, dk);
+            if (cur == 0) cur = dk;
+          }
+          if (cur == dk) {
+            atomicAdd(&s.nnz[h], 1u);
+            atomicAdd(&s.sum[h], c);
+            break;
+          }
+          h = h + 1 == kLocCT ? 0 : h + 1;
+        }
+      }
+    }
+    __syncthreads();
+    for (int j = tid; j < kLocCT; j += kLocThreads) {
+      if (s.key[j]) {
+        a_cnt += 1;
+        a_fanin = max(a_fanin, (unsigned long long)s.nnz[j]);
+        a_pk = max(a_pk, (unsigned long long)s.sum[j]);
+        s.key[j] = 0;
+        s.nnz[j] = 0;
+        s.sum[j] = 0;
+      }
+    }
+    if (tid == 0 && s.sp_nnz) {
+      a_cnt += 1;
+      a_fanin = max(a_fanin, (unsigned long long)s.sp_nnz);
+      a_pk = max(a_pk, (unsigned long long)s.sp_sum);
+    }
+    __syncthreads();
+    if (tid == 0) s.sp_nnz = s.sp_sum = 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a_cnt += __shfl_xor_sync(FULL, a_cnt, o);
+    a_fanin = max(a_fanin, __shfl_xor_sync(FULL, a_fanin, o));
+    a_pk = max(a_pk, __shfl_xor_sync(FULL, a_pk, o));
+  }
+  if (lane == 0) {
+    if (a_cnt) atomicAdd(stats + S_DSTS, a_cnt);
+    if (a_fanin) atomicMax(stats + S_MAXFANIN, a_fanin);
+    if (a_pk) atomicMax(stats + S_MAXDSTPK, a_pk);
+  }
+}
+
+// gather heavy (dst, count) ranges into contiguous arrays
+__global__ void gather_pairs_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
+                                    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ dstoff,
+                                    uint32_t nranges, uint32_t* __restrict__ ok, uint32_t* __restrict__ ov) {
+  for (uint32_t r = blockIdx.x; r < nranges; r += gridDim.x) {
+    const uint32_t lo = ranges[2 * r], hi = ranges[2 * r + 1], o = dstoff[r];
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      ok[o + (i - lo)] = ck[i];
+      ov[o + (i - lo)] = cv[i];
+    }
   }
 }
 
