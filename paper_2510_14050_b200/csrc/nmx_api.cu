@@ -122,6 +122,7 @@ struct nmx_ctx {
   // materialised outputs (drop-in TrafficMatrix / FlatContainers)
   uint64_t coo_nnz = 0, flat_nnz = 0, flat_r = 0, flat_c = 0;
   int coo_b = 0;
+  int msd_levels = 0;
 
   uint32_t next_epoch() {
     if (++epoch >= (1u << 22)) {
@@ -492,21 +493,29 @@ std::pair<uint32_t*, uint32_t*> sort_u32_pairs(nmx_ctx* c, uint32_t* k, uint32_t
 template <typename Src, typename KeyT, bool HAS_VAL>
 uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, KeyT* outA, uint32_t* voutA,
                        KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v) {
-  const int D1 = std::min(11, D), D2 = D - D1;
+  // levels of <= kMsdLevelBits bits: 128 bins per tile keeps the reservation
+  // atomics at one per 32 keys and every digit's run in a tile ~32 keys long
+  const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
+  int dl[8], cum[8];
+  for (int l = 0, acc = 0; l < L; ++l) {
+    dl[l] = D / L + (l < D % L ? 1 : 0);
+    acc += dl[l];
+    cum[l] = acc;
+  }
   const uint32_t nb = 1u << D;
   uint32_t* d_small = c->small.as<uint32_t>();
   auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
   CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
   CK(cudaMemsetAsync(gcount, 0, 8, c->st));
   const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
-  msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - D1, d_small + kHist, gcount);
+  msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - dl[0], d_small + kHist, gcount);
   CK_LAUNCH();
   c->mcur.grow(((size_t)nb + 8) * 4);
   c->moff.grow(((size_t)nb + 8) * 4);
   c->mhist2.grow(((size_t)nb + 8) * 4);
   uint32_t* cur = c->mcur.as<uint32_t>();
   uint32_t* off = c->moff.as<uint32_t>();
-  big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(d_small + kHist, 1u << D1, off, cur);
+  big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(d_small + kHist, 1u << dl[0], off, cur);
   CK_LAUNCH();
   unsigned long long m = 0;
   CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
@@ -518,27 +527,36 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   using S1 = MsdSmem<KeyT, HAS_VAL>;
   set_smem(msd_scatter_kernel<Src, KeyT, HAS_VAL, 1>, sizeof(S1));
   msd_scatter_kernel<Src, KeyT, HAS_VAL, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
-      src, n, outA, voutA, kb - D1, D1, 0, cur);
+      src, n, outA, voutA, kb - dl[0], dl[0], 0, cur);
   CK_LAUNCH();
   ++c->launches;
-  if (D2 > 0) {
+  KeyT* in_k = outA;
+  uint32_t* in_v = voutA;
+  KeyT* out_k = outB;
+  uint32_t* out_v = voutB;
+  for (int l = 1; l < L; ++l) {
+    const int shift = kb - cum[l], bshift = kb - cum[l - 1];
+    const uint32_t nbl = 1u << cum[l];
     uint32_t* h2 = c->mhist2.as<uint32_t>();
-    CK(cudaMemsetAsync(h2, 0, (size_t)nb * 4, c->st));
-    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(outA, m, kb - D, D2, kb - D1,
+    CK(cudaMemsetAsync(h2, 0, (size_t)nbl * 4, c->st));
+    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(in_k, m, shift, dl[l], bshift,
                                                                                          h2);
     CK_LAUNCH();
-    big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(h2, nb, off, cur);
+    big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(h2, nbl, off, cur);
     CK_LAUNCH();
-    KeySrc<KeyT, HAS_VAL> ks{outA, voutA, m};
+    KeySrc<KeyT, HAS_VAL> ks{in_k, in_v, m};
     set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>, sizeof(S1));
     msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>
-        <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(ks, m, outB, voutB, kb - D, D2,
-                                                                               kb - D1, cur);
+        <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(ks, m, out_k, out_v, shift, dl[l],
+                                                                               bshift, cur);
     CK_LAUNCH();
     c->launches += 3;
-    *res_k = outB;
-    *res_v = voutB;
+    std::swap(in_k, out_k);
+    std::swap(in_v, out_v);
   }
+  *res_k = in_k;
+  *res_v = in_v;
+  c->msd_levels = L;
   return m;
 }
 
@@ -585,7 +603,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   uint32_t* dummy = nullptr;
   const uint64_t m = msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
                                                                c->keysB.as<uint64_t>(), nullptr, &keys, &dummy);
-  c->last_sort_launches = D > 11 ? 2 : 1;
+  c->last_sort_launches = c->msd_levels;
   c->mark();  // 2: row partition end
   if (!m) {
     stage_finish(c, 1);

@@ -23,7 +23,8 @@ namespace nmx {
 constexpr int kMsdThreads = 512;
 constexpr int kMsdIPT = 8;
 constexpr int kMsdTile = kMsdThreads * kMsdIPT;  // 4096 keys
-constexpr int kMsdMaxBins = 2048;                // 2 x 2^10 (level 2 spans <= 2 level-1 buckets per bin set)
+constexpr int kMsdMaxBins = 2048;                // histogram bins of the first level (<= 2^11)
+constexpr int kMsdLevelBits = 7;                 // digit bits per partition level
 
 // block exclusive scan of NB counters held in smem (512 threads, NB % 512 == 0 or NB <= 512)
 template <int NB>
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
   for (int i = 0; i < kMsdIPT; ++i)
     if (bin[i] >= 0) rank[i] = atomicAdd(&S.cnt[bin[i]], 1u);
   __syncthreads();
-  if (LEVEL == 1 && (1 << dbits) <= kMsdThreads)
+  if (nbins <= kMsdThreads)
     smem_excl_scan<kMsdThreads>(S.cnt, S.tstart, S.wt);
   else
     smem_excl_scan<kMsdMaxBins>(S.cnt, S.tstart, S.wt);
@@ -285,18 +286,65 @@ struct LocSmem {
   unsigned long long t1key[kLocT1];  // key + 1 (0 = empty)
   uint32_t t1cnt[kLocT1];
   uint32_t t2key[kLocT2];  // src + 1 (0 = empty)
-  uint32_t t2pk[kLocT2];
-  uint32_t t2fo[kLocT2];
+  uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
+  uint16_t list1[kLocMaxKeys];  // occupied link slots, in insertion order
+  uint16_t list2[kLocMaxKeys];  // occupied source slots
+  uint32_t nl, ns;
   uint32_t heavy_lo[kLocMaxHeavy], heavy_hi[kLocMaxHeavy];
   uint32_t nheavy;
   uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
-  uint32_t wt[kLocThreads / 32 + 1];
-  uint32_t group, blo, bhi, klo, khi;
+  uint32_t blo, bhi, klo, khi;             // current group
+  uint32_t nblo, nbhi, nklo, nkhi;         // prefetched next group
 };
 
 __device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
   const uint64_t h = x * 0x9E3779B97F4A7C15ull;
   return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
+}
+
+// group g: buckets [gb[g], gb[g+1]) = keys [off[gb[g]], off[gb[g+1]])
+__device__ __forceinline__ void group_fetch(const uint32_t* gb, const uint32_t* off, uint32_t g, uint32_t ngroups,
+                                            uint32_t& blo, uint32_t& bhi, uint32_t& klo, uint32_t& khi) {
+  if (g < ngroups) {
+    blo = gb[g];
+    bhi = gb[g + 1];
+    klo = off[blo];
+    khi = off[bhi];
+  }
+}
+
+// Heavy buckets of the current group: recorded for the LSD fallback (globally)
+// and as excluded ranges (in smem). Returns the light segments of [klo, khi).
+__device__ __forceinline__ uint32_t group_segments(const uint32_t* off, uint32_t blo, uint32_t bhi, uint32_t klo,
+                                                   uint32_t khi, uint32_t capb, uint32_t* heavy, uint32_t* nheavy_out,
+                                                   uint32_t* s_nheavy, uint32_t* s_hlo, uint32_t* s_hhi,
+                                                   uint32_t* seg_lo, uint32_t* seg_hi) {
+  for (uint32_t j = blo + threadIdx.x; j < bhi; j += blockDim.x) {
+    const uint32_t lo = off[j], hi = off[j + 1];
+    if (hi - lo > capb) {
+      const uint32_t q = atomicAdd(s_nheavy, 1u);
+      if (q < kLocMaxHeavy) {
+        s_hlo[q] = lo;
+        s_hhi[q] = hi;
+      }
+      const uint32_t gq = atomicAdd(nheavy_out, 1u);
+      heavy[2 * gq] = lo;
+      heavy[2 * gq + 1] = hi;
+    }
+  }
+  __syncthreads();
+  // a heavy bucket has > capb >= S keys and buckets start inside an S-key chunk,
+  // so a group holds at most one heavy bucket
+  if (*s_nheavy == 0) {
+    seg_lo[0] = klo;
+    seg_hi[0] = khi;
+    return 1;
+  }
+  seg_lo[0] = klo;
+  seg_hi[0] = s_hlo[0];
+  seg_lo[1] = s_hhi[0];
+  seg_hi[1] = khi;
+  return 2;
 }
 
 __global__ void __launch_bounds__(kLocThreads, 3)
@@ -307,67 +355,37 @@ __global__ void __launch_bounds__(kLocThreads, 3)
                       unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kLocT1; i += kLocThreads) {
     s.t1key[i] = 0;
     s.t1cnt[i] = 0;
   }
   for (int i = tid; i < kLocT2; i += kLocThreads) {
     s.t2key[i] = 0;
-    s.t2pk[i] = 0;
-    s.t2fo[i] = 0;
+    s.t2pf[i] = 0;
   }
-  if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+  if (tid == 0) {
+    s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+    s.nl = s.ns = 0;
+    group_fetch(gb, off, blockIdx.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
+  }
+  (void)group_counter;
   const uint64_t dmask = (1ull << b) - 1;
   unsigned long long a_valid = 0, a_links = 0, a_srcs = 0, a_mlink = 0, a_msrc = 0, a_mfan = 0;
-  for (;;) {
+  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     if (tid == 0) {
-      const uint32_t g = atomicAdd(group_counter, 1u);
-      s.group = g;
-      if (g < ngroups) {
-        s.blo = gb[g];
-        s.bhi = gb[g + 1];
-        s.klo = off[s.blo];
-        s.khi = off[s.bhi];
-      }
+      s.blo = s.nblo;
+      s.bhi = s.nbhi;
+      s.klo = s.nklo;
+      s.khi = s.nkhi;
       s.nheavy = 0;
     }
     __syncthreads();
-    if (s.group >= ngroups) break;
     const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
-    // heavy buckets of this group: excluded here, finished by the LSD path
-    for (uint32_t j = blo + tid; j < bhi; j += kLocThreads) {
-      const uint32_t lo = off[j], hi = off[j + 1];
-      if (hi - lo > capb) {
-        const uint32_t q = atomicAdd(&s.nheavy, 1u);
-        if (q < kLocMaxHeavy) {
-          s.heavy_lo[q] = lo;
-          s.heavy_hi[q] = hi;
-        }
-        const uint32_t gq = atomicAdd(nheavy_out, 1u);
-        heavy[2 * gq] = lo;
-        heavy[2 * gq + 1] = hi;
-      }
-    }
-    __syncthreads();
-    const uint32_t nh = min(s.nheavy, (uint32_t)kLocMaxHeavy);
-    // light segments of [klo, khi): heavy ranges removed (their column slots are
-    // zeroed by gather_ranges_kernel). Buckets start inside a chunk of S keys and a
-    // heavy bucket has > capb >= S keys, so nh <= 1 and there are <= 2 segments.
+    if (tid == 0) group_fetch(gb, off, g + gridDim.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);  // prefetch
     uint32_t seg_lo[2], seg_hi[2];
-    uint32_t nseg = 0;
-    if (nh == 0) {
-      seg_lo[0] = klo;
-      seg_hi[0] = khi;
-      nseg = 1;
-    } else {
-      seg_lo[0] = klo;
-      seg_hi[0] = s.heavy_lo[0];
-      seg_lo[1] = s.heavy_hi[0];
-      seg_hi[1] = khi;
-      nseg = 2;
-    }
-    // insert every light key
+    const uint32_t nseg = group_segments(off, blo, bhi, klo, khi, capb, heavy, nheavy_out, &s.nheavy, s.heavy_lo,
+                                         s.heavy_hi, seg_lo, seg_hi);
     for (uint32_t sg = 0; sg < nseg; ++sg) {
       for (uint32_t i = seg_lo[sg] + tid; i < seg_hi[sg]; i += kLocThreads) {
         const uint64_t key = keys[i];
@@ -383,6 +401,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
               cur = atomicCAS(&s.t1key[h], 0ull, kk);
               if (cur == 0) {
                 atomicAdd(&s.t1cnt[h], 1u);
+                s.list1[atomicAdd(&s.nl, 1u)] = (uint16_t)h;
                 fresh = true;
                 break;
               }
@@ -406,11 +425,13 @@ __global__ void __launch_bounds__(kLocThreads, 3)
             uint32_t cur = s.t2key[h];
             if (cur == 0) {
               cur = atomicCAS(&s.t2key[h], 0u, sk);
-              if (cur == 0) cur = sk;
+              if (cur == 0) {
+                s.list2[atomicAdd(&s.ns, 1u)] = (uint16_t)h;
+                cur = sk;
+              }
             }
             if (cur == sk) {
-              atomicAdd(&s.t2pk[h], 1u);
-              if (fresh) atomicAdd(&s.t2fo[h], 1u);
+              atomicAdd(&s.t2pf[h], 1u | (fresh ? 0x10000u : 0u));
               break;
             }
             h = h + 1 == kLocT2 ? 0 : h + 1;
@@ -419,34 +440,27 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       }
     }
     __syncthreads();
-    // links: occupied slots -> compacted (dst, count) in the light slots of this group
-    uint32_t mine = 0;
-    for (int j = tid; j < kLocT1; j += kLocThreads) mine += s.t1key[j] != 0;
-    uint32_t total;
-    uint32_t at = block_excl_scan_n<kLocThreads>(mine, s.wt, &total);
+    const uint32_t nl = s.nl, ns = s.ns, sp = s.sp_link;
     const uint32_t len0 = seg_hi[0] - seg_lo[0];
     auto slot_of = [&](uint32_t j) -> uint32_t { return j < len0 ? seg_lo[0] + j : seg_lo[1] + (j - len0); };
-    const uint32_t sp = s.sp_link;
-    for (int j = tid; j < kLocT1; j += kLocThreads) {
-      const unsigned long long kk = s.t1key[j];
-      if (kk) {
-        const uint64_t key = kk - 1;
-        const uint32_t c = s.t1cnt[j];
-        const uint32_t pos = slot_of(at);
-        col_dst[pos] = (uint32_t)(key & dmask);
-        col_cnt[pos] = c;
-        ++at;
-        a_links += 1;
-        a_valid += c;
-        a_mlink = max(a_mlink, (unsigned long long)c);
-        s.t1key[j] = 0;
-        s.t1cnt[j] = 0;
-      }
+    // links -> compacted (dst, count) column entries in this group's light slots
+    for (uint32_t j = tid; j < nl; j += kLocThreads) {
+      const uint32_t h = s.list1[j];
+      const uint64_t key = s.t1key[h] - 1;
+      const uint32_t c = s.t1cnt[h];
+      const uint32_t pos = slot_of(j);
+      col_dst[pos] = (uint32_t)(key & dmask);
+      col_cnt[pos] = c;
+      a_links += 1;
+      a_valid += c;
+      a_mlink = max(a_mlink, (unsigned long long)c);
+      s.t1key[h] = 0;
+      s.t1cnt[h] = 0;
     }
-    uint32_t used = total;
+    uint32_t used = nl;
     if (sp) {
       if (tid == 0) {
-        const uint32_t pos = slot_of(total);
+        const uint32_t pos = slot_of(nl);
         col_dst[pos] = (uint32_t)dmask;
         col_cnt[pos] = sp;
         a_links += 1;
@@ -455,20 +469,17 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       }
       used += 1;
     }
-    // the remaining light slots become holes (count 0)
     uint32_t nlight = 0;
     for (uint32_t sg = 0; sg < nseg; ++sg) nlight += seg_hi[sg] - seg_lo[sg];
-    for (uint32_t j = used + tid; j < nlight; j += kLocThreads) col_cnt[slot_of(j)] = 0;
-    // sources
-    for (int j = tid; j < kLocT2; j += kLocThreads) {
-      if (s.t2key[j]) {
-        a_srcs += 1;
-        a_msrc = max(a_msrc, (unsigned long long)s.t2pk[j]);
-        a_mfan = max(a_mfan, (unsigned long long)s.t2fo[j]);
-        s.t2key[j] = 0;
-        s.t2pk[j] = 0;
-        s.t2fo[j] = 0;
-      }
+    for (uint32_t j = used + tid; j < nlight; j += kLocThreads) col_cnt[slot_of(j)] = 0;  // holes
+    for (uint32_t j = tid; j < ns; j += kLocThreads) {
+      const uint32_t h = s.list2[j];
+      const uint32_t pf = s.t2pf[h];
+      a_srcs += 1;
+      a_msrc = max(a_msrc, (unsigned long long)(pf & 0xFFFFu));
+      a_mfan = max(a_mfan, (unsigned long long)(pf >> 16));
+      s.t2key[h] = 0;
+      s.t2pf[h] = 0;
     }
     if (tid == 0 && s.sp_src_pk) {
       a_srcs += 1;
@@ -476,7 +487,10 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo);
     }
     __syncthreads();
-    if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+    if (tid == 0) {
+      s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+      s.nl = s.ns = 0;
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -495,7 +509,6 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     if (a_msrc) atomicMax(stats + S_MAXSRCPK, a_msrc);
     if (a_mfan) atomicMax(stats + S_MAXFANOUT, a_mfan);
   }
-  (void)warp;
 }
 
 // gather heavy bucket ranges into one contiguous array
@@ -566,13 +579,15 @@ __global__ void __launch_bounds__(256) hist_concat_kernel(ColConcatSrc src, uint
 // ---------------------------------------------------------------------------
 constexpr int kLocCT = 3072;
 struct LocColSmem {
-  uint32_t key[kLocCT];  // dst + 1 (0 = empty)
-  uint32_t nnz[kLocCT];
-  uint32_t sum[kLocCT];
+  uint32_t key[kLocCT];             // dst + 1 (0 = empty)
+  unsigned long long ns[kLocCT];    // fan-in << 32 | packets
+  uint16_t list[kLocMaxKeys];
+  uint32_t nl;
   uint32_t heavy_lo[kLocMaxHeavy], heavy_hi[kLocMaxHeavy];
   uint32_t nheavy;
-  uint32_t sp_nnz, sp_sum;  // dst == 0xFFFFFFFF
-  uint32_t group, blo, bhi, klo, khi;
+  unsigned long long sp;  // dst == 0xFFFFFFFF
+  uint32_t blo, bhi, klo, khi;
+  uint32_t nblo, nbhi, nklo, nkhi;
 };
 
 __global__ void __launch_bounds__(kLocThreads, 4)
@@ -585,58 +600,35 @@ __global__ void __launch_bounds__(kLocThreads, 4)
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kLocCT; i += kLocThreads) {
     s.key[i] = 0;
-    s.nnz[i] = 0;
-    s.sum[i] = 0;
+    s.ns[i] = 0;
   }
-  if (tid == 0) s.sp_nnz = s.sp_sum = 0;
+  if (tid == 0) {
+    s.sp = 0;
+    s.nl = 0;
+    group_fetch(gb, off, blockIdx.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
+  }
+  (void)group_counter;
   unsigned long long a_cnt = 0, a_fanin = 0, a_pk = 0;
-  for (;;) {
+  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
     if (tid == 0) {
-      const uint32_t g = atomicAdd(group_counter, 1u);
-      s.group = g;
-      if (g < ngroups) {
-        s.blo = gb[g];
-        s.bhi = gb[g + 1];
-        s.klo = off[s.blo];
-        s.khi = off[s.bhi];
-      }
+      s.blo = s.nblo;
+      s.bhi = s.nbhi;
+      s.klo = s.nklo;
+      s.khi = s.nkhi;
       s.nheavy = 0;
     }
     __syncthreads();
-    if (s.group >= ngroups) break;
     const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
-    for (uint32_t j = blo + tid; j < bhi; j += kLocThreads) {
-      const uint32_t lo = off[j], hi = off[j + 1];
-      if (hi - lo > capb) {
-        const uint32_t q = atomicAdd(&s.nheavy, 1u);
-        if (q < kLocMaxHeavy) {
-          s.heavy_lo[q] = lo;
-          s.heavy_hi[q] = hi;
-        }
-        const uint32_t gq = atomicAdd(nheavy_out, 1u);
-        heavy[2 * gq] = lo;
-        heavy[2 * gq + 1] = hi;
-      }
-    }
-    __syncthreads();
-    uint32_t seg_lo[2], seg_hi[2], nseg;
-    if (s.nheavy == 0) {
-      seg_lo[0] = klo;
-      seg_hi[0] = khi;
-      nseg = 1;
-    } else {
-      seg_lo[0] = klo;
-      seg_hi[0] = s.heavy_lo[0];
-      seg_lo[1] = s.heavy_hi[0];
-      seg_hi[1] = khi;
-      nseg = 2;
-    }
+    if (tid == 0) group_fetch(gb, off, g + gridDim.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
+    uint32_t seg_lo[2], seg_hi[2];
+    const uint32_t nseg = group_segments(off, blo, bhi, klo, khi, capb, heavy, nheavy_out, &s.nheavy, s.heavy_lo,
+                                         s.heavy_hi, seg_lo, seg_hi);
     for (uint32_t sg = 0; sg < nseg; ++sg) {
       for (uint32_t i = seg_lo[sg] + tid; i < seg_hi[sg]; i += kLocThreads) {
-        const uint32_t d = ck[i], c = cv[i];
+        const uint32_t d = ck[i];
+        const unsigned long long add = (1ull << 32) | cv[i];
         if (d == 0xFFFFFFFFu) {
-          atomicAdd(&s.sp_nnz, 1u);
-          atomicAdd(&s.sp_sum, c);
+          atomicAdd(&s.sp, add);
           continue;
         }
         const uint32_t dk = d + 1;
@@ -645,11 +637,13 @@ __global__ void __launch_bounds__(kLocThreads, 4)
           uint32_t cur = s.key[h];
           if (cur == 0) {
             cur = atomicCAS(&s.key[h], 0u, dk);
-            if (cur == 0) cur = dk;
+            if (cur == 0) {
+              s.list[atomicAdd(&s.nl, 1u)] = (uint16_t)h;
+              cur = dk;
+            }
           }
           if (cur == dk) {
-            atomicAdd(&s.nnz[h], 1u);
-            atomicAdd(&s.sum[h], c);
+            atomicAdd(&s.ns[h], add);
             break;
           }
           h = h + 1 == kLocCT ? 0 : h + 1;
@@ -657,23 +651,26 @@ __global__ void __launch_bounds__(kLocThreads, 4)
       }
     }
     __syncthreads();
-    for (int j = tid; j < kLocCT; j += kLocThreads) {
-      if (s.key[j]) {
-        a_cnt += 1;
-        a_fanin = max(a_fanin, (unsigned long long)s.nnz[j]);
-        a_pk = max(a_pk, (unsigned long long)s.sum[j]);
-        s.key[j] = 0;
-        s.nnz[j] = 0;
-        s.sum[j] = 0;
-      }
-    }
-    if (tid == 0 && s.sp_nnz) {
+    const uint32_t nl = s.nl;
+    for (uint32_t j = tid; j < nl; j += kLocThreads) {
+      const uint32_t h = s.list[j];
+      const unsigned long long v = s.ns[h];
       a_cnt += 1;
-      a_fanin = max(a_fanin, (unsigned long long)s.sp_nnz);
-      a_pk = max(a_pk, (unsigned long long)s.sp_sum);
+      a_fanin = max(a_fanin, v >> 32);
+      a_pk = max(a_pk, v & 0xFFFFFFFFull);
+      s.key[h] = 0;
+      s.ns[h] = 0;
+    }
+    if (tid == 0 && s.sp) {
+      a_cnt += 1;
+      a_fanin = max(a_fanin, s.sp >> 32);
+      a_pk = max(a_pk, s.sp & 0xFFFFFFFFull);
     }
     __syncthreads();
-    if (tid == 0) s.sp_nnz = s.sp_sum = 0;
+    if (tid == 0) {
+      s.sp = 0;
+      s.nl = 0;
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
