@@ -51,14 +51,19 @@ struct PacketSrc {
   uint64_t n;
   uint64_t window_size;  // 0 -> single window
   int b;                 // bits per address
+  // branch-free: the loads are issued unconditionally (clamped index) so a
+  // thread's whole tile of loads can be in flight at once
   __device__ __forceinline__ bool load(uint64_t i, uint64_t& key, uint32_t& val) const {
-    if (i >= n) return false;
-    if (valid && !__ldg(valid + i)) return false;
-    uint64_t k = ((uint64_t)__ldg(src + i) << b) | __ldg(dst + i);
-    if (window_size) k |= (i / window_size) << (2 * b);
+    const bool in = i < n;
+    const uint64_t j = in ? i : 0;
+    const uint32_t s = __ldg(src + j), d = __ldg(dst + j);
+    bool ok = in;
+    if (valid) ok = ok && __ldg(valid + j) != 0;
+    uint64_t k = ((uint64_t)s << b) | d;
+    if (window_size) k |= (j / window_size) << (2 * b);
     key = k;
     val = 0;
-    return true;
+    return ok;
   }
 };
 
@@ -68,10 +73,11 @@ struct KeySrc {
   const uint32_t* vals;
   uint64_t n;
   __device__ __forceinline__ bool load(uint64_t i, KeyT& key, uint32_t& val) const {
-    if (i >= n) return false;
-    key = keys[i];
-    val = HAS_VAL ? vals[i] : 0u;
-    return true;
+    const bool in = i < n;
+    const uint64_t j = in ? i : 0;
+    key = keys[j];
+    val = HAS_VAL ? vals[j] : 0u;
+    return in;
   }
 };
 

@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     s.nl = s.ns = 0;
     group_fetch(gb, off, blockIdx.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
   }
+  uint32_t pf_blo = 0, pf_bhi = 0, pf_klo = 0, pf_khi = 0;  // thread 0's in-flight prefetch
   (void)group_counter;
   const uint64_t dmask = (1ull << b) - 1;
   unsigned long long a_valid = 0, a_links = 0, a_srcs = 0, a_mlink = 0, a_msrc = 0, a_mfan = 0;
@@ -382,7 +383,11 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     }
     __syncthreads();
     const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
-    if (tid == 0) group_fetch(gb, off, g + gridDim.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);  // prefetch
+    const uint32_t gn = g + gridDim.x;
+    if (tid == 0 && gn < ngroups) {  // issue only: consumed after the inserts
+      pf_blo = gb[gn];
+      pf_bhi = gb[gn + 1];
+    }
     uint32_t seg_lo[2], seg_hi[2];
     const uint32_t nseg = group_segments(off, blo, bhi, klo, khi, capb, heavy, nheavy_out, &s.nheavy, s.heavy_lo,
                                          s.heavy_hi, seg_lo, seg_hi);
@@ -439,6 +444,10 @@ __global__ void __launch_bounds__(kLocThreads, 3)
         }
       }
     }
+    if (tid == 0 && gn < ngroups) {
+      pf_klo = off[pf_blo];
+      pf_khi = off[pf_bhi];
+    }
     __syncthreads();
     const uint32_t nl = s.nl, ns = s.ns, sp = s.sp_link;
     const uint32_t len0 = seg_hi[0] - seg_lo[0];
@@ -490,6 +499,10 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     if (tid == 0) {
       s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
       s.nl = s.ns = 0;
+      s.nblo = pf_blo;
+      s.nbhi = pf_bhi;
+      s.nklo = pf_klo;
+      s.nkhi = pf_khi;
     }
   }
 #pragma unroll
@@ -535,16 +548,12 @@ struct ColConcatSrc {
   uint64_t n2;
   uint64_t n;  // n1 + n2
   __device__ __forceinline__ bool load(uint64_t i, uint32_t& key, uint32_t& val) const {
-    if (i >= n) return false;
-    if (i < n1) {
-      val = v1[i];
-      if (!val) return false;
-      key = k1[i];
-    } else {
-      key = k2[i - n1];
-      val = v2[i - n1];
-    }
-    return true;
+    const bool in = i < n;
+    const uint64_t j = in ? i : 0;
+    const bool first = j < n1;
+    key = first ? k1[j] : k2[j - n1];
+    val = first ? v1[j] : v2[j - n1];
+    return in && val != 0;
   }
 };
 
@@ -607,6 +616,7 @@ __global__ void __launch_bounds__(kLocThreads, 4)
     s.nl = 0;
     group_fetch(gb, off, blockIdx.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
   }
+  uint32_t pf_blo = 0, pf_bhi = 0, pf_klo = 0, pf_khi = 0;  // thread 0's in-flight prefetch
   (void)group_counter;
   unsigned long long a_cnt = 0, a_fanin = 0, a_pk = 0;
   for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
@@ -619,7 +629,11 @@ __global__ void __launch_bounds__(kLocThreads, 4)
     }
     __syncthreads();
     const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
-    if (tid == 0) group_fetch(gb, off, g + gridDim.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
+    const uint32_t gn = g + gridDim.x;
+    if (tid == 0 && gn < ngroups) {  // issue only: consumed after the inserts
+      pf_blo = gb[gn];
+      pf_bhi = gb[gn + 1];
+    }
     uint32_t seg_lo[2], seg_hi[2];
     const uint32_t nseg = group_segments(off, blo, bhi, klo, khi, capb, heavy, nheavy_out, &s.nheavy, s.heavy_lo,
                                          s.heavy_hi, seg_lo, seg_hi);
@@ -650,6 +664,10 @@ __global__ void __launch_bounds__(kLocThreads, 4)
         }
       }
     }
+    if (tid == 0 && gn < ngroups) {
+      pf_klo = off[pf_blo];
+      pf_khi = off[pf_bhi];
+    }
     __syncthreads();
     const uint32_t nl = s.nl;
     for (uint32_t j = tid; j < nl; j += kLocThreads) {
@@ -670,6 +688,10 @@ __global__ void __launch_bounds__(kLocThreads, 4)
     if (tid == 0) {
       s.sp = 0;
       s.nl = 0;
+      s.nblo = pf_blo;
+      s.nbhi = pf_bhi;
+      s.nklo = pf_klo;
+      s.nkhi = pf_khi;
     }
   }
 #pragma unroll
