@@ -105,7 +105,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
+  DevBuf mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
@@ -580,6 +580,29 @@ uint64_t fetch_heavy(nmx_ctx* c, uint32_t* d_count, uint32_t* nheavy_out) {
   return total;
 }
 
+// groups of whole buckets (bucket starts inside one S-key chunk), their heavy
+// bucket, and the global heavy list (count at small[kCounters + 31])
+void plan_groups(nmx_ctx* c, const uint32_t* off, uint32_t nb, uint64_t m, uint32_t S, uint32_t capb) {
+  uint32_t* d_small = c->small.as<uint32_t>();
+  const uint32_t ngroups = (uint32_t)((m + S - 1) / S);
+  c->mgb.grow(((size_t)ngroups + 2) * 4);
+  c->mgh.grow(((size_t)ngroups + 2) * 8);
+  c->mplan.grow(((size_t)ngroups + 2) * 16);
+  c->mheavy.grow(((size_t)ngroups + 2) * 8);
+  const unsigned g1 = (unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8);
+  group_bounds_kernel<<<g1, 256, 0, c->st>>>(off, nb, S, ngroups, c->mgb.as<uint32_t>());
+  CK_LAUNCH();
+  CK(cudaMemsetAsync(c->mgh.p, 0, (size_t)ngroups * 8, c->st));
+  CK(cudaMemsetAsync(d_small + kCounters + 31, 0, 4, c->st));
+  bucket_heavy_kernel<<<(unsigned)std::min<uint64_t>((nb + 255) / 256, (uint64_t)c->sms * 8), 256, 0, c->st>>>(
+      off, nb, S, capb, c->mgh.as<uint2>(), c->mheavy.as<uint32_t>(), d_small + kCounters + 31);
+  CK_LAUNCH();
+  group_plan_kernel<<<g1, 256, 0, c->st>>>(off, c->mgb.as<uint32_t>(), c->mgh.as<uint2>(), ngroups,
+                                           c->mplan.as<uint4>());
+  CK_LAUNCH();
+  c->launches += 3;
+}
+
 void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
                       int b, int D) {
   const int kb = 2 * b;
@@ -598,6 +621,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
 
   // ---- rows: MSD partition of the packed keys by source bits ----
   PacketSrc ps{d_src, d_dst, d_valid, n, 0, b};
+  ps.quad = !(((uintptr_t)d_src | (uintptr_t)d_dst) & 15) && !((uintptr_t)d_valid & 3);
   c->mark();  // 1: row partition start
   uint64_t* keys = nullptr;
   uint32_t* dummy = nullptr;
@@ -612,18 +636,13 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   const uint32_t nb = 1u << D;
   uint32_t* off = c->moff.as<uint32_t>();
   uint32_t ngroups = (uint32_t)((m + S - 1) / S);
-  c->mgb.grow(((size_t)ngroups + 2) * 4);
-  c->mheavy.grow(((size_t)ngroups + 2) * 8);
-  group_bounds_kernel<<<(unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8), 256, 0, c->st>>>(
-      off, nb, S, ngroups, c->mgb.as<uint32_t>());
-  CK_LAUNCH();
-  CK(cudaMemsetAsync(d_small + kCounters + 30, 0, 8, c->st));
+  plan_groups(c, off, nb, m, S, capb);
   set_smem(local_rows_kernel, sizeof(LocSmem));
   local_rows_kernel<<<(unsigned)(c->sms * 3), kLocThreads, sizeof(LocSmem), c->st>>>(
-      keys, off, c->mgb.as<uint32_t>(), ngroups, capb, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
-      c->mheavy.as<uint32_t>(), d_small + kCounters + 31, d_small + kCounters + 30, c->stats.as<unsigned long long>());
+      keys, c->mplan.as<uint4>(), ngroups, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
+      c->stats.as<unsigned long long>());
   CK_LAUNCH();
-  c->launches += 2;
+  ++c->launches;
   c->mark();  // 3: local rows end
   uint32_t nheavy = 0;
   const uint64_t mh = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
@@ -648,6 +667,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   // ---- columns: MSD partition of the (dst, count) entries by destination bits ----
   ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), m,
                   c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh, m + uh};
+  cs.quad = true;  // context buffers are cudaMalloc-aligned
   const int Dc = std::min(D, b);
   uint32_t* ck = nullptr;
   uint32_t* cv = nullptr;
@@ -657,18 +677,12 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   c->mark();  // 5: column partition end
   const uint32_t nbc = 1u << Dc;
   ngroups = (uint32_t)((u + S - 1) / S);
-  c->mgb.grow(((size_t)ngroups + 2) * 4);
-  c->mheavy.grow(((size_t)ngroups + 2) * 8);
-  group_bounds_kernel<<<(unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8), 256, 0, c->st>>>(
-      off, nbc, S, ngroups, c->mgb.as<uint32_t>());
-  CK_LAUNCH();
-  CK(cudaMemsetAsync(d_small + kCounters + 30, 0, 8, c->st));
+  plan_groups(c, off, nbc, u, S, capb);
   set_smem(local_cols_kernel, sizeof(LocColSmem));
   local_cols_kernel<<<(unsigned)(c->sms * 4), kLocThreads, sizeof(LocColSmem), c->st>>>(
-      ck, cv, off, c->mgb.as<uint32_t>(), ngroups, capb, c->mheavy.as<uint32_t>(), d_small + kCounters + 31,
-      d_small + kCounters + 30, c->stats.as<unsigned long long>());
+      ck, cv, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>());
   CK_LAUNCH();
-  c->launches += 2;
+  ++c->launches;
   c->mark();  // 6: local columns end
   const uint64_t ch = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
   if (ch) {  // heavy destination buckets: gather -> LSD sort -> column kernel
@@ -872,7 +886,7 @@ void nmx_destroy(nmx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (DevBuf* b : {&c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
+  for (DevBuf* b : {&c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
                     &c->mhist2, &c->mgb, &c->mheavy, &c->mdst, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})

@@ -51,6 +51,29 @@ struct PacketSrc {
   uint64_t n;
   uint64_t window_size;  // 0 -> single window
   int b;                 // bits per address
+  bool quad = false;     // src/dst 16-byte aligned (and valid 4-byte aligned): 128-bit loads allowed
+  // four consecutive packets [4q, 4q+4) with two 128-bit loads (scalar at the tail)
+  __device__ __forceinline__ void load_quad(uint64_t q, uint64_t* key, bool* ok) const {
+    const uint64_t i = 4 * q;
+    if (quad && i + 4 <= n && !window_size) {
+      const uint4 s4 = __ldg(reinterpret_cast<const uint4*>(src) + q);
+      const uint4 d4 = __ldg(reinterpret_cast<const uint4*>(dst) + q);
+      uint32_t vv = 0x01010101u;
+      if (valid) vv = __ldg(reinterpret_cast<const uint32_t*>(valid) + q);
+      key[0] = ((uint64_t)s4.x << b) | d4.x;
+      key[1] = ((uint64_t)s4.y << b) | d4.y;
+      key[2] = ((uint64_t)s4.z << b) | d4.z;
+      key[3] = ((uint64_t)s4.w << b) | d4.w;
+      ok[0] = (vv & 0xFFu) != 0;
+      ok[1] = (vv & 0xFF00u) != 0;
+      ok[2] = (vv & 0xFF0000u) != 0;
+      ok[3] = (vv & 0xFF000000u) != 0;
+    } else {
+      uint32_t v;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ok[t] = load(i + t, key[t], v);
+    }
+  }
   // branch-free: the loads are issued unconditionally (clamped index) so a
   // thread's whole tile of loads can be in flight at once
   __device__ __forceinline__ bool load(uint64_t i, uint64_t& key, uint32_t& val) const {

@@ -58,6 +58,20 @@ __device__ __forceinline__ void smem_excl_scan(uint32_t* cnt, uint32_t* out, uin
   __syncthreads();
 }
 
+// 8 items per thread as two quads (quad indices q0 and q0 + qstride)
+__device__ __forceinline__ void quad_items(const PacketSrc& s, uint64_t q, uint64_t* k, uint32_t* v, bool* ok) {
+  s.load_quad(q, k, ok);
+  v[0] = v[1] = v[2] = v[3] = 0;
+}
+struct ColConcatSrc;
+__device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok);
+template <typename Src, typename KeyT>
+__device__ __forceinline__ void load_items(const Src& s, uint64_t q0, uint64_t qstride, KeyT* k, uint32_t* v,
+                                           bool* ok) {
+  quad_items(s, q0, k, v, ok);
+  quad_items(s, q0 + qstride, k + 4, v + 4, ok + 4);
+}
+
 // Level 1 (cursor indexed by the D1-bit digit) and level 2 (cursor indexed by
 // the D-bit bucket id; a tile lies in one or two level-1 buckets, keys of further
 // buckets take a per-key global atomic). KeyT u64 = packed row keys; KeyT u32
@@ -89,13 +103,18 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
     src.load(base, k0, v);
     S.b1first = (uint64_t)k0 >> bshift;
   }
-  // issue every load of the tile before using any (memory-level parallelism)
+  // issue every load of the tile before using any (memory-level parallelism);
+  // order inside a tile is irrelevant to a non-stable partition
   KeyT k[kMsdIPT];
   uint32_t v[kMsdIPT];
   bool ok[kMsdIPT];
+  if constexpr (LEVEL == 1) {
+    load_items<Src, KeyT>(src, base / 4 + tid, kMsdThreads, k, v, ok);
+  } else {
 #pragma unroll
-  for (int i = 0; i < kMsdIPT; ++i)
-    ok[i] = src.load(base + (uint64_t)warp * 32 * kMsdIPT + (uint64_t)i * 32 + lane, k[i], v[i]);
+    for (int i = 0; i < kMsdIPT; ++i)
+      ok[i] = src.load(base + (uint64_t)warp * 32 * kMsdIPT + (uint64_t)i * 32 + lane, k[i], v[i]);
+  }
   __syncthreads();
   const uint64_t b1first = S.b1first;
   const uint32_t dmask = (1u << dbits) - 1;
@@ -172,8 +191,8 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
     KeyT k[U];
     uint32_t v[U];
     bool ok[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) ok[u] = src.load(base + (uint64_t)u * 256 + threadIdx.x, k[u], v[u]);
+    // two quads per thread: packets base + 4*(u*256 + tid) .. +4
+    load_items<Src, KeyT>(src, base / 4 + threadIdx.x, 256, k, v, ok);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (ok[u]) {
@@ -282,6 +301,40 @@ constexpr int kLocT1 = 3072;       // link table slots (load <= 2/3)
 constexpr int kLocT2 = 3072;       // source table slots
 constexpr int kLocMaxHeavy = 8;
 
+// heavy buckets (size > capb): recorded once in the global list for the LSD
+// fallback and as the (single) excluded range of the group their start lies in
+__global__ void bucket_heavy_kernel(const uint32_t* __restrict__ off, uint32_t nb, uint32_t S, uint32_t capb,
+                                    uint2* __restrict__ gheavy, uint32_t* __restrict__ heavy,
+                                    uint32_t* __restrict__ nheavy) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += gridDim.x * blockDim.x) {
+    const uint32_t lo = off[j], hi = off[j + 1];
+    if (hi - lo > capb) {
+      gheavy[lo / S] = make_uint2(lo, hi);
+      const uint32_t q = atomicAdd(nheavy, 1u);
+      heavy[2 * q] = lo;
+      heavy[2 * q + 1] = hi;
+    }
+  }
+}
+
+// plan[g] = {klo, khi, hlo, hhi}: group g's keys and its excluded heavy range
+__global__ void group_plan_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ gb,
+                                  const uint2* __restrict__ gheavy, uint32_t ngroups, uint4* __restrict__ plan) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+    const uint2 h = gheavy[g];
+    plan[g] = make_uint4(off[gb[g]], off[gb[g + 1]], h.x, h.y);
+  }
+}
+
+// light position j of a group -> global index (the heavy range is skipped)
+__device__ __forceinline__ uint32_t light_index(const uint4& p, uint32_t j) {
+  const uint32_t len0 = (p.w > p.z ? p.z : p.y) - p.x;
+  return j < len0 ? p.x + j : p.w + (j - len0);
+}
+__device__ __forceinline__ uint32_t light_count(const uint4& p) { return (p.y - p.x) - (p.w - p.z); }
+
+constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 4 keys in registers per thread
+
 struct LocSmem {
   unsigned long long t1key[kLocT1];  // key + 1 (0 = empty)
   uint32_t t1cnt[kLocT1];
@@ -289,12 +342,11 @@ struct LocSmem {
   uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
   uint16_t list1[kLocMaxKeys];  // occupied link slots, in insertion order
   uint16_t list2[kLocMaxKeys];  // occupied source slots
-  uint32_t nl, ns;
-  uint32_t heavy_lo[kLocMaxHeavy], heavy_hi[kLocMaxHeavy];
-  uint32_t nheavy;
-  uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
-  uint32_t blo, bhi, klo, khi;             // current group
-  uint32_t nblo, nbhi, nklo, nkhi;         // prefetched next group
+  // per-iteration-parity counters: the parity not in use is reset in the middle
+  // of an iteration, so one barrier pair per group suffices
+  uint32_t nl[2], ns[2];
+  uint32_t sp_link[2], sp_src_pk[2], sp_src_fo[2];  // the all-ones key / source (cannot be stored +1)
+  uint4 plan[2];                                    // current / next group (by iteration parity)
 };
 
 __device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
@@ -302,56 +354,12 @@ __device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
   return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
 }
 
-// group g: buckets [gb[g], gb[g+1]) = keys [off[gb[g]], off[gb[g+1]])
-__device__ __forceinline__ void group_fetch(const uint32_t* gb, const uint32_t* off, uint32_t g, uint32_t ngroups,
-                                            uint32_t& blo, uint32_t& bhi, uint32_t& klo, uint32_t& khi) {
-  if (g < ngroups) {
-    blo = gb[g];
-    bhi = gb[g + 1];
-    klo = off[blo];
-    khi = off[bhi];
-  }
-}
-
-// Heavy buckets of the current group: recorded for the LSD fallback (globally)
-// and as excluded ranges (in smem). Returns the light segments of [klo, khi).
-__device__ __forceinline__ uint32_t group_segments(const uint32_t* off, uint32_t blo, uint32_t bhi, uint32_t klo,
-                                                   uint32_t khi, uint32_t capb, uint32_t* heavy, uint32_t* nheavy_out,
-                                                   uint32_t* s_nheavy, uint32_t* s_hlo, uint32_t* s_hhi,
-                                                   uint32_t* seg_lo, uint32_t* seg_hi) {
-  for (uint32_t j = blo + threadIdx.x; j < bhi; j += blockDim.x) {
-    const uint32_t lo = off[j], hi = off[j + 1];
-    if (hi - lo > capb) {
-      const uint32_t q = atomicAdd(s_nheavy, 1u);
-      if (q < kLocMaxHeavy) {
-        s_hlo[q] = lo;
-        s_hhi[q] = hi;
-      }
-      const uint32_t gq = atomicAdd(nheavy_out, 1u);
-      heavy[2 * gq] = lo;
-      heavy[2 * gq + 1] = hi;
-    }
-  }
-  __syncthreads();
-  // a heavy bucket has > capb >= S keys and buckets start inside an S-key chunk,
-  // so a group holds at most one heavy bucket
-  if (*s_nheavy == 0) {
-    seg_lo[0] = klo;
-    seg_hi[0] = khi;
-    return 1;
-  }
-  seg_lo[0] = klo;
-  seg_hi[0] = s_hlo[0];
-  seg_lo[1] = s_hhi[0];
-  seg_hi[1] = khi;
-  return 2;
-}
-
+// Groups are statically round-robined over persistent CTAs. While group g is
+// hashed, thread 0 fetches plan[g + G]; after the barrier every thread issues the
+// loads of its next-group keys, which land while group g's results are written.
 __global__ void __launch_bounds__(kLocThreads, 3)
-    local_rows_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ off,
-                      const uint32_t* __restrict__ gb, uint32_t ngroups, uint32_t capb, int b,
-                      uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt, uint32_t* __restrict__ heavy,
-                      uint32_t* __restrict__ nheavy_out, uint32_t* __restrict__ group_counter,
+    local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
+                      uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt,
                       unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
@@ -364,100 +372,112 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     s.t2key[i] = 0;
     s.t2pf[i] = 0;
   }
-  if (tid == 0) {
-    s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
-    s.nl = s.ns = 0;
-    group_fetch(gb, off, blockIdx.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
+  if (tid < 2) {
+    s.sp_link[tid] = s.sp_src_pk[tid] = s.sp_src_fo[tid] = 0;
+    s.nl[tid] = s.ns[tid] = 0;
   }
-  uint32_t pf_blo = 0, pf_bhi = 0, pf_klo = 0, pf_khi = 0;  // thread 0's in-flight prefetch
-  (void)group_counter;
+  if (tid == 0 && blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
+  __syncthreads();
   const uint64_t dmask = (1ull << b) - 1;
+  uint64_t kr[kLocPerThread];
+  uint32_t nmine = 0;
+  if (blockIdx.x < ngroups) {
+    const uint4 p = s.plan[0];
+    const uint32_t nlight = light_count(p);
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) {
+      const uint32_t j = tid + r * kLocThreads;
+      if (j < nlight) {
+        kr[r] = keys[light_index(p, j)];
+        ++nmine;
+      }
+    }
+  }
   unsigned long long a_valid = 0, a_links = 0, a_srcs = 0, a_mlink = 0, a_msrc = 0, a_mfan = 0;
-  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    if (tid == 0) {
-      s.blo = s.nblo;
-      s.bhi = s.nbhi;
-      s.klo = s.nklo;
-      s.khi = s.nkhi;
-      s.nheavy = 0;
-    }
-    __syncthreads();
-    const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
+  uint32_t it = 0;
+  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+    const uint32_t cur = it & 1;
     const uint32_t gn = g + gridDim.x;
-    if (tid == 0 && gn < ngroups) {  // issue only: consumed after the inserts
-      pf_blo = gb[gn];
-      pf_bhi = gb[gn + 1];
-    }
-    uint32_t seg_lo[2], seg_hi[2];
-    const uint32_t nseg = group_segments(off, blo, bhi, klo, khi, capb, heavy, nheavy_out, &s.nheavy, s.heavy_lo,
-                                         s.heavy_hi, seg_lo, seg_hi);
-    for (uint32_t sg = 0; sg < nseg; ++sg) {
-      for (uint32_t i = seg_lo[sg] + tid; i < seg_hi[sg]; i += kLocThreads) {
-        const uint64_t key = keys[i];
-        bool fresh;
-        if (key == ~0ull) {
-          fresh = atomicAdd(&s.sp_link, 1u) == 0;
-        } else {
-          const unsigned long long kk = key + 1;
-          uint32_t h = hslot(kk, kLocT1);
-          for (;;) {
-            unsigned long long cur = s.t1key[h];
-            if (cur == 0) {
-              cur = atomicCAS(&s.t1key[h], 0ull, kk);
-              if (cur == 0) {
-                atomicAdd(&s.t1cnt[h], 1u);
-                s.list1[atomicAdd(&s.nl, 1u)] = (uint16_t)h;
-                fresh = true;
-                break;
-              }
-            }
-            if (cur == kk) {
+    uint4 pnext = make_uint4(0, 0, 0, 0);
+    if (tid == 0 && gn < ngroups) pnext = plan[gn];  // in flight during the inserts
+    for (uint32_t r = 0; r < nmine; ++r) {
+      const uint64_t key = kr[r];
+      bool fresh;
+      if (key == ~0ull) {
+        fresh = atomicAdd(&s.sp_link[cur], 1u) == 0;
+      } else {
+        const unsigned long long kk = key + 1;
+        uint32_t h = hslot(kk, kLocT1);
+        for (;;) {
+          unsigned long long c0 = s.t1key[h];
+          if (c0 == 0) {
+            c0 = atomicCAS(&s.t1key[h], 0ull, kk);
+            if (c0 == 0) {
               atomicAdd(&s.t1cnt[h], 1u);
-              fresh = false;
+              s.list1[atomicAdd(&s.nl[cur], 1u)] = (uint16_t)h;
+              fresh = true;
               break;
             }
-            h = h + 1 == kLocT1 ? 0 : h + 1;
           }
+          if (c0 == kk) {
+            atomicAdd(&s.t1cnt[h], 1u);
+            fresh = false;
+            break;
+          }
+          h = h + 1 == kLocT1 ? 0 : h + 1;
         }
-        const uint32_t src = (uint32_t)(key >> b);
-        if (src == 0xFFFFFFFFu) {
-          atomicAdd(&s.sp_src_pk, 1u);
-          if (fresh) atomicAdd(&s.sp_src_fo, 1u);
-        } else {
-          const uint32_t sk = src + 1;
-          uint32_t h = hslot(sk, kLocT2);
-          for (;;) {
-            uint32_t cur = s.t2key[h];
-            if (cur == 0) {
-              cur = atomicCAS(&s.t2key[h], 0u, sk);
-              if (cur == 0) {
-                s.list2[atomicAdd(&s.ns, 1u)] = (uint16_t)h;
-                cur = sk;
-              }
+      }
+      const uint32_t src = (uint32_t)(key >> b);
+      if (src == 0xFFFFFFFFu) {
+        atomicAdd(&s.sp_src_pk[cur], 1u);
+        if (fresh) atomicAdd(&s.sp_src_fo[cur], 1u);
+      } else {
+        const uint32_t sk = src + 1;
+        uint32_t h = hslot(sk, kLocT2);
+        for (;;) {
+          uint32_t c0 = s.t2key[h];
+          if (c0 == 0) {
+            c0 = atomicCAS(&s.t2key[h], 0u, sk);
+            if (c0 == 0) {
+              s.list2[atomicAdd(&s.ns[cur], 1u)] = (uint16_t)h;
+              c0 = sk;
             }
-            if (cur == sk) {
-              atomicAdd(&s.t2pf[h], 1u | (fresh ? 0x10000u : 0u));
-              break;
-            }
-            h = h + 1 == kLocT2 ? 0 : h + 1;
           }
+          if (c0 == sk) {
+            atomicAdd(&s.t2pf[h], 1u | (fresh ? 0x10000u : 0u));
+            break;
+          }
+          h = h + 1 == kLocT2 ? 0 : h + 1;
         }
       }
     }
-    if (tid == 0 && gn < ngroups) {
-      pf_klo = off[pf_blo];
-      pf_khi = off[pf_bhi];
-    }
+    if (tid == 0) s.plan[cur ^ 1] = pnext;
     __syncthreads();
-    const uint32_t nl = s.nl, ns = s.ns, sp = s.sp_link;
-    const uint32_t len0 = seg_hi[0] - seg_lo[0];
-    auto slot_of = [&](uint32_t j) -> uint32_t { return j < len0 ? seg_lo[0] + j : seg_lo[1] + (j - len0); };
-    // links -> compacted (dst, count) column entries in this group's light slots
-    for (uint32_t j = tid; j < nl; j += kLocThreads) {
+    // prefetch the next group's keys (registers), then write this group's results
+    const uint4 p = s.plan[cur];
+    const uint4 pn = s.plan[cur ^ 1];
+    nmine = 0;
+    if (gn < ngroups) {
+      const uint32_t nl2 = light_count(pn);
+#pragma unroll
+      for (int r = 0; r < kLocPerThread; ++r) {
+        const uint32_t j = tid + r * kLocThreads;
+        if (j < nl2) {
+          kr[r] = keys[light_index(pn, j)];
+          ++nmine;
+        }
+      }
+    }
+    if (tid == 0) {  // the other parity was last read before the previous barrier
+      s.nl[cur ^ 1] = s.ns[cur ^ 1] = 0;
+      s.sp_link[cur ^ 1] = s.sp_src_pk[cur ^ 1] = s.sp_src_fo[cur ^ 1] = 0;
+    }
+    const uint32_t nl = s.nl[cur], ns = s.ns[cur], sp = s.sp_link[cur];
+    for (uint32_t j = tid; j < nl; j += kLocThreads) {  // links -> (dst, count) column entries
       const uint32_t h = s.list1[j];
       const uint64_t key = s.t1key[h] - 1;
       const uint32_t c = s.t1cnt[h];
-      const uint32_t pos = slot_of(j);
+      const uint32_t pos = light_index(p, j);
       col_dst[pos] = (uint32_t)(key & dmask);
       col_cnt[pos] = c;
       a_links += 1;
@@ -469,7 +489,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     uint32_t used = nl;
     if (sp) {
       if (tid == 0) {
-        const uint32_t pos = slot_of(nl);
+        const uint32_t pos = light_index(p, nl);
         col_dst[pos] = (uint32_t)dmask;
         col_cnt[pos] = sp;
         a_links += 1;
@@ -478,9 +498,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       }
       used += 1;
     }
-    uint32_t nlight = 0;
-    for (uint32_t sg = 0; sg < nseg; ++sg) nlight += seg_hi[sg] - seg_lo[sg];
-    for (uint32_t j = used + tid; j < nlight; j += kLocThreads) col_cnt[slot_of(j)] = 0;  // holes
+    const uint32_t nlight = light_count(p);
+    for (uint32_t j = used + tid; j < nlight; j += kLocThreads) col_cnt[light_index(p, j)] = 0;  // holes
     for (uint32_t j = tid; j < ns; j += kLocThreads) {
       const uint32_t h = s.list2[j];
       const uint32_t pf = s.t2pf[h];
@@ -490,20 +509,12 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       s.t2key[h] = 0;
       s.t2pf[h] = 0;
     }
-    if (tid == 0 && s.sp_src_pk) {
+    if (tid == 0 && s.sp_src_pk[cur]) {
       a_srcs += 1;
-      a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk);
-      a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo);
+      a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk[cur]);
+      a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo[cur]);
     }
     __syncthreads();
-    if (tid == 0) {
-      s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
-      s.nl = s.ns = 0;
-      s.nblo = pf_blo;
-      s.nbhi = pf_bhi;
-      s.nklo = pf_klo;
-      s.nkhi = pf_khi;
-    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -547,6 +558,21 @@ struct ColConcatSrc {
   const uint32_t* v2;
   uint64_t n2;
   uint64_t n;  // n1 + n2
+  bool quad = false;  // k1 / v1 16-byte aligned
+  __device__ __forceinline__ void load_quad(uint64_t q, uint32_t* key, uint32_t* val, bool* ok) const {
+    const uint64_t i = 4 * q;
+    if (quad && i + 4 <= n1) {
+      const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(k1) + q);
+      const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(v1) + q);
+      key[0] = k4.x, key[1] = k4.y, key[2] = k4.z, key[3] = k4.w;
+      val[0] = v4.x, val[1] = v4.y, val[2] = v4.z, val[3] = v4.w;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ok[t] = val[t] != 0;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ok[t] = load(i + t, key[t], val[t]);
+    }
+  }
   __device__ __forceinline__ bool load(uint64_t i, uint32_t& key, uint32_t& val) const {
     const bool in = i < n;
     const uint64_t j = in ? i : 0;
@@ -556,6 +582,10 @@ struct ColConcatSrc {
     return in && val != 0;
   }
 };
+
+__device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok) {
+  s.load_quad(q, k, v, ok);
+}
 
 template <int NPASS>
 __global__ void __launch_bounds__(256) hist_concat_kernel(ColConcatSrc src, uint32_t* __restrict__ ghist,
@@ -588,22 +618,17 @@ __global__ void __launch_bounds__(256) hist_concat_kernel(ColConcatSrc src, uint
 // ---------------------------------------------------------------------------
 constexpr int kLocCT = 3072;
 struct LocColSmem {
-  uint32_t key[kLocCT];             // dst + 1 (0 = empty)
-  unsigned long long ns[kLocCT];    // fan-in << 32 | packets
+  uint32_t key[kLocCT];           // dst + 1 (0 = empty)
+  unsigned long long ns[kLocCT];  // fan-in << 32 | packets
   uint16_t list[kLocMaxKeys];
-  uint32_t nl;
-  uint32_t heavy_lo[kLocMaxHeavy], heavy_hi[kLocMaxHeavy];
-  uint32_t nheavy;
-  unsigned long long sp;  // dst == 0xFFFFFFFF
-  uint32_t blo, bhi, klo, khi;
-  uint32_t nblo, nbhi, nklo, nkhi;
+  uint32_t nl[2];
+  unsigned long long sp[2];  // dst == 0xFFFFFFFF
+  uint4 plan[2];
 };
 
 __global__ void __launch_bounds__(kLocThreads, 4)
     local_cols_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
-                      const uint32_t* __restrict__ off, const uint32_t* __restrict__ gb, uint32_t ngroups,
-                      uint32_t capb, uint32_t* __restrict__ heavy, uint32_t* __restrict__ nheavy_out,
-                      uint32_t* __restrict__ group_counter, unsigned long long* __restrict__ stats) {
+                      const uint4* __restrict__ plan, uint32_t ngroups, unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -611,65 +636,82 @@ __global__ void __launch_bounds__(kLocThreads, 4)
     s.key[i] = 0;
     s.ns[i] = 0;
   }
-  if (tid == 0) {
-    s.sp = 0;
-    s.nl = 0;
-    group_fetch(gb, off, blockIdx.x, ngroups, s.nblo, s.nbhi, s.nklo, s.nkhi);
+  if (tid < 2) {
+    s.sp[tid] = 0;
+    s.nl[tid] = 0;
   }
-  uint32_t pf_blo = 0, pf_bhi = 0, pf_klo = 0, pf_khi = 0;  // thread 0's in-flight prefetch
-  (void)group_counter;
+  if (tid == 0 && blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
+  __syncthreads();
+  uint32_t kr[kLocPerThread], vr[kLocPerThread];
+  uint32_t nmine = 0;
+  if (blockIdx.x < ngroups) {
+    const uint4 p = s.plan[0];
+    const uint32_t nlight = light_count(p);
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) {
+      const uint32_t j = tid + r * kLocThreads;
+      if (j < nlight) {
+        const uint32_t i = light_index(p, j);
+        kr[r] = ck[i];
+        vr[r] = cv[i];
+        ++nmine;
+      }
+    }
+  }
   unsigned long long a_cnt = 0, a_fanin = 0, a_pk = 0;
-  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    if (tid == 0) {
-      s.blo = s.nblo;
-      s.bhi = s.nbhi;
-      s.klo = s.nklo;
-      s.khi = s.nkhi;
-      s.nheavy = 0;
-    }
-    __syncthreads();
-    const uint32_t blo = s.blo, bhi = s.bhi, klo = s.klo, khi = s.khi;
+  uint32_t it = 0;
+  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+    const uint32_t cur = it & 1;
     const uint32_t gn = g + gridDim.x;
-    if (tid == 0 && gn < ngroups) {  // issue only: consumed after the inserts
-      pf_blo = gb[gn];
-      pf_bhi = gb[gn + 1];
-    }
-    uint32_t seg_lo[2], seg_hi[2];
-    const uint32_t nseg = group_segments(off, blo, bhi, klo, khi, capb, heavy, nheavy_out, &s.nheavy, s.heavy_lo,
-                                         s.heavy_hi, seg_lo, seg_hi);
-    for (uint32_t sg = 0; sg < nseg; ++sg) {
-      for (uint32_t i = seg_lo[sg] + tid; i < seg_hi[sg]; i += kLocThreads) {
-        const uint32_t d = ck[i];
-        const unsigned long long add = (1ull << 32) | cv[i];
-        if (d == 0xFFFFFFFFu) {
-          atomicAdd(&s.sp, add);
-          continue;
+    uint4 pnext = make_uint4(0, 0, 0, 0);
+    if (tid == 0 && gn < ngroups) pnext = plan[gn];
+    for (uint32_t r = 0; r < nmine; ++r) {
+      const uint32_t d = kr[r];
+      const unsigned long long add = (1ull << 32) | vr[r];
+      if (d == 0xFFFFFFFFu) {
+        atomicAdd(&s.sp[cur], add);
+        continue;
+      }
+      const uint32_t dk = d + 1;
+      uint32_t h = hslot(dk, kLocCT);
+      for (;;) {
+        uint32_t c0 = s.key[h];
+        if (c0 == 0) {
+          c0 = atomicCAS(&s.key[h], 0u, dk);
+          if (c0 == 0) {
+            s.list[atomicAdd(&s.nl[cur], 1u)] = (uint16_t)h;
+            c0 = dk;
+          }
         }
-        const uint32_t dk = d + 1;
-        uint32_t h = hslot(dk, kLocCT);
-        for (;;) {
-          uint32_t cur = s.key[h];
-          if (cur == 0) {
-            cur = atomicCAS(&s.key[h], 0u, dk);
-            if (cur == 0) {
-              s.list[atomicAdd(&s.nl, 1u)] = (uint16_t)h;
-              cur = dk;
-            }
-          }
-          if (cur == dk) {
-            atomicAdd(&s.ns[h], add);
-            break;
-          }
-          h = h + 1 == kLocCT ? 0 : h + 1;
+        if (c0 == dk) {
+          atomicAdd(&s.ns[h], add);
+          break;
+        }
+        h = h + 1 == kLocCT ? 0 : h + 1;
+      }
+    }
+    if (tid == 0) s.plan[cur ^ 1] = pnext;
+    __syncthreads();
+    const uint4 pn = s.plan[cur ^ 1];
+    nmine = 0;
+    if (gn < ngroups) {
+      const uint32_t nl2 = light_count(pn);
+#pragma unroll
+      for (int r = 0; r < kLocPerThread; ++r) {
+        const uint32_t j = tid + r * kLocThreads;
+        if (j < nl2) {
+          const uint32_t i = light_index(pn, j);
+          kr[r] = ck[i];
+          vr[r] = cv[i];
+          ++nmine;
         }
       }
     }
-    if (tid == 0 && gn < ngroups) {
-      pf_klo = off[pf_blo];
-      pf_khi = off[pf_bhi];
+    if (tid == 0) {
+      s.nl[cur ^ 1] = 0;
+      s.sp[cur ^ 1] = 0;
     }
-    __syncthreads();
-    const uint32_t nl = s.nl;
+    const uint32_t nl = s.nl[cur];
     for (uint32_t j = tid; j < nl; j += kLocThreads) {
       const uint32_t h = s.list[j];
       const unsigned long long v = s.ns[h];
@@ -679,20 +721,12 @@ __global__ void __launch_bounds__(kLocThreads, 4)
       s.key[h] = 0;
       s.ns[h] = 0;
     }
-    if (tid == 0 && s.sp) {
+    if (tid == 0 && s.sp[cur]) {
       a_cnt += 1;
-      a_fanin = max(a_fanin, s.sp >> 32);
-      a_pk = max(a_pk, s.sp & 0xFFFFFFFFull);
+      a_fanin = max(a_fanin, s.sp[cur] >> 32);
+      a_pk = max(a_pk, s.sp[cur] & 0xFFFFFFFFull);
     }
     __syncthreads();
-    if (tid == 0) {
-      s.sp = 0;
-      s.nl = 0;
-      s.nblo = pf_blo;
-      s.nbhi = pf_bhi;
-      s.nklo = pf_klo;
-      s.nkhi = pf_khi;
-    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
