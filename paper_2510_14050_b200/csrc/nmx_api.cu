@@ -638,7 +638,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   uint32_t ngroups = (uint32_t)((m + S - 1) / S);
   plan_groups(c, off, nb, m, S, capb);
   set_smem(local_rows_kernel, sizeof(LocSmem));
-  local_rows_kernel<<<(unsigned)(c->sms * 3), kLocThreads, sizeof(LocSmem), c->st>>>(
+  local_rows_kernel<<<(unsigned)(c->sms * 2), kLocThreads, sizeof(LocSmem), c->st>>>(
       keys, c->mplan.as<uint4>(), ngroups, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
       c->stats.as<unsigned long long>());
   CK_LAUNCH();
@@ -679,7 +679,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   ngroups = (uint32_t)((u + S - 1) / S);
   plan_groups(c, off, nbc, u, S, capb);
   set_smem(local_cols_kernel, sizeof(LocColSmem));
-  local_cols_kernel<<<(unsigned)(c->sms * 4), kLocThreads, sizeof(LocColSmem), c->st>>>(
+  local_cols_kernel<<<(unsigned)(c->sms * 3), kLocThreads, sizeof(LocColSmem), c->st>>>(
       ck, cv, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>());
   CK_LAUNCH();
   ++c->launches;

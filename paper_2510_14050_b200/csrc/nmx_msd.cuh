@@ -334,36 +334,52 @@ __device__ __forceinline__ uint32_t light_index(const uint4& p, uint32_t j) {
 __device__ __forceinline__ uint32_t light_count(const uint4& p) { return (p.y - p.x) - (p.w - p.z); }
 
 constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 4 keys in registers per thread
-
-struct LocSmem {
-  unsigned long long t1key[kLocT1];  // key + 1 (0 = empty)
-  uint32_t t1cnt[kLocT1];
-  uint32_t t2key[kLocT2];  // src + 1 (0 = empty)
-  uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
-  uint16_t list1[kLocMaxKeys];  // occupied link slots, in insertion order
-  uint16_t list2[kLocMaxKeys];  // occupied source slots
-  // per-iteration-parity counters: the parity not in use is reset in the middle
-  // of an iteration, so one barrier pair per group suffices
-  uint32_t nl[2], ns[2];
-  uint32_t sp_link[2], sp_src_pk[2], sp_src_fo[2];  // the all-ones key / source (cannot be stored +1)
-  uint4 plan[2];                                    // current / next group (by iteration parity)
-};
+constexpr int kBmWords = 4096;                             // 65536 two-bit saturating counters
 
 __device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
   const uint64_t h = x * 0x9E3779B97F4A7C15ull;
   return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
 }
+__device__ __forceinline__ uint32_t h16(uint64_t x) { return (uint32_t)((x * 0xD6E8FEB86659FD93ull) >> 48); }
+// count one occurrence in a 2-bit saturating counter (01 = once, 11 = twice or more)
+__device__ __forceinline__ void bm_hit(uint32_t* bm, uint32_t h) {
+  const uint32_t bit = 1u << ((h & 15) * 2);
+  if (atomicOr(bm + (h >> 4), bit) & bit) atomicOr(bm + (h >> 4), bit << 1);
+}
+__device__ __forceinline__ bool bm_once(const uint32_t* bm, uint32_t h) {
+  return ((bm[h >> 4] >> ((h & 15) * 2)) & 3u) == 1u;
+}
 
-// Groups are statically round-robined over persistent CTAs. While group g is
-// hashed, thread 0 fetches plan[g + G]; after the barrier every thread issues the
-// loads of its next-group keys, which land while group g's results are written.
-__global__ void __launch_bounds__(kLocThreads, 3)
+struct LocSmem {
+  uint32_t bml[kBmWords];            // link-key hash counters
+  uint32_t bms[kBmWords];            // source hash counters
+  unsigned long long t1key[kLocT1];  // exact link table for colliding keys: key + 1 (0 = empty)
+  uint32_t t1cnt[kLocT1];
+  uint32_t t2key[kLocT2];  // exact source table: src + 1 (0 = empty)
+  uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
+  uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
+  uint4 plan[2];                           // current / next group (by iteration parity)
+};
+
+// Per group (<= 2048 light keys, 4 per thread, in registers):
+//   1. every key counts its key-hash and source-hash in two 2-bit saturating
+//      counter arrays (two shared atomics, no probing);
+//   2. a key whose key-hash counter reads "once" is a unique link of count 1; a
+//      key whose source-hash counter reads "once" is a source with one packet and
+//      one link. Only the others go through exact hash tables (linear probing);
+//   3. every key writes its own column slot: (dst, count) for the first copy of a
+//      link, a hole (count 0) for later copies; table creators report and clear.
+// Groups are statically round-robined over persistent CTAs; thread 0 fetches the
+// next group's plan during the counting and every thread loads its next keys
+// into registers while the current group's results are written.
+__global__ void __launch_bounds__(kLocThreads, 2)
     local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
                       uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt,
                       unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kBmWords; i += kLocThreads) s.bml[i] = s.bms[i] = 0;
   for (int i = tid; i < kLocT1; i += kLocThreads) {
     s.t1key[i] = 0;
     s.t1cnt[i] = 0;
@@ -372,11 +388,10 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     s.t2key[i] = 0;
     s.t2pf[i] = 0;
   }
-  if (tid < 2) {
-    s.sp_link[tid] = s.sp_src_pk[tid] = s.sp_src_fo[tid] = 0;
-    s.nl[tid] = s.ns[tid] = 0;
+  if (tid == 0) {
+    s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+    if (blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   }
-  if (tid == 0 && blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   __syncthreads();
   const uint64_t dmask = (1ull << b) - 1;
   uint64_t kr[kLocPerThread];
@@ -399,12 +414,49 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     const uint32_t cur = it & 1;
     const uint32_t gn = g + gridDim.x;
     uint4 pnext = make_uint4(0, 0, 0, 0);
-    if (tid == 0 && gn < ngroups) pnext = plan[gn];  // in flight during the inserts
-    for (uint32_t r = 0; r < nmine; ++r) {
+    if (tid == 0 && gn < ngroups) pnext = plan[gn];
+    // 1. hash counters
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) {
+      if ((uint32_t)r < nmine) {
+        bm_hit(s.bml, h16(kr[r]));
+        bm_hit(s.bms, h16(kr[r] >> b));
+      }
+    }
+    if (tid == 0) s.plan[cur ^ 1] = pnext;
+    __syncthreads();
+    // next group's keys: issue the loads now, they land during phases 2-3
+    const uint4 p = s.plan[cur];
+    const uint4 pn = s.plan[cur ^ 1];
+    uint64_t kn[kLocPerThread];
+    uint32_t nnext = 0;
+    if (gn < ngroups) {
+      const uint32_t nl2 = light_count(pn);
+#pragma unroll
+      for (int r = 0; r < kLocPerThread; ++r) {
+        const uint32_t j = tid + r * kLocThreads;
+        if (j < nl2) {
+          kn[r] = keys[light_index(pn, j)];
+          ++nnext;
+        }
+      }
+    }
+    // 2. classify; exact tables for colliding keys only
+    uint32_t st[kLocPerThread];   // bit0 fast link, bit1 fresh (table creator), bit2 fast source, bit3 source creator
+    uint32_t hl[kLocPerThread], hs[kLocPerThread];
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) {
+      st[r] = 0;
+      if ((uint32_t)r >= nmine) continue;
       const uint64_t key = kr[r];
+      const uint32_t src = (uint32_t)(key >> b);
       bool fresh;
       if (key == ~0ull) {
-        fresh = atomicAdd(&s.sp_link[cur], 1u) == 0;
+        fresh = atomicAdd(&s.sp_link, 1u) == 0;
+        if (fresh) st[r] |= 2;
+      } else if (bm_once(s.bml, h16(key))) {
+        fresh = true;
+        st[r] |= 1;
       } else {
         const unsigned long long kk = key + 1;
         uint32_t h = hslot(kk, kLocT1);
@@ -414,8 +466,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
             c0 = atomicCAS(&s.t1key[h], 0ull, kk);
             if (c0 == 0) {
               atomicAdd(&s.t1cnt[h], 1u);
-              s.list1[atomicAdd(&s.nl[cur], 1u)] = (uint16_t)h;
               fresh = true;
+              st[r] |= 2;
               break;
             }
           }
@@ -426,11 +478,13 @@ __global__ void __launch_bounds__(kLocThreads, 3)
           }
           h = h + 1 == kLocT1 ? 0 : h + 1;
         }
+        hl[r] = h;
       }
-      const uint32_t src = (uint32_t)(key >> b);
       if (src == 0xFFFFFFFFu) {
-        atomicAdd(&s.sp_src_pk[cur], 1u);
-        if (fresh) atomicAdd(&s.sp_src_fo[cur], 1u);
+        atomicAdd(&s.sp_src_pk, 1u);
+        if (fresh) atomicAdd(&s.sp_src_fo, 1u);
+      } else if (bm_once(s.bms, h16(src))) {
+        st[r] |= 4;
       } else {
         const uint32_t sk = src + 1;
         uint32_t h = hslot(sk, kLocT2);
@@ -439,7 +493,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
           if (c0 == 0) {
             c0 = atomicCAS(&s.t2key[h], 0u, sk);
             if (c0 == 0) {
-              s.list2[atomicAdd(&s.ns[cur], 1u)] = (uint16_t)h;
+              st[r] |= 8;
               c0 = sk;
             }
           }
@@ -449,72 +503,60 @@ __global__ void __launch_bounds__(kLocThreads, 3)
           }
           h = h + 1 == kLocT2 ? 0 : h + 1;
         }
+        hs[r] = h;
       }
     }
-    if (tid == 0) s.plan[cur ^ 1] = pnext;
     __syncthreads();
-    // prefetch the next group's keys (registers), then write this group's results
-    const uint4 p = s.plan[cur];
-    const uint4 pn = s.plan[cur ^ 1];
-    nmine = 0;
-    if (gn < ngroups) {
-      const uint32_t nl2 = light_count(pn);
+    // 3. results: one column slot per key, creators report and clear
 #pragma unroll
-      for (int r = 0; r < kLocPerThread; ++r) {
-        const uint32_t j = tid + r * kLocThreads;
-        if (j < nl2) {
-          kr[r] = keys[light_index(pn, j)];
-          ++nmine;
+    for (int r = 0; r < kLocPerThread; ++r) {
+      if ((uint32_t)r >= nmine) continue;
+      const uint64_t key = kr[r];
+      const uint32_t pos = light_index(p, tid + r * kLocThreads);
+      uint32_t c = 0;
+      if (st[r] & 1) {
+        c = 1;
+      } else if (st[r] & 2) {
+        if (key == ~0ull) {
+          c = s.sp_link;
+        } else {
+          c = s.t1cnt[hl[r]];
+          s.t1key[hl[r]] = 0;
+          s.t1cnt[hl[r]] = 0;
         }
       }
-    }
-    if (tid == 0) {  // the other parity was last read before the previous barrier
-      s.nl[cur ^ 1] = s.ns[cur ^ 1] = 0;
-      s.sp_link[cur ^ 1] = s.sp_src_pk[cur ^ 1] = s.sp_src_fo[cur ^ 1] = 0;
-    }
-    const uint32_t nl = s.nl[cur], ns = s.ns[cur], sp = s.sp_link[cur];
-    for (uint32_t j = tid; j < nl; j += kLocThreads) {  // links -> (dst, count) column entries
-      const uint32_t h = s.list1[j];
-      const uint64_t key = s.t1key[h] - 1;
-      const uint32_t c = s.t1cnt[h];
-      const uint32_t pos = light_index(p, j);
       col_dst[pos] = (uint32_t)(key & dmask);
       col_cnt[pos] = c;
-      a_links += 1;
-      a_valid += c;
-      a_mlink = max(a_mlink, (unsigned long long)c);
-      s.t1key[h] = 0;
-      s.t1cnt[h] = 0;
-    }
-    uint32_t used = nl;
-    if (sp) {
-      if (tid == 0) {
-        const uint32_t pos = light_index(p, nl);
-        col_dst[pos] = (uint32_t)dmask;
-        col_cnt[pos] = sp;
+      if (c) {
         a_links += 1;
-        a_valid += sp;
-        a_mlink = max(a_mlink, (unsigned long long)sp);
+        a_valid += c;
+        a_mlink = max(a_mlink, (unsigned long long)c);
       }
-      used += 1;
+      if (st[r] & 4) {
+        a_srcs += 1;
+        a_msrc = max(a_msrc, 1ull);
+        a_mfan = max(a_mfan, 1ull);
+      } else if (st[r] & 8) {
+        const uint32_t pf = s.t2pf[hs[r]];
+        a_srcs += 1;
+        a_msrc = max(a_msrc, (unsigned long long)(pf & 0xFFFFu));
+        a_mfan = max(a_mfan, (unsigned long long)(pf >> 16));
+        s.t2key[hs[r]] = 0;
+        s.t2pf[hs[r]] = 0;
+      }
+      s.bml[h16(key) >> 4] = 0;  // benign: every writer stores 0
+      s.bms[h16(key >> b) >> 4] = 0;
     }
-    const uint32_t nlight = light_count(p);
-    for (uint32_t j = used + tid; j < nlight; j += kLocThreads) col_cnt[light_index(p, j)] = 0;  // holes
-    for (uint32_t j = tid; j < ns; j += kLocThreads) {
-      const uint32_t h = s.list2[j];
-      const uint32_t pf = s.t2pf[h];
+    if (tid == 0 && s.sp_src_pk) {
       a_srcs += 1;
-      a_msrc = max(a_msrc, (unsigned long long)(pf & 0xFFFFu));
-      a_mfan = max(a_mfan, (unsigned long long)(pf >> 16));
-      s.t2key[h] = 0;
-      s.t2pf[h] = 0;
-    }
-    if (tid == 0 && s.sp_src_pk[cur]) {
-      a_srcs += 1;
-      a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk[cur]);
-      a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo[cur]);
+      a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk);
+      a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo);
     }
     __syncthreads();
+    if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;  // not touched before the next barrier
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) kr[r] = kn[r];
+    nmine = nnext;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -618,29 +660,30 @@ __global__ void __launch_bounds__(256) hist_concat_kernel(ColConcatSrc src, uint
 // ---------------------------------------------------------------------------
 constexpr int kLocCT = 3072;
 struct LocColSmem {
-  uint32_t key[kLocCT];           // dst + 1 (0 = empty)
+  uint32_t bm[kBmWords];          // destination hash counters
+  uint32_t key[kLocCT];           // exact table for colliding destinations: dst + 1 (0 = empty)
   unsigned long long ns[kLocCT];  // fan-in << 32 | packets
-  uint16_t list[kLocMaxKeys];
-  uint32_t nl[2];
-  unsigned long long sp[2];  // dst == 0xFFFFFFFF
+  unsigned long long sp;          // dst == 0xFFFFFFFF
   uint4 plan[2];
 };
 
-__global__ void __launch_bounds__(kLocThreads, 4)
+// Same three phases as local_rows_kernel over (dst, count) column entries: a
+// destination whose hash counter reads "once" has fan-in 1 and `count` packets.
+__global__ void __launch_bounds__(kLocThreads, 3)
     local_cols_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
                       const uint4* __restrict__ plan, uint32_t ngroups, unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kBmWords; i += kLocThreads) s.bm[i] = 0;
   for (int i = tid; i < kLocCT; i += kLocThreads) {
     s.key[i] = 0;
     s.ns[i] = 0;
   }
-  if (tid < 2) {
-    s.sp[tid] = 0;
-    s.nl[tid] = 0;
+  if (tid == 0) {
+    s.sp = 0;
+    if (blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   }
-  if (tid == 0 && blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   __syncthreads();
   uint32_t kr[kLocPerThread], vr[kLocPerThread];
   uint32_t nmine = 0;
@@ -665,35 +708,14 @@ __global__ void __launch_bounds__(kLocThreads, 4)
     const uint32_t gn = g + gridDim.x;
     uint4 pnext = make_uint4(0, 0, 0, 0);
     if (tid == 0 && gn < ngroups) pnext = plan[gn];
-    for (uint32_t r = 0; r < nmine; ++r) {
-      const uint32_t d = kr[r];
-      const unsigned long long add = (1ull << 32) | vr[r];
-      if (d == 0xFFFFFFFFu) {
-        atomicAdd(&s.sp[cur], add);
-        continue;
-      }
-      const uint32_t dk = d + 1;
-      uint32_t h = hslot(dk, kLocCT);
-      for (;;) {
-        uint32_t c0 = s.key[h];
-        if (c0 == 0) {
-          c0 = atomicCAS(&s.key[h], 0u, dk);
-          if (c0 == 0) {
-            s.list[atomicAdd(&s.nl[cur], 1u)] = (uint16_t)h;
-            c0 = dk;
-          }
-        }
-        if (c0 == dk) {
-          atomicAdd(&s.ns[h], add);
-          break;
-        }
-        h = h + 1 == kLocCT ? 0 : h + 1;
-      }
-    }
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r)
+      if ((uint32_t)r < nmine) bm_hit(s.bm, h16(kr[r]));
     if (tid == 0) s.plan[cur ^ 1] = pnext;
     __syncthreads();
     const uint4 pn = s.plan[cur ^ 1];
-    nmine = 0;
+    uint32_t kn[kLocPerThread], vn[kLocPerThread];
+    uint32_t nnext = 0;
     if (gn < ngroups) {
       const uint32_t nl2 = light_count(pn);
 #pragma unroll
@@ -701,32 +723,75 @@ __global__ void __launch_bounds__(kLocThreads, 4)
         const uint32_t j = tid + r * kLocThreads;
         if (j < nl2) {
           const uint32_t i = light_index(pn, j);
-          kr[r] = ck[i];
-          vr[r] = cv[i];
-          ++nmine;
+          kn[r] = ck[i];
+          vn[r] = cv[i];
+          ++nnext;
         }
       }
     }
-    if (tid == 0) {
-      s.nl[cur ^ 1] = 0;
-      s.sp[cur ^ 1] = 0;
-    }
-    const uint32_t nl = s.nl[cur];
-    for (uint32_t j = tid; j < nl; j += kLocThreads) {
-      const uint32_t h = s.list[j];
-      const unsigned long long v = s.ns[h];
-      a_cnt += 1;
-      a_fanin = max(a_fanin, v >> 32);
-      a_pk = max(a_pk, v & 0xFFFFFFFFull);
-      s.key[h] = 0;
-      s.ns[h] = 0;
-    }
-    if (tid == 0 && s.sp[cur]) {
-      a_cnt += 1;
-      a_fanin = max(a_fanin, s.sp[cur] >> 32);
-      a_pk = max(a_pk, s.sp[cur] & 0xFFFFFFFFull);
+    uint32_t hh[kLocPerThread];
+    uint32_t stc = 0;  // bit r: fast, bit r+4: table creator
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) {
+      if ((uint32_t)r >= nmine) continue;
+      const uint32_t d = kr[r];
+      const unsigned long long add = (1ull << 32) | vr[r];
+      if (d == 0xFFFFFFFFu) {
+        atomicAdd(&s.sp, add);
+      } else if (bm_once(s.bm, h16(d))) {
+        stc |= 1u << r;
+      } else {
+        const uint32_t dk = d + 1;
+        uint32_t h = hslot(dk, kLocCT);
+        for (;;) {
+          uint32_t c0 = s.key[h];
+          if (c0 == 0) {
+            c0 = atomicCAS(&s.key[h], 0u, dk);
+            if (c0 == 0) {
+              stc |= 16u << r;
+              c0 = dk;
+            }
+          }
+          if (c0 == dk) {
+            atomicAdd(&s.ns[h], add);
+            break;
+          }
+          h = h + 1 == kLocCT ? 0 : h + 1;
+        }
+        hh[r] = h;
+      }
     }
     __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) {
+      if ((uint32_t)r >= nmine) continue;
+      if (stc & (1u << r)) {
+        a_cnt += 1;
+        a_fanin = max(a_fanin, 1ull);
+        a_pk = max(a_pk, (unsigned long long)vr[r]);
+      } else if (stc & (16u << r)) {
+        const unsigned long long v = s.ns[hh[r]];
+        a_cnt += 1;
+        a_fanin = max(a_fanin, v >> 32);
+        a_pk = max(a_pk, v & 0xFFFFFFFFull);
+        s.key[hh[r]] = 0;
+        s.ns[hh[r]] = 0;
+      }
+      s.bm[h16(kr[r]) >> 4] = 0;
+    }
+    if (tid == 0 && s.sp) {
+      a_cnt += 1;
+      a_fanin = max(a_fanin, s.sp >> 32);
+      a_pk = max(a_pk, s.sp & 0xFFFFFFFFull);
+    }
+    __syncthreads();
+    if (tid == 0) s.sp = 0;
+#pragma unroll
+    for (int r = 0; r < kLocPerThread; ++r) {
+      kr[r] = kn[r];
+      vr[r] = vn[r];
+    }
+    nmine = nnext;
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
