@@ -490,9 +490,14 @@ std::pair<uint32_t*, uint32_t*> sort_u32_pairs(nmx_ctx* c, uint32_t* k, uint32_t
 // Two-level non-stable MSD partition of the valid items of `src` (kb-bit keys)
 // by their top D bits. Leaves bucket offsets in c->moff (2^D + 1 entries) and
 // returns the partitioned keys / values and the number of valid items.
+int msd_first_bits(int D) {
+  const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
+  return D / L + (0 < D % L ? 1 : 0);
+}
+
 template <typename Src, typename KeyT, bool HAS_VAL>
 uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, KeyT* outA, uint32_t* voutA,
-                       KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v) {
+                       KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v, bool prehist = false) {
   // levels of <= kMsdLevelBits bits: 128 bins per tile keeps the reservation
   // atomics at one per 32 keys and every digit's run in a tile ~32 keys long
   const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
@@ -505,11 +510,13 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   const uint32_t nb = 1u << D;
   uint32_t* d_small = c->small.as<uint32_t>();
   auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
-  CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
-  CK(cudaMemsetAsync(gcount, 0, 8, c->st));
-  const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
-  msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - dl[0], d_small + kHist, gcount);
-  CK_LAUNCH();
+  if (!prehist) {  // else small[kHist] / gcount were filled by the producer of `src`
+    CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
+    CK(cudaMemsetAsync(gcount, 0, 8, c->st));
+    const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
+    msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - dl[0], d_small + kHist, gcount);
+    CK_LAUNCH();
+  }
   c->mcur.grow(((size_t)nb + 8) * 4);
   c->moff.grow(((size_t)nb + 8) * 4);
   c->mhist2.grow(((size_t)nb + 8) * 4);
@@ -637,10 +644,15 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   uint32_t* off = c->moff.as<uint32_t>();
   uint32_t ngroups = (uint32_t)((m + S - 1) / S);
   plan_groups(c, off, nb, m, S, capb);
+  const int Dc = std::min(D, b);
+  const int cshift = b - msd_first_bits(Dc);
+  auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
+  CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
+  CK(cudaMemsetAsync(gcount, 0, 8, c->st));
   set_smem(local_rows_kernel, sizeof(LocSmem));
   local_rows_kernel<<<(unsigned)(c->sms * 2), kLocThreads, sizeof(LocSmem), c->st>>>(
-      keys, c->mplan.as<uint4>(), ngroups, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
-      c->stats.as<unsigned long long>());
+      keys, c->mplan.as<uint4>(), ngroups, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), cshift,
+      d_small + kHist, gcount, c->stats.as<unsigned long long>());
   CK_LAUNCH();
   ++c->launches;
   c->mark();  // 3: local rows end
@@ -661,6 +673,13 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     CK(cudaMemcpyAsync(c->h_small + kU, d_small + kU, 4, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     uh = c->h_small[kU];
+    if (uh) {  // their share of the column partition's first-level histogram
+      KeySrc<uint32_t, true> hk{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh};
+      const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uh + 2047) / 2048, (uint64_t)c->sms * 8));
+      msd_hist1_kernel<KeySrc<uint32_t, true>, uint32_t><<<hgrid, 256, 0, c->st>>>(hk, uh, cshift, d_small + kHist,
+                                                                                   gcount);
+      CK_LAUNCH();
+    }
   }
   c->mark();  // 4: heavy rows end
 
@@ -668,12 +687,11 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), m,
                   c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh, m + uh};
   cs.quad = true;  // context buffers are cudaMalloc-aligned
-  const int Dc = std::min(D, b);
   uint32_t* ck = nullptr;
   uint32_t* cv = nullptr;
   const uint64_t u = msd_partition<ColConcatSrc, uint32_t, true>(c, cs, m + uh, b, Dc, c->ckB.as<uint32_t>(),
                                                                  c->cvB.as<uint32_t>(), c->ckA.as<uint32_t>(),
-                                                                 c->cvA.as<uint32_t>(), &ck, &cv);
+                                                                 c->cvA.as<uint32_t>(), &ck, &cv, true);
   c->mark();  // 5: column partition end
   const uint32_t nbc = 1u << Dc;
   ngroups = (uint32_t)((u + S - 1) / S);

@@ -63,6 +63,12 @@ __device__ __forceinline__ void quad_items(const PacketSrc& s, uint64_t q, uint6
   s.load_quad(q, k, ok);
   v[0] = v[1] = v[2] = v[3] = 0;
 }
+template <typename KeyT, bool HAS_VAL>
+__device__ __forceinline__ void quad_items(const KeySrc<KeyT, HAS_VAL>& s, uint64_t q, KeyT* k, uint32_t* v,
+                                           bool* ok) {
+#pragma unroll
+  for (int t = 0; t < 4; ++t) ok[t] = s.load(4 * q + t, k[t], v[t]);
+}
 struct ColConcatSrc;
 __device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok);
 template <typename Src, typename KeyT>
@@ -143,18 +149,27 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
   for (int i = 0; i < kMsdIPT; ++i)
     if (bin[i] >= 0) rank[i] = atomicAdd(&S.cnt[bin[i]], 1u);
   __syncthreads();
+  // reserve each digit's output range first: the global atomics are in flight
+  // while the block scan and the staging run
+  uint32_t resv[kMsdMaxBins / kMsdThreads];
+#pragma unroll
+  for (int q = 0; q < kMsdMaxBins / kMsdThreads; ++q) {
+    const int i = tid + q * kMsdThreads;
+    resv[q] = 0;
+    if (i < nbins) {
+      const uint32_t c = S.cnt[i];
+      if (c) {
+        const uint32_t g = LEVEL == 1
+                               ? (uint32_t)i
+                               : (uint32_t)(((b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask));
+        resv[q] = atomicAdd(cursor + g, c);
+      }
+    }
+  }
   if (nbins <= kMsdThreads)
     smem_excl_scan<kMsdThreads>(S.cnt, S.tstart, S.wt);
   else
     smem_excl_scan<kMsdMaxBins>(S.cnt, S.tstart, S.wt);
-  for (int i = tid; i < nbins; i += kMsdThreads) {  // reserve each digit's output range
-    const uint32_t c = S.cnt[i];
-    if (c) {
-      const uint32_t g = LEVEL == 1 ? (uint32_t)i
-                                    : (uint32_t)(((b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask));
-      S.gbase[i] = atomicAdd(cursor + g, c) - S.tstart[i];
-    }
-  }
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i)
     if (bin[i] >= 0) {
@@ -162,6 +177,11 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
       S.stage[at] = k[i];
       if (HAS_VAL) S.vstage[at] = v[i];
     }
+#pragma unroll
+  for (int q = 0; q < kMsdMaxBins / kMsdThreads; ++q) {
+    const int i = tid + q * kMsdThreads;
+    if (i < nbins && S.cnt[i]) S.gbase[i] = resv[q] - S.tstart[i];
+  }
   __syncthreads();
   const uint32_t total = S.tstart[nbins - 1] + S.cnt[nbins - 1];
   for (uint32_t j = tid; j < total; j += kMsdThreads) {
@@ -359,6 +379,7 @@ struct LocSmem {
   uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
   uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
   uint4 plan[2];                           // current / next group (by iteration parity)
+  uint32_t chist[1 << kMsdLevelBits];      // first-level histogram of the emitted column entries
 };
 
 // Per group (<= 2048 light keys, 4 per thread, in registers):
@@ -374,12 +395,14 @@ struct LocSmem {
 // into registers while the current group's results are written.
 __global__ void __launch_bounds__(kLocThreads, 2)
     local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
-                      uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt,
+                      uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt, int cshift,
+                      uint32_t* __restrict__ chist, unsigned long long* __restrict__ ccount,
                       unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kBmWords; i += kLocThreads) s.bml[i] = s.bms[i] = 0;
+  if (tid < (1 << kMsdLevelBits)) s.chist[tid] = 0;
   for (int i = tid; i < kLocT1; i += kLocThreads) {
     s.t1key[i] = 0;
     s.t1cnt[i] = 0;
@@ -528,6 +551,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       col_dst[pos] = (uint32_t)(key & dmask);
       col_cnt[pos] = c;
       if (c) {
+        atomicAdd(&s.chist[(uint32_t)(key & dmask) >> cshift], 1u);  // the column partition's first level
         a_links += 1;
         a_valid += c;
         a_mlink = max(a_mlink, (unsigned long long)c);
@@ -568,6 +592,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     a_mfan = max(a_mfan, __shfl_xor_sync(FULL, a_mfan, o));
   }
   if (lane == 0) {
+    if (a_links) atomicAdd(ccount, a_links);
     if (a_valid) atomicAdd(stats + S_VALID, a_valid);
     if (a_links) atomicAdd(stats + S_LINKS, a_links);
     if (a_srcs) atomicAdd(stats + S_SRCS, a_srcs);
@@ -575,6 +600,8 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     if (a_msrc) atomicMax(stats + S_MAXSRCPK, a_msrc);
     if (a_mfan) atomicMax(stats + S_MAXFANOUT, a_mfan);
   }
+  __syncthreads();
+  if (tid < (1 << kMsdLevelBits) && s.chist[tid]) atomicAdd(chist + tid, s.chist[tid]);
 }
 
 // gather heavy bucket ranges into one contiguous array
