@@ -44,6 +44,21 @@ CONFIGS = {
 }
 
 
+def _traffic(kernel: str, bytes_per_launch: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu
+    capture (profiles/traffic_latest.json, tools/ncu_traffic.py), scaled from the
+    captured size to this launch's size by the per-item ratio; None if absent."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic_latest.json").read_text())
+    except Exception:
+        return None
+    ks = [v for k, v in t["kernels"].items() if kernel and kernel in k]
+    if not ks:
+        return None
+    per_item = sum(v["dram_bytes"] for v in ks) / sum(v["launches"] for v in ks) / t["items_per_launch"]
+    return round(per_item * bytes_per_launch / 16)
+
+
 def _peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
@@ -201,15 +216,16 @@ def run_nmx(args) -> None:
 
     # ---- device-resident timed region (value) ----
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sort_ms, sort_launch, launches, totals = 0.0, 0, 0, []
+    dom_ms, dom_launch, dom_bytes, launches, totals = 0.0, 0, 0, 0, []
     barrier()
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             stats = step()
             t = ctx.last_timing()
-            sort_ms += t["sort_ms"]
-            sort_launch += t["sort_launches"]
+            dom_ms += t["dom_ms"]
+            dom_launch += t["dom_launches"]
+            dom_bytes += t["dom_bytes"]
             launches += t["kernel_launches"]
             totals.append(t)
         e1.record(stream)
@@ -263,16 +279,19 @@ def run_nmx(args) -> None:
         return
 
     peaks, peak_kind = _peaks()
-    # dominant kernel: the onesweep LSD pass (16 B of key traffic per packet per launch)
-    pass_ms = sort_ms / max(sort_launch, 1)
-    bytes_per_launch = 16 * n
-    achieved = bytes_per_launch / (pass_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "kernel": "onesweep_pass (row sort, u64 keys)", "achieved": round(achieved, 1),
+    # dominant kernel class (MSD partition scatter; onesweep pass on the LSD path):
+    # 8 B in + 8 B out per item per launch, timed by CUDA events around every launch
+    pass_ms = dom_ms / max(dom_launch, 1)
+    bytes_per_launch = dom_bytes // max(dom_launch, 1)
+    achieved = bytes_per_launch / (pass_ms / 1e3) / 1e9 if pass_ms else 0.0
+    roof = {"bound": "hbm", "kernel": timing_last.get("dom_name", ""), "achieved": round(achieved, 1),
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-            "peak_kind": peak_kind, "traffic": None,
+            "peak_kind": peak_kind, "traffic": _traffic(timing_last.get("dom_name", ""), bytes_per_launch),
+            "launches_per_step": dom_launch // max(args.steps, 1),
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(pass_ms, 4),
-            "note": "algorithmic bytes = 8 B read + 8 B write per key per pass (SURVEY.md 8(d)); traffic: see "
-                    "profiles/ (ncu dram__bytes per launch)"}
+            "share_of_step": round(dom_ms / ms, 4) if ms else None,
+            "note": "algorithmic bytes = 8 B read + 8 B write per item per launch; traffic per launch from ncu "
+                    "dram__bytes in profiles/"}
     # whole-step algorithmic bytes: n(16+16P) + u(36+16Pc), P = 2*ceil(b/8), Pc = ceil(b/8)
     b = 32 if space == 1 << 32 else max(1, (space - 1).bit_length())
     P, Pc = 2 * ((b + 7) // 8), (b + 7) // 8
@@ -301,7 +320,10 @@ def run_nmx(args) -> None:
         "roofline": roof,
         "whole_step": {"b_alg_bytes": b_alg, "achieved_gbs": round(whole, 1),
                        "frac": round(whole / peaks["hbm_gbs"], 4), "stages_ms": stage_ms,
-                       "stages": ["hist+plan", "row sort", "link/row", "col sort", "col+d2h"]},
+                       "stages": (["setup", "row partition", "row groups (smem)", "heavy rows", "column partition",
+                                   "column groups (smem)", "heavy columns + d2h"]
+                                  if timing_last.get("dom_name") == "msd_scatter" else
+                                  ["hist+plan", "row sort", "link/row", "col sort", "col+d2h"])},
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),

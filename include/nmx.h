@@ -144,6 +144,10 @@ int nmx_last_timing(nmx_ctx* ctx, float* total_ms, float* sort_ms, int* sort_lau
  * (+ host pass planning), [1] row sort (onesweep passes), [2] fused link/row
  * kernel, [3] column sort, [4] column kernel + result copy. Returns the count. */
 int nmx_last_stages(nmx_ctx* ctx, float* ms, int cap);
+/* The dominant kernel class of the last hot-path call (the MSD partition scatter,
+ * or the onesweep pass on the LSD path): summed CUDA-event time of its launches,
+ * launch count, algorithmic bytes (8 B in + 8 B out per item per launch) and name. */
+int nmx_last_kernel_class(nmx_ctx* ctx, float* ms, int* launches, uint64_t* bytes, char* name, int name_cap);
 
 #ifdef __cplusplus
 }

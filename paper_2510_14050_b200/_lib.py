@@ -58,6 +58,8 @@ SIGNATURES = {
     "nmx_partition_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.c_int, _VP, _VP, _VP]),
     "nmx_shard_rows": (C.c_int, [_VP, _VP, _VP, _U64, _U64, C.c_int, _VP, _VP, _VP, _VP]),
     "nmx_shard_cols": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_last_kernel_class": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_int), C.POINTER(_U64), C.c_char_p,
+                                         C.c_int]),
     "nmx_last_stages": (C.c_int, [_VP, C.POINTER(C.c_float), C.c_int]),
     "nmx_last_timing": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_int),
                                   C.POINTER(C.c_int)]),
@@ -142,8 +144,12 @@ class Context:
         check(self._lib.nmx_last_timing(self._h, C.byref(t), C.byref(s), C.byref(sl), C.byref(kl)))
         st = (C.c_float * 8)()
         k = self._lib.nmx_last_stages(self._h, st, 8)
+        dms, dl, db = C.c_float(), C.c_int(), C.c_uint64()
+        name = C.create_string_buffer(64)
+        check(self._lib.nmx_last_kernel_class(self._h, C.byref(dms), C.byref(dl), C.byref(db), name, 64))
         return dict(total_ms=t.value, sort_ms=s.value, sort_launches=sl.value, kernel_launches=kl.value,
-                    stages_ms=[round(st[i], 4) for i in range(max(k, 0))])
+                    stages_ms=[round(st[i], 4) for i in range(max(k, 0))],
+                    dom_ms=dms.value, dom_launches=dl.value, dom_bytes=db.value, dom_name=name.value.decode())
 
 
 _contexts: dict[int, Context] = {}

@@ -105,7 +105,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
+  DevBuf mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
@@ -144,6 +144,27 @@ struct nmx_ctx {
     h_stats_cap = words;
   }
   void mark() { CK(cudaEventRecord(ev[nev++], st)); }
+  // dominant-kernel accounting (event pairs around each launch of the class)
+  cudaEvent_t evk[64];
+  int nevk = 0;
+  uint64_t dom_bytes = 0;
+  float dom_ms = 0;
+  int dom_launches = 0;
+  const char* dom_name = "";
+  bool dom_cur = false;
+  // the first kernel class that reports in a call owns the accounting
+  void dom_begin(const char* nm) {
+    if (!dom_name[0]) dom_name = nm;
+    dom_cur = strcmp(dom_name, nm) == 0 && nevk + 2 <= 64;
+    if (dom_cur) CK(cudaEventRecord(evk[nevk], st));
+  }
+  void dom_end(uint64_t bytes) {
+    if (!dom_cur) return;
+    CK(cudaEventRecord(evk[nevk + 1], st));
+    nevk += 2;
+    dom_bytes += bytes;
+    ++dom_launches;
+  }
 };
 
 namespace {
@@ -170,9 +191,11 @@ void launch_pass_v(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32
   set_smem(kern, sizeof(S));
   const uint64_t t = tiles_of(items, THREADS * IPT);
   if (!t) return;
+  c->dom_begin("onesweep_pass");
   kern<<<(unsigned)t, THREADS, sizeof(S), c->st>>>(src, out, vout, shift, binbase, c->status.as<uint64_t>(),
                                                      c->next_epoch(), counter);
   CK_LAUNCH();
+  c->dom_end(items * 2 * (sizeof(KeyT) + (HAS_VAL ? 4 : 0)));
   ++c->launches;
 }
 
@@ -272,6 +295,11 @@ void launch_hist(nmx_ctx* c, const Src& ps, int npass, uint32_t* d_small) {
 // ---- pipeline stages -------------------------------------------------------
 void stage_begin(nmx_ctx* c, uint64_t W) {
   c->nev = 0;
+  c->nevk = 0;
+  c->dom_bytes = 0;
+  c->dom_ms = 0;
+  c->dom_launches = 0;
+  c->dom_name = "";
   c->launches = 0;
   c->last_sort_launches = 0;
   c->last_sort_ms = 0;
@@ -295,6 +323,12 @@ void stage_finish(nmx_ctx* c, uint64_t W) {
   for (int i = 0; i + 1 < c->nev && i < 8; ++i) CK(cudaEventElapsedTime(&c->last_stage_ms[i], c->ev[i], c->ev[i + 1]));
   c->last_nstage = std::min(c->nev - 1, 8);
   c->last_launches = c->launches;
+  c->dom_ms = 0;
+  for (int i = 0; i + 1 < c->nevk; i += 2) {
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, c->evk[i], c->evk[i + 1]));
+    c->dom_ms += t;
+  }
 }
 
 struct RowsOut {
@@ -497,7 +531,8 @@ int msd_first_bits(int D) {
 
 template <typename Src, typename KeyT, bool HAS_VAL>
 uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, KeyT* outA, uint32_t* voutA,
-                       KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v, bool prehist = false) {
+                       KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v,
+                       const uint32_t* prehist = nullptr) {
   // levels of <= kMsdLevelBits bits: 128 bins per tile keeps the reservation
   // atomics at one per 32 keys and every digit's run in a tile ~32 keys long
   const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
@@ -510,7 +545,10 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   const uint32_t nb = 1u << D;
   uint32_t* d_small = c->small.as<uint32_t>();
   auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
-  if (!prehist) {  // else small[kHist] / gcount were filled by the producer of `src`
+  if (prehist) {  // first-level histogram (+ count) filled by the producer of `src`
+    CK(cudaMemcpyAsync(d_small + kHist, prehist, sizeof(uint32_t) * kMsdMaxBins, cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(gcount, prehist + kMsdMaxBins, 8, cudaMemcpyDeviceToDevice, c->st));
+  } else {
     CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
     CK(cudaMemsetAsync(gcount, 0, 8, c->st));
     const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
@@ -532,10 +570,13 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   *res_v = voutA;
   if (!m) return 0;
   using S1 = MsdSmem<KeyT, HAS_VAL>;
+  constexpr uint64_t kItem = sizeof(KeyT) + (HAS_VAL ? 4 : 0);  // 8 B per item in and out
   set_smem(msd_scatter_kernel<Src, KeyT, HAS_VAL, 1>, sizeof(S1));
+  c->dom_begin("msd_scatter");
   msd_scatter_kernel<Src, KeyT, HAS_VAL, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
       src, n, outA, voutA, kb - dl[0], dl[0], 0, cur);
   CK_LAUNCH();
+  c->dom_end(2 * kItem * m);
   ++c->launches;
   KeyT* in_k = outA;
   uint32_t* in_v = voutA;
@@ -553,10 +594,12 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     CK_LAUNCH();
     KeySrc<KeyT, HAS_VAL> ks{in_k, in_v, m};
     set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>, sizeof(S1));
+    c->dom_begin("msd_scatter");
     msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>
         <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(ks, m, out_k, out_v, shift, dl[l],
                                                                                bshift, cur);
     CK_LAUNCH();
+    c->dom_end(2 * kItem * m);
     c->launches += 3;
     std::swap(in_k, out_k);
     std::swap(in_v, out_v);
@@ -646,13 +689,15 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   plan_groups(c, off, nb, m, S, capb);
   const int Dc = std::min(D, b);
   const int cshift = b - msd_first_bits(Dc);
-  auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
-  CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
-  CK(cudaMemsetAsync(gcount, 0, 8, c->st));
+  // the column partition's first-level histogram + entry count, produced by the row stages
+  c->mch.grow((kMsdMaxBins + 4) * 4);
+  uint32_t* chist = c->mch.as<uint32_t>();
+  auto* ccount = reinterpret_cast<unsigned long long*>(chist + kMsdMaxBins);
+  CK(cudaMemsetAsync(chist, 0, (kMsdMaxBins + 4) * 4, c->st));
   set_smem(local_rows_kernel, sizeof(LocSmem));
   local_rows_kernel<<<(unsigned)(c->sms * 2), kLocThreads, sizeof(LocSmem), c->st>>>(
       keys, c->mplan.as<uint4>(), ngroups, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), cshift,
-      d_small + kHist, gcount, c->stats.as<unsigned long long>());
+      chist, ccount, c->stats.as<unsigned long long>());
   CK_LAUNCH();
   ++c->launches;
   c->mark();  // 3: local rows end
@@ -676,8 +721,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     if (uh) {  // their share of the column partition's first-level histogram
       KeySrc<uint32_t, true> hk{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh};
       const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uh + 2047) / 2048, (uint64_t)c->sms * 8));
-      msd_hist1_kernel<KeySrc<uint32_t, true>, uint32_t><<<hgrid, 256, 0, c->st>>>(hk, uh, cshift, d_small + kHist,
-                                                                                   gcount);
+      msd_hist1_kernel<KeySrc<uint32_t, true>, uint32_t><<<hgrid, 256, 0, c->st>>>(hk, uh, cshift, chist, ccount);
       CK_LAUNCH();
     }
   }
@@ -691,7 +735,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   uint32_t* cv = nullptr;
   const uint64_t u = msd_partition<ColConcatSrc, uint32_t, true>(c, cs, m + uh, b, Dc, c->ckB.as<uint32_t>(),
                                                                  c->cvB.as<uint32_t>(), c->ckA.as<uint32_t>(),
-                                                                 c->cvA.as<uint32_t>(), &ck, &cv, true);
+                                                                 c->cvA.as<uint32_t>(), &ck, &cv, chist);
   c->mark();  // 5: column partition end
   const uint32_t nbc = 1u << Dc;
   ngroups = (uint32_t)((u + S - 1) / S);
@@ -891,6 +935,7 @@ int nmx_create(int device, nmx_ctx** out) {
     c->sms = p.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    for (auto& e : c->evk) CK(cudaEventCreate(&e));
   } catch (const CudaError& e) {
     cudaGetLastError();
     delete c;
@@ -904,7 +949,7 @@ void nmx_destroy(nmx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (DevBuf* b : {&c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
+  for (DevBuf* b : {&c->mch, &c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
                     &c->mhist2, &c->mgb, &c->mheavy, &c->mdst, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
@@ -912,6 +957,7 @@ void nmx_destroy(nmx_ctx* c) {
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (auto& e : c->ev) cudaEventDestroy(e);
+  for (auto& e : c->evk) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -1286,6 +1332,15 @@ int nmx_flat_fetch(nmx_ctx* c, int64_t* edge_src, int64_t* row_ids, int64_t* row
     }
     return NMX_OK;
   });
+}
+
+int nmx_last_kernel_class(nmx_ctx* c, float* ms, int* launches, uint64_t* bytes, char* name, int name_cap) {
+  if (!c) return fail(NMX_EINVAL, "null context");
+  if (ms) *ms = c->dom_ms;
+  if (launches) *launches = c->dom_launches;
+  if (bytes) *bytes = c->dom_bytes;
+  if (name && name_cap > 0) snprintf(name, name_cap, "%s", c->dom_name);
+  return NMX_OK;
 }
 
 int nmx_last_stages(nmx_ctx* c, float* ms, int cap) {

@@ -20,11 +20,12 @@
 
 namespace nmx {
 
-constexpr int kMsdThreads = 512;
+constexpr int kMsdThreads = 256;
 constexpr int kMsdIPT = 8;
-constexpr int kMsdTile = kMsdThreads * kMsdIPT;  // 4096 keys
+constexpr int kMsdTile = kMsdThreads * kMsdIPT;  // 2048 keys per scatter tile
 constexpr int kMsdMaxBins = 2048;                // histogram bins of the first level (<= 2^11)
 constexpr int kMsdLevelBits = 7;                 // digit bits per partition level
+constexpr int kMsdScBins = 2 << kMsdLevelBits;   // scatter bins: a tile spans <= 2 parent buckets
 
 // block exclusive scan of NB counters held in smem (512 threads, NB % 512 == 0 or NB <= 512)
 template <int NB>
@@ -86,9 +87,9 @@ template <typename KeyT, bool HAS_VAL>
 struct MsdSmem {
   KeyT stage[kMsdTile];
   uint32_t vstage[HAS_VAL ? kMsdTile : 1];
-  uint32_t cnt[kMsdMaxBins];
-  uint32_t tstart[kMsdMaxBins];
-  uint32_t gbase[kMsdMaxBins];
+  uint32_t cnt[kMsdScBins];
+  uint32_t tstart[kMsdScBins];
+  uint32_t gbase[kMsdScBins];
   uint32_t wt[kMsdThreads / 32 + 1];
   uint64_t b1first;
 };
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
   auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbins = LEVEL == 1 ? (1 << dbits) : (2 << dbits);
-  for (int i = tid; i < kMsdMaxBins; i += kMsdThreads) S.cnt[i] = 0;
+  for (int i = tid; i < kMsdScBins; i += kMsdThreads) S.cnt[i] = 0;
   const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
   if (LEVEL == 2 && tid == 0) {
     KeyT k0 = 0;
@@ -151,9 +152,9 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
   __syncthreads();
   // reserve each digit's output range first: the global atomics are in flight
   // while the block scan and the staging run
-  uint32_t resv[kMsdMaxBins / kMsdThreads];
+  uint32_t resv[kMsdScBins / kMsdThreads];
 #pragma unroll
-  for (int q = 0; q < kMsdMaxBins / kMsdThreads; ++q) {
+  for (int q = 0; q < kMsdScBins / kMsdThreads; ++q) {
     const int i = tid + q * kMsdThreads;
     resv[q] = 0;
     if (i < nbins) {
@@ -166,10 +167,7 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
       }
     }
   }
-  if (nbins <= kMsdThreads)
-    smem_excl_scan<kMsdThreads>(S.cnt, S.tstart, S.wt);
-  else
-    smem_excl_scan<kMsdMaxBins>(S.cnt, S.tstart, S.wt);
+  smem_excl_scan<kMsdScBins>(S.cnt, S.tstart, S.wt);
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i)
     if (bin[i] >= 0) {
@@ -178,7 +176,7 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
       if (HAS_VAL) S.vstage[at] = v[i];
     }
 #pragma unroll
-  for (int q = 0; q < kMsdMaxBins / kMsdThreads; ++q) {
+  for (int q = 0; q < kMsdScBins / kMsdThreads; ++q) {
     const int i = tid + q * kMsdThreads;
     if (i < nbins && S.cnt[i]) S.gbase[i] = resv[q] - S.tstart[i];
   }
@@ -232,10 +230,10 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
 template <typename KeyT>
 __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __restrict__ keys, uint64_t m, int shift,
                                                                   int dbits, int bshift, uint32_t* __restrict__ hist2) {
-  __shared__ uint32_t cnt[kMsdMaxBins];
+  __shared__ uint32_t cnt[kMsdScBins];
   __shared__ uint64_t s_b1first;
   const int tid = threadIdx.x;
-  for (int i = tid; i < kMsdMaxBins; i += kMsdThreads) cnt[i] = 0;
+  for (int i = tid; i < kMsdScBins; i += kMsdThreads) cnt[i] = 0;
   const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
   KeyT k[kMsdIPT];
 #pragma unroll
