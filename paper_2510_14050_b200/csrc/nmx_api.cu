@@ -105,7 +105,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
-  DevBuf mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
+  DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red;
   uint32_t epoch = 0;
@@ -524,6 +524,20 @@ std::pair<uint32_t*, uint32_t*> sort_u32_pairs(nmx_ctx* c, uint32_t* k, uint32_t
 // Two-level non-stable MSD partition of the valid items of `src` (kb-bit keys)
 // by their top D bits. Leaves bucket offsets in c->moff (2^D + 1 entries) and
 // returns the partitioned keys / values and the number of valid items.
+// exclusive scan of n counters -> off[0..n] (off[n] = total) and cursor = off
+void scan_counts(nmx_ctx* c, const uint32_t* cnt, uint32_t n, uint32_t* off, uint32_t* cursor) {
+  const uint32_t nb = (n + kScanItems - 1) / kScanItems;
+  c->mscan.grow(((size_t)nb + 4) * 4);
+  uint32_t* bsum = c->mscan.as<uint32_t>();
+  scan_block_sums_kernel<<<nb, 256, 0, c->st>>>(cnt, n, bsum);
+  CK_LAUNCH();
+  scan_top_kernel<<<1, 1024, 0, c->st>>>(bsum, nb, bsum + nb);
+  CK_LAUNCH();
+  scan_apply_kernel<<<nb, 256, 0, c->st>>>(cnt, n, bsum, bsum + nb, off, cursor);
+  CK_LAUNCH();
+  c->launches += 3;
+}
+
 int msd_first_bits(int D) {
   const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
   return D / L + (0 < D % L ? 1 : 0);
@@ -560,8 +574,7 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   c->mhist2.grow(((size_t)nb + 8) * 4);
   uint32_t* cur = c->mcur.as<uint32_t>();
   uint32_t* off = c->moff.as<uint32_t>();
-  big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(d_small + kHist, 1u << dl[0], off, cur);
-  CK_LAUNCH();
+  scan_counts(c, d_small + kHist, 1u << dl[0], off, cur);
   unsigned long long m = 0;
   CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -590,8 +603,7 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(in_k, m, shift, dl[l], bshift,
                                                                                          h2);
     CK_LAUNCH();
-    big_excl_scan_kernel<<<1, 1024, 0, c->st>>>(h2, nbl, off, cur);
-    CK_LAUNCH();
+    scan_counts(c, h2, nbl, off, cur);
     KeySrc<KeyT, HAS_VAL> ks{in_k, in_v, m};
     set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>, sizeof(S1));
     c->dom_begin("msd_scatter");
@@ -707,8 +719,8 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   if (mh) {  // heavy row buckets: gather -> LSD sort -> fused link/row kernel
     c->keysC.grow(mh * 8);
     c->keysD.grow(mh * 8);
-    gather_ranges_kernel<<<(unsigned)std::min<uint32_t>(nheavy, c->sms * 8), 256, 0, c->st>>>(
-        keys, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, c->keysC.as<uint64_t>(),
+    gather_ranges_kernel<<<(unsigned)std::min<uint64_t>((mh + 255) / 256, (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+        keys, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, (uint32_t)mh, c->keysC.as<uint64_t>(),
         c->colL_cnt.as<uint32_t>());
     CK_LAUNCH();
     uint64_t* hs = sort_keys_u64(c, c->keysC.as<uint64_t>(), mh, kb, c->keysD.as<uint64_t>());
@@ -752,8 +764,8 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     c->cgv.grow(ch * 4);
     c->cgk2.grow(ch * 4);
     c->cgv2.grow(ch * 4);
-    gather_pairs_kernel<<<(unsigned)std::min<uint32_t>(nheavy, c->sms * 8), 256, 0, c->st>>>(
-        ck, cv, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, c->cgk.as<uint32_t>(),
+    gather_pairs_kernel<<<(unsigned)std::min<uint64_t>((ch + 255) / 256, (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+        ck, cv, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, (uint32_t)ch, c->cgk.as<uint32_t>(),
         c->cgv.as<uint32_t>());
     CK_LAUNCH();
     auto sorted = sort_u32_pairs(c, c->cgk.as<uint32_t>(), c->cgv.as<uint32_t>(), ch, b, c->cgk2.as<uint32_t>(),
@@ -949,7 +961,7 @@ void nmx_destroy(nmx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (DevBuf* b : {&c->mch, &c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
+  for (DevBuf* b : {&c->mscan, &c->mch, &c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
                     &c->mhist2, &c->mgb, &c->mheavy, &c->mdst, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})

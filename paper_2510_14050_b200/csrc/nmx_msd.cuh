@@ -293,6 +293,74 @@ __global__ void __launch_bounds__(1024) big_excl_scan_kernel(const uint32_t* __r
   if (tid == 0) off[nb] = wt[32];
 }
 
+// multi-CTA exclusive scan of n u32 counters (4096 per block, coalesced):
+// scan_block_sums -> scan_top (one CTA over the block sums) -> scan_apply
+constexpr int kScanItems = 4096;
+__global__ void __launch_bounds__(256) scan_block_sums_kernel(const uint32_t* __restrict__ cnt, uint32_t n,
+                                                             uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t wt[kWarps + 1];
+  const uint32_t base = blockIdx.x * kScanItems;
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems / 256; ++q) {
+    const uint32_t i = base + q * 256 + threadIdx.x;
+    s += i < n ? cnt[i] : 0u;
+  }
+  uint32_t tot;
+  block_excl_scan<uint32_t>(s, wt, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* __restrict__ bsum, uint32_t nb,
+                                                       uint32_t* __restrict__ total) {
+  __shared__ uint32_t wt[33];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nb; base += 1024) {
+    const uint32_t i = base + tid;
+    const uint32_t x = i < nb ? bsum[i] : 0u;
+    const uint32_t inc = warp_incl_scan(x, lane);
+    if (lane == 31) wt[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t v = wt[lane];
+      const uint32_t vi = warp_incl_scan(v, lane);
+      wt[lane] = vi - v;
+      if (lane == 31) wt[32] = vi;
+    }
+    __syncthreads();
+    if (i < nb) bsum[i] = carry + wt[warp] + inc - x;
+    carry += wt[32];
+    __syncthreads();
+  }
+  if (tid == 0) *total = carry;
+}
+__global__ void __launch_bounds__(256) scan_apply_kernel(const uint32_t* __restrict__ cnt, uint32_t n,
+                                                        const uint32_t* __restrict__ bexcl,
+                                                        const uint32_t* __restrict__ total, uint32_t* __restrict__ off,
+                                                        uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t wt[kWarps + 1];
+  constexpr int PER = kScanItems / 256;  // 16 consecutive counters per thread
+  const uint32_t base = blockIdx.x * kScanItems + threadIdx.x * PER;
+  uint32_t v[PER];
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    v[q] = base + q < n ? cnt[base + q] : 0u;
+    s += v[q];
+  }
+  uint32_t tot;
+  uint32_t run = bexcl[blockIdx.x] + block_excl_scan<uint32_t>(s, wt, &tot);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (base + q < n) {
+      off[base + q] = run;
+      if (cursor) cursor[base + q] = run;
+    }
+    run += v[q];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) off[n] = *total;
+}
+
 // group g covers the buckets whose start lies in [g*S, (g+1)*S)
 __global__ void group_bounds_kernel(const uint32_t* __restrict__ off, uint32_t nb, uint32_t S, uint32_t ngroups,
                                     uint32_t* __restrict__ gb) {
@@ -603,16 +671,27 @@ __global__ void __launch_bounds__(kLocThreads, 2)
 }
 
 // gather heavy bucket ranges into one contiguous array
-// (and turn their slots of the light column array into holes)
+// (and turn their slots of the light column array into holes). One thread per
+// gathered key: range r found by binary search over the destination offsets.
+__device__ __forceinline__ uint32_t range_of(const uint32_t* dstoff, uint32_t nranges, uint32_t t) {
+  uint32_t a = 0, z = nranges - 1;  // last r with dstoff[r] <= t
+  while (a < z) {
+    const uint32_t mid = (a + z + 1) >> 1;
+    if (dstoff[mid] <= t)
+      a = mid;
+    else
+      z = mid - 1;
+  }
+  return a;
+}
 __global__ void gather_ranges_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ranges,
-                                     const uint32_t* __restrict__ dstoff, uint32_t nranges,
+                                     const uint32_t* __restrict__ dstoff, uint32_t nranges, uint32_t total,
                                      uint64_t* __restrict__ out, uint32_t* __restrict__ col_cnt) {
-  for (uint32_t r = blockIdx.x; r < nranges; r += gridDim.x) {
-    const uint32_t lo = ranges[2 * r], hi = ranges[2 * r + 1], o = dstoff[r];
-    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      out[o + (i - lo)] = keys[i];
-      col_cnt[i] = 0;
-    }
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t r = range_of(dstoff, nranges, t);
+    const uint32_t i = ranges[2 * r] + (t - dstoff[r]);
+    out[t] = keys[i];
+    col_cnt[i] = 0;
   }
 }
 
@@ -834,13 +913,13 @@ __global__ void __launch_bounds__(kLocThreads, 3)
 // gather heavy (dst, count) ranges into contiguous arrays
 __global__ void gather_pairs_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
                                     const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ dstoff,
-                                    uint32_t nranges, uint32_t* __restrict__ ok, uint32_t* __restrict__ ov) {
-  for (uint32_t r = blockIdx.x; r < nranges; r += gridDim.x) {
-    const uint32_t lo = ranges[2 * r], hi = ranges[2 * r + 1], o = dstoff[r];
-    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      ok[o + (i - lo)] = ck[i];
-      ov[o + (i - lo)] = cv[i];
-    }
+                                    uint32_t nranges, uint32_t total, uint32_t* __restrict__ ok,
+                                    uint32_t* __restrict__ ov) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t r = range_of(dstoff, nranges, t);
+    const uint32_t i = ranges[2 * r] + (t - dstoff[r]);
+    ok[t] = ck[i];
+    ov[t] = cv[i];
   }
 }
 
