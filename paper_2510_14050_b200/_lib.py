@@ -55,6 +55,12 @@ SIGNATURES = {
     "nmx_coo_rowptr": (C.c_int, [_VP, _U64, _U64, _U64, _U64, _VP]),
     "nmx_flat_build": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _U64, C.POINTER(_U64), C.POINTER(_U64)]),
     "nmx_flat_fetch": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "nmx_coo_from_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.POINTER(_VP)]),
+    "nmx_coo_merge_add": (C.c_int, [_VP, _VP, _VP, C.POINTER(_VP)]),
+    "nmx_coo_stats9": (C.c_int, [_VP, _VP, _VP]),
+    "nmx_coo_nnz": (C.c_int, [_VP, C.POINTER(_U64)]),
+    "nmx_coo_download": (C.c_int, [_VP, _VP, _VP, _VP]),
+    "nmx_coo_free": (None, [_VP]),
     "nmx_partition_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.c_int, _VP, _VP, _VP]),
     "nmx_shard_rows": (C.c_int, [_VP, _VP, _VP, _U64, _U64, C.c_int, _VP, _VP, _VP, _VP]),
     "nmx_shard_cols": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),

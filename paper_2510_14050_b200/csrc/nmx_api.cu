@@ -167,6 +167,14 @@ struct nmx_ctx {
   }
 };
 
+// device-resident sorted unique COO: keys (src<<32)|dst, u32 counts
+struct nmx_coo {
+  int device = 0;
+  uint64_t nnz = 0;
+  uint64_t* keys = nullptr;
+  uint32_t* counts = nullptr;
+};
+
 namespace {
 
 uint64_t tiles_of(uint64_t items, int tile = kTile) { return (items + tile - 1) / tile; }
@@ -1344,6 +1352,160 @@ int nmx_flat_fetch(nmx_ctx* c, int64_t* edge_src, int64_t* row_ids, int64_t* row
     }
     return NMX_OK;
   });
+}
+
+nmx_coo* coo_alloc(uint64_t nnz, int device) {
+  nmx_coo* o = new nmx_coo();
+  o->device = device;
+  o->nnz = nnz;
+  if (nnz) {
+    CK(cudaMalloc(&o->keys, nnz * 8));
+    CK(cudaMalloc(&o->counts, nnz * 4));
+  }
+  return o;
+}
+
+int nmx_coo_from_packets(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                         uint64_t n, nmx_coo** out) {
+  if (!out) return fail(NMX_EINVAL, "null output");
+  if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call");
+  return guarded(c, [&] {
+    stage_begin(c, 1);
+    uint64_t m = 0;
+    uint64_t u = 0;
+    if (n) {
+      PacketSrc ps{d_src, d_dst, d_valid, n, 0, 32};
+      uint64_t* keys = sort_rows(c, ps, 32, 0, &m);
+      if (m) {
+        c->mkeys.grow(m * 8);
+        c->mlen.grow(m * 4);
+        u = run_rbk<uint64_t>(c, keys, nullptr, (uint32_t)m, 0, c->mkeys.as<unsigned long long>(),
+                              c->mlen.as<uint32_t>(), nullptr, 27);
+      }
+    }
+    nmx_coo* o = coo_alloc(u, c->device);
+    if (u) {
+      CK(cudaMemcpyAsync(o->keys, c->mkeys.p, u * 8, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(o->counts, c->mlen.p, u * 4, cudaMemcpyDeviceToDevice, c->st));
+    }
+    stage_finish(c, 1);
+    *out = o;
+    return NMX_OK;
+  });
+}
+
+int nmx_coo_merge_add(nmx_ctx* c, const nmx_coo* a, const nmx_coo* b, nmx_coo** out) {
+  if (!a || !b || !out) return fail(NMX_EINVAL, "null argument");
+  return guarded(c, [&] {
+    stage_begin(c, 1);
+    const uint64_t n = a->nnz + b->nnz;
+    const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
+    nmx_coo* o = nullptr;
+    if (tiles) {
+      c->mhist2.grow((tiles + 8) * 4);
+      c->moff.grow((tiles + 8) * 4);
+      c->part.grow(64);
+      auto* ovf = c->part.as<unsigned long long>();
+      CK(cudaMemsetAsync(ovf, 0, 8, c->st));
+      c->dom_begin("merge_add");
+      merge_add_kernel<false><<<(unsigned)tiles, 256, 0, c->st>>>(a->keys, a->counts, a->nnz, b->keys, b->counts,
+                                                                  b->nnz, c->mhist2.as<uint32_t>(), nullptr, nullptr,
+                                                                  nullptr, ovf);
+      CK_LAUNCH();
+      scan_counts(c, c->mhist2.as<uint32_t>(), (uint32_t)tiles, c->moff.as<uint32_t>(), nullptr);
+      uint32_t nc = 0;
+      CK(cudaMemcpyAsync(&nc, c->moff.as<uint32_t>() + tiles, 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      o = coo_alloc(nc, c->device);
+      merge_add_kernel<true><<<(unsigned)tiles, 256, 0, c->st>>>(a->keys, a->counts, a->nnz, b->keys, b->counts,
+                                                                 b->nnz, nullptr, c->moff.as<uint32_t>(), o->keys,
+                                                                 o->counts, ovf);
+      CK_LAUNCH();
+      c->dom_end(16 * n + 12 * (uint64_t)nc);
+      c->launches += 2;
+      unsigned long long ov = 0;
+      CK(cudaMemcpyAsync(&ov, ovf, 8, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      if (ov) {
+        nmx_coo_free(o);
+        return fail(NMX_EINVAL, "merged link count exceeds 2^32-1");
+      }
+    } else {
+      o = coo_alloc(0, c->device);
+    }
+    stage_finish(c, 1);
+    *out = o;
+    return NMX_OK;
+  });
+}
+
+int nmx_coo_stats9(nmx_ctx* c, const nmx_coo* a, int64_t out[9]) {
+  if (!a || !out) return fail(NMX_EINVAL, "null argument");
+  return guarded(c, [&] {
+    stage_begin(c, 1);
+    const uint64_t u = a->nnz;
+    if (u) {
+      if (u >= (1ull << 32)) throw std::runtime_error("COO too large for one statistics call");
+      uint32_t* d_small = c->small.as<uint32_t>();
+      unsigned long long* st = c->stats.as<unsigned long long>();
+      const unsigned grid = (unsigned)std::min<uint64_t>((u + 255) / 256, (uint64_t)c->sms * 8);
+      coo_link_stats_kernel<<<grid, 256, 0, c->st>>>(a->counts, u, st);
+      CK_LAUNCH();
+      CK(cudaMemcpyAsync(st + S_LINKS, &u, 8, cudaMemcpyHostToDevice, c->st));
+      if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
+        CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+      // rows: segments of equal src over the sorted keys (fan-out = links, packets = counts)
+      col_kernel<uint64_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
+          a->keys, a->counts, (uint32_t)u, 32, 0, c->csstatus.as<CSStatus>(), c->next_epoch(), d_small + kCounters + 27,
+          st, 32, S_SRCS, S_MAXFANOUT, S_MAXSRCPK);
+      CK_LAUNCH();
+      // columns: (dst, count) entries sorted by dst
+      c->ckA.grow(u * 4);
+      c->cvA.grow(u * 4);
+      c->ckB.grow(u * 4);
+      c->cvB.grow(u * 4);
+      coo_col_entries_kernel<<<grid, 256, 0, c->st>>>(a->keys, a->counts, u, c->ckA.as<uint32_t>(),
+                                                      c->cvA.as<uint32_t>());
+      CK_LAUNCH();
+      auto sorted = sort_u32_pairs(c, c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u, 32, c->ckB.as<uint32_t>(),
+                                   c->cvB.as<uint32_t>());
+      col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
+          sorted.first, sorted.second, (uint32_t)u, 32, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
+          d_small + kCounters + 26, st);
+      CK_LAUNCH();
+      c->launches += 4;
+    }
+    stage_finish(c, 1);
+    copy_out9(c->h_stats, out, 1);
+    return NMX_OK;
+  });
+}
+
+int nmx_coo_nnz(const nmx_coo* a, uint64_t* nnz) {
+  if (!a || !nnz) return fail(NMX_EINVAL, "null argument");
+  *nnz = a->nnz;
+  return NMX_OK;
+}
+
+int nmx_coo_download(nmx_ctx* c, const nmx_coo* a, uint64_t* keys, int64_t* counts) {
+  if (!a) return fail(NMX_EINVAL, "null argument");
+  return guarded(c, [&] {
+    if (!a->nnz) return NMX_OK;
+    std::vector<uint32_t> tmp(counts ? a->nnz : 0);
+    if (keys) CK(cudaMemcpyAsync(keys, a->keys, a->nnz * 8, cudaMemcpyDeviceToHost, c->st));
+    if (counts) CK(cudaMemcpyAsync(tmp.data(), a->counts, a->nnz * 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (uint64_t i = 0; counts && i < a->nnz; ++i) counts[i] = tmp[i];
+    return NMX_OK;
+  });
+}
+
+void nmx_coo_free(nmx_coo* a) {
+  if (!a) return;
+  cudaSetDevice(a->device);
+  if (a->keys) cudaFree(a->keys);
+  if (a->counts) cudaFree(a->counts);
+  delete a;
 }
 
 int nmx_last_kernel_class(nmx_ctx* c, float* ms, int* launches, uint64_t* bytes, char* name, int name_cap) {

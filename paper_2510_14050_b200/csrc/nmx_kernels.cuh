@@ -636,7 +636,8 @@ __global__ void __launch_bounds__(256) col_kernel(const ColKeyT* __restrict__ ck
                                                  const uint32_t* __restrict__ ccounts, uint32_t u, int b, int wb,
                                                  CSStatus* status, uint32_t epoch,
                                                  uint32_t* __restrict__ tile_counter,
-                                                 unsigned long long* __restrict__ stats) {
+                                                 unsigned long long* __restrict__ stats, int segshift = 0,
+                                                 int s_cnt = S_DSTS, int s_len = S_MAXFANIN, int s_sum = S_MAXDSTPK) {
   constexpr int TILE = 256 * IPT;
   __shared__ __align__(16) uint64_t sk[TILE + TILE / 16];
   __shared__ uint32_t sw[TILE + TILE / 16];
@@ -655,13 +656,13 @@ __global__ void __launch_bounds__(256) col_kernel(const ColKeyT* __restrict__ ck
   for (int j = 0; j < IPT; ++j) {
     const uint32_t i = j * 256 + tid;
     if (i < cnt) {
-      sk[pad16(i)] = (uint64_t)ckeys[t0 + i];
+      sk[pad16(i)] = (uint64_t)ckeys[t0 + i] >> segshift;
       sw[pad16(i)] = ccounts[t0 + i];
     }
   }
   if (tid == 0) {
-    s_prev = t0 ? (uint64_t)ckeys[t0 - 1] : ~(uint64_t)ckeys[0];
-    s_next = last_tile ? 0 : (uint64_t)ckeys[t0 + cnt];
+    s_prev = t0 ? ((uint64_t)ckeys[t0 - 1] >> segshift) : ~((uint64_t)ckeys[0] >> segshift);
+    s_next = last_tile ? 0 : ((uint64_t)ckeys[t0 + cnt] >> segshift);
   }
   __syncthreads();
   const uint64_t first_key = sk[0], last_key = sk[pad16(cnt - 1)];
@@ -706,8 +707,8 @@ __global__ void __launch_bounds__(256) col_kernel(const ColKeyT* __restrict__ ck
       a_sum = max(a_sum, (unsigned long long)sum);
     } else {
       unsigned long long* st = stats + win(key) * S_COUNT;
-      atomicMax(st + S_MAXFANIN, (unsigned long long)len);
-      atomicMax(st + S_MAXDSTPK, (unsigned long long)sum);
+      atomicMax(st + s_len, (unsigned long long)len);
+      atomicMax(st + s_sum, (unsigned long long)sum);
     }
   };
   prev = prev0;
@@ -722,7 +723,7 @@ __global__ void __launch_bounds__(256) col_kernel(const ColKeyT* __restrict__ ck
       if (uniform)
         a_cnt += h;
       else if (h)
-        atomicAdd(stats + win(key) * S_COUNT + S_DSTS, 1ull);
+        atomicAdd(stats + win(key) * S_COUNT + s_cnt, 1ull);
       if (i == cnt - 1 && (last_tile || snext != key)) close(key, run.len, run.sum);
       prev = key;
     }
@@ -748,9 +749,9 @@ __global__ void __launch_bounds__(256) col_kernel(const ColKeyT* __restrict__ ck
         r2 = max(r2, sm_red[w][2]);
       }
       unsigned long long* st = stats + wfirst * S_COUNT;
-      if (r0) atomicAdd(st + S_DSTS, r0);
-      if (r1) atomicMax(st + S_MAXFANIN, r1);
-      if (r2) atomicMax(st + S_MAXDSTPK, r2);
+      if (r0) atomicAdd(st + s_cnt, r0);
+      if (r1) atomicMax(st + s_len, r1);
+      if (r2) atomicMax(st + s_sum, r2);
     }
   }
 }

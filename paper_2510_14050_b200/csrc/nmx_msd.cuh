@@ -924,3 +924,167 @@ __global__ void gather_pairs_kernel(const uint32_t* __restrict__ ck, const uint3
 }
 
 }  // namespace nmx
+
+namespace nmx {
+
+// ---------------------------------------------------------------------------
+// K10: merge-path element-wise addition of two sorted unique COO matrices
+// (keys (src<<32)|dst, u32 counts). C = A + B: union of the keys, counts of a
+// key present in both are added. Tile t owns merged positions [t*T, (t+1)*T)
+// of A ++ B; its split (ia, ib) comes from a merge-path binary search. A key
+// present in both inputs occupies two adjacent merged positions (A's first);
+// the A copy is kept with the sum, the B copy is dropped — if they straddle a
+// tile boundary the earlier tile peeks one element past its end.
+// Pass 1 counts kept elements per tile, scan_counts turns that into output
+// offsets, pass 2 re-merges and writes.
+// ---------------------------------------------------------------------------
+constexpr int kMergeTile = 2048;
+
+// first i in [max(0,d-nb), min(d,na)] with A[i] > B[d-1-i] (merge-path split)
+__device__ __forceinline__ uint64_t merge_split(const uint64_t* a, uint64_t na, const uint64_t* b, uint64_t nb,
+                                                uint64_t d) {
+  uint64_t lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+  while (lo < hi) {
+    const uint64_t i = (lo + hi) >> 1;
+    if (a[i] <= b[d - 1 - i])  // a[i] goes before b[d-1-i] (ties: A first)
+      lo = i + 1;
+    else
+      hi = i;
+  }
+  return lo;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(256) merge_add_kernel(const uint64_t* __restrict__ ak, const uint32_t* __restrict__ ac,
+                                                       uint64_t na, const uint64_t* __restrict__ bk,
+                                                       const uint32_t* __restrict__ bc, uint64_t nb,
+                                                       uint32_t* __restrict__ tile_kept,
+                                                       const uint32_t* __restrict__ tile_off, uint64_t* __restrict__ ck,
+                                                       uint32_t* __restrict__ cc, unsigned long long* __restrict__ overflow) {
+  __shared__ uint64_t sk[kMergeTile + 2];
+  __shared__ uint32_t sc[kMergeTile + 2];
+  __shared__ uint32_t sfrom[kMergeTile + 2];  // 0 = A, 1 = B
+  __shared__ uint32_t wt[kWarps + 1];
+  __shared__ uint64_t s_ia, s_ib, s_ja, s_jb;
+  const int tid = threadIdx.x;
+  const uint64_t n = na + nb;
+  const uint64_t d0 = (uint64_t)blockIdx.x * kMergeTile, d1 = d0 + kMergeTile < n ? d0 + kMergeTile : n;
+  if (tid == 0) {
+    s_ia = merge_split(ak, na, bk, nb, d0);
+    s_ib = d0 - s_ia;
+    s_ja = merge_split(ak, na, bk, nb, d1);
+    s_jb = d1 - s_ja;
+  }
+  __syncthreads();
+  const uint64_t ia = s_ia, ib = s_ib, ja = s_ja, jb = s_jb;
+  const uint32_t la = (uint32_t)(ja - ia), lb = (uint32_t)(jb - ib), len = la + lb;
+  // stage both runs, then merge by per-element rank (position = own index + rank in the other run)
+  for (uint32_t i = tid; i < la; i += 256) {
+    const uint64_t k = ak[ia + i];
+    uint32_t lo = 0, hi = lb;  // # of B elements strictly below k (ties: A first)
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (bk[ib + mid] < k)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    sk[i + lo] = k;
+    sc[i + lo] = ac[ia + i];
+    sfrom[i + lo] = 0;
+  }
+  for (uint32_t i = tid; i < lb; i += 256) {
+    const uint64_t k = bk[ib + i];
+    uint32_t lo = 0, hi = la;  // # of A elements <= k
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (ak[ia + mid] <= k)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    sk[i + lo] = k;
+    sc[i + lo] = bc[ib + i];
+    sfrom[i + lo] = 1;
+  }
+  __syncthreads();
+  // element e is dropped iff it is a B copy whose predecessor (in merged order) has the same key
+  const uint64_t prev0 = d0 == 0 ? ~0ull
+                                 : ((ia > 0 && (ib == 0 || ak[ia - 1] >= bk[ib - 1])) ? ak[ia - 1] : bk[ib - 1]);
+  const bool prev0_valid = d0 > 0;
+  // the element right after the tile (to add a straddling B copy to our last kept A copy)
+  uint64_t next_k = 0;
+  uint32_t next_c = 0;
+  bool next_is_b = false;
+  if (d1 < n) {
+    if (ja < na && (jb >= nb || ak[ja] <= bk[jb])) {
+      next_k = ak[ja];
+    } else {
+      next_k = bk[jb];
+      next_c = bc[jb];
+      next_is_b = true;
+    }
+  }
+  uint32_t kept = 0;
+  const uint32_t PER = (len + 255) / 256;
+  const uint32_t e0 = tid * PER;
+  for (uint32_t q = 0; q < PER; ++q) {
+    const uint32_t e = e0 + q;
+    if (e >= len) break;
+    const bool dup = sfrom[e] == 1 && (e > 0 ? sk[e - 1] == sk[e] : (prev0_valid && prev0 == sk[e]));
+    kept += !dup;
+  }
+  uint32_t total;
+  uint32_t at = block_excl_scan<uint32_t>(kept, wt, &total);
+  if (!WRITE) {
+    if (tid == 0) tile_kept[blockIdx.x] = total;
+    return;
+  }
+  at += tile_off[blockIdx.x];
+  for (uint32_t q = 0; q < PER; ++q) {
+    const uint32_t e = e0 + q;
+    if (e >= len) break;
+    const bool dup = sfrom[e] == 1 && (e > 0 ? sk[e - 1] == sk[e] : (prev0_valid && prev0 == sk[e]));
+    if (dup) continue;
+    unsigned long long c = sc[e];
+    if (e + 1 < len) {
+      if (sfrom[e + 1] == 1 && sk[e + 1] == sk[e]) c += sc[e + 1];
+    } else if (next_is_b && next_k == sk[e]) {
+      c += next_c;
+    }
+    if (c > 0xFFFFFFFFull) atomicAdd(overflow, 1ull);
+    ck[at] = sk[e];
+    cc[at] = (uint32_t)c;
+    ++at;
+  }
+}
+
+// link statistics of a COO (valid, links, max link)
+__global__ void coo_link_stats_kernel(const uint32_t* __restrict__ cnt, uint64_t n,
+                                      unsigned long long* __restrict__ stats) {
+  unsigned long long v = 0, mx = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    v += cnt[i];
+    mx = max(mx, (unsigned long long)cnt[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    v += __shfl_xor_sync(FULL, v, o);
+    mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(stats + S_VALID, v);
+    atomicMax(stats + S_MAXLINK, mx);
+  }
+}
+
+// destinations of a COO as (dst, count) column entries
+__global__ void coo_col_entries_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ cnt, uint64_t n,
+                                       uint32_t* __restrict__ ck, uint32_t* __restrict__ cv) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    ck[i] = (uint32_t)keys[i];
+    cv[i] = cnt[i];
+  }
+}
+
+}  // namespace nmx

@@ -1,0 +1,71 @@
+"""Merge-path element-wise addition (K10) and device COO statistics vs the oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import netmeter_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def coo():
+    from paper_2510_14050_b200 import coo as c
+
+    return c
+
+
+def _gen(kind, seed, off, n, space):
+    g = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
+    return g(seed, off, n, space)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
+@pytest.mark.parametrize("space", [1 << 32, 5000, 7])
+def test_coo_from_packets_and_stats(coo, kind, space):
+    s, d = _gen(kind, 3, 0, 200_000, space)
+    v = np.random.default_rng(1).random(len(s)) > 0.1
+    m = coo.coo_from_packets(s, d, v)
+    keys, counts = m.download()
+    wk, wc = orc.coo_packed(s, d, v)
+    assert np.array_equal(keys, wk) and np.array_equal(counts, wc)
+    assert m.stats9() == orc.stats9_packed(s, d, v)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
+@pytest.mark.parametrize("space", [1 << 32, 3000, 2])
+def test_merge_add_equals_concatenation(coo, kind, space):
+    s, d = _gen(kind, 5, 0, 300_000, space)
+    cut = [0, 70_000, 70_001, 190_000, 300_000]
+    parts = [coo.coo_from_packets(s[a:b], d[a:b]) for a, b in zip(cut[:-1], cut[1:])]
+    acc = parts[0]
+    for p in parts[1:]:
+        acc = coo.merge_add(acc, p)
+    keys, counts = acc.download()
+    wk, wc = orc.coo_packed(s, d)
+    assert np.array_equal(keys, wk) and np.array_equal(counts, wc)
+    assert acc.stats9() == orc.stats9_packed(s, d)
+
+
+def test_merge_add_edge_cases(coo):
+    e = coo.coo_from_packets(np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+    assert e.nnz == 0 and e.stats9() == (0,) * 9
+    a = coo.coo_from_packets(np.array([1, 1, 2], np.uint32), np.array([5, 5, 6], np.uint32))
+    assert (e + a).download()[1].tolist() == [2, 1]
+    assert (a + e).stats9() == a.stats9()
+    b = coo.coo_from_packets(np.array([1, 3], np.uint32), np.array([5, 0], np.uint32))
+    k, c = (a + b).download()
+    assert k.tolist() == [(1 << 32) | 5, (2 << 32) | 6, (3 << 32) | 0] and c.tolist() == [3, 1, 1]
+    # identical inputs: every key duplicated across a tile boundary somewhere
+    s, d = _gen("uniform", 9, 0, 50_000, 1 << 32)
+    x = coo.coo_from_packets(s, d)
+    kk, cc = (x + x).download()
+    k1, c1 = x.download()
+    assert np.array_equal(kk, k1) and np.array_equal(cc, 2 * c1)
+
+
+def test_streamed_windows_log_structured(coo):
+    s, d = _gen("powerlaw", 11, 0, 1 << 20, 1 << 32)
+    w = 1 << 16
+    got = coo.stream_stats9((s[i:i + w], d[i:i + w]) for i in range(0, len(s), w))
+    assert got == orc.stats9_packed(s, d)
