@@ -178,9 +178,6 @@ def stream_stats9_pinned(windows, device: int = 0) -> tuple:
         n = len(windows[k][0])
         h = C.c_void_p()
         _lib.check(ctx._lib.nmx_coo_from_packets(ctx.handle, ds.data_ptr(), dd.data_ptr(), None, n, C.byref(h)))
-        if k + 1 < len(windows):
-            # the next upload may start overwriting the other buffer only; this one is free now
-            pass
         acc.add(DeviceCOO(h, device))
     out = acc.result().stats9()
     for ds, dd in bufs:

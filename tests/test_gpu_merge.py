@@ -69,3 +69,18 @@ def test_streamed_windows_log_structured(coo):
     w = 1 << 16
     got = coo.stream_stats9((s[i:i + w], d[i:i + w]) for i in range(0, len(s), w))
     assert got == orc.stats9_packed(s, d)
+
+
+def test_streamed_pinned_windows_overlapped(coo):
+    from paper_2510_14050_b200 import _lib
+
+    s, d = _gen("uniform", 13, 0, 3 << 18, 1 << 32)
+    w = 1 << 18
+    wins = []
+    for i in range(0, len(s), w):
+        ps, pd = _lib.PinnedArray(w), _lib.PinnedArray(w)
+        ps.array[:] = s[i:i + w]
+        pd.array[:] = d[i:i + w]
+        wins.append((ps, pd))
+    got = coo.stream_stats9_pinned([(a.array, b.array) for a, b in wins])
+    assert got == orc.stats9_packed(s, d)
