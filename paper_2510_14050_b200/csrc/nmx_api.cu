@@ -673,6 +673,56 @@ void plan_groups(nmx_ctx* c, const uint32_t* off, uint32_t nb, uint64_t m, uint3
   c->launches += 3;
 }
 
+// Column statistics of (dst, count) entries (holes allowed) read through `cs`,
+// whose arrays may alias ckA / cvA (the first level reads them all before the
+// second level writes ckA / cvA): MSD partition by destination bits ->
+// shared-memory grouping -> heavy destinations via LSD + col_kernel.
+void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32_t* prehist) {
+  const uint32_t S = 1024, capb = 1024;
+  uint32_t* d_small = c->small.as<uint32_t>();
+  uint32_t* ck = nullptr;
+  uint32_t* cv = nullptr;
+  const uint64_t need = cs.n;
+  c->ckB.grow(need * 4);
+  c->cvB.grow(need * 4);
+  const uint64_t u = msd_partition<ColConcatSrc, uint32_t, true>(c, cs, cs.n, b, Dc, c->ckB.as<uint32_t>(),
+                                                                 c->cvB.as<uint32_t>(), c->ckA.as<uint32_t>(),
+                                                                 c->cvA.as<uint32_t>(), &ck, &cv, prehist);
+  c->mark();  // column partition end
+  if (!u) return;
+  const uint32_t nbc = 1u << Dc;
+  uint32_t* off = c->moff.as<uint32_t>();
+  const uint32_t ngroups = (uint32_t)((u + S - 1) / S);
+  plan_groups(c, off, nbc, u, S, capb);
+  set_smem(local_cols_kernel, sizeof(LocColSmem));
+  local_cols_kernel<<<(unsigned)(c->sms * 3), kLocThreads, sizeof(LocColSmem), c->st>>>(
+      ck, cv, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>());
+  CK_LAUNCH();
+  ++c->launches;
+  c->mark();  // local columns end
+  uint32_t nheavy = 0;
+  const uint64_t ch = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
+  if (ch) {  // heavy destination buckets: gather -> LSD sort -> column kernel
+    c->cgk.grow(ch * 4);
+    c->cgv.grow(ch * 4);
+    c->cgk2.grow(ch * 4);
+    c->cgv2.grow(ch * 4);
+    gather_pairs_kernel<<<(unsigned)std::min<uint64_t>((ch + 255) / 256, (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+        ck, cv, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, (uint32_t)ch, c->cgk.as<uint32_t>(),
+        c->cgv.as<uint32_t>());
+    CK_LAUNCH();
+    auto sorted = sort_u32_pairs(c, c->cgk.as<uint32_t>(), c->cgv.as<uint32_t>(), ch, b, c->cgk2.as<uint32_t>(),
+                                 c->cgv2.as<uint32_t>());
+    if (c->csstatus.grow(tiles_of(ch, kSegTile) * sizeof(CSStatus)))
+      CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+    col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(ch, kSegTile), 256, 0, c->st>>>(
+        sorted.first, sorted.second, (uint32_t)ch, b, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
+        d_small + kCounters + 26, c->stats.as<unsigned long long>());
+    CK_LAUNCH();
+    ++c->launches;
+  }
+}
+
 void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
                       int b, int D) {
   const int kb = 2 * b;
@@ -751,41 +801,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), m,
                   c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh, m + uh};
   cs.quad = true;  // context buffers are cudaMalloc-aligned
-  uint32_t* ck = nullptr;
-  uint32_t* cv = nullptr;
-  const uint64_t u = msd_partition<ColConcatSrc, uint32_t, true>(c, cs, m + uh, b, Dc, c->ckB.as<uint32_t>(),
-                                                                 c->cvB.as<uint32_t>(), c->ckA.as<uint32_t>(),
-                                                                 c->cvA.as<uint32_t>(), &ck, &cv, chist);
-  c->mark();  // 5: column partition end
-  const uint32_t nbc = 1u << Dc;
-  ngroups = (uint32_t)((u + S - 1) / S);
-  plan_groups(c, off, nbc, u, S, capb);
-  set_smem(local_cols_kernel, sizeof(LocColSmem));
-  local_cols_kernel<<<(unsigned)(c->sms * 3), kLocThreads, sizeof(LocColSmem), c->st>>>(
-      ck, cv, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>());
-  CK_LAUNCH();
-  ++c->launches;
-  c->mark();  // 6: local columns end
-  const uint64_t ch = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
-  if (ch) {  // heavy destination buckets: gather -> LSD sort -> column kernel
-    c->cgk.grow(ch * 4);
-    c->cgv.grow(ch * 4);
-    c->cgk2.grow(ch * 4);
-    c->cgv2.grow(ch * 4);
-    gather_pairs_kernel<<<(unsigned)std::min<uint64_t>((ch + 255) / 256, (uint64_t)c->sms * 16), 256, 0, c->st>>>(
-        ck, cv, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, (uint32_t)ch, c->cgk.as<uint32_t>(),
-        c->cgv.as<uint32_t>());
-    CK_LAUNCH();
-    auto sorted = sort_u32_pairs(c, c->cgk.as<uint32_t>(), c->cgv.as<uint32_t>(), ch, b, c->cgk2.as<uint32_t>(),
-                                 c->cgv2.as<uint32_t>());
-    if (c->csstatus.grow(tiles_of(ch, kSegTile) * sizeof(CSStatus)))
-      CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
-    col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(ch, kSegTile), 256, 0, c->st>>>(
-        sorted.first, sorted.second, (uint32_t)ch, b, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
-        d_small + kCounters + 26, c->stats.as<unsigned long long>());
-    CK_LAUNCH();
-    ++c->launches;
-  }
+  msd_columns(c, cs, b, Dc, chist);
   stage_finish(c, 1);
 }
 
@@ -1354,13 +1370,24 @@ int nmx_flat_fetch(nmx_ctx* c, int64_t* edge_src, int64_t* row_ids, int64_t* row
   });
 }
 
-nmx_coo* coo_alloc(uint64_t nnz, int device) {
+// COO storage is stream-ordered (cudaMallocAsync / cudaFreeAsync from the device's
+// default pool, kept resident): a plain cudaFree would synchronise the whole
+// device and serialise the overlapped H2D copies of the streamed path.
+nmx_coo* coo_alloc(nmx_ctx* c, uint64_t nnz) {
+  static bool pool_ready[64] = {false};
+  if (c->device < 64 && !pool_ready[c->device]) {
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+    uint64_t keep = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pool_ready[c->device] = true;
+  }
   nmx_coo* o = new nmx_coo();
-  o->device = device;
+  o->device = c->device;
   o->nnz = nnz;
   if (nnz) {
-    CK(cudaMalloc(&o->keys, nnz * 8));
-    CK(cudaMalloc(&o->counts, nnz * 4));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&o->keys), nnz * 8, c->st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&o->counts), nnz * 4, c->st));
   }
   return o;
 }
@@ -1383,7 +1410,7 @@ int nmx_coo_from_packets(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_ds
                               c->mlen.as<uint32_t>(), nullptr, 27);
       }
     }
-    nmx_coo* o = coo_alloc(u, c->device);
+    nmx_coo* o = coo_alloc(c, u);
     if (u) {
       CK(cudaMemcpyAsync(o->keys, c->mkeys.p, u * 8, cudaMemcpyDeviceToDevice, c->st));
       CK(cudaMemcpyAsync(o->counts, c->mlen.p, u * 4, cudaMemcpyDeviceToDevice, c->st));
@@ -1416,7 +1443,7 @@ int nmx_coo_merge_add(nmx_ctx* c, const nmx_coo* a, const nmx_coo* b, nmx_coo** 
       uint32_t nc = 0;
       CK(cudaMemcpyAsync(&nc, c->moff.as<uint32_t>() + tiles, 4, cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
-      o = coo_alloc(nc, c->device);
+      o = coo_alloc(c, nc);
       merge_add_kernel<true><<<(unsigned)tiles, 256, 0, c->st>>>(a->keys, a->counts, a->nnz, b->keys, b->counts,
                                                                  b->nnz, nullptr, c->moff.as<uint32_t>(), o->keys,
                                                                  o->counts, ovf);
@@ -1431,7 +1458,7 @@ int nmx_coo_merge_add(nmx_ctx* c, const nmx_coo* a, const nmx_coo* b, nmx_coo** 
         return fail(NMX_EINVAL, "merged link count exceeds 2^32-1");
       }
     } else {
-      o = coo_alloc(0, c->device);
+      o = coo_alloc(c, 0);
     }
     stage_finish(c, 1);
     *out = o;
@@ -1467,12 +1494,19 @@ int nmx_coo_stats9(nmx_ctx* c, const nmx_coo* a, int64_t out[9]) {
       coo_col_entries_kernel<<<grid, 256, 0, c->st>>>(a->keys, a->counts, u, c->ckA.as<uint32_t>(),
                                                       c->cvA.as<uint32_t>());
       CK_LAUNCH();
-      auto sorted = sort_u32_pairs(c, c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u, 32, c->ckB.as<uint32_t>(),
-                                   c->cvB.as<uint32_t>());
-      col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
-          sorted.first, sorted.second, (uint32_t)u, 32, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
-          d_small + kCounters + 26, st);
-      CK_LAUNCH();
+      const int Dc = std::min(21, std::max(11, (int)ceil_log2(u) - 9));
+      if (u >= (1ull << 20)) {  // MSD partition + shared-memory grouping
+        ColConcatSrc cs{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u, nullptr, nullptr, 0, u};
+        cs.quad = true;
+        msd_columns(c, cs, 32, Dc, nullptr);
+      } else {
+        auto sorted = sort_u32_pairs(c, c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u, 32, c->ckB.as<uint32_t>(),
+                                     c->cvB.as<uint32_t>());
+        col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
+            sorted.first, sorted.second, (uint32_t)u, 32, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
+            d_small + kCounters + 26, st);
+        CK_LAUNCH();
+      }
       c->launches += 4;
     }
     stage_finish(c, 1);
@@ -1503,8 +1537,11 @@ int nmx_coo_download(nmx_ctx* c, const nmx_coo* a, uint64_t* keys, int64_t* coun
 void nmx_coo_free(nmx_coo* a) {
   if (!a) return;
   cudaSetDevice(a->device);
-  if (a->keys) cudaFree(a->keys);
-  if (a->counts) cudaFree(a->counts);
+  // stream-ordered on the legacy stream: ordered after every prior launch that
+  // could read the matrix on blocking streams; the context streams are
+  // non-blocking, so callers free only after their synchronous calls returned
+  if (a->keys) cudaFreeAsync(a->keys, 0);
+  if (a->counts) cudaFreeAsync(a->counts, 0);
   delete a;
 }
 

@@ -72,11 +72,11 @@ __device__ __forceinline__ void quad_items(const KeySrc<KeyT, HAS_VAL>& s, uint6
 }
 struct ColConcatSrc;
 __device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok);
-template <typename Src, typename KeyT>
+template <typename Src, typename KeyT, int NQ = 2>
 __device__ __forceinline__ void load_items(const Src& s, uint64_t q0, uint64_t qstride, KeyT* k, uint32_t* v,
                                            bool* ok) {
-  quad_items(s, q0, k, v, ok);
-  quad_items(s, q0 + qstride, k + 4, v + 4, ok + 4);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) quad_items(s, q0 + q * qstride, k + 4 * q, v + 4 * q, ok + 4 * q);
 }
 
 // Level 1 (cursor indexed by the D1-bit digit) and level 2 (cursor indexed by
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
   uint32_t v[kMsdIPT];
   bool ok[kMsdIPT];
   if constexpr (LEVEL == 1) {
-    load_items<Src, KeyT>(src, base / 4 + tid, kMsdThreads, k, v, ok);
+    load_items<Src, KeyT, kMsdIPT / 4>(src, base / 4 + tid, kMsdThreads, k, v, ok);
   } else {
 #pragma unroll
     for (int i = 0; i < kMsdIPT; ++i)
