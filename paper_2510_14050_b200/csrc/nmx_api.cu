@@ -1404,17 +1404,32 @@ int nmx_coo_from_packets(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_ds
       PacketSrc ps{d_src, d_dst, d_valid, n, 0, 32};
       uint64_t* keys = sort_rows(c, ps, 32, 0, &m);
       if (m) {
-        c->mkeys.grow(m * 8);
-        c->mlen.grow(m * 4);
-        u = run_rbk<uint64_t>(c, keys, nullptr, (uint32_t)m, 0, c->mkeys.as<unsigned long long>(),
-                              c->mlen.as<uint32_t>(), nullptr, 27);
+        const uint64_t tiles = (m + kUniqTile - 1) / kUniqTile;
+        c->mhist2.grow((tiles + 8) * 4);
+        c->moff.grow((tiles + 8) * 4);
+        unique_heads_kernel<false><<<(unsigned)tiles, 256, 0, c->st>>>(keys, m, c->mhist2.as<uint32_t>(), nullptr,
+                                                                      nullptr, nullptr);
+        CK_LAUNCH();
+        scan_counts(c, c->mhist2.as<uint32_t>(), (uint32_t)tiles, c->moff.as<uint32_t>(), nullptr);
+        uint32_t uu = 0;
+        CK(cudaMemcpyAsync(&uu, c->moff.as<uint32_t>() + tiles, 4, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        u = uu;
+        c->mlen.grow(u * 4 + 8);
+        nmx_coo* o = coo_alloc(c, u);
+        unique_heads_kernel<true><<<(unsigned)tiles, 256, 0, c->st>>>(keys, m, nullptr, c->moff.as<uint32_t>(),
+                                                                     o->keys, c->mlen.as<uint32_t>());
+        CK_LAUNCH();
+        run_counts_kernel<<<(unsigned)std::min<uint64_t>((u + 255) / 256, (uint64_t)c->sms * 16), 256, 0, c->st>>>(
+            c->mlen.as<uint32_t>(), u, m, o->counts);
+        CK_LAUNCH();
+        c->launches += 3;
+        stage_finish(c, 1);
+        *out = o;
+        return NMX_OK;
       }
     }
     nmx_coo* o = coo_alloc(c, u);
-    if (u) {
-      CK(cudaMemcpyAsync(o->keys, c->mkeys.p, u * 8, cudaMemcpyDeviceToDevice, c->st));
-      CK(cudaMemcpyAsync(o->counts, c->mlen.p, u * 4, cudaMemcpyDeviceToDevice, c->st));
-    }
     stage_finish(c, 1);
     *out = o;
     return NMX_OK;

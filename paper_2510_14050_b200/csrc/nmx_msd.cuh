@@ -938,7 +938,7 @@ namespace nmx {
 // Pass 1 counts kept elements per tile, scan_counts turns that into output
 // offsets, pass 2 re-merges and writes.
 // ---------------------------------------------------------------------------
-constexpr int kMergeTile = 2048;
+constexpr int kMergeTile = 1536;
 
 // first i in [max(0,d-nb), min(d,na)] with A[i] > B[d-1-i] (merge-path split)
 __device__ __forceinline__ uint64_t merge_split(const uint64_t* a, uint64_t na, const uint64_t* b, uint64_t nb,
@@ -963,7 +963,7 @@ __global__ void __launch_bounds__(256) merge_add_kernel(const uint64_t* __restri
                                                        uint32_t* __restrict__ cc, unsigned long long* __restrict__ overflow) {
   __shared__ uint64_t sk[kMergeTile + 2];
   __shared__ uint32_t sc[kMergeTile + 2];
-  __shared__ uint32_t sfrom[kMergeTile + 2];  // 0 = A, 1 = B
+  __shared__ uint8_t sfrom[kMergeTile + 2];  // 0 = A, 1 = B
   __shared__ uint32_t wt[kWarps + 1];
   __shared__ uint64_t s_ia, s_ib, s_ja, s_jb;
   const int tid = threadIdx.x;
@@ -978,13 +978,18 @@ __global__ void __launch_bounds__(256) merge_add_kernel(const uint64_t* __restri
   __syncthreads();
   const uint64_t ia = s_ia, ib = s_ib, ja = s_ja, jb = s_jb;
   const uint32_t la = (uint32_t)(ja - ia), lb = (uint32_t)(jb - ib), len = la + lb;
-  // stage both runs, then merge by per-element rank (position = own index + rank in the other run)
+  // stage both runs in shared memory (coalesced), then merge by per-element rank
+  // (position = own index + rank in the other run, binary search in smem)
+  __shared__ uint64_t ra[kMergeTile], rb[kMergeTile];
+  for (uint32_t i = tid; i < la; i += 256) ra[i] = ak[ia + i];
+  for (uint32_t i = tid; i < lb; i += 256) rb[i] = bk[ib + i];
+  __syncthreads();
   for (uint32_t i = tid; i < la; i += 256) {
-    const uint64_t k = ak[ia + i];
+    const uint64_t k = ra[i];
     uint32_t lo = 0, hi = lb;  // # of B elements strictly below k (ties: A first)
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (bk[ib + mid] < k)
+      if (rb[mid] < k)
         lo = mid + 1;
       else
         hi = mid;
@@ -994,11 +999,11 @@ __global__ void __launch_bounds__(256) merge_add_kernel(const uint64_t* __restri
     sfrom[i + lo] = 0;
   }
   for (uint32_t i = tid; i < lb; i += 256) {
-    const uint64_t k = bk[ib + i];
+    const uint64_t k = rb[i];
     uint32_t lo = 0, hi = la;  // # of A elements <= k
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (ak[ia + mid] <= k)
+      if (ra[mid] <= k)
         lo = mid + 1;
       else
         hi = mid;
@@ -1057,6 +1062,73 @@ __global__ void __launch_bounds__(256) merge_add_kernel(const uint64_t* __restri
     cc[at] = (uint32_t)c;
     ++at;
   }
+}
+
+// Unique keys of a sorted array with their run lengths, without a lookback
+// chain: pass 1 counts run heads per tile, scan_counts gives every tile its first
+// output index, pass 2 writes (key, start position) of each head through shared
+// memory; run_counts_kernel turns start positions into counts.
+constexpr int kUniqTile = 2048;
+template <bool WRITE>
+__global__ void __launch_bounds__(256) unique_heads_kernel(const uint64_t* __restrict__ keys, uint64_t n,
+                                                          uint32_t* __restrict__ tile_heads,
+                                                          const uint32_t* __restrict__ tile_off,
+                                                          uint64_t* __restrict__ ukeys, uint32_t* __restrict__ ustart) {
+  __shared__ __align__(16) uint64_t sk[kUniqTile + kUniqTile / 16];
+  __shared__ uint32_t ss[kUniqTile];
+  __shared__ uint32_t wt[kWarps + 1];
+  __shared__ uint64_t s_prev;
+  const int tid = threadIdx.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * kUniqTile;
+  const uint32_t cnt = (uint32_t)umin64(kUniqTile, n - t0);
+  constexpr int PER = kUniqTile / 256;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {  // coalesced load, padded for the blocked reads below
+    const uint32_t i = q * 256 + tid;
+    if (i < cnt) sk[pad16(i)] = keys[t0 + i];
+  }
+  if (tid == 0) s_prev = t0 ? keys[t0 - 1] : ~keys[0];
+  __syncthreads();
+  uint64_t k[PER];
+  uint32_t hmask = 0, nh = 0;
+  const uint32_t i0 = tid * PER;
+  uint64_t prev = i0 == 0 ? s_prev : (i0 < cnt ? sk[pad16(i0 - 1)] : 0);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const uint32_t i = i0 + q;
+    if (i < cnt) {
+      k[q] = sk[pad16(i)];
+      const bool h = k[q] != prev;
+      hmask |= (uint32_t)h << q;
+      nh += h;
+      prev = k[q];
+    }
+  }
+  uint32_t total;
+  uint32_t at = block_excl_scan<uint32_t>(nh, wt, &total);  // (its barriers also end the sk reads)
+  if (!WRITE) {
+    if (tid == 0) tile_heads[blockIdx.x] = total;
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if ((hmask >> q) & 1u) {
+      sk[at] = k[q];
+      ss[at] = (uint32_t)(t0 + i0 + q);
+      ++at;
+    }
+  }
+  __syncthreads();
+  const uint32_t base = tile_off[blockIdx.x];
+  for (uint32_t j = tid; j < total; j += 256) {
+    ukeys[base + j] = sk[j];
+    ustart[base + j] = ss[j];
+  }
+}
+__global__ void run_counts_kernel(const uint32_t* __restrict__ ustart, uint64_t u, uint64_t n,
+                                  uint32_t* __restrict__ counts) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < u; j += (uint64_t)gridDim.x * blockDim.x)
+    counts[j] = (uint32_t)((j + 1 < u ? ustart[j + 1] : n) - ustart[j]);
 }
 
 // link statistics of a COO (valid, links, max link)
