@@ -126,7 +126,9 @@ int nmx_flat_fetch(nmx_ctx* ctx, int64_t* edge_src, int64_t* row_ids, int64_t* r
  *  - nmx_coo_from_packets: unique links of device packet columns;
  *  - nmx_coo_merge_add: C = A + B by merge path (counts of shared keys added);
  *  - nmx_coo_stats9: the nine statistics of a COO;
- *  - nmx_coo_nnz / nmx_coo_download / nmx_coo_free. */
+ *  - nmx_coo_nnz / nmx_coo_download / nmx_coo_free;
+ *  - nmx_coo_reserve: keep `bytes` of device memory mapped in the pool COOs are
+ *    allocated from (stream-ordered allocations then never grow the pool). */
 int nmx_coo_from_packets(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
                          uint64_t n, nmx_coo** out);
 int nmx_coo_merge_add(nmx_ctx* ctx, const nmx_coo* a, const nmx_coo* b, nmx_coo** out);
@@ -134,6 +136,7 @@ int nmx_coo_stats9(nmx_ctx* ctx, const nmx_coo* a, int64_t out[9]);
 int nmx_coo_nnz(const nmx_coo* a, uint64_t* nnz);
 int nmx_coo_download(nmx_ctx* ctx, const nmx_coo* a, uint64_t* keys, int64_t* counts);
 void nmx_coo_free(nmx_coo* a);
+int nmx_coo_reserve(nmx_ctx* ctx, uint64_t bytes);
 
 /* Multi-GPU building blocks (one process per GPU; the exchange itself is NCCL
  * all-to-all driven by paper_2510_14050_b200/distributed.py). owner(x) =

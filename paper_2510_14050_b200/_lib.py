@@ -61,6 +61,7 @@ SIGNATURES = {
     "nmx_coo_nnz": (C.c_int, [_VP, C.POINTER(_U64)]),
     "nmx_coo_download": (C.c_int, [_VP, _VP, _VP, _VP]),
     "nmx_coo_free": (None, [_VP]),
+    "nmx_coo_reserve": (C.c_int, [_VP, _U64]),
     "nmx_partition_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.c_int, _VP, _VP, _VP]),
     "nmx_shard_rows": (C.c_int, [_VP, _VP, _VP, _U64, _U64, C.c_int, _VP, _VP, _VP, _VP]),
     "nmx_shard_cols": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),

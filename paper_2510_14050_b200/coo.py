@@ -61,6 +61,12 @@ class DeviceCOO:
             pass
 
 
+def reserve(nbytes: int, device: int = 0) -> None:
+    """Keep ``nbytes`` of device memory mapped in the COO allocation pool."""
+    ctx = _lib.context(device)
+    _lib.check(ctx._lib.nmx_coo_reserve(ctx.handle, int(nbytes)))
+
+
 def coo_from_packets(src, dst, valid=None, device: int = 0) -> DeviceCOO:
     """Unique links of one window. ``src``/``dst``: host arrays (copied) or device arrays."""
     ctx = _lib.context(device)
@@ -150,6 +156,10 @@ def stream_stats9_pinned(windows, device: int = 0) -> tuple:
     if not windows:
         return (0,) * 9
     ctx = _lib.context(device)
+    total = sum(len(w[0]) for w in windows)
+    # unique links <= packets, 12 B each; the log-structured sum holds at most about
+    # two copies plus one window's matrix at a time
+    reserve(min(int(total * 12 * 2.2), 120 << 30), device)
     copier = _lib.Context(device)  # its own stream
     cap = max(len(w[0]) for w in windows)
     bufs = [(_lib.DeviceArray(cap, device=device), _lib.DeviceArray(cap, device=device)) for _ in range(2)]

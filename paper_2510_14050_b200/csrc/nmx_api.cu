@@ -1530,6 +1530,18 @@ int nmx_coo_stats9(nmx_ctx* c, const nmx_coo* a, int64_t out[9]) {
   });
 }
 
+int nmx_coo_reserve(nmx_ctx* c, uint64_t bytes) {
+  return guarded(c, [&] {
+    nmx_coo* probe = coo_alloc(c, 0);  // configures the pool (release threshold = keep)
+    delete probe;
+    void* p = nullptr;
+    CK(cudaMallocAsync(&p, std::max<uint64_t>(bytes, 1), c->st));
+    CK(cudaFreeAsync(p, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return NMX_OK;
+  });
+}
+
 int nmx_coo_nnz(const nmx_coo* a, uint64_t* nnz) {
   if (!a || !nnz) return fail(NMX_EINVAL, "null argument");
   *nnz = a->nnz;

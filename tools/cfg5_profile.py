@@ -14,6 +14,7 @@ for k in range(2):
     ps, pd = _lib.PinnedArray(w), _lib.PinnedArray(w)
     ps.array[:] = ds.download(); pd.array[:] = dd.download()
     pins.append((ps, pd))
+nc.reserve(64 << 30)
 def T(f, *a):
     t0 = time.perf_counter(); r = f(*a); return r, (time.perf_counter() - t0) * 1e3
 _, t = T(lambda: ds.upload(pins[0][0].array)); print(f"H2D one column 1 GiB: {t:.1f} ms", flush=True)
