@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "../../include/nmx.h"
-#include "nmx_msd.cuh"
+#include "nmx_seg.cuh"
 
 using namespace nmx;
 
@@ -107,7 +107,8 @@ struct nmx_ctx {
   std::mutex mu;
   DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
-      red;
+      red, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
+      hcount;
   uint32_t epoch = 0;
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
   unsigned long long* h_stats = nullptr;
@@ -551,10 +552,48 @@ int msd_first_bits(int D) {
   return D / L + (0 < D % L ? 1 : 0);
 }
 
+struct SegTotals {
+  uint32_t light, big, nbig;
+};
+
+// classify C child counts (light <= kSegCap, big otherwise): cursors with the
+// light bit in scur, light offsets in sloff[0..C], big offsets (= next parents)
+// compacted into npoff; totals on the host
+SegTotals seg_classify(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* npoff) {
+  c->scur.grow(((size_t)C + 8) * 4);
+  c->sloff.grow(((size_t)C + 8) * 4);
+  const uint32_t nb = (C + kSegScanItems - 1) / kSegScanItems;
+  c->sbsum.grow(((size_t)nb + 8) * 8);
+  c->sbflag.grow(((size_t)nb + 8) * 4);
+  c->stot.grow(64);
+  seg_scan_sums_kernel<<<nb, 256, 0, c->st>>>(ccnt, C, c->sbsum.as<unsigned long long>(), c->sbflag.as<uint32_t>());
+  CK_LAUNCH();
+  seg_scan_top_kernel<<<1, 1024, 0, c->st>>>(c->sbsum.as<unsigned long long>(), c->sbflag.as<uint32_t>(), nb,
+                                             c->stot.as<uint32_t>());
+  CK_LAUNCH();
+  seg_scan_apply_kernel<<<nb, 256, 0, c->st>>>(ccnt, C, c->sbsum.as<unsigned long long>(), c->sbflag.as<uint32_t>(),
+                                               c->stot.as<uint32_t>(), c->scur.as<uint32_t>(), c->sloff.as<uint32_t>(),
+                                               npoff);
+  CK_LAUNCH();
+  c->launches += 3;
+  SegTotals t{};
+  CK(cudaMemcpyAsync(&t, c->stot.p, sizeof(t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return t;
+}
+
+// last-level split of the dense MSD partition: light buckets stay in the level
+// output, heavy ones (> kSegCap) go compacted to (hk, hv), their offsets to spoffA
+struct MsdSplit {
+  void* hk = nullptr;
+  uint32_t* hv = nullptr;
+  SegTotals t{};
+};
+
 template <typename Src, typename KeyT, bool HAS_VAL>
 uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, KeyT* outA, uint32_t* voutA,
                        KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v,
-                       const uint32_t* prehist = nullptr) {
+                       const uint32_t* prehist = nullptr, MsdSplit* split = nullptr) {
   // levels of <= kMsdLevelBits bits: 128 bins per tile keeps the reservation
   // atomics at one per 32 keys and every digit's run in a tile ~32 keys long
   const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
@@ -611,13 +650,27 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(in_k, m, shift, dl[l], bshift,
                                                                                          h2);
     CK_LAUNCH();
-    scan_counts(c, h2, nbl, off, cur);
     KeySrc<KeyT, HAS_VAL> ks{in_k, in_v, m};
-    set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>, sizeof(S1));
-    c->dom_begin("msd_scatter");
-    msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>
-        <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(ks, m, out_k, out_v, shift, dl[l],
-                                                                               bshift, cur);
+    if (split && l + 1 == L) {  // heavy buckets leave compacted (nmx_seg.cuh continues them)
+      c->spoffA.grow(((size_t)std::min<uint64_t>(nbl, m / (kSegCap + 1) + 1) + 8) * 4);
+      split->t = seg_classify(c, h2, nbl, c->spoffA.as<uint32_t>());
+      if (getenv("NMX_DEBUG"))
+        fprintf(stderr, "dense split m=%llu C=%u light=%u big=%u nbig=%u\n", (unsigned long long)m, nbl,
+                split->t.light, split->t.big, split->t.nbig);
+      set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>, sizeof(S1));
+      c->dom_begin("msd_scatter");
+      msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>
+          <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
+              ks, m, out_k, out_v, shift, dl[l], bshift, c->scur.as<uint32_t>(), reinterpret_cast<KeyT*>(split->hk),
+              split->hv);
+    } else {
+      scan_counts(c, h2, nbl, off, cur);
+      set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>, sizeof(S1));
+      c->dom_begin("msd_scatter");
+      msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>
+          <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(ks, m, out_k, out_v, shift, dl[l],
+                                                                                 bshift, cur);
+    }
     CK_LAUNCH();
     c->dom_end(2 * kItem * m);
     c->launches += 3;
@@ -630,47 +683,227 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   return m;
 }
 
-// heavy bucket list of the last local kernel -> (count, host ranges, device dst offsets)
-uint64_t fetch_heavy(nmx_ctx* c, uint32_t* d_count, uint32_t* nheavy_out) {
-  uint32_t nheavy = 0;
-  CK(cudaMemcpyAsync(&nheavy, d_count, 4, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  *nheavy_out = nheavy;
-  if (!nheavy) return 0;
-  std::vector<uint32_t> hr(2 * (size_t)nheavy), dof(nheavy);
-  CK(cudaMemcpyAsync(hr.data(), c->mheavy.p, hr.size() * 4, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  uint64_t total = 0;
-  for (uint32_t r = 0; r < nheavy; ++r) {
-    dof[r] = (uint32_t)total;
-    total += hr[2 * r + 1] - hr[2 * r];
-  }
-  c->mdst.grow((size_t)nheavy * 4);
-  CK(cudaMemcpyAsync(c->mdst.p, dof.data(), (size_t)nheavy * 4, cudaMemcpyHostToDevice, c->st));
-  return total;
+// ---- segmented MSD levels over heavy buckets (nmx_seg.cuh) ------------------
+// split `bits` into ceil(bits / 7) near-equal level widths
+int split_levels(int bits, int* out) {
+  if (bits <= 0) return 0;
+  const int L = (bits + kMsdLevelBits - 1) / kMsdLevelBits;
+  for (int l = 0; l < L; ++l) out[l] = bits / L + (l < bits % L ? 1 : 0);
+  return L;
 }
 
-// groups of whole buckets (bucket starts inside one S-key chunk), their heavy
-// bucket, and the global heavy list (count at small[kCounters + 31])
-void plan_groups(nmx_ctx* c, const uint32_t* off, uint32_t nb, uint64_t m, uint32_t S, uint32_t capb) {
-  uint32_t* d_small = c->small.as<uint32_t>();
-  const uint32_t ngroups = (uint32_t)((m + S - 1) / S);
+// count + classify one level of P positional parents (m items) into C = P << dbits
+// children; leaves child counts in sccnt, cursors in scur, light offsets in
+// sloff, next parents in `npoff`
+template <typename KeyT, bool HAS_VAL>
+SegTotals seg_level_plan(nmx_ctx* c, const KeyT* k, const uint32_t* v, uint32_t m, const uint32_t* poff, uint32_t P,
+                         int shift, int dbits, uint32_t* npoff) {
+  const uint32_t C = P << dbits;
+  c->sccnt.grow(((size_t)C + 8) * 4);
+  uint32_t* ccnt = c->sccnt.as<uint32_t>();
+  CK(cudaMemsetAsync(ccnt, 0, (size_t)C * 4, c->st));
+  seg_count_kernel<KeyT, HAS_VAL, false><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(
+      k, v, m, poff, P, shift, dbits, ccnt, nullptr, nullptr);
+  CK_LAUNCH();
+  ++c->launches;
+  return seg_classify(c, ccnt, C, npoff);
+}
+
+// shared-memory groups over this level's light children (loff = sloff, C children)
+uint32_t seg_plan_groups(nmx_ctx* c, uint32_t C, uint32_t light) {
+  const uint32_t S = kSegCap;
+  const uint32_t ngroups = (light + S - 1) / S;
   c->mgb.grow(((size_t)ngroups + 2) * 4);
-  c->mgh.grow(((size_t)ngroups + 2) * 8);
   c->mplan.grow(((size_t)ngroups + 2) * 16);
-  c->mheavy.grow(((size_t)ngroups + 2) * 8);
   const unsigned g1 = (unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8);
-  group_bounds_kernel<<<g1, 256, 0, c->st>>>(off, nb, S, ngroups, c->mgb.as<uint32_t>());
+  group_bounds_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), C, S, ngroups, c->mgb.as<uint32_t>());
   CK_LAUNCH();
-  CK(cudaMemsetAsync(c->mgh.p, 0, (size_t)ngroups * 8, c->st));
-  CK(cudaMemsetAsync(d_small + kCounters + 31, 0, 4, c->st));
-  bucket_heavy_kernel<<<(unsigned)std::min<uint64_t>((nb + 255) / 256, (uint64_t)c->sms * 8), 256, 0, c->st>>>(
-      off, nb, S, capb, c->mgh.as<uint2>(), c->mheavy.as<uint32_t>(), d_small + kCounters + 31);
+  seg_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), ngroups,
+                                         c->mplan.as<uint4>());
   CK_LAUNCH();
-  group_plan_kernel<<<g1, 256, 0, c->st>>>(off, c->mgb.as<uint32_t>(), c->mgh.as<uint2>(), ngroups,
-                                           c->mplan.as<uint4>());
-  CK_LAUNCH();
-  c->launches += 3;
+  c->launches += 2;
+  return ngroups;
+}
+
+// Heavy row buckets (mh keys in keysC, nheavy parents at spoffA):
+// levels over the remaining b - D source bits (children stay whole sources,
+// local_rows_kernel<false>), then over the b destination bits (every parent is
+// one source: local_rows_kernel<true> with the SrcTable), final level
+// count-only (one link per child). Column entries go to ckA / cvA; returns
+// their number.
+uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int cshift, uint32_t* chist,
+                    unsigned long long* ccount) {
+  int w[16];
+  int L = split_levels(b - D, w);
+  const int Ls = L;
+  L += split_levels(b, w + L);
+  const int kb = 2 * b;
+  c->lightK.grow(mh * 8);
+  uint32_t* poff = c->spoffA.as<uint32_t>();
+  uint64_t* in = c->keysC.as<uint64_t>();
+  uint64_t* out = c->keysD.as<uint64_t>();
+  uint32_t* hcol_dst = c->ckA.as<uint32_t>();
+  uint32_t* hcol_cnt = c->cvA.as<uint32_t>();
+  uint32_t P = nheavy, m = (uint32_t)mh;
+  uint64_t lbase = 0;
+  int consumed = D;
+  SrcTable gsrc;
+  bool table = false;
+  set_smem(seg_scatter_kernel<uint64_t, false>, sizeof(SegSmem<uint64_t, false>));
+  set_smem(local_rows_kernel<false>, sizeof(LocSmem));
+  set_smem(local_rows_kernel<true>, sizeof(LocSmem));
+  for (int l = 0; l < L && m; ++l) {
+    const int dbits = w[l];
+    const bool partial = l >= Ls;  // parents are single sources
+    if (partial && !table) {       // roots = the parents of the first destination level
+      uint32_t cap = 1024;
+      while (cap < 2 * P + 16) cap <<= 1;
+      c->gsk.grow(((size_t)cap + 2) * 4);
+      c->gsv.grow(((size_t)cap + 2) * 8);
+      CK(cudaMemsetAsync(c->gsk.p, 0, ((size_t)cap + 2) * 4, c->st));
+      CK(cudaMemsetAsync(c->gsv.p, 0, ((size_t)cap + 2) * 8, c->st));
+      gsrc.keys = c->gsk.as<uint32_t>();
+      gsrc.vals = c->gsv.as<unsigned long long>();
+      gsrc.mask = cap - 1;
+      table = true;
+    }
+    consumed += dbits;
+    const int shift = kb - consumed;
+    const uint32_t C = P << dbits;
+    if (l + 1 == L) {  // final level: count only, one link per child
+      c->sccnt.grow(((size_t)C + 8) * 4);
+      c->srep.grow(((size_t)C + 8) * 8);
+      c->hcount.grow(64);
+      uint32_t* ccnt = c->sccnt.as<uint32_t>();
+      CK(cudaMemsetAsync(ccnt, 0, (size_t)C * 4, c->st));
+      CK(cudaMemsetAsync(c->hcount.p, 0, 8, c->st));
+      seg_count_kernel<uint64_t, false, true><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(
+          in, nullptr, m, poff, P, shift, dbits, ccnt, nullptr, c->srep.as<uint64_t>());
+      CK_LAUNCH();
+      const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((C + 4095) / 4096, (uint64_t)c->sms * 4));
+      seg_emit_rows_kernel<<<g, 256, 0, c->st>>>(ccnt, c->srep.as<uint64_t>(), C, b, hcol_dst + lbase,
+                                                 hcol_cnt + lbase, c->hcount.as<unsigned long long>(), cshift, chist,
+                                                 ccount, c->stats.as<unsigned long long>(), gsrc);
+      CK_LAUNCH();
+      c->launches += 2;
+      unsigned long long hc = 0;
+      CK(cudaMemcpyAsync(&hc, c->hcount.p, 8, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      lbase += hc;
+      m = 0;
+      break;
+    }
+    DevBuf& nb = (l & 1) ? c->spoffA : c->spoffB;
+    // next parents: at most min(C, m / (kSegCap + 1)) big children
+    nb.grow(((size_t)std::min<uint64_t>(C, m / (kSegCap + 1) + 1) + 8) * 4);
+    uint32_t* npoff = nb.as<uint32_t>();
+    const SegTotals t = seg_level_plan<uint64_t, false>(c, in, nullptr, m, poff, P, shift, dbits, npoff);
+    if (getenv("NMX_DEBUG"))
+      fprintf(stderr, "heavy_rows l=%d P=%u m=%u C=%u dbits=%d shift=%d light=%u big=%u nbig=%u\n", l, P, m, C, dbits,
+              shift, t.light, t.big, t.nbig);
+    seg_scatter_kernel<uint64_t, false><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads,
+                                          sizeof(SegSmem<uint64_t, false>), c->st>>>(
+        in, nullptr, m, poff, P, shift, dbits, c->scur.as<uint32_t>(), c->lightK.as<uint64_t>() + lbase, nullptr, out,
+        nullptr);
+    CK_LAUNCH();
+    ++c->launches;
+    if (t.light) {
+      const uint32_t ngroups = seg_plan_groups(c, C, t.light);
+      const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 2);
+      if (partial)
+        local_rows_kernel<true><<<grid, kLocThreads, sizeof(LocSmem), c->st>>>(
+            c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol_dst + lbase, hcol_cnt + lbase,
+            cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc);
+      else
+        local_rows_kernel<false><<<grid, kLocThreads, sizeof(LocSmem), c->st>>>(
+            c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol_dst + lbase, hcol_cnt + lbase,
+            cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc);
+      CK_LAUNCH();
+      ++c->launches;
+    }
+    lbase += t.light;
+    std::swap(in, out);
+    poff = npoff;
+    P = t.nbig;
+    m = t.big;
+  }
+  if (table) {
+    const uint32_t ents = gsrc.mask + 2;
+    src_table_stats_kernel<<<(unsigned)std::min<uint64_t>((ents + 255) / 256, (uint64_t)c->sms * 4), 256, 0, c->st>>>(
+        gsrc, c->stats.as<unsigned long long>());
+    CK_LAUNCH();
+    ++c->launches;
+  }
+  return lbase;
+}
+
+// Heavy destination buckets ((dst, count) entries in cgk / cgv, nheavy
+// parents at spoffA): levels over the remaining b - Dc destination bits
+// (children stay whole destinations, local_cols_kernel), final level
+// count-only with packet sums (one destination per child).
+void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
+  int w[8];
+  int L = split_levels(b - Dc, w);
+  if (!L) w[L++] = 0;  // the dense levels already isolate single destinations
+  c->lightCK.grow(ch * 4);
+  c->lightCV.grow(ch * 4);
+  uint32_t* poff = c->spoffA.as<uint32_t>();
+  uint32_t* ink = c->cgk.as<uint32_t>();
+  uint32_t* inv = c->cgv.as<uint32_t>();
+  uint32_t* outk = c->cgk2.as<uint32_t>();
+  uint32_t* outv = c->cgv2.as<uint32_t>();
+  uint32_t P = nheavy, m = (uint32_t)ch;
+  uint64_t lbase = 0;
+  int consumed = Dc;
+  set_smem(seg_scatter_kernel<uint32_t, true>, sizeof(SegSmem<uint32_t, true>));
+  set_smem(local_cols_kernel, sizeof(LocColSmem));
+  for (int l = 0; l < L && m; ++l) {
+    const int dbits = w[l];
+    consumed += dbits;
+    const int shift = b - consumed;
+    const uint32_t C = P << dbits;
+    if (l + 1 == L) {
+      c->sccnt.grow(((size_t)C + 8) * 4);
+      c->ssum.grow(((size_t)C + 8) * 8);
+      uint32_t* ccnt = c->sccnt.as<uint32_t>();
+      CK(cudaMemsetAsync(ccnt, 0, (size_t)C * 4, c->st));
+      CK(cudaMemsetAsync(c->ssum.p, 0, (size_t)C * 8, c->st));
+      seg_count_kernel<uint32_t, true, true><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(
+          ink, inv, m, poff, P, shift, dbits, ccnt, c->ssum.as<unsigned long long>(), nullptr);
+      CK_LAUNCH();
+      const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((C + 255) / 256, (uint64_t)c->sms * 8));
+      seg_emit_cols_kernel<<<g, 256, 0, c->st>>>(ccnt, c->ssum.as<unsigned long long>(), C,
+                                                 c->stats.as<unsigned long long>());
+      CK_LAUNCH();
+      c->launches += 2;
+      break;
+    }
+    DevBuf& nb = (l & 1) ? c->spoffA : c->spoffB;
+    nb.grow(((size_t)std::min<uint64_t>(C, m / (kSegCap + 1) + 1) + 8) * 4);
+    uint32_t* npoff = nb.as<uint32_t>();
+    const SegTotals t = seg_level_plan<uint32_t, true>(c, ink, inv, m, poff, P, shift, dbits, npoff);
+    seg_scatter_kernel<uint32_t, true><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads,
+                                         sizeof(SegSmem<uint32_t, true>), c->st>>>(
+        ink, inv, m, poff, P, shift, dbits, c->scur.as<uint32_t>(), c->lightCK.as<uint32_t>() + lbase,
+        c->lightCV.as<uint32_t>() + lbase, outk, outv);
+    CK_LAUNCH();
+    ++c->launches;
+    if (t.light) {
+      const uint32_t ngroups = seg_plan_groups(c, C, t.light);
+      const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3);
+      local_cols_kernel<<<grid, kLocThreads, sizeof(LocColSmem), c->st>>>(
+          c->lightCK.as<uint32_t>() + lbase, c->lightCV.as<uint32_t>() + lbase, c->mplan.as<uint4>(), ngroups,
+          c->stats.as<unsigned long long>());
+      CK_LAUNCH();
+      ++c->launches;
+    }
+    lbase += t.light;
+    std::swap(ink, outk);
+    std::swap(inv, outv);
+    poff = npoff;
+    P = t.nbig;
+    m = t.big;
+  }
 }
 
 // Column statistics of (dst, count) entries (holes allowed) read through `cs`,
@@ -678,60 +911,46 @@ void plan_groups(nmx_ctx* c, const uint32_t* off, uint32_t nb, uint64_t m, uint3
 // second level writes ckA / cvA): MSD partition by destination bits ->
 // shared-memory grouping -> heavy destinations via LSD + col_kernel.
 void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32_t* prehist) {
-  const uint32_t S = 1024, capb = 1024;
-  uint32_t* d_small = c->small.as<uint32_t>();
   uint32_t* ck = nullptr;
   uint32_t* cv = nullptr;
   const uint64_t need = cs.n;
   c->ckB.grow(need * 4);
   c->cvB.grow(need * 4);
+  c->cgk.grow(need * 4);
+  c->cgv.grow(need * 4);
+  MsdSplit sp;
+  sp.hk = c->cgk.p;
+  sp.hv = c->cgv.as<uint32_t>();
   const uint64_t u = msd_partition<ColConcatSrc, uint32_t, true>(c, cs, cs.n, b, Dc, c->ckB.as<uint32_t>(),
                                                                  c->cvB.as<uint32_t>(), c->ckA.as<uint32_t>(),
-                                                                 c->cvA.as<uint32_t>(), &ck, &cv, prehist);
+                                                                 c->cvA.as<uint32_t>(), &ck, &cv, prehist, &sp);
   c->mark();  // column partition end
   if (!u) return;
-  const uint32_t nbc = 1u << Dc;
-  uint32_t* off = c->moff.as<uint32_t>();
-  const uint32_t ngroups = (uint32_t)((u + S - 1) / S);
-  plan_groups(c, off, nbc, u, S, capb);
-  set_smem(local_cols_kernel, sizeof(LocColSmem));
-  local_cols_kernel<<<(unsigned)(c->sms * 3), kLocThreads, sizeof(LocColSmem), c->st>>>(
-      ck, cv, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>());
-  CK_LAUNCH();
-  ++c->launches;
-  c->mark();  // local columns end
-  uint32_t nheavy = 0;
-  const uint64_t ch = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
-  if (ch) {  // heavy destination buckets: gather -> LSD sort -> column kernel
-    c->cgk.grow(ch * 4);
-    c->cgv.grow(ch * 4);
-    c->cgk2.grow(ch * 4);
-    c->cgv2.grow(ch * 4);
-    gather_pairs_kernel<<<(unsigned)std::min<uint64_t>((ch + 255) / 256, (uint64_t)c->sms * 16), 256, 0, c->st>>>(
-        ck, cv, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, (uint32_t)ch, c->cgk.as<uint32_t>(),
-        c->cgv.as<uint32_t>());
-    CK_LAUNCH();
-    auto sorted = sort_u32_pairs(c, c->cgk.as<uint32_t>(), c->cgv.as<uint32_t>(), ch, b, c->cgk2.as<uint32_t>(),
-                                 c->cgv2.as<uint32_t>());
-    if (c->csstatus.grow(tiles_of(ch, kSegTile) * sizeof(CSStatus)))
-      CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
-    col_kernel<uint32_t, kSegIPT><<<(unsigned)tiles_of(ch, kSegTile), 256, 0, c->st>>>(
-        sorted.first, sorted.second, (uint32_t)ch, b, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
-        d_small + kCounters + 26, c->stats.as<unsigned long long>());
+  if (sp.t.light) {
+    const uint32_t ngroups = seg_plan_groups(c, 1u << Dc, sp.t.light);
+    set_smem(local_cols_kernel, sizeof(LocColSmem));
+    local_cols_kernel<<<(unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3), kLocThreads,
+                        sizeof(LocColSmem), c->st>>>(ck, cv, c->mplan.as<uint4>(), ngroups,
+                                                     c->stats.as<unsigned long long>());
     CK_LAUNCH();
     ++c->launches;
+  }
+  c->mark();  // local columns end
+  if (sp.t.big) {  // heavy destination buckets: segmented MSD levels (nmx_seg.cuh)
+    c->cgk2.grow((size_t)sp.t.big * 4);
+    c->cgv2.grow((size_t)sp.t.big * 4);
+    heavy_cols(c, sp.t.big, sp.t.nbig, b, Dc);
   }
 }
 
 void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
                       int b, int D) {
   const int kb = 2 * b;
-  const uint32_t S = 1024, capb = 1024;
   stage_begin(c, 1);
-  uint32_t* d_small = c->small.as<uint32_t>();
   // every buffer the step needs is sized up front (n bounds m, u and the heavy parts)
   c->keysA.grow(n * 8);
   c->keysB.grow(n * 8);
+  c->keysC.grow(n * 8);
   c->colL_dst.grow(n * 4);
   c->colL_cnt.grow(n * 4);
   c->ckA.grow(n * 4);
@@ -745,8 +964,11 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   c->mark();  // 1: row partition start
   uint64_t* keys = nullptr;
   uint32_t* dummy = nullptr;
+  MsdSplit sp;
+  sp.hk = c->keysC.p;
   const uint64_t m = msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
-                                                               c->keysB.as<uint64_t>(), nullptr, &keys, &dummy);
+                                                               c->keysB.as<uint64_t>(), nullptr, &keys, &dummy,
+                                                               nullptr, &sp);
   c->last_sort_launches = c->msd_levels;
   c->mark();  // 2: row partition end
   if (!m) {
@@ -754,9 +976,6 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     return;
   }
   const uint32_t nb = 1u << D;
-  uint32_t* off = c->moff.as<uint32_t>();
-  uint32_t ngroups = (uint32_t)((m + S - 1) / S);
-  plan_groups(c, off, nb, m, S, capb);
   const int Dc = std::min(D, b);
   const int cshift = b - msd_first_bits(Dc);
   // the column partition's first-level histogram + entry count, produced by the row stages
@@ -764,42 +983,29 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   uint32_t* chist = c->mch.as<uint32_t>();
   auto* ccount = reinterpret_cast<unsigned long long*>(chist + kMsdMaxBins);
   CK(cudaMemsetAsync(chist, 0, (kMsdMaxBins + 4) * 4, c->st));
-  set_smem(local_rows_kernel, sizeof(LocSmem));
-  local_rows_kernel<<<(unsigned)(c->sms * 2), kLocThreads, sizeof(LocSmem), c->st>>>(
-      keys, c->mplan.as<uint4>(), ngroups, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), cshift,
-      chist, ccount, c->stats.as<unsigned long long>());
-  CK_LAUNCH();
-  ++c->launches;
-  c->mark();  // 3: local rows end
-  uint32_t nheavy = 0;
-  const uint64_t mh = fetch_heavy(c, d_small + kCounters + 31, &nheavy);
-  uint64_t uh = 0;
-  if (mh) {  // heavy row buckets: gather -> LSD sort -> fused link/row kernel
-    c->keysC.grow(mh * 8);
-    c->keysD.grow(mh * 8);
-    gather_ranges_kernel<<<(unsigned)std::min<uint64_t>((mh + 255) / 256, (uint64_t)c->sms * 16), 256, 0, c->st>>>(
-        keys, c->mheavy.as<uint32_t>(), c->mdst.as<uint32_t>(), nheavy, (uint32_t)mh, c->keysC.as<uint64_t>(),
-        c->colL_cnt.as<uint32_t>());
+  if (sp.t.light) {
+    const uint32_t ngroups = seg_plan_groups(c, nb, sp.t.light);
+    set_smem(local_rows_kernel<false>, sizeof(LocSmem));
+    local_rows_kernel<false><<<(unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 2), kLocThreads,
+                               sizeof(LocSmem), c->st>>>(keys, c->mplan.as<uint4>(), ngroups, b,
+                                                         c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
+                                                         cshift, chist, ccount, c->stats.as<unsigned long long>(),
+                                                         SrcTable{});
     CK_LAUNCH();
-    uint64_t* hs = sort_keys_u64(c, c->keysC.as<uint64_t>(), mh, kb, c->keysD.as<uint64_t>());
-    if (c->lrstatus.grow(tiles_of(mh, kSegTile) * sizeof(LRStatus)))
-      CK(cudaMemsetAsync(c->lrstatus.p, 0, c->lrstatus.cap, c->st));
-    launch_link_row<uint32_t>(c, hs, (uint32_t)mh, b, 0, d_small);  // entries -> ckA / cvA
-    CK(cudaMemcpyAsync(c->h_small + kU, d_small + kU, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    uh = c->h_small[kU];
-    if (uh) {  // their share of the column partition's first-level histogram
-      KeySrc<uint32_t, true> hk{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh};
-      const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uh + 2047) / 2048, (uint64_t)c->sms * 8));
-      msd_hist1_kernel<KeySrc<uint32_t, true>, uint32_t><<<hgrid, 256, 0, c->st>>>(hk, uh, cshift, chist, ccount);
-      CK_LAUNCH();
-    }
+    ++c->launches;
+  }
+  c->mark();  // 3: local rows end
+  uint64_t uh = 0;
+  if (sp.t.big) {  // heavy row buckets: segmented MSD levels (nmx_seg.cuh)
+    c->keysD.grow((size_t)sp.t.big * 8);
+    uh = heavy_rows(c, sp.t.big, sp.t.nbig, b, D, cshift, chist, ccount);
   }
   c->mark();  // 4: heavy rows end
 
   // ---- columns: MSD partition of the (dst, count) entries by destination bits ----
-  ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), m,
-                  c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), uh, m + uh};
+  ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), sp.t.light,
+                  c->ckA.as<uint32_t>(),      c->cvA.as<uint32_t>(),      uh,
+                  sp.t.light + uh};
   cs.quad = true;  // context buffers are cudaMalloc-aligned
   msd_columns(c, cs, b, Dc, chist);
   stage_finish(c, 1);

@@ -60,6 +60,53 @@ __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Warp-aggregated shared-memory counters for skewed (power-law) tiles: when all
+// 32 lanes of a round carry the same bin (a tile of one heavy source or
+// destination) one lane adds 32; otherwise every lane adds its own 1 (no extra
+// dependency on the uniform path). Must be called by all 32 lanes; bin < 0 =
+// no item. agg_rank returns the lane's rank within its bin.
+// Cheap per-warp skew probe (one round): at least half the lanes share lane
+// 0's bin. Only skewed warps pay for the per-round uniformity checks below.
+__device__ __forceinline__ bool warp_skewed(int bin) {
+  const int b0 = __shfl_sync(FULL, bin, 0);
+  return b0 >= 0 && __popc(__ballot_sync(FULL, bin == b0)) >= 16;
+}
+__device__ __forceinline__ uint32_t agg_rank(uint32_t* cnt, int bin) {
+  const int b0 = __shfl_sync(FULL, bin, 0);
+  if (__all_sync(FULL, bin == b0) && b0 >= 0) {
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&cnt[b0], 32u);
+    return __shfl_sync(FULL, base, 0) + (uint32_t)lane;
+  }
+  return bin >= 0 ? atomicAdd(&cnt[bin], 1u) : 0u;
+}
+__device__ __forceinline__ void agg_count(uint32_t* cnt, int bin) {
+  const int b0 = __shfl_sync(FULL, bin, 0);
+  if (__all_sync(FULL, bin == b0)) {
+    if (b0 >= 0 && (threadIdx.x & 31) == 0) atomicAdd(&cnt[b0], 32u);
+  } else if (bin >= 0) {
+    atomicAdd(&cnt[bin], 1u);
+  }
+}
+// + a u64 value per item (final column level: packet sums per destination)
+__device__ __forceinline__ void agg_count_sum(uint32_t* cnt, unsigned long long* sum, int bin, uint32_t v) {
+  const int b0 = __shfl_sync(FULL, bin, 0);
+  if (__all_sync(FULL, bin == b0)) {
+    if (b0 < 0) return;
+    unsigned long long x = v;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd(&cnt[b0], 32u);
+      atomicAdd(&sum[b0], x);
+    }
+  } else if (bin >= 0) {
+    atomicAdd(&cnt[bin], 1u);
+    atomicAdd(&sum[bin], (unsigned long long)v);
+  }
+}
+
 // Tile status word for single-value lookback scans:
 //   [63:42] epoch (22 bits, never 0 once written) | [41:40] flag | [39:0] value
 // The epoch tag lets one status array serve every pass without a memset: a

@@ -94,10 +94,16 @@ struct MsdSmem {
   uint64_t b1first;
 };
 
-template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL>
+// SPLIT (last level): cursor values with kLightBit set address the light
+// output (out, vout), the others the heavy output (hout, hvout) -- buckets too
+// large for a shared-memory group leave the dense levels already compacted.
+constexpr uint32_t kLightBit = 0x80000000u;
+template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false>
 __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
                                                                    uint32_t* __restrict__ vout, int shift, int dbits,
-                                                                   int bshift, uint32_t* __restrict__ cursor) {
+                                                                   int bshift, uint32_t* __restrict__ cursor,
+                                                                   KeyT* __restrict__ hout = nullptr,
+                                                                   uint32_t* __restrict__ hvout = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -139,16 +145,27 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
         if (rel < 2) {
           bin[i] = (int)((rel << dbits) | d);
         } else {  // third+ level-1 bucket inside one tile: direct placement
-          const uint32_t pos = atomicAdd(cursor + (uint32_t)((uint64_t)k[i] >> shift), 1u);
-          out[pos] = k[i];
-          if (HAS_VAL) vout[pos] = v[i];
+          const uint32_t r = atomicAdd(cursor + (uint32_t)((uint64_t)k[i] >> shift), 1u);
+          if (!SPLIT || (r & kLightBit)) {
+            const uint32_t pos = SPLIT ? r & ~kLightBit : r;
+            out[pos] = k[i];
+            if (HAS_VAL) vout[pos] = v[i];
+          } else {
+            hout[r] = k[i];
+            if (HAS_VAL) hvout[r] = v[i];
+          }
         }
       }
     }
   }
+  if (warp_skewed(bin[0])) {
 #pragma unroll
-  for (int i = 0; i < kMsdIPT; ++i)
-    if (bin[i] >= 0) rank[i] = atomicAdd(&S.cnt[bin[i]], 1u);
+    for (int i = 0; i < kMsdIPT; ++i) rank[i] = agg_rank(S.cnt, bin[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kMsdIPT; ++i)
+      if (bin[i] >= 0) rank[i] = atomicAdd(&S.cnt[bin[i]], 1u);
+  }
   __syncthreads();
   // reserve each digit's output range first: the global atomics are in flight
   // while the block scan and the staging run
@@ -178,7 +195,8 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
 #pragma unroll
   for (int q = 0; q < kMsdScBins / kMsdThreads; ++q) {
     const int i = tid + q * kMsdThreads;
-    if (i < nbins && S.cnt[i]) S.gbase[i] = resv[q] - S.tstart[i];
+    if (i < nbins && S.cnt[i])
+      S.gbase[i] = SPLIT ? (resv[q] & kLightBit) | ((resv[q] - S.tstart[i]) & ~kLightBit) : resv[q] - S.tstart[i];
   }
   __syncthreads();
   const uint32_t total = S.tstart[nbins - 1] + S.cnt[nbins - 1];
@@ -189,9 +207,16 @@ __global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint6
       b = (int)((uint32_t)((uint64_t)key >> shift) & dmask);
     else
       b = (int)(((((uint64_t)key >> bshift) - b1first) << dbits) | (((uint64_t)key >> shift) & dmask));
-    const uint32_t pos = S.gbase[b] + j;
-    out[pos] = key;
-    if (HAS_VAL) vout[pos] = S.vstage[j];
+    const uint32_t g = S.gbase[b];
+    if (!SPLIT || (g & kLightBit)) {
+      const uint32_t pos = SPLIT ? (g + j) & ~kLightBit : g + j;
+      out[pos] = key;
+      if (HAS_VAL) vout[pos] = S.vstage[j];
+    } else {
+      const uint32_t pos = (g + j) & ~kLightBit;  // position arithmetic is modulo 2^31
+      hout[pos] = key;
+      if (HAS_VAL) hvout[pos] = S.vstage[j];
+    }
   }
 }
 
@@ -212,11 +237,10 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
     // two quads per thread: packets base + 4*(u*256 + tid) .. +4
     load_items<Src, KeyT>(src, base / 4 + threadIdx.x, 256, k, v, ok);
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (ok[u]) {
-        ++c;
-        atomicAdd(&h[(uint32_t)((uint64_t)k[u] >> shift)], 1u);
-      }
+    for (int u = 0; u < U; ++u) {
+      c += ok[u];
+      agg_count(h, ok[u] ? (int)((uint64_t)k[u] >> shift) : -1);
+    }
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
@@ -248,14 +272,16 @@ __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __r
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i) {
     const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
+    int bin = -1;
     if (idx < m) {
       const uint64_t key = (uint64_t)k[i];
       const uint64_t rel = (key >> bshift) - b1first;
       if (rel < 2)
-        atomicAdd(&cnt[(rel << dbits) | ((key >> shift) & dmask)], 1u);
+        bin = (int)((rel << dbits) | ((key >> shift) & dmask));
       else
         atomicAdd(hist2 + (uint32_t)(key >> shift), 1u);
     }
+    agg_count(cnt, bin);
   }
   __syncthreads();
   const int nbins = 2 << dbits;
@@ -263,34 +289,6 @@ __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __r
     const uint32_t c = cnt[i];
     if (c) atomicAdd(hist2 + (((b1first + (uint64_t)(i >> dbits)) << dbits) | (uint64_t)(i & dmask)), c);
   }
-}
-
-// exclusive scan of nb counters (single CTA, 1024 threads): off[0..nb], cursor = off
-__global__ void __launch_bounds__(1024) big_excl_scan_kernel(const uint32_t* __restrict__ cnt, uint32_t nb,
-                                                            uint32_t* __restrict__ off, uint32_t* __restrict__ cursor) {
-  __shared__ uint32_t wt[33];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t per = (nb + 1023) / 1024;
-  const uint32_t lo = tid * per, hi = min(nb, lo + per);
-  uint32_t s = 0;
-  for (uint32_t i = lo; i < hi; ++i) s += cnt[i];
-  const uint32_t inc = warp_incl_scan(s, lane);
-  if (lane == 31) wt[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t v = wt[lane];
-    const uint32_t vi = warp_incl_scan(v, lane);
-    wt[lane] = vi - v;
-    if (lane == 31) wt[32] = vi;
-  }
-  __syncthreads();
-  uint32_t run = wt[warp] + inc - s;
-  for (uint32_t i = lo; i < hi; ++i) {
-    off[i] = run;
-    if (cursor) cursor[i] = run;
-    run += cnt[i];
-  }
-  if (tid == 0) off[nb] = wt[32];
 }
 
 // multi-CTA exclusive scan of n u32 counters (4096 per block, coalesced):
@@ -385,32 +383,6 @@ constexpr int kLocThreads = 512;
 constexpr int kLocMaxKeys = 2048;  // light keys per group (chunk S + one light bucket)
 constexpr int kLocT1 = 3072;       // link table slots (load <= 2/3)
 constexpr int kLocT2 = 3072;       // source table slots
-constexpr int kLocMaxHeavy = 8;
-
-// heavy buckets (size > capb): recorded once in the global list for the LSD
-// fallback and as the (single) excluded range of the group their start lies in
-__global__ void bucket_heavy_kernel(const uint32_t* __restrict__ off, uint32_t nb, uint32_t S, uint32_t capb,
-                                    uint2* __restrict__ gheavy, uint32_t* __restrict__ heavy,
-                                    uint32_t* __restrict__ nheavy) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nb; j += gridDim.x * blockDim.x) {
-    const uint32_t lo = off[j], hi = off[j + 1];
-    if (hi - lo > capb) {
-      gheavy[lo / S] = make_uint2(lo, hi);
-      const uint32_t q = atomicAdd(nheavy, 1u);
-      heavy[2 * q] = lo;
-      heavy[2 * q + 1] = hi;
-    }
-  }
-}
-
-// plan[g] = {klo, khi, hlo, hhi}: group g's keys and its excluded heavy range
-__global__ void group_plan_kernel(const uint32_t* __restrict__ off, const uint32_t* __restrict__ gb,
-                                  const uint2* __restrict__ gheavy, uint32_t ngroups, uint4* __restrict__ plan) {
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
-    const uint2 h = gheavy[g];
-    plan[g] = make_uint4(off[gb[g]], off[gb[g + 1]], h.x, h.y);
-  }
-}
 
 // light position j of a group -> global index (the heavy range is skipped)
 __device__ __forceinline__ uint32_t light_index(const uint4& p, uint32_t j) {
@@ -436,6 +408,32 @@ __device__ __forceinline__ bool bm_once(const uint32_t* bm, uint32_t h) {
   return ((bm[h >> 4] >> ((h & 15) * 2)) & 3u) == 1u;
 }
 
+// Global per-source accumulator for sources split across groups: open
+// addressing over src + 1 (0 = empty), value = fan-out << 32 | packets (both
+// < 2^32 since n < 2^32); slot mask + 1 is reserved for src 0xFFFFFFFF.
+struct SrcTable {
+  uint32_t* keys = nullptr;
+  unsigned long long* vals = nullptr;
+  uint32_t mask = 0;
+  __device__ __forceinline__ void add(uint32_t src, unsigned long long v) const {
+    if (src == 0xFFFFFFFFu) {
+      keys[mask + 1] = 1u;
+      atomicAdd(vals + mask + 1, v);
+      return;
+    }
+    const uint32_t k = src + 1;
+    uint32_t h = (uint32_t)(((uint64_t)k * 0x9E3779B97F4A7C15ull) >> 40) & mask;
+    for (;;) {
+      const uint32_t c0 = atomicCAS(keys + h, 0u, k);
+      if (c0 == 0u || c0 == k) {
+        atomicAdd(vals + h, v);
+        return;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+};
+
 struct LocSmem {
   uint32_t bml[kBmWords];            // link-key hash counters
   uint32_t bms[kBmWords];            // source hash counters
@@ -459,11 +457,18 @@ struct LocSmem {
 // Groups are statically round-robined over persistent CTAs; thread 0 fetches the
 // next group's plan during the counting and every thread loads its next keys
 // into registers while the current group's results are written.
+//
+// PARTIAL (heavy sources split over several groups by destination-bit levels,
+// nmx_seg.cuh): links are still complete per group, but each source's packets
+// and fan-out are partial; they are summed per warp (all lanes usually share
+// one source), per group in the exact source table, and per source in the
+// global table `gsrc` (one atomic per source and group).
+template <bool PARTIAL>
 __global__ void __launch_bounds__(kLocThreads, 2)
     local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
                       uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt, int cshift,
                       uint32_t* __restrict__ chist, unsigned long long* __restrict__ ccount,
-                      unsigned long long* __restrict__ stats) {
+                      unsigned long long* __restrict__ stats, SrcTable gsrc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     for (int r = 0; r < kLocPerThread; ++r) {
       if ((uint32_t)r < nmine) {
         bm_hit(s.bml, h16(kr[r]));
-        bm_hit(s.bms, h16(kr[r] >> b));
+        if (!PARTIAL) bm_hit(s.bms, h16(kr[r] >> b));
       }
     }
     if (tid == 0) s.plan[cur ^ 1] = pnext;
@@ -569,6 +574,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         }
         hl[r] = h;
       }
+      if (PARTIAL) continue;  // sources: warp-aggregated below
       if (src == 0xFFFFFFFFu) {
         atomicAdd(&s.sp_src_pk, 1u);
         if (fresh) atomicAdd(&s.sp_src_fo, 1u);
@@ -593,6 +599,53 @@ __global__ void __launch_bounds__(kLocThreads, 2)
           h = h + 1 == kLocT2 ? 0 : h + 1;
         }
         hs[r] = h;
+      }
+    }
+    if constexpr (PARTIAL) {
+      // every lane runs every r (ballots): lanes sharing the warp leader's source
+      // add once; the source-table creator (bit 8) flushes it after the barrier
+#pragma unroll
+      for (int r = 0; r < kLocPerThread; ++r) {
+        const bool v = (uint32_t)r < nmine;
+        const uint32_t src = v ? (uint32_t)(kr[r] >> b) : 0u;
+        const bool fr = v && (st[r] & 3u);
+        const uint32_t vm = __ballot_sync(FULL, v);
+        if (!vm) continue;
+        const int leader = __ffs(vm) - 1;
+        const uint32_t ls = __shfl_sync(FULL, src, leader);
+        const uint32_t same = __ballot_sync(FULL, v && src == ls);
+        const uint32_t fm = __ballot_sync(FULL, fr);
+        uint32_t add_pk = 0, add_fo = 0;
+        if (same == vm) {
+          if (lane == leader) add_pk = __popc(vm), add_fo = __popc(fm);
+        } else if (v) {
+          add_pk = 1, add_fo = fr ? 1u : 0u;
+        }
+        if (add_pk) {
+          if (src == 0xFFFFFFFFu) {
+            atomicAdd(&s.sp_src_pk, add_pk);
+            atomicAdd(&s.sp_src_fo, add_fo);
+          } else {
+            const uint32_t sk = src + 1;
+            uint32_t h = hslot(sk, kLocT2);
+            for (;;) {
+              uint32_t c0 = s.t2key[h];
+              if (c0 == 0) {
+                c0 = atomicCAS(&s.t2key[h], 0u, sk);
+                if (c0 == 0) {
+                  st[r] |= 8;
+                  c0 = sk;
+                }
+              }
+              if (c0 == sk) {
+                atomicAdd(&s.t2pf[h], add_pk | (add_fo << 16));
+                break;
+              }
+              h = h + 1 == kLocT2 ? 0 : h + 1;
+            }
+            hs[r] = h;
+          }
+        }
       }
     }
     __syncthreads();
@@ -628,9 +681,13 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         a_mfan = max(a_mfan, 1ull);
       } else if (st[r] & 8) {
         const uint32_t pf = s.t2pf[hs[r]];
-        a_srcs += 1;
-        a_msrc = max(a_msrc, (unsigned long long)(pf & 0xFFFFu));
-        a_mfan = max(a_mfan, (unsigned long long)(pf >> 16));
+        if (PARTIAL) {
+          gsrc.add((uint32_t)(key >> b), ((unsigned long long)(pf >> 16) << 32) | (pf & 0xFFFFu));
+        } else {
+          a_srcs += 1;
+          a_msrc = max(a_msrc, (unsigned long long)(pf & 0xFFFFu));
+          a_mfan = max(a_mfan, (unsigned long long)(pf >> 16));
+        }
         s.t2key[hs[r]] = 0;
         s.t2pf[hs[r]] = 0;
       }
@@ -638,9 +695,13 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       s.bms[h16(key >> b) >> 4] = 0;
     }
     if (tid == 0 && s.sp_src_pk) {
-      a_srcs += 1;
-      a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk);
-      a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo);
+      if (PARTIAL) {
+        gsrc.add(0xFFFFFFFFu, ((unsigned long long)s.sp_src_fo << 32) | s.sp_src_pk);
+      } else {
+        a_srcs += 1;
+        a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk);
+        a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo);
+      }
     }
     __syncthreads();
     if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;  // not touched before the next barrier
@@ -668,31 +729,6 @@ __global__ void __launch_bounds__(kLocThreads, 2)
   }
   __syncthreads();
   if (tid < (1 << kMsdLevelBits) && s.chist[tid]) atomicAdd(chist + tid, s.chist[tid]);
-}
-
-// gather heavy bucket ranges into one contiguous array
-// (and turn their slots of the light column array into holes). One thread per
-// gathered key: range r found by binary search over the destination offsets.
-__device__ __forceinline__ uint32_t range_of(const uint32_t* dstoff, uint32_t nranges, uint32_t t) {
-  uint32_t a = 0, z = nranges - 1;  // last r with dstoff[r] <= t
-  while (a < z) {
-    const uint32_t mid = (a + z + 1) >> 1;
-    if (dstoff[mid] <= t)
-      a = mid;
-    else
-      z = mid - 1;
-  }
-  return a;
-}
-__global__ void gather_ranges_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ranges,
-                                     const uint32_t* __restrict__ dstoff, uint32_t nranges, uint32_t total,
-                                     uint64_t* __restrict__ out, uint32_t* __restrict__ col_cnt) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const uint32_t r = range_of(dstoff, nranges, t);
-    const uint32_t i = ranges[2 * r] + (t - dstoff[r]);
-    out[t] = keys[i];
-    col_cnt[i] = 0;
-  }
 }
 
 // column entries from two arrays; entries with a zero count are holes
@@ -731,31 +767,6 @@ struct ColConcatSrc {
 
 __device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok) {
   s.load_quad(q, k, v, ok);
-}
-
-template <int NPASS>
-__global__ void __launch_bounds__(256) hist_concat_kernel(ColConcatSrc src, uint32_t* __restrict__ ghist,
-                                                         unsigned long long* __restrict__ gcount) {
-  __shared__ uint32_t h[NPASS][kRadix];
-  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) (&h[0][0])[i] = 0;
-  __syncthreads();
-  uint32_t c = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * 256 + threadIdx.x; i < src.n; i += (uint64_t)gridDim.x * 256) {
-    uint32_t k, v;
-    if (src.load(i, k, v)) {
-      ++c;
-#pragma unroll
-      for (int p = 0; p < NPASS; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFFu], 1u);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(gcount, (unsigned long long)c);
-  __syncthreads();
-  for (int i = threadIdx.x; i < NPASS * kRadix; i += 256) {
-    const uint32_t v = (&h[0][0])[i];
-    if (v) atomicAdd(ghist + i, v);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -907,19 +918,6 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     if (a_cnt) atomicAdd(stats + S_DSTS, a_cnt);
     if (a_fanin) atomicMax(stats + S_MAXFANIN, a_fanin);
     if (a_pk) atomicMax(stats + S_MAXDSTPK, a_pk);
-  }
-}
-
-// gather heavy (dst, count) ranges into contiguous arrays
-__global__ void gather_pairs_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
-                                    const uint32_t* __restrict__ ranges, const uint32_t* __restrict__ dstoff,
-                                    uint32_t nranges, uint32_t total, uint32_t* __restrict__ ok,
-                                    uint32_t* __restrict__ ov) {
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const uint32_t r = range_of(dstoff, nranges, t);
-    const uint32_t i = ranges[2 * r] + (t - dstoff[r]);
-    ok[t] = ck[i];
-    ov[t] = cv[i];
   }
 }
 
