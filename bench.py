@@ -217,8 +217,9 @@ def run_cfg5(args) -> None:
         "warmup": args.warmup, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"cfg5: {nwin} windows x 2^{int(np.log2(w))} packets {gen} streamed from pinned host "
-                               "memory (H2D of window t+1 overlaps the build of window t), log-structured merge-add, "
-                               "9 statistics of the summed matrix", "packets": n_total,
+                               "memory (nmx_stream_stats9: the H2D of window t+1 on a copy stream overlaps the "
+                               "level-1 partition of window t into the device-resident running sum; the remaining "
+                               "levels and the 9 statistics of the summed matrix run once)", "packets": n_total,
                    "timing": "wall clock of the host call (it is host-synchronous), best of steps"},
         "stats9": list(stats),
         "e2e": {"value": n_total / best, "unit": "packets/s", "h2d_bytes_per_step": 8 * n_total,

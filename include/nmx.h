@@ -84,6 +84,16 @@ int nmx_stats9_device(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst
 int nmx_stats9_host(nmx_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t address_space, int64_t out[9]);
 
+/* Streamed windows (BASELINE config 5): nine statistics of the matrix summed over
+ * `nwin` windows of HOST packet columns (src[k], dst[k], valid[k] or NULL, lens[k]
+ * packets; pinned memory for full host-link bandwidth), i.e. the cross-window sum
+ * A = sum_t A_t = build_matrices(concatenation, window_size=total) (traffic.py:221-242).
+ * The H2D copy of window k+1 overlaps the device work of window k (two streams);
+ * the total must be < 2^32 packets per device. valid may be NULL (all valid). */
+int nmx_stream_stats9(nmx_ctx* ctx, const uint32_t* const* src, const uint32_t* const* dst,
+                      const uint8_t* const* valid, const uint64_t* lens, uint64_t nwin, uint64_t address_space,
+                      int64_t out[9]);
+
 /* Per-window statistics: window t = packets [t*W, (t+1)*W) by raw position,
  * invalid packets keep their position (traffic.py:221-242); out has
  * ceil(n/W) rows of 9 (analyze_dataset per-window reports, analytics.py:109-130). */

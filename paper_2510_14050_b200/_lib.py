@@ -47,6 +47,7 @@ SIGNATURES = {
     "nmx_generate": (C.c_int, [_VP, C.c_int, _U64, _U64, _U64, _U64, _VP, _VP]),
     "nmx_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_stream_stats9": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_window_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_reduce_i64": (C.c_int, [_VP, _VP, _U64, C.c_int, _VP]),
@@ -227,6 +228,32 @@ def stats9(src, dst, valid=None, address_space: int = 1 << 32, device: int = 0) 
             raise ValueError("src, dst and valid must have equal lengths")
         check(ctx._lib.nmx_stats9_host(ctx.handle, _ptr(s), _ptr(d), _ptr(v), len(s), int(address_space),
                                        out.ctypes.data))
+    return tuple(int(x) for x in out)
+
+
+def stream_stats9(windows, address_space: int = 1 << 32, device: int = 0) -> tuple:
+    """Nine statistics of the matrix summed over host packet windows
+    (nmx_stream_stats9): ``windows`` = [(src, dst) or (src, dst, valid), ...] host
+    arrays (uint32 columns; pinned memory streams at full host-link bandwidth).
+    The H2D copy of window k+1 overlaps the device work of window k."""
+    ctx = context(device)
+    cols = []
+    for w in windows:
+        s, d = _u32_host(w[0]), _u32_host(w[1])
+        v = _valid_host(w[2]) if len(w) > 2 else None
+        if len(s) != len(d) or (v is not None and len(v) != len(s)):
+            raise ValueError("src, dst and valid must have equal lengths")
+        cols.append((s, d, v))
+    k = len(cols)
+    srcp = (C.c_void_p * max(k, 1))(*[c[0].ctypes.data for c in cols])
+    dstp = (C.c_void_p * max(k, 1))(*[c[1].ctypes.data for c in cols])
+    anyv = any(c[2] is not None for c in cols)
+    valp = (C.c_void_p * max(k, 1))(*[(c[2].ctypes.data if c[2] is not None else None) for c in cols])
+    lens = (C.c_uint64 * max(k, 1))(*[len(c[0]) for c in cols])
+    out = np.zeros(9, dtype=np.int64)
+    check(ctx._lib.nmx_stream_stats9(ctx.handle, srcp, dstp, valp if anyv else None, lens, k, int(address_space),
+                                     out.ctypes.data))
+    del cols
     return tuple(int(x) for x in out)
 
 

@@ -145,53 +145,10 @@ def stream_stats9(windows: Iterable, device: int = 0) -> tuple:
     return acc.result().stats9()
 
 
-def stream_stats9_pinned(windows, device: int = 0) -> tuple:
-    """BASELINE config 5: windows of packets in (pinned) host memory, streamed to
-    the device with the H2D copy of window t+1 on a second context's stream
-    overlapping the device build of window t, each window's COO folded into a
-    log-structured running sum (merge path). ``windows``: list of (src, dst)
-    uint32 host arrays (pinned for full PCIe bandwidth)."""
-    import threading
-
-    if not windows:
-        return (0,) * 9
-    ctx = _lib.context(device)
-    total = sum(len(w[0]) for w in windows)
-    # unique links <= packets, 12 B each; the log-structured sum holds at most about
-    # two copies plus one window's matrix at a time
-    reserve(min(int(total * 12 * 2.2), 120 << 30), device)
-    copier = _lib.Context(device)  # its own stream
-    cap = max(len(w[0]) for w in windows)
-    bufs = [(_lib.DeviceArray(cap, device=device), _lib.DeviceArray(cap, device=device)) for _ in range(2)]
-    errors: list = []
-
-    def upload(k):
-        s, d = windows[k]
-        ds, dd = bufs[k % 2]
-        try:
-            _lib.check(copier._lib.nmx_memcpy_h2d(copier.handle, ds._p, s.ctypes.data, s.nbytes))
-            _lib.check(copier._lib.nmx_memcpy_h2d(copier.handle, dd._p, d.ctypes.data, d.nbytes))
-        except Exception as e:  # pragma: no cover - surfaced below
-            errors.append(e)
-
-    acc = SummedMatrix(device)
-    t = threading.Thread(target=upload, args=(0,))
-    t.start()
-    for k in range(len(windows)):
-        t.join()
-        if errors:
-            raise errors[0]
-        if k + 1 < len(windows):
-            t = threading.Thread(target=upload, args=(k + 1,))
-            t.start()
-        ds, dd = bufs[k % 2]
-        n = len(windows[k][0])
-        h = C.c_void_p()
-        _lib.check(ctx._lib.nmx_coo_from_packets(ctx.handle, ds.data_ptr(), dd.data_ptr(), None, n, C.byref(h)))
-        acc.add(DeviceCOO(h, device))
-    out = acc.result().stats9()
-    for ds, dd in bufs:
-        ds.close()
-        dd.close()
-    copier.close()
-    return out
+def stream_stats9_pinned(windows, device: int = 0, address_space: int = 1 << 32) -> tuple:
+    """BASELINE config 5: windows of packets in (pinned) host memory streamed to the
+    device (nmx_stream_stats9): the H2D copy of window t+1 runs on a second stream
+    while window t is partitioned into the device-resident running sum; the
+    remaining partition levels and the statistics run once over the sum.
+    ``windows``: list of (src, dst[, valid]) host arrays."""
+    return _lib.stream_stats9(windows, address_space, device)

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/nmx.h"
+#include "nmx_merge.cuh"
 #include "nmx_seg.cuh"
 
 using namespace nmx;
@@ -75,6 +76,10 @@ struct DevBuf {
     p = nullptr;
     cap = 0;
   }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
 };
 
 // small device block layout (u32 words)
@@ -107,9 +112,11 @@ struct nmx_ctx {
   std::mutex mu;
   DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
-      red, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
+      red, ws0, ws1, wd0, wd1, wv0, wv1, msplit, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
       hcount;
   uint32_t epoch = 0;
+  cudaStream_t st2 = nullptr;  // copy stream of the streamed path
+  cudaEvent_t evc[2] = {nullptr, nullptr}, evu[2] = {nullptr, nullptr}, evs = nullptr;
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
   unsigned long long* h_stats = nullptr;
   size_t h_stats_cap = 0;
@@ -458,8 +465,9 @@ uint32_t run_rbk(nmx_ctx* c, const KeyT* keys, const uint32_t* w, uint32_t n, in
 int msd_bits(uint64_t n, int b) {
   const char* e = getenv("NMX_PATH");
   if (e && std::string(e) == "lsd") return 0;
-  if (n < (1ull << 20) || n > (1ull << 30)) return 0;
-  const int D = std::min(21, std::max(11, (int)ceil_log2(n) - 9));
+  // positions carry a light flag in bit 31 (nmx_seg.cuh): at most 2^31 keys
+  if (n < (1ull << 20) || n > (1ull << 31)) return 0;
+  const int D = std::min(22, std::max(11, (int)ceil_log2(n) - 9));
   return D <= b ? D : 0;
 }
 
@@ -582,6 +590,19 @@ SegTotals seg_classify(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* n
   return t;
 }
 
+// level widths of a D-bit dense partition: levels of <= kMsdLevelBits bits (128
+// bins per tile keeps the reservation atomics at one per 32 keys and every
+// digit's run in a tile ~32 keys long); returns the number of levels
+int msd_level_bits(int D, int* dl, int* cum) {
+  const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
+  for (int l = 0, acc = 0; l < L; ++l) {
+    dl[l] = D / L + (l < D % L ? 1 : 0);
+    acc += dl[l];
+    cum[l] = acc;
+  }
+  return L;
+}
+
 // last-level split of the dense MSD partition: light buckets stay in the level
 // output, heavy ones (> kSegCap) go compacted to (hk, hv), their offsets to spoffA
 struct MsdSplit {
@@ -593,20 +614,25 @@ struct MsdSplit {
 template <typename Src, typename KeyT, bool HAS_VAL>
 uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, KeyT* outA, uint32_t* voutA,
                        KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v,
-                       const uint32_t* prehist = nullptr, MsdSplit* split = nullptr) {
-  // levels of <= kMsdLevelBits bits: 128 bins per tile keeps the reservation
-  // atomics at one per 32 keys and every digit's run in a tile ~32 keys long
-  const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
+                       const uint32_t* prehist = nullptr, MsdSplit* split = nullptr, uint64_t pre_m = 0) {
   int dl[8], cum[8];
-  for (int l = 0, acc = 0; l < L; ++l) {
-    dl[l] = D / L + (l < D % L ? 1 : 0);
-    acc += dl[l];
-    cum[l] = acc;
-  }
+  const int L = msd_level_bits(D, dl, cum);
   const uint32_t nb = 1u << D;
   uint32_t* d_small = c->small.as<uint32_t>();
   auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
-  if (prehist) {  // first-level histogram (+ count) filled by the producer of `src`
+  c->mcur.grow(((size_t)nb + 8) * 4);
+  c->moff.grow(((size_t)nb + 8) * 4);
+  c->mhist2.grow(((size_t)nb + 8) * 4);
+  uint32_t* cur = c->mcur.as<uint32_t>();
+  uint32_t* off = c->moff.as<uint32_t>();
+  using S1 = MsdSmem<KeyT, HAS_VAL>;
+  constexpr uint64_t kItem = sizeof(KeyT) + (HAS_VAL ? 4 : 0);  // 8 B per item in and out
+  unsigned long long m = pre_m;
+  *res_k = outA;
+  *res_v = voutA;
+  if (pre_m) {
+    // level 1 already done window by window into outA (msd_window_level1)
+  } else if (prehist) {  // first-level histogram (+ count) filled by the producer of `src`
     CK(cudaMemcpyAsync(d_small + kHist, prehist, sizeof(uint32_t) * kMsdMaxBins, cudaMemcpyDeviceToDevice, c->st));
     CK(cudaMemcpyAsync(gcount, prehist + kMsdMaxBins, 8, cudaMemcpyDeviceToDevice, c->st));
   } else {
@@ -616,28 +642,20 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - dl[0], d_small + kHist, gcount);
     CK_LAUNCH();
   }
-  c->mcur.grow(((size_t)nb + 8) * 4);
-  c->moff.grow(((size_t)nb + 8) * 4);
-  c->mhist2.grow(((size_t)nb + 8) * 4);
-  uint32_t* cur = c->mcur.as<uint32_t>();
-  uint32_t* off = c->moff.as<uint32_t>();
-  scan_counts(c, d_small + kHist, 1u << dl[0], off, cur);
-  unsigned long long m = 0;
-  CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  c->launches += 2;
-  *res_k = outA;
-  *res_v = voutA;
-  if (!m) return 0;
-  using S1 = MsdSmem<KeyT, HAS_VAL>;
-  constexpr uint64_t kItem = sizeof(KeyT) + (HAS_VAL ? 4 : 0);  // 8 B per item in and out
-  set_smem(msd_scatter_kernel<Src, KeyT, HAS_VAL, 1>, sizeof(S1));
-  c->dom_begin("msd_scatter");
-  msd_scatter_kernel<Src, KeyT, HAS_VAL, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
-      src, n, outA, voutA, kb - dl[0], dl[0], 0, cur);
-  CK_LAUNCH();
-  c->dom_end(2 * kItem * m);
-  ++c->launches;
+  if (!pre_m) {
+    scan_counts(c, d_small + kHist, 1u << dl[0], off, cur);
+    CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->launches += 2;
+    if (!m) return 0;
+    set_smem(msd_scatter_kernel<Src, KeyT, HAS_VAL, 1>, sizeof(S1));
+    c->dom_begin("msd_scatter");
+    msd_scatter_kernel<Src, KeyT, HAS_VAL, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
+        src, n, outA, voutA, kb - dl[0], dl[0], 0, cur);
+    CK_LAUNCH();
+    c->dom_end(2 * kItem * m);
+    ++c->launches;
+  }
   KeyT* in_k = outA;
   uint32_t* in_v = voutA;
   KeyT* out_k = outB;
@@ -943,8 +961,43 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   }
 }
 
+// Level 1 of the dense row partition for one window of packets (streaming):
+// its keys land in `out` (the window's region of the arena keysA), partitioned
+// by the top dl[0] key bits; later levels only need every tile to span few
+// level-1 buckets, which window-contiguous regions satisfy. Returns the window's
+// valid packets (host sync; the scatter stays queued).
+uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint64_t* out) {
+  int dl[8], cum[8];
+  msd_level_bits(D, dl, cum);
+  uint32_t* d_small = c->small.as<uint32_t>();
+  auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
+  c->mcur.grow(((size_t)(1u << D) + 8) * 4);
+  c->moff.grow(((size_t)(1u << D) + 8) * 4);
+  CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
+  CK(cudaMemsetAsync(gcount, 0, 8, c->st));
+  const uint64_t n = ps.n;
+  const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
+  msd_hist1_kernel<PacketSrc, uint64_t><<<hgrid, 256, 0, c->st>>>(ps, n, kb - dl[0], d_small + kHist, gcount);
+  CK_LAUNCH();
+  scan_counts(c, d_small + kHist, 1u << dl[0], c->moff.as<uint32_t>(), c->mcur.as<uint32_t>());
+  unsigned long long m = 0;
+  CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (m) {
+    using S1 = MsdSmem<uint64_t, false>;
+    set_smem(msd_scatter_kernel<PacketSrc, uint64_t, false, 1>, sizeof(S1));
+    msd_scatter_kernel<PacketSrc, uint64_t, false, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1),
+                                                        c->st>>>(ps, n, out, nullptr, kb - dl[0], dl[0], 0,
+                                                                 c->mcur.as<uint32_t>());
+    CK_LAUNCH();
+  }
+  return m;
+}
+
+// pre_m > 0: keysA already holds the level-1 partition of pre_m valid keys
+// (streamed windows); n bounds the buffers.
 void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
-                      int b, int D) {
+                      int b, int D, uint64_t pre_m = 0) {
   const int kb = 2 * b;
   stage_begin(c, 1);
   // every buffer the step needs is sized up front (n bounds m, u and the heavy parts)
@@ -968,7 +1021,7 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   sp.hk = c->keysC.p;
   const uint64_t m = msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
                                                                c->keysB.as<uint64_t>(), nullptr, &keys, &dummy,
-                                                               nullptr, &sp);
+                                                               nullptr, &sp, pre_m);
   c->last_sort_launches = c->msd_levels;
   c->mark();  // 2: row partition end
   if (!m) {
@@ -1115,8 +1168,118 @@ int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   return NMX_OK;
 }
 
+// Streamed summed-matrix statistics (BASELINE config 5; also nmx_stats9_host):
+// windows of host packets are copied on a second stream into two alternating
+// device slots; the H2D copy of window k+1 overlaps the level-1 MSD partition of
+// window k into the arena keysA, and the remaining levels, the shared-memory
+// groups and the column statistics run once over the sum. Windows with a
+// null valid pointer are all valid.
+int stream_impl(nmx_ctx* c, const uint32_t* const* src, const uint32_t* const* dst, const uint8_t* const* valid,
+                const uint64_t* lens, uint64_t nwin, uint64_t space, int64_t* out) {
+  int b;
+  if (int r = check_space(space, b)) return r;
+  if (!out || (nwin && (!src || !dst || !lens))) return fail(NMX_EINVAL, "null argument");
+  uint64_t N = 0, wmax = 0;
+  bool any_valid = false;
+  for (uint64_t k = 0; k < nwin; ++k) {
+    if (lens[k] && (!src[k] || !dst[k])) return fail(NMX_EINVAL, "null packet columns in window %llu", (unsigned long long)k);
+    N += lens[k];
+    wmax = std::max(wmax, lens[k]);
+    any_valid = any_valid || (valid && valid[k]);
+  }
+  if (N >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per device, got %llu", (unsigned long long)N);
+  const int D = msd_bits(N, b);
+  if (!D) {  // small (or address space too narrow for the MSD path): one device call
+    c->in_src.grow(std::max<uint64_t>(N, 1) * 4);
+    c->in_dst.grow(std::max<uint64_t>(N, 1) * 4);
+    if (any_valid) c->in_valid.grow(std::max<uint64_t>(N, 1));
+    uint64_t at = 0;
+    for (uint64_t k = 0; k < nwin; ++k) {
+      if (!lens[k]) continue;
+      CK(cudaMemcpyAsync(c->in_src.as<uint32_t>() + at, src[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(c->in_dst.as<uint32_t>() + at, dst[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st));
+      if (any_valid) {
+        if (valid[k])
+          CK(cudaMemcpyAsync(c->in_valid.as<uint8_t>() + at, valid[k], lens[k], cudaMemcpyHostToDevice, c->st));
+        else
+          CK(cudaMemsetAsync(c->in_valid.as<uint8_t>() + at, 1, lens[k], c->st));
+      }
+      at += lens[k];
+    }
+    return stats_device_impl(c, c->in_src.as<uint32_t>(), c->in_dst.as<uint32_t>(),
+                             any_valid ? c->in_valid.as<uint8_t>() : nullptr, N, space, 0, out);
+  }
+  if (!c->st2) CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    if (!c->evc[i]) CK(cudaEventCreateWithFlags(&c->evc[i], cudaEventDisableTiming));
+    if (!c->evu[i]) CK(cudaEventCreateWithFlags(&c->evu[i], cudaEventDisableTiming));
+  }
+  if (!c->evs) CK(cudaEventCreate(&c->evs));
+  c->small.grow(kSmallWords * sizeof(uint32_t));  // level-1 histograms before run_pipeline_msd's stage_begin
+  c->keysA.grow(N * 8);  // the arena: level-1 partitions of every window, back to back
+  DevBuf* ws[2] = {&c->ws0, &c->ws1};
+  DevBuf* wd[2] = {&c->wd0, &c->wd1};
+  DevBuf* wv[2] = {&c->wv0, &c->wv1};
+  for (int i = 0; i < 2; ++i) {
+    ws[i]->grow(wmax * 4);
+    wd[i]->grow(wmax * 4);
+    if (any_valid) wv[i]->grow(wmax + 4);
+  }
+  CK(cudaEventRecord(c->evs, c->st));
+  CK(cudaStreamWaitEvent(c->st2, c->evs, 0));  // copies start after the caller's prior work
+  bool used[2] = {false, false};
+  auto enqueue_copy = [&](uint64_t k) {
+    const int sl = (int)(k & 1);
+    if (used[sl]) CK(cudaStreamWaitEvent(c->st2, c->evu[sl], 0));
+    if (lens[k]) {
+      CK(cudaMemcpyAsync(ws[sl]->p, src[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st2));
+      CK(cudaMemcpyAsync(wd[sl]->p, dst[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st2));
+      if (valid && valid[k]) CK(cudaMemcpyAsync(wv[sl]->p, valid[k], lens[k], cudaMemcpyHostToDevice, c->st2));
+    }
+    CK(cudaEventRecord(c->evc[sl], c->st2));
+  };
+  if (nwin) enqueue_copy(0);
+  uint64_t M = 0;
+  for (uint64_t k = 0; k < nwin; ++k) {
+    if (k + 1 < nwin) enqueue_copy(k + 1);
+    const int sl = (int)(k & 1);
+    CK(cudaStreamWaitEvent(c->st, c->evc[sl], 0));
+    if (lens[k]) {
+      const uint8_t* v = (valid && valid[k]) ? wv[sl]->as<uint8_t>() : nullptr;
+      PacketSrc ps{ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), v, lens[k], 0, b};
+      ps.quad = true;  // slots are cudaMalloc-aligned
+      M += msd_window_level1(c, ps, 2 * b, D, c->keysA.as<uint64_t>() + M);
+    }
+    CK(cudaEventRecord(c->evu[sl], c->st));
+    used[sl] = true;
+  }
+  if (!M) {
+    CK(cudaStreamSynchronize(c->st));
+    std::fill(out, out + S_COUNT, 0);
+    return NMX_OK;
+  }
+  run_pipeline_msd(c, nullptr, nullptr, nullptr, N, b, D, M);
+  CK(cudaEventElapsedTime(&c->last_total_ms, c->evs, c->ev[c->nev - 1]));  // whole streamed call
+  copy_out9(c->h_stats, out, 1);
+  return NMX_OK;
+}
+
 int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t space, uint64_t window_size, int64_t* out) {
+  if (window_size == 0 && n >= (1ull << 20) && n < (1ull << 32) && src && dst) {
+    // H2D in chunks overlapped with the level-1 partition of the previous chunk
+    constexpr uint64_t kChunk = 1ull << 25;
+    std::vector<const uint32_t*> ss, dd;
+    std::vector<const uint8_t*> vv;
+    std::vector<uint64_t> ll;
+    for (uint64_t lo = 0; lo < n; lo += kChunk) {
+      ss.push_back(src + lo);
+      dd.push_back(dst + lo);
+      vv.push_back(valid ? valid + lo : nullptr);
+      ll.push_back(std::min(kChunk, n - lo));
+    }
+    return stream_impl(c, ss.data(), dd.data(), valid ? vv.data() : nullptr, ll.data(), ll.size(), space, out);
+  }
   if (n && (!src || !dst)) return fail(NMX_EINVAL, "null packet columns");
   if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call, got %llu", (unsigned long long)n);
   if (n) {
@@ -1200,6 +1363,9 @@ void nmx_destroy(nmx_ctx* c) {
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->evk) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->evc[0], c->evc[1], c->evu[0], c->evu[1], c->evs})
+    if (e) cudaEventDestroy(e);
+  if (c->st2) cudaStreamDestroy(c->st2);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -1290,6 +1456,11 @@ int nmx_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
 int nmx_stats9_host(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t address_space, int64_t out[9]) {
   return guarded(c, [&] { return stats_host_impl(c, src, dst, valid, n, address_space, 0, out); });
+}
+
+int nmx_stream_stats9(nmx_ctx* c, const uint32_t* const* src, const uint32_t* const* dst, const uint8_t* const* valid,
+                      const uint64_t* lens, uint64_t nwin, uint64_t address_space, int64_t out[9]) {
+  return guarded(c, [&] { return stream_impl(c, src, dst, valid, lens, nwin, address_space, out); });
 }
 
 int nmx_window_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
@@ -1647,39 +1818,37 @@ int nmx_coo_merge_add(nmx_ctx* c, const nmx_coo* a, const nmx_coo* b, nmx_coo** 
   return guarded(c, [&] {
     stage_begin(c, 1);
     const uint64_t n = a->nnz + b->nnz;
-    const uint64_t tiles = (n + kMergeTile - 1) / kMergeTile;
-    nmx_coo* o = nullptr;
+    if (n >= (1ull << 32)) throw std::runtime_error("merged matrix would exceed 2^32-1 links");
+    const uint64_t tiles = (n + kMgTile - 1) / kMgTile;
+    nmx_coo* o = coo_alloc(c, n);  // capacity na + nb; nnz set below
     if (tiles) {
-      c->mhist2.grow((tiles + 8) * 4);
-      c->moff.grow((tiles + 8) * 4);
+      c->msplit.grow((tiles + 2) * 8);
       c->part.grow(64);
       auto* ovf = c->part.as<unsigned long long>();
-      CK(cudaMemsetAsync(ovf, 0, 8, c->st));
+      CK(cudaMemsetAsync(ovf, 0, 16, c->st));
+      c->grow_status(tiles + 1);
+      const unsigned pg = (unsigned)std::min<uint64_t>((tiles + 256) / 256, (uint64_t)c->sms * 8);
+      merge_partition_kernel<<<pg, 256, 0, c->st>>>(a->keys, a->nnz, b->keys, b->nnz, tiles,
+                                                    c->msplit.as<uint64_t>());
+      CK_LAUNCH();
+      set_smem(merge_add_kernel, sizeof(MergeSmem));
       c->dom_begin("merge_add");
-      merge_add_kernel<false><<<(unsigned)tiles, 256, 0, c->st>>>(a->keys, a->counts, a->nnz, b->keys, b->counts,
-                                                                  b->nnz, c->mhist2.as<uint32_t>(), nullptr, nullptr,
-                                                                  nullptr, ovf);
+      merge_add_kernel<<<(unsigned)tiles, kMgThreads, sizeof(MergeSmem), c->st>>>(
+          a->keys, a->counts, a->nnz, b->keys, b->counts, b->nnz, c->msplit.as<uint64_t>(),
+          c->status.as<uint64_t>(), c->next_epoch(), c->small.as<uint32_t>() + kCounters + 28, o->keys, o->counts,
+          ovf, ovf + 1);
       CK_LAUNCH();
-      scan_counts(c, c->mhist2.as<uint32_t>(), (uint32_t)tiles, c->moff.as<uint32_t>(), nullptr);
-      uint32_t nc = 0;
-      CK(cudaMemcpyAsync(&nc, c->moff.as<uint32_t>() + tiles, 4, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      o = coo_alloc(c, nc);
-      merge_add_kernel<true><<<(unsigned)tiles, 256, 0, c->st>>>(a->keys, a->counts, a->nnz, b->keys, b->counts,
-                                                                 b->nnz, nullptr, c->moff.as<uint32_t>(), o->keys,
-                                                                 o->counts, ovf);
-      CK_LAUNCH();
-      c->dom_end(16 * n + 12 * (uint64_t)nc);
+      c->dom_end(12 * n);  // + 12 B per output link, added below
       c->launches += 2;
-      unsigned long long ov = 0;
-      CK(cudaMemcpyAsync(&ov, ovf, 8, cudaMemcpyDeviceToHost, c->st));
+      unsigned long long res[2] = {0, 0};
+      CK(cudaMemcpyAsync(res, ovf, 16, cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
-      if (ov) {
+      c->dom_bytes += 12 * (uint64_t)res[1];
+      o->nnz = res[1];
+      if (res[0]) {
         nmx_coo_free(o);
         return fail(NMX_EINVAL, "merged link count exceeds 2^32-1");
       }
-    } else {
-      o = coo_alloc(c, 0);
     }
     stage_finish(c, 1);
     *out = o;

@@ -925,143 +925,6 @@ __global__ void __launch_bounds__(kLocThreads, 3)
 
 namespace nmx {
 
-// ---------------------------------------------------------------------------
-// K10: merge-path element-wise addition of two sorted unique COO matrices
-// (keys (src<<32)|dst, u32 counts). C = A + B: union of the keys, counts of a
-// key present in both are added. Tile t owns merged positions [t*T, (t+1)*T)
-// of A ++ B; its split (ia, ib) comes from a merge-path binary search. A key
-// present in both inputs occupies two adjacent merged positions (A's first);
-// the A copy is kept with the sum, the B copy is dropped — if they straddle a
-// tile boundary the earlier tile peeks one element past its end.
-// Pass 1 counts kept elements per tile, scan_counts turns that into output
-// offsets, pass 2 re-merges and writes.
-// ---------------------------------------------------------------------------
-constexpr int kMergeTile = 1536;
-
-// first i in [max(0,d-nb), min(d,na)] with A[i] > B[d-1-i] (merge-path split)
-__device__ __forceinline__ uint64_t merge_split(const uint64_t* a, uint64_t na, const uint64_t* b, uint64_t nb,
-                                                uint64_t d) {
-  uint64_t lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
-  while (lo < hi) {
-    const uint64_t i = (lo + hi) >> 1;
-    if (a[i] <= b[d - 1 - i])  // a[i] goes before b[d-1-i] (ties: A first)
-      lo = i + 1;
-    else
-      hi = i;
-  }
-  return lo;
-}
-
-template <bool WRITE>
-__global__ void __launch_bounds__(256) merge_add_kernel(const uint64_t* __restrict__ ak, const uint32_t* __restrict__ ac,
-                                                       uint64_t na, const uint64_t* __restrict__ bk,
-                                                       const uint32_t* __restrict__ bc, uint64_t nb,
-                                                       uint32_t* __restrict__ tile_kept,
-                                                       const uint32_t* __restrict__ tile_off, uint64_t* __restrict__ ck,
-                                                       uint32_t* __restrict__ cc, unsigned long long* __restrict__ overflow) {
-  __shared__ uint64_t sk[kMergeTile + 2];
-  __shared__ uint32_t sc[kMergeTile + 2];
-  __shared__ uint8_t sfrom[kMergeTile + 2];  // 0 = A, 1 = B
-  __shared__ uint32_t wt[kWarps + 1];
-  __shared__ uint64_t s_ia, s_ib, s_ja, s_jb;
-  const int tid = threadIdx.x;
-  const uint64_t n = na + nb;
-  const uint64_t d0 = (uint64_t)blockIdx.x * kMergeTile, d1 = d0 + kMergeTile < n ? d0 + kMergeTile : n;
-  if (tid == 0) {
-    s_ia = merge_split(ak, na, bk, nb, d0);
-    s_ib = d0 - s_ia;
-    s_ja = merge_split(ak, na, bk, nb, d1);
-    s_jb = d1 - s_ja;
-  }
-  __syncthreads();
-  const uint64_t ia = s_ia, ib = s_ib, ja = s_ja, jb = s_jb;
-  const uint32_t la = (uint32_t)(ja - ia), lb = (uint32_t)(jb - ib), len = la + lb;
-  // stage both runs in shared memory (coalesced), then merge by per-element rank
-  // (position = own index + rank in the other run, binary search in smem)
-  __shared__ uint64_t ra[kMergeTile], rb[kMergeTile];
-  for (uint32_t i = tid; i < la; i += 256) ra[i] = ak[ia + i];
-  for (uint32_t i = tid; i < lb; i += 256) rb[i] = bk[ib + i];
-  __syncthreads();
-  for (uint32_t i = tid; i < la; i += 256) {
-    const uint64_t k = ra[i];
-    uint32_t lo = 0, hi = lb;  // # of B elements strictly below k (ties: A first)
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (rb[mid] < k)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    sk[i + lo] = k;
-    sc[i + lo] = ac[ia + i];
-    sfrom[i + lo] = 0;
-  }
-  for (uint32_t i = tid; i < lb; i += 256) {
-    const uint64_t k = rb[i];
-    uint32_t lo = 0, hi = la;  // # of A elements <= k
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (ra[mid] <= k)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    sk[i + lo] = k;
-    sc[i + lo] = bc[ib + i];
-    sfrom[i + lo] = 1;
-  }
-  __syncthreads();
-  // element e is dropped iff it is a B copy whose predecessor (in merged order) has the same key
-  const uint64_t prev0 = d0 == 0 ? ~0ull
-                                 : ((ia > 0 && (ib == 0 || ak[ia - 1] >= bk[ib - 1])) ? ak[ia - 1] : bk[ib - 1]);
-  const bool prev0_valid = d0 > 0;
-  // the element right after the tile (to add a straddling B copy to our last kept A copy)
-  uint64_t next_k = 0;
-  uint32_t next_c = 0;
-  bool next_is_b = false;
-  if (d1 < n) {
-    if (ja < na && (jb >= nb || ak[ja] <= bk[jb])) {
-      next_k = ak[ja];
-    } else {
-      next_k = bk[jb];
-      next_c = bc[jb];
-      next_is_b = true;
-    }
-  }
-  uint32_t kept = 0;
-  const uint32_t PER = (len + 255) / 256;
-  const uint32_t e0 = tid * PER;
-  for (uint32_t q = 0; q < PER; ++q) {
-    const uint32_t e = e0 + q;
-    if (e >= len) break;
-    const bool dup = sfrom[e] == 1 && (e > 0 ? sk[e - 1] == sk[e] : (prev0_valid && prev0 == sk[e]));
-    kept += !dup;
-  }
-  uint32_t total;
-  uint32_t at = block_excl_scan<uint32_t>(kept, wt, &total);
-  if (!WRITE) {
-    if (tid == 0) tile_kept[blockIdx.x] = total;
-    return;
-  }
-  at += tile_off[blockIdx.x];
-  for (uint32_t q = 0; q < PER; ++q) {
-    const uint32_t e = e0 + q;
-    if (e >= len) break;
-    const bool dup = sfrom[e] == 1 && (e > 0 ? sk[e - 1] == sk[e] : (prev0_valid && prev0 == sk[e]));
-    if (dup) continue;
-    unsigned long long c = sc[e];
-    if (e + 1 < len) {
-      if (sfrom[e + 1] == 1 && sk[e + 1] == sk[e]) c += sc[e + 1];
-    } else if (next_is_b && next_k == sk[e]) {
-      c += next_c;
-    }
-    if (c > 0xFFFFFFFFull) atomicAdd(overflow, 1ull);
-    ck[at] = sk[e];
-    cc[at] = (uint32_t)c;
-    ++at;
-  }
-}
-
 // Unique keys of a sorted array with their run lengths, without a lookback
 // chain: pass 1 counts run heads per tile, scan_counts gives every tile its first
 // output index, pass 2 writes (key, start position) of each head through shared

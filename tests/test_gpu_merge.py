@@ -84,3 +84,22 @@ def test_streamed_pinned_windows_overlapped(coo):
         wins.append((ps, pd))
     got = coo.stream_stats9_pinned([(a.array, b.array) for a, b in wins])
     assert got == orc.stats9_packed(s, d)
+
+
+@pytest.mark.parametrize("overlap", [0.0, 0.5, 1.0])
+def test_merge_add_many_tiles(coo, overlap):
+    # ~2^20 links per side, a fraction shared (duplicates straddle tile boundaries)
+    rng = np.random.default_rng(int(overlap * 10) + 3)
+    n = 1 << 20
+    s = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    d = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    k = int(n * overlap)
+    s2 = np.concatenate([s[:k], rng.integers(0, 1 << 32, n - k, dtype=np.uint64).astype(np.uint32)])
+    d2 = np.concatenate([d[:k], rng.integers(0, 1 << 32, n - k, dtype=np.uint64).astype(np.uint32)])
+    a = coo.coo_from_packets(s, d)
+    b = coo.coo_from_packets(s2, d2)
+    m = coo.merge_add(a, b)
+    keys, counts = m.download()
+    wk, wc = orc.coo_packed(np.concatenate([s, s2]), np.concatenate([d, d2]))
+    assert np.array_equal(keys, wk) and np.array_equal(counts, wc)
+    assert m.stats9() == orc.stats9_packed(np.concatenate([s, s2]), np.concatenate([d, d2]))
