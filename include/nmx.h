@@ -94,6 +94,20 @@ int nmx_stream_stats9(nmx_ctx* ctx, const uint32_t* const* src, const uint32_t* 
                       const uint8_t* const* valid, const uint64_t* lens, uint64_t nwin, uint64_t address_space,
                       int64_t out[9]);
 
+/* Packet files: the reference's binary records, 9 bytes each,
+ * little-endian {u32 src, u32 dst, u8 valid} (traffic.py:25 _PACKET_DTYPE,
+ * write_packets / read_packets traffic.py:370-388).
+ *  - nmx_stream_records: like nmx_stream_stats9 over windows of HOST records
+ *    (rec[k], lens[k] records), streamed raw (9 B/packet) and unpacked on the device.
+ *  - nmx_unpack_records: device records -> device columns (d_rec 4-byte aligned,
+ *    d_src / d_dst 16-byte, d_valid 4-byte aligned).
+ * Both reject any address >= address_space with NMX_EINVAL, as PacketStream does
+ * (traffic.py:56-64). */
+int nmx_stream_records(nmx_ctx* ctx, const uint8_t* const* rec, const uint64_t* lens, uint64_t nwin,
+                       uint64_t address_space, int64_t out[9]);
+int nmx_unpack_records(nmx_ctx* ctx, const uint8_t* d_rec, uint64_t n, uint32_t* d_src, uint32_t* d_dst,
+                       uint8_t* d_valid, uint64_t address_space);
+
 /* Per-window statistics: window t = packets [t*W, (t+1)*W) by raw position,
  * invalid packets keep their position (traffic.py:221-242); out has
  * ceil(n/W) rows of 9 (analyze_dataset per-window reports, analytics.py:109-130). */

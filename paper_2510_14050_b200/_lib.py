@@ -48,6 +48,8 @@ SIGNATURES = {
     "nmx_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stream_stats9": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_stream_records": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_unpack_records": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _VP, _U64]),
     "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_window_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_reduce_i64": (C.c_int, [_VP, _VP, _U64, C.c_int, _VP]),
@@ -255,6 +257,37 @@ def stream_stats9(windows, address_space: int = 1 << 32, device: int = 0) -> tup
                                      out.ctypes.data))
     del cols
     return tuple(int(x) for x in out)
+
+
+def _record_bytes(w) -> np.ndarray:
+    a = np.asarray(w)
+    if a.dtype.itemsize == 9 and a.dtype.names:  # structured packet records
+        a = a.view(np.uint8).reshape(-1)
+    if a.dtype != np.uint8 or a.ndim != 1 or len(a) % 9:
+        raise ValueError("packet records must be whole 9-byte records (traffic.py:25)")
+    return np.ascontiguousarray(a)
+
+
+def stream_records(windows, address_space: int = 1 << 32, device: int = 0) -> tuple:
+    """Nine statistics of the matrix summed over windows of raw packet-file records
+    (9-byte {u32 src, u32 dst, u8 valid}, traffic.py:25) in host memory
+    (nmx_stream_records; pinned memory streams at full host-link bandwidth)."""
+    ctx = context(device)
+    recs = [_record_bytes(w) for w in windows]
+    k = len(recs)
+    ptrs = (C.c_void_p * max(k, 1))(*[r.ctypes.data for r in recs])
+    lens = (C.c_uint64 * max(k, 1))(*[len(r) // 9 for r in recs])
+    out = np.zeros(9, dtype=np.int64)
+    check(ctx._lib.nmx_stream_records(ctx.handle, ptrs, lens, k, int(address_space), out.ctypes.data))
+    del recs
+    return tuple(int(x) for x in out)
+
+
+def unpack_records(d_rec, n: int, d_src, d_dst, d_valid, address_space: int = 1 << 32, device: int = 0) -> None:
+    """Device records -> device u32 src / dst + u8 valid columns (nmx_unpack_records)."""
+    ctx = context(device)
+    check(ctx._lib.nmx_unpack_records(ctx.handle, _ptr(d_rec), int(n), _ptr(d_src), _ptr(d_dst), _ptr(d_valid),
+                                      int(address_space)))
 
 
 def window_stats9(src, dst, valid, address_space: int, window_size: int, device: int = 0) -> np.ndarray:

@@ -193,3 +193,42 @@ def analyze_windows(stream: PacketStream, window_size: int, device: int = 0) -> 
     sums = {0, 1, 3, 6}
     tot = [sum(r.astuple()[k] for r in per) if k in sums else max(r.astuple()[k] for r in per) for k in range(9)]
     return per, Stats9(*tot)
+
+
+def stats9_file(path, address_space: int | None = None, window_packets: int = 1 << 25, device: int = 0) -> Stats9:
+    """Nine statistics of the matrix summed over every valid packet of a binary
+    packet file (9-byte records, traffic.py:25, 370-388) -- read_packets ->
+    build_matrices(stream, len(stream)) -> to_flat -> analyze_matrix + max_scan
+    without materialising anything on the host: the file is read once into pinned
+    memory and streamed to the GPU in windows of raw records, unpacked there
+    (nmx_stream_records). ``address_space=None`` accepts any 32-bit address (the
+    statistics do not depend on it); otherwise addresses >= address_space raise
+    ValueError, like PacketStream."""
+    import os
+
+    size = os.path.getsize(path)
+    if size % 9:
+        raise ValueError(f"{path}: size {size} is not a whole number of 9-byte packet records")
+    n = size // 9
+    space = (1 << 32) if address_space is None else int(address_space)
+    if n == 0:
+        if space < 1:
+            raise ValueError("address_space must be >= 1")
+        return Stats9.zero()
+    buf = _lib.PinnedArray(size, dtype=np.uint8)
+    try:
+        with open(path, "rb") as f:
+            got = f.readinto(memoryview(buf.array))
+        if got != size:
+            raise OSError(f"{path}: short read ({got} of {size} bytes)")
+        w = max(1, int(window_packets)) * 9
+        windows = [buf.array[i:i + w] for i in range(0, size, w)]
+        try:
+            out = _lib.stream_records(windows, space, device)
+        except _lib.NmxError as e:
+            if "address_space" in str(e):
+                raise ValueError(str(e)) from None
+            raise
+    finally:
+        buf.close()
+    return Stats9(*out)

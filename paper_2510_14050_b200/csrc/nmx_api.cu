@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/nmx.h"
+#include "nmx_io.cuh"
 #include "nmx_merge.cuh"
 #include "nmx_seg.cuh"
 
@@ -112,7 +113,7 @@ struct nmx_ctx {
   std::mutex mu;
   DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
-      red, ws0, ws1, wd0, wd1, wv0, wv1, msplit, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
+      red, ws0, ws1, wd0, wd1, wv0, wv1, wr0, wr1, rmax, msplit, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
       hcount;
   uint32_t epoch = 0;
   cudaStream_t st2 = nullptr;  // copy stream of the streamed path
@@ -1168,44 +1169,95 @@ int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   return NMX_OK;
 }
 
-// Streamed summed-matrix statistics (BASELINE config 5; also nmx_stats9_host):
-// windows of host packets are copied on a second stream into two alternating
-// device slots; the H2D copy of window k+1 overlaps the level-1 MSD partition of
-// window k into the arena keysA, and the remaining levels, the shared-memory
-// groups and the column statistics run once over the sum. Windows with a
-// null valid pointer are all valid.
-int stream_impl(nmx_ctx* c, const uint32_t* const* src, const uint32_t* const* dst, const uint8_t* const* valid,
-                const uint64_t* lens, uint64_t nwin, uint64_t space, int64_t* out) {
+// Host windows of packets: u32 src / dst columns (+ u8 valid or NULL per window),
+// or raw 9-byte packet-file records (traffic.py:25) when `rec` is set.
+struct HostWindows {
+  const uint32_t* const* src = nullptr;
+  const uint32_t* const* dst = nullptr;
+  const uint8_t* const* valid = nullptr;
+  const uint8_t* const* rec = nullptr;
+  const uint64_t* lens = nullptr;
+  uint64_t nwin = 0;
+};
+
+// device records -> columns; the largest address seen is max-reduced into *maxaddr
+void unpack_records(nmx_ctx* c, const uint8_t* rec, uint64_t n, uint32_t* s, uint32_t* d, uint8_t* v,
+                    unsigned int* maxaddr) {
+  if (!n) return;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n / 4 + 256) / 256, (uint64_t)c->sms * 8));
+  unpack_records_kernel<<<grid, 256, 0, c->st>>>(rec, n, s, d, v, maxaddr);
+  CK_LAUNCH();
+  ++c->launches;
+}
+
+int check_maxaddr(nmx_ctx* c, uint64_t space) {
+  unsigned int mx = 0;
+  CK(cudaMemcpyAsync(&mx, c->rmax.p, 4, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if ((uint64_t)mx >= space)
+    return fail(NMX_EINVAL, "addresses must lie in [0, address_space): found %u >= %llu", mx,
+                (unsigned long long)space);
+  return NMX_OK;
+}
+
+// Streamed summed-matrix statistics (BASELINE config 5; also nmx_stats9_host and
+// packet files): windows of host packets are copied on a second stream into two
+// alternating device slots; the H2D copy of window k+1 overlaps the level-1 MSD
+// partition of window k into the arena keysA, and the remaining levels, the
+// shared-memory groups and the column statistics run once over the sum.
+int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out) {
   int b;
   if (int r = check_space(space, b)) return r;
-  if (!out || (nwin && (!src || !dst || !lens))) return fail(NMX_EINVAL, "null argument");
+  const bool recs = hw.rec != nullptr;
+  if (!out || (hw.nwin && (!hw.lens || (!recs && (!hw.src || !hw.dst))))) return fail(NMX_EINVAL, "null argument");
   uint64_t N = 0, wmax = 0;
-  bool any_valid = false;
-  for (uint64_t k = 0; k < nwin; ++k) {
-    if (lens[k] && (!src[k] || !dst[k])) return fail(NMX_EINVAL, "null packet columns in window %llu", (unsigned long long)k);
-    N += lens[k];
-    wmax = std::max(wmax, lens[k]);
-    any_valid = any_valid || (valid && valid[k]);
+  bool any_valid = recs;
+  for (uint64_t k = 0; k < hw.nwin; ++k) {
+    const bool null_cols = recs ? !hw.rec[k] : (!hw.src[k] || !hw.dst[k]);
+    if (hw.lens[k] && null_cols) return fail(NMX_EINVAL, "null packet data in window %llu", (unsigned long long)k);
+    N += hw.lens[k];
+    wmax = std::max(wmax, hw.lens[k]);
+    any_valid = any_valid || (hw.valid && hw.valid[k]);
   }
   if (N >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per device, got %llu", (unsigned long long)N);
+  if (recs) {
+    c->rmax.grow(64);
+    CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
+  }
   const int D = msd_bits(N, b);
   if (!D) {  // small (or address space too narrow for the MSD path): one device call
-    c->in_src.grow(std::max<uint64_t>(N, 1) * 4);
-    c->in_dst.grow(std::max<uint64_t>(N, 1) * 4);
-    if (any_valid) c->in_valid.grow(std::max<uint64_t>(N, 1));
+    c->in_src.grow(std::max<uint64_t>(N, 1) * 4 + 16);
+    c->in_dst.grow(std::max<uint64_t>(N, 1) * 4 + 16);
+    if (any_valid) c->in_valid.grow(std::max<uint64_t>(N, 1) + 16);
+    if (recs) c->wr0.grow(std::max<uint64_t>(wmax, 1) * 9 + 16);
     uint64_t at = 0;
-    for (uint64_t k = 0; k < nwin; ++k) {
-      if (!lens[k]) continue;
-      CK(cudaMemcpyAsync(c->in_src.as<uint32_t>() + at, src[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st));
-      CK(cudaMemcpyAsync(c->in_dst.as<uint32_t>() + at, dst[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st));
-      if (any_valid) {
-        if (valid[k])
-          CK(cudaMemcpyAsync(c->in_valid.as<uint8_t>() + at, valid[k], lens[k], cudaMemcpyHostToDevice, c->st));
-        else
-          CK(cudaMemsetAsync(c->in_valid.as<uint8_t>() + at, 1, lens[k], c->st));
+    for (uint64_t k = 0; k < hw.nwin; ++k) {
+      const uint64_t L = hw.lens[k];
+      if (!L) continue;
+      if (recs) {  // window by window through one record slot (offsets stay 16-byte aligned only at 0)
+        CK(cudaMemcpyAsync(c->wr0.p, hw.rec[k], L * 9, cudaMemcpyHostToDevice, c->st));
+        c->ws0.grow(L * 4 + 16);
+        c->wd0.grow(L * 4 + 16);
+        c->wv0.grow(L + 16);
+        unpack_records(c, c->wr0.as<uint8_t>(), L, c->ws0.as<uint32_t>(), c->wd0.as<uint32_t>(), c->wv0.as<uint8_t>(),
+                       c->rmax.as<unsigned int>());
+        CK(cudaMemcpyAsync(c->in_src.as<uint32_t>() + at, c->ws0.p, L * 4, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(c->in_dst.as<uint32_t>() + at, c->wd0.p, L * 4, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(c->in_valid.as<uint8_t>() + at, c->wv0.p, L, cudaMemcpyDeviceToDevice, c->st));
+      } else {
+        CK(cudaMemcpyAsync(c->in_src.as<uint32_t>() + at, hw.src[k], L * 4, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->in_dst.as<uint32_t>() + at, hw.dst[k], L * 4, cudaMemcpyHostToDevice, c->st));
+        if (any_valid) {
+          if (hw.valid[k])
+            CK(cudaMemcpyAsync(c->in_valid.as<uint8_t>() + at, hw.valid[k], L, cudaMemcpyHostToDevice, c->st));
+          else
+            CK(cudaMemsetAsync(c->in_valid.as<uint8_t>() + at, 1, L, c->st));
+        }
       }
-      at += lens[k];
+      at += L;
     }
+    if (recs)
+      if (int r = check_maxaddr(c, space)) return r;
     return stats_device_impl(c, c->in_src.as<uint32_t>(), c->in_dst.as<uint32_t>(),
                              any_valid ? c->in_valid.as<uint8_t>() : nullptr, N, space, 0, out);
   }
@@ -1220,10 +1272,12 @@ int stream_impl(nmx_ctx* c, const uint32_t* const* src, const uint32_t* const* d
   DevBuf* ws[2] = {&c->ws0, &c->ws1};
   DevBuf* wd[2] = {&c->wd0, &c->wd1};
   DevBuf* wv[2] = {&c->wv0, &c->wv1};
+  DevBuf* wr[2] = {&c->wr0, &c->wr1};
   for (int i = 0; i < 2; ++i) {
-    ws[i]->grow(wmax * 4);
-    wd[i]->grow(wmax * 4);
-    if (any_valid) wv[i]->grow(wmax + 4);
+    ws[i]->grow(wmax * 4 + 16);
+    wd[i]->grow(wmax * 4 + 16);
+    if (any_valid) wv[i]->grow(wmax + 16);
+    if (recs) wr[i]->grow(wmax * 9 + 16);
   }
   CK(cudaEventRecord(c->evs, c->st));
   CK(cudaStreamWaitEvent(c->st2, c->evs, 0));  // copies start after the caller's prior work
@@ -1231,28 +1285,37 @@ int stream_impl(nmx_ctx* c, const uint32_t* const* src, const uint32_t* const* d
   auto enqueue_copy = [&](uint64_t k) {
     const int sl = (int)(k & 1);
     if (used[sl]) CK(cudaStreamWaitEvent(c->st2, c->evu[sl], 0));
-    if (lens[k]) {
-      CK(cudaMemcpyAsync(ws[sl]->p, src[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st2));
-      CK(cudaMemcpyAsync(wd[sl]->p, dst[k], lens[k] * 4, cudaMemcpyHostToDevice, c->st2));
-      if (valid && valid[k]) CK(cudaMemcpyAsync(wv[sl]->p, valid[k], lens[k], cudaMemcpyHostToDevice, c->st2));
+    const uint64_t L = hw.lens[k];
+    if (L && recs) {
+      CK(cudaMemcpyAsync(wr[sl]->p, hw.rec[k], L * 9, cudaMemcpyHostToDevice, c->st2));
+    } else if (L) {
+      CK(cudaMemcpyAsync(ws[sl]->p, hw.src[k], L * 4, cudaMemcpyHostToDevice, c->st2));
+      CK(cudaMemcpyAsync(wd[sl]->p, hw.dst[k], L * 4, cudaMemcpyHostToDevice, c->st2));
+      if (hw.valid && hw.valid[k]) CK(cudaMemcpyAsync(wv[sl]->p, hw.valid[k], L, cudaMemcpyHostToDevice, c->st2));
     }
     CK(cudaEventRecord(c->evc[sl], c->st2));
   };
-  if (nwin) enqueue_copy(0);
+  if (hw.nwin) enqueue_copy(0);
   uint64_t M = 0;
-  for (uint64_t k = 0; k < nwin; ++k) {
-    if (k + 1 < nwin) enqueue_copy(k + 1);
+  for (uint64_t k = 0; k < hw.nwin; ++k) {
+    if (k + 1 < hw.nwin) enqueue_copy(k + 1);
     const int sl = (int)(k & 1);
     CK(cudaStreamWaitEvent(c->st, c->evc[sl], 0));
-    if (lens[k]) {
-      const uint8_t* v = (valid && valid[k]) ? wv[sl]->as<uint8_t>() : nullptr;
-      PacketSrc ps{ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), v, lens[k], 0, b};
+    const uint64_t L = hw.lens[k];
+    if (L) {
+      if (recs)
+        unpack_records(c, wr[sl]->as<uint8_t>(), L, ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(),
+                       wv[sl]->as<uint8_t>(), c->rmax.as<unsigned int>());
+      const uint8_t* v = (recs || (hw.valid && hw.valid[k])) ? wv[sl]->as<uint8_t>() : nullptr;
+      PacketSrc ps{ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), v, L, 0, b};
       ps.quad = true;  // slots are cudaMalloc-aligned
       M += msd_window_level1(c, ps, 2 * b, D, c->keysA.as<uint64_t>() + M);
     }
     CK(cudaEventRecord(c->evu[sl], c->st));
     used[sl] = true;
   }
+  if (recs)
+    if (int r = check_maxaddr(c, space)) return r;
   if (!M) {
     CK(cudaStreamSynchronize(c->st));
     std::fill(out, out + S_COUNT, 0);
@@ -1278,7 +1341,13 @@ int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const 
       vv.push_back(valid ? valid + lo : nullptr);
       ll.push_back(std::min(kChunk, n - lo));
     }
-    return stream_impl(c, ss.data(), dd.data(), valid ? vv.data() : nullptr, ll.data(), ll.size(), space, out);
+    HostWindows hw;
+    hw.src = ss.data();
+    hw.dst = dd.data();
+    hw.valid = valid ? vv.data() : nullptr;
+    hw.lens = ll.data();
+    hw.nwin = ll.size();
+    return stream_impl(c, hw, space, out);
   }
   if (n && (!src || !dst)) return fail(NMX_EINVAL, "null packet columns");
   if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call, got %llu", (unsigned long long)n);
@@ -1460,7 +1529,38 @@ int nmx_stats9_host(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const 
 
 int nmx_stream_stats9(nmx_ctx* c, const uint32_t* const* src, const uint32_t* const* dst, const uint8_t* const* valid,
                       const uint64_t* lens, uint64_t nwin, uint64_t address_space, int64_t out[9]) {
-  return guarded(c, [&] { return stream_impl(c, src, dst, valid, lens, nwin, address_space, out); });
+  HostWindows hw;
+  hw.src = src;
+  hw.dst = dst;
+  hw.valid = valid;
+  hw.lens = lens;
+  hw.nwin = nwin;
+  return guarded(c, [&] { return stream_impl(c, hw, address_space, out); });
+}
+
+int nmx_stream_records(nmx_ctx* c, const uint8_t* const* rec, const uint64_t* lens, uint64_t nwin,
+                       uint64_t address_space, int64_t out[9]) {
+  if (nwin && !rec) return fail(NMX_EINVAL, "null record windows");
+  HostWindows hw;
+  hw.rec = rec;
+  hw.lens = lens;
+  hw.nwin = nwin;
+  return guarded(c, [&] { return stream_impl(c, hw, address_space, out); });
+}
+
+int nmx_unpack_records(nmx_ctx* c, const uint8_t* d_rec, uint64_t n, uint32_t* d_src, uint32_t* d_dst,
+                       uint8_t* d_valid, uint64_t address_space) {
+  if (n && (!d_rec || !d_src || !d_dst || !d_valid)) return fail(NMX_EINVAL, "null argument");
+  if (((uintptr_t)d_rec & 3) || ((uintptr_t)d_src & 15) || ((uintptr_t)d_dst & 15) || ((uintptr_t)d_valid & 3))
+    return fail(NMX_EINVAL, "records need 4-byte, src/dst 16-byte, valid 4-byte alignment");
+  return guarded(c, [&] {
+    int b;
+    if (int r = check_space(address_space, b)) return r;
+    c->rmax.grow(64);
+    CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
+    unpack_records(c, d_rec, n, d_src, d_dst, d_valid, c->rmax.as<unsigned int>());
+    return check_maxaddr(c, address_space);
+  });
 }
 
 int nmx_window_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,

@@ -288,3 +288,29 @@ def to_flat(matrix: TrafficMatrix, device: int = 0) -> FlatContainers:
         row_sums=np.column_stack([rid, rsum]),
         col_sums=np.column_stack([cid, csum]),
     )
+
+
+# ---------------------------------------------------------------------------
+# binary packet files (traffic.py:370-388): 9-byte little-endian records
+# ---------------------------------------------------------------------------
+def write_packets(stream: PacketStream, path) -> None:
+    """Binary packet file: little-endian u32 src, u32 dst, u8 valid per record
+    (traffic.py:370-378)."""
+    if len(stream) and max(stream.src.max(), stream.dst.max()) >= 2**32:
+        raise ValueError("addresses exceed the 32-bit record format")
+    out = np.empty(len(stream), dtype=_PACKET_DTYPE)
+    out["src"] = stream.src
+    out["dst"] = stream.dst
+    out["valid"] = stream.valid
+    out.tofile(str(path))
+
+
+def read_packets(path, address_space: int | None = None) -> PacketStream:
+    """Read a binary packet file; address_space defaults to max address + 1
+    (traffic.py:381-388)."""
+    raw = np.fromfile(str(path), dtype=_PACKET_DTYPE)
+    src = raw["src"].astype(np.int64)
+    dst = raw["dst"].astype(np.int64)
+    if address_space is None:
+        address_space = int(max(src.max(), dst.max())) + 1 if len(raw) else 1
+    return PacketStream(src=src, dst=dst, valid=raw["valid"] != 0, address_space=address_space)
