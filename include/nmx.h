@@ -108,6 +108,19 @@ int nmx_stream_records(nmx_ctx* ctx, const uint8_t* const* rec, const uint64_t* 
 int nmx_unpack_records(nmx_ctx* ctx, const uint8_t* d_rec, uint64_t n, uint32_t* d_src, uint32_t* d_dst,
                        uint8_t* d_valid, uint64_t address_space);
 
+/* anonymize (traffic.py:107-137) on the device: every address of
+ * the interleaved stream src0, dst0, src1, dst1, ... is relabelled with
+ * perm[first-seen rank], perm = numpy default_rng(key).permutation(k) drawn by the
+ * caller once k (the number of distinct addresses) is known. Two calls:
+ *  - nmx_anonymize_begin: device columns (n < 2^31 packets) -> k; the sorted
+ *    state stays in the context (one anonymization per context at a time);
+ *  - nmx_anonymize_finish: host perm[k] (u32) -> relabelled device columns, and
+ *    optionally the host tables distinct_out[k] (ascending raw addresses) and
+ *    code_out[k] (their codes) of the AnonymizationMap. */
+int nmx_anonymize_begin(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, uint64_t* k_out);
+int nmx_anonymize_finish(nmx_ctx* ctx, const uint32_t* perm, uint32_t* d_src_out, uint32_t* d_dst_out,
+                         uint32_t* distinct_out, uint32_t* code_out);
+
 /* Per-window statistics: window t = packets [t*W, (t+1)*W) by raw position,
  * invalid packets keep their position (traffic.py:221-242); out has
  * ceil(n/W) rows of 9 (analyze_dataset per-window reports, analytics.py:109-130). */

@@ -49,6 +49,8 @@ SIGNATURES = {
     "nmx_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stream_stats9": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stream_records": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_anonymize_begin": (C.c_int, [_VP, _VP, _VP, _U64, _VP]),
+    "nmx_anonymize_finish": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "nmx_unpack_records": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _VP, _U64]),
     "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_window_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
@@ -288,6 +290,41 @@ def unpack_records(d_rec, n: int, d_src, d_dst, d_valid, address_space: int = 1 
     ctx = context(device)
     check(ctx._lib.nmx_unpack_records(ctx.handle, _ptr(d_rec), int(n), _ptr(d_src), _ptr(d_dst), _ptr(d_valid),
                                       int(address_space)))
+
+
+def anonymize_device(src, dst, key: int, device: int = 0, tables: bool = True):
+    """Keyed first-seen dense relabel (traffic.py:107-137) on the GPU.
+
+    ``src``/``dst``: host uint32-compatible arrays or DeviceArrays of n packets.
+    Returns (src', dst' as DeviceArrays, k, distinct, code) -- ``distinct`` (ascending
+    raw addresses) and ``code`` (their new labels) as uint32 numpy arrays when
+    ``tables``, else None. perm = numpy default_rng(key).permutation(k), exactly
+    the reference's draw, is generated here on the host between the two calls."""
+    ctx = context(device)
+    keep = []
+    if not _is_device(src):
+        s, d = _u32_host(src), _u32_host(dst)
+        if len(s) != len(d):
+            raise ValueError("src and dst must have equal lengths")
+        ds, dd = DeviceArray(len(s), device=device), DeviceArray(len(s), device=device)
+        if len(s):
+            ds.upload(s)
+            dd.upload(d)
+        keep = [ds, dd]
+        src, dst = ds, dd
+    n = int(src.numel())
+    k = C.c_uint64()
+    check(ctx._lib.nmx_anonymize_begin(ctx.handle, _ptr(src), _ptr(dst), n, C.byref(k)))
+    k = int(k.value)
+    perm = np.ascontiguousarray(np.random.default_rng(key).permutation(k), dtype=np.uint32)
+    so, do = DeviceArray(max(n, 1), device=device), DeviceArray(max(n, 1), device=device)
+    distinct = np.empty(k, np.uint32) if tables else None
+    code = np.empty(k, np.uint32) if tables else None
+    check(ctx._lib.nmx_anonymize_finish(ctx.handle, perm.ctypes.data, _ptr(so), _ptr(do),
+                                        distinct.ctypes.data if tables and k else None,
+                                        code.ctypes.data if tables and k else None))
+    del keep
+    return so, do, k, distinct, code
 
 
 def window_stats9(src, dst, valid, address_space: int, window_size: int, device: int = 0) -> np.ndarray:

@@ -113,7 +113,8 @@ struct nmx_ctx {
   std::mutex mu;
   DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
-      red, ws0, ws1, wd0, wd1, wv0, wv1, wr0, wr1, rmax, msplit, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
+      red, ws0, ws1, wd0, wd1, wv0, wv1, wr0, wr1, rmax, anAk, anAv, anBk, anBv, anHead, anHoff, anDistinct,
+      anFirst, anFlag, anFoff, anPerm, anCode, msplit, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
       hcount;
   uint32_t epoch = 0;
   cudaStream_t st2 = nullptr;  // copy stream of the streamed path
@@ -132,6 +133,9 @@ struct nmx_ctx {
   uint64_t coo_nnz = 0, flat_nnz = 0, flat_r = 0, flat_c = 0;
   int coo_b = 0;
   int msd_levels = 0;
+  // anonymize state between nmx_anonymize_begin and nmx_anonymize_finish
+  uint64_t an_m = 0, an_k = 0;
+  const uint32_t* an_pos = nullptr;
 
   uint32_t next_epoch() {
     if (++epoch >= (1u << 22)) {
@@ -1560,6 +1564,82 @@ int nmx_unpack_records(nmx_ctx* c, const uint8_t* d_rec, uint64_t n, uint32_t* d
     CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
     unpack_records(c, d_rec, n, d_src, d_dst, d_valid, c->rmax.as<unsigned int>());
     return check_maxaddr(c, address_space);
+  });
+}
+
+int nmx_anonymize_begin(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, uint64_t* k_out) {
+  if (!k_out || (n && (!d_src || !d_dst))) return fail(NMX_EINVAL, "null argument");
+  if (n >= (1ull << 31)) return fail(NMX_EINVAL, "anonymize takes < 2^31 packets per call, got %llu",
+                                     (unsigned long long)n);
+  return guarded(c, [&] {
+    stage_begin(c, 1);
+    const uint64_t m = 2 * n;
+    c->an_m = m;
+    c->an_k = 0;
+    c->an_pos = nullptr;
+    *k_out = 0;
+    if (!n) {
+      stage_finish(c, 1);
+      return NMX_OK;
+    }
+    for (DevBuf* bf : {&c->anAk, &c->anAv, &c->anBk, &c->anBv, &c->anHead, &c->anFlag}) bf->grow(m * 4 + 16);
+    c->anHoff.grow((m + 1) * 4 + 16);
+    c->anFoff.grow((m + 1) * 4 + 16);
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m + 255) / 256, (uint64_t)c->sms * 16));
+    anon_pairs_kernel<<<g, 256, 0, c->st>>>(d_src, d_dst, n, c->anAk.as<uint32_t>(), c->anAv.as<uint32_t>());
+    CK_LAUNCH();
+    // stable LSD sort of (address, position): positions stay ascending inside a run
+    auto sorted = sort_u32_pairs(c, c->anAk.as<uint32_t>(), c->anAv.as<uint32_t>(), m, 32, c->anBk.as<uint32_t>(),
+                                 c->anBv.as<uint32_t>());
+    anon_heads_kernel<<<g, 256, 0, c->st>>>(sorted.first, m, c->anHead.as<uint32_t>());
+    CK_LAUNCH();
+    scan_counts(c, c->anHead.as<uint32_t>(), (uint32_t)m, c->anHoff.as<uint32_t>(), nullptr);
+    uint32_t k = 0;
+    CK(cudaMemcpyAsync(&k, c->anHoff.as<uint32_t>() + m, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->anDistinct.grow((uint64_t)k * 4 + 16);
+    c->anFirst.grow((uint64_t)k * 4 + 16);
+    CK(cudaMemsetAsync(c->anFlag.p, 0, m * 4, c->st));
+    anon_uniques_kernel<<<g, 256, 0, c->st>>>(sorted.first, sorted.second, c->anHead.as<uint32_t>(),
+                                              c->anHoff.as<uint32_t>(), m, c->anDistinct.as<uint32_t>(),
+                                              c->anFirst.as<uint32_t>(), c->anFlag.as<uint32_t>());
+    CK_LAUNCH();
+    scan_counts(c, c->anFlag.as<uint32_t>(), (uint32_t)m, c->anFoff.as<uint32_t>(), nullptr);
+    c->launches += 3;
+    c->an_k = k;
+    c->an_pos = sorted.second;
+    *k_out = k;
+    return NMX_OK;
+  });
+}
+
+int nmx_anonymize_finish(nmx_ctx* c, const uint32_t* perm, uint32_t* d_src_out, uint32_t* d_dst_out,
+                         uint32_t* distinct_out, uint32_t* code_out) {
+  return guarded(c, [&] {
+    const uint64_t k = c->an_k, m = c->an_m;
+    if (!k) {
+      stage_finish(c, 1);
+      return NMX_OK;
+    }
+    if (!perm || !d_src_out || !d_dst_out || !c->an_pos) return fail(NMX_EINVAL, "null argument or no begin");
+    c->anPerm.grow(k * 4 + 16);
+    c->anCode.grow(k * 4 + 16);
+    CK(cudaMemcpyAsync(c->anPerm.p, perm, k * 4, cudaMemcpyHostToDevice, c->st));
+    const unsigned gk = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((k + 255) / 256, (uint64_t)c->sms * 16));
+    anon_codes_kernel<<<gk, 256, 0, c->st>>>(c->anFirst.as<uint32_t>(), c->anFoff.as<uint32_t>(),
+                                             c->anPerm.as<uint32_t>(), k, c->anCode.as<uint32_t>());
+    CK_LAUNCH();
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m + 255) / 256, (uint64_t)c->sms * 16));
+    anon_scatter_kernel<<<g, 256, 0, c->st>>>(c->an_pos, c->anHead.as<uint32_t>(), c->anHoff.as<uint32_t>(), m,
+                                              c->anCode.as<uint32_t>(), d_src_out, d_dst_out);
+    CK_LAUNCH();
+    c->launches += 2;
+    if (distinct_out) CK(cudaMemcpyAsync(distinct_out, c->anDistinct.p, k * 4, cudaMemcpyDeviceToHost, c->st));
+    if (code_out) CK(cudaMemcpyAsync(code_out, c->anCode.p, k * 4, cudaMemcpyDeviceToHost, c->st));
+    c->an_pos = nullptr;
+    c->an_k = 0;
+    stage_finish(c, 1);
+    return NMX_OK;
   });
 }
 

@@ -60,3 +60,66 @@ __global__ void __launch_bounds__(256) unpack_records_kernel(const uint8_t* __re
 }
 
 }  // namespace nmx
+
+namespace nmx {
+
+// ---------------------------------------------------------------------------
+// anonymize (traffic.py:107-137) on the device, SURVEY.md 8(f) f3.
+// Addresses of the interleaved stream e = 2p (src of packet p), 2p + 1 (dst)
+// are stably sorted with their positions; run heads give the distinct addresses
+// and their first positions; the first-seen rank of an address is the number of
+// first positions before its own (a flag scan over positions); its code is
+// perm[rank] with perm = default_rng(key).permutation(k) drawn by the caller.
+// ---------------------------------------------------------------------------
+__global__ void anon_pairs_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst, uint64_t n,
+                                  uint32_t* __restrict__ keys, uint32_t* __restrict__ pos) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    reinterpret_cast<uint2*>(keys)[p] = make_uint2(src[p], dst[p]);
+    reinterpret_cast<uint2*>(pos)[p] = make_uint2((uint32_t)(2 * p), (uint32_t)(2 * p + 1));
+  }
+}
+
+// head[j] = 1 where a new address starts in the sorted keys
+__global__ void anon_heads_kernel(const uint32_t* __restrict__ keys, uint64_t m, uint32_t* __restrict__ head) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x)
+    head[j] = (j == 0 || keys[j] != keys[j - 1]) ? 1u : 0u;
+}
+
+// per head j (uid = hoff[j]): distinct[uid] = address, first[uid] = its first
+// position (stable sort: the run's first element), flag[first] = 1
+__global__ void anon_uniques_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ pos,
+                                    const uint32_t* __restrict__ head, const uint32_t* __restrict__ hoff, uint64_t m,
+                                    uint32_t* __restrict__ distinct, uint32_t* __restrict__ first,
+                                    uint32_t* __restrict__ flag) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x) {
+    if (!head[j]) continue;
+    const uint32_t u = hoff[j];
+    distinct[u] = keys[j];
+    first[u] = pos[j];
+    flag[pos[j]] = 1u;
+  }
+}
+
+// code[u] = perm[rank(u)], rank(u) = number of first positions before first[u]
+__global__ void anon_codes_kernel(const uint32_t* __restrict__ first, const uint32_t* __restrict__ foff,
+                                  const uint32_t* __restrict__ perm, uint64_t k, uint32_t* __restrict__ code) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < k; u += (uint64_t)gridDim.x * blockDim.x)
+    code[u] = perm[foff[first[u]]];
+}
+
+// relabel: element j of the sorted stream (address run uid = hoff[j] + head[j] - 1)
+// writes its code back to its packet position
+__global__ void anon_scatter_kernel(const uint32_t* __restrict__ pos, const uint32_t* __restrict__ head,
+                                    const uint32_t* __restrict__ hoff, uint64_t m, const uint32_t* __restrict__ code,
+                                    uint32_t* __restrict__ src_out, uint32_t* __restrict__ dst_out) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t e = pos[j];
+    const uint32_t c = code[hoff[j] + head[j] - 1];
+    if (e & 1u)
+      dst_out[e >> 1] = c;
+    else
+      src_out[e >> 1] = c;
+  }
+}
+
+}  // namespace nmx

@@ -17,6 +17,7 @@ reference's own tests and callers work unchanged. The hot path itself
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import Mapping
 from dataclasses import dataclass, field
 from typing import Iterator
 
@@ -101,19 +102,50 @@ def generate_packets(n: int, address_space: int, seed: int, invalid_fraction: fl
     return PacketStream(src=src, dst=dst, valid=valid, address_space=address_space)
 
 
+class AddressMap(Mapping):
+    """Raw address -> anonymized index, the ``AnonymizationMap.mapping`` of
+    traffic.py:74-79 as a read-only Mapping over two device-produced tables
+    (ascending distinct addresses, their codes) instead of a k-entry Python dict."""
+
+    def __init__(self, distinct: np.ndarray, code: np.ndarray):
+        self._d = distinct
+        self._c = code
+
+    def __getitem__(self, address):
+        try:
+            a = int(address)
+        except (TypeError, ValueError):
+            raise KeyError(address) from None
+        i = int(np.searchsorted(self._d, a)) if 0 <= a < 2**32 else len(self._d)
+        if i < len(self._d) and int(self._d[i]) == a:
+            return int(self._c[i])
+        raise KeyError(address)
+
+    def __iter__(self):
+        return iter(self._d.tolist())
+
+    def __len__(self) -> int:
+        return len(self._d)
+
+    def values(self):
+        return self._c.astype(np.int64).tolist()
+
+
 def anonymize(stream: PacketStream, key: int) -> tuple[PacketStream, AnonymizationMap]:
-    """Keyed first-seen dense relabel (traffic.py:107-137; host input preparation,
-    SURVEY.md 8(f) f3 lists the GPU version as a next step)."""
-    both = np.empty(2 * len(stream), dtype=np.int64)
-    both[0::2], both[1::2] = stream.src, stream.dst
-    distinct, first, inverse = np.unique(both, return_index=True, return_inverse=True)
-    rank = np.empty(len(distinct), dtype=np.int64)
-    rank[np.argsort(first, kind="stable")] = np.arange(len(distinct), dtype=np.int64)
-    code = np.random.default_rng(key).permutation(len(distinct)).astype(np.int64)[rank]
-    relabeled = code[inverse]
-    anon = PacketStream(src=relabeled[0::2].copy(), dst=relabeled[1::2].copy(), valid=stream.valid.copy(),
-                        address_space=max(1, len(distinct)))
-    return anon, AnonymizationMap(key=key, mapping=dict(zip(distinct.tolist(), code.tolist())))
+    """Relabel every observed address with a keyed pseudorandom dense index
+    (traffic.py:107-137): first-seen order over src0, dst0, src1, dst1, ...,
+    mapped through default_rng(key).permutation(k). The sort, run detection,
+    first-seen ranking and relabel run on the GPU (nmx_anonymize_begin/finish,
+    SURVEY.md 8(f) f3); addresses must fit the 32-bit packet format."""
+    src, dst, _ = stream.wire()
+    so, do, k, distinct, code = _lib.anonymize_device(src, dst, key)
+    n = len(stream)
+    s_out = so.download()[:n].astype(np.int64)
+    d_out = do.download()[:n].astype(np.int64)
+    so.close()
+    do.close()
+    anon = PacketStream(src=s_out, dst=d_out, valid=stream.valid.copy(), address_space=max(1, k))
+    return anon, AnonymizationMap(key=key, mapping=AddressMap(distinct, code))
 
 
 @dataclass(eq=False)

@@ -55,10 +55,7 @@ def test_generate_packets_matches_reference_restatement():
     s = nm.generate_packets(5000, 77, seed=42, invalid_fraction=0.2)
     rs, rd, rv = orc.generate_packets(5000, 77, 42, 0.2)
     assert np.array_equal(s.src, rs) and np.array_equal(s.dst, rd) and np.array_equal(s.valid, rv)
-    a, amap = nm.anonymize(s, key=9)
-    os_, od, space = orc.anonymize(rs, rd, 9)
-    assert np.array_equal(a.src, os_) and np.array_equal(a.dst, od) and a.address_space == space
-    assert sorted(amap.mapping.values()) == list(range(len(amap.mapping)))
+    # anonymize runs on the GPU: tests/test_gpu_anonymize.py
 
 
 def test_partition_rules_exhaustive_small():
