@@ -41,10 +41,15 @@ CONFIGS = {
     "cfg4": (30, 1 << 32, "powerlaw"),
     "cfg2": (23, 1 << 24, "uniform"),
     "cfg1": (17, 1 << 18, "uniform"),
-    # config 5 streamed from pinned host buffers in 2^28-packet windows with
-    # cross-window merge-add; 2^31 of the 2^32 packets (a matrix keeps u32 link
-    # indices, and 2^32 uniform packets would reach 2^32 unique links)
+    # config 5 streamed from pinned host buffers in 2^28-packet windows into one
+    # device-resident running sum; 2^31 of the 2^32 packets fit one B200 (positions
+    # are u32 with a flag bit), 8 B200 take 2^29 each
     "cfg5": (31, 1 << 32, "uniform"),
+    # 9-byte packet-file records (traffic.py:25) in pinned host
+    # memory, streamed raw and unpacked on the GPU (nmx_stream_records)
+    "file": (29, 1 << 32, "uniform"),
+    # anonymize (traffic.py:107-137) of a cfg2-sized stream
+    "anon": (23, 1 << 32, "uniform"),
 }
 
 
@@ -229,6 +234,105 @@ def run_cfg5(args) -> None:
     for a, b in wins:
         a.close()
         b.close()
+
+
+def run_file(args) -> None:
+    """Packet-file records (9 B/packet) in pinned host memory -> nine statistics; rank 0 only."""
+    import numpy as np
+
+    from paper_2510_14050_b200 import _lib
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    log2n, space, gen = CONFIGS["file"]
+    if args.log2n:
+        log2n = args.log2n
+    n = 1 << log2n
+    w = 1 << min(25, log2n)
+    kind = _lib.GEN_UNIFORM if gen == "uniform" else _lib.GEN_POWERLAW
+    rec = _lib.PinnedArray(9 * n, dtype=np.uint8)  # the file image, prepared outside the timed region
+    view = rec.array.view(np.dtype([("src", "<u4"), ("dst", "<u4"), ("valid", "u1")]))
+    ds, dd = _lib.DeviceArray(w), _lib.DeviceArray(w)
+    for k in range(n // w):
+        _lib.generate(kind, 7, k * w, w, space, ds, dd)
+        view["src"][k * w:(k + 1) * w] = ds.download()
+        view["dst"][k * w:(k + 1) * w] = dd.download()
+    view["valid"][:] = 1
+    ds.close()
+    dd.close()
+    windows = [rec.array[i:i + 9 * w] for i in range(0, 9 * n, 9 * w)]
+    stats = _lib.stream_records(windows, space)
+    times = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            stats = _lib.stream_records(windows, space)
+            times.append(time.perf_counter() - t0)
+    best = min(times)
+    print(json.dumps({
+        "metric": METRIC, "value": n / best, "unit": "packets/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": 1, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"file: 2^{log2n} packets as 9-byte packet-file records (traffic.py:25) in pinned host "
+                               f"memory, {n // w} windows of 2^{int(np.log2(w))} streamed raw (9 B/packet H2D on a "
+                               "copy stream), unpacked on the GPU, summed matrix, 9 statistics (nmx_stream_records)",
+                   "packets": n, "timing": "wall clock of the host call (host-synchronous), best of steps"},
+        "stats9": list(stats),
+        "e2e": {"value": n / best, "unit": "packets/s", "h2d_bytes_per_step": 9 * n, "d2h_bytes_per_step": 72},
+        "clocks": clk.summary(),
+    }), flush=True)
+    rec.close()
+
+
+def run_anon(args) -> None:
+    """anonymize (traffic.py:107-137) on the GPU vs the numpy restatement; rank 0 only."""
+    import numpy as np
+
+    from oracle import netmeter_oracle as orc
+    from paper_2510_14050_b200 import _lib
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    log2n, space, gen = CONFIGS["anon"]
+    if args.log2n:
+        log2n = args.log2n
+    n = 1 << log2n
+    src, dst = (orc.gen_uniform if gen == "uniform" else orc.gen_powerlaw)(3, 0, n, space)
+    ds, dd = _lib.DeviceArray(n), _lib.DeviceArray(n)
+    ds.upload(src)
+    dd.upload(dst)
+    dev_t, host_t = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        so, do, k, _, _ = _lib.anonymize_device(ds, dd, 17, tables=False)  # device in, device out
+        t1 = time.perf_counter()
+        so.close(); do.close()
+        so, do, k, dist, code = _lib.anonymize_device(src, dst, 17)  # host in, host out (+ tables)
+        s_out, d_out = so.download(), do.download()
+        t2 = time.perf_counter()
+        so.close(); do.close()
+        if i >= args.warmup:
+            dev_t.append(t1 - t0)
+            host_t.append(t2 - t1)
+    t0 = time.perf_counter()
+    rs, rd, rk = orc.anonymize(src.astype(np.int64), dst.astype(np.int64), 17)
+    cpu = time.perf_counter() - t0
+    assert k == rk and np.array_equal(s_out, rs) and np.array_equal(d_out, rd)
+    print(json.dumps({
+        "metric": "packets/sec for anonymize (traffic.py:107-137)", "value": n / min(dev_t), "unit": "packets/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": min(dev_t) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"anon: anonymize 2^{log2n} {gen} packets over {space} addresses, key 17; value = "
+                               "device columns in/out incl. the host permutation draw (numpy default_rng(key)."
+                               "permutation(k), the reference's own RNG); e2e = host arrays in, host arrays + "
+                               "distinct/code tables out", "packets": n, "distinct": k,
+                   "timing": "wall clock of the host calls, best of steps"},
+        "e2e": {"value": n / min(host_t), "unit": "packets/s", "h2d_bytes_per_step": 8 * n + 4 * k,
+                "d2h_bytes_per_step": 8 * n + 8 * k},
+        "cpu_baseline": {"value": n / cpu, "unit": "packets/s", "cores": 1, "kind": "port",
+                         "sample": f"the same 2^{log2n} packets through oracle/netmeter_oracle.py anonymize "
+                                   "(numpy restatement of traffic.py:107-137 without its Python dict)"},
+    }), flush=True)
 
 
 def run_nmx(args) -> None:
@@ -417,6 +521,10 @@ def main() -> None:
         run_reference(args)
     elif args.config == "cfg5":
         run_cfg5(args)
+    elif args.config == "file":
+        run_file(args)
+    elif args.config == "anon":
+        run_anon(args)
     else:
         run_nmx(args)
 
