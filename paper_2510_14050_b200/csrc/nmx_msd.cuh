@@ -399,6 +399,8 @@ __device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
   return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
 }
 __device__ __forceinline__ uint32_t h16(uint64_t x) { return (uint32_t)((x * 0xD6E8FEB86659FD93ull) >> 48); }
+// 16-bit counter index of a 32-bit value (sources, destinations): one IMAD
+__device__ __forceinline__ uint32_t h16u(uint32_t x) { return (x * 0x9E3779B1u) >> 16; }
 // count one occurrence in a 2-bit saturating counter (01 = once, 11 = twice or more)
 __device__ __forceinline__ void bm_hit(uint32_t* bm, uint32_t h) {
   const uint32_t bit = 1u << ((h & 15) * 2);
@@ -509,12 +511,15 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     const uint32_t gn = g + gridDim.x;
     uint4 pnext = make_uint4(0, 0, 0, 0);
     if (tid == 0 && gn < ngroups) pnext = plan[gn];
-    // 1. hash counters
+    // 1. hash counters (the 16-bit counter indices stay in registers for phases 2-3)
+    uint32_t kh[kLocPerThread], sh[kLocPerThread];
 #pragma unroll
     for (int r = 0; r < kLocPerThread; ++r) {
+      kh[r] = h16(kr[r]);
+      sh[r] = h16u((uint32_t)(kr[r] >> b));
       if ((uint32_t)r < nmine) {
-        bm_hit(s.bml, h16(kr[r]));
-        if (!PARTIAL) bm_hit(s.bms, h16(kr[r] >> b));
+        bm_hit(s.bml, kh[r]);
+        if (!PARTIAL) bm_hit(s.bms, sh[r]);
       }
     }
     if (tid == 0) s.plan[cur ^ 1] = pnext;
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       if (key == ~0ull) {
         fresh = atomicAdd(&s.sp_link, 1u) == 0;
         if (fresh) st[r] |= 2;
-      } else if (bm_once(s.bml, h16(key))) {
+      } else if (bm_once(s.bml, kh[r])) {
         fresh = true;
         st[r] |= 1;
       } else {
@@ -578,7 +583,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       if (src == 0xFFFFFFFFu) {
         atomicAdd(&s.sp_src_pk, 1u);
         if (fresh) atomicAdd(&s.sp_src_fo, 1u);
-      } else if (bm_once(s.bms, h16(src))) {
+      } else if (bm_once(s.bms, sh[r])) {
         st[r] |= 4;
       } else {
         const uint32_t sk = src + 1;
@@ -691,8 +696,8 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         s.t2key[hs[r]] = 0;
         s.t2pf[hs[r]] = 0;
       }
-      s.bml[h16(key) >> 4] = 0;  // benign: every writer stores 0
-      s.bms[h16(key >> b) >> 4] = 0;
+      s.bml[kh[r] >> 4] = 0;  // benign: every writer stores 0
+      if (!PARTIAL) s.bms[sh[r] >> 4] = 0;
     }
     if (tid == 0 && s.sp_src_pk) {
       if (PARTIAL) {
@@ -825,7 +830,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     if (tid == 0 && gn < ngroups) pnext = plan[gn];
 #pragma unroll
     for (int r = 0; r < kLocPerThread; ++r)
-      if ((uint32_t)r < nmine) bm_hit(s.bm, h16(kr[r]));
+      if ((uint32_t)r < nmine) bm_hit(s.bm, h16u(kr[r]));  // one IMAD: recomputed below, not kept
     if (tid == 0) s.plan[cur ^ 1] = pnext;
     __syncthreads();
     const uint4 pn = s.plan[cur ^ 1];
@@ -853,7 +858,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       const unsigned long long add = (1ull << 32) | vr[r];
       if (d == 0xFFFFFFFFu) {
         atomicAdd(&s.sp, add);
-      } else if (bm_once(s.bm, h16(d))) {
+      } else if (bm_once(s.bm, h16u(d))) {
         stc |= 1u << r;
       } else {
         const uint32_t dk = d + 1;
@@ -892,7 +897,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
         s.key[hh[r]] = 0;
         s.ns[hh[r]] = 0;
       }
-      s.bm[h16(kr[r]) >> 4] = 0;
+      s.bm[h16u(kr[r]) >> 4] = 0;
     }
     if (tid == 0 && s.sp) {
       a_cnt += 1;
