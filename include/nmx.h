@@ -37,6 +37,7 @@ extern "C" {
 #define NMX_ENOMEM -2  /* device or pinned-host allocation failed  */
 #define NMX_ECUDA -3   /* CUDA runtime / kernel error              */
 #define NMX_ENODEV -4  /* no CUDA device                           */
+#define NMX_EFORMAT -5 /* text outside the device fast path: re-parse on the host */
 
 #define NMX_GEN_UNIFORM 0  /* SURVEY.md 8(d) cfg3 generator */
 #define NMX_GEN_POWERLAW 1 /* SURVEY.md 8(d) cfg4 "octave" generator */
@@ -121,6 +122,18 @@ int nmx_anonymize_begin(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_d
 int nmx_anonymize_finish(nmx_ctx* ctx, const uint32_t* perm, uint32_t* d_src_out, uint32_t* d_dst_out,
                          uint32_t* distinct_out, uint32_t* code_out);
 
+/* Text matrix files (traffic.py:295-367): header "dim nnz", then
+ * "row col value" lines sorted row-major without duplicates.
+ *  - nmx_parse_matrix_text: host text -> device COO (keys row << 32 | col, u32 values)
+ *    + header; NMX_EFORMAT when the text is not in the device fast path (bytes other
+ *    than digits, signs, ' ', '\t', '\n') or fails validation (token counts, bounds,
+ *    value >= 1, order, nnz) -- the caller re-parses on the host for the exact error.
+ *  - nmx_format_matrix_text: entry columns -> the "row col value\n" lines (without the
+ *    header); call with out == NULL (or cap too small) to get *bytes first. */
+int nmx_parse_matrix_text(nmx_ctx* ctx, const char* text, uint64_t bytes, int64_t hdr[2], nmx_coo** out);
+int nmx_format_matrix_text(nmx_ctx* ctx, const int64_t* rows, const int64_t* cols, const int64_t* vals, uint64_t nnz,
+                           char* out, uint64_t cap, uint64_t* bytes);
+
 /* Per-window statistics: window t = packets [t*W, (t+1)*W) by raw position,
  * invalid packets keep their position (traffic.py:221-242); out has
  * ceil(n/W) rows of 9 (analyze_dataset per-window reports, analytics.py:109-130). */
@@ -169,6 +182,8 @@ int nmx_flat_fetch(nmx_ctx* ctx, int64_t* edge_src, int64_t* row_ids, int64_t* r
 int nmx_coo_from_packets(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
                          uint64_t n, nmx_coo** out);
 int nmx_coo_merge_add(nmx_ctx* ctx, const nmx_coo* a, const nmx_coo* b, nmx_coo** out);
+/* host sorted unique keys (src << 32 | dst) + counts in [1, 2^32-1] -> device COO */
+int nmx_coo_upload(nmx_ctx* ctx, const uint64_t* keys, const int64_t* counts, uint64_t nnz, nmx_coo** out);
 int nmx_coo_stats9(nmx_ctx* ctx, const nmx_coo* a, int64_t out[9]);
 int nmx_coo_nnz(const nmx_coo* a, uint64_t* nnz);
 int nmx_coo_download(nmx_ctx* ctx, const nmx_coo* a, uint64_t* keys, int64_t* counts);

@@ -50,6 +50,8 @@ SIGNATURES = {
     "nmx_stream_stats9": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stream_records": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_anonymize_begin": (C.c_int, [_VP, _VP, _VP, _U64, _VP]),
+    "nmx_parse_matrix_text": (C.c_int, [_VP, _VP, _U64, _VP, _VP]),
+    "nmx_format_matrix_text": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _VP, _U64, _VP]),
     "nmx_anonymize_finish": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "nmx_unpack_records": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _VP, _U64]),
     "nmx_window_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
@@ -61,6 +63,7 @@ SIGNATURES = {
     "nmx_flat_build": (C.c_int, [_VP, _VP, _U64, _VP, _VP, _U64, C.POINTER(_U64), C.POINTER(_U64)]),
     "nmx_flat_fetch": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "nmx_coo_from_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.POINTER(_VP)]),
+    "nmx_coo_upload": (C.c_int, [_VP, _VP, _VP, _U64, C.POINTER(_VP)]),
     "nmx_coo_merge_add": (C.c_int, [_VP, _VP, _VP, C.POINTER(_VP)]),
     "nmx_coo_stats9": (C.c_int, [_VP, _VP, _VP]),
     "nmx_coo_nnz": (C.c_int, [_VP, C.POINTER(_U64)]),
@@ -325,6 +328,41 @@ def anonymize_device(src, dst, key: int, device: int = 0, tables: bool = True):
                                         code.ctypes.data if tables and k else None))
     del keep
     return so, do, k, distinct, code
+
+
+EFORMAT = -5
+
+
+def parse_matrix_text(text: bytes, device: int = 0):
+    """Text matrix file bytes -> (dim, nnz, COO handle) parsed on the GPU, or None when
+    the text is outside the device fast path (the caller re-parses on the host)."""
+    ctx = context(device)
+    hdr = np.zeros(2, dtype=np.int64)
+    h = C.c_void_p()
+    buf = np.frombuffer(text, dtype=np.uint8) if len(text) else np.zeros(1, np.uint8)
+    rc = ctx._lib.nmx_parse_matrix_text(ctx.handle, buf.ctypes.data, len(text), hdr.ctypes.data, C.byref(h))
+    if rc == EFORMAT:
+        return None
+    check(rc)
+    return int(hdr[0]), int(hdr[1]), h
+
+
+def format_matrix_text(rows, cols, values, device: int = 0) -> bytes:
+    """The "row col value\n" lines of a matrix file, formatted on the GPU."""
+    ctx = context(device)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    v = np.ascontiguousarray(values, dtype=np.int64)
+    n = len(r)
+    if n == 0:
+        return b""
+    size = C.c_uint64()
+    check(ctx._lib.nmx_format_matrix_text(ctx.handle, r.ctypes.data, c.ctypes.data, v.ctypes.data, n, None, 0,
+                                          C.byref(size)))
+    out = np.empty(int(size.value), dtype=np.uint8)
+    check(ctx._lib.nmx_format_matrix_text(ctx.handle, r.ctypes.data, c.ctypes.data, v.ctypes.data, n,
+                                          out.ctypes.data, out.nbytes, C.byref(size)))
+    return out.tobytes()
 
 
 def window_stats9(src, dst, valid, address_space: int, window_size: int, device: int = 0) -> np.ndarray:

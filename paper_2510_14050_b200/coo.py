@@ -95,6 +95,18 @@ def coo_from_packets(src, dst, valid=None, device: int = 0) -> DeviceCOO:
     return DeviceCOO(h, device)
 
 
+def coo_from_keys(keys, counts, device: int = 0) -> DeviceCOO:
+    """Upload host sorted unique keys ((src << 32) | dst) with counts as a DeviceCOO."""
+    ctx = _lib.context(device)
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    if len(k) != len(c):
+        raise ValueError("keys and counts must have equal lengths")
+    h = C.c_void_p()
+    _lib.check(ctx._lib.nmx_coo_upload(ctx.handle, k.ctypes.data, c.ctypes.data, len(k), C.byref(h)))
+    return DeviceCOO(h, device)
+
+
 def merge_add(a: DeviceCOO, b: DeviceCOO) -> DeviceCOO:
     """Element-wise sum C = A + B (merge path over sorted keys)."""
     ctx = _lib.context(a.device)

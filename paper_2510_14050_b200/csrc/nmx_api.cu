@@ -15,6 +15,7 @@
 #include "../../include/nmx.h"
 #include "nmx_io.cuh"
 #include "nmx_merge.cuh"
+#include "nmx_text.cuh"
 #include "nmx_seg.cuh"
 
 using namespace nmx;
@@ -114,7 +115,8 @@ struct nmx_ctx {
   DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red, ws0, ws1, wd0, wd1, wv0, wv1, wr0, wr1, rmax, anAk, anAv, anBk, anBv, anHead, anHoff, anDistinct,
-      anFirst, anFlag, anFoff, anPerm, anCode, msplit, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
+      anFirst, anFlag, anFoff, anPerm, anCode, txt, tcnt, toff, tends, tntok, tvals, tnb, tnboff, thdr, tbad, trows,
+      tcols, tval, tlen, tloff, msplit, lightK, lightCK, lightCV, sccnt, scur, sloff, spoffA, spoffB, srep, ssum, sbsum, sbflag, stot, gsk, gsv,
       hcount;
   uint32_t epoch = 0;
   cudaStream_t st2 = nullptr;  // copy stream of the streamed path
@@ -187,6 +189,8 @@ struct nmx_coo {
   uint64_t* keys = nullptr;
   uint32_t* counts = nullptr;
 };
+
+extern "C" nmx_coo* coo_alloc(nmx_ctx* c, uint64_t nnz);  // stream-ordered COO storage (below)
 
 namespace {
 
@@ -1643,6 +1647,128 @@ int nmx_anonymize_finish(nmx_ctx* c, const uint32_t* perm, uint32_t* d_src_out, 
   });
 }
 
+// ---- text matrix files (nmx_text.cuh, traffic.py:295-367) -------------------
+int nmx_parse_matrix_text(nmx_ctx* c, const char* text, uint64_t T, int64_t hdr_out[2], nmx_coo** out) {
+  if (!out || !hdr_out || (T && !text)) return fail(NMX_EINVAL, "null argument");
+  *out = nullptr;
+  if (T == 0 || T >= (1ull << 40)) return NMX_EFORMAT;
+  return guarded(c, [&] {
+    c->txt.grow(T + 16);
+    CK(cudaMemcpyAsync(c->txt.p, text, T, cudaMemcpyHostToDevice, c->st));
+    const uint64_t nb = (T + kTextChunk - 1) / kTextChunk;
+    c->tcnt.grow((nb + 8) * 4);
+    c->toff.grow((nb + 8) * 4);
+    c->tbad.grow(64);
+    unsigned int* bad = c->tbad.as<unsigned int>();
+    CK(cudaMemsetAsync(bad, 0, 4, c->st));
+    text_nl_count_kernel<<<(unsigned)nb, 256, 0, c->st>>>(c->txt.as<char>(), T, c->tcnt.as<uint32_t>());
+    CK_LAUNCH();
+    scan_counts(c, c->tcnt.as<uint32_t>(), (uint32_t)nb, c->toff.as<uint32_t>(), nullptr);
+    uint32_t nl = 0;
+    CK(cudaMemcpyAsync(&nl, c->toff.as<uint32_t>() + nb, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const bool open_end = text[T - 1] != '\n';
+    const uint64_t L = (uint64_t)nl + (open_end ? 1 : 0);
+    c->tends.grow((L + 8) * 8);
+    text_nl_write_kernel<<<(unsigned)nb, 256, 0, c->st>>>(c->txt.as<char>(), T, c->toff.as<uint32_t>(),
+                                                          c->tends.as<uint64_t>());
+    CK_LAUNCH();
+    if (open_end) CK(cudaMemcpyAsync(c->tends.as<uint64_t>() + L - 1, &T, 8, cudaMemcpyHostToDevice, c->st));
+    c->tntok.grow(L + 16);
+    c->tvals.grow((L + 8) * 24);
+    c->tnb.grow((L + 8) * 4);
+    c->tnboff.grow((L + 8) * 4);
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((L + 255) / 256, (uint64_t)c->sms * 16));
+    text_parse_lines_kernel<<<g, 256, 0, c->st>>>(c->txt.as<char>(), c->tends.as<uint64_t>(), L,
+                                                  c->tntok.as<uint8_t>(), c->tvals.as<long long>(), bad);
+    CK_LAUNCH();
+    text_nonblank_kernel<<<g, 256, 0, c->st>>>(c->tntok.as<uint8_t>(), L, c->tnb.as<uint32_t>());
+    CK_LAUNCH();
+    scan_counts(c, c->tnb.as<uint32_t>(), (uint32_t)L, c->tnboff.as<uint32_t>(), nullptr);
+    uint32_t nbl = 0;
+    unsigned int b0 = 0;
+    CK(cudaMemcpyAsync(&nbl, c->tnboff.as<uint32_t>() + L, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&b0, bad, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->launches += 5;
+    if (b0 || nbl == 0) return NMX_EFORMAT;
+    const uint64_t nnz = nbl - 1;
+    nmx_coo* o = coo_alloc(c, nnz);
+    c->thdr.grow(64);
+    long long* hdr = c->thdr.as<long long>();
+    text_entries_kernel<<<g, 256, 0, c->st>>>(c->tntok.as<uint8_t>(), c->tvals.as<long long>(),
+                                              c->tnboff.as<uint32_t>(), L, hdr,
+                                              reinterpret_cast<unsigned long long*>(o->keys), o->counts, bad);
+    CK_LAUNCH();
+    long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, hdr, 16, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&b0, bad, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (b0 || h[0] < 1 || h[1] < 0 || (uint64_t)h[1] != nnz || h[0] > (1ll << 31)) {
+      nmx_coo_free(o);
+      return NMX_EFORMAT;
+    }
+    if (nnz) {
+      const unsigned gn =
+          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nnz + 255) / 256, (uint64_t)c->sms * 16));
+      text_check_kernel<<<gn, 256, 0, c->st>>>(reinterpret_cast<const unsigned long long*>(o->keys), nnz, h[0], bad);
+      CK_LAUNCH();
+      CK(cudaMemcpyAsync(&b0, bad, 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      if (b0) {
+        nmx_coo_free(o);
+        return NMX_EFORMAT;
+      }
+    }
+    c->launches += 2;
+    hdr_out[0] = h[0];
+    hdr_out[1] = h[1];
+    *out = o;
+    return NMX_OK;
+  });
+}
+
+int nmx_format_matrix_text(nmx_ctx* c, const int64_t* rows, const int64_t* cols, const int64_t* vals, uint64_t nnz,
+                           char* out, uint64_t cap, uint64_t* bytes) {
+  if (!bytes || (nnz && (!rows || !cols || !vals))) return fail(NMX_EINVAL, "null argument");
+  return guarded(c, [&] {
+    *bytes = 0;
+    if (!nnz) return NMX_OK;
+    c->trows.grow(nnz * 8);
+    c->tcols.grow(nnz * 8);
+    c->tval.grow(nnz * 8);
+    c->tlen.grow((nnz + 8) * 4);
+    c->tloff.grow((nnz + 8) * 8);
+    CK(cudaMemcpyAsync(c->trows.p, rows, nnz * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->tcols.p, cols, nnz * 8, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->tval.p, vals, nnz * 8, cudaMemcpyHostToDevice, c->st));
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nnz + 255) / 256, (uint64_t)c->sms * 16));
+    auto* R = c->trows.as<unsigned long long>();
+    auto* Cc = c->tcols.as<unsigned long long>();
+    auto* V = c->tval.as<unsigned long long>();
+    text_line_len_kernel<<<g, 256, 0, c->st>>>(R, Cc, V, nnz, c->tlen.as<uint32_t>());
+    CK_LAUNCH();
+    // line offsets: the u32 scan gives offsets < 2^32; the text stays below 4 GiB per call
+    if (nnz >= (1ull << 32) / 64) throw std::runtime_error("matrix too large for one text call");
+    c->toff.grow((nnz + 8) * 4);
+    scan_counts(c, c->tlen.as<uint32_t>(), (uint32_t)nnz, c->toff.as<uint32_t>(), nullptr);
+    uint32_t total = 0;
+    CK(cudaMemcpyAsync(&total, c->toff.as<uint32_t>() + nnz, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    *bytes = total;
+    if (!out || cap < total) return NMX_OK;
+    c->txt.grow((uint64_t)total + 16);
+    widen_offsets_kernel<<<g, 256, 0, c->st>>>(c->toff.as<uint32_t>(), nnz, c->tloff.as<unsigned long long>());
+    CK_LAUNCH();
+    text_write_lines_kernel<<<g, 256, 0, c->st>>>(R, Cc, V, nnz, c->tloff.as<unsigned long long>(), c->txt.as<char>());
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(out, c->txt.p, total, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->launches += 4;
+    return NMX_OK;
+  });
+}
+
 int nmx_window_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
                              uint64_t n, uint64_t address_space, uint64_t window_size, int64_t* out) {
   if (window_size < 1) return fail(NMX_EINVAL, "window_size must be >= 1");
@@ -1988,6 +2114,24 @@ int nmx_coo_from_packets(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_ds
     }
     nmx_coo* o = coo_alloc(c, u);
     stage_finish(c, 1);
+    *out = o;
+    return NMX_OK;
+  });
+}
+
+int nmx_coo_upload(nmx_ctx* c, const uint64_t* keys, const int64_t* counts, uint64_t nnz, nmx_coo** out) {
+  if (!out || (nnz && (!keys || !counts))) return fail(NMX_EINVAL, "null argument");
+  for (uint64_t i = 0; i < nnz; ++i)
+    if (counts[i] < 1 || counts[i] > 0xFFFFFFFFll) return fail(NMX_EINVAL, "COO counts must lie in [1, 2^32-1]");
+  return guarded(c, [&] {
+    std::vector<uint32_t> cc(nnz);
+    for (uint64_t i = 0; i < nnz; ++i) cc[i] = (uint32_t)counts[i];
+    nmx_coo* o = coo_alloc(c, nnz);
+    if (nnz) {
+      CK(cudaMemcpyAsync(o->keys, keys, nnz * 8, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(o->counts, cc.data(), nnz * 4, cudaMemcpyHostToDevice, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
     *out = o;
     return NMX_OK;
   });

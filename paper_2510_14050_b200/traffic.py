@@ -346,3 +346,101 @@ def read_packets(path, address_space: int | None = None) -> PacketStream:
     if address_space is None:
         address_space = int(max(src.max(), dst.max())) + 1 if len(raw) else 1
     return PacketStream(src=src, dst=dst, valid=raw["valid"] != 0, address_space=address_space)
+
+
+# ---------------------------------------------------------------------------
+# text matrix files (traffic.py:295-367)
+# ---------------------------------------------------------------------------
+def write_matrix(matrix: TrafficMatrix, path) -> None:
+    """Coordinate text form: ``dim nnz`` header, then sorted ``row col value`` lines
+    (traffic.py:295-304); the lines are formatted on the GPU."""
+    matrix.validate()
+    rows = np.repeat(np.arange(matrix.dim, dtype=np.int64), np.diff(matrix.row_ptr))
+    body = _lib.format_matrix_text(rows, matrix.col_idx, matrix.values)
+    with open(path, "wb") as f:
+        f.write(f"{matrix.dim} {matrix.nnz}\n".encode())
+        f.write(body)
+
+
+def _read_matrix_host(path, text: str, window_id: int) -> TrafficMatrix:
+    """The reference's parser (traffic.py:307-367) for text outside the device fast
+    path: identical acceptance rules and MatrixFileError messages."""
+    lines = [(lineno, parts) for lineno, parts in enumerate((ln.split() for ln in text.splitlines()), 1) if parts]
+
+    def fail(lineno: int, why: str) -> MatrixFileError:
+        return MatrixFileError(f"{path}: line {lineno}: {why}")
+
+    if not lines:
+        raise fail(1, "expected header 'dim nnz'")
+    if len(lines[0][1]) != 2:
+        raise fail(lines[0][0], "expected header 'dim nnz'")
+    try:
+        dim, nnz = (int(tok) for tok in lines[0][1])
+    except ValueError:
+        raise fail(lines[0][0], "expected header 'dim nnz'") from None
+    if dim < 1:
+        raise fail(lines[0][0], "dim must be >= 1")
+    if nnz < 0:
+        raise fail(lines[0][0], "nnz must be >= 0")
+    entry_lines = lines[1:]
+    entries = np.empty((len(entry_lines), 3), dtype=np.int64)
+    for k, (lineno, parts) in enumerate(entry_lines):
+        if len(parts) != 3:
+            raise fail(lineno, "expected 'row col value'")
+        try:
+            entries[k] = [int(tok) for tok in parts]
+        except (ValueError, OverflowError):
+            raise fail(lineno, "expected 'row col value' integers") from None
+    if len(entry_lines) != nnz:
+        raise MatrixFileError(f"{path}: header claims {nnz} entries, file has {len(entry_lines)}")
+    rows, cols, values = entries[:, 0], entries[:, 1], entries[:, 2]
+    line_no = np.array([lineno for lineno, _ in entry_lines], dtype=np.int64)
+    if nnz:
+        bounds = (rows < 0) | (rows >= dim) | (cols < 0) | (cols >= dim)
+        if np.any(bounds):
+            raise fail(int(line_no[np.argmax(bounds)]), f"row/col outside [0, {dim})")
+        if np.any(values < 1):
+            raise fail(int(line_no[np.argmax(values < 1)]), "value must be >= 1")
+        disorder = np.diff(rows * dim + cols) <= 0
+        if np.any(disorder):
+            raise fail(int(line_no[np.argmax(disorder) + 1]), "entries must be sorted row-major with no duplicates")
+    row_ptr = np.zeros(dim + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=dim), out=row_ptr[1:])
+    return TrafficMatrix(window_id=window_id, dim=dim, row_ptr=row_ptr, col_idx=cols, values=values)
+
+
+def read_matrix_device(path, window_id: int = 0):
+    """Parse a matrix file on the GPU into a device COO (keys row << 32 | col, u32
+    counts) without host containers: (dim, DeviceCOO). Text outside the device fast
+    path goes through the reference parser (exact errors) and is uploaded."""
+    from .coo import DeviceCOO, coo_from_keys
+
+    data = open(path, "rb").read()
+    got = _lib.parse_matrix_text(data)
+    if got is not None:
+        dim, _, h = got
+        return dim, DeviceCOO(h)
+    m = _read_matrix_host(path, data.decode("utf-8", errors="replace"), window_id)
+    rows = np.repeat(np.arange(m.dim, dtype=np.int64), np.diff(m.row_ptr))
+    return m.dim, coo_from_keys((rows.astype(np.uint64) << np.uint64(32)) | m.col_idx.astype(np.uint64), m.values)
+
+
+def read_matrix(path, window_id: int = 0) -> TrafficMatrix:
+    """Parse a matrix file written by write_matrix (traffic.py:307-367): tokenised
+    and validated on the GPU; malformed files raise MatrixFileError naming the file
+    and line, exactly as the reference (they take the host parser)."""
+    data = open(path, "rb").read()
+    got = _lib.parse_matrix_text(data)
+    if got is None:
+        return _read_matrix_host(path, data.decode("utf-8", errors="replace"), window_id)
+    from .coo import DeviceCOO
+
+    dim, nnz, h = got
+    coo = DeviceCOO(h)
+    keys, counts = coo.download()
+    coo.close()
+    rows = (keys >> np.uint64(32)).astype(np.int64)
+    cols = (keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    row_ptr = np.zeros(dim + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=dim), out=row_ptr[1:])
+    return TrafficMatrix(window_id=window_id, dim=dim, row_ptr=row_ptr, col_idx=cols, values=counts)
