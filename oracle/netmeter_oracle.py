@@ -220,6 +220,24 @@ def ref_to_flat(row_ptr, col_idx, values, dim: int) -> dict:
     )
 
 
+def ref_read_matrix(path):
+    """traffic.py:307-367 restated for well-formed files, with the reference's own
+    per-line Python tokenising (the cost the CLI end-to-end clock is dominated
+    by): -> (dim, row_ptr, col_idx, values)."""
+    from pathlib import Path
+
+    lines = [parts for parts in (ln.split() for ln in Path(path).read_text().splitlines()) if parts]
+    dim, nnz = (int(t) for t in lines[0])
+    entries = np.empty((len(lines) - 1, 3), dtype=np.int64)
+    for k, parts in enumerate(lines[1:]):
+        entries[k] = [int(t) for t in parts]
+    assert len(entries) == nnz
+    rows, cols, values = entries[:, 0], entries[:, 1], entries[:, 2]
+    row_ptr = np.zeros(dim + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=dim), out=row_ptr[1:])
+    return dim, row_ptr, cols, values
+
+
 def _max0(a) -> int:
     """max_scan semantics (analytics.py:89-92): empty -> 0, INT64_MIN -> 0."""
     a = np.asarray(a, dtype=np.int64)
