@@ -384,12 +384,10 @@ constexpr int kLocMaxKeys = 2048;  // light keys per group (chunk S + one light 
 constexpr int kLocT1 = 3072;       // link table slots (load <= 2/3)
 constexpr int kLocT2 = 3072;       // source table slots
 
-// light position j of a group -> global index (the heavy range is skipped)
-__device__ __forceinline__ uint32_t light_index(const uint4& p, uint32_t j) {
-  const uint32_t len0 = (p.w > p.z ? p.z : p.y) - p.x;
-  return j < len0 ? p.x + j : p.w + (j - len0);
-}
-__device__ __forceinline__ uint32_t light_count(const uint4& p) { return (p.y - p.x) - (p.w - p.z); }
+// group plans are plain key ranges {klo, khi, -, -} (heavy buckets leave the
+// dense levels separately, nmx_seg.cuh)
+__device__ __forceinline__ uint32_t light_index(const uint4& p, uint32_t j) { return p.x + j; }
+__device__ __forceinline__ uint32_t light_count(const uint4& p) { return p.y - p.x; }
 
 constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 4 keys in registers per thread
 constexpr int kBmWords = 4096;                             // 65536 two-bit saturating counters
@@ -398,7 +396,11 @@ __device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
   const uint64_t h = x * 0x9E3779B97F4A7C15ull;
   return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
 }
-__device__ __forceinline__ uint32_t h16(uint64_t x) { return (uint32_t)((x * 0xD6E8FEB86659FD93ull) >> 48); }
+// 16-bit counter index of a 64-bit key: two 32-bit multiplies (a counter
+// collision only sends a key through the exact table)
+__device__ __forceinline__ uint32_t h16(uint64_t x) {
+  return ((uint32_t)x * 0x9E3779B1u + (uint32_t)(x >> 32) * 0x85EBCA6Bu) >> 16;
+}
 // 16-bit counter index of a 32-bit value (sources, destinations): one IMAD
 __device__ __forceinline__ uint32_t h16u(uint32_t x) { return (x * 0x9E3779B1u) >> 16; }
 // count one occurrence in a 2-bit saturating counter (01 = once, 11 = twice or more)
@@ -504,7 +506,8 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       }
     }
   }
-  unsigned long long a_valid = 0, a_links = 0, a_srcs = 0, a_mlink = 0, a_msrc = 0, a_mfan = 0;
+  // per-thread totals in 32 bits (a thread sees < 2^32 keys; per-group maxima <= 2048)
+  uint32_t a_valid = 0, a_links = 0, a_srcs = 0, a_mlink = 0, a_msrc = 0, a_mfan = 0;
   uint32_t it = 0;
   for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
     const uint32_t cur = it & 1;
@@ -678,20 +681,20 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         atomicAdd(&s.chist[(uint32_t)(key & dmask) >> cshift], 1u);  // the column partition's first level
         a_links += 1;
         a_valid += c;
-        a_mlink = max(a_mlink, (unsigned long long)c);
+        a_mlink = max(a_mlink, c);
       }
       if (st[r] & 4) {
         a_srcs += 1;
-        a_msrc = max(a_msrc, 1ull);
-        a_mfan = max(a_mfan, 1ull);
+        a_msrc = max(a_msrc, 1u);
+        a_mfan = max(a_mfan, 1u);
       } else if (st[r] & 8) {
         const uint32_t pf = s.t2pf[hs[r]];
         if (PARTIAL) {
           gsrc.add((uint32_t)(key >> b), ((unsigned long long)(pf >> 16) << 32) | (pf & 0xFFFFu));
         } else {
           a_srcs += 1;
-          a_msrc = max(a_msrc, (unsigned long long)(pf & 0xFFFFu));
-          a_mfan = max(a_mfan, (unsigned long long)(pf >> 16));
+          a_msrc = max(a_msrc, pf & 0xFFFFu);
+          a_mfan = max(a_mfan, pf >> 16);
         }
         s.t2key[hs[r]] = 0;
         s.t2pf[hs[r]] = 0;
@@ -704,8 +707,8 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         gsrc.add(0xFFFFFFFFu, ((unsigned long long)s.sp_src_fo << 32) | s.sp_src_pk);
       } else {
         a_srcs += 1;
-        a_msrc = max(a_msrc, (unsigned long long)s.sp_src_pk);
-        a_mfan = max(a_mfan, (unsigned long long)s.sp_src_fo);
+        a_msrc = max(a_msrc, s.sp_src_pk);
+        a_mfan = max(a_mfan, s.sp_src_fo);
       }
     }
     __syncthreads();
@@ -714,23 +717,24 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     for (int r = 0; r < kLocPerThread; ++r) kr[r] = kn[r];
     nmine = nnext;
   }
+  unsigned long long w_valid = a_valid, w_links = a_links, w_srcs = a_srcs;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    a_valid += __shfl_xor_sync(FULL, a_valid, o);
-    a_links += __shfl_xor_sync(FULL, a_links, o);
-    a_srcs += __shfl_xor_sync(FULL, a_srcs, o);
+    w_valid += __shfl_xor_sync(FULL, w_valid, o);
+    w_links += __shfl_xor_sync(FULL, w_links, o);
+    w_srcs += __shfl_xor_sync(FULL, w_srcs, o);
     a_mlink = max(a_mlink, __shfl_xor_sync(FULL, a_mlink, o));
     a_msrc = max(a_msrc, __shfl_xor_sync(FULL, a_msrc, o));
     a_mfan = max(a_mfan, __shfl_xor_sync(FULL, a_mfan, o));
   }
   if (lane == 0) {
-    if (a_links) atomicAdd(ccount, a_links);
-    if (a_valid) atomicAdd(stats + S_VALID, a_valid);
-    if (a_links) atomicAdd(stats + S_LINKS, a_links);
-    if (a_srcs) atomicAdd(stats + S_SRCS, a_srcs);
-    if (a_mlink) atomicMax(stats + S_MAXLINK, a_mlink);
-    if (a_msrc) atomicMax(stats + S_MAXSRCPK, a_msrc);
-    if (a_mfan) atomicMax(stats + S_MAXFANOUT, a_mfan);
+    if (w_links) atomicAdd(ccount, w_links);
+    if (w_valid) atomicAdd(stats + S_VALID, w_valid);
+    if (w_links) atomicAdd(stats + S_LINKS, w_links);
+    if (w_srcs) atomicAdd(stats + S_SRCS, w_srcs);
+    if (a_mlink) atomicMax(stats + S_MAXLINK, (unsigned long long)a_mlink);
+    if (a_msrc) atomicMax(stats + S_MAXSRCPK, (unsigned long long)a_msrc);
+    if (a_mfan) atomicMax(stats + S_MAXFANOUT, (unsigned long long)a_mfan);
   }
   __syncthreads();
   if (tid < (1 << kMsdLevelBits) && s.chist[tid]) atomicAdd(chist + tid, s.chist[tid]);
@@ -821,7 +825,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       }
     }
   }
-  unsigned long long a_cnt = 0, a_fanin = 0, a_pk = 0;
+  // per-thread totals in 32 bits (fan-in and packets of one destination < 2^32)
+  uint32_t a_cnt = 0, a_fanin = 0, a_pk = 0;
   uint32_t it = 0;
   for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
     const uint32_t cur = it & 1;
@@ -887,13 +892,13 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       if ((uint32_t)r >= nmine) continue;
       if (stc & (1u << r)) {
         a_cnt += 1;
-        a_fanin = max(a_fanin, 1ull);
-        a_pk = max(a_pk, (unsigned long long)vr[r]);
+        a_fanin = max(a_fanin, 1u);
+        a_pk = max(a_pk, vr[r]);
       } else if (stc & (16u << r)) {
         const unsigned long long v = s.ns[hh[r]];
         a_cnt += 1;
-        a_fanin = max(a_fanin, v >> 32);
-        a_pk = max(a_pk, v & 0xFFFFFFFFull);
+        a_fanin = max(a_fanin, (uint32_t)(v >> 32));
+        a_pk = max(a_pk, (uint32_t)v);
         s.key[hh[r]] = 0;
         s.ns[hh[r]] = 0;
       }
@@ -901,8 +906,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     }
     if (tid == 0 && s.sp) {
       a_cnt += 1;
-      a_fanin = max(a_fanin, s.sp >> 32);
-      a_pk = max(a_pk, s.sp & 0xFFFFFFFFull);
+      a_fanin = max(a_fanin, (uint32_t)(s.sp >> 32));
+      a_pk = max(a_pk, (uint32_t)s.sp);
     }
     __syncthreads();
     if (tid == 0) s.sp = 0;
@@ -913,16 +918,17 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     }
     nmine = nnext;
   }
+  unsigned long long w_cnt = a_cnt;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    a_cnt += __shfl_xor_sync(FULL, a_cnt, o);
+    w_cnt += __shfl_xor_sync(FULL, w_cnt, o);
     a_fanin = max(a_fanin, __shfl_xor_sync(FULL, a_fanin, o));
     a_pk = max(a_pk, __shfl_xor_sync(FULL, a_pk, o));
   }
   if (lane == 0) {
-    if (a_cnt) atomicAdd(stats + S_DSTS, a_cnt);
-    if (a_fanin) atomicMax(stats + S_MAXFANIN, a_fanin);
-    if (a_pk) atomicMax(stats + S_MAXDSTPK, a_pk);
+    if (w_cnt) atomicAdd(stats + S_DSTS, w_cnt);
+    if (a_fanin) atomicMax(stats + S_MAXFANIN, (unsigned long long)a_fanin);
+    if (a_pk) atomicMax(stats + S_MAXDSTPK, (unsigned long long)a_pk);
   }
 }
 
