@@ -392,9 +392,9 @@ __device__ __forceinline__ uint32_t light_count(const uint4& p) { return p.y - p
 constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 4 keys in registers per thread
 constexpr int kBmWords = 4096;                             // 65536 two-bit saturating counters
 
+// exact-table home slot in [0, n): 32-bit mix, then a multiply-high range reduction
 __device__ __forceinline__ uint32_t hslot(uint64_t x, uint32_t n) {
-  const uint64_t h = x * 0x9E3779B97F4A7C15ull;
-  return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
+  return __umulhi((uint32_t)x * 0x9E3779B1u ^ (uint32_t)(x >> 32) * 0xC2B2AE35u, n);
 }
 // 16-bit counter index of a 64-bit key: two 32-bit multiplies (a counter
 // collision only sends a key through the exact table)
