@@ -89,12 +89,13 @@ __device__ __forceinline__ void agg_count(uint32_t* cnt, int bin) {
     atomicAdd(&cnt[bin], 1u);
   }
 }
-// + a u64 value per item (final column level: packet sums per destination)
-__device__ __forceinline__ void agg_count_sum(uint32_t* cnt, unsigned long long* sum, int bin, uint32_t v) {
+// + a 32-bit value per item (final column level: packet sums per destination; the
+// sums stay below 2^32 since a call holds < 2^32 packets)
+__device__ __forceinline__ void agg_count_sum(uint32_t* cnt, uint32_t* sum, int bin, uint32_t v) {
   const int b0 = __shfl_sync(FULL, bin, 0);
   if (__all_sync(FULL, bin == b0)) {
     if (b0 < 0) return;
-    unsigned long long x = v;
+    uint32_t x = v;
 #pragma unroll
     for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
     if ((threadIdx.x & 31) == 0) {
@@ -103,7 +104,7 @@ __device__ __forceinline__ void agg_count_sum(uint32_t* cnt, unsigned long long*
     }
   } else if (bin >= 0) {
     atomicAdd(&cnt[bin], 1u);
-    atomicAdd(&sum[bin], (unsigned long long)v);
+    atomicAdd(&sum[bin], v);
   }
 }
 

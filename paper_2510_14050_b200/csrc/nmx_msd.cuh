@@ -786,8 +786,10 @@ constexpr int kLocCT = 3072;
 struct LocColSmem {
   uint32_t bm[kBmWords];          // destination hash counters
   uint32_t key[kLocCT];           // exact table for colliding destinations: dst + 1 (0 = empty)
-  unsigned long long ns[kLocCT];  // fan-in << 32 | packets
-  unsigned long long sp;          // dst == 0xFFFFFFFF
+  // fan-in and packets per destination: two native 32-bit shared atomics (a 64-bit
+  // shared atomicAdd is a CAS loop, which a hot destination turns into a retry storm)
+  uint32_t nfan[kLocCT], npk[kLocCT];
+  uint32_t spf, spp;  // dst == 0xFFFFFFFF
   uint4 plan[2];
 };
 
@@ -802,10 +804,11 @@ __global__ void __launch_bounds__(kLocThreads, 3)
   for (int i = tid; i < kBmWords; i += kLocThreads) s.bm[i] = 0;
   for (int i = tid; i < kLocCT; i += kLocThreads) {
     s.key[i] = 0;
-    s.ns[i] = 0;
+    s.nfan[i] = 0;
+    s.npk[i] = 0;
   }
   if (tid == 0) {
-    s.sp = 0;
+    s.spf = s.spp = 0;
     if (blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   }
   __syncthreads();
@@ -860,9 +863,9 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     for (int r = 0; r < kLocPerThread; ++r) {
       if ((uint32_t)r >= nmine) continue;
       const uint32_t d = kr[r];
-      const unsigned long long add = (1ull << 32) | vr[r];
       if (d == 0xFFFFFFFFu) {
-        atomicAdd(&s.sp, add);
+        atomicAdd(&s.spf, 1u);
+        atomicAdd(&s.spp, vr[r]);
       } else if (bm_once(s.bm, h16u(d))) {
         stc |= 1u << r;
       } else {
@@ -878,7 +881,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
             }
           }
           if (c0 == dk) {
-            atomicAdd(&s.ns[h], add);
+            atomicAdd(&s.nfan[h], 1u);
+            atomicAdd(&s.npk[h], vr[r]);
             break;
           }
           h = h + 1 == kLocCT ? 0 : h + 1;
@@ -895,22 +899,22 @@ __global__ void __launch_bounds__(kLocThreads, 3)
         a_fanin = max(a_fanin, 1u);
         a_pk = max(a_pk, vr[r]);
       } else if (stc & (16u << r)) {
-        const unsigned long long v = s.ns[hh[r]];
         a_cnt += 1;
-        a_fanin = max(a_fanin, (uint32_t)(v >> 32));
-        a_pk = max(a_pk, (uint32_t)v);
+        a_fanin = max(a_fanin, s.nfan[hh[r]]);
+        a_pk = max(a_pk, s.npk[hh[r]]);
         s.key[hh[r]] = 0;
-        s.ns[hh[r]] = 0;
+        s.nfan[hh[r]] = 0;
+        s.npk[hh[r]] = 0;
       }
       s.bm[h16u(kr[r]) >> 4] = 0;
     }
-    if (tid == 0 && s.sp) {
+    if (tid == 0 && s.spf) {
       a_cnt += 1;
-      a_fanin = max(a_fanin, (uint32_t)(s.sp >> 32));
-      a_pk = max(a_pk, (uint32_t)s.sp);
+      a_fanin = max(a_fanin, s.spf);
+      a_pk = max(a_pk, s.spp);
     }
     __syncthreads();
-    if (tid == 0) s.sp = 0;
+    if (tid == 0) s.spf = s.spp = 0;
 #pragma unroll
     for (int r = 0; r < kLocPerThread; ++r) {
       kr[r] = kn[r];

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kMsdThreads) seg_count_kernel(const KeyT* __re
   constexpr bool SUM = FINAL && HAS_VAL;
   constexpr bool REP = FINAL && !HAS_VAL;
   __shared__ uint32_t cnt[kSegBins];
-  __shared__ unsigned long long sum[SUM ? kSegBins : 1];
+  __shared__ uint32_t sum[SUM ? kSegBins : 1];  // < 2^32 packets per call: 32-bit shared atomics
   __shared__ KeyT srep[REP ? kSegBins : 1];
   __shared__ uint32_t s_p0, s_bound[kSegMaxRel];
   const int tid = threadIdx.x;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kMsdThreads) seg_count_kernel(const KeyT* __re
     if (!cb) continue;
     const uint32_t c = ((p0 + (uint32_t)(bin >> dbits)) << dbits) | ((uint32_t)bin & dmask);
     atomicAdd(ccnt + c, cb);
-    if (SUM) atomicAdd(csum + c, sum[bin]);
+    if (SUM) atomicAdd(csum + c, (unsigned long long)sum[bin]);
     if (REP) rep[c] = srep[bin];
   }
 }
