@@ -1003,12 +1003,15 @@ uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint6
   return m;
 }
 
+// Row half of the MSD path: partition the packed keys by source bits, group them
+// in shared memory (links + rows into c->stats), heavy buckets through the
+// segmented levels. Returns the column entries ((dst, count) slots, holes = count
+// 0) as a ColConcatSrc; *chist_out = their first-level histogram + count.
 // pre_m > 0: keysA already holds the level-1 partition of pre_m valid keys
-// (streamed windows); n bounds the buffers.
-void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
-                      int b, int D, uint64_t pre_m = 0) {
+// (streamed windows); n bounds the buffers. Empty (n1 = n2 = 0) if no valid packet.
+ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                      int b, int D, uint64_t pre_m, uint32_t** chist_out) {
   const int kb = 2 * b;
-  stage_begin(c, 1);
   // every buffer the step needs is sized up front (n bounds m, u and the heavy parts)
   c->keysA.grow(n * 8);
   c->keysB.grow(n * 8);
@@ -1019,8 +1022,12 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   c->cvA.grow(n * 4);
   c->ckB.grow(n * 4);
   c->cvB.grow(n * 4);
+  c->mch.grow((kMsdMaxBins + 4) * 4);
+  uint32_t* chist = c->mch.as<uint32_t>();
+  *chist_out = chist;
+  auto* ccount = reinterpret_cast<unsigned long long*>(chist + kMsdMaxBins);
+  CK(cudaMemsetAsync(chist, 0, (kMsdMaxBins + 4) * 4, c->st));
 
-  // ---- rows: MSD partition of the packed keys by source bits ----
   PacketSrc ps{d_src, d_dst, d_valid, n, 0, b};
   ps.quad = !(((uintptr_t)d_src | (uintptr_t)d_dst) & 15) && !((uintptr_t)d_valid & 3);
   c->mark();  // 1: row partition start
@@ -1033,18 +1040,13 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
                                                                nullptr, &sp, pre_m);
   c->last_sort_launches = c->msd_levels;
   c->mark();  // 2: row partition end
-  if (!m) {
-    stage_finish(c, 1);
-    return;
-  }
+  ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), 0, c->ckA.as<uint32_t>(),
+                  c->cvA.as<uint32_t>(),      0,                          0};
+  cs.quad = true;  // context buffers are cudaMalloc-aligned
+  if (!m) return cs;
   const uint32_t nb = 1u << D;
   const int Dc = std::min(D, b);
   const int cshift = b - msd_first_bits(Dc);
-  // the column partition's first-level histogram + entry count, produced by the row stages
-  c->mch.grow((kMsdMaxBins + 4) * 4);
-  uint32_t* chist = c->mch.as<uint32_t>();
-  auto* ccount = reinterpret_cast<unsigned long long*>(chist + kMsdMaxBins);
-  CK(cudaMemsetAsync(chist, 0, (kMsdMaxBins + 4) * 4, c->st));
   if (sp.t.light) {
     const uint32_t ngroups = seg_plan_groups(c, nb, sp.t.light);
     set_smem(local_rows_kernel<false>, sizeof(LocSmem));
@@ -1063,13 +1065,19 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     uh = heavy_rows(c, sp.t.big, sp.t.nbig, b, D, cshift, chist, ccount);
   }
   c->mark();  // 4: heavy rows end
+  cs.n1 = sp.t.light;
+  cs.n2 = uh;
+  cs.n = sp.t.light + uh;
+  return cs;
+}
 
+void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                      int b, int D, uint64_t pre_m = 0) {
+  stage_begin(c, 1);
+  uint32_t* chist = nullptr;
+  const ColConcatSrc cs = msd_rows(c, d_src, d_dst, d_valid, n, b, D, pre_m, &chist);
   // ---- columns: MSD partition of the (dst, count) entries by destination bits ----
-  ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), sp.t.light,
-                  c->ckA.as<uint32_t>(),      c->cvA.as<uint32_t>(),      uh,
-                  sp.t.light + uh};
-  cs.quad = true;  // context buffers are cudaMalloc-aligned
-  msd_columns(c, cs, b, Dc, chist);
+  if (cs.n) msd_columns(c, cs, b, std::min(D, b), chist);
   stage_finish(c, 1);
 }
 
@@ -1837,11 +1845,20 @@ int nmx_shard_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, uin
     std::fill(counts, counts + nparts, 0);
     if (!n) return NMX_OK;
     stage_begin(c, 1);
-    PacketSrc ps{d_src, d_dst, nullptr, n, 0, b};
-    const RowsOut r = stage_rows(c, ps, b, 0);
-    if (r.u) {
-      ColPart it{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), d_out_dst, d_out_count};
-      partition_items(c, it, r.u, nparts, counts);
+    if (const int D = msd_bits(n, b)) {  // MSD rows; column slots (holes skipped) by owner(dst)
+      uint32_t* chist = nullptr;
+      const ColConcatSrc cs = msd_rows(c, d_src, d_dst, nullptr, n, b, D, 0, &chist);
+      if (cs.n) {
+        ColConcatPart it{cs, d_out_dst, d_out_count};
+        partition_items(c, it, cs.n, nparts, counts);
+      }
+    } else {
+      PacketSrc ps{d_src, d_dst, nullptr, n, 0, b};
+      const RowsOut r = stage_rows(c, ps, b, 0);
+      if (r.u) {
+        ColPart it{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), d_out_dst, d_out_count};
+        partition_items(c, it, r.u, nparts, counts);
+      }
     }
     stage_finish(c, 1);
     copy_out9(c->h_stats, out, 1);
@@ -1863,6 +1880,16 @@ int nmx_shard_cols(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, u
     c->ckB.grow(u * 4);
     c->cvA.grow(u * 4);
     c->cvB.grow(u * 4);
+    if (const int Dc = msd_bits(u, b)) {  // MSD column partition + shared-memory groups
+      CK(cudaMemcpyAsync(c->ckA.p, d_dst, u * 4, cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(c->cvA.p, d_count, u * 4, cudaMemcpyDeviceToDevice, c->st));
+      ColConcatSrc cs{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u, nullptr, nullptr, 0, u};
+      cs.quad = true;
+      msd_columns(c, cs, b, Dc, nullptr);
+      stage_finish(c, 1);
+      copy_out9(c->h_stats, out, 1);
+      return NMX_OK;
+    }
     if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
       CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
     CK(cudaMemcpyAsync(c->ckA.p, d_dst, u * 4, cudaMemcpyDeviceToDevice, c->st));

@@ -1035,4 +1035,21 @@ __global__ void coo_col_entries_kernel(const uint64_t* __restrict__ keys, const 
   }
 }
 
+// owner partition (multi-GPU exchange 2) of column slots, holes skipped
+struct ColConcatPart {
+  ColConcatSrc s;
+  uint32_t* out_ck;
+  uint32_t* out_cv;
+  __device__ __forceinline__ bool key(uint64_t i, uint32_t& k) const {
+    uint32_t v;
+    return s.load(i, k, v);
+  }
+  __device__ __forceinline__ void store(uint64_t i, uint64_t pos) const {
+    uint32_t k, v;
+    s.load(i, k, v);
+    out_ck[pos] = k;
+    out_cv[pos] = v;
+  }
+};
+
 }  // namespace nmx

@@ -75,6 +75,17 @@ def test_simulated_ranks_match_oracle(ops, G, kind):
         assert _simulate(ops, s, d, valid, space, G) == orc.stats9_packed(s, d, valid), (G, kind, lg)
 
 
+@pytest.mark.parametrize("G", [1, 2, 3])
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
+def test_simulated_ranks_msd_sizes(ops, G, kind):
+    # >= 2^20 packets per rank: the shard stages take the MSD path (rows with
+    # heavy buckets, column slots with holes partitioned by owner(dst))
+    gen = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
+    s, d = gen(23, 0, (1 << 22) + 7, 1 << 32)
+    valid = np.random.default_rng(3).random(len(s)) >= 0.1
+    assert _simulate(ops, s, d, valid, 1 << 32, G) == orc.stats9_packed(s, d, valid), (G, kind)
+
+
 def test_nccl_world_of_one():
     import torch
     import torch.distributed as dist
