@@ -674,7 +674,8 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     const uint32_t nbl = 1u << cum[l];
     uint32_t* h2 = c->mhist2.as<uint32_t>();
     CK(cudaMemsetAsync(h2, 0, (size_t)nbl * 4, c->st));
-    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(in_k, m, shift, dl[l], bshift,
+    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile * kCount2Tiles), kMsdThreads, 0, c->st>>>(in_k, m, shift,
+                                                                                                      dl[l], bshift,
                                                                                          h2);
     CK_LAUNCH();
     KeySrc<KeyT, HAS_VAL> ks{in_k, in_v, m};

@@ -26,6 +26,7 @@ constexpr int kMsdTile = kMsdThreads * kMsdIPT;  // 2048 keys per scatter tile
 constexpr int kMsdMaxBins = 2048;                // histogram bins of the first level (<= 2^11)
 constexpr int kMsdLevelBits = 7;                 // digit bits per partition level
 constexpr int kMsdScBins = 2 << kMsdLevelBits;   // scatter bins: a tile spans <= 2 parent buckets
+constexpr int kCount2Tiles = 4;                  // tiles per CTA of the next-level counting pass
 
 // block exclusive scan of NB counters held in smem (512 threads, NB % 512 == 0 or NB <= 512)
 template <int NB>
@@ -254,34 +255,40 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
 template <typename KeyT>
 __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __restrict__ keys, uint64_t m, int shift,
                                                                   int dbits, int bshift, uint32_t* __restrict__ hist2) {
+  // kCount2Tiles consecutive tiles per CTA share one shared histogram, so the
+  // global flush costs one atomic per bin per 8192 keys instead of per 2048
   __shared__ uint32_t cnt[kMsdScBins];
   __shared__ uint64_t s_b1first;
   const int tid = threadIdx.x;
   for (int i = tid; i < kMsdScBins; i += kMsdThreads) cnt[i] = 0;
-  const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
-  KeyT k[kMsdIPT];
-#pragma unroll
-  for (int i = 0; i < kMsdIPT; ++i) {
-    const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
-    k[i] = idx < m ? keys[idx] : KeyT(0);
-  }
-  if (tid == 0) s_b1first = (uint64_t)keys[base] >> bshift;
+  const uint64_t base0 = (uint64_t)blockIdx.x * kMsdTile * kCount2Tiles;
+  if (tid == 0) s_b1first = (uint64_t)keys[base0] >> bshift;
   __syncthreads();
   const uint32_t dmask = (1u << dbits) - 1;
   const uint64_t b1first = s_b1first;
+  for (int t = 0; t < kCount2Tiles; ++t) {
+    const uint64_t base = base0 + (uint64_t)t * kMsdTile;
+    if (base >= m) break;
+    KeyT k[kMsdIPT];
 #pragma unroll
-  for (int i = 0; i < kMsdIPT; ++i) {
-    const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
-    int bin = -1;
-    if (idx < m) {
-      const uint64_t key = (uint64_t)k[i];
-      const uint64_t rel = (key >> bshift) - b1first;
-      if (rel < 2)
-        bin = (int)((rel << dbits) | ((key >> shift) & dmask));
-      else
-        atomicAdd(hist2 + (uint32_t)(key >> shift), 1u);
+    for (int i = 0; i < kMsdIPT; ++i) {
+      const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
+      k[i] = idx < m ? keys[idx] : KeyT(0);
     }
-    agg_count(cnt, bin);
+#pragma unroll
+    for (int i = 0; i < kMsdIPT; ++i) {
+      const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
+      int bin = -1;
+      if (idx < m) {
+        const uint64_t key = (uint64_t)k[i];
+        const uint64_t rel = (key >> bshift) - b1first;
+        if (rel < 2)
+          bin = (int)((rel << dbits) | ((key >> shift) & dmask));
+        else
+          atomicAdd(hist2 + (uint32_t)(key >> shift), 1u);
+      }
+      agg_count(cnt, bin);
+    }
   }
   __syncthreads();
   const int nbins = 2 << dbits;
