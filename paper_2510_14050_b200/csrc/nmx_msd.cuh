@@ -100,7 +100,7 @@ struct MsdSmem {
 // large for a shared-memory group leave the dense levels already compacted.
 constexpr uint32_t kLightBit = 0x80000000u;
 template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false>
-__global__ void __launch_bounds__(kMsdThreads) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
+__global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
                                                                    uint32_t* __restrict__ vout, int shift, int dbits,
                                                                    int bshift, uint32_t* __restrict__ cursor,
                                                                    KeyT* __restrict__ hout = nullptr,
