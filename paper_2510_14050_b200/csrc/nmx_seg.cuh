@@ -270,7 +270,7 @@ struct SegSmem {
 // msd_scatter_kernel; the bin of every staged item is kept (it cannot be
 // recomputed from the key: parents are positional).
 template <typename KeyT, bool HAS_VAL>
-__global__ void __launch_bounds__(kMsdThreads) seg_scatter_kernel(const KeyT* __restrict__ keys,
+__global__ void __launch_bounds__(kMsdThreads, 5) seg_scatter_kernel(const KeyT* __restrict__ keys,
                                                                  const uint32_t* __restrict__ vals, uint32_t m,
                                                                  const uint32_t* __restrict__ poff, uint32_t P,
                                                                  int shift, int dbits, uint32_t* __restrict__ cursor,
