@@ -761,11 +761,35 @@ uint32_t seg_plan_groups(nmx_ctx* c, uint32_t C, uint32_t light) {
 // their number.
 uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int cshift, uint32_t* chist,
                     unsigned long long* ccount) {
-  int w[16];
-  int L = split_levels(b - D, w);
-  const int Ls = L;
-  L += split_levels(b, w + L);
-  const int kb = 2 * b;
+  // Key fields per level (shift, width): one level of the remaining source bits
+  // (children stay whole sources: NORMAL groups), then the destination bits
+  // (parents mostly one heavy source: PARTIAL groups + SrcTable), then the last
+  // source bits in the count-only final level, where every child is one key.
+  // Heavy parents are dominated by one source, so the low source bits carry
+  // almost no entropy and would only re-copy the bucket if split first.
+  int w[16], sh[16];
+  bool part[16];
+  int L = 0;
+  const int r = b - D;                          // source bits below the dense prefix
+  const int r0 = r > 0 ? std::min(r, (r + 1) / 2 > kMsdLevelBits ? kMsdLevelBits : (r + 1) / 2) : 0;
+  if (r0) w[L] = r0, sh[L] = 2 * b - D - r0, part[L] = false, ++L;
+  {
+    int dw[8];
+    const int Ld = split_levels(b, dw);
+    for (int i = 0, at = b; i < Ld; ++i) {
+      at -= dw[i];
+      w[L] = dw[i], sh[L] = at, part[L] = true, ++L;
+    }
+  }
+  const int rlow = r - r0;                      // low source bits, last (the final level is count-only)
+  {
+    int lw[8];
+    const int Ll = split_levels(rlow, lw);
+    for (int i = 0, at = b + rlow; i < Ll; ++i) {
+      at -= lw[i];
+      w[L] = lw[i], sh[L] = at, part[L] = true, ++L;
+    }
+  }
   c->lightK.grow(mh * 8);
   uint32_t* poff = c->spoffA.as<uint32_t>();
   uint64_t* in = c->keysC.as<uint64_t>();
@@ -774,7 +798,6 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
   uint32_t* hcol_cnt = c->cvA.as<uint32_t>();
   uint32_t P = nheavy, m = (uint32_t)mh;
   uint64_t lbase = 0;
-  int consumed = D;
   SrcTable gsrc;
   bool table = false;
   set_smem(seg_scatter_kernel<uint64_t, false>, sizeof(SegSmem<uint64_t, false>));
@@ -782,10 +805,11 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
   set_smem(local_rows_kernel<true>, sizeof(LocSmem));
   for (int l = 0; l < L && m; ++l) {
     const int dbits = w[l];
-    const bool partial = l >= Ls;  // parents are single sources
-    if (partial && !table) {       // roots = the parents of the first destination level
+    const bool partial = part[l];  // sources may be split over several children
+    if (partial && !table) {       // at most 2^rlow sources per parent of the first destination level
+      const uint64_t bound = std::min<uint64_t>(m, (uint64_t)P << rlow);
       uint32_t cap = 1024;
-      while (cap < 2 * P + 16) cap <<= 1;
+      while (cap < 2 * bound + 16) cap <<= 1;
       c->gsk.grow(((size_t)cap + 2) * 4);
       c->gsv.grow(((size_t)cap + 2) * 8);
       CK(cudaMemsetAsync(c->gsk.p, 0, ((size_t)cap + 2) * 4, c->st));
@@ -795,8 +819,7 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
       gsrc.mask = cap - 1;
       table = true;
     }
-    consumed += dbits;
-    const int shift = kb - consumed;
+    const int shift = sh[l];
     const uint32_t C = P << dbits;
     if (l + 1 == L) {  // final level: count only, one link per child
       c->sccnt.grow(((size_t)C + 8) * 4);
