@@ -738,8 +738,7 @@ SegTotals seg_level_plan(nmx_ctx* c, const KeyT* k, const uint32_t* v, uint32_t 
 }
 
 // shared-memory groups over this level's light children (loff = sloff, C children)
-uint32_t seg_plan_groups(nmx_ctx* c, uint32_t C, uint32_t light) {
-  const uint32_t S = kSegCap;
+uint32_t seg_plan_groups(nmx_ctx* c, uint32_t C, uint32_t light, uint32_t S) {
   const uint32_t ngroups = (light + S - 1) / S;
   c->mgb.grow(((size_t)ngroups + 2) * 4);
   c->mplan.grow(((size_t)ngroups + 2) * 16);
@@ -859,7 +858,7 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
     CK_LAUNCH();
     ++c->launches;
     if (t.light) {
-      const uint32_t ngroups = seg_plan_groups(c, C, t.light);
+      const uint32_t ngroups = seg_plan_groups(c, C, t.light, kLocChunk);
       const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 2);
       if (partial)
         local_rows_kernel<true><<<grid, kLocThreads, sizeof(LocSmem), c->st>>>(
@@ -940,7 +939,7 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
     CK_LAUNCH();
     ++c->launches;
     if (t.light) {
-      const uint32_t ngroups = seg_plan_groups(c, C, t.light);
+      const uint32_t ngroups = seg_plan_groups(c, C, t.light, kLocColChunk);
       const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3);
       local_cols_kernel<<<grid, kLocThreads, sizeof(LocColSmem), c->st>>>(
           c->lightCK.as<uint32_t>() + lbase, c->lightCV.as<uint32_t>() + lbase, c->mplan.as<uint4>(), ngroups,
@@ -978,7 +977,7 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   c->mark();  // column partition end
   if (!u) return;
   if (sp.t.light) {
-    const uint32_t ngroups = seg_plan_groups(c, 1u << Dc, sp.t.light);
+    const uint32_t ngroups = seg_plan_groups(c, 1u << Dc, sp.t.light, kLocColChunk);
     set_smem(local_cols_kernel, sizeof(LocColSmem));
     local_cols_kernel<<<(unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3), kLocThreads,
                         sizeof(LocColSmem), c->st>>>(ck, cv, c->mplan.as<uint4>(), ngroups,
@@ -1072,7 +1071,7 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   const int Dc = std::min(D, b);
   const int cshift = b - msd_first_bits(Dc);
   if (sp.t.light) {
-    const uint32_t ngroups = seg_plan_groups(c, nb, sp.t.light);
+    const uint32_t ngroups = seg_plan_groups(c, nb, sp.t.light, kLocChunk);
     set_smem(local_rows_kernel<false>, sizeof(LocSmem));
     local_rows_kernel<false><<<(unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 2), kLocThreads,
                                sizeof(LocSmem), c->st>>>(keys, c->mplan.as<uint4>(), ngroups, b,

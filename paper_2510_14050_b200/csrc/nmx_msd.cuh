@@ -387,16 +387,21 @@ __global__ void group_bounds_kernel(const uint32_t* __restrict__ off, uint32_t n
 // LOC: per group of buckets, shared-memory hash grouping
 // ---------------------------------------------------------------------------
 constexpr int kLocThreads = 512;
-constexpr int kLocMaxKeys = 2048;  // light keys per group (chunk S + one light bucket)
-constexpr int kLocT1 = 3072;       // link table slots (load <= 2/3)
-constexpr int kLocT2 = 3072;       // source table slots
+constexpr int kLocChunk = 1536;    // row groups: the light buckets whose start lies in one chunk
+constexpr int kLocMaxKeys = 2560;  // light keys per row group (chunk + one light bucket of <= 1024)
+constexpr int kLocColChunk = 1024; // column groups (fewer registers per item: 4 per thread)
+constexpr int kLocColMaxKeys = 2048;
+constexpr int kLocT1 = 3840;       // link table slots (load <= 2/3)
+constexpr int kLocT2 = 3840;       // source table slots
 
 // group plans are plain key ranges {klo, khi, -, -} (heavy buckets leave the
 // dense levels separately, nmx_seg.cuh)
 __device__ __forceinline__ uint32_t light_index(const uint4& p, uint32_t j) { return p.x + j; }
 __device__ __forceinline__ uint32_t light_count(const uint4& p) { return p.y - p.x; }
 
-constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 4 keys in registers per thread
+constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 5 keys in registers per thread
+constexpr int kLocColPerThread = kLocColMaxKeys / kLocThreads;  // 4
+static_assert(kLocColPerThread <= 8, "local_cols packs per-slot flags into 8-bit fields");
 constexpr int kBmWords = 4096;                             // 65536 two-bit saturating counters
 
 // exact-table home slot in [0, n): 32-bit mix, then a multiply-high range reduction
@@ -819,13 +824,13 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     if (blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   }
   __syncthreads();
-  uint32_t kr[kLocPerThread], vr[kLocPerThread];
+  uint32_t kr[kLocColPerThread], vr[kLocColPerThread];
   uint32_t nmine = 0;
   if (blockIdx.x < ngroups) {
     const uint4 p = s.plan[0];
     const uint32_t nlight = light_count(p);
 #pragma unroll
-    for (int r = 0; r < kLocPerThread; ++r) {
+    for (int r = 0; r < kLocColPerThread; ++r) {
       const uint32_t j = tid + r * kLocThreads;
       if (j < nlight) {
         const uint32_t i = light_index(p, j);
@@ -844,17 +849,17 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     uint4 pnext = make_uint4(0, 0, 0, 0);
     if (tid == 0 && gn < ngroups) pnext = plan[gn];
 #pragma unroll
-    for (int r = 0; r < kLocPerThread; ++r)
+    for (int r = 0; r < kLocColPerThread; ++r)
       if ((uint32_t)r < nmine) bm_hit(s.bm, h16u(kr[r]));  // one IMAD: recomputed below, not kept
     if (tid == 0) s.plan[cur ^ 1] = pnext;
     __syncthreads();
     const uint4 pn = s.plan[cur ^ 1];
-    uint32_t kn[kLocPerThread], vn[kLocPerThread];
+    uint32_t kn[kLocColPerThread], vn[kLocColPerThread];
     uint32_t nnext = 0;
     if (gn < ngroups) {
       const uint32_t nl2 = light_count(pn);
 #pragma unroll
-      for (int r = 0; r < kLocPerThread; ++r) {
+      for (int r = 0; r < kLocColPerThread; ++r) {
         const uint32_t j = tid + r * kLocThreads;
         if (j < nl2) {
           const uint32_t i = light_index(pn, j);
@@ -864,10 +869,10 @@ __global__ void __launch_bounds__(kLocThreads, 3)
         }
       }
     }
-    uint32_t hh[kLocPerThread];
-    uint32_t stc = 0;  // bit r: fast, bit r+4: table creator
+    uint32_t hh[kLocColPerThread];
+    uint32_t stc = 0;  // bit r: fast, bit r+8: table creator
 #pragma unroll
-    for (int r = 0; r < kLocPerThread; ++r) {
+    for (int r = 0; r < kLocColPerThread; ++r) {
       if ((uint32_t)r >= nmine) continue;
       const uint32_t d = kr[r];
       if (d == 0xFFFFFFFFu) {
@@ -883,7 +888,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
           if (c0 == 0) {
             c0 = atomicCAS(&s.key[h], 0u, dk);
             if (c0 == 0) {
-              stc |= 16u << r;
+              stc |= 256u << r;
               c0 = dk;
             }
           }
@@ -899,13 +904,13 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kLocPerThread; ++r) {
+    for (int r = 0; r < kLocColPerThread; ++r) {
       if ((uint32_t)r >= nmine) continue;
       if (stc & (1u << r)) {
         a_cnt += 1;
         a_fanin = max(a_fanin, 1u);
         a_pk = max(a_pk, vr[r]);
-      } else if (stc & (16u << r)) {
+      } else if (stc & (256u << r)) {
         a_cnt += 1;
         a_fanin = max(a_fanin, s.nfan[hh[r]]);
         a_pk = max(a_pk, s.npk[hh[r]]);
@@ -923,7 +928,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     __syncthreads();
     if (tid == 0) s.spf = s.spp = 0;
 #pragma unroll
-    for (int r = 0; r < kLocPerThread; ++r) {
+    for (int r = 0; r < kLocColPerThread; ++r) {
       kr[r] = kn[r];
       vr[r] = vn[r];
     }
