@@ -565,8 +565,25 @@ void scan_counts(nmx_ctx* c, const uint32_t* cnt, uint32_t n, uint32_t* off, uin
 }
 
 int msd_first_bits(int D) {
-  const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
+  const int L = (D + kMsdMaxLevelBits - 1) / kMsdMaxLevelBits;
   return D / L + (0 < D % L ? 1 : 0);
+}
+
+// dense scatter launch with the bin capacity of this level's digit width
+template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false>
+void launch_msd_scatter(nmx_ctx* c, int dbits, uint64_t tiles, const Src& src, uint64_t n, KeyT* out, uint32_t* vout,
+                        int shift, int bshift, uint32_t* cursor, KeyT* hout = nullptr, uint32_t* hvout = nullptr) {
+  if (dbits > kMsdLevelBits) {
+    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdMaxLevelBits>;
+    constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdMaxLevelBits)>);
+    set_smem(k, sm);
+    k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout);
+  } else {
+    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdLevelBits>;
+    constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdLevelBits)>);
+    set_smem(k, sm);
+    k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout);
+  }
 }
 
 struct SegTotals {
@@ -599,11 +616,12 @@ SegTotals seg_classify(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* n
   return t;
 }
 
-// level widths of a D-bit dense partition: levels of <= kMsdLevelBits bits (128
-// bins per tile keeps the reservation atomics at one per 32 keys and every
-// digit's run in a tile ~32 keys long); returns the number of levels
+// level widths of a D-bit dense partition: the fewest levels of <= 8 bits, split
+// evenly (7-bit levels keep a digit's run in a 2048-key tile ~16 keys long; an
+// 8-bit level is only used where it saves a whole level: D = 15, 16, 22-24);
+// returns the number of levels
 int msd_level_bits(int D, int* dl, int* cum) {
-  const int L = (D + kMsdLevelBits - 1) / kMsdLevelBits;
+  const int L = (D + kMsdMaxLevelBits - 1) / kMsdMaxLevelBits;
   for (int l = 0, acc = 0; l < L; ++l) {
     dl[l] = D / L + (l < D % L ? 1 : 0);
     acc += dl[l];
@@ -634,7 +652,6 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   c->mhist2.grow(((size_t)nb + 8) * 4);
   uint32_t* cur = c->mcur.as<uint32_t>();
   uint32_t* off = c->moff.as<uint32_t>();
-  using S1 = MsdSmem<KeyT, HAS_VAL>;
   constexpr uint64_t kItem = sizeof(KeyT) + (HAS_VAL ? 4 : 0);  // 8 B per item in and out
   unsigned long long m = pre_m;
   *res_k = outA;
@@ -657,10 +674,9 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     CK(cudaStreamSynchronize(c->st));
     c->launches += 2;
     if (!m) return 0;
-    set_smem(msd_scatter_kernel<Src, KeyT, HAS_VAL, 1>, sizeof(S1));
     c->dom_begin("msd_scatter");
-    msd_scatter_kernel<Src, KeyT, HAS_VAL, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
-        src, n, outA, voutA, kb - dl[0], dl[0], 0, cur);
+    launch_msd_scatter<Src, KeyT, HAS_VAL, 1>(c, dl[0], tiles_of(n, kMsdTile), src, n, outA, voutA, kb - dl[0], 0,
+                                              cur);
     CK_LAUNCH();
     c->dom_end(2 * kItem * m);
     ++c->launches;
@@ -685,19 +701,15 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
       if (getenv("NMX_DEBUG"))
         fprintf(stderr, "dense split m=%llu C=%u light=%u big=%u nbig=%u\n", (unsigned long long)m, nbl,
                 split->t.light, split->t.big, split->t.nbig);
-      set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>, sizeof(S1));
       c->dom_begin("msd_scatter");
-      msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>
-          <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(
-              ks, m, out_k, out_v, shift, dl[l], bshift, c->scur.as<uint32_t>(), reinterpret_cast<KeyT*>(split->hk),
-              split->hv);
+      launch_msd_scatter<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>(
+          c, dl[l], tiles_of(m, kMsdTile), ks, m, out_k, out_v, shift, bshift, c->scur.as<uint32_t>(),
+          reinterpret_cast<KeyT*>(split->hk), split->hv);
     } else {
       scan_counts(c, h2, nbl, off, cur);
-      set_smem(msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>, sizeof(S1));
       c->dom_begin("msd_scatter");
-      msd_scatter_kernel<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>
-          <<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, sizeof(S1), c->st>>>(ks, m, out_k, out_v, shift, dl[l],
-                                                                                 bshift, cur);
+      launch_msd_scatter<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>(c, dl[l], tiles_of(m, kMsdTile), ks, m, out_k, out_v,
+                                                                  shift, bshift, cur);
     }
     CK_LAUNCH();
     c->dom_end(2 * kItem * m);
@@ -1016,11 +1028,8 @@ uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint6
   CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   if (m) {
-    using S1 = MsdSmem<uint64_t, false>;
-    set_smem(msd_scatter_kernel<PacketSrc, uint64_t, false, 1>, sizeof(S1));
-    msd_scatter_kernel<PacketSrc, uint64_t, false, 1><<<(unsigned)tiles_of(n, kMsdTile), kMsdThreads, sizeof(S1),
-                                                        c->st>>>(ps, n, out, nullptr, kb - dl[0], dl[0], 0,
-                                                                 c->mcur.as<uint32_t>());
+    launch_msd_scatter<PacketSrc, uint64_t, false, 1>(c, dl[0], tiles_of(n, kMsdTile), ps, n, out, nullptr,
+                                                      kb - dl[0], 0, c->mcur.as<uint32_t>());
     CK_LAUNCH();
   }
   return m;

@@ -24,8 +24,9 @@ constexpr int kMsdThreads = 256;
 constexpr int kMsdIPT = 8;
 constexpr int kMsdTile = kMsdThreads * kMsdIPT;  // 2048 keys per scatter tile
 constexpr int kMsdMaxBins = 2048;                // histogram bins of the first level (<= 2^11)
-constexpr int kMsdLevelBits = 7;                 // digit bits per partition level
-constexpr int kMsdScBins = 2 << kMsdLevelBits;   // scatter bins: a tile spans <= 2 parent buckets
+constexpr int kMsdLevelBits = 7;                 // digit bits per segmented (heavy) level
+constexpr int kMsdMaxLevelBits = 8;              // dense levels: <= 8 bits (3 levels up to D = 24)
+constexpr int kMsdScBins = 2 << kMsdMaxLevelBits;  // scatter bins: a tile spans <= 2 parent buckets
 constexpr int kCount2Tiles = 4;                  // tiles per CTA of the next-level counting pass
 
 // block exclusive scan of NB counters held in smem (512 threads, NB % 512 == 0 or NB <= 512)
@@ -84,13 +85,13 @@ __device__ __forceinline__ void load_items(const Src& s, uint64_t q0, uint64_t q
 // the D-bit bucket id; a tile lies in one or two level-1 buckets, keys of further
 // buckets take a per-key global atomic). KeyT u64 = packed row keys; KeyT u32
 // with a u32 payload = column entries (dst, count).
-template <typename KeyT, bool HAS_VAL>
+template <typename KeyT, bool HAS_VAL, int NB = (2 << kMsdLevelBits)>
 struct MsdSmem {
   KeyT stage[kMsdTile];
   uint32_t vstage[HAS_VAL ? kMsdTile : 1];
-  uint32_t cnt[kMsdScBins];
-  uint32_t tstart[kMsdScBins];
-  uint32_t gbase[kMsdScBins];
+  uint32_t cnt[NB];
+  uint32_t tstart[NB];
+  uint32_t gbase[NB];
   uint32_t wt[kMsdThreads / 32 + 1];
   uint64_t b1first;
 };
@@ -99,17 +100,19 @@ struct MsdSmem {
 // output (out, vout), the others the heavy output (hout, hvout) -- buckets too
 // large for a shared-memory group leave the dense levels already compacted.
 constexpr uint32_t kLightBit = 0x80000000u;
-template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false>
+// LB: digit-bit capacity (7, or 8 for the levels that save a whole level)
+template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int LB = kMsdLevelBits>
 __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
                                                                    uint32_t* __restrict__ vout, int shift, int dbits,
                                                                    int bshift, uint32_t* __restrict__ cursor,
                                                                    KeyT* __restrict__ hout = nullptr,
                                                                    uint32_t* __restrict__ hvout = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL>*>(smem_raw);
+  constexpr int NBINS = 2 << LB;
+  auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL, NBINS>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbins = LEVEL == 1 ? (1 << dbits) : (2 << dbits);
-  for (int i = tid; i < kMsdScBins; i += kMsdThreads) S.cnt[i] = 0;
+  for (int i = tid; i < NBINS; i += kMsdThreads) S.cnt[i] = 0;
   const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
   if (LEVEL == 2 && tid == 0) {
     KeyT k0 = 0;
@@ -170,9 +173,9 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   __syncthreads();
   // reserve each digit's output range first: the global atomics are in flight
   // while the block scan and the staging run
-  uint32_t resv[kMsdScBins / kMsdThreads];
+  uint32_t resv[NBINS / kMsdThreads];
 #pragma unroll
-  for (int q = 0; q < kMsdScBins / kMsdThreads; ++q) {
+  for (int q = 0; q < NBINS / kMsdThreads; ++q) {
     const int i = tid + q * kMsdThreads;
     resv[q] = 0;
     if (i < nbins) {
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
       }
     }
   }
-  smem_excl_scan<kMsdScBins>(S.cnt, S.tstart, S.wt);
+  smem_excl_scan<NBINS>(S.cnt, S.tstart, S.wt);
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i)
     if (bin[i] >= 0) {
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
       if (HAS_VAL) S.vstage[at] = v[i];
     }
 #pragma unroll
-  for (int q = 0; q < kMsdScBins / kMsdThreads; ++q) {
+  for (int q = 0; q < NBINS / kMsdThreads; ++q) {
     const int i = tid + q * kMsdThreads;
     if (i < nbins && S.cnt[i])
       S.gbase[i] = SPLIT ? (resv[q] & kLightBit) | ((resv[q] - S.tstart[i]) & ~kLightBit) : resv[q] - S.tstart[i];
@@ -459,7 +462,7 @@ struct LocSmem {
   uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
   uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
   uint4 plan[2];                           // current / next group (by iteration parity)
-  uint32_t chist[1 << kMsdLevelBits];      // first-level histogram of the emitted column entries
+  uint32_t chist[1 << kMsdMaxLevelBits];   // first-level histogram of the emitted column entries
 };
 
 // Per group (<= 2048 light keys, 4 per thread, in registers):
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kBmWords; i += kLocThreads) s.bml[i] = s.bms[i] = 0;
-  if (tid < (1 << kMsdLevelBits)) s.chist[tid] = 0;
+  if (tid < (1 << kMsdMaxLevelBits)) s.chist[tid] = 0;
   for (int i = tid; i < kLocT1; i += kLocThreads) {
     s.t1key[i] = 0;
     s.t1cnt[i] = 0;
@@ -749,7 +752,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     if (a_mfan) atomicMax(stats + S_MAXFANOUT, (unsigned long long)a_mfan);
   }
   __syncthreads();
-  if (tid < (1 << kMsdLevelBits) && s.chist[tid]) atomicAdd(chist + tid, s.chist[tid]);
+  if (tid < (1 << kMsdMaxLevelBits) && s.chist[tid]) atomicAdd(chist + tid, s.chist[tid]);
 }
 
 // column entries from two arrays; entries with a zero count are holes

@@ -402,11 +402,11 @@ __global__ void __launch_bounds__(256) seg_emit_rows_kernel(const uint32_t* __re
                                                            uint32_t* __restrict__ chist,
                                                            unsigned long long* __restrict__ ccount,
                                                            unsigned long long* __restrict__ stats, SrcTable gsrc) {
-  __shared__ uint32_t h[1 << kMsdLevelBits];
+  __shared__ uint32_t h[1 << kMsdMaxLevelBits];
   __shared__ uint32_t wt[kWarps + 1];
   __shared__ unsigned long long s_base;
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid < (1 << kMsdLevelBits)) h[tid] = 0;
+  if (tid < (1 << kMsdMaxLevelBits)) h[tid] = 0;
   __syncthreads();
   constexpr int PER = 16;
   const uint64_t dmask = (1ull << b) - 1;
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256) seg_emit_rows_kernel(const uint32_t* __re
     atomicMax(stats + S_MAXLINK, a_mlink);
   }
   __syncthreads();
-  if (tid < (1 << kMsdLevelBits) && h[tid]) atomicAdd(chist + tid, h[tid]);
+  if (tid < (1 << kMsdMaxLevelBits) && h[tid]) atomicAdd(chist + tid, h[tid]);
 }
 
 // Columns: every non-empty child is one destination: fan-in = entries, packets = sum
