@@ -103,3 +103,24 @@ def test_skewed_uniform_blend(lib):
     s = srcs[rng.integers(0, 900, n)]
     d = rng.integers(0, 1 << 20, n).astype(np.uint32)
     _check(lib, s, d, 1 << 32)
+
+
+def test_u8_count_escapes_on_the_column_path(lib):
+    # links with 255 / 256 / 257 / 1000 / 65536 packets: counts >= 256 leave the
+    # column path's u8 counts through the destination table (incl. dst 0xFFFFFFFF
+    # and a destination that only receives escaped links)
+    rng = np.random.default_rng(8)
+    parts_s, parts_d = [], []
+    for i, c in enumerate([255, 256, 257, 1000, 65536, 300, 299]):
+        parts_s.append(np.full(c, 1000 + i, np.uint32))
+        parts_d.append(np.full(c, 77 if i < 5 else 0xFFFFFFFF, np.uint32))
+    parts_s.append(np.full(400, 5, np.uint32))
+    parts_d.append(np.full(400, 123456, np.uint32))  # only escaped links
+    parts_s.append(np.full(600, 6, np.uint32))
+    parts_d.append(np.full(600, 123456, np.uint32))
+    n_bg = (1 << 21) - sum(len(x) for x in parts_s)
+    parts_s.append(rng.integers(0, 1 << 32, n_bg, dtype=np.uint64).astype(np.uint32))
+    parts_d.append(rng.integers(0, 1 << 32, n_bg, dtype=np.uint64).astype(np.uint32))
+    s, d = np.concatenate(parts_s), np.concatenate(parts_d)
+    perm = rng.permutation(len(s))
+    _check(lib, s[perm], d[perm], 1 << 32)
