@@ -240,10 +240,19 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
     bool ok[U];
     // two quads per thread: packets base + 4*(u*256 + tid) .. +4
     load_items<Src, KeyT>(src, base / 4 + threadIdx.x, 256, k, v, ok);
+    int bin[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       c += ok[u];
-      agg_count(h, ok[u] ? (int)((uint64_t)k[u] >> shift) : -1);
+      bin[u] = ok[u] ? (int)((uint64_t)k[u] >> shift) : -1;
+    }
+    if (warp_skewed(bin[0])) {  // only skewed warps pay for the per-round aggregation
+#pragma unroll
+      for (int u = 0; u < U; ++u) agg_count(h, bin[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (bin[u] >= 0) atomicAdd(&h[bin[u]], 1u);
     }
   }
 #pragma unroll
@@ -278,19 +287,27 @@ __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __r
       const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
       k[i] = idx < m ? keys[idx] : KeyT(0);
     }
+    int bin[kMsdIPT];
 #pragma unroll
     for (int i = 0; i < kMsdIPT; ++i) {
       const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
-      int bin = -1;
+      bin[i] = -1;
       if (idx < m) {
         const uint64_t key = (uint64_t)k[i];
         const uint64_t rel = (key >> bshift) - b1first;
         if (rel < 2)
-          bin = (int)((rel << dbits) | ((key >> shift) & dmask));
+          bin[i] = (int)((rel << dbits) | ((key >> shift) & dmask));
         else
           atomicAdd(hist2 + (uint32_t)(key >> shift), 1u);
       }
-      agg_count(cnt, bin);
+    }
+    if (warp_skewed(bin[0])) {
+#pragma unroll
+      for (int i = 0; i < kMsdIPT; ++i) agg_count(cnt, bin[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < kMsdIPT; ++i)
+        if (bin[i] >= 0) atomicAdd(&cnt[bin[i]], 1u);
     }
   }
   __syncthreads();
