@@ -592,8 +592,8 @@ struct SegTotals {
 
 // classify C child counts (light <= kSegCap, big otherwise): cursors with the
 // light bit in scur, light offsets in sloff[0..C], big offsets (= next parents)
-// compacted into npoff; totals on the host
-SegTotals seg_classify(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* npoff) {
+// compacted into npoff; totals in stot (seg_classify: read back to the host)
+void seg_classify_enqueue(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* npoff) {
   c->scur.grow(((size_t)C + 8) * 4);
   c->sloff.grow(((size_t)C + 8) * 4);
   const uint32_t nb = (C + kSegScanItems - 1) / kSegScanItems;
@@ -610,6 +610,9 @@ SegTotals seg_classify(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* n
                                                npoff);
   CK_LAUNCH();
   c->launches += 3;
+}
+SegTotals seg_classify(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* npoff) {
+  seg_classify_enqueue(c, ccnt, C, npoff);
   SegTotals t{};
   CK(cudaMemcpyAsync(&t, c->stot.p, sizeof(t), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -668,17 +671,23 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - dl[0], d_small + kHist, gcount);
     CK_LAUNCH();
   }
-  if (!pre_m) {
+  // The valid count m stays on the device (gcount) until the last level's split
+  // totals come back: later levels size their grids by n and read m there, so
+  // the whole dense partition is queued without a host round trip.
+  int dom_pending = 0;  // dominant-class launches whose bytes (2 kItem m each) wait for m
+  if (pre_m) {
+    set_u64_kernel<<<1, 1, 0, c->st>>>(gcount, pre_m);
+    CK_LAUNCH();
+    ++c->launches;
+  } else {
     scan_counts(c, d_small + kHist, 1u << dl[0], off, cur);
-    CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
     c->launches += 2;
-    if (!m) return 0;
     c->dom_begin("msd_scatter");
     launch_msd_scatter<Src, KeyT, HAS_VAL, 1>(c, dl[0], tiles_of(n, kMsdTile), src, n, outA, voutA, kb - dl[0], 0,
                                               cur);
     CK_LAUNCH();
-    c->dom_end(2 * kItem * m);
+    dom_pending += c->dom_cur;
+    c->dom_end(0);
     ++c->launches;
   }
   KeyT* in_k = outA;
@@ -690,29 +699,26 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     const uint32_t nbl = 1u << cum[l];
     uint32_t* h2 = c->mhist2.as<uint32_t>();
     CK(cudaMemsetAsync(h2, 0, (size_t)nbl * 4, c->st));
-    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(m, kMsdTile * kCount2Tiles), kMsdThreads, 0, c->st>>>(in_k, m, shift,
-                                                                                                      dl[l], bshift,
-                                                                                         h2);
+    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(n, kMsdTile * kCount2Tiles), kMsdThreads, 0, c->st>>>(
+        in_k, gcount, shift, dl[l], bshift, h2);
     CK_LAUNCH();
-    KeySrc<KeyT, HAS_VAL> ks{in_k, in_v, m};
+    KeySrcD<KeyT, HAS_VAL> ks{in_k, in_v, gcount};
     if (split && l + 1 == L) {  // heavy buckets leave compacted (nmx_seg.cuh continues them)
-      c->spoffA.grow(((size_t)std::min<uint64_t>(nbl, m / (kSegCap + 1) + 1) + 8) * 4);
-      split->t = seg_classify(c, h2, nbl, c->spoffA.as<uint32_t>());
-      if (getenv("NMX_DEBUG"))
-        fprintf(stderr, "dense split m=%llu C=%u light=%u big=%u nbig=%u\n", (unsigned long long)m, nbl,
-                split->t.light, split->t.big, split->t.nbig);
+      c->spoffA.grow(((size_t)std::min<uint64_t>(nbl, n / (kSegCap + 1) + 1) + 8) * 4);
+      seg_classify_enqueue(c, h2, nbl, c->spoffA.as<uint32_t>());
       c->dom_begin("msd_scatter");
-      launch_msd_scatter<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>(
-          c, dl[l], tiles_of(m, kMsdTile), ks, m, out_k, out_v, shift, bshift, c->scur.as<uint32_t>(),
+      launch_msd_scatter<KeySrcD<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>(
+          c, dl[l], tiles_of(n, kMsdTile), ks, n, out_k, out_v, shift, bshift, c->scur.as<uint32_t>(),
           reinterpret_cast<KeyT*>(split->hk), split->hv);
     } else {
       scan_counts(c, h2, nbl, off, cur);
       c->dom_begin("msd_scatter");
-      launch_msd_scatter<KeySrc<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>(c, dl[l], tiles_of(m, kMsdTile), ks, m, out_k, out_v,
-                                                                  shift, bshift, cur);
+      launch_msd_scatter<KeySrcD<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2>(c, dl[l], tiles_of(n, kMsdTile), ks, n, out_k,
+                                                                   out_v, shift, bshift, cur);
     }
     CK_LAUNCH();
-    c->dom_end(2 * kItem * m);
+    dom_pending += c->dom_cur;
+    c->dom_end(0);
     c->launches += 3;
     std::swap(in_k, out_k);
     std::swap(in_v, out_v);
@@ -720,6 +726,23 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   *res_k = in_k;
   *res_v = in_v;
   c->msd_levels = L;
+  // one round trip for the whole partition: m and (with a split) its totals
+  struct {
+    SegTotals t;
+    uint32_t pad;
+    unsigned long long m;
+  } back{};
+  if (split) CK(cudaMemcpyAsync(&back.t, c->stot.p, sizeof(SegTotals), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&back.m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  m = back.m;
+  if (split) {
+    split->t = L > 1 ? back.t : SegTotals{};
+    if (getenv("NMX_DEBUG"))
+      fprintf(stderr, "dense split m=%llu light=%u big=%u nbig=%u\n", (unsigned long long)m, split->t.light,
+              split->t.big, split->t.nbig);
+  }
+  c->dom_bytes += (uint64_t)dom_pending * 2 * kItem * m;
   return m;
 }
 
@@ -875,11 +898,11 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
       if (partial)
         local_rows_kernel<true><<<grid, kLocThreads, sizeof(LocSmem), c->st>>>(
             c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol_dst + lbase, hcol_cnt + lbase,
-            cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc);
+            cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc, kNoDirect);
       else
         local_rows_kernel<false><<<grid, kLocThreads, sizeof(LocSmem), c->st>>>(
             c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol_dst + lbase, hcol_cnt + lbase,
-            cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc);
+            cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc, kNoDirect);
       CK_LAUNCH();
       ++c->launches;
     }
@@ -955,7 +978,7 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
       const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3);
       local_cols_kernel<<<grid, kLocThreads, sizeof(LocColSmem), c->st>>>(
           c->lightCK.as<uint32_t>() + lbase, c->lightCV.as<uint32_t>() + lbase, c->mplan.as<uint4>(), ngroups,
-          c->stats.as<unsigned long long>());
+          c->stats.as<unsigned long long>(), kNoDirect);
       CK_LAUNCH();
       ++c->launches;
     }
@@ -993,7 +1016,7 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
     set_smem(local_cols_kernel, sizeof(LocColSmem));
     local_cols_kernel<<<(unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3), kLocThreads,
                         sizeof(LocColSmem), c->st>>>(ck, cv, c->mplan.as<uint4>(), ngroups,
-                                                     c->stats.as<unsigned long long>());
+                                                     c->stats.as<unsigned long long>(), b - Dc);
     CK_LAUNCH();
     ++c->launches;
   }
@@ -1086,7 +1109,7 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
                                sizeof(LocSmem), c->st>>>(keys, c->mplan.as<uint4>(), ngroups, b,
                                                          c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
                                                          cshift, chist, ccount, c->stats.as<unsigned long long>(),
-                                                         SrcTable{});
+                                                         SrcTable{}, b - D);
     CK_LAUNCH();
     ++c->launches;
   }

@@ -8,6 +8,9 @@
 
 namespace nmx {
 
+// stream-ordered store of a host-known count into device memory
+__global__ void set_u64_kernel(unsigned long long* p, unsigned long long v) { *p = v; }
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kThreads = 256;  // every tile kernel runs 8 warps
 constexpr int kWarps = kThreads / 32;

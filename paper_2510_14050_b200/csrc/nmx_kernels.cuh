@@ -102,6 +102,25 @@ struct KeySrc {
     val = HAS_VAL ? vals[j] : 0u;
     return in;
   }
+  __device__ __forceinline__ uint64_t size() const { return n; }
+};
+
+// KeySrc whose item count lives in device memory (written by an earlier kernel
+// on the stream), so the host launches the next level without reading it back;
+// grids are sized by an upper bound and tiles past the count exit at once
+template <typename KeyT, bool HAS_VAL>
+struct KeySrcD {
+  const KeyT* keys;
+  const uint32_t* vals;
+  const unsigned long long* np;
+  __device__ __forceinline__ bool load(uint64_t i, KeyT& key, uint32_t& val) const {
+    const bool in = i < *np;
+    const uint64_t j = in ? i : 0;
+    key = keys[j];
+    val = HAS_VAL ? vals[j] : 0u;
+    return in;
+  }
+  __device__ __forceinline__ uint64_t size() const { return *np; }
 };
 
 // ---------------------------------------------------------------------------

@@ -112,8 +112,11 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL, NBINS>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbins = LEVEL == 1 ? (1 << dbits) : (2 << dbits);
-  for (int i = tid; i < NBINS; i += kMsdThreads) S.cnt[i] = 0;
   const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
+  if constexpr (LEVEL == 2) {
+    if (base >= src.size()) return;  // grid sized by an upper bound (KeySrcD)
+  }
+  for (int i = tid; i < NBINS; i += kMsdThreads) S.cnt[i] = 0;
   if (LEVEL == 2 && tid == 0) {
     KeyT k0 = 0;
     uint32_t v;
@@ -265,8 +268,11 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
 
 // level-2 digit counts per level-1 bucket over the level-1 output
 template <typename KeyT>
-__global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __restrict__ keys, uint64_t m, int shift,
+__global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __restrict__ keys,
+                                                                  const unsigned long long* __restrict__ mp, int shift,
                                                                   int dbits, int bshift, uint32_t* __restrict__ hist2) {
+  const uint64_t m = *mp;  // valid count from the level-1 histogram (grid sized by an upper bound)
+  if ((uint64_t)blockIdx.x * kMsdTile * kCount2Tiles >= m) return;
   // kCount2Tiles consecutive tiles per CTA share one shared histogram, so the
   // global flush costs one atomic per bin per 8192 keys instead of per 2048
   __shared__ uint32_t cnt[kMsdScBins];
@@ -470,11 +476,16 @@ struct SrcTable {
   }
 };
 
+// direct source slots (source - first source of the group), aliasing bms + t2key + t2pf
+constexpr uint32_t kLocDirect = kBmWords + 2 * kLocT2;
+constexpr int kNoDirect = 127;
 struct LocSmem {
   uint32_t bml[kBmWords];            // link-key hash counters
-  uint32_t bms[kBmWords];            // source hash counters
   unsigned long long t1key[kLocT1];  // exact link table for colliding keys: key + 1 (0 = empty)
   uint32_t t1cnt[kLocT1];
+  // hashed source path: counters + exact table; direct path: kLocDirect slots of
+  // packets | fan-out << 16 (all zero between groups in both modes)
+  uint32_t bms[kBmWords];  // source hash counters
   uint32_t t2key[kLocT2];  // exact source table: src + 1 (0 = empty)
   uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
   uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
@@ -494,6 +505,12 @@ struct LocSmem {
 // next group's plan during the counting and every thread loads its next keys
 // into registers while the current group's results are written.
 //
+// Direct sources (dense levels, dsb != kNoDirect): a group's buckets (plan .z/.w)
+// cover a contiguous source range; when it spans <= kLocDirect sources, each key
+// adds packets | fresh-link << 16 to slot src - lo with one shared atomic (the
+// first adder reports) -- no source counters, probing or all-ones special case.
+// dsb = b - D: bucket id -> first source (bucket << dsb, or >> -dsb).
+//
 // PARTIAL (heavy sources split over several groups by destination-bit levels,
 // nmx_seg.cuh): links are still complete per group, but each source's packets
 // and fan-out are partial; they are summed per warp (all lanes usually share
@@ -504,9 +521,10 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
                       uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt, int cshift,
                       uint32_t* __restrict__ chist, unsigned long long* __restrict__ ccount,
-                      unsigned long long* __restrict__ stats, SrcTable gsrc) {
+                      unsigned long long* __restrict__ stats, SrcTable gsrc, int dsb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
+  uint32_t* dir = s.bms;  // kLocDirect slots (bms, t2key, t2pf are contiguous)
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kBmWords; i += kLocThreads) s.bml[i] = s.bms[i] = 0;
   if (tid < (1 << kMsdMaxLevelBits)) s.chist[tid] = 0;
@@ -546,6 +564,21 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     const uint32_t gn = g + gridDim.x;
     uint4 pnext = make_uint4(0, 0, 0, 0);
     if (tid == 0 && gn < ngroups) pnext = plan[gn];
+    // source range of the group's buckets -> direct source slots when it fits
+    uint64_t slo = 0;
+    bool direct = false;
+    if (!PARTIAL && dsb != kNoDirect) {
+      const uint4 pc = s.plan[cur];
+      uint64_t shi;
+      if (dsb >= 0) {
+        slo = (uint64_t)pc.z << dsb;
+        shi = (uint64_t)pc.w << dsb;
+      } else {
+        slo = pc.z >> -dsb;
+        shi = (uint64_t)((pc.w - 1) >> -dsb) + 1;
+      }
+      direct = shi - slo <= kLocDirect;
+    }
     // 1. hash counters (the 16-bit counter indices stay in registers for phases 2-3)
     uint32_t kh[kLocPerThread], sh[kLocPerThread];
 #pragma unroll
@@ -554,7 +587,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       sh[r] = h16u((uint32_t)(kr[r] >> b));
       if ((uint32_t)r < nmine) {
         bm_hit(s.bml, kh[r]);
-        if (!PARTIAL) bm_hit(s.bms, sh[r]);
+        if (!PARTIAL && !direct) bm_hit(s.bms, sh[r]);
       }
     }
     if (tid == 0) s.plan[cur ^ 1] = pnext;
@@ -615,7 +648,11 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         hl[r] = h;
       }
       if (PARTIAL) continue;  // sources: warp-aggregated below
-      if (src == 0xFFFFFFFFu) {
+      if (direct) {
+        const uint32_t o = (uint32_t)(src - slo);
+        if (atomicAdd(&dir[o], 1u | (fresh ? 0x10000u : 0u)) == 0) st[r] |= 8;
+        hs[r] = o;
+      } else if (src == 0xFFFFFFFFu) {
         atomicAdd(&s.sp_src_pk, 1u);
         if (fresh) atomicAdd(&s.sp_src_fo, 1u);
       } else if (bm_once(s.bms, sh[r])) {
@@ -720,7 +757,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         a_msrc = max(a_msrc, 1u);
         a_mfan = max(a_mfan, 1u);
       } else if (st[r] & 8) {
-        const uint32_t pf = s.t2pf[hs[r]];
+        const uint32_t pf = direct ? dir[hs[r]] : s.t2pf[hs[r]];
         if (PARTIAL) {
           gsrc.add((uint32_t)(key >> b), ((unsigned long long)(pf >> 16) << 32) | (pf & 0xFFFFu));
         } else {
@@ -728,11 +765,15 @@ __global__ void __launch_bounds__(kLocThreads, 2)
           a_msrc = max(a_msrc, pf & 0xFFFFu);
           a_mfan = max(a_mfan, pf >> 16);
         }
-        s.t2key[hs[r]] = 0;
-        s.t2pf[hs[r]] = 0;
+        if (direct) {
+          dir[hs[r]] = 0;
+        } else {
+          s.t2key[hs[r]] = 0;
+          s.t2pf[hs[r]] = 0;
+        }
       }
       s.bml[kh[r] >> 4] = 0;  // benign: every writer stores 0
-      if (!PARTIAL) s.bms[sh[r] >> 4] = 0;
+      if (!PARTIAL && !direct) s.bms[sh[r] >> 4] = 0;
     }
     if (tid == 0 && s.sp_src_pk) {
       if (PARTIAL) {
@@ -824,14 +865,22 @@ struct LocColSmem {
   uint32_t spf, spp;  // dst == 0xFFFFFFFF
   uint4 plan[2];
 };
+// direct destination slots: fan-in at words [0, kLocColDirect), packets at
+// [kLocColDirect, 2 kLocColDirect) of bm .. npk (contiguous)
+constexpr uint32_t kLocColDirect = (kBmWords + 3 * kLocCT) / 2;
 
 // Same three phases as local_rows_kernel over (dst, count) column entries: a
 // destination whose hash counter reads "once" has fan-in 1 and `count` packets.
+// Direct destinations as in local_rows_kernel: groups whose buckets span
+// <= kLocColDirect destinations (bucket << dsb) count in slots dst - lo.
 __global__ void __launch_bounds__(kLocThreads, 3)
     local_cols_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
-                      const uint4* __restrict__ plan, uint32_t ngroups, unsigned long long* __restrict__ stats) {
+                      const uint4* __restrict__ plan, uint32_t ngroups, unsigned long long* __restrict__ stats,
+                      int dsb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
+  uint32_t* dfan = s.bm;
+  uint32_t* dpk = s.bm + kLocColDirect;
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kBmWords; i += kLocThreads) s.bm[i] = 0;
   for (int i = tid; i < kLocCT; i += kLocThreads) {
@@ -868,9 +917,18 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     const uint32_t gn = g + gridDim.x;
     uint4 pnext = make_uint4(0, 0, 0, 0);
     if (tid == 0 && gn < ngroups) pnext = plan[gn];
+    uint32_t dlo = 0;
+    bool direct = false;
+    if (dsb != kNoDirect) {
+      const uint4 pc = s.plan[cur];
+      dlo = pc.z << dsb;
+      direct = ((uint64_t)pc.w << dsb) - dlo <= kLocColDirect;
+    }
+    if (!direct) {
 #pragma unroll
-    for (int r = 0; r < kLocColPerThread; ++r)
-      if ((uint32_t)r < nmine) bm_hit(s.bm, h16u(kr[r]));  // one IMAD: recomputed below, not kept
+      for (int r = 0; r < kLocColPerThread; ++r)
+        if ((uint32_t)r < nmine) bm_hit(s.bm, h16u(kr[r]));  // one IMAD: recomputed below, not kept
+    }
     if (tid == 0) s.plan[cur ^ 1] = pnext;
     __syncthreads();
     const uint4 pn = s.plan[cur ^ 1];
@@ -895,7 +953,12 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     for (int r = 0; r < kLocColPerThread; ++r) {
       if ((uint32_t)r >= nmine) continue;
       const uint32_t d = kr[r];
-      if (d == 0xFFFFFFFFu) {
+      if (direct) {
+        const uint32_t o = d - dlo;
+        if (atomicAdd(&dfan[o], 1u) == 0) stc |= 256u << r;
+        atomicAdd(&dpk[o], vr[r]);
+        hh[r] = o;
+      } else if (d == 0xFFFFFFFFu) {
         atomicAdd(&s.spf, 1u);
         atomicAdd(&s.spp, vr[r]);
       } else if (bm_once(s.bm, h16u(d))) {
@@ -932,13 +995,20 @@ __global__ void __launch_bounds__(kLocThreads, 3)
         a_pk = max(a_pk, vr[r]);
       } else if (stc & (256u << r)) {
         a_cnt += 1;
-        a_fanin = max(a_fanin, s.nfan[hh[r]]);
-        a_pk = max(a_pk, s.npk[hh[r]]);
-        s.key[hh[r]] = 0;
-        s.nfan[hh[r]] = 0;
-        s.npk[hh[r]] = 0;
+        if (direct) {
+          a_fanin = max(a_fanin, dfan[hh[r]]);
+          a_pk = max(a_pk, dpk[hh[r]]);
+          dfan[hh[r]] = 0;
+          dpk[hh[r]] = 0;
+        } else {
+          a_fanin = max(a_fanin, s.nfan[hh[r]]);
+          a_pk = max(a_pk, s.npk[hh[r]]);
+          s.key[hh[r]] = 0;
+          s.nfan[hh[r]] = 0;
+          s.npk[hh[r]] = 0;
+        }
       }
-      s.bm[h16u(kr[r]) >> 4] = 0;
+      if (!direct) s.bm[h16u(kr[r]) >> 4] = 0;
     }
     if (tid == 0 && s.spf) {
       a_cnt += 1;

@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kMsdThreads, 5) seg_scatter_kernel(const KeyT*
 __global__ void seg_plan_kernel(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ gb, uint32_t ngroups,
                                 uint4* __restrict__ plan) {
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x)
-    plan[g] = make_uint4(loff[gb[g]], loff[gb[g + 1]], 0, 0);
+    plan[g] = make_uint4(loff[gb[g]], loff[gb[g + 1]], gb[g], gb[g + 1]);  // key range, bucket range
 }
 
 // ---- final level emitters ------------------------------------------------------

@@ -124,3 +124,21 @@ def test_u8_count_escapes_on_the_column_path(lib):
     s, d = np.concatenate(parts_s), np.concatenate(parts_d)
     perm = rng.permutation(len(s))
     _check(lib, s[perm], d[perm], 1 << 32)
+
+
+@pytest.mark.parametrize("logn,bits,law", [(25, 27, "uniform"), (26, 28, "powerlaw"), (22, 12, "powerlaw"),
+                                           (23, 20, "uniform")])
+def test_direct_source_and_destination_slots(lib, logn, bits, law):
+    # groups whose buckets span few addresses index sources (and destinations)
+    # directly: 2^(bits - D) addresses per bucket (D = logn - 9; D > bits at 2^22 / 2^12)
+    n = 1 << logn
+    space = 1 << bits
+    if law == "uniform":
+        rng = np.random.default_rng(logn + bits)
+        s = rng.integers(0, space, n, dtype=np.uint64).astype(np.uint32)
+        d = rng.integers(0, space, n, dtype=np.uint64).astype(np.uint32)
+        s[:1000] = space - 1  # the last source / destination of the space
+        d[500:1500] = space - 1
+    else:
+        s, d = orc.gen_powerlaw(logn, 0, n, space)
+    _check(lib, s, d, space)
