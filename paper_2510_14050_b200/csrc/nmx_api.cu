@@ -122,10 +122,19 @@ struct nmx_ctx {
   cudaStream_t st2 = nullptr;  // copy stream of the streamed path
   cudaEvent_t evc[2] = {nullptr, nullptr}, evu[2] = {nullptr, nullptr}, evs = nullptr;
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
+  unsigned long long* h_scr = nullptr;  // pinned scalars read back mid-pipeline (one round trip each)
+  unsigned long long* scr() {
+    if (!h_scr) CK(cudaMallocHost(&h_scr, 64 * sizeof(unsigned long long)));
+    return h_scr;
+  }
   unsigned long long* h_stats = nullptr;
   size_t h_stats_cap = 0;
   cudaEvent_t ev[40];
   int nev = 0;
+  // deferred partition read-back (msd_partition(defer) -> msd_partition_wait)
+  cudaEvent_t evw = nullptr;
+  uint64_t pend_bytes_per_m = 0;
+  int pend_L = 0;
   float last_total_ms = 0, last_sort_ms = 0;
   float last_stage_ms[8] = {0};
   int last_nstage = 0;
@@ -613,10 +622,10 @@ void seg_classify_enqueue(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t
 }
 SegTotals seg_classify(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* npoff) {
   seg_classify_enqueue(c, ccnt, C, npoff);
-  SegTotals t{};
-  CK(cudaMemcpyAsync(&t, c->stot.p, sizeof(t), cudaMemcpyDeviceToHost, c->st));
+  auto* h = reinterpret_cast<SegTotals*>(c->scr());
+  CK(cudaMemcpyAsync(h, c->stot.p, sizeof(SegTotals), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  return t;
+  return *h;
 }
 
 // level widths of a D-bit dense partition: the fewest levels of <= 8 bits, split
@@ -641,10 +650,29 @@ struct MsdSplit {
   SegTotals t{};
 };
 
+// Waits for a partition's read-back (work queued after it keeps the GPU busy
+// meanwhile): returns m, fills split->t.
+uint64_t msd_partition_wait(nmx_ctx* c, MsdSplit* split) {
+  CK(cudaEventSynchronize(c->evw));
+  const unsigned long long* h = c->scr();
+  const uint64_t m = h[0];
+  if (split) {
+    split->t = c->pend_L > 1 ? *reinterpret_cast<const SegTotals*>(h + 1) : SegTotals{};
+    if (getenv("NMX_DEBUG"))
+      fprintf(stderr, "dense split m=%llu light=%u big=%u nbig=%u\n", (unsigned long long)m, split->t.light,
+              split->t.big, split->t.nbig);
+  }
+  c->dom_bytes += c->pend_bytes_per_m * m;
+  return m;
+}
+
+// defer: return 0 at once; the caller queues more work (sized from device-side
+// totals) and then calls msd_partition_wait
 template <typename Src, typename KeyT, bool HAS_VAL>
 uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, KeyT* outA, uint32_t* voutA,
                        KeyT* outB, uint32_t* voutB, KeyT** res_k, uint32_t** res_v,
-                       const uint32_t* prehist = nullptr, MsdSplit* split = nullptr, uint64_t pre_m = 0) {
+                       const uint32_t* prehist = nullptr, MsdSplit* split = nullptr, uint64_t pre_m = 0,
+                       bool defer = false) {
   int dl[8], cum[8];
   const int L = msd_level_bits(D, dl, cum);
   const uint32_t nb = 1u << D;
@@ -727,23 +755,14 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   *res_v = in_v;
   c->msd_levels = L;
   // one round trip for the whole partition: m and (with a split) its totals
-  struct {
-    SegTotals t;
-    uint32_t pad;
-    unsigned long long m;
-  } back{};
-  if (split) CK(cudaMemcpyAsync(&back.t, c->stot.p, sizeof(SegTotals), cudaMemcpyDeviceToHost, c->st));
-  CK(cudaMemcpyAsync(&back.m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  m = back.m;
-  if (split) {
-    split->t = L > 1 ? back.t : SegTotals{};
-    if (getenv("NMX_DEBUG"))
-      fprintf(stderr, "dense split m=%llu light=%u big=%u nbig=%u\n", (unsigned long long)m, split->t.light,
-              split->t.big, split->t.nbig);
-  }
-  c->dom_bytes += (uint64_t)dom_pending * 2 * kItem * m;
-  return m;
+  unsigned long long* h = c->scr();  // [0] m, [1..2] split totals
+  if (split) CK(cudaMemcpyAsync(h + 1, c->stot.p, sizeof(SegTotals), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(h, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+  if (!c->evw) CK(cudaEventCreateWithFlags(&c->evw, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->evw, c->st));
+  c->pend_bytes_per_m = (uint64_t)dom_pending * 2 * kItem;
+  c->pend_L = L;
+  return defer ? 0 : msd_partition_wait(c, split);
 }
 
 // ---- segmented MSD levels over heavy buckets (nmx_seg.cuh) ------------------
@@ -773,6 +792,24 @@ SegTotals seg_level_plan(nmx_ctx* c, const KeyT* k, const uint32_t* v, uint32_t 
 }
 
 // shared-memory groups over this level's light children (loff = sloff, C children)
+// the same with the light total still on the device (stot[0], deferred
+// partition read-back): plans for at most `upper` keys; returns the device
+// group count for the grouping kernel
+const uint32_t* seg_plan_groups_dev(nmx_ctx* c, uint32_t C, uint64_t upper, uint32_t S) {
+  const uint64_t ng_max = (upper + S - 1) / S;
+  c->mgb.grow(((size_t)ng_max + 2) * 4);
+  c->mplan.grow(((size_t)ng_max + 2) * 16);
+  uint32_t* ngp = c->stot.as<uint32_t>() + 12;
+  const unsigned g1 = (unsigned)std::min<uint64_t>((ng_max + 256) / 256, (uint64_t)c->sms * 8);
+  group_bounds_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), C, S, 0, c->mgb.as<uint32_t>(),
+                                             c->stot.as<uint32_t>(), ngp);
+  CK_LAUNCH();
+  seg_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), 0, c->mplan.as<uint4>(), ngp);
+  CK_LAUNCH();
+  c->launches += 2;
+  return ngp;
+}
+
 uint32_t seg_plan_groups(nmx_ctx* c, uint32_t C, uint32_t light, uint32_t S) {
   const uint32_t ngroups = (light + S - 1) / S;
   c->mgb.grow(((size_t)ngroups + 2) * 4);
@@ -871,10 +908,10 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
                                                  ccount, c->stats.as<unsigned long long>(), gsrc);
       CK_LAUNCH();
       c->launches += 2;
-      unsigned long long hc = 0;
-      CK(cudaMemcpyAsync(&hc, c->hcount.p, 8, cudaMemcpyDeviceToHost, c->st));
+      unsigned long long* hc = c->scr();
+      CK(cudaMemcpyAsync(hc, c->hcount.p, 8, cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
-      lbase += hc;
+      lbase += *hc;
       m = 0;
       break;
     }
@@ -1006,21 +1043,21 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   MsdSplit sp;
   sp.hk = c->cgk.p;
   sp.hv = c->cgv.as<uint32_t>();
-  const uint64_t u = msd_partition<ColConcatSrc, uint32_t, true>(c, cs, cs.n, b, Dc, c->ckB.as<uint32_t>(),
-                                                                 c->cvB.as<uint32_t>(), c->ckA.as<uint32_t>(),
-                                                                 c->cvA.as<uint32_t>(), &ck, &cv, prehist, &sp);
+  msd_partition<ColConcatSrc, uint32_t, true>(c, cs, cs.n, b, Dc, c->ckB.as<uint32_t>(), c->cvB.as<uint32_t>(),
+                                              c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), &ck, &cv, prehist, &sp, 0,
+                                              true);
   c->mark();  // column partition end
-  if (!u) return;
-  if (sp.t.light) {
-    const uint32_t ngroups = seg_plan_groups(c, 1u << Dc, sp.t.light, kLocColChunk);
+  {
+    const uint32_t* ngp = seg_plan_groups_dev(c, 1u << Dc, cs.n, kLocColChunk);
     set_smem(local_cols_kernel, sizeof(LocColSmem));
-    local_cols_kernel<<<(unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3), kLocThreads,
-                        sizeof(LocColSmem), c->st>>>(ck, cv, c->mplan.as<uint4>(), ngroups,
-                                                     c->stats.as<unsigned long long>(), b - Dc);
+    local_cols_kernel<<<c->sms * 3, kLocThreads, sizeof(LocColSmem), c->st>>>(
+        ck, cv, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp);
     CK_LAUNCH();
     ++c->launches;
   }
   c->mark();  // local columns end
+  const uint64_t u = msd_partition_wait(c, &sp);
+  if (!u) return;
   if (sp.t.big) {  // heavy destination buckets: segmented MSD levels (nmx_seg.cuh)
     c->cgk2.grow((size_t)sp.t.big * 4);
     c->cgv2.grow((size_t)sp.t.big * 4);
@@ -1047,9 +1084,10 @@ uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint6
   msd_hist1_kernel<PacketSrc, uint64_t><<<hgrid, 256, 0, c->st>>>(ps, n, kb - dl[0], d_small + kHist, gcount);
   CK_LAUNCH();
   scan_counts(c, d_small + kHist, 1u << dl[0], c->moff.as<uint32_t>(), c->mcur.as<uint32_t>());
-  unsigned long long m = 0;
-  CK(cudaMemcpyAsync(&m, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+  unsigned long long* hm = c->scr();
+  CK(cudaMemcpyAsync(hm, gcount, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  const unsigned long long m = *hm;
   if (m) {
     launch_msd_scatter<PacketSrc, uint64_t, false, 1>(c, dl[0], tiles_of(n, kMsdTile), ps, n, out, nullptr,
                                                       kb - dl[0], 0, c->mcur.as<uint32_t>());
@@ -1090,30 +1128,31 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   uint32_t* dummy = nullptr;
   MsdSplit sp;
   sp.hk = c->keysC.p;
-  const uint64_t m = msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
-                                                               c->keysB.as<uint64_t>(), nullptr, &keys, &dummy,
-                                                               nullptr, &sp, pre_m);
+  // the partition's totals come back while the light groups run (plans and
+  // group count derived on the device)
+  msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
+                                            c->keysB.as<uint64_t>(), nullptr, &keys, &dummy, nullptr, &sp, pre_m,
+                                            true);
   c->last_sort_launches = c->msd_levels;
   c->mark();  // 2: row partition end
   ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), 0, c->ckA.as<uint32_t>(),
                   c->cvA.as<uint32_t>(),      0,                          0};
   cs.quad = true;  // context buffers are cudaMalloc-aligned
-  if (!m) return cs;
   const uint32_t nb = 1u << D;
   const int Dc = std::min(D, b);
   const int cshift = b - msd_first_bits(Dc);
-  if (sp.t.light) {
-    const uint32_t ngroups = seg_plan_groups(c, nb, sp.t.light, kLocChunk);
+  {
+    const uint32_t* ngp = seg_plan_groups_dev(c, nb, pre_m ? pre_m : n, kLocChunk);
     set_smem(local_rows_kernel<false>, sizeof(LocSmem));
-    local_rows_kernel<false><<<(unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 2), kLocThreads,
-                               sizeof(LocSmem), c->st>>>(keys, c->mplan.as<uint4>(), ngroups, b,
-                                                         c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(),
-                                                         cshift, chist, ccount, c->stats.as<unsigned long long>(),
-                                                         SrcTable{}, b - D);
+    local_rows_kernel<false><<<c->sms * 2, kLocThreads, sizeof(LocSmem), c->st>>>(
+        keys, c->mplan.as<uint4>(), 0, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), cshift, chist,
+        ccount, c->stats.as<unsigned long long>(), SrcTable{}, b - D, ngp);
     CK_LAUNCH();
     ++c->launches;
   }
   c->mark();  // 3: local rows end
+  const uint64_t m = msd_partition_wait(c, &sp);
+  if (!m) return cs;
   uint64_t uh = 0;
   if (sp.t.big) {  // heavy row buckets: segmented MSD levels (nmx_seg.cuh)
     c->keysD.grow((size_t)sp.t.big * 8);
@@ -1500,6 +1539,8 @@ void nmx_destroy(nmx_ctx* c) {
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
     b->release();
   if (c->h_small) cudaFreeHost(c->h_small);
+  if (c->h_scr) cudaFreeHost(c->h_scr);
+  if (c->evw) cudaEventDestroy(c->evw);
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->evk) cudaEventDestroy(e);

@@ -393,8 +393,15 @@ __global__ void __launch_bounds__(256) scan_apply_kernel(const uint32_t* __restr
 }
 
 // group g covers the buckets whose start lies in [g*S, (g+1)*S)
+// lightp != nullptr: the light total is on the device (deferred partition
+// read-back); ngroups = ceil(light / S) is derived here and stored to *ngout
 __global__ void group_bounds_kernel(const uint32_t* __restrict__ off, uint32_t nb, uint32_t S, uint32_t ngroups,
-                                    uint32_t* __restrict__ gb) {
+                                    uint32_t* __restrict__ gb, const uint32_t* __restrict__ lightp = nullptr,
+                                    uint32_t* __restrict__ ngout = nullptr) {
+  if (lightp) {
+    ngroups = (*lightp + S - 1) / S;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ngout = ngroups;
+  }
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g <= ngroups; g += gridDim.x * blockDim.x) {
     const uint64_t target = (uint64_t)g * S;
     uint32_t a = 0, z = nb;  // first bucket with off >= target (nb if none)
@@ -521,7 +528,9 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
                       uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt, int cshift,
                       uint32_t* __restrict__ chist, unsigned long long* __restrict__ ccount,
-                      unsigned long long* __restrict__ stats, SrcTable gsrc, int dsb) {
+                      unsigned long long* __restrict__ stats, SrcTable gsrc, int dsb,
+                      const uint32_t* __restrict__ ngp = nullptr) {
+  if (ngp) ngroups = *ngp;  // group count on the device (grid sized for the SMs)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
   uint32_t* dir = s.bms;  // kLocDirect slots (bms, t2key, t2pf are contiguous)
@@ -876,7 +885,8 @@ constexpr uint32_t kLocColDirect = (kBmWords + 3 * kLocCT) / 2;
 __global__ void __launch_bounds__(kLocThreads, 3)
     local_cols_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
                       const uint4* __restrict__ plan, uint32_t ngroups, unsigned long long* __restrict__ stats,
-                      int dsb) {
+                      int dsb, const uint32_t* __restrict__ ngp = nullptr) {
+  if (ngp) ngroups = *ngp;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
   uint32_t* dfan = s.bm;
