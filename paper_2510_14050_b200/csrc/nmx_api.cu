@@ -685,6 +685,7 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   uint32_t* off = c->moff.as<uint32_t>();
   constexpr uint64_t kItem = sizeof(KeyT) + (HAS_VAL ? 4 : 0);  // 8 B per item in and out
   unsigned long long m = pre_m;
+  bool joint = false;  // level-2 counts already in mhist2 (msd_hist12_kernel)
   *res_k = outA;
   *res_v = voutA;
   if (pre_m) {
@@ -695,8 +696,21 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   } else {
     CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
     CK(cudaMemsetAsync(gcount, 0, 8, c->st));
-    const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
-    msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - dl[0], d_small + kHist, gcount);
+    // levels 1 + 2 counted together when the per-CTA flush of the joint bins
+    // stays below 1/16 of the keys (large inputs)
+    if (L >= 2 && cum[1] <= kJointMaxBits && dl[1] >= 5 && n >= ((uint64_t)c->sms * 3 << (cum[1] + 4))) {
+      joint = true;
+      CK(cudaMemsetAsync(c->mhist2.p, 0, sizeof(uint32_t) << cum[1], c->st));
+      auto k = msd_hist12_kernel<Src, KeyT>;
+      const size_t sm = sizeof(uint32_t) << cum[1];
+      set_smem(k, sm);
+      const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 3));
+      k<<<hgrid, 256, sm, c->st>>>(src, n, kb - cum[1], cum[1], dl[1], d_small + kHist, c->mhist2.as<uint32_t>(),
+                                   gcount);
+    } else {
+      const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
+      msd_hist1_kernel<Src, KeyT><<<hgrid, 256, 0, c->st>>>(src, n, kb - dl[0], d_small + kHist, gcount);
+    }
     CK_LAUNCH();
   }
   // The valid count m stays on the device (gcount) until the last level's split
@@ -726,10 +740,12 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     const int shift = kb - cum[l], bshift = kb - cum[l - 1];
     const uint32_t nbl = 1u << cum[l];
     uint32_t* h2 = c->mhist2.as<uint32_t>();
-    CK(cudaMemsetAsync(h2, 0, (size_t)nbl * 4, c->st));
-    msd_count2_kernel<KeyT><<<(unsigned)tiles_of(n, kMsdTile * kCount2Tiles), kMsdThreads, 0, c->st>>>(
-        in_k, gcount, shift, dl[l], bshift, h2);
-    CK_LAUNCH();
+    if (!(joint && l == 1)) {
+      CK(cudaMemsetAsync(h2, 0, (size_t)nbl * 4, c->st));
+      msd_count2_kernel<KeyT><<<(unsigned)tiles_of(n, kMsdTile * kCount2Tiles), kMsdThreads, 0, c->st>>>(
+          in_k, gcount, shift, dl[l], bshift, h2);
+      CK_LAUNCH();
+    }
     KeySrcD<KeyT, HAS_VAL> ks{in_k, in_v, gcount};
     if (split && l + 1 == L) {  // heavy buckets leave compacted (nmx_seg.cuh continues them)
       c->spoffA.grow(((size_t)std::min<uint64_t>(nbl, n / (kSegCap + 1) + 1) + 8) * 4);

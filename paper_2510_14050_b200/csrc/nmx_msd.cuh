@@ -266,6 +266,58 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
     if (h[i]) atomicAdd(hist1 + i, h[i]);
 }
 
+// Levels 1 and 2 counted in one pass over the source: the joint histogram of the
+// top cum2 = d1 + d2 key bits (<= 2^14 bins, dynamic shared memory) goes to
+// hist2 -- exactly what msd_count2_kernel would count over the level-1 output --
+// and its d1-row sums to hist1. One streaming pass instead of two.
+constexpr int kJointMaxBits = 14;
+template <typename Src, typename KeyT>
+__global__ void __launch_bounds__(256) msd_hist12_kernel(Src src, uint64_t n, int jshift, int jbits, int d2bits,
+                                                        uint32_t* __restrict__ hist1, uint32_t* __restrict__ hist2,
+                                                        unsigned long long* __restrict__ gcount) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+  const int nbins = 1 << jbits;
+  for (int i = threadIdx.x; i < nbins; i += 256) h[i] = 0;
+  __syncthreads();
+  uint32_t c = 0;
+  constexpr int U = 8;
+  const uint64_t stride = (uint64_t)gridDim.x * 256 * U;
+  for (uint64_t base = (uint64_t)blockIdx.x * 256 * U; base < n; base += stride) {
+    KeyT k[U];
+    uint32_t v[U];
+    bool ok[U];
+    load_items<Src, KeyT>(src, base / 4 + threadIdx.x, 256, k, v, ok);
+    int bin[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      c += ok[u];
+      bin[u] = ok[u] ? (int)((uint64_t)k[u] >> jshift) : -1;
+    }
+    if (warp_skewed(bin[0])) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) agg_count(h, bin[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (bin[u] >= 0) atomicAdd(&h[bin[u]], 1u);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(gcount, (unsigned long long)c);
+  __syncthreads();
+  // d2bits >= 5: the 32 bins of a warp share one level-1 digit
+  for (int i = threadIdx.x; i < nbins; i += 256) {
+    const uint32_t x = h[i];
+    if (x) atomicAdd(hist2 + i, x);
+    uint32_t r = x;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(FULL, r, o);
+    if ((threadIdx.x & 31) == 0 && r) atomicAdd(hist1 + (i >> d2bits), r);
+  }
+}
+
 // level-2 digit counts per level-1 bucket over the level-1 output
 template <typename KeyT>
 __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __restrict__ keys,
