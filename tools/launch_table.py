@@ -14,7 +14,7 @@ seq = []
 for r in rows[1 + skip:]:
     name = r[ki].split("(")[0].replace("void ", "")[:90]
     v = float(r[vi].replace(",", ""))
-    v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(r[ui], 1.0)
+    v *= {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(r[ui], 1.0)
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1
     a[1] += v
