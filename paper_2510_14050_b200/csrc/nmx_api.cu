@@ -980,25 +980,24 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
 // (children stay whole destinations, local_cols_kernel), final level
 // count-only with packet sums (one destination per child).
 void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
+  // packed items (dst << 32 | count): key bits [32, 32 + b)
   int w[8];
   int L = split_levels(b - Dc, w);
   if (!L) w[L++] = 0;  // the dense levels already isolate single destinations
-  c->lightCK.grow(ch * 4);
-  c->lightCV.grow(ch * 4);
+  c->lightCK.grow(ch * 8);
   uint32_t* poff = c->spoffA.as<uint32_t>();
-  uint32_t* ink = c->cgk.as<uint32_t>();
-  uint32_t* inv = c->cgv.as<uint32_t>();
-  uint32_t* outk = c->cgk2.as<uint32_t>();
-  uint32_t* outv = c->cgv2.as<uint32_t>();
+  uint64_t* ink = c->cgk.as<uint64_t>();
+  uint64_t* outk = c->cgk2.as<uint64_t>();
+  uint64_t* light = c->lightCK.as<uint64_t>();
   uint32_t P = nheavy, m = (uint32_t)ch;
   uint64_t lbase = 0;
   int consumed = Dc;
-  set_smem(seg_scatter_kernel<uint32_t, true>, sizeof(SegSmem<uint32_t, true>));
+  set_smem(seg_scatter_kernel<uint64_t, false>, sizeof(SegSmem<uint64_t, false>));
   set_smem(local_cols_kernel, sizeof(LocColSmem));
   for (int l = 0; l < L && m; ++l) {
     const int dbits = w[l];
     consumed += dbits;
-    const int shift = b - consumed;
+    const int shift = b + 32 - consumed;
     const uint32_t C = P << dbits;
     if (l + 1 == L) {
       c->sccnt.grow(((size_t)C + 8) * 4);
@@ -1006,8 +1005,8 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
       uint32_t* ccnt = c->sccnt.as<uint32_t>();
       CK(cudaMemsetAsync(ccnt, 0, (size_t)C * 4, c->st));
       CK(cudaMemsetAsync(c->ssum.p, 0, (size_t)C * 8, c->st));
-      seg_count_kernel<uint32_t, true, true><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(
-          ink, inv, m, poff, P, shift, dbits, ccnt, c->ssum.as<unsigned long long>(), nullptr);
+      seg_count_kernel<uint64_t, false, true, true><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads, 0, c->st>>>(
+          ink, nullptr, m, poff, P, shift, dbits, ccnt, c->ssum.as<unsigned long long>(), nullptr);
       CK_LAUNCH();
       const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((C + 255) / 256, (uint64_t)c->sms * 8));
       seg_emit_cols_kernel<<<g, 256, 0, c->st>>>(ccnt, c->ssum.as<unsigned long long>(), C,
@@ -1019,25 +1018,22 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
     DevBuf& nb = (l & 1) ? c->spoffA : c->spoffB;
     nb.grow(((size_t)std::min<uint64_t>(C, m / (kSegCap + 1) + 1) + 8) * 4);
     uint32_t* npoff = nb.as<uint32_t>();
-    const SegTotals t = seg_level_plan<uint32_t, true>(c, ink, inv, m, poff, P, shift, dbits, npoff);
-    seg_scatter_kernel<uint32_t, true><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads,
-                                         sizeof(SegSmem<uint32_t, true>), c->st>>>(
-        ink, inv, m, poff, P, shift, dbits, c->scur.as<uint32_t>(), c->lightCK.as<uint32_t>() + lbase,
-        c->lightCV.as<uint32_t>() + lbase, outk, outv);
+    const SegTotals t = seg_level_plan<uint64_t, false>(c, ink, nullptr, m, poff, P, shift, dbits, npoff);
+    seg_scatter_kernel<uint64_t, false><<<(unsigned)tiles_of(m, kMsdTile), kMsdThreads,
+                                          sizeof(SegSmem<uint64_t, false>), c->st>>>(
+        ink, nullptr, m, poff, P, shift, dbits, c->scur.as<uint32_t>(), light + lbase, nullptr, outk, nullptr);
     CK_LAUNCH();
     ++c->launches;
     if (t.light) {
       const uint32_t ngroups = seg_plan_groups(c, C, t.light, kLocColChunk);
       const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3);
       local_cols_kernel<<<grid, kLocThreads, sizeof(LocColSmem), c->st>>>(
-          c->lightCK.as<uint32_t>() + lbase, c->lightCV.as<uint32_t>() + lbase, c->mplan.as<uint4>(), ngroups,
-          c->stats.as<unsigned long long>(), kNoDirect);
+          light + lbase, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>(), kNoDirect);
       CK_LAUNCH();
       ++c->launches;
     }
     lbase += t.light;
     std::swap(ink, outk);
-    std::swap(inv, outv);
     poff = npoff;
     P = t.nbig;
     m = t.big;
@@ -1049,25 +1045,24 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
 // second level writes ckA / cvA): MSD partition by destination bits ->
 // shared-memory grouping -> heavy destinations via LSD + col_kernel.
 void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32_t* prehist) {
-  uint32_t* ck = nullptr;
-  uint32_t* cv = nullptr;
+  // the levels move packed u64 items (dst << 32 | count, key bits [32, 32 + b))
+  // through the row key buffers, free once the row half is queued
+  uint64_t* ce = nullptr;
+  uint32_t* unused = nullptr;
   const uint64_t need = cs.n;
-  c->ckB.grow(need * 4);
-  c->cvB.grow(need * 4);
-  c->cgk.grow(need * 4);
-  c->cgv.grow(need * 4);
+  c->keysA.grow(need * 8);
+  c->keysB.grow(need * 8);
+  c->cgk.grow(need * 8);
   MsdSplit sp;
   sp.hk = c->cgk.p;
-  sp.hv = c->cgv.as<uint32_t>();
-  msd_partition<ColConcatSrc, uint32_t, true>(c, cs, cs.n, b, Dc, c->ckB.as<uint32_t>(), c->cvB.as<uint32_t>(),
-                                              c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), &ck, &cv, prehist, &sp, 0,
-                                              true);
+  msd_partition<ColConcatSrc, uint64_t, false>(c, cs, cs.n, b + 32, Dc, c->keysA.as<uint64_t>(), nullptr,
+                                               c->keysB.as<uint64_t>(), nullptr, &ce, &unused, prehist, &sp, 0, true);
   c->mark();  // column partition end
   {
     const uint32_t* ngp = seg_plan_groups_dev(c, 1u << Dc, cs.n, kLocColChunk);
     set_smem(local_cols_kernel, sizeof(LocColSmem));
     local_cols_kernel<<<c->sms * 3, kLocThreads, sizeof(LocColSmem), c->st>>>(
-        ck, cv, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp);
+        ce, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp);
     CK_LAUNCH();
     ++c->launches;
   }
@@ -1075,8 +1070,7 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   const uint64_t u = msd_partition_wait(c, &sp);
   if (!u) return;
   if (sp.t.big) {  // heavy destination buckets: segmented MSD levels (nmx_seg.cuh)
-    c->cgk2.grow((size_t)sp.t.big * 4);
-    c->cgv2.grow((size_t)sp.t.big * 4);
+    c->cgk2.grow((size_t)sp.t.big * 8);
     heavy_cols(c, sp.t.big, sp.t.nbig, b, Dc);
   }
 }

@@ -74,6 +74,7 @@ __device__ __forceinline__ void quad_items(const KeySrc<KeyT, HAS_VAL>& s, uint6
 }
 struct ColConcatSrc;
 __device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok);
+__device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint64_t* k, uint32_t* v, bool* ok);
 template <typename Src, typename KeyT, int NQ = 2>
 __device__ __forceinline__ void load_items(const Src& s, uint64_t q0, uint64_t qstride, KeyT* k, uint32_t* v,
                                            bool* ok) {
@@ -906,10 +907,29 @@ struct ColConcatSrc {
     val = first ? v1[j] : v2[j - n1];
     return in && val != 0;
   }
+  // packed column item: dst << 32 | count
+  __device__ __forceinline__ bool load(uint64_t i, uint64_t& item, uint32_t& val) const {
+    uint32_t d, c;
+    const bool ok = load(i, d, c);
+    item = ((uint64_t)d << 32) | c;
+    val = 0;
+    return ok;
+  }
 };
 
 __device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok) {
   s.load_quad(q, k, v, ok);
+}
+// the column partition moves packed u64 items (dst << 32 | count): one 8-byte
+// stream per level instead of two 4-byte ones (whole 128-byte runs per digit)
+__device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint64_t* k, uint32_t* v, bool* ok) {
+  uint32_t d[4], c[4];
+  s.load_quad(q, d, c, ok);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    k[t] = ((uint64_t)d[t] << 32) | c[t];
+    v[t] = 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -935,9 +955,8 @@ constexpr uint32_t kLocColDirect = (kBmWords + 3 * kLocCT) / 2;
 // Direct destinations as in local_rows_kernel: groups whose buckets span
 // <= kLocColDirect destinations (bucket << dsb) count in slots dst - lo.
 __global__ void __launch_bounds__(kLocThreads, 3)
-    local_cols_kernel(const uint32_t* __restrict__ ck, const uint32_t* __restrict__ cv,
-                      const uint4* __restrict__ plan, uint32_t ngroups, unsigned long long* __restrict__ stats,
-                      int dsb, const uint32_t* __restrict__ ngp = nullptr) {
+    local_cols_kernel(const uint64_t* __restrict__ ce, const uint4* __restrict__ plan, uint32_t ngroups,
+                      unsigned long long* __restrict__ stats, int dsb, const uint32_t* __restrict__ ngp = nullptr) {
   if (ngp) ngroups = *ngp;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
@@ -964,9 +983,9 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     for (int r = 0; r < kLocColPerThread; ++r) {
       const uint32_t j = tid + r * kLocThreads;
       if (j < nlight) {
-        const uint32_t i = light_index(p, j);
-        kr[r] = ck[i];
-        vr[r] = cv[i];
+        const uint64_t e = ce[light_index(p, j)];
+        kr[r] = (uint32_t)(e >> 32);
+        vr[r] = (uint32_t)e;
         ++nmine;
       }
     }
@@ -1002,9 +1021,9 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       for (int r = 0; r < kLocColPerThread; ++r) {
         const uint32_t j = tid + r * kLocThreads;
         if (j < nl2) {
-          const uint32_t i = light_index(pn, j);
-          kn[r] = ck[i];
-          vn[r] = cv[i];
+          const uint64_t e = ce[light_index(pn, j)];
+          kn[r] = (uint32_t)(e >> 32);
+          vn[r] = (uint32_t)e;
           ++nnext;
         }
       }

@@ -50,15 +50,16 @@ __device__ __forceinline__ uint32_t seg_digit(KeyT key, int shift, uint32_t dmas
 
 // Child counts (FINAL: + per-child packet sums for (dst, count) items, or one
 // representative key per child for row keys -- all keys of a final child are equal).
-template <typename KeyT, bool HAS_VAL, bool FINAL>
+// PACKED: u64 column items (dst << 32 | count), summed like a value
+template <typename KeyT, bool HAS_VAL, bool FINAL, bool PACKED = false>
 __global__ void __launch_bounds__(kMsdThreads) seg_count_kernel(const KeyT* __restrict__ keys,
                                                                const uint32_t* __restrict__ vals, uint32_t m,
                                                                const uint32_t* __restrict__ poff, uint32_t P,
                                                                int shift, int dbits, uint32_t* __restrict__ ccnt,
                                                                unsigned long long* __restrict__ csum,
                                                                KeyT* __restrict__ rep) {
-  constexpr bool SUM = FINAL && HAS_VAL;
-  constexpr bool REP = FINAL && !HAS_VAL;
+  constexpr bool SUM = FINAL && (HAS_VAL || PACKED);
+  constexpr bool REP = FINAL && !HAS_VAL && !PACKED;
   __shared__ uint32_t cnt[kSegBins];
   __shared__ uint32_t sum[SUM ? kSegBins : 1];  // < 2^32 packets per call: 32-bit shared atomics
   __shared__ KeyT srep[REP ? kSegBins : 1];
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(kMsdThreads) seg_count_kernel(const KeyT* __re
     const uint32_t idx = base + i * kMsdThreads + tid;
     const uint32_t j = idx < m ? idx : 0;
     k[i] = keys[j];
-    v[i] = HAS_VAL ? vals[j] : 0u;
+    v[i] = HAS_VAL ? vals[j] : PACKED ? (uint32_t)(uint64_t)k[i] : 0u;
   }
   __syncthreads();
   const uint32_t p0 = s_p0;
