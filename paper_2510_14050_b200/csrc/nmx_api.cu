@@ -881,8 +881,7 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
   uint32_t* poff = c->spoffA.as<uint32_t>();
   uint64_t* in = c->keysC.as<uint64_t>();
   uint64_t* out = c->keysD.as<uint64_t>();
-  uint32_t* hcol_dst = c->ckA.as<uint32_t>();
-  uint32_t* hcol_cnt = c->cvA.as<uint32_t>();
+  uint64_t* hcol = c->ckA.as<uint64_t>();  // packed column items of the heavy sources
   uint32_t P = nheavy, m = (uint32_t)mh;
   uint64_t lbase = 0;
   SrcTable gsrc;
@@ -919,8 +918,8 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
           in, nullptr, m, poff, P, shift, dbits, ccnt, nullptr, c->srep.as<uint64_t>());
       CK_LAUNCH();
       const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((C + 4095) / 4096, (uint64_t)c->sms * 4));
-      seg_emit_rows_kernel<<<g, 256, 0, c->st>>>(ccnt, c->srep.as<uint64_t>(), C, b, hcol_dst + lbase,
-                                                 hcol_cnt + lbase, c->hcount.as<unsigned long long>(), cshift, chist,
+      seg_emit_rows_kernel<<<g, 256, 0, c->st>>>(ccnt, c->srep.as<uint64_t>(), C, b, hcol + lbase,
+                                                 c->hcount.as<unsigned long long>(), cshift, chist,
                                                  ccount, c->stats.as<unsigned long long>(), gsrc);
       CK_LAUNCH();
       c->launches += 2;
@@ -950,11 +949,11 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
       const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 2);
       if (partial)
         local_rows_kernel<true><<<grid, kLocThreads, sizeof(LocSmem), c->st>>>(
-            c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol_dst + lbase, hcol_cnt + lbase,
+            c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol + lbase,
             cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc, kNoDirect);
       else
         local_rows_kernel<false><<<grid, kLocThreads, sizeof(LocSmem), c->st>>>(
-            c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol_dst + lbase, hcol_cnt + lbase,
+            c->lightK.as<uint64_t>() + lbase, c->mplan.as<uint4>(), ngroups, b, hcol + lbase,
             cshift, chist, ccount, c->stats.as<unsigned long long>(), gsrc, kNoDirect);
       CK_LAUNCH();
       ++c->launches;
@@ -1119,12 +1118,8 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   c->keysA.grow(n * 8);
   c->keysB.grow(n * 8);
   c->keysC.grow(n * 8);
-  c->colL_dst.grow(n * 4);
-  c->colL_cnt.grow(n * 4);
-  c->ckA.grow(n * 4);
-  c->cvA.grow(n * 4);
-  c->ckB.grow(n * 4);
-  c->cvB.grow(n * 4);
+  c->colL_dst.grow(n * 8);  // packed column slots of the light groups
+  c->ckA.grow(n * 8);       // packed column items of the heavy sources
   c->mch.grow((kMsdMaxBins + 4) * 4);
   uint32_t* chist = c->mch.as<uint32_t>();
   *chist_out = chist;
@@ -1145,8 +1140,7 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
                                             true);
   c->last_sort_launches = c->msd_levels;
   c->mark();  // 2: row partition end
-  ColConcatSrc cs{c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), 0, c->ckA.as<uint32_t>(),
-                  c->cvA.as<uint32_t>(),      0,                          0};
+  ColConcatSrc cs{c->colL_dst.as<uint64_t>(), 0, c->ckA.as<uint64_t>(), 0, 0};
   cs.quad = true;  // context buffers are cudaMalloc-aligned
   const uint32_t nb = 1u << D;
   const int Dc = std::min(D, b);
@@ -1155,7 +1149,7 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     const uint32_t* ngp = seg_plan_groups_dev(c, nb, pre_m ? pre_m : n, kLocChunk);
     set_smem(local_rows_kernel<false>, sizeof(LocSmem));
     local_rows_kernel<false><<<c->sms * 2, kLocThreads, sizeof(LocSmem), c->st>>>(
-        keys, c->mplan.as<uint4>(), 0, b, c->colL_dst.as<uint32_t>(), c->colL_cnt.as<uint32_t>(), cshift, chist,
+        keys, c->mplan.as<uint4>(), 0, b, c->colL_dst.as<uint64_t>(), cshift, chist,
         ccount, c->stats.as<unsigned long long>(), SrcTable{}, b - D, ngp);
     CK_LAUNCH();
     ++c->launches;
@@ -1987,9 +1981,11 @@ int nmx_shard_cols(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, u
     c->cvA.grow(u * 4);
     c->cvB.grow(u * 4);
     if (const int Dc = msd_bits(u, b)) {  // MSD column partition + shared-memory groups
-      CK(cudaMemcpyAsync(c->ckA.p, d_dst, u * 4, cudaMemcpyDeviceToDevice, c->st));
-      CK(cudaMemcpyAsync(c->cvA.p, d_count, u * 4, cudaMemcpyDeviceToDevice, c->st));
-      ColConcatSrc cs{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u, nullptr, nullptr, 0, u};
+      c->colL_dst.grow(u * 8);
+      pack_cols_kernel<<<c->sms * 8, 256, 0, c->st>>>(d_dst, d_count, u, c->colL_dst.as<uint64_t>());
+      CK_LAUNCH();
+      ++c->launches;
+      ColConcatSrc cs{c->colL_dst.as<uint64_t>(), u, nullptr, 0, u};
       cs.quad = true;
       msd_columns(c, cs, b, Dc, nullptr);
       stage_finish(c, 1);
@@ -2343,7 +2339,11 @@ int nmx_coo_stats9(nmx_ctx* c, const nmx_coo* a, int64_t out[9]) {
       CK_LAUNCH();
       const int Dc = std::min(21, std::max(11, (int)ceil_log2(u) - 9));
       if (u >= (1ull << 20)) {  // MSD partition + shared-memory grouping
-        ColConcatSrc cs{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u, nullptr, nullptr, 0, u};
+        c->colL_dst.grow(u * 8);
+        pack_cols_kernel<<<c->sms * 8, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), u,
+                                                        c->colL_dst.as<uint64_t>());
+        CK_LAUNCH();
+        ColConcatSrc cs{c->colL_dst.as<uint64_t>(), u, nullptr, 0, u};
         cs.quad = true;
         msd_columns(c, cs, 32, Dc, nullptr);
       } else {

@@ -73,7 +73,6 @@ __device__ __forceinline__ void quad_items(const KeySrc<KeyT, HAS_VAL>& s, uint6
   for (int t = 0; t < 4; ++t) ok[t] = s.load(4 * q + t, k[t], v[t]);
 }
 struct ColConcatSrc;
-__device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok);
 __device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint64_t* k, uint32_t* v, bool* ok);
 template <typename Src, typename KeyT, int NQ = 2>
 __device__ __forceinline__ void load_items(const Src& s, uint64_t q0, uint64_t qstride, KeyT* k, uint32_t* v,
@@ -579,7 +578,7 @@ struct LocSmem {
 template <bool PARTIAL>
 __global__ void __launch_bounds__(kLocThreads, 2)
     local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
-                      uint32_t* __restrict__ col_dst, uint32_t* __restrict__ col_cnt, int cshift,
+                      uint64_t* __restrict__ col, int cshift,
                       uint32_t* __restrict__ chist, unsigned long long* __restrict__ ccount,
                       unsigned long long* __restrict__ stats, SrcTable gsrc, int dsb,
                       const uint32_t* __restrict__ ngp = nullptr) {
@@ -806,8 +805,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
           s.t1cnt[hl[r]] = 0;
         }
       }
-      col_dst[pos] = (uint32_t)(key & dmask);
-      col_cnt[pos] = c;
+      col[pos] = ((key & dmask) << 32) | c;  // packed column slot (dst << 32 | count; 0 = hole)
       if (c) {
         atomicAdd(&s.chist[(uint32_t)(key & dmask) >> cshift], 1u);  // the column partition's first level
         a_links += 1;
@@ -875,63 +873,57 @@ __global__ void __launch_bounds__(kLocThreads, 2)
   if (tid < (1 << kMsdMaxLevelBits) && s.chist[tid]) atomicAdd(chist + tid, s.chist[tid]);
 }
 
-// column entries from two arrays; entries with a zero count are holes
+// (dst, count) u32 pairs -> packed column items
+__global__ void pack_cols_kernel(const uint32_t* __restrict__ dst, const uint32_t* __restrict__ cnt, uint64_t n,
+                                 uint64_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = ((uint64_t)dst[i] << 32) | cnt[i];
+}
+
+// packed column items (dst << 32 | count) from two arrays; a zero count is a hole
 struct ColConcatSrc {
-  const uint32_t* k1;
-  const uint32_t* v1;
+  const uint64_t* e1;
   uint64_t n1;
-  const uint32_t* k2;
-  const uint32_t* v2;
+  const uint64_t* e2;
   uint64_t n2;
   uint64_t n;  // n1 + n2
-  bool quad = false;  // k1 / v1 16-byte aligned
-  __device__ __forceinline__ void load_quad(uint64_t q, uint32_t* key, uint32_t* val, bool* ok) const {
-    const uint64_t i = 4 * q;
-    if (quad && i + 4 <= n1) {
-      const uint4 k4 = __ldg(reinterpret_cast<const uint4*>(k1) + q);
-      const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(v1) + q);
-      key[0] = k4.x, key[1] = k4.y, key[2] = k4.z, key[3] = k4.w;
-      val[0] = v4.x, val[1] = v4.y, val[2] = v4.z, val[3] = v4.w;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) ok[t] = val[t] != 0;
-    } else {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) ok[t] = load(i + t, key[t], val[t]);
-    }
-  }
-  __device__ __forceinline__ bool load(uint64_t i, uint32_t& key, uint32_t& val) const {
+  bool quad = false;  // e1 16-byte aligned
+  __device__ __forceinline__ bool load(uint64_t i, uint64_t& item, uint32_t& val) const {
     const bool in = i < n;
     const uint64_t j = in ? i : 0;
-    const bool first = j < n1;
-    key = first ? k1[j] : k2[j - n1];
-    val = first ? v1[j] : v2[j - n1];
-    return in && val != 0;
-  }
-  // packed column item: dst << 32 | count
-  __device__ __forceinline__ bool load(uint64_t i, uint64_t& item, uint32_t& val) const {
-    uint32_t d, c;
-    const bool ok = load(i, d, c);
-    item = ((uint64_t)d << 32) | c;
+    item = j < n1 ? e1[j] : e2[j - n1];
     val = 0;
+    return in && (uint32_t)item != 0;
+  }
+  __device__ __forceinline__ bool load(uint64_t i, uint32_t& key, uint32_t& val) const {
+    uint64_t e;
+    const bool ok = load(i, e, val);
+    key = (uint32_t)(e >> 32);
+    val = (uint32_t)e;
     return ok;
+  }
+  __device__ __forceinline__ void load_quad(uint64_t q, uint64_t* item, bool* ok) const {
+    const uint64_t i = 4 * q;
+    if (quad && i + 4 <= n1) {
+      const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(e1) + 2 * q);
+      const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(e1) + 2 * q + 1);
+      item[0] = a.x, item[1] = a.y, item[2] = b.x, item[3] = b.y;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ok[t] = (uint32_t)item[t] != 0;
+    } else {
+      uint32_t v;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ok[t] = load(i + t, item[t], v);
+    }
   }
 };
 
-__device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint32_t* k, uint32_t* v, bool* ok) {
-  s.load_quad(q, k, v, ok);
-}
 // the column partition moves packed u64 items (dst << 32 | count): one 8-byte
-// stream per level instead of two 4-byte ones (whole 128-byte runs per digit)
+// stream per level (whole 128-byte runs per digit)
 __device__ __forceinline__ void quad_items(const ColConcatSrc& s, uint64_t q, uint64_t* k, uint32_t* v, bool* ok) {
-  uint32_t d[4], c[4];
-  s.load_quad(q, d, c, ok);
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    k[t] = ((uint64_t)d[t] << 32) | c[t];
-    v[t] = 0;
-  }
+  s.load_quad(q, k, ok);
+  v[0] = v[1] = v[2] = v[3] = 0;
 }
-
 // ---------------------------------------------------------------------------
 // LOC (columns): per group of destination buckets, shared-memory hash of dst ->
 // (fan-in, packets); heavy buckets go to the LSD column path

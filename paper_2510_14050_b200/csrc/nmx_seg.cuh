@@ -398,8 +398,7 @@ __global__ void seg_plan_kernel(const uint32_t* __restrict__ loff, const uint32_
 // per warp before the global table.
 __global__ void __launch_bounds__(256) seg_emit_rows_kernel(const uint32_t* __restrict__ ccnt,
                                                            const uint64_t* __restrict__ rep, uint32_t C, int b,
-                                                           uint32_t* __restrict__ hcol_dst,
-                                                           uint32_t* __restrict__ hcol_cnt,
+                                                           uint64_t* __restrict__ hcol,
                                                            unsigned long long* __restrict__ hcount, int cshift,
                                                            uint32_t* __restrict__ chist,
                                                            unsigned long long* __restrict__ ccount,
@@ -437,8 +436,7 @@ __global__ void __launch_bounds__(256) seg_emit_rows_kernel(const uint32_t* __re
       a_links += 1;
       a_mlink = max(a_mlink, (unsigned long long)cnt);
       const unsigned long long pos = obase + at++;
-      hcol_dst[pos] = dst;
-      hcol_cnt[pos] = cnt;
+      hcol[pos] = ((uint64_t)dst << 32) | cnt;  // packed column item
       atomicAdd(&h[dst >> cshift], 1u);
       if (have && src != run_src) {  // a source boundary inside this thread's children
         gsrc.add(run_src, run_v);
