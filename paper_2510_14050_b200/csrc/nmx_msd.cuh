@@ -641,14 +641,14 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       direct = shi - slo <= kLocDirect;
     }
     // 1. hash counters (the 16-bit counter indices stay in registers for phases 2-3)
-    uint32_t kh[kLocPerThread], sh[kLocPerThread];
+    // (source counter indices are recomputed where the hashed source path needs them)
+    uint32_t kh[kLocPerThread];
 #pragma unroll
     for (int r = 0; r < kLocPerThread; ++r) {
       kh[r] = h16(kr[r]);
-      sh[r] = h16u((uint32_t)(kr[r] >> b));
       if ((uint32_t)r < nmine) {
         bm_hit(s.bml, kh[r]);
-        if (!PARTIAL && !direct) bm_hit(s.bms, sh[r]);
+        if (!PARTIAL && !direct) bm_hit(s.bms, h16u((uint32_t)(kr[r] >> b)));
       }
     }
     if (tid == 0) s.plan[cur ^ 1] = pnext;
@@ -716,7 +716,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       } else if (src == 0xFFFFFFFFu) {
         atomicAdd(&s.sp_src_pk, 1u);
         if (fresh) atomicAdd(&s.sp_src_fo, 1u);
-      } else if (bm_once(s.bms, sh[r])) {
+      } else if (bm_once(s.bms, h16u(src))) {
         st[r] |= 4;
       } else {
         const uint32_t sk = src + 1;
@@ -812,10 +812,8 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         a_valid += c;
         a_mlink = max(a_mlink, c);
       }
-      if (st[r] & 4) {
+      if (st[r] & 4) {  // single-packet source (its maxima of 1 are folded in at the end)
         a_srcs += 1;
-        a_msrc = max(a_msrc, 1u);
-        a_mfan = max(a_mfan, 1u);
       } else if (st[r] & 8) {
         const uint32_t pf = direct ? dir[hs[r]] : s.t2pf[hs[r]];
         if (PARTIAL) {
@@ -833,7 +831,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         }
       }
       s.bml[kh[r] >> 4] = 0;  // benign: every writer stores 0
-      if (!PARTIAL && !direct) s.bms[sh[r] >> 4] = 0;
+      if (!PARTIAL && !direct) s.bms[h16u((uint32_t)(key >> b)) >> 4] = 0;
     }
     if (tid == 0 && s.sp_src_pk) {
       if (PARTIAL) {
@@ -849,6 +847,10 @@ __global__ void __launch_bounds__(kLocThreads, 2)
 #pragma unroll
     for (int r = 0; r < kLocPerThread; ++r) kr[r] = kn[r];
     nmine = nnext;
+  }
+  if (a_srcs) {  // every counted source has >= 1 packet and >= 1 link
+    a_msrc = max(a_msrc, 1u);
+    a_mfan = max(a_mfan, 1u);
   }
   unsigned long long w_valid = a_valid, w_links = a_links, w_srcs = a_srcs;
 #pragma unroll
@@ -1062,9 +1064,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
 #pragma unroll
     for (int r = 0; r < kLocColPerThread; ++r) {
       if ((uint32_t)r >= nmine) continue;
-      if (stc & (1u << r)) {
+      if (stc & (1u << r)) {  // single-link destination (fan-in 1 folded in at the end)
         a_cnt += 1;
-        a_fanin = max(a_fanin, 1u);
         a_pk = max(a_pk, vr[r]);
       } else if (stc & (256u << r)) {
         a_cnt += 1;
@@ -1097,6 +1098,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     }
     nmine = nnext;
   }
+  if (a_cnt) a_fanin = max(a_fanin, 1u);
   unsigned long long w_cnt = a_cnt;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
