@@ -705,7 +705,8 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
       const size_t sm = sizeof(uint32_t) << cum[1];
       set_smem(k, sm);
       const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 3));
-      k<<<hgrid, 256, sm, c->st>>>(src, n, kb - cum[1], cum[1], dl[1], d_small + kHist, c->mhist2.as<uint32_t>(),
+      k<<<hgrid, kH12Threads, sm, c->st>>>(src, n, kb - cum[1], cum[1], dl[1], d_small + kHist,
+                                           c->mhist2.as<uint32_t>(),
                                    gcount);
     } else {
       const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));

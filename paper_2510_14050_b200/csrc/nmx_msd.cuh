@@ -271,23 +271,24 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
 // hist2 -- exactly what msd_count2_kernel would count over the level-1 output --
 // and its d1-row sums to hist1. One streaming pass instead of two.
 constexpr int kJointMaxBits = 14;
+constexpr int kH12Threads = 512;  // 3 CTAs (64 KB each) per SM: 1536 threads of loads in flight
 template <typename Src, typename KeyT>
-__global__ void __launch_bounds__(256) msd_hist12_kernel(Src src, uint64_t n, int jshift, int jbits, int d2bits,
+__global__ void __launch_bounds__(kH12Threads) msd_hist12_kernel(Src src, uint64_t n, int jshift, int jbits, int d2bits,
                                                         uint32_t* __restrict__ hist1, uint32_t* __restrict__ hist2,
                                                         unsigned long long* __restrict__ gcount) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
   const int nbins = 1 << jbits;
-  for (int i = threadIdx.x; i < nbins; i += 256) h[i] = 0;
+  for (int i = threadIdx.x; i < nbins; i += kH12Threads) h[i] = 0;
   __syncthreads();
   uint32_t c = 0;
   constexpr int U = 8;
-  const uint64_t stride = (uint64_t)gridDim.x * 256 * U;
-  for (uint64_t base = (uint64_t)blockIdx.x * 256 * U; base < n; base += stride) {
+  const uint64_t stride = (uint64_t)gridDim.x * kH12Threads * U;
+  for (uint64_t base = (uint64_t)blockIdx.x * kH12Threads * U; base < n; base += stride) {
     KeyT k[U];
     uint32_t v[U];
     bool ok[U];
-    load_items<Src, KeyT>(src, base / 4 + threadIdx.x, 256, k, v, ok);
+    load_items<Src, KeyT>(src, base / 4 + threadIdx.x, kH12Threads, k, v, ok);
     int bin[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(256) msd_hist12_kernel(Src src, uint64_t n, in
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(gcount, (unsigned long long)c);
   __syncthreads();
   // d2bits >= 5: the 32 bins of a warp share one level-1 digit
-  for (int i = threadIdx.x; i < nbins; i += 256) {
+  for (int i = threadIdx.x; i < nbins; i += kH12Threads) {
     const uint32_t x = h[i];
     if (x) atomicAdd(hist2 + i, x);
     uint32_t r = x;
@@ -339,24 +340,27 @@ __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __r
   for (int t = 0; t < kCount2Tiles; ++t) {
     const uint64_t base = base0 + (uint64_t)t * kMsdTile;
     if (base >= m) break;
+    // 32-bit index math inside the tile; one 64-bit shift per key (bshift = shift + dbits)
+    const uint32_t rem = m - base < (uint64_t)kMsdTile ? (uint32_t)(m - base) : (uint32_t)kMsdTile;
+    const KeyT* kt = keys + base;
     KeyT k[kMsdIPT];
 #pragma unroll
     for (int i = 0; i < kMsdIPT; ++i) {
-      const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
-      k[i] = idx < m ? keys[idx] : KeyT(0);
+      const uint32_t o = (uint32_t)i * kMsdThreads + tid;
+      k[i] = o < rem ? kt[o] : KeyT(0);
     }
     int bin[kMsdIPT];
 #pragma unroll
     for (int i = 0; i < kMsdIPT; ++i) {
-      const uint64_t idx = base + (uint64_t)i * kMsdThreads + tid;
+      const uint32_t o = (uint32_t)i * kMsdThreads + tid;
       bin[i] = -1;
-      if (idx < m) {
-        const uint64_t key = (uint64_t)k[i];
-        const uint64_t rel = (key >> bshift) - b1first;
+      if (o < rem) {
+        const uint64_t x = (uint64_t)k[i] >> shift;  // level-1 bucket id | digit
+        const uint64_t rel = (x >> dbits) - b1first;
         if (rel < 2)
-          bin[i] = (int)((rel << dbits) | ((key >> shift) & dmask));
+          bin[i] = (int)(((uint32_t)rel << dbits) | ((uint32_t)x & dmask));
         else
-          atomicAdd(hist2 + (uint32_t)(key >> shift), 1u);
+          atomicAdd(hist2 + (uint32_t)x, 1u);
       }
     }
     if (warp_skewed(bin[0])) {
