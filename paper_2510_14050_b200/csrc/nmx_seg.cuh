@@ -92,18 +92,22 @@ __global__ void __launch_bounds__(kMsdThreads) seg_count_kernel(const KeyT* __re
   uint32_t bd[kSegMaxRel];
 #pragma unroll
   for (int q = 0; q < kSegMaxRel; ++q) bd[q] = s_bound[q];
+  const bool one = bd[0] >= base + (uint32_t)kMsdTile;  // the whole tile in parent p0
+  int bin[kMsdIPT];
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i) {
     const uint32_t idx = base + i * kMsdThreads + tid;
-    int bin = -1;
+    bin[i] = -1;
     if (idx < m) {
       const uint32_t d = seg_digit(k[i], shift, dmask);
       uint32_t rel = 0;
+      if (!one) {
 #pragma unroll
-      for (int q = 0; q < kSegMaxRel; ++q) rel += idx >= bd[q];
+        for (int q = 0; q < kSegMaxRel; ++q) rel += idx >= bd[q];
+      }
       if (rel < kSegMaxRel) {
-        bin = (int)((rel << dbits) | d);
-        if (REP) srep[bin] = k[i];
+        bin[i] = (int)((rel << dbits) | d);
+        if (REP) srep[bin[i]] = k[i];
       } else {  // a fifth parent inside one tile (tiny parents): direct global update
         const uint32_t c = (seg_parent(poff, P, idx) << dbits) | d;
         atomicAdd(ccnt + c, 1u);
@@ -111,10 +115,23 @@ __global__ void __launch_bounds__(kMsdThreads) seg_count_kernel(const KeyT* __re
         if (REP) rep[c] = k[i];
       }
     }
-    if (SUM)
-      agg_count_sum(cnt, sum, bin, v[i]);
-    else
-      agg_count(cnt, bin);
+  }
+  // warp aggregation only for skewed warps (one hot link / destination)
+  if (warp_skewed(bin[0])) {
+#pragma unroll
+    for (int i = 0; i < kMsdIPT; ++i) {
+      if (SUM)
+        agg_count_sum(cnt, sum, bin[i], v[i]);
+      else
+        agg_count(cnt, bin[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kMsdIPT; ++i)
+      if (bin[i] >= 0) {
+        atomicAdd(&cnt[bin[i]], 1u);
+        if (SUM) atomicAdd(&sum[bin[i]], v[i]);
+      }
   }
   __syncthreads();
   for (int bin = tid; bin < nbins; bin += kMsdThreads) {
@@ -308,14 +325,18 @@ __global__ void __launch_bounds__(kMsdThreads, 5) seg_scatter_kernel(const KeyT*
   for (int q = 0; q < kSegMaxRel; ++q) bd[q] = S.bound[q];
   int bin[kMsdIPT];
   uint32_t rank[kMsdIPT];
+  // heavy parents usually cover whole tiles: then every key's parent is p0
+  const bool one = bd[0] >= base + (uint32_t)kMsdTile;
 #pragma unroll
   for (int i = 0; i < kMsdIPT; ++i) {
     bin[i] = -1;
     if (idxs[i] >= m) continue;
     const uint32_t d = seg_digit(k[i], shift, dmask);
     uint32_t rel = 0;
+    if (!one) {
 #pragma unroll
-    for (int q = 0; q < kSegMaxRel; ++q) rel += idxs[i] >= bd[q];
+      for (int q = 0; q < kSegMaxRel; ++q) rel += idxs[i] >= bd[q];
+    }
     if (rel < kSegMaxRel) {
       bin[i] = (int)((rel << dbits) | d);
     } else {
