@@ -490,6 +490,8 @@ __device__ __forceinline__ uint32_t light_count(const uint4& p) { return p.y - p
 
 constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 5 keys in registers per thread
 constexpr int kLocColPerThread = kLocColMaxKeys / kLocThreads;  // 4
+static_assert(kLocColMaxKeys <= 2048 && kLocColMaxKeys * 511 < (1 << 20),
+              "local_cols packs fan-in (bits 20+) and small-count packets (bits 0-19) in one word");
 static_assert(kLocColPerThread <= 8, "local_cols packs per-slot flags into 8-bit fields");
 constexpr int kBmWords = 4096;                             // 65536 two-bit saturating counters
 
@@ -683,12 +685,12 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       const uint64_t key = kr[r];
       const uint32_t src = (uint32_t)(key >> b);
       bool fresh;
-      if (key == ~0ull) {
-        fresh = atomicAdd(&s.sp_link, 1u) == 0;
-        if (fresh) st[r] |= 2;
-      } else if (bm_once(s.bml, kh[r])) {
+      if (bm_once(s.bml, kh[r])) {  // unique link (the all-ones key included)
         fresh = true;
         st[r] |= 1;
+      } else if (key == ~0ull) {  // key + 1 would wrap: its own counter
+        fresh = atomicAdd(&s.sp_link, 1u) == 0;
+        if (fresh) st[r] |= 2;
       } else {
         const unsigned long long kk = key + 1;
         uint32_t h = hslot(kk, kLocT1);
@@ -1034,8 +1036,12 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       const uint32_t d = kr[r];
       if (direct) {
         const uint32_t o = d - dlo;
-        if (atomicAdd(&dfan[o], 1u) == 0) stc |= 256u << r;
-        atomicAdd(&dpk[o], vr[r]);
+        // one atomic: fan-in in bits 20+ (<= 2048 entries) | packets of counts < 512
+        // (a group's sum of those stays < 2^20); larger counts add to dpk
+        const uint32_t c = vr[r];
+        const uint32_t small = c < 512u ? c : 0u;
+        if (atomicAdd(&dfan[o], (1u << 20) | small) == 0) stc |= 256u << r;
+        if (!small) atomicAdd(&dpk[o], c);
         hh[r] = o;
       } else if (d == 0xFFFFFFFFu) {
         atomicAdd(&s.spf, 1u);
@@ -1074,8 +1080,9 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       } else if (stc & (256u << r)) {
         a_cnt += 1;
         if (direct) {
-          a_fanin = max(a_fanin, dfan[hh[r]]);
-          a_pk = max(a_pk, dpk[hh[r]]);
+          const uint32_t f = dfan[hh[r]];
+          a_fanin = max(a_fanin, f >> 20);
+          a_pk = max(a_pk, (f & 0xFFFFFu) + dpk[hh[r]]);
           dfan[hh[r]] = 0;
           dpk[hh[r]] = 0;
         } else {
