@@ -133,6 +133,7 @@ struct nmx_ctx {
   int nev = 0;
   // deferred partition read-back (msd_partition(defer) -> msd_partition_wait)
   cudaEvent_t evw = nullptr;
+  bool joint_ready = false;  // streamed windows left the level-2 counts in mhist2
   uint64_t pend_bytes_per_m = 0;
   int pend_L = 0;
   float last_total_ms = 0, last_sort_ms = 0;
@@ -686,6 +687,10 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   constexpr uint64_t kItem = sizeof(KeyT) + (HAS_VAL ? 4 : 0);  // 8 B per item in and out
   unsigned long long m = pre_m;
   bool joint = false;  // level-2 counts already in mhist2 (msd_hist12_kernel)
+  if (pre_m) {
+    joint = c->joint_ready;
+    c->joint_ready = false;
+  }
   *res_k = outA;
   *res_v = voutA;
   if (pre_m) {
@@ -1080,7 +1085,7 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
 // by the top dl[0] key bits; later levels only need every tile to span few
 // level-1 buckets, which window-contiguous regions satisfy. Returns the window's
 // valid packets (host sync; the scatter stays queued).
-uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint64_t* out) {
+uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint64_t* out, uint32_t* joint) {
   int dl[8], cum[8];
   msd_level_bits(D, dl, cum);
   uint32_t* d_small = c->small.as<uint32_t>();
@@ -1090,8 +1095,16 @@ uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint6
   CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * kMsdMaxBins, c->st));
   CK(cudaMemsetAsync(gcount, 0, 8, c->st));
   const uint64_t n = ps.n;
-  const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
-  msd_hist1_kernel<PacketSrc, uint64_t><<<hgrid, 256, 0, c->st>>>(ps, n, kb - dl[0], d_small + kHist, gcount);
+  if (joint) {  // level-2 counts accumulate over the windows (hidden under the copies)
+    auto k = msd_hist12_kernel<PacketSrc, uint64_t>;
+    const size_t sm = sizeof(uint32_t) << cum[1];
+    set_smem(k, sm);
+    const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, (uint64_t)c->sms * 3));
+    k<<<hgrid, kH12Threads, sm, c->st>>>(ps, n, kb - cum[1], cum[1], dl[1], d_small + kHist, joint, gcount);
+  } else {
+    const unsigned hgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 2047) / 2048, (uint64_t)c->sms * 8));
+    msd_hist1_kernel<PacketSrc, uint64_t><<<hgrid, 256, 0, c->st>>>(ps, n, kb - dl[0], d_small + kHist, gcount);
+  }
   CK_LAUNCH();
   scan_counts(c, d_small + kHist, 1u << dl[0], c->moff.as<uint32_t>(), c->mcur.as<uint32_t>());
   unsigned long long* hm = c->scr();
@@ -1384,6 +1397,18 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
   if (!c->evs) CK(cudaEventCreate(&c->evs));
   c->small.grow(kSmallWords * sizeof(uint32_t));  // level-1 histograms before run_pipeline_msd's stage_begin
   c->keysA.grow(N * 8);  // the arena: level-1 partitions of every window, back to back
+  // levels 1 + 2 counted per window (joint histogram) when the dense split allows it
+  uint32_t* joint = nullptr;
+  {
+    int dl[8], cum[8];
+    const int L = msd_level_bits(D, dl, cum);
+    c->mhist2.grow(((size_t)(1u << D) + 8) * 4);  // the size msd_partition asks for: no reallocation
+    if (L >= 2 && cum[1] <= kJointMaxBits && dl[1] >= 5) {
+      joint = c->mhist2.as<uint32_t>();
+      CK(cudaMemsetAsync(joint, 0, sizeof(uint32_t) << cum[1], c->st));
+    }
+  }
+  c->joint_ready = false;
   DevBuf* ws[2] = {&c->ws0, &c->ws1};
   DevBuf* wd[2] = {&c->wd0, &c->wd1};
   DevBuf* wv[2] = {&c->wv0, &c->wv1};
@@ -1424,7 +1449,7 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
       const uint8_t* v = (recs || (hw.valid && hw.valid[k])) ? wv[sl]->as<uint8_t>() : nullptr;
       PacketSrc ps{ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), v, L, 0, b};
       ps.quad = true;  // slots are cudaMalloc-aligned
-      M += msd_window_level1(c, ps, 2 * b, D, c->keysA.as<uint64_t>() + M);
+      M += msd_window_level1(c, ps, 2 * b, D, c->keysA.as<uint64_t>() + M, joint);
     }
     CK(cudaEventRecord(c->evu[sl], c->st));
     used[sl] = true;
@@ -1436,6 +1461,7 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
     std::fill(out, out + S_COUNT, 0);
     return NMX_OK;
   }
+  c->joint_ready = joint != nullptr;
   run_pipeline_msd(c, nullptr, nullptr, nullptr, N, b, D, M);
   CK(cudaEventElapsedTime(&c->last_total_ms, c->evs, c->ev[c->nev - 1]));  // whole streamed call
   copy_out9(c->h_stats, out, 1);

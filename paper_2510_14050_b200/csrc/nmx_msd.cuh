@@ -16,6 +16,7 @@
 // there is no lookback chain; order inside a bucket is irrelevant to the
 // statistics.
 #pragma once
+#include <type_traits>
 #include "nmx_kernels.cuh"
 
 namespace nmx {
@@ -131,9 +132,28 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   if constexpr (LEVEL == 1) {
     load_items<Src, KeyT, kMsdIPT / 4>(src, base / 4 + tid, kMsdThreads, k, v, ok);
   } else {
+    const uint64_t wbase = base + (uint64_t)warp * 32 * kMsdIPT;
+    if constexpr (sizeof(KeyT) == 8 && !HAS_VAL && std::is_same<Src, KeySrcD<KeyT, HAS_VAL>>::value) {
+      // 16-byte loads: lane takes keys 2 lane, 2 lane + 1 of each 64-key slice
+      const uint64_t nn = src.size();
+      if (wbase + 32 * kMsdIPT <= nn) {
+        const ulonglong2* p = reinterpret_cast<const ulonglong2*>(src.keys + wbase);
 #pragma unroll
-    for (int i = 0; i < kMsdIPT; ++i)
-      ok[i] = src.load(base + (uint64_t)warp * 32 * kMsdIPT + (uint64_t)i * 32 + lane, k[i], v[i]);
+        for (int i = 0; i < kMsdIPT / 2; ++i) {
+          const ulonglong2 x = p[i * 32 + lane];
+          k[2 * i] = (KeyT)x.x;
+          k[2 * i + 1] = (KeyT)x.y;
+          ok[2 * i] = ok[2 * i + 1] = true;
+          v[2 * i] = v[2 * i + 1] = 0;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kMsdIPT; ++i) ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kMsdIPT; ++i) ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
+    }
   }
   __syncthreads();
   const uint64_t b1first = S.b1first;
@@ -247,7 +267,7 @@ __global__ void __launch_bounds__(256) msd_hist1_kernel(Src src, uint64_t n, int
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       c += ok[u];
-      bin[u] = ok[u] ? (int)((uint64_t)k[u] >> shift) : -1;
+      bin[u] = ok[u] ? (int)(((uint64_t)k[u] >> shift) & (uint64_t)(kMsdMaxBins - 1)) : -1;
     }
     if (warp_skewed(bin[0])) {  // only skewed warps pay for the per-round aggregation
 #pragma unroll
@@ -293,7 +313,8 @@ __global__ void __launch_bounds__(kH12Threads) msd_hist12_kernel(Src src, uint64
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       c += ok[u];
-      bin[u] = ok[u] ? (int)((uint64_t)k[u] >> jshift) : -1;
+      // masked: keys of out-of-range addresses (rejected after the pass) stay in bounds
+      bin[u] = ok[u] ? (int)(((uint64_t)k[u] >> jshift) & (uint64_t)(nbins - 1)) : -1;
     }
     if (warp_skewed(bin[0])) {
 #pragma unroll
