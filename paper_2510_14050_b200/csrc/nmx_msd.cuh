@@ -16,6 +16,7 @@
 // there is no lookback chain; order inside a bucket is irrelevant to the
 // statistics.
 #pragma once
+#include <cstddef>
 #include <type_traits>
 #include "nmx_kernels.cuh"
 
@@ -578,6 +579,9 @@ struct LocSmem {
   uint4 plan[2];                           // current / next group (by iteration parity)
   uint32_t chist[1 << kMsdMaxLevelBits];   // first-level histogram of the emitted column entries
 };
+static_assert(offsetof(LocSmem, t2key) == offsetof(LocSmem, bms) + 4 * kBmWords &&
+                  offsetof(LocSmem, t2pf) == offsetof(LocSmem, t2key) + 4 * kLocT2,
+              "direct source slots span bms, t2key, t2pf");
 
 // Per group (<= 2048 light keys, 4 per thread, in registers):
 //   1. every key counts its key-hash and source-hash in two 2-bit saturating
@@ -612,7 +616,8 @@ __global__ void __launch_bounds__(kLocThreads, 2)
   if (ngp) ngroups = *ngp;  // group count on the device (grid sized for the SMs)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
-  uint32_t* dir = s.bms;  // kLocDirect slots (bms, t2key, t2pf are contiguous)
+  // kLocDirect slots over bms, t2key, t2pf (contiguous members), addressed from the raw buffer
+  uint32_t* dir = reinterpret_cast<uint32_t*>(smem_raw + offsetof(LocSmem, bms));
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kBmWords; i += kLocThreads) s.bml[i] = s.bms[i] = 0;
   if (tid < (1 << kMsdMaxLevelBits)) s.chist[tid] = 0;
@@ -970,6 +975,9 @@ struct LocColSmem {
 // direct destination slots: fan-in at words [0, kLocColDirect), packets at
 // [kLocColDirect, 2 kLocColDirect) of bm .. npk (contiguous)
 constexpr uint32_t kLocColDirect = (kBmWords + 3 * kLocCT) / 2;
+static_assert(offsetof(LocColSmem, key) == offsetof(LocColSmem, bm) + 4 * kBmWords &&
+                  offsetof(LocColSmem, npk) + 4 * kLocCT == offsetof(LocColSmem, bm) + 8 * kLocColDirect,
+              "direct destination slots span bm .. npk");
 
 // Same three phases as local_rows_kernel over (dst, count) column entries: a
 // destination whose hash counter reads "once" has fan-in 1 and `count` packets.
@@ -981,8 +989,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
   if (ngp) ngroups = *ngp;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
-  uint32_t* dfan = s.bm;
-  uint32_t* dpk = s.bm + kLocColDirect;
+  uint32_t* dfan = reinterpret_cast<uint32_t*>(smem_raw + offsetof(LocColSmem, bm));  // bm .. npk contiguous
+  uint32_t* dpk = dfan + kLocColDirect;
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kBmWords; i += kLocThreads) s.bm[i] = 0;
   for (int i = tid; i < kLocCT; i += kLocThreads) {
