@@ -1031,8 +1031,8 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
     ++c->launches;
     if (t.light) {
       const uint32_t ngroups = seg_plan_groups(c, C, t.light, kLocColChunk);
-      const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 3);
-      local_cols_kernel<<<grid, kLocThreads, sizeof(LocColSmem), c->st>>>(
+      const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 4);
+      local_cols_kernel<<<grid, kLocColThreads, sizeof(LocColSmem), c->st>>>(
           light + lbase, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>(), kNoDirect);
       CK_LAUNCH();
       ++c->launches;
@@ -1066,7 +1066,7 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   {
     const uint32_t* ngp = seg_plan_groups_dev(c, 1u << Dc, cs.n, kLocColChunk);
     set_smem(local_cols_kernel, sizeof(LocColSmem));
-    local_cols_kernel<<<c->sms * 3, kLocThreads, sizeof(LocColSmem), c->st>>>(
+    local_cols_kernel<<<c->sms * 4, kLocColThreads, sizeof(LocColSmem), c->st>>>(
         ce, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp);
     CK_LAUNCH();
     ++c->launches;

@@ -511,7 +511,8 @@ __device__ __forceinline__ uint32_t light_index(const uint4& p, uint32_t j) { re
 __device__ __forceinline__ uint32_t light_count(const uint4& p) { return p.y - p.x; }
 
 constexpr int kLocPerThread = kLocMaxKeys / kLocThreads;  // 5 keys in registers per thread
-constexpr int kLocColPerThread = kLocColMaxKeys / kLocThreads;  // 4
+constexpr int kLocColThreads = 256;  // 8 entries per thread: the per-group work is shared by fewer threads
+constexpr int kLocColPerThread = kLocColMaxKeys / kLocColThreads;  // 8
 static_assert(kLocColMaxKeys <= 2048 && kLocColMaxKeys * 511 < (1 << 20),
               "local_cols packs fan-in (bits 20+) and small-count packets (bits 0-19) in one word");
 static_assert(kLocColPerThread <= 8, "local_cols packs per-slot flags into 8-bit fields");
@@ -983,7 +984,7 @@ static_assert(offsetof(LocColSmem, key) == offsetof(LocColSmem, bm) + 4 * kBmWor
 // destination whose hash counter reads "once" has fan-in 1 and `count` packets.
 // Direct destinations as in local_rows_kernel: groups whose buckets span
 // <= kLocColDirect destinations (bucket << dsb) count in slots dst - lo.
-__global__ void __launch_bounds__(kLocThreads, 3)
+__global__ void __launch_bounds__(kLocColThreads, 4)
     local_cols_kernel(const uint64_t* __restrict__ ce, const uint4* __restrict__ plan, uint32_t ngroups,
                       unsigned long long* __restrict__ stats, int dsb, const uint32_t* __restrict__ ngp = nullptr) {
   if (ngp) ngroups = *ngp;
@@ -992,8 +993,8 @@ __global__ void __launch_bounds__(kLocThreads, 3)
   uint32_t* dfan = reinterpret_cast<uint32_t*>(smem_raw + offsetof(LocColSmem, bm));  // bm .. npk contiguous
   uint32_t* dpk = dfan + kLocColDirect;
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < kBmWords; i += kLocThreads) s.bm[i] = 0;
-  for (int i = tid; i < kLocCT; i += kLocThreads) {
+  for (int i = tid; i < kBmWords; i += kLocColThreads) s.bm[i] = 0;
+  for (int i = tid; i < kLocCT; i += kLocColThreads) {
     s.key[i] = 0;
     s.nfan[i] = 0;
     s.npk[i] = 0;
@@ -1010,7 +1011,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
     const uint32_t nlight = light_count(p);
 #pragma unroll
     for (int r = 0; r < kLocColPerThread; ++r) {
-      const uint32_t j = tid + r * kLocThreads;
+      const uint32_t j = tid + r * kLocColThreads;
       if (j < nlight) {
         const uint64_t e = ce[light_index(p, j)];
         kr[r] = (uint32_t)(e >> 32);
@@ -1048,7 +1049,7 @@ __global__ void __launch_bounds__(kLocThreads, 3)
       const uint32_t nl2 = light_count(pn);
 #pragma unroll
       for (int r = 0; r < kLocColPerThread; ++r) {
-        const uint32_t j = tid + r * kLocThreads;
+        const uint32_t j = tid + r * kLocColThreads;
         if (j < nl2) {
           const uint64_t e = ce[light_index(pn, j)];
           kn[r] = (uint32_t)(e >> 32);
