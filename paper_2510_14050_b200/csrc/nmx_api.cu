@@ -562,6 +562,12 @@ std::pair<uint32_t*, uint32_t*> sort_u32_pairs(nmx_ctx* c, uint32_t* k, uint32_t
 // returns the partitioned keys / values and the number of valid items.
 // exclusive scan of n counters -> off[0..n] (off[n] = total) and cursor = off
 void scan_counts(nmx_ctx* c, const uint32_t* cnt, uint32_t n, uint32_t* off, uint32_t* cursor) {
+  if (n <= (uint32_t)kScanItems) {
+    scan_small_kernel<<<1, 256, 0, c->st>>>(cnt, n, off, cursor);
+    CK_LAUNCH();
+    ++c->launches;
+    return;
+  }
   const uint32_t nb = (n + kScanItems - 1) / kScanItems;
   c->mscan.grow(((size_t)nb + 4) * 4);
   uint32_t* bsum = c->mscan.as<uint32_t>();

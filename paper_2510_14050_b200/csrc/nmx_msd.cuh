@@ -443,6 +443,32 @@ __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* __restrict__ b
   }
   if (tid == 0) *total = carry;
 }
+// n <= kScanItems: the whole exclusive scan in one block (one launch instead of three)
+__global__ void __launch_bounds__(256) scan_small_kernel(const uint32_t* __restrict__ cnt, uint32_t n,
+                                                        uint32_t* __restrict__ off, uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t wt[kWarps + 1];
+  constexpr int PER = kScanItems / 256;
+  const uint32_t base = threadIdx.x * PER;
+  uint32_t v[PER];
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    v[q] = base + q < n ? cnt[base + q] : 0u;
+    s += v[q];
+  }
+  uint32_t tot;
+  uint32_t run = block_excl_scan<uint32_t>(s, wt, &tot);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (base + q < n) {
+      off[base + q] = run;
+      if (cursor) cursor[base + q] = run;
+    }
+    run += v[q];
+  }
+  if (threadIdx.x == 0) off[n] = tot;
+}
+
 __global__ void __launch_bounds__(256) scan_apply_kernel(const uint32_t* __restrict__ cnt, uint32_t n,
                                                         const uint32_t* __restrict__ bexcl,
                                                         const uint32_t* __restrict__ total, uint32_t* __restrict__ off,
