@@ -490,36 +490,6 @@ int msd_bits(uint64_t n, int b) {
   return D <= b ? D : 0;
 }
 
-// LSD onesweep sort of m u64 keys (kb significant bits) between two buffers
-uint64_t* sort_keys_u64(nmx_ctx* c, uint64_t* keys, uint64_t m, int kb, uint64_t* other) {
-  uint32_t* d_small = c->small.as<uint32_t>();
-  const int npass = (kb + 7) / 8;
-  CK(cudaMemsetAsync(d_small + kHist, 0, sizeof(uint32_t) * 8 * kRadix, c->st));
-  KeySrc<uint64_t, false> ks{keys, nullptr, m};
-  launch_hist(c, ks, npass, d_small);
-  bin_scan_kernel<<<1, 256, 0, c->st>>>(d_small + kHist, npass, d_small + kBase);
-  CK_LAUNCH();
-  CK(cudaMemcpyAsync(c->h_small, d_small, sizeof(uint32_t) * 8 * kRadix, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  c->grow_status(tiles_of(m, kMinPassTile) * kRadix);
-  uint64_t* cur = keys;
-  uint64_t* alt = other;
-  int idx = 0;
-  for (int p = 0; p < npass; ++p) {
-    const uint32_t* hp = c->h_small + kHist + p * kRadix;
-    bool trivial = false;
-    for (int d = 0; d < kRadix; ++d)
-      if (hp[d] == m) trivial = true;
-    if (trivial) continue;
-    KeySrc<uint64_t, false> src{cur, nullptr, m};
-    launch_pass<KeySrc<uint64_t, false>, uint64_t, false>(c, src, m, alt, nullptr, 8 * p,
-                                                          d_small + kBase + p * kRadix, d_small + kCounters + idx);
-    std::swap(cur, alt);
-    ++idx;
-  }
-  return cur;
-}
-
 // LSD onesweep sort of n (u32 key, u32 value) pairs (nbits significant key bits)
 std::pair<uint32_t*, uint32_t*> sort_u32_pairs(nmx_ctx* c, uint32_t* k, uint32_t* v, uint64_t n, int nbits,
                                                uint32_t* k2, uint32_t* v2) {
@@ -691,7 +661,6 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   uint32_t* cur = c->mcur.as<uint32_t>();
   uint32_t* off = c->moff.as<uint32_t>();
   constexpr uint64_t kItem = sizeof(KeyT) + (HAS_VAL ? 4 : 0);  // 8 B per item in and out
-  unsigned long long m = pre_m;
   bool joint = false;  // level-2 counts already in mhist2 (msd_hist12_kernel)
   if (pre_m) {
     joint = c->joint_ready;
