@@ -142,3 +142,25 @@ def test_direct_source_and_destination_slots(lib, logn, bits, law):
     else:
         s, d = orc.gen_powerlaw(logn, 0, n, space)
     _check(lib, s, d, space)
+
+
+def test_direct_destination_slots_with_large_counts(lib):
+    # direct destination slots (2^25 packets over 2^27: 2048 destinations per bucket)
+    # pack fan-in with counts < 512 in one word; counts >= 512 take the second
+    # word: a destination with 400 links of 511 packets (its bucket stays light,
+    # ~900 entries), one with counts around and far above 512
+    rng = np.random.default_rng(12)
+    space = 1 << 27
+    n_bg = 1 << 25
+    s = [rng.integers(0, space, n_bg, dtype=np.uint64).astype(np.uint32)]
+    d = [rng.integers(0, space, n_bg, dtype=np.uint64).astype(np.uint32)]
+    x, y = 123_456_789 % space, 98_765_432 % space
+    srcs = rng.choice(space, 400, replace=False).astype(np.uint32)
+    s.append(np.repeat(srcs, 511))
+    d.append(np.full(400 * 511, x, np.uint32))
+    for i, c in enumerate([512, 513, 1000, 5000, 100_000, 511, 1]):
+        s.append(np.full(c, 7 + i, np.uint32))
+        d.append(np.full(c, y, np.uint32))
+    s, d = np.concatenate(s), np.concatenate(d)
+    perm = rng.permutation(len(s))
+    _check(lib, s[perm], d[perm], space)
