@@ -112,6 +112,7 @@ struct nmx_ctx {
   int sms = 148;
   cudaStream_t st = nullptr;
   std::mutex mu;
+  DevBuf mpcnt, mpoff;  // group pieces (seg_plan_groups_dev with a bucket cap)
   DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red, ws0, ws1, wd0, wd1, wv0, wv1, wr0, wr1, rmax, anAk, anAv, anBk, anBv, anHead, anHoff, anDistinct,
@@ -792,19 +793,36 @@ SegTotals seg_level_plan(nmx_ctx* c, const KeyT* k, const uint32_t* v, uint32_t 
 // the same with the light total still on the device (stot[0], deferred
 // partition read-back): plans for at most `upper` keys; returns the device
 // group count for the grouping kernel
-const uint32_t* seg_plan_groups_dev(nmx_ctx* c, uint32_t C, uint64_t upper, uint32_t S) {
+// K > 0: groups are cut into pieces of <= K buckets (direct-slot eligibility)
+const uint32_t* seg_plan_groups_dev(nmx_ctx* c, uint32_t C, uint64_t upper, uint32_t S, uint32_t K = 0) {
   const uint64_t ng_max = (upper + S - 1) / S;
+  if (K >= C) K = 0;  // a piece could never exceed K buckets
+  const uint64_t np_max = ng_max + (K ? (uint64_t)C / K + 2 : 0);
   c->mgb.grow(((size_t)ng_max + 2) * 4);
-  c->mplan.grow(((size_t)ng_max + 2) * 16);
+  c->mplan.grow(((size_t)np_max + 2) * 16);
   uint32_t* ngp = c->stot.as<uint32_t>() + 12;
   const unsigned g1 = (unsigned)std::min<uint64_t>((ng_max + 256) / 256, (uint64_t)c->sms * 8);
   group_bounds_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), C, S, 0, c->mgb.as<uint32_t>(),
                                              c->stot.as<uint32_t>(), ngp);
   CK_LAUNCH();
-  seg_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), 0, c->mplan.as<uint4>(), ngp);
+  if (!K) {
+    seg_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), 0, c->mplan.as<uint4>(),
+                                           ngp);
+    CK_LAUNCH();
+    c->launches += 2;
+    return ngp;
+  }
+  c->mpcnt.grow(((size_t)ng_max + 2) * 4);
+  c->mpoff.grow(((size_t)ng_max + 2) * 4);
+  group_split_count_kernel<<<g1, 256, 0, c->st>>>(c->mgb.as<uint32_t>(), ngp, (uint32_t)ng_max, K,
+                                                  c->mpcnt.as<uint32_t>());
   CK_LAUNCH();
-  c->launches += 2;
-  return ngp;
+  scan_counts(c, c->mpcnt.as<uint32_t>(), (uint32_t)ng_max, c->mpoff.as<uint32_t>(), nullptr);
+  seg_plan_split_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), ngp,
+                                               c->mpoff.as<uint32_t>(), K, c->mplan.as<uint4>());
+  CK_LAUNCH();
+  c->launches += 3;
+  return c->mpoff.as<uint32_t>() + ng_max;  // the piece count (scan total)
 }
 
 uint32_t seg_plan_groups(nmx_ctx* c, uint32_t C, uint32_t light, uint32_t S) {
@@ -1039,7 +1057,8 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
                                                c->keysB.as<uint64_t>(), nullptr, &ce, &unused, prehist, &sp, 0, true);
   c->mark();  // column partition end
   {
-    const uint32_t* ngp = seg_plan_groups_dev(c, 1u << Dc, cs.n, kLocColChunk);
+    const uint32_t* ngp = seg_plan_groups_dev(c, 1u << Dc, cs.n, kLocColChunk,
+                                              b - Dc < 31 ? kLocColDirect >> (b - Dc) : 0);
     set_smem(local_cols_kernel, sizeof(LocColSmem));
     local_cols_kernel<<<c->sms * 4, kLocColThreads, sizeof(LocColSmem), c->st>>>(
         ce, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp);
@@ -1135,7 +1154,8 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   const int Dc = std::min(D, b);
   const int cshift = b - msd_first_bits(Dc);
   {
-    const uint32_t* ngp = seg_plan_groups_dev(c, nb, pre_m ? pre_m : n, kLocChunk);
+    const uint32_t* ngp = seg_plan_groups_dev(c, nb, pre_m ? pre_m : n, kLocChunk,
+                                              b - D < 31 ? kLocDirect >> (b - D) : 0);
     set_smem(local_rows_kernel<false>, sizeof(LocSmem));
     local_rows_kernel<false><<<c->sms * 2, kLocThreads, sizeof(LocSmem), c->st>>>(
         keys, c->mplan.as<uint4>(), 0, b, c->colL_dst.as<uint64_t>(), cshift, chist,
@@ -1539,7 +1559,7 @@ void nmx_destroy(nmx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  for (DevBuf* b : {&c->mscan, &c->mch, &c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
+  for (DevBuf* b : {&c->mpcnt, &c->mpoff, &c->mscan, &c->mch, &c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
                     &c->mhist2, &c->mgb, &c->mheavy, &c->mdst, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})

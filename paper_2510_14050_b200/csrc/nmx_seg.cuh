@@ -411,6 +411,35 @@ __global__ void seg_plan_kernel(const uint32_t* __restrict__ loff, const uint32_
     plan[g] = make_uint4(loff[gb[g]], loff[gb[g + 1]], gb[g], gb[g + 1]);  // key range, bucket range
 }
 
+// Groups spanning more than K buckets are cut into pieces of <= K buckets, so the
+// grouping kernels can index sources / destinations directly (a piece covers at
+// most K << dsb addresses): pieces per group, then (after an exclusive scan) the
+// piece plans. The group count is the device-side *ngp.
+__global__ void group_split_count_kernel(const uint32_t* __restrict__ gb, const uint32_t* __restrict__ ngp,
+                                         uint32_t ng_max, uint32_t K, uint32_t* __restrict__ cnt) {
+  const uint32_t ng = *ngp;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng_max; g += gridDim.x * blockDim.x)
+    cnt[g] = g < ng ? max(1u, (gb[g + 1] - gb[g] + K - 1) / K) : 0u;
+}
+__global__ void seg_plan_split_kernel(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ gb,
+                                      const uint32_t* __restrict__ ngp, const uint32_t* __restrict__ poff, uint32_t K,
+                                      uint4* __restrict__ plan) {
+  const uint32_t ng = *ngp;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+    const uint32_t b0 = gb[g], b1 = gb[g + 1];
+    uint32_t at = poff[g];
+    if (b0 == b1) {
+      plan[at] = make_uint4(loff[b0], loff[b0], b0, b0);
+      continue;
+    }
+    const uint32_t span = b1 - b0, np = (span + K - 1) / K;  // np even pieces of <= K buckets
+    for (uint32_t j = 0; j < np; ++j) {
+      const uint32_t x = b0 + (uint32_t)((uint64_t)span * j / np), y = b0 + (uint32_t)((uint64_t)span * (j + 1) / np);
+      plan[at++] = make_uint4(loff[x], loff[y], x, y);
+    }
+  }
+}
+
 // ---- final level emitters ------------------------------------------------------
 // Rows: every non-empty child is one link (key rep[c], count ccnt[c]) of a
 // heavy source: link statistics, its (dst, count) column entry (appended at
