@@ -392,6 +392,12 @@ def run_nmx(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # validation of the multi-rank flow on a one-GPU box: NMX_BENCH_DEVICE pins every
+    # rank to one device and NMX_DIST_BACKEND=gloo stages the exchanges through the host
+    # (numbers from such a run are not scaling measurements)
+    backend = os.environ.get("NMX_DIST_BACKEND", "nccl")
+    if "NMX_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["NMX_BENCH_DEVICE"])
     log2n, space, gen = CONFIGS[args.config]
     if args.log2n:
         log2n = args.log2n
@@ -402,7 +408,10 @@ def run_nmx(args) -> None:
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     ctx = _lib.context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
@@ -449,7 +458,7 @@ def run_nmx(args) -> None:
         barrier()
     ms = e0.elapsed_time(e1)
     if dist is not None:
-        mt = torch.tensor([ms], device=f"cuda:{local}")
+        mt = torch.tensor([ms], device=f"cuda:{local}" if backend == "nccl" else "cpu")
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)
         ms = float(mt.item())
     ms_per_step = ms / args.steps
@@ -480,7 +489,7 @@ def run_nmx(args) -> None:
         barrier()
         ems = e0.elapsed_time(e1) / args.e2e_steps
         if dist is not None:
-            mt = torch.tensor([ems], device=f"cuda:{local}")
+            mt = torch.tensor([ems], device=f"cuda:{local}" if backend == "nccl" else "cpu")
             dist.all_reduce(mt, op=dist.ReduceOp.MAX)
             ems = float(mt.item())
         e2e = {"value": n_total / (ems / 1e3), "unit": "packets/s", "h2d_bytes_per_step": 8 * n_total,
@@ -539,8 +548,9 @@ def run_nmx(args) -> None:
                        "frac": round(whole / peaks["hbm_gbs"], 4), "stages_ms": stage_ms,
                        "stages": (["setup", "row partition", "row groups (smem)", "heavy rows", "column partition",
                                    "column groups (smem)", "heavy columns + d2h"]
-                                  if timing_last.get("dom_name") == "msd_scatter" else
-                                  ["hist+plan", "row sort", "link/row", "col sort", "col+d2h"])},
+                                  if timing_last.get("dom_name") == "msd_scatter" and len(stage_ms) == 7 else
+                                  ["hist+plan", "row sort", "link/row", "col sort", "col+d2h"]
+                                  if len(stage_ms) == 5 else "stages of the rank's last library call")},
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),

@@ -105,17 +105,42 @@ class CudaShardOps:
         return self.torch.tensor(list(values), dtype=self.torch.int64, device=f"cuda:{self.device}")
 
 
+def _host_staged(dist, group) -> bool:
+    """gloo exchanges host tensors only: device tensors are staged through the host
+    (used to run the multi-rank flow with several ranks on one GPU; NCCL in production)."""
+    return dist.get_backend(group) == "gloo"
+
+
 def _alltoall_counts(torch, dist, counts, ops, group):
     send = ops.int64_tensor(counts)
     recv = ops.int64_tensor([0] * len(counts))
+    if _host_staged(dist, group):
+        r = torch.zeros(len(counts), dtype=torch.int64)
+        dist.all_to_all_single(r, send.cpu(), group=group)
+        return [int(x) for x in r.tolist()]
     dist.all_to_all_single(recv, send, group=group)
     return [int(x) for x in recv.tolist()]
 
 
 def _alltoall(dist, ops, send, send_counts, recv_counts, group):
     recv = ops.empty(sum(recv_counts))
+    if _host_staged(dist, group) and recv.is_cuda:
+        r = recv.new_empty(recv.shape, device="cpu")
+        dist.all_to_all_single(r, send.cpu(), output_split_sizes=recv_counts, input_split_sizes=send_counts,
+                               group=group)
+        recv.copy_(r)
+        return recv
     dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=send_counts, group=group)
     return recv
+
+
+def _all_reduce(dist, t, op, group):
+    if _host_staged(dist, group) and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
 
 
 def sharded_stats9(src, dst, valid, address_space: int, ops, group=None) -> tuple:
@@ -143,8 +168,8 @@ def sharded_stats9(src, dst, valid, address_space: int, ops, group=None) -> tupl
     mine = [int(row9[i]) for i in ROW_FIELDS] + [int(col9[i]) for i in COL_FIELDS]
     s = ops.int64_tensor([mine[i] for i in SUM_FIELDS])
     m = ops.int64_tensor([mine[i] for i in MAX_FIELDS])
-    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    _all_reduce(dist, s, dist.ReduceOp.SUM, group)
+    _all_reduce(dist, m, dist.ReduceOp.MAX, group)
     out = [0] * 9
     for i, v in zip(SUM_FIELDS, s.tolist()):
         out[i] = int(v)
