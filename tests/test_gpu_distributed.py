@@ -108,3 +108,54 @@ def test_nccl_world_of_one():
         assert nd.sharded_stats9_host(hs, hd, 1 << 32) == got
     finally:
         dist.destroy_process_group()
+
+
+def _gpu_worker(rank, world, port, cases, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_14050_b200 import distributed as nd
+    from paper_2510_14050_b200.partitioning import partition_even
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = []
+        for (gen, lg, space) in cases:
+            g = orc.gen_uniform if gen == "uniform" else orc.gen_powerlaw
+            s, d = g(5, 0, 1 << lg, space)
+            off, ln = partition_even(len(s), world).spans[rank]
+            st = torch.from_numpy(s[off:off + ln].view(np.int32).copy()).to("cuda:0")
+            dt = torch.from_numpy(d[off:off + ln].view(np.int32).copy()).to("cuda:0")
+            out.append(nd.sharded_stats9_device(st, dt, space, device=0))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_process_device_stages(world):
+    # every rank a real process running the libnmx shard stages on the one GPU; the
+    # exchanges go through gloo staged on the host (NCCL in production): the same
+    # orchestration bench.py runs under torchrun, MSD-sized shards included
+    import multiprocessing as mp
+
+    cases = [("uniform", 21, 1 << 32), ("powerlaw", 22, 1 << 32), ("powerlaw", 20, 1 << 16)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for k, (gen, lg, space) in enumerate(cases):
+        g = orc.gen_uniform if gen == "uniform" else orc.gen_powerlaw
+        s, d = g(5, 0, 1 << lg, space)
+        want = orc.stats9_packed(s, d)
+        for r in range(world):
+            assert tuple(results[r][k]) == want, (world, r, k)
