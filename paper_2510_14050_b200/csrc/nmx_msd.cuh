@@ -603,6 +603,7 @@ struct LocSmem {
   uint32_t t2key[kLocT2];  // exact source table: src + 1 (0 = empty)
   uint32_t t2pf[kLocT2];   // packets (low 16 bits) | fan-out (high 16 bits), both <= 2048
   uint32_t sp_link, sp_src_pk, sp_src_fo;  // the all-ones key / source (cannot be stored +1)
+  uint32_t one_fo;                          // PARTIAL single-source groups: fresh links
   uint4 plan[2];                           // current / next group (by iteration parity)
   uint32_t chist[1 << kMsdMaxLevelBits];   // first-level histogram of the emitted column entries
 };
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     s.t2pf[i] = 0;
   }
   if (tid == 0) {
-    s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;
+    s.sp_link = s.sp_src_pk = s.sp_src_fo = s.one_fo = 0;
     if (blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   }
   __syncthreads();
@@ -711,7 +712,22 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       }
     }
     if (tid == 0) s.plan[cur ^ 1] = pnext;
-    __syncthreads();
+    // PARTIAL: a group whose keys all share one source (a heavy source's slice)
+    // sums it once per group instead of per warp and key
+    bool single = false;
+    if constexpr (PARTIAL) {
+      const uint4 pc = s.plan[cur];
+      bool mine_same = true;
+      if (light_count(pc)) {
+        const uint32_t src0 = (uint32_t)(keys[light_index(pc, 0)] >> b);
+#pragma unroll
+        for (int r = 0; r < kLocPerThread; ++r)
+          if ((uint32_t)r < nmine && (uint32_t)(kr[r] >> b) != src0) mine_same = false;
+      }
+      single = __syncthreads_and(mine_same) != 0;
+    } else {
+      __syncthreads();
+    }
     // next group's keys: issue the loads now, they land during phases 2-3
     const uint4 p = s.plan[cur];
     const uint4 pn = s.plan[cur ^ 1];
@@ -799,6 +815,15 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       }
     }
     if constexpr (PARTIAL) {
+      if (single) {  // fresh links of the group's one source: per warp, then one shared add
+        uint32_t nf = 0;
+#pragma unroll
+        for (int r = 0; r < kLocPerThread; ++r) nf += ((uint32_t)r < nmine && (st[r] & 3u)) ? 1u : 0u;
+        nf = __reduce_add_sync(FULL, nf);
+        if (lane == 0 && nf) atomicAdd(&s.one_fo, nf);
+      }
+    }
+    if constexpr (PARTIAL) if (!single) {
       // every lane runs every r (ballots): lanes sharing the warp leader's source
       // add once; the source-table creator (bit 8) flushes it after the barrier
 #pragma unroll
@@ -892,6 +917,8 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       s.bml[kh[r] >> 4] = 0;  // benign: every writer stores 0
       if (!PARTIAL && !direct) s.bms[h16u((uint32_t)(key >> b)) >> 4] = 0;
     }
+    if (PARTIAL && single && tid == 0 && light_count(p))
+      gsrc.add((uint32_t)(keys[light_index(p, 0)] >> b), ((unsigned long long)s.one_fo << 32) | light_count(p));
     if (tid == 0 && s.sp_src_pk) {
       if (PARTIAL) {
         gsrc.add(0xFFFFFFFFu, ((unsigned long long)s.sp_src_fo << 32) | s.sp_src_pk);
@@ -902,7 +929,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
       }
     }
     __syncthreads();
-    if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = 0;  // not touched before the next barrier
+    if (tid == 0) s.sp_link = s.sp_src_pk = s.sp_src_fo = s.one_fo = 0;  // not touched before the next barrier
 #pragma unroll
     for (int r = 0; r < kLocPerThread; ++r) kr[r] = kn[r];
     nmine = nnext;
