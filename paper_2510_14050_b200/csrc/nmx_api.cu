@@ -796,7 +796,8 @@ SegTotals seg_level_plan(nmx_ctx* c, const KeyT* k, const uint32_t* v, uint32_t 
 // K > 0: groups are cut into pieces of <= K buckets (direct-slot eligibility)
 const uint32_t* seg_plan_groups_dev(nmx_ctx* c, uint32_t C, uint64_t upper, uint32_t S, uint32_t K = 0) {
   const uint64_t ng_max = (upper + S - 1) / S;
-  if (K >= C) K = 0;  // a piece could never exceed K buckets
+  // a piece could never exceed K buckets; small calls keep their few launches
+  if (K >= C || upper < (1ull << 26)) K = 0;
   const uint64_t np_max = ng_max + (K ? (uint64_t)C / K + 2 : 0);
   c->mgb.grow(((size_t)ng_max + 2) * 4);
   c->mplan.grow(((size_t)np_max + 2) * 16);
