@@ -485,8 +485,9 @@ uint32_t run_rbk(nmx_ctx* c, const KeyT* keys, const uint32_t* w, uint32_t n, in
 int msd_bits(uint64_t n, int b) {
   const char* e = getenv("NMX_PATH");
   if (e && std::string(e) == "lsd") return 0;
-  // positions carry a light flag in bit 31 (nmx_seg.cuh): at most 2^31 keys
-  if (n < (1ull << 20) || n > (1ull << 31)) return 0;
+  // positions carry a light flag in bit 31 (nmx_seg.cuh): at most 2^31 keys; from
+  // 2^16 packets the MSD path (fewer host round trips) beats the LSD sort
+  if (n < (1ull << 16) || n > (1ull << 31)) return 0;
   const int D = std::min(22, std::max(11, (int)ceil_log2(n) - 9));
   return D <= b ? D : 0;
 }

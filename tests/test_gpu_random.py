@@ -1,5 +1,5 @@
 """Seeded random configurations on the GPU against the packed-key oracle
-(SURVEY.md 8(c)): sizes across the MSD path's range, address widths from 11 to
+(SURVEY.md 8(c)): sizes across the MSD path's range (2^16 up), address widths from 11 to
 32 bits (direct and hashed grouping, light and heavy buckets), invalid packets,
 device, host-chunked and streamed entry points."""
 
@@ -21,7 +21,7 @@ def lib():
 
 def _case(seed):
     rng = np.random.default_rng(1000 + seed)
-    n = int(rng.integers(1 << 20, (1 << 23) + 1))
+    n = int(rng.integers(1 << 16, (1 << 23) + 1))
     bits = int(rng.integers(11, 33))
     space = 1 << bits
     law = "powerlaw" if seed % 2 else "uniform"
