@@ -6,10 +6,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/nmx.h"
@@ -102,7 +104,16 @@ uint32_t ceil_log2(uint64_t x) {  // x >= 1
 
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
+  // once per (device, kernel, size): the attribute call costs host time on every launch
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*>, size_t> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[std::make_tuple(dev, reinterpret_cast<const void*>(kernel))];
+  if (have >= bytes) return;
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
 }
 
 }  // namespace
