@@ -111,6 +111,14 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.post = False
+        if self.proc and not self.lines:
+            # a region shorter than the 20 ms sampling period: report the sample taken
+            # right after it (flagged) rather than none
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 1 and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.post = bool(self.lines)
         if self.proc:
             self.proc.terminate()
             try:
@@ -133,8 +141,11 @@ class ClockSampler:
             for nm, v in zip(names, parts[2:]):
                 if v.lower() in ("active", "1", "yes"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if getattr(self, "post", False):
+            out["sampled"] = "right after the timed region (shorter than the 20 ms sampling period)"
+        return out
 
 
 def cpu_port_rate(log2n: int, space: int, gen: str, reps: int = 1):
