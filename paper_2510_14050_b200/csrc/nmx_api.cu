@@ -595,6 +595,14 @@ struct SegTotals {
 void seg_classify_enqueue(nmx_ctx* c, const uint32_t* ccnt, uint32_t C, uint32_t* npoff) {
   c->scur.grow(((size_t)C + 8) * 4);
   c->sloff.grow(((size_t)C + 8) * 4);
+  c->stot.grow(64);
+  if (C <= kSegSmallC) {
+    seg_classify_small_kernel<<<1, 256, 0, c->st>>>(ccnt, C, c->stot.as<uint32_t>(), c->scur.as<uint32_t>(),
+                                                    c->sloff.as<uint32_t>(), npoff);
+    CK_LAUNCH();
+    ++c->launches;
+    return;
+  }
   const uint32_t nb = (C + kSegScanItems - 1) / kSegScanItems;
   c->sbsum.grow(((size_t)nb + 8) * 8);
   c->sbflag.grow(((size_t)nb + 8) * 4);
@@ -815,16 +823,16 @@ const uint32_t* seg_plan_groups_dev(nmx_ctx* c, uint32_t C, uint64_t upper, uint
   c->mplan.grow(((size_t)np_max + 2) * 16);
   uint32_t* ngp = c->stot.as<uint32_t>() + 12;
   const unsigned g1 = (unsigned)std::min<uint64_t>((ng_max + 256) / 256, (uint64_t)c->sms * 8);
+  if (!K) {  // bounds and plans in one pass
+    group_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), C, S, 0, c->mplan.as<uint4>(),
+                                             c->stot.as<uint32_t>(), ngp);
+    CK_LAUNCH();
+    ++c->launches;
+    return ngp;
+  }
   group_bounds_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), C, S, 0, c->mgb.as<uint32_t>(),
                                              c->stot.as<uint32_t>(), ngp);
   CK_LAUNCH();
-  if (!K) {
-    seg_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), 0, c->mplan.as<uint4>(),
-                                           ngp);
-    CK_LAUNCH();
-    c->launches += 2;
-    return ngp;
-  }
   c->mpcnt.grow(((size_t)ng_max + 2) * 4);
   c->mpoff.grow(((size_t)ng_max + 2) * 4);
   group_split_count_kernel<<<g1, 256, 0, c->st>>>(c->mgb.as<uint32_t>(), ngp, (uint32_t)ng_max, K,
@@ -834,7 +842,7 @@ const uint32_t* seg_plan_groups_dev(nmx_ctx* c, uint32_t C, uint64_t upper, uint
   seg_plan_split_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), ngp,
                                                c->mpoff.as<uint32_t>(), K, c->mplan.as<uint4>());
   CK_LAUNCH();
-  c->launches += 3;
+  c->launches += 4;
   return c->mpoff.as<uint32_t>() + ng_max;  // the piece count (scan total)
 }
 
@@ -843,12 +851,10 @@ uint32_t seg_plan_groups(nmx_ctx* c, uint32_t C, uint32_t light, uint32_t S) {
   c->mgb.grow(((size_t)ngroups + 2) * 4);
   c->mplan.grow(((size_t)ngroups + 2) * 16);
   const unsigned g1 = (unsigned)std::min<uint64_t>((ngroups + 256) / 256, (uint64_t)c->sms * 8);
-  group_bounds_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), C, S, ngroups, c->mgb.as<uint32_t>());
+  group_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), C, S, ngroups, c->mplan.as<uint4>(), nullptr,
+                                           nullptr);
   CK_LAUNCH();
-  seg_plan_kernel<<<g1, 256, 0, c->st>>>(c->sloff.as<uint32_t>(), c->mgb.as<uint32_t>(), ngroups,
-                                         c->mplan.as<uint4>());
-  CK_LAUNCH();
-  c->launches += 2;
+  ++c->launches;
   return ngroups;
 }
 

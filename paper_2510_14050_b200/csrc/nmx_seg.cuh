@@ -269,6 +269,90 @@ __global__ void __launch_bounds__(256) seg_scan_apply_kernel(const uint32_t* __r
   if (blockIdx.x == 0 && threadIdx.x == 0) loff[C] = totals[0];
 }
 
+// C <= kSegSmallC: the whole classification in one block (chunks of 4096 with
+// carries) -- one launch instead of three for small calls; same outputs + totals
+constexpr uint32_t kSegSmallC = 2 * kSegScanItems;
+__global__ void __launch_bounds__(256) seg_classify_small_kernel(const uint32_t* __restrict__ ccnt, uint32_t C,
+                                                                uint32_t* __restrict__ totals,
+                                                                uint32_t* __restrict__ cursor,
+                                                                uint32_t* __restrict__ loff,
+                                                                uint32_t* __restrict__ npoff) {
+  __shared__ unsigned long long wt64[kWarps + 1];
+  __shared__ uint32_t wt32[kWarps + 1];
+  constexpr int PER = kSegScanItems / 256;
+  unsigned long long carry64 = 0;
+  uint32_t carry32 = 0;
+  for (uint32_t chunk = 0; chunk < C; chunk += kSegScanItems) {
+    const uint32_t base = chunk + threadIdx.x * PER;
+    uint32_t sz[PER];
+    unsigned long long s = 0;
+    uint32_t f = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      sz[q] = base + q < C ? ccnt[base + q] : 0u;
+      uint64_t lb;
+      uint32_t ff;
+      seg_class(sz[q], lb, ff);
+      s += lb;
+      f += ff;
+    }
+    unsigned long long t64;
+    uint32_t t32;
+    unsigned long long run = carry64 + block_excl_scan<unsigned long long>(s, wt64, &t64);
+    uint32_t rank = carry32 + block_excl_scan<uint32_t>(f, wt32, &t32);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const uint32_t c = base + q;
+      if (c >= C) break;
+      const uint32_t lo = (uint32_t)(run & 0xFFFFFFFFull), hi = (uint32_t)(run >> 32);
+      const bool big = sz[q] > (uint32_t)kSegCap;
+      cursor[c] = big ? hi : (kLightBit | lo);
+      loff[c] = lo;
+      if (big) npoff[rank++] = hi;
+      uint64_t lb;
+      uint32_t ff;
+      seg_class(sz[q], lb, ff);
+      run += lb;
+    }
+    carry64 += t64;
+    carry32 += t32;
+  }
+  if (threadIdx.x == 0) {
+    totals[0] = (uint32_t)(carry64 & 0xFFFFFFFFull);
+    totals[1] = (uint32_t)(carry64 >> 32);
+    totals[2] = carry32;
+    loff[C] = (uint32_t)(carry64 & 0xFFFFFFFFull);
+  }
+}
+
+// group bounds and plans in one pass: group g = the buckets whose start lies in
+// [g*S, (g+1)*S) (two binary searches per group); lightp: group count from the
+// device-side light total, stored to *ngout
+__global__ void group_plan_kernel(const uint32_t* __restrict__ off, uint32_t nb, uint32_t S, uint32_t ngroups,
+                                  uint4* __restrict__ plan, const uint32_t* __restrict__ lightp,
+                                  uint32_t* __restrict__ ngout) {
+  if (lightp) {
+    ngroups = (*lightp + S - 1) / S;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ngout = ngroups;
+  }
+  auto first_at = [&](uint64_t target) {
+    uint32_t a = 0, z = nb;
+    while (a < z) {
+      const uint32_t mid = (a + z) >> 1;
+      if (off[mid] < target)
+        a = mid + 1;
+      else
+        z = mid;
+    }
+    return a;
+  };
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+    const uint32_t b0 = first_at((uint64_t)g * S);
+    const uint32_t b1 = g + 1 == ngroups ? nb : first_at((uint64_t)(g + 1) * S);
+    plan[g] = make_uint4(off[b0], off[b1], b0, b1);
+  }
+}
+
 // ---- scatter -----------------------------------------------------------------
 template <typename KeyT, bool HAS_VAL>
 struct SegSmem {
