@@ -486,15 +486,6 @@ __global__ void __launch_bounds__(kMsdThreads, 5) seg_scatter_kernel(const KeyT*
   }
 }
 
-// plan[g] = {klo, khi, 0, 0}: group g = the light children whose start lies in
-// [g*S, (g+1)*S) (gb from group_bounds_kernel over loff)
-__global__ void seg_plan_kernel(const uint32_t* __restrict__ loff, const uint32_t* __restrict__ gb, uint32_t ngroups,
-                                uint4* __restrict__ plan, const uint32_t* __restrict__ ngp = nullptr) {
-  if (ngp) ngroups = *ngp;
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x)
-    plan[g] = make_uint4(loff[gb[g]], loff[gb[g + 1]], gb[g], gb[g + 1]);  // key range, bucket range
-}
-
 // Groups spanning more than K buckets are cut into pieces of <= K buckets, so the
 // grouping kernels can index sources / destinations directly (a piece covers at
 // most K << dsb addresses): pieces per group, then (after an exclusive scan) the
