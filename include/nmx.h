@@ -208,12 +208,15 @@ int nmx_shard_cols(nmx_ctx* ctx, const uint32_t* d_dst, const uint32_t* d_count,
                    int64_t out[9]);
 
 /* Timing hooks used by bench.py: CUDA-event time (ms) of the last hot-path
- * call's whole device section, and of its dominant kernel class (the onesweep
- * passes) summed over launches, plus the number of kernels it launched. */
+ * call's whole device section, and of its sort / partition section (the MSD
+ * row partition, or the onesweep passes on the LSD path) summed over launches,
+ * plus the number of kernels it launched. */
 int nmx_last_timing(nmx_ctx* ctx, float* total_ms, float* sort_ms, int* sort_launches, int* kernel_launches);
-/* Per-stage CUDA-event times (ms) of the last hot-path call: [0] ingest histogram
- * (+ host pass planning), [1] row sort (onesweep passes), [2] fused link/row
- * kernel, [3] column sort, [4] column kernel + result copy. Returns the count. */
+/* Per-stage CUDA-event times (ms) of the last hot-path call. MSD path (7): [0] setup,
+ * [1] row partition, [2] row groups, [3] heavy rows, [4] column partition,
+ * [5] column groups, [6] heavy columns + result copy. LSD path (5): [0] ingest
+ * histogram (+ host pass planning), [1] row sort (onesweep passes), [2] fused
+ * link/row kernel, [3] column sort, [4] column kernel + result copy. Returns the count. */
 int nmx_last_stages(nmx_ctx* ctx, float* ms, int cap);
 /* The dominant kernel class of the last hot-path call (the MSD partition scatter,
  * or the onesweep pass on the LSD path): summed CUDA-event time of its launches,
