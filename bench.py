@@ -9,14 +9,18 @@ columns -> 9 int64 to host) over the whole batch.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nmx|reference]
                   [--config cfg3|cfg4|cfg2|cfg1] [--log2n L]
 
-N > 1 is launched by torchrun (one rank per GPU): the 2^30 packets are sharded
-across ranks and exchanged by owner(src) / owner(dst) over NCCL
+N > 1 runs one rank per GPU: under torchrun (the driver's launch) it uses the
+ranks torchrun made; `python bench.py --gpus N` without torchrun re-launches
+itself under `torch.distributed.run --nproc-per-node N`. The 2^30 packets are
+sharded across ranks and exchanged by owner(src) / owner(dst) over NCCL
 (paper_2510_14050_b200/distributed.py), total work fixed -> "scaling": "strong".
 
-`--impl reference` times the reference's CPU path (the numpy port in
-oracle/netmeter_oracle.py of build_matrices -> to_flat -> analyze_matrix, the
-reference is pure Python and cannot travel to the GPU box) on the host cores,
-rank 0 only, on a bounded sample of the same workload per step.
+`--impl reference` times the reference's own CPU path -- the unmodified
+`netmeter` package installed in baseline/_ref (build_matrices -> to_flat ->
+analyze_matrix + 3 x max_scan with make_group_scheduler(1, os.cpu_count())) --
+on the host cores, rank 0 only, on a bounded sample of the same workload per
+step (ids compacted outside the timed region: the reference rejects dim > 2^31).
+Without baseline/_ref it falls back to the numpy port in oracle/ (kind "port").
 """
 
 from __future__ import annotations
@@ -148,23 +152,100 @@ class ClockSampler:
         return out
 
 
-def cpu_port_rate(log2n: int, space: int, gen: str, reps: int = 1):
-    """The reference's CPU path (numpy port) on a bounded sample: packets/s."""
+def host_info() -> dict:
+    """Host cores and RAM of the box the CPU legs run on."""
+    ram = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal:"):
+                ram = round(int(ln.split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return {"os_cpu_count": os.cpu_count(), "ram_gib": ram}
+
+
+def _sample_packets(config: str, log2n: int, space: int, gen: str):
+    """The CPU legs' input sample (prepared outside the timed region): cfg1 / cfg2 are
+    generate_packets + anonymize (BASELINE configs 1-2; anonymized ids are already
+    dense), the splitmix64 configs are compacted with np.unique(return_inverse)
+    because the reference rejects dim > 2^31 (traffic.py:203-204)."""
     import numpy as np
 
     from oracle import netmeter_oracle as orc
 
+    if config in ("cfg1", "cfg2"):
+        seed = 1 if config == "cfg1" else 2
+        s, d, _ = orc.generate_packets(1 << log2n, 1 << 32, seed)
+        return orc.anonymize(s, d, seed)
     g = orc.gen_uniform if gen == "uniform" else orc.gen_powerlaw
     s, d = g(7, 0, 1 << log2n, space)
-    cs, cd, dim = orc.compact_ids(s, d)  # excluded from timing (BASELINE.md 3)
-    valid = np.ones(len(cs), dtype=bool)
-    best = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        orc.ref_stats9(cs, cd, valid, dim)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return (1 << log2n) / best, best
+    return orc.compact_ids(s, d)
+
+
+def _reference_pkg():
+    """The unmodified reference package from baseline/_ref (None if not installed)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "netmeter").is_dir():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import netmeter
+    from netmeter import analytics, resources, traffic
+
+    return netmeter, traffic, analytics, resources
+
+
+def cpu_reference_rate(config: str, log2n: int, space: int, gen: str, reps: int = 1):
+    """The reference's own path on a bounded sample: PacketStream -> build_matrices(stream,
+    len) -> to_flat -> analyze_matrix + max_scan over weights / row_sums[:,1] /
+    col_sums[:,1] (traffic.py:221-292, analytics.py:89-106) with
+    make_group_scheduler(1, os.cpu_count()) (resources.py:139-159).
+    Returns (packets/s, best seconds, stats9, kind, cores)."""
+    import numpy as np
+
+    s, d, dim = _sample_packets(config, log2n, space, gen)
+    pkg = _reference_pkg()
+    n = len(s)
+    if pkg is None:  # numpy port fallback
+        from oracle import netmeter_oracle as orc
+
+        valid = np.ones(n, dtype=bool)
+        best, st = None, None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            st = orc.ref_stats9(s, d, valid, dim)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return n / best, best, st, "port", 1
+    _, traffic, analytics, resources = pkg
+    cores = os.cpu_count() or 1
+    stream = traffic.PacketStream(s, d, np.ones(n, dtype=bool), dim)
+    best, st = None, None
+    with resources.make_group_scheduler(1, cores) as sched:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            (m,) = traffic.build_matrices(stream, window_size=n)
+            flat = traffic.to_flat(m)
+            r = analytics.analyze_matrix(flat, sched)
+            mx_link = analytics.max_scan(flat.weights, sched)
+            mx_src = analytics.max_scan(flat.row_sums[:, 1] if len(flat.row_sums) else [], sched)
+            mx_dst = analytics.max_scan(flat.col_sums[:, 1] if len(flat.col_sums) else [], sched)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+            st = (r.valid_packets, r.unique_links, mx_link, r.unique_sources, mx_src, r.max_fanout,
+                  r.unique_destinations, mx_dst, r.max_fanin)
+    return n / best, best, st, "reference", cores
+
+
+def _cpu_sample_desc(config, sample, kind, cores, secs=None, reps=None):
+    what = ("baseline/_ref netmeter (the unmodified reference): build_matrices -> to_flat -> analyze_matrix "
+            f"+ 3 x max_scan, make_group_scheduler(1, {cores}); numpy's unique/sort/bincount run on one core, "
+            "the reductions on the pool" if kind == "reference" else
+            "oracle/netmeter_oracle.py ref_stats9 (numpy port of traffic.py:197-292 + analytics.py:95-106)")
+    inp = ("generate_packets + anonymize (BASELINE input)" if config in ("cfg1", "cfg2") else
+           "the same generator, ids compacted outside the timed region")
+    t = f", best of {reps} ({secs:.2f} s each)" if secs is not None else ""
+    return f"2^{sample} packets per step, {inp}{t}; {what}"
 
 
 def run_reference(args) -> None:
@@ -172,13 +253,16 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     log2n, space, gen = CONFIGS[args.config]
+    if args.log2n:
+        log2n = args.log2n
     sample = min(log2n, args.ref_log2n)
     for _ in range(args.warmup):
-        cpu_port_rate(sample, space, gen)
+        cpu_reference_rate(args.config, sample, space, gen)
     rates = []
     t0 = time.perf_counter()
+    kind, cores = "port", 1
     for _ in range(args.steps):
-        r, _ = cpu_port_rate(sample, space, gen)
+        r, _, _, kind, cores = cpu_reference_rate(args.config, sample, space, gen)
         rates.append(r)
     wall = time.perf_counter() - t0
     value = statistics.median(rates)
@@ -187,10 +271,9 @@ def run_reference(args) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": f"{args.config}: 2^{log2n} packets {gen} over {space} addresses, summed matrix, 9 stats",
-                   "sample": f"2^{sample} packets of the same generator per step (ids compacted outside the timed region)"},
-        "cpu_baseline": {"value": value, "unit": "packets/s", "cores": 1, "kind": "port",
-                         "sample": f"2^{sample} packets/step; oracle/netmeter_oracle.py ref_stats9 = numpy port of "
-                                   "traffic.py:197-292 + analytics.py:95-106 (numpy build is single-threaded)"},
+                   "sample": f"2^{sample} packets of the same workload per step"},
+        "cpu_baseline": {"value": value, "unit": "packets/s", "cores": cores, "kind": kind,
+                         "sample": _cpu_sample_desc(args.config, sample, kind, cores), "host": host_info()},
         "e2e": {"value": value, "unit": "packets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -395,6 +478,43 @@ def run_cli(args) -> None:
     }), flush=True)
 
 
+def golden_parity(config: str, log2n: int, gen: str, stats) -> dict:
+    """The printed stats9 against the committed goldens: tests/golden/full_size.json
+    (bounded-RAM chunked CPU oracle, oracle/make_full_size.py) for the splitmix64
+    configs, tests/golden/golden.json (made by the reference package itself) for the
+    generate_packets + anonymize configs 1-2."""
+    try:
+        if gen in ("uniform", "powerlaw"):
+            g = json.loads((ROOT / "tests" / "golden" / "full_size.json").read_text())["cases"]
+            name = {(30, "uniform"): "cfg3_seed7", (30, "powerlaw"): "cfg4_seed7", (31, "uniform"): "cfg5_2^31_seed7",
+                    (32, "uniform"): "cfg5_2^32_seed7", (32, "powerlaw"): "cfg5pl_2^32_seed7"}.get((log2n, gen))
+            src = "tests/golden/full_size.json (oracle/nmx_oracle.c chunked CPU oracle)"
+        else:
+            g = json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())["cases"]
+            name = config
+            src = "tests/golden/golden.json (the reference netmeter package's own output)"
+        if name is None or name not in g:
+            return {"golden": None}
+        want = list(g[name]["stats9"])
+        return {"golden": f"{src}: {name}", "equal": list(stats) == want, "want": want}
+    except (OSError, KeyError, ValueError):
+        return {"golden": None}
+
+
+def _step_traffic(config: str, n_total: int, world: int):
+    """Measured DRAM bytes of one hot-path call from profiles/traffic_<config>.json."""
+    if world != 1:
+        return None
+    try:
+        t = json.loads((ROOT / "profiles" / f"traffic_{config}.json").read_text())
+    except Exception:
+        return None
+    if t.get("items_per_launch") != n_total or not t.get("calls"):
+        return None
+    return {"bytes": round(sum(v["dram_bytes"] for v in t["kernels"].values()) / t["calls"]),
+            "source": f"profiles/traffic_{config}.json ({t.get('report', '')}, ncu --set full, {t['calls']} call(s))"}
+
+
 def run_nmx(args) -> None:
     import torch
 
@@ -414,10 +534,16 @@ def run_nmx(args) -> None:
         log2n = args.log2n
     n_total = 1 << log2n
     kind = _lib.GEN_UNIFORM if gen == "uniform" else _lib.GEN_POWERLAW
+    if local >= torch.cuda.device_count():
+        sys.exit(f"bench: rank {rank} wants cuda:{local} but only {torch.cuda.device_count()} GPU(s) are visible "
+                 "(NMX_BENCH_DEVICE=0 NMX_DIST_BACKEND=gloo pins every rank to one GPU for a functional run)")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
+
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines: every rank's device on record
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -431,7 +557,20 @@ def run_nmx(args) -> None:
     n = base + (1 if rank < rem else 0)
     off = rank * base + min(rank, rem)
     ds, dd = _lib.DeviceArray(n, device=local), _lib.DeviceArray(n, device=local)
-    _lib.generate(kind, 7, off, n, space, ds, dd, device=local)  # this rank's shard, chunk-addressable
+    if args.config in ("cfg1", "cfg2") and not args.log2n:
+        # BASELINE configs 1-2: generate_packets(n, 2^32, seed) -> anonymize(key=seed) through
+        # the package's own API (the anonymize runs on the GPU), outside the timed region
+        from paper_2510_14050_b200 import traffic as nt
+
+        seed = 1 if args.config == "cfg1" else 2
+        st, _ = nt.anonymize(nt.generate_packets(n_total, 1 << 32, seed), key=seed)
+        space = st.address_space
+        ws, wd, _ = st.wire()
+        ds.upload(ws[off:off + n])
+        dd.upload(wd[off:off + n])
+        gen = "generate_packets + anonymize"
+    else:
+        _lib.generate(kind, 7, off, n, space, ds, dd, device=local)  # this rank's shard, chunk-addressable
 
     if world > 1:
         from paper_2510_14050_b200 import distributed as nd
@@ -509,6 +648,7 @@ def run_nmx(args) -> None:
         hs.close()
         hd.close()
 
+    parity = golden_parity(args.config, log2n, gen, stats)
     if rank != 0:
         if dist is not None:
             dist.barrier()
@@ -529,34 +669,43 @@ def run_nmx(args) -> None:
             "share_of_step": round(dom_ms / ms, 4) if ms else None,
             "note": "algorithmic bytes = 8 B read + 8 B write per item per launch; traffic per launch from ncu "
                     "dram__bytes in profiles/"}
-    # whole-step algorithmic bytes: n(16+16P) + u(36+16Pc), P = 2*ceil(b/8), Pc = ceil(b/8)
+    # whole step: DRAM bytes the step actually moves (sum over its kernels of ncu
+    # dram__bytes_read + write, profiles/traffic_<config>.json, one captured call of the
+    # same configuration) / step time. SURVEY.md 8(d)'s canonical LSD byte count
+    # (n(16+16P) + u(36+16Pc)) is reported beside it for reference only: this design moves
+    # fewer bytes than that pipeline, so dividing it by the step time is not a bandwidth.
     b = 32 if space == 1 << 32 else max(1, (space - 1).bit_length())
     P, Pc = 2 * ((b + 7) // 8), (b + 7) // 8
-    u = stats[1]
-    b_alg = n_total * (16 + 16 * P) + u * (36 + 16 * Pc)
-    whole = b_alg / (ms_per_step / 1e3) / 1e9
+    b_lsd = n_total * (16 + 16 * P) + stats[1] * (36 + 16 * Pc)
+    measured = _step_traffic(args.config, n_total, world)
+    whole = {"survey_lsd_bytes": b_lsd}
+    if measured:
+        gbs = measured["bytes"] / (ms_per_step / 1e3) / 1e9
+        whole.update({"dram_bytes_per_step": measured["bytes"], "bytes_per_packet": round(measured["bytes"] / n_total, 2),
+                      "achieved_gbs": round(gbs, 1), "frac": round(gbs / peaks["hbm_gbs"], 4),
+                      "source": measured["source"]})
 
     cpu = None
-    if not args.no_cpu and world == 1:
+    if not args.no_cpu:
         sample = min(log2n, args.cpu_log2n)
-        rate, secs = cpu_port_rate(sample, space, gen, reps=2)
-        cpu = {"value": rate, "unit": "packets/s", "cores": 1, "kind": "port",
-               "sample": f"2^{sample} packets of the {args.config} generator, best of 2 ({secs:.2f} s each); "
-                         "oracle/netmeter_oracle.py ref_stats9 (numpy port of traffic.py:197-292 + "
-                         "analytics.py:95-106; ids compacted outside the timed region)"}
+        rate, secs, _, ckind, cores = cpu_reference_rate(args.config, sample, space if args.config not in
+                                                         ("cfg1", "cfg2") else 1 << 32, gen, reps=2)
+        cpu = {"value": rate, "unit": "packets/s", "cores": cores, "kind": ckind,
+               "sample": _cpu_sample_desc(args.config, sample, ckind, cores, secs, 2), "host": host_info()}
     stage_ms = timing_last.get("stages_ms", [])
     line = {
         "metric": METRIC, "value": value, "unit": "packets/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: 2^{log2n} packets {gen} over {space} addresses (splitmix64, "
-                               "SURVEY.md 8(d)) summed into one traffic matrix, 9 statistics",
+        "config": {"workload": f"{args.config}: 2^{log2n} packets {gen} over {space} addresses "
+                               f"({'splitmix64, SURVEY.md 8(d)' if gen in ('uniform', 'powerlaw') else 'BASELINE.md'}) "
+                               "summed into one traffic matrix, 9 statistics",
                    "packets": n_total, "address_space": space, "parallelism": f"shards{world}",
                    "l2": "inputs (8 GiB) and sort buffers larger than L2; no flush needed"},
         "stats9": list(stats),
+        "parity": parity,
         "roofline": roof,
-        "whole_step": {"b_alg_bytes": b_alg, "achieved_gbs": round(whole, 1),
-                       "frac": round(whole / peaks["hbm_gbs"], 4), "stages_ms": stage_ms,
+        "whole_step": {**whole, "stages_ms": stage_ms,
                        "stages": (["setup", "row partition", "row groups (smem)", "heavy rows", "column partition",
                                    "column groups (smem)", "heavy columns + d2h"]
                                   if timing_last.get("dom_name") == "msd_scatter" and len(stage_ms) == 7 else
@@ -571,6 +720,26 @@ def run_nmx(args) -> None:
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    if parity.get("equal") is False:
+        sys.exit(f"bench: stats9 {list(stats)} differ from the golden {parity['want']}")
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch under torch.distributed.run with one
+    rank per GPU (127.0.0.1 rendezvous, a free port); rank 0 prints the JSON line.
+    NCCL's communicator set-up lines (NCCL_DEBUG=INFO, INIT) go to the log so every
+    rank's device is on record."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
 
 
 def main() -> None:
@@ -587,6 +756,10 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.exit(f"bench: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "cfg5":

@@ -136,23 +136,32 @@ def analyze_dataset(matrices, scheduler, batch_count: int = 1) -> tuple[list[Agg
     return reports, _totals6(reports)
 
 
-def _pairs_of(window):
-    if isinstance(window, PacketStream):
-        return window.src[window.valid], window.dst[window.valid], None
-    arr = np.asarray([(int(s), int(d)) for s, d in window], dtype=np.int64).reshape(-1, 2)
-    return arr[:, 0], arr[:, 1], None
-
-
 def oracle_analyze(window) -> AggregateReport:
-    """Measures straight from raw pairs, no matrix (analytics.py:133-157), computed by the
-    device hot path (use oracle/ for an independent CPU cross-check)."""
-    s, d, _ = _pairs_of(window)
-    if len(s) == 0:
-        return AggregateReport.zero()
-    space = int(max(s.max(), d.max())) + 1
-    if min(s.min(), d.min()) < 0 or space > 1 << 32:
-        raise ValueError("addresses must lie in [0, 2^32)")
-    return Stats9(*_lib.stats9(s, d, None, space)).report()
+    """The reference's independent cross-check (analytics.py:133-157): the six measures
+    straight from raw pairs with host hash sets -- no matrix, no scheduler, and
+    deliberately NOT the device hot path, so that comparing ``analyze_dataset`` /
+    ``stats9`` against it compares two independent computations (as the reference's
+    own tests do, tests/test_analytics.py:81-89). ``window``: a PacketStream (invalid
+    packets skipped) or an iterable of (src, dst) pairs; any integer addresses."""
+    if isinstance(window, PacketStream):
+        keep = window.valid
+        pairs = list(zip(window.src[keep].tolist(), window.dst[keep].tolist()))
+    else:
+        pairs = [(int(s), int(d)) for s, d in window]
+    distinct = set(pairs)
+    fanout: dict[int, int] = {}
+    fanin: dict[int, int] = {}
+    for s, d in distinct:  # every distinct link adds one to its row's and its column's nnz
+        fanout[s] = fanout.get(s, 0) + 1
+        fanin[d] = fanin.get(d, 0) + 1
+    return AggregateReport(
+        valid_packets=len(pairs),
+        unique_links=len(distinct),
+        unique_sources=len(fanout),
+        max_fanout=max(fanout.values(), default=0),
+        unique_destinations=len(fanin),
+        max_fanin=max(fanin.values(), default=0),
+    )
 
 
 # ---------------------------------------------------------------------------

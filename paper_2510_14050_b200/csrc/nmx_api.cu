@@ -1279,6 +1279,25 @@ void copy_out9(const unsigned long long* s, int64_t* out, uint64_t W) {
   for (uint64_t i = 0; i < W * S_COUNT; ++i) out[i] = (int64_t)s[i];
 }
 
+int check_maxaddr(nmx_ctx* c, uint64_t space);
+
+// Addresses >= address_space -> NMX_EINVAL before any key is packed (PacketStream,
+// traffic.py:56-64): an out-of-range address would carry bits above the 2b-bit key
+// and index past the partition's bucket arrays. Free at address_space = 2^32.
+void launch_max_addr(nmx_ctx* c, const uint32_t* s, const uint32_t* d, uint64_t n) {
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n / 4 + 255) / 256, (uint64_t)c->sms * 8));
+  max_addr_kernel<<<grid, 256, 0, c->st>>>(s, d, n, c->rmax.as<unsigned int>());
+  CK_LAUNCH();
+  ++c->launches;
+}
+int check_addresses(nmx_ctx* c, const uint32_t* s, const uint32_t* d, uint64_t n, uint64_t space) {
+  if (space >= (1ull << 32) || !n) return NMX_OK;
+  c->rmax.grow(64);
+  CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
+  launch_max_addr(c, s, d, n);
+  return check_maxaddr(c, space);
+}
+
 int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
                       uint64_t space, uint64_t window_size, int64_t* out) {
   int b;
@@ -1290,6 +1309,7 @@ int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     return NMX_OK;
   }
   if (!d_src || !d_dst) return fail(NMX_EINVAL, "null packet columns");
+  if (int r = check_addresses(c, d_src, d_dst, n, space)) return r;
   if (window_size == 0 || window_size >= n) {
     run_pipeline(c, d_src, d_dst, d_valid, n, b, 0, 1);
     copy_out9(c->h_stats, out, 1);
@@ -1362,7 +1382,8 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
     any_valid = any_valid || (hw.valid && hw.valid[k]);
   }
   if (N >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per device, got %llu", (unsigned long long)N);
-  if (recs) {
+  const bool range = recs || space < (1ull << 32);  // address range checked on the device
+  if (range) {
     c->rmax.grow(64);
     CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
   }
@@ -1460,6 +1481,8 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
       if (recs)
         unpack_records(c, wr[sl]->as<uint8_t>(), L, ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(),
                        wv[sl]->as<uint8_t>(), c->rmax.as<unsigned int>());
+      else if (range)
+        launch_max_addr(c, ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), L);
       const uint8_t* v = (recs || (hw.valid && hw.valid[k])) ? wv[sl]->as<uint8_t>() : nullptr;
       PacketSrc ps{ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), v, L, 0, b};
       ps.quad = true;  // slots are cudaMalloc-aligned
@@ -1468,7 +1491,7 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
     CK(cudaEventRecord(c->evu[sl], c->st));
     used[sl] = true;
   }
-  if (recs)
+  if (range)
     if (int r = check_maxaddr(c, space)) return r;
   if (!M) {
     CK(cudaStreamSynchronize(c->st));
@@ -1985,6 +2008,7 @@ int nmx_shard_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, uin
     std::fill(out, out + S_COUNT, 0);
     std::fill(counts, counts + nparts, 0);
     if (!n) return NMX_OK;
+    if (int r = check_addresses(c, d_src, d_dst, n, address_space)) return r;
     stage_begin(c, 1);
     if (const int D = msd_bits(n, b)) {  // MSD rows; column slots (holes skipped) by owner(dst)
       uint32_t* chist = nullptr;
@@ -2016,6 +2040,7 @@ int nmx_shard_cols(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, u
   return guarded(c, [&] {
     std::fill(out, out + S_COUNT, 0);
     if (!u) return NMX_OK;
+    if (int r = check_addresses(c, d_dst, d_dst, u, address_space)) return r;
     stage_begin(c, 1);
     c->ckA.grow(u * 4);
     c->ckB.grow(u * 4);
@@ -2077,6 +2102,7 @@ int nmx_coo_build(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const ui
       c->in_valid.grow(n);
       CK(cudaMemcpyAsync(c->in_valid.p, valid, n, cudaMemcpyHostToDevice, c->st));
     }
+    if (int r = check_addresses(c, c->in_src.as<uint32_t>(), c->in_dst.as<uint32_t>(), n, address_space)) return r;
     stage_begin(c, 1);
     PacketSrc ps{c->in_src.as<uint32_t>(), c->in_dst.as<uint32_t>(), valid ? c->in_valid.as<uint8_t>() : nullptr, n,
                  W > 1 ? window_size : 0, b};

@@ -122,4 +122,32 @@ __global__ void anon_scatter_kernel(const uint32_t* __restrict__ pos, const uint
   }
 }
 
+
+// Largest address of u32 src / dst columns (every packet, valid or not, like
+// PacketStream.__post_init__, traffic.py:56-64), max-reduced into *maxaddr. Run by
+// every device entry whose address_space is below 2^32 before any key is packed:
+// an out-of-range address would otherwise carry bits above the 2b-bit key.
+__global__ void __launch_bounds__(256) max_addr_kernel(const uint32_t* __restrict__ src,
+                                                       const uint32_t* __restrict__ dst, uint64_t n,
+                                                       unsigned int* __restrict__ maxaddr) {
+  uint32_t mx = 0;
+  const bool vec = !(((uintptr_t)src | (uintptr_t)dst) & 15);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    const uint64_t nq = n / 4;
+    for (uint64_t q = i0; q < nq; q += stride) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(src) + q);
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(dst) + q);
+      mx = max(mx, max(max(max(a.x, a.y), max(a.z, a.w)), max(max(b.x, b.y), max(b.z, b.w))));
+    }
+    for (uint64_t i = 4 * nq + i0; i < n; i += stride) mx = max(mx, max(src[i], dst[i]));
+  } else {
+    for (uint64_t i = i0; i < n; i += stride) mx = max(mx, max(src[i], dst[i]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(maxaddr, mx);
+}
+
 }  // namespace nmx

@@ -216,6 +216,9 @@ def sharded_stats9_host(src: np.ndarray, dst: np.ndarray, address_space: int, de
     """Host shard -> H2D -> sharded statistics (the multi-GPU e2e entry)."""
     import torch
 
-    s = torch.from_numpy(np.ascontiguousarray(src).view(np.int32)).to(f"cuda:{device}", non_blocking=True)
-    d = torch.from_numpy(np.ascontiguousarray(dst).view(np.int32)).to(f"cuda:{device}", non_blocking=True)
+    from ._lib import _u32_host
+
+    # range-checked u32 first (an int64 column reinterpreted as int32 would be two words per address)
+    s = torch.from_numpy(_u32_host(src).view(np.int32)).to(f"cuda:{device}", non_blocking=True)
+    d = torch.from_numpy(_u32_host(dst).view(np.int32)).to(f"cuda:{device}", non_blocking=True)
     return sharded_stats9(s, d, None, address_space, _cuda_ops(device), group)

@@ -159,3 +159,33 @@ def test_multi_process_device_stages(world):
         want = orc.stats9_packed(s, d)
         for r in range(world):
             assert tuple(results[r][k]) == want, (world, r, k)
+
+
+def test_bench_spawns_ranks():
+    """`bench.py --gpus 2` launches its own two ranks (torch.distributed.run) without an
+    external torchrun; with both ranks pinned to the one GPU and gloo staging the
+    exchanges, the printed line has n_gpus == 2 and the one-GPU statistics."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    from paper_2510_14050_b200 import _lib
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, NMX_BENCH_DEVICE="0", NMX_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "3",
+                        "--log2n", "22", "--no-cpu", "--no-e2e"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    n = 1 << 22
+    ds, dd = _lib.DeviceArray(n), _lib.DeviceArray(n)
+    try:
+        _lib.generate(_lib.GEN_UNIFORM, 7, 0, n, 1 << 32, ds, dd)
+        assert line["stats9"] == list(_lib.stats9(ds, dd, None, 1 << 32))
+    finally:
+        ds.close()
+        dd.close()

@@ -72,3 +72,40 @@ def test_full_size_paths_and_relabeling(lib, kind):
         ds.close()
         dd.close()
         torch.cuda.empty_cache()
+
+
+def _full_golden(name):
+    import json
+    from pathlib import Path
+
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "full_size.json").read_text())
+    return tuple(g["cases"][name]["stats9"])
+
+
+@pytest.mark.parametrize("name", ["cfg3_seed7", "cfg3_seed11", "cfg4_seed7", "cfg4_seed11"])
+def test_full_size_equals_chunked_oracle(lib, name):
+    """N1: bit-exact nine statistics at 2^30 packets over 2^32 against the bounded-RAM
+    chunked CPU oracle (oracle/nmx_oracle.c -> tests/golden/full_size.json), on the
+    device path and the host (pinned, streamed) path."""
+    import torch
+
+    kind = lib.GEN_UNIFORM if name.startswith("cfg3") else lib.GEN_POWERLAW
+    seed = int(name.split("seed")[1])
+    want = _full_golden(name)
+    ds, dd = lib.DeviceArray(N), lib.DeviceArray(N)
+    try:
+        lib.generate(kind, seed, 0, N, SPACE, ds, dd)
+        assert lib.stats9(ds, dd, None, SPACE) == want
+        if name == "cfg3_seed7":
+            hs, hd = lib.PinnedArray(N), lib.PinnedArray(N)
+            try:
+                hs.array[:] = ds.download()
+                hd.array[:] = dd.download()
+                assert lib.stats9(hs.array, hd.array, None, SPACE) == want
+            finally:
+                hs.close()
+                hd.close()
+    finally:
+        ds.close()
+        dd.close()
+        torch.cuda.empty_cache()

@@ -130,3 +130,34 @@ def test_reduce_quirks(lib):
     data = np.random.default_rng(1).integers(-10**12, 10**12, 1_000_003)
     assert lib.reduce_i64(data, lib.REDUCE_SUM) == int(data.sum())
     assert lib.reduce_i64(data, lib.REDUCE_MAX) == int(data.max())
+
+
+@pytest.mark.parametrize("n", [1000, 1 << 20])
+def test_out_of_range_address_rejected_on_device(n):
+    """Device columns are range-checked like PacketStream (traffic.py:56-64): an address
+    >= address_space raises ValueError (NMX_EINVAL) instead of packing a key wider than
+    2b bits (nmx_api.cu stats_device_impl)."""
+    import torch
+
+    from paper_2510_14050_b200 import _lib
+
+    space = 1 << 20
+    rng = np.random.default_rng(3)
+    s = rng.integers(0, space, n).astype(np.uint32)
+    d = rng.integers(0, space, n).astype(np.uint32)
+    ts = torch.from_numpy(s.view(np.int32)).cuda()
+    td = torch.from_numpy(d.view(np.int32)).cuda()
+    ok = _lib.stats9(ts, td, None, space)
+    assert ok == orc.stats9_packed(s, d)
+    td[n // 2] = space  # one address out of range
+    with pytest.raises(ValueError, match="address_space"):
+        _lib.stats9(ts, td, None, space)
+    with pytest.raises(ValueError, match="address_space"):
+        _lib.window_stats9(ts, td, None, space, max(1, n // 4))
+    d2 = d.copy()
+    d2[-1] = 0xFFFFFFFF
+    with pytest.raises(ValueError, match="address_space"):
+        _lib.stats9(s, d2, None, space)  # host columns (streamed path for large n)
+    # the context is still usable afterwards
+    td[n // 2] = 0
+    assert _lib.stats9(ts, td, None, space)[0] == n

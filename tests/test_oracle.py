@@ -94,3 +94,56 @@ def test_max_scan_quirks():
     assert orc._max0([]) == 0
     assert orc._max0([np.iinfo(np.int64).min]) == 0
     assert orc._max0([-5, -2, -9]) == -2
+
+
+# ---------------------------------------------------------------------------
+# the bounded-RAM chunked oracle (oracle/nmx_oracle.c) behind tests/golden/full_size.json
+# ---------------------------------------------------------------------------
+def test_chunked_oracle_pinned_to_reference_goldens(golden):
+    from oracle import big
+
+    for name, c in golden["cases"]["splitmix"].items():
+        if c["n"] > 1 << 22:
+            continue
+        kind = big.UNIFORM if c["kind"] == "uniform" else big.POWERLAW
+        for bb in (0, 3):  # one bucket, and 8 buckets (the chunked path)
+            assert big.stats9_gen(kind, c["seed"], 0, c["n"], c["space"], bucket_bits=bb) == tuple(c["stats9"]), name
+
+
+def test_chunked_oracle_generator_equals_numpy():
+    from oracle import big
+
+    for kind, gen in ((big.UNIFORM, orc.gen_uniform), (big.POWERLAW, orc.gen_powerlaw)):
+        for space in (1 << 32, 1 << 20, 300):
+            s, d = big.generate(kind, 11, 12345, 4096, space)
+            s2, d2 = gen(11, 12345, 4096, space)
+            assert np.array_equal(s, s2) and np.array_equal(d, d2)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_chunked_oracle_pairs_with_invalid(seed):
+    from oracle import big
+
+    rng = np.random.default_rng(seed)
+    n = 20000
+    hot = rng.integers(0, 1 << 32, 8, dtype=np.uint64).astype(np.uint32)
+    s = np.where(rng.random(n) < 0.3, hot[rng.integers(0, 8, n)], rng.integers(0, 1 << 32, n, dtype=np.uint64))
+    d = np.where(rng.random(n) < 0.3, hot[rng.integers(0, 8, n)], rng.integers(0, 1 << 32, n, dtype=np.uint64))
+    s, d = s.astype(np.uint32), d.astype(np.uint32)
+    v = rng.random(n) < 0.8
+    for bb in (0, 4, 9):
+        assert big.stats9_pairs(s, d, v, bucket_bits=bb) == orc.stats9_packed(s, d, v)
+    assert big.stats9_pairs(s[:0], d[:0]) == (0,) * 9
+
+
+def test_full_size_goldens_recorded():
+    """tests/golden/full_size.json (oracle/make_full_size.py) holds the BASELINE-size cases."""
+    import json
+    from pathlib import Path
+
+    p = Path(__file__).resolve().parent / "golden" / "full_size.json"
+    g = json.loads(p.read_text())
+    for name in ("cfg3_seed7", "cfg3_seed11", "cfg4_seed7", "cfg4_seed11"):
+        c = g["cases"][name]
+        assert c["n"] == 1 << 30 and c["stats9"][0] == 1 << 30
+    assert any(r.startswith("uniform_2^24") for r in g["pinned_against"]["reference_goldens"])
