@@ -750,7 +750,7 @@ def main() -> None:
     ap.add_argument("--impl", default="nmx", choices=["nmx", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--log2n", type=int, default=0)
-    ap.add_argument("--ref-log2n", type=int, default=22, help="reference-arm sample per step")
+    ap.add_argument("--ref-log2n", type=int, default=24, help="reference-arm sample per step")
     ap.add_argument("--cpu-log2n", type=int, default=24, help="cpu_baseline sample (about 10-30 s of CPU work)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")

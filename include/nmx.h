@@ -207,6 +207,33 @@ int nmx_shard_rows(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, u
 int nmx_shard_cols(nmx_ctx* ctx, const uint32_t* d_dst, const uint32_t* d_count, uint64_t u, uint64_t address_space,
                    int64_t out[9]);
 
+/* Device groups: one process driving G ranks, each an nmx_ctx (own stream and
+ * workspace) on devices[r] -- the B200 counterpart of make_group_scheduler(G)
+ * (resources.py:139-159), whose resource_count is G. Several ranks may name the same
+ * device (virtual ranks). The summed-matrix statistics of a group run the sharded
+ * pipeline of SURVEY.md 8(e) inside the library, one host thread per rank:
+ * valid packets to owner(src) = (fmix32(src) * G) >> 32, links + rows locally, unique
+ * links' (dst, count) to owner(dst), columns locally, SUM / MAX combine. Both
+ * all-to-all exchanges are peer copies (cudaMemcpyPeerAsync over NVLink / NVSwitch
+ * between distinct devices, with peer access enabled at creation) ordered by
+ * cross-stream events; bit-identical to one device for every G.
+ *  - nmx_group_stats9_device: rank r's n[r] packets are device columns of devices[r];
+ *  - nmx_group_stats9_host: one host stream split by partition_even into G spans
+ *    (partitioning.py:62-70), each copied to its rank in batch_count chunks (the
+ *    reference's b_n sub-batches, partitioning.py:89-98);
+ *  - nmx_group_context: rank r's context (for nmx_malloc etc. on its device);
+ *  - nmx_group_last_exchange: bytes moved by the last call's two exchanges. */
+typedef struct nmx_group nmx_group;
+int nmx_group_create(const int* devices, int g, nmx_group** out);
+void nmx_group_destroy(nmx_group* grp);
+int nmx_group_size(const nmx_group* grp, int* g);
+int nmx_group_context(nmx_group* grp, int rank, nmx_ctx** out);
+int nmx_group_stats9_device(nmx_group* grp, const uint32_t* const* d_src, const uint32_t* const* d_dst,
+                            const uint8_t* const* d_valid, const uint64_t* n, uint64_t address_space, int64_t out[9]);
+int nmx_group_stats9_host(nmx_group* grp, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                          uint64_t address_space, uint64_t batch_count, int64_t out[9]);
+int nmx_group_last_exchange(nmx_group* grp, uint64_t* bytes1, uint64_t* bytes2);
+
 /* Timing hooks used by bench.py: CUDA-event time (ms) of the last hot-path
  * call's whole device section, and of its sort / partition section (the MSD
  * row partition, or the onesweep passes on the LSD path) summed over launches,

@@ -73,6 +73,13 @@ SIGNATURES = {
     "nmx_partition_packets": (C.c_int, [_VP, _VP, _VP, _VP, _U64, C.c_int, _VP, _VP, _VP]),
     "nmx_shard_rows": (C.c_int, [_VP, _VP, _VP, _U64, _U64, C.c_int, _VP, _VP, _VP, _VP]),
     "nmx_shard_cols": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_group_create": (C.c_int, [_VP, C.c_int, C.POINTER(_VP)]),
+    "nmx_group_destroy": (None, [_VP]),
+    "nmx_group_size": (C.c_int, [_VP, C.POINTER(C.c_int)]),
+    "nmx_group_context": (C.c_int, [_VP, C.c_int, C.POINTER(_VP)]),
+    "nmx_group_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
+    "nmx_group_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
+    "nmx_group_last_exchange": (C.c_int, [_VP, C.POINTER(_U64), C.POINTER(_U64)]),
     "nmx_last_kernel_class": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_int), C.POINTER(_U64), C.c_char_p,
                                          C.c_int]),
     "nmx_last_stages": (C.c_int, [_VP, C.POINTER(C.c_float), C.c_int]),
@@ -126,11 +133,15 @@ def check(rc: int) -> None:
 class Context:
     """One device + one CUDA stream (include/nmx.h nmx_ctx)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, handle=None, owner=None):
         lib = load()
-        h = C.c_void_p()
-        check(lib.nmx_create(int(device), C.byref(h)))
+        if handle is None:
+            h = C.c_void_p()
+            check(lib.nmx_create(int(device), C.byref(h)))
+        else:  # a group rank's context: owned (and destroyed) by the group
+            h = handle
         self._h = h
+        self._owner = owner
         self.device = int(device)
         self._lib = lib
 
@@ -139,9 +150,9 @@ class Context:
         return self._h
 
     def close(self) -> None:
-        if self._h:
+        if self._h and self._owner is None:
             self._lib.nmx_destroy(self._h)
-            self._h = C.c_void_p()
+        self._h = C.c_void_p()
 
     def __del__(self):  # pragma: no cover - interpreter shutdown ordering
         try:
@@ -169,16 +180,101 @@ class Context:
 
 _contexts: dict[int, Context] = {}
 _ctx_lock = threading.Lock()
+_current = threading.local()
 
 
 def context(device: int = 0) -> Context:
-    """Process-wide cached context per device."""
+    """The calling thread's bound context (``using``), else the process-wide cached
+    context of ``device``."""
+    c = getattr(_current, "ctx", None)
+    if c is not None:
+        return c
     with _ctx_lock:
         c = _contexts.get(device)
         if c is None:
             c = Context(device)
             _contexts[device] = c
         return c
+
+
+class using:
+    """``with using(ctx):`` routes this thread's library calls to ``ctx`` (a group
+    rank's own stream and workspace) whatever device argument they carry."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def __enter__(self):
+        self.prev = getattr(_current, "ctx", None)
+        _current.ctx = self.ctx
+        return self.ctx
+
+    def __exit__(self, *exc):
+        _current.ctx = self.prev
+
+
+class Group:
+    """G ranks (nmx_group), rank r on CUDA device ``devices[r]`` (several ranks may share
+    a device). Owns one context per rank; the sharded statistics run in the library."""
+
+    def __init__(self, devices):
+        lib = load()
+        devs = [int(d) for d in devices]
+        arr = (C.c_int * len(devs))(*devs)
+        h = C.c_void_p()
+        check(lib.nmx_group_create(arr, len(devs), C.byref(h)))
+        self._h = h
+        self._lib = lib
+        self.devices = devs
+        self.contexts = []
+        for r, d in enumerate(devs):
+            ch = C.c_void_p()
+            check(lib.nmx_group_context(h, r, C.byref(ch)))
+            self.contexts.append(Context(d, handle=ch, owner=self))
+
+    @property
+    def size(self) -> int:
+        return len(self.devices)
+
+    def stats9_host(self, src, dst, valid=None, address_space: int = 1 << 32, batch_count: int = 1) -> tuple:
+        s, d, v = _u32_host(src), _u32_host(dst), _valid_host(valid)
+        if len(s) != len(d) or (v is not None and len(v) != len(s)):
+            raise ValueError("src, dst and valid must have equal lengths")
+        out = np.zeros(9, dtype=np.int64)
+        check(self._lib.nmx_group_stats9_host(self._h, _ptr(s), _ptr(d), _ptr(v), len(s), int(address_space),
+                                              int(batch_count), out.ctypes.data))
+        return tuple(int(x) for x in out)
+
+    def stats9_device(self, srcs, dsts, address_space: int = 1 << 32, valids=None) -> tuple:
+        """Rank r's packets: device columns srcs[r] / dsts[r] on devices[r]."""
+        g = self.size
+        if len(srcs) != g or len(dsts) != g:
+            raise ValueError(f"need one (src, dst) pair per rank ({g})")
+        sp = (C.c_void_p * g)(*[_ptr(a) for a in srcs])
+        dp = (C.c_void_p * g)(*[_ptr(a) for a in dsts])
+        vp = (C.c_void_p * g)(*[_ptr(a) for a in valids]) if valids is not None else None
+        ns = (C.c_uint64 * g)(*[int(a.numel()) for a in srcs])
+        out = np.zeros(9, dtype=np.int64)
+        check(self._lib.nmx_group_stats9_device(self._h, sp, dp, vp, ns, int(address_space), out.ctypes.data))
+        return tuple(int(x) for x in out)
+
+    def last_exchange(self) -> tuple[int, int]:
+        a, b = C.c_uint64(), C.c_uint64()
+        check(self._lib.nmx_group_last_exchange(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+    def close(self) -> None:
+        if self._h:
+            for c in self.contexts:
+                c._h = C.c_void_p()
+            self._lib.nmx_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def device_count() -> int:

@@ -3,9 +3,9 @@
 Reference-compatible entry points (same names, argument meaning and errors):
 ``sum_reduce``, ``max_scan``, ``analyze_matrix``, ``analyze_dataset``,
 ``oracle_analyze``, ``AggregateReport``. Their reductions run in libnmx.so
-(``nmx_reduce_i64``); the scheduler argument only contributes its
-``resource_count`` / ``batch_count`` validation because a device reduction has
-no per-resource partial slots to fill.
+(``nmx_reduce_i64``); a device-group scheduler (resources.py) spreads views and
+windows over its ranks, and ``batch_count`` chunks each rank's share, as the
+reference's resources / batches do.
 
 The hot path (BASELINE.json north star) is ``stats9`` / ``analyze_summed``:
 packets -> summed traffic matrix -> the nine Graph Challenge statistics, with
@@ -20,6 +20,7 @@ from dataclasses import asdict, dataclass
 import numpy as np
 
 from . import _lib
+from .partitioning import even_spans
 from .traffic import FlatContainers, PacketStream, TrafficMatrix, to_flat
 
 _INT64_MIN = np.iinfo(np.int64).min
@@ -91,17 +92,59 @@ def _device_of(scheduler) -> int:
     return int(getattr(scheduler, "device", 0) or 0)
 
 
+def _group(scheduler):
+    """The scheduler as a DeviceGroup (None for an unknown SchedulerLike)."""
+    from .resources import DeviceGroup
+
+    return scheduler if isinstance(scheduler, DeviceGroup) else None
+
+
+def _reduce(a: np.ndarray, scheduler, batch_count: int, op: int) -> int:
+    """Per-resource partials like the reference's _batched_reduce (analytics.py:54-81):
+    the view split by partition_even over the group's ranks, each rank's span in
+    batch_count chunks reduced on its own device context, partials combined here
+    (SUM wraps mod 2^64 as int64; MAX keeps the INT64_MIN empty sentinel)."""
+    g = _group(scheduler)
+    if g is None or (g.resource_count == 1 and batch_count == 1) or a.size < 2:
+        if g is not None:
+            with _lib.using(g.native.contexts[0]):
+                return _lib.reduce_i64(a, op)
+        return _lib.reduce_i64(a, op, device=_device_of(scheduler))
+
+    def rank_part(r, lo, hi):
+        return [_lib.reduce_i64(a[o:o + ln], op) for o, ln in even_spans(lo, hi - lo, batch_count) if ln]
+
+    parts = [v for chunk in g.map_ranks(len(a), rank_part) for v in chunk]
+    if op == _lib.REDUCE_SUM:
+        t = sum(parts) & 0xFFFFFFFFFFFFFFFF
+        return t - (1 << 64) if t >> 63 else t
+    return max(parts, default=_INT64_MIN)
+
+
 def sum_reduce(data, scheduler, batch_count: int = 1) -> int:
     """Sum of an integer view (int64 wrap-around, analytics.py:84-86); empty -> 0."""
-    a = _check_view(data, batch_count)
-    return _lib.reduce_i64(a, _lib.REDUCE_SUM, device=_device_of(scheduler))
+    return _reduce(_check_view(data, batch_count), scheduler, batch_count, _lib.REDUCE_SUM)
 
 
 def max_scan(data, scheduler, batch_count: int = 1) -> int:
     """Maximum of an integer view; empty view (and INT64_MIN) -> 0 (analytics.py:89-92)."""
-    a = _check_view(data, batch_count)
-    peak = _lib.reduce_i64(a, _lib.REDUCE_MAX, device=_device_of(scheduler))
+    peak = _reduce(_check_view(data, batch_count), scheduler, batch_count, _lib.REDUCE_MAX)
     return 0 if peak == _INT64_MIN else peak
+
+
+def _report_local(flat: FlatContainers) -> AggregateReport:
+    """analyze_matrix on the calling thread's context (one rank of a group)."""
+    w = _check_view(flat.weights, 1)
+    fo = _lib.reduce_i64(_check_view(flat.out_degrees, 1), _lib.REDUCE_MAX)
+    fi = _lib.reduce_i64(_check_view(flat.in_degrees, 1), _lib.REDUCE_MAX)
+    return AggregateReport(
+        valid_packets=_lib.reduce_i64(w, _lib.REDUCE_SUM),
+        unique_links=len(flat.edges),
+        unique_sources=len(flat.row_sums),
+        max_fanout=0 if fo == _INT64_MIN else fo,
+        unique_destinations=len(flat.col_sums),
+        max_fanin=0 if fi == _INT64_MIN else fi,
+    )
 
 
 def analyze_matrix(flat: FlatContainers, scheduler, batch_count: int = 1) -> AggregateReport:
@@ -128,11 +171,25 @@ def _totals6(reports) -> AggregateReport:
 
 
 def analyze_dataset(matrices, scheduler, batch_count: int = 1) -> tuple[list[AggregateReport], AggregateReport]:
-    """Per-matrix reports plus dataset totals (analytics.py:109-130)."""
-    reports = []
-    for item in matrices:
-        flat = to_flat(item, device=_device_of(scheduler)) if isinstance(item, TrafficMatrix) else item
-        reports.append(analyze_matrix(flat, scheduler, batch_count))
+    """Per-matrix reports plus dataset totals (analytics.py:109-130). With a device
+    group the matrices are spread over its ranks by partition_even(len, G) (SURVEY.md
+    8(e): windows shard with no collective), each rank building its containers and
+    reports on its own device context concurrently."""
+    if batch_count < 1:
+        raise ValueError("batch_count must be >= 1")
+    items = list(matrices)
+    g = _group(scheduler)
+    if g is None or g.resource_count == 1 or len(items) < 2:
+        reports = []
+        for item in items:
+            flat = to_flat(item, device=_device_of(scheduler)) if isinstance(item, TrafficMatrix) else item
+            reports.append(analyze_matrix(flat, scheduler, batch_count))
+        return reports, _totals6(reports)
+
+    def rank_part(r, lo, hi):
+        return [_report_local(to_flat(it) if isinstance(it, TrafficMatrix) else it) for it in items[lo:hi]]
+
+    reports = [rep for chunk in g.map_ranks(len(items), rank_part) for rep in chunk]
     return reports, _totals6(reports)
 
 
@@ -167,16 +224,30 @@ def oracle_analyze(window) -> AggregateReport:
 # ---------------------------------------------------------------------------
 # the north-star hot path
 # ---------------------------------------------------------------------------
-def stats9(stream: PacketStream, device: int = 0) -> Stats9:
+def stats9(stream: PacketStream, device: int = 0, scheduler=None, batch_count: int = 1) -> Stats9:
     """Nine statistics of the matrix summed over all valid packets of ``stream``
-    (= build_matrices(stream, len(stream)) -> to_flat -> analyze_matrix + 3 max_scan)."""
+    (= build_matrices(stream, len(stream)) -> to_flat -> analyze_matrix + 3 max_scan).
+
+    ``scheduler``: a device group (make_group_scheduler(G)) shards the stream over its G
+    ranks -- partition_even spans, ``batch_count`` H2D chunks per rank, owner(src) /
+    owner(dst) exchanges inside libnmx.so (nmx_group_stats9_host); bit-identical for
+    every G and batch_count."""
+    if batch_count < 1:
+        raise ValueError("batch_count must be >= 1")
     if len(stream) == 0:
         return Stats9.zero()
     s, d, v = stream.wire()
-    return Stats9(*_lib.stats9(s, d, None if stream.valid.all() else v, stream.address_space, device=device))
+    v = None if stream.valid.all() else v
+    g = _group(scheduler)
+    if g is not None and (g.resource_count > 1 or batch_count > 1):
+        return Stats9(*g.native.stats9_host(s, d, v, stream.address_space, batch_count))
+    if g is not None:
+        with _lib.using(g.native.contexts[0]):
+            return Stats9(*_lib.stats9(s, d, v, stream.address_space))
+    return Stats9(*_lib.stats9(s, d, v, stream.address_space, device=device))
 
 
-def analyze_summed(streams, device: int = 0) -> Stats9:
+def analyze_summed(streams, device: int = 0, scheduler=None, batch_count: int = 1) -> Stats9:
     """Statistics of sum_t A_t over several streams (windows) of one address space:
     the element-wise sum of count matrices is the count matrix of the concatenated
     packets, so one device pass over all of them is exact."""
@@ -186,22 +257,46 @@ def analyze_summed(streams, device: int = 0) -> Stats9:
     space = max(s.address_space for s in streams)
     cat = PacketStream(np.concatenate([s.src for s in streams]), np.concatenate([s.dst for s in streams]),
                        np.concatenate([s.valid for s in streams]), space)
-    return stats9(cat, device=device)
+    return stats9(cat, device=device, scheduler=scheduler, batch_count=batch_count)
 
 
-def analyze_windows(stream: PacketStream, window_size: int, device: int = 0) -> tuple[list[Stats9], Stats9]:
+def _totals9(per) -> Stats9:
+    sums = {0, 1, 3, 6}
+    tot = [sum(r.astuple()[k] for r in per) if k in sums else max((r.astuple()[k] for r in per), default=0)
+           for k in range(9)]
+    return Stats9(*tot)
+
+
+def analyze_windows(stream: PacketStream, window_size: int, device: int = 0,
+                    scheduler=None) -> tuple[list[Stats9], Stats9]:
     """Per-window nine statistics with analyze_dataset totals (sums of the counting
-    measures, maxima of the max measures; analytics.py:122-129)."""
+    measures, maxima of the max measures; analytics.py:122-129). A device group
+    spreads the windows over its ranks (partition_even(window_count, G)), no collective."""
     if window_size < 1:
         raise ValueError("window_size must be >= 1")
     if len(stream) == 0:
         return [], Stats9.zero()
     s, d, v = stream.wire()
-    rows = _lib.window_stats9(s, d, v, stream.address_space, window_size, device=device)
-    per = [Stats9(*map(int, r)) for r in rows]
-    sums = {0, 1, 3, 6}
-    tot = [sum(r.astuple()[k] for r in per) if k in sums else max(r.astuple()[k] for r in per) for k in range(9)]
-    return per, Stats9(*tot)
+    g = _group(scheduler)
+    nwin = (len(stream) + window_size - 1) // window_size
+    if g is None or g.resource_count == 1 or nwin < 2:
+        if g is not None:
+            with _lib.using(g.native.contexts[0]):
+                rows = _lib.window_stats9(s, d, v, stream.address_space, window_size)
+        else:
+            rows = _lib.window_stats9(s, d, v, stream.address_space, window_size, device=device)
+        per = [Stats9(*map(int, r)) for r in rows]
+        return per, _totals9(per)
+
+    def rank_part(r, lo, hi):
+        if hi <= lo:
+            return []
+        a, b = lo * window_size, min(hi * window_size, len(stream))
+        rows = _lib.window_stats9(s[a:b], d[a:b], v[a:b], stream.address_space, window_size)
+        return [Stats9(*map(int, row)) for row in rows]
+
+    per = [r for chunk in g.map_ranks(nwin, rank_part) for r in chunk]
+    return per, _totals9(per)
 
 
 def stats9_file(path, address_space: int | None = None, window_packets: int = 1 << 25, device: int = 0) -> Stats9:

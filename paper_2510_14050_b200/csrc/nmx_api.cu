@@ -2,6 +2,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1543,6 +1546,279 @@ int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const 
                            valid ? c->in_valid.as<uint8_t>() : nullptr, n, space, window_size, out);
 }
 
+// ---- multi-GPU shard stages; callers hold the context lock ----
+// link + row statistics (fields 0-5) of the packets whose sources this rank owns,
+// and its unique links' (dst, count) column entries routed by owner(dst)
+int shard_rows_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, uint64_t space, int nparts,
+                    uint32_t* d_out_dst, uint32_t* d_out_count, uint64_t* counts, int64_t* out) {
+  int b;
+  if (int r = check_space(space, b)) return r;
+  std::fill(out, out + S_COUNT, 0);
+  std::fill(counts, counts + nparts, 0);
+  if (!n) return NMX_OK;
+  if (int r = check_addresses(c, d_src, d_dst, n, space)) return r;
+  stage_begin(c, 1);
+  if (const int D = msd_bits(n, b)) {  // MSD rows; column slots (holes skipped) by owner(dst)
+    uint32_t* chist = nullptr;
+    const ColConcatSrc cs = msd_rows(c, d_src, d_dst, nullptr, n, b, D, 0, &chist);
+    if (cs.n) {
+      ColConcatPart it{cs, d_out_dst, d_out_count};
+      partition_items(c, it, cs.n, nparts, counts);
+    }
+  } else {
+    PacketSrc ps{d_src, d_dst, nullptr, n, 0, b};
+    const RowsOut r = stage_rows(c, ps, b, 0);
+    if (r.u) {
+      ColPart it{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), d_out_dst, d_out_count};
+      partition_items(c, it, r.u, nparts, counts);
+    }
+  }
+  stage_finish(c, 1);
+  copy_out9(c->h_stats, out, 1);
+  return NMX_OK;
+}
+
+// column statistics (fields 6-8) of the received column entries of this rank's destinations
+int shard_cols_impl(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, uint64_t u, uint64_t space,
+                    int64_t* out) {
+  int b;
+  if (int r = check_space(space, b)) return r;
+  std::fill(out, out + S_COUNT, 0);
+  if (!u) return NMX_OK;
+  if (int r = check_addresses(c, d_dst, d_dst, u, space)) return r;
+  stage_begin(c, 1);
+  c->ckA.grow(u * 4);
+  c->ckB.grow(u * 4);
+  c->cvA.grow(u * 4);
+  c->cvB.grow(u * 4);
+  if (const int Dc = msd_bits(u, b)) {  // MSD column partition + shared-memory groups
+    c->colL_dst.grow(u * 8);
+    pack_cols_kernel<<<c->sms * 8, 256, 0, c->st>>>(d_dst, d_count, u, c->colL_dst.as<uint64_t>());
+    CK_LAUNCH();
+    ++c->launches;
+    ColConcatSrc cs{c->colL_dst.as<uint64_t>(), u, nullptr, 0, u};
+    cs.quad = true;
+    msd_columns(c, cs, b, Dc, nullptr);
+    stage_finish(c, 1);
+    copy_out9(c->h_stats, out, 1);
+    return NMX_OK;
+  }
+  if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
+    CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+  CK(cudaMemcpyAsync(c->ckA.p, d_dst, u * 4, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(c->cvA.p, d_count, u * 4, cudaMemcpyDeviceToDevice, c->st));
+  const int ncolpass = (b + 7) / 8;
+  uint32_t* d_small = c->small.as<uint32_t>();
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((u + 1023) / 1024, (uint64_t)c->sms * 8));
+  switch (ncolpass) {
+    case 1: hist_u32_kernel<1><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+    case 2: hist_u32_kernel<2><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+    case 3: hist_u32_kernel<3><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+    default: hist_u32_kernel<4><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
+  }
+  CK_LAUNCH();
+  ++c->launches;
+  stage_cols(c, (uint32_t)u, b, 0, false);
+  stage_finish(c, 1);
+  copy_out9(c->h_stats, out, 1);
+  return NMX_OK;
+}
+
+// ---- device groups: one process driving G contexts ----------
+// A group is G ranks, each an nmx_ctx (its own stream and workspace) on a device;
+// virtual ranks may share a device. nmx_group_stats9_* run one host thread per
+// rank through the owner(src) / owner(dst) pipeline of distributed.py, with the two
+// all-to-all exchanges done in-library as peer copies (cudaMemcpyPeerAsync: NVLink /
+// NVSwitch between distinct B200s, a device-local copy between virtual ranks) and
+// cross-stream events instead of a host round trip through NCCL.
+
+// barrier that a failing rank can abort (the others then unwind instead of hanging)
+struct GroupBarrier {
+  std::mutex mu;
+  std::condition_variable cv;
+  int n = 0, waiting = 0;
+  uint64_t gen = 0;
+  bool aborted = false;
+  void arrive() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (aborted) throw std::runtime_error("group aborted by another rank");
+    const uint64_t g = gen;
+    if (++waiting == n) {
+      waiting = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    cv.wait(lk, [&] { return gen != g || aborted; });
+    if (aborted) throw std::runtime_error("group aborted by another rank");
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
+struct GroupRank {
+  nmx_ctx* ctx = nullptr;
+  DevBuf ps, pd;    // exchange 1 send: packets by owner(src)
+  DevBuf rs, rd;    // exchange 1 receive
+  DevBuf cs, cc;    // exchange 2 send: column entries by owner(dst)
+  DevBuf qs, qc;    // exchange 2 receive
+  DevBuf hs, hd, hv;  // host variant: this rank's span on the device
+  uint64_t cnt1[kMaxParts] = {0}, cnt2[kMaxParts] = {0};
+  int64_t st[S_COUNT] = {0};
+  cudaEvent_t ev = nullptr;
+  int rc = NMX_OK;
+  std::string err;
+};
+
+}  // namespace
+
+struct nmx_group {
+  int g = 0;
+  std::vector<int> devices;
+  std::vector<GroupRank> ranks;
+  std::mutex mu;  // one group call at a time
+  GroupBarrier bar;
+  uint64_t last_x1 = 0, last_x2 = 0;  // bytes moved by the last call's exchanges
+};
+
+namespace {
+
+// exchange `k` of rank r: its part p (count cnt[p], at offset sum_{q<p} cnt[q] of the
+// send buffers) goes to rank p at offset sum_{r'<r} cnt_{r'}[p]; two u32 columns.
+void group_exchange(nmx_group* G, int r, DevBuf GroupRank::*sa, DevBuf GroupRank::*sb, DevBuf GroupRank::*ra,
+                    DevBuf GroupRank::*rb, uint64_t (GroupRank::*cnt)[kMaxParts], uint64_t* recv_total) {
+  GroupRank& me = G->ranks[r];
+  // receive size, then buffers grown before anyone writes into them
+  uint64_t tot = 0;
+  for (int q = 0; q < G->g; ++q) tot += (G->ranks[q].*cnt)[r];
+  (me.*ra).grow(std::max<uint64_t>(tot, 1) * 4);
+  (me.*rb).grow(std::max<uint64_t>(tot, 1) * 4);
+  *recv_total = tot;
+  G->bar.arrive();  // every receive buffer exists
+  uint64_t soff = 0;
+  for (int p = 0; p < G->g; ++p) {
+    const uint64_t len = (me.*cnt)[p];
+    if (len) {
+      uint64_t roff = 0;
+      for (int q = 0; q < r; ++q) roff += (G->ranks[q].*cnt)[p];
+      GroupRank& peer = G->ranks[p];
+      const int sdev = me.ctx->device, ddev = peer.ctx->device;
+      CK(cudaMemcpyPeerAsync((peer.*ra).as<uint32_t>() + roff, ddev,
+                             (me.*sa).as<uint32_t>() + soff, sdev, len * 4, me.ctx->st));
+      CK(cudaMemcpyPeerAsync((peer.*rb).as<uint32_t>() + roff, ddev, (me.*sb).as<uint32_t>() + soff, sdev, len * 4,
+                             me.ctx->st));
+    }
+    soff += len;
+  }
+  CK(cudaEventRecord(me.ev, me.ctx->st));
+  G->bar.arrive();  // every send is queued (events recorded)
+  for (int q = 0; q < G->g; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(me.ctx->st, G->ranks[q].ev, 0));
+}
+
+// rank r's share of a group call; d_src / d_dst / d_valid = its n packets on its device
+void group_rank_run(nmx_group* G, int r, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                    uint64_t n, uint64_t space) {
+  GroupRank& me = G->ranks[r];
+  nmx_ctx* c = me.ctx;
+  const int g = G->g;
+  // exchange 1: valid packets by owner(src)
+  me.ps.grow(std::max<uint64_t>(n, 1) * 4);
+  me.pd.grow(std::max<uint64_t>(n, 1) * 4);
+  std::fill(me.cnt1, me.cnt1 + kMaxParts, 0);
+  std::fill(me.cnt2, me.cnt2 + kMaxParts, 0);
+  if (n) {
+    if (int rc = check_addresses(c, d_src, d_dst, n, space)) throw std::runtime_error(g_err);
+    PacketPart it{d_src, d_dst, d_valid, me.ps.as<uint32_t>(), me.pd.as<uint32_t>()};
+    partition_items(c, it, n, g, me.cnt1);
+  }
+  G->bar.arrive();  // counts published
+  uint64_t m = 0;
+  group_exchange(G, r, &GroupRank::ps, &GroupRank::pd, &GroupRank::rs, &GroupRank::rd, &GroupRank::cnt1, &m);
+  // links + rows of this rank's sources; column entries by owner(dst)
+  me.cs.grow(std::max<uint64_t>(m, 1) * 4);
+  me.cc.grow(std::max<uint64_t>(m, 1) * 4);
+  int64_t row9[S_COUNT], col9[S_COUNT];
+  if (m >= (1ull << 32)) throw std::runtime_error("more than 2^32-1 packets routed to one rank");
+  if (int rc = shard_rows_impl(c, me.rs.as<uint32_t>(), me.rd.as<uint32_t>(), m, space, g, me.cs.as<uint32_t>(),
+                               me.cc.as<uint32_t>(), me.cnt2, row9))
+    throw std::runtime_error(g_err);
+  G->bar.arrive();  // counts published
+  uint64_t u = 0;
+  group_exchange(G, r, &GroupRank::cs, &GroupRank::cc, &GroupRank::qs, &GroupRank::qc, &GroupRank::cnt2, &u);
+  if (int rc = shard_cols_impl(c, me.qs.as<uint32_t>(), me.qc.as<uint32_t>(), u, space, col9))
+    throw std::runtime_error(g_err);
+  CK(cudaStreamSynchronize(c->st));
+  for (int i = 0; i < S_COUNT; ++i) me.st[i] = i < 6 ? row9[i] : col9[i];
+}
+
+// one host thread per rank; results combined as the final SUM / MAX all-reduce
+int group_run(nmx_group* G, const std::function<void(int)>& body, int64_t* out) {
+  std::lock_guard<std::mutex> lk(G->mu);
+  G->bar.n = G->g;
+  G->bar.waiting = 0;
+  G->bar.aborted = false;
+  std::vector<std::thread> th;
+  for (int r = 0; r < G->g; ++r) {
+    G->ranks[r].rc = NMX_OK;
+    th.emplace_back([G, r, &body] {
+      GroupRank& me = G->ranks[r];
+      std::lock_guard<std::mutex> clk(me.ctx->mu);
+      try {
+        CK(cudaSetDevice(me.ctx->device));
+        if (!me.ev) CK(cudaEventCreateWithFlags(&me.ev, cudaEventDisableTiming));
+        body(r);
+      } catch (const CudaError& e) {
+        cudaGetLastError();
+        me.rc = NMX_ECUDA;
+        char b[256];
+        snprintf(b, sizeof(b), "rank %d: CUDA error %s (%s) at nmx_api.cu:%d", r, cudaGetErrorString(e.e), e.what,
+                 e.line);
+        me.err = b;
+        G->bar.abort();
+      } catch (const std::bad_alloc&) {
+        me.rc = NMX_ENOMEM;
+        me.err = "host allocation failed";
+        G->bar.abort();
+      } catch (const std::exception& e) {
+        me.rc = NMX_EINVAL;
+        me.err = std::string("rank ") + std::to_string(r) + ": " + e.what();
+        G->bar.abort();
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  // the first real failure wins over the "aborted by another rank" echoes
+  int rc = NMX_OK;
+  std::string msg;
+  for (auto& rk : G->ranks)
+    if (rk.rc != NMX_OK && (rc == NMX_OK || msg.find("aborted") != std::string::npos) &&
+        rk.err.find("aborted by another rank") == std::string::npos) {
+      rc = rk.rc;
+      msg = rk.err;
+    }
+  if (rc == NMX_OK)
+    for (auto& rk : G->ranks)
+      if (rk.rc != NMX_OK) rc = rk.rc, msg = rk.err;
+  if (rc != NMX_OK) return fail(rc, "%s", msg.c_str());
+  static const bool kSum[S_COUNT] = {true, true, false, true, false, false, true, false, false};
+  for (int i = 0; i < S_COUNT; ++i) {
+    int64_t v = 0;
+    for (auto& rk : G->ranks) v = kSum[i] ? v + rk.st[i] : std::max(v, rk.st[i]);
+    out[i] = v;
+  }
+  G->last_x1 = G->last_x2 = 0;
+  for (auto& rk : G->ranks)
+    for (int p = 0; p < G->g; ++p) {
+      G->last_x1 += rk.cnt1[p] * 8;
+      G->last_x2 += rk.cnt2[p] * 8;
+    }
+  return NMX_OK;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -2005,29 +2281,7 @@ int nmx_shard_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, uin
   if (int r = check_space(address_space, b)) return r;
   if (n >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per call");
   return guarded(c, [&] {
-    std::fill(out, out + S_COUNT, 0);
-    std::fill(counts, counts + nparts, 0);
-    if (!n) return NMX_OK;
-    if (int r = check_addresses(c, d_src, d_dst, n, address_space)) return r;
-    stage_begin(c, 1);
-    if (const int D = msd_bits(n, b)) {  // MSD rows; column slots (holes skipped) by owner(dst)
-      uint32_t* chist = nullptr;
-      const ColConcatSrc cs = msd_rows(c, d_src, d_dst, nullptr, n, b, D, 0, &chist);
-      if (cs.n) {
-        ColConcatPart it{cs, d_out_dst, d_out_count};
-        partition_items(c, it, cs.n, nparts, counts);
-      }
-    } else {
-      PacketSrc ps{d_src, d_dst, nullptr, n, 0, b};
-      const RowsOut r = stage_rows(c, ps, b, 0);
-      if (r.u) {
-        ColPart it{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), d_out_dst, d_out_count};
-        partition_items(c, it, r.u, nparts, counts);
-      }
-    }
-    stage_finish(c, 1);
-    copy_out9(c->h_stats, out, 1);
-    return NMX_OK;
+    return shard_rows_impl(c, d_src, d_dst, n, address_space, nparts, d_out_dst, d_out_count, counts, out);
   });
 }
 
@@ -2037,47 +2291,7 @@ int nmx_shard_cols(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, u
   int b;
   if (int r = check_space(address_space, b)) return r;
   if (u >= (1ull << 32)) return fail(NMX_EINVAL, "u must be < 2^32 per call");
-  return guarded(c, [&] {
-    std::fill(out, out + S_COUNT, 0);
-    if (!u) return NMX_OK;
-    if (int r = check_addresses(c, d_dst, d_dst, u, address_space)) return r;
-    stage_begin(c, 1);
-    c->ckA.grow(u * 4);
-    c->ckB.grow(u * 4);
-    c->cvA.grow(u * 4);
-    c->cvB.grow(u * 4);
-    if (const int Dc = msd_bits(u, b)) {  // MSD column partition + shared-memory groups
-      c->colL_dst.grow(u * 8);
-      pack_cols_kernel<<<c->sms * 8, 256, 0, c->st>>>(d_dst, d_count, u, c->colL_dst.as<uint64_t>());
-      CK_LAUNCH();
-      ++c->launches;
-      ColConcatSrc cs{c->colL_dst.as<uint64_t>(), u, nullptr, 0, u};
-      cs.quad = true;
-      msd_columns(c, cs, b, Dc, nullptr);
-      stage_finish(c, 1);
-      copy_out9(c->h_stats, out, 1);
-      return NMX_OK;
-    }
-    if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
-      CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
-    CK(cudaMemcpyAsync(c->ckA.p, d_dst, u * 4, cudaMemcpyDeviceToDevice, c->st));
-    CK(cudaMemcpyAsync(c->cvA.p, d_count, u * 4, cudaMemcpyDeviceToDevice, c->st));
-    const int ncolpass = (b + 7) / 8;
-    uint32_t* d_small = c->small.as<uint32_t>();
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((u + 1023) / 1024, (uint64_t)c->sms * 8));
-    switch (ncolpass) {
-      case 1: hist_u32_kernel<1><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
-      case 2: hist_u32_kernel<2><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
-      case 3: hist_u32_kernel<3><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
-      default: hist_u32_kernel<4><<<grid, 256, 0, c->st>>>(c->ckA.as<uint32_t>(), u, d_small + kCHist); break;
-    }
-    CK_LAUNCH();
-    ++c->launches;
-    stage_cols(c, (uint32_t)u, b, 0, false);
-    stage_finish(c, 1);
-    copy_out9(c->h_stats, out, 1);
-    return NMX_OK;
-  });
+  return guarded(c, [&] { return shard_cols_impl(c, d_dst, d_count, u, address_space, out); });
 }
 
 int nmx_coo_build(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
@@ -2493,6 +2707,130 @@ int nmx_last_timing(nmx_ctx* c, float* total_ms, float* sort_ms, int* sort_launc
   if (sort_ms) *sort_ms = c->last_sort_ms;
   if (sort_launches) *sort_launches = c->last_sort_launches;
   if (kernel_launches) *kernel_launches = c->last_launches;
+  return NMX_OK;
+}
+
+
+// ---- device groups -----------------------------------------------------------
+int nmx_group_create(const int* devices, int g, nmx_group** out) {
+  if (!out || !devices) return fail(NMX_EINVAL, "null argument");
+  *out = nullptr;
+  if (g < 1 || g > kMaxParts) return fail(NMX_EINVAL, "group size must lie in [1, %d], got %d", kMaxParts, g);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    cudaGetLastError();
+    return fail(NMX_ENODEV, "no CUDA device");
+  }
+  for (int r = 0; r < g; ++r)
+    if (devices[r] < 0 || devices[r] >= ndev)
+      return fail(NMX_EINVAL, "rank %d: device %d out of range (%d visible)", r, devices[r], ndev);
+  auto* G = new (std::nothrow) nmx_group();
+  if (!G) return fail(NMX_ENOMEM, "host allocation failed");
+  G->g = g;
+  G->devices.assign(devices, devices + g);
+  G->ranks = std::vector<GroupRank>(g);
+  for (int r = 0; r < g; ++r) {
+    if (int rc = nmx_create(devices[r], &G->ranks[r].ctx)) {
+      nmx_group_destroy(G);
+      return rc;
+    }
+  }
+  // NVLink peer access between the distinct devices of the group (copies fall back
+  // to staging through the host path of cudaMemcpyPeer when a pair has none)
+  for (int a = 0; a < g; ++a)
+    for (int b = 0; b < g; ++b) {
+      const int da = devices[a], db = devices[b];
+      if (da == db) continue;
+      int ok = 0;
+      if (cudaDeviceCanAccessPeer(&ok, da, db) == cudaSuccess && ok) {
+        cudaSetDevice(da);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+        if (e != cudaSuccess) cudaGetLastError();  // already enabled
+      }
+    }
+  *out = G;
+  return NMX_OK;
+}
+
+void nmx_group_destroy(nmx_group* G) {
+  if (!G) return;
+  for (auto& rk : G->ranks) {
+    if (!rk.ctx) continue;
+    cudaSetDevice(rk.ctx->device);
+    if (rk.ev) cudaEventDestroy(rk.ev);
+    for (DevBuf* b : {&rk.ps, &rk.pd, &rk.rs, &rk.rd, &rk.cs, &rk.cc, &rk.qs, &rk.qc, &rk.hs, &rk.hd, &rk.hv})
+      b->release();
+    nmx_destroy(rk.ctx);
+    rk.ctx = nullptr;
+  }
+  delete G;
+}
+
+int nmx_group_size(const nmx_group* G, int* g) {
+  if (!G || !g) return fail(NMX_EINVAL, "null argument");
+  *g = G->g;
+  return NMX_OK;
+}
+
+int nmx_group_context(nmx_group* G, int rank, nmx_ctx** out) {
+  if (!G || !out) return fail(NMX_EINVAL, "null argument");
+  if (rank < 0 || rank >= G->g) return fail(NMX_EINVAL, "rank %d out of range", rank);
+  *out = G->ranks[rank].ctx;
+  return NMX_OK;
+}
+
+int nmx_group_stats9_device(nmx_group* G, const uint32_t* const* d_src, const uint32_t* const* d_dst,
+                            const uint8_t* const* d_valid, const uint64_t* n, uint64_t address_space, int64_t out[9]) {
+  if (!G || !d_src || !d_dst || !n || !out) return fail(NMX_EINVAL, "null argument");
+  int b;
+  if (int r = check_space(address_space, b)) return r;
+  for (int r = 0; r < G->g; ++r) {
+    if (n[r] >= (1ull << 32)) return fail(NMX_EINVAL, "rank %d: n must be < 2^32 per rank", r);
+    if (n[r] && (!d_src[r] || !d_dst[r])) return fail(NMX_EINVAL, "rank %d: null packet columns", r);
+  }
+  return group_run(
+      G, [&](int r) { group_rank_run(G, r, d_src[r], d_dst[r], d_valid ? d_valid[r] : nullptr, n[r], address_space); },
+      out);
+}
+
+int nmx_group_stats9_host(nmx_group* G, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
+                          uint64_t address_space, uint64_t batch_count, int64_t out[9]) {
+  if (!G || !out || (n && (!src || !dst))) return fail(NMX_EINVAL, "null argument");
+  if (batch_count < 1) return fail(NMX_EINVAL, "batch_count must be >= 1");
+  int b;
+  if (int r = check_space(address_space, b)) return r;
+  return group_run(
+      G,
+      [&](int r) {
+        // partition_even (partitioning.py:62-70): rank r's contiguous span, remainder to the front
+        const uint64_t q = n / G->g, rem = n % G->g;
+        const uint64_t len = q + ((uint64_t)r < rem ? 1 : 0), off = r * q + std::min<uint64_t>(r, rem);
+        GroupRank& me = G->ranks[r];
+        nmx_ctx* c = me.ctx;
+        me.hs.grow(std::max<uint64_t>(len, 1) * 4);
+        me.hd.grow(std::max<uint64_t>(len, 1) * 4);
+        if (valid) me.hv.grow(std::max<uint64_t>(len, 1));
+        // b_n streaming chunks per rank (batch_table, partitioning.py:89-98)
+        const uint64_t bq = len / batch_count, brem = len % batch_count;
+        for (uint64_t k = 0, at = 0; k < batch_count; ++k) {
+          const uint64_t bl = bq + (k < brem ? 1 : 0);
+          if (!bl) continue;
+          CK(cudaMemcpyAsync(me.hs.as<uint32_t>() + at, src + off + at, bl * 4, cudaMemcpyHostToDevice, c->st));
+          CK(cudaMemcpyAsync(me.hd.as<uint32_t>() + at, dst + off + at, bl * 4, cudaMemcpyHostToDevice, c->st));
+          if (valid)
+            CK(cudaMemcpyAsync(me.hv.as<uint8_t>() + at, valid + off + at, bl, cudaMemcpyHostToDevice, c->st));
+          at += bl;
+        }
+        group_rank_run(G, r, me.hs.as<uint32_t>(), me.hd.as<uint32_t>(), valid ? me.hv.as<uint8_t>() : nullptr, len,
+                       address_space);
+      },
+      out);
+}
+
+int nmx_group_last_exchange(nmx_group* G, uint64_t* bytes1, uint64_t* bytes2) {
+  if (!G) return fail(NMX_EINVAL, "null group");
+  if (bytes1) *bytes1 = G->last_x1;
+  if (bytes2) *bytes2 = G->last_x2;
   return NMX_OK;
 }
 
