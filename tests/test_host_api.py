@@ -100,3 +100,36 @@ def test_report_serialisation_order():
     assert nm.AggregateReport.from_dict(r.to_dict()) == r
     s = nm.Stats9(6, 3, 3, 2, 3, 2, 2, 4, 2)
     assert s.report() == r and s.astuple() == (6, 3, 3, 2, 3, 2, 2, 4, 2)
+
+
+def test_group_run_bulk_every_index_once_concurrently():
+    """run_bulk (senders.py:32-38 contract): each index once, contiguous partition_even
+    spans per resource (resources.py:107-113), the resources' spans concurrent."""
+    import threading
+
+    seen = []
+    lock = threading.Lock()
+    meet = threading.Barrier(4, timeout=10)  # only passable if the 4 spans run at once
+    spans = nm.partition_even(10, 4).spans
+
+    def task(i, rid, scale):
+        with lock:
+            seen.append((i, rid, scale))
+        if i == spans[rid][0]:
+            meet.wait()
+
+    with nm.make_group_scheduler(4) as g:
+        g.run_bulk(10, task, (3,))
+    assert sorted(i for i, _, _ in seen) == list(range(10))
+    for i, rid, scale in seen:
+        off, ln = spans[rid]
+        assert off <= i < off + ln and scale == 3
+
+    def boom(i, rid):
+        if i == 7:
+            raise RuntimeError("task failed")
+
+    with pytest.raises(RuntimeError, match="task failed"):
+        nm.make_group_scheduler(3).run_bulk(9, boom, ())
+    with pytest.raises(ValueError):
+        nm.make_group_scheduler([1, 0])
