@@ -37,7 +37,6 @@ extern "C" {
 #define NMX_ENOMEM -2  /* device or pinned-host allocation failed  */
 #define NMX_ECUDA -3   /* CUDA runtime / kernel error              */
 #define NMX_ENODEV -4  /* no CUDA device                           */
-#define NMX_EFORMAT -5 /* text outside the device fast path: re-parse on the host */
 
 #define NMX_GEN_UNIFORM 0  /* SURVEY.md 8(d) cfg3 generator */
 #define NMX_GEN_POWERLAW 1 /* SURVEY.md 8(d) cfg4 "octave" generator */
@@ -124,13 +123,29 @@ int nmx_anonymize_finish(nmx_ctx* ctx, const uint32_t* perm, uint32_t* d_src_out
 
 /* Text matrix files (traffic.py:295-367): header "dim nnz", then
  * "row col value" lines sorted row-major without duplicates.
- *  - nmx_parse_matrix_text: host text -> device COO (keys row << 32 | col, u32 values)
- *    + header; NMX_EFORMAT when the text is not in the device fast path (bytes other
- *    than digits, signs, ' ', '\t', '\n') or fails validation (token counts, bounds,
- *    value >= 1, order, nnz) -- the caller re-parses on the host for the exact error.
+ *  - nmx_parse_matrix_text: host text -> device COO (keys row << 32 | col, u32 values),
+ *    tokenised, converted and validated on the device with the reference's rules
+ *    (str.splitlines / str.split / int(), int64 entries) and its check order. info[8]:
+ *    [0] dim, [1] nnz (header), [2] entry lines, [3] NMX_TXT_* diagnosis (0 = parsed,
+ *    *out set), [4] the 1-based physical line it names (0 = none). A malformed file is
+ *    NMX_OK with info[3] != 0 (the caller words the MatrixFileError); NMX_TXT_ENCODING
+ *    asks the caller to normalise non-ASCII text (str.split semantics) and call again;
+ *    NMX_TXT_WIDE = values >= 2^32 or dim > 2^32 (beyond the device COO).
  *  - nmx_format_matrix_text: entry columns -> the "row col value\n" lines (without the
  *    header); call with out == NULL (or cap too small) to get *bytes first. */
-int nmx_parse_matrix_text(nmx_ctx* ctx, const char* text, uint64_t bytes, int64_t hdr[2], nmx_coo** out);
+#define NMX_TXT_OK 0
+#define NMX_TXT_HEADER 1    /* "expected header 'dim nnz'" */
+#define NMX_TXT_DIM 2       /* "dim must be >= 1" */
+#define NMX_TXT_NNZ 3       /* "nnz must be >= 0" */
+#define NMX_TXT_FIELDS 4    /* "expected 'row col value'" */
+#define NMX_TXT_INTEGERS 5  /* "expected 'row col value' integers" */
+#define NMX_TXT_COUNT 6     /* "header claims {nnz} entries, file has {k}" */
+#define NMX_TXT_BOUNDS 7    /* "row/col outside [0, {dim})" */
+#define NMX_TXT_VALUE 8     /* "value must be >= 1" */
+#define NMX_TXT_ORDER 9     /* "entries must be sorted row-major with no duplicates" */
+#define NMX_TXT_WIDE 10
+#define NMX_TXT_ENCODING 11
+int nmx_parse_matrix_text(nmx_ctx* ctx, const char* text, uint64_t bytes, int64_t info[8], nmx_coo** out);
 int nmx_format_matrix_text(nmx_ctx* ctx, const int64_t* rows, const int64_t* cols, const int64_t* vals, uint64_t nnz,
                            char* out, uint64_t cap, uint64_t* bytes);
 

@@ -426,21 +426,21 @@ def anonymize_device(src, dst, key: int, device: int = 0, tables: bool = True):
     return so, do, k, distinct, code
 
 
-EFORMAT = -5
+# nmx_parse_matrix_text diagnoses (include/nmx.h NMX_TXT_*)
+TXT_OK, TXT_HEADER, TXT_DIM, TXT_NNZ, TXT_FIELDS, TXT_INTEGERS, TXT_COUNT, TXT_BOUNDS, TXT_VALUE, TXT_ORDER, \
+    TXT_WIDE, TXT_ENCODING = range(12)
 
 
 def parse_matrix_text(text: bytes, device: int = 0):
-    """Text matrix file bytes -> (dim, nnz, COO handle) parsed on the GPU, or None when
-    the text is outside the device fast path (the caller re-parses on the host)."""
+    """Text matrix file bytes -> (info, COO handle or None), tokenised and validated on
+    the GPU. info = (dim, nnz, entry lines, diagnosis, line): diagnosis TXT_OK with a
+    handle, or the first rule the file breaks (the caller words the error)."""
     ctx = context(device)
-    hdr = np.zeros(2, dtype=np.int64)
+    info = np.zeros(8, dtype=np.int64)
     h = C.c_void_p()
     buf = np.frombuffer(text, dtype=np.uint8) if len(text) else np.zeros(1, np.uint8)
-    rc = ctx._lib.nmx_parse_matrix_text(ctx.handle, buf.ctypes.data, len(text), hdr.ctypes.data, C.byref(h))
-    if rc == EFORMAT:
-        return None
-    check(rc)
-    return int(hdr[0]), int(hdr[1]), h
+    check(ctx._lib.nmx_parse_matrix_text(ctx.handle, buf.ctypes.data, len(text), info.ctypes.data, C.byref(h)))
+    return tuple(int(x) for x in info[:5]), (h if h.value else None)
 
 
 def format_matrix_text(rows, cols, values, device: int = 0) -> bytes:

@@ -64,7 +64,8 @@ struct DevBuf {
     if (p) CK(cudaFree(p));
     p = nullptr;
     cap = 0;
-    size_t want = std::max<size_t>(bytes + bytes / 8, 1 << 16);
+    // 1/8 headroom against regrowth, at most 256 MiB on the multi-GB buffers
+    size_t want = std::max<size_t>(bytes + std::min<size_t>(bytes / 8, 256ull << 20), 1 << 16);
     cudaError_t e = cudaMalloc(&p, want);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -127,6 +128,7 @@ struct nmx_ctx {
   cudaStream_t st = nullptr;
   std::mutex mu;
   DevBuf mpcnt, mpoff;  // group pieces (seg_plan_groups_dev with a bucket cap)
+  DevBuf parS, parD, pcolD, pcolC;  // out-of-core source / destination part arenas (> 2^31 packets)
   DevBuf mscan, mch, mgh, mplan, keysA, keysB, keysC, keysD, cgk, cgv, cgk2, cgv2, colL_dst, colL_cnt, mcur, moff, mhist2, mgb, mheavy, mdst, ckA, ckB, cvA, cvB, status, lrstatus, csstatus, small, part, rbstatus, mkeys, mlen, msum,
       ckeys2, clen2, csum2, frows, stats, in_src, in_dst, in_valid,
       red, ws0, ws1, wd0, wd1, wv0, wv1, wr0, wr1, rmax, anAk, anAv, anBk, anBv, anHead, anHoff, anDistinct,
@@ -1228,8 +1230,13 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
 
 // ---- owner partitions for the multi-GPU exchange ----------
 // returns per-part counts on the host; items scattered part-contiguously
+// base_add (host, optional): part p's items go to absolute positions base_add[p] + ..
+// (separate per-part arenas) instead of part-contiguously from 0
+// cap_left (host, optional): part p may take at most cap_left[p] items (checked
+// before anything is written; std::length_error otherwise)
 template <typename Item>
-void partition_items(nmx_ctx* c, const Item& it, uint64_t n, int nparts, uint64_t* counts_host) {
+void partition_items(nmx_ctx* c, const Item& it, uint64_t n, int nparts, uint64_t* counts_host,
+                     const uint64_t* base_add = nullptr, const uint64_t* cap_left = nullptr) {
   c->part.grow(2 * kMaxParts * sizeof(unsigned long long));
   auto* d_counts = c->part.as<unsigned long long>();
   auto* d_cursor = d_counts + kMaxParts;
@@ -1240,9 +1247,12 @@ void partition_items(nmx_ctx* c, const Item& it, uint64_t n, int nparts, uint64_
   unsigned long long hc[kMaxParts];
   CK(cudaMemcpyAsync(hc, d_counts, sizeof(hc), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  if (cap_left)
+    for (int p = 0; p < nparts; ++p)
+      if (hc[p] > cap_left[p]) throw std::length_error("part capacity exceeded (skewed owner split)");
   unsigned long long base[kMaxParts], acc = 0;
   for (int p = 0; p < nparts; ++p) {
-    base[p] = acc;
+    base[p] = base_add ? base_add[p] : acc;
     acc += hc[p];
     counts_host[p] = hc[p];
   }
@@ -1266,6 +1276,8 @@ int guarded(nmx_ctx* c, F&& f) {
     return fail(NMX_ECUDA, "CUDA error %s (%s) at nmx_api.cu:%d", cudaGetErrorString(e.e), e.what, e.line);
   } catch (const std::bad_alloc&) {
     return fail(NMX_ENOMEM, "host allocation failed");
+  } catch (const std::length_error& e) {
+    return fail(NMX_ENOMEM, "%s", e.what());
   } catch (const std::exception& e) {
     return fail(NMX_EINVAL, "%s", e.what());
   }
@@ -1312,6 +1324,7 @@ int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
     return NMX_OK;
   }
   if (!d_src || !d_dst) return fail(NMX_EINVAL, "null packet columns");
+  for (DevBuf* d : {&c->parS, &c->parD, &c->pcolD, &c->pcolC}) d->release();  // a previous out-of-core call's arenas
   if (int r = check_addresses(c, d_src, d_dst, n, space)) return r;
   if (window_size == 0 || window_size >= n) {
     run_pipeline(c, d_src, d_dst, d_valid, n, b, 0, 1);
@@ -1370,6 +1383,9 @@ int check_maxaddr(nmx_ctx* c, uint64_t space) {
 // alternating device slots; the H2D copy of window k+1 overlaps the level-1 MSD
 // partition of window k into the arena keysA, and the remaining levels, the
 // shared-memory groups and the column statistics run once over the sum.
+int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wmax, uint64_t space, bool any_valid,
+                      int64_t* out);
+
 int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out) {
   int b;
   if (int r = check_space(space, b)) return r;
@@ -1384,7 +1400,12 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
     wmax = std::max(wmax, hw.lens[k]);
     any_valid = any_valid || (hw.valid && hw.valid[k]);
   }
-  if (N >= (1ull << 32)) return fail(NMX_EINVAL, "n must be < 2^32 per device, got %llu", (unsigned long long)N);
+  if (N >= (1ull << 35)) return fail(NMX_EINVAL, "n must be < 2^35 per device, got %llu", (unsigned long long)N);
+  // above 2^31 packets the out-of-core part split (NMX_PARTS_MIN lowers the threshold for tests)
+  const char* pm = getenv("NMX_PARTS_MIN");
+  const uint64_t parts_min = pm ? strtoull(pm, nullptr, 10) : (1ull << 31);
+  if (N > parts_min) return stream_parts_impl(c, hw, N, wmax, space, any_valid, out);
+  for (DevBuf* d : {&c->parS, &c->parD, &c->pcolD, &c->pcolC}) d->release();  // a previous out-of-core call's arenas
   const bool range = recs || space < (1ull << 32);  // address range checked on the device
   if (range) {
     c->rmax.grow(64);
@@ -1510,7 +1531,7 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
 
 int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t space, uint64_t window_size, int64_t* out) {
-  if (window_size == 0 && n >= (1ull << 20) && n < (1ull << 32) && src && dst) {
+  if (window_size == 0 && n >= (1ull << 20) && n < (1ull << 35) && src && dst) {
     // H2D in chunks overlapped with the level-1 partition of the previous chunk
     constexpr uint64_t kChunk = 1ull << 25;
     std::vector<const uint32_t*> ss, dd;
@@ -1550,7 +1571,8 @@ int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const 
 // link + row statistics (fields 0-5) of the packets whose sources this rank owns,
 // and its unique links' (dst, count) column entries routed by owner(dst)
 int shard_rows_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, uint64_t n, uint64_t space, int nparts,
-                    uint32_t* d_out_dst, uint32_t* d_out_count, uint64_t* counts, int64_t* out) {
+                    uint32_t* d_out_dst, uint32_t* d_out_count, uint64_t* counts, int64_t* out,
+                    const uint64_t* base_add = nullptr, const uint64_t* cap_left = nullptr) {
   int b;
   if (int r = check_space(space, b)) return r;
   std::fill(out, out + S_COUNT, 0);
@@ -1563,14 +1585,14 @@ int shard_rows_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, ui
     const ColConcatSrc cs = msd_rows(c, d_src, d_dst, nullptr, n, b, D, 0, &chist);
     if (cs.n) {
       ColConcatPart it{cs, d_out_dst, d_out_count};
-      partition_items(c, it, cs.n, nparts, counts);
+      partition_items(c, it, cs.n, nparts, counts, base_add, cap_left);
     }
   } else {
     PacketSrc ps{d_src, d_dst, nullptr, n, 0, b};
     const RowsOut r = stage_rows(c, ps, b, 0);
     if (r.u) {
       ColPart it{c->ckA.as<uint32_t>(), c->cvA.as<uint32_t>(), d_out_dst, d_out_count};
-      partition_items(c, it, r.u, nparts, counts);
+      partition_items(c, it, r.u, nparts, counts, base_add, cap_left);
     }
   }
   stage_finish(c, 1);
@@ -1621,6 +1643,131 @@ int shard_cols_impl(nmx_ctx* c, const uint32_t* d_dst, const uint32_t* d_count, 
   stage_cols(c, (uint32_t)u, b, 0, false);
   stage_finish(c, 1);
   copy_out9(c->h_stats, out, 1);
+  return NMX_OK;
+}
+
+// Out-of-core summed statistics of more than 2^31 packets on one device (BASELINE
+// config 5: 2^32 packets streamed from pinned host memory): the sharded pipeline of
+// SURVEY.md 8(e) with its ranks run one after another on this context. Every window is
+// partitioned on arrival into P source-part arenas by owner(src) = (fmix32(src) P) >> 32
+// (a part holds whole sources, < 2^31 packets); each part's links and rows are finished
+// by the MSD row half, its unique links' (dst, count) routed by owner(dst) into P
+// column-part arenas; each column part is finished by the MSD column half. Parts are
+// disjoint by source / destination, so the statistics combine by SUM / MAX -- exactly
+// the one-pass result (bit-identical, tests/golden/full_size.json cfg5 cases).
+int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wmax, uint64_t space, bool any_valid,
+                      int64_t* out) {
+  const bool recs = hw.rec != nullptr;
+  const bool range = recs || space < (1ull << 32);
+  int P = 2;
+  auto cap_of = [&](int parts) { return N / parts + N / (4 * (uint64_t)parts) + (1ull << 22); };
+  while (cap_of(P) >= (1ull << 31) - (1ull << 22)) P *= 2;
+  if (P > kMaxParts) return fail(NMX_EINVAL, "too many packets for one device");
+  const uint64_t cap = cap_of(P);
+  // the part arenas come first: workspace grown by earlier (larger single-pass) calls is
+  // dropped and regrown at part size
+  for (DevBuf* d : {&c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->colL_dst, &c->ckA, &c->ckB, &c->cvA, &c->cvB,
+                    &c->cgk, &c->cgk2, &c->in_src, &c->in_dst, &c->in_valid, &c->lightK, &c->pcolD, &c->pcolC})
+    if (d->cap > (64ull << 20)) d->release();
+  c->parS.grow((size_t)P * cap * 4);
+  c->parD.grow((size_t)P * cap * 4);
+  if (range) {
+    c->rmax.grow(64);
+    CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
+  }
+  if (!c->st2) CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    if (!c->evc[i]) CK(cudaEventCreateWithFlags(&c->evc[i], cudaEventDisableTiming));
+    if (!c->evu[i]) CK(cudaEventCreateWithFlags(&c->evu[i], cudaEventDisableTiming));
+  }
+  if (!c->evs) CK(cudaEventCreate(&c->evs));
+  DevBuf* ws[2] = {&c->ws0, &c->ws1};
+  DevBuf* wd[2] = {&c->wd0, &c->wd1};
+  DevBuf* wv[2] = {&c->wv0, &c->wv1};
+  DevBuf* wr[2] = {&c->wr0, &c->wr1};
+  for (int i = 0; i < 2; ++i) {
+    ws[i]->grow(wmax * 4 + 16);
+    wd[i]->grow(wmax * 4 + 16);
+    if (any_valid) wv[i]->grow(wmax + 16);
+    if (recs) wr[i]->grow(wmax * 9 + 16);
+  }
+  CK(cudaEventRecord(c->evs, c->st));
+  CK(cudaStreamWaitEvent(c->st2, c->evs, 0));
+  bool used[2] = {false, false};
+  auto enqueue_copy = [&](uint64_t k) {
+    const int sl = (int)(k & 1);
+    if (used[sl]) CK(cudaStreamWaitEvent(c->st2, c->evu[sl], 0));
+    const uint64_t L = hw.lens[k];
+    if (L && recs) {
+      CK(cudaMemcpyAsync(wr[sl]->p, hw.rec[k], L * 9, cudaMemcpyHostToDevice, c->st2));
+    } else if (L) {
+      CK(cudaMemcpyAsync(ws[sl]->p, hw.src[k], L * 4, cudaMemcpyHostToDevice, c->st2));
+      CK(cudaMemcpyAsync(wd[sl]->p, hw.dst[k], L * 4, cudaMemcpyHostToDevice, c->st2));
+      if (hw.valid && hw.valid[k]) CK(cudaMemcpyAsync(wv[sl]->p, hw.valid[k], L, cudaMemcpyHostToDevice, c->st2));
+    }
+    CK(cudaEventRecord(c->evc[sl], c->st2));
+  };
+  // 1. windows -> source-part arenas (the copy of window k+1 overlaps window k's split)
+  uint64_t fill[kMaxParts] = {0}, base[kMaxParts], left[kMaxParts], cnt[kMaxParts];
+  if (hw.nwin) enqueue_copy(0);
+  for (uint64_t k = 0; k < hw.nwin; ++k) {
+    if (k + 1 < hw.nwin) enqueue_copy(k + 1);
+    const int sl = (int)(k & 1);
+    CK(cudaStreamWaitEvent(c->st, c->evc[sl], 0));
+    const uint64_t L = hw.lens[k];
+    if (L) {
+      if (recs)
+        unpack_records(c, wr[sl]->as<uint8_t>(), L, ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(),
+                       wv[sl]->as<uint8_t>(), c->rmax.as<unsigned int>());
+      else if (range)
+        launch_max_addr(c, ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), L);
+      const uint8_t* v = (recs || (hw.valid && hw.valid[k])) ? wv[sl]->as<uint8_t>() : nullptr;
+      for (int p = 0; p < P; ++p) {
+        base[p] = p * cap + fill[p];
+        left[p] = cap - fill[p];
+      }
+      PacketPart it{ws[sl]->as<uint32_t>(), wd[sl]->as<uint32_t>(), v, c->parS.as<uint32_t>(), c->parD.as<uint32_t>()};
+      partition_items(c, it, L, P, cnt, base, left);  // host-synchronous: the next copy is already queued
+      for (int p = 0; p < P; ++p) fill[p] += cnt[p];
+    }
+    CK(cudaEventRecord(c->evu[sl], c->st));
+    used[sl] = true;
+  }
+  if (range)
+    if (int r = check_maxaddr(c, space)) return r;
+  // 2. rows per source part; column entries -> destination-part arenas
+  c->pcolD.grow((size_t)P * cap * 4);
+  c->pcolC.grow((size_t)P * cap * 4);
+  uint64_t cfill[kMaxParts] = {0};
+  int64_t tot[S_COUNT] = {0};
+  static const bool kSum[S_COUNT] = {true, true, false, true, false, false, true, false, false};
+  auto fold = [&](const int64_t* s9, int lo, int hi) {
+    for (int i = lo; i < hi; ++i) tot[i] = kSum[i] ? tot[i] + s9[i] : std::max(tot[i], s9[i]);
+  };
+  for (int p = 0; p < P; ++p) {
+    if (!fill[p]) continue;
+    for (int q = 0; q < P; ++q) {
+      base[q] = q * cap + cfill[q];
+      left[q] = cap - cfill[q];
+    }
+    int64_t row9[S_COUNT];
+    if (int r = shard_rows_impl(c, c->parS.as<uint32_t>() + p * cap, c->parD.as<uint32_t>() + p * cap, fill[p], space,
+                                P, c->pcolD.as<uint32_t>(), c->pcolC.as<uint32_t>(), cnt, row9, base, left))
+      return r;
+    for (int q = 0; q < P; ++q) cfill[q] += cnt[q];
+    fold(row9, 0, 6);
+  }
+  // 3. columns per destination part
+  for (int q = 0; q < P; ++q) {
+    if (!cfill[q]) continue;
+    int64_t col9[S_COUNT];
+    if (int r = shard_cols_impl(c, c->pcolD.as<uint32_t>() + q * cap, c->pcolC.as<uint32_t>() + q * cap, cfill[q],
+                                space, col9))
+      return r;
+    fold(col9, 6, 9);
+  }
+  std::copy(tot, tot + S_COUNT, out);
+  c->last_nstage = 0;
   return NMX_OK;
 }
 
@@ -2096,81 +2243,113 @@ int nmx_anonymize_finish(nmx_ctx* c, const uint32_t* perm, uint32_t* d_src_out, 
 }
 
 // ---- text matrix files (nmx_text.cuh, traffic.py:295-367) -------------------
-int nmx_parse_matrix_text(nmx_ctx* c, const char* text, uint64_t T, int64_t hdr_out[2], nmx_coo** out) {
-  if (!out || !hdr_out || (T && !text)) return fail(NMX_EINVAL, "null argument");
+int nmx_parse_matrix_text(nmx_ctx* c, const char* text, uint64_t T, int64_t info[8], nmx_coo** out) {
+  if (!out || !info || (T && !text)) return fail(NMX_EINVAL, "null argument");
   *out = nullptr;
-  if (T == 0 || T >= (1ull << 40)) return NMX_EFORMAT;
+  std::fill(info, info + 8, 0);
+  auto diag = [&](int64_t code, uint64_t line) {
+    info[3] = code;
+    info[4] = (int64_t)line;
+    return NMX_OK;
+  };
+  if (T == 0) return diag(TXT_HEADER, 1);
+  if (T >= (1ull << 40)) return fail(NMX_EINVAL, "text larger than 2^40 bytes");
   return guarded(c, [&] {
     c->txt.grow(T + 16);
     CK(cudaMemcpyAsync(c->txt.p, text, T, cudaMemcpyHostToDevice, c->st));
     const uint64_t nb = (T + kTextChunk - 1) / kTextChunk;
     c->tcnt.grow((nb + 8) * 4);
     c->toff.grow((nb + 8) * 4);
-    c->tbad.grow(64);
-    unsigned int* bad = c->tbad.as<unsigned int>();
-    CK(cudaMemsetAsync(bad, 0, 4, c->st));
+    c->tbad.grow(TR_N * 8);
+    auto* red = c->tbad.as<unsigned long long>();
+    CK(cudaMemsetAsync(red, 0xFF, TR_N * 8, c->st));  // min-reductions start at UINT64_MAX
+    CK(cudaMemsetAsync(red + TR_ENC, 0, 8, c->st));
     text_nl_count_kernel<<<(unsigned)nb, 256, 0, c->st>>>(c->txt.as<char>(), T, c->tcnt.as<uint32_t>());
     CK_LAUNCH();
     scan_counts(c, c->tcnt.as<uint32_t>(), (uint32_t)nb, c->toff.as<uint32_t>(), nullptr);
     uint32_t nl = 0;
     CK(cudaMemcpyAsync(&nl, c->toff.as<uint32_t>() + nb, 4, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    const bool open_end = text[T - 1] != '\n';
-    const uint64_t L = (uint64_t)nl + (open_end ? 1 : 0);
+    // a text not ending on a break has one more (open) line
+    const unsigned char tail = (unsigned char)text[T - 1];
+    const bool closed = tail == '\n' || tail == '\r' || tail == '\v' || tail == '\f' || (tail >= 0x1c && tail <= 0x1e);
+    const uint64_t L = (uint64_t)nl + (closed ? 0 : 1);
     c->tends.grow((L + 8) * 8);
     text_nl_write_kernel<<<(unsigned)nb, 256, 0, c->st>>>(c->txt.as<char>(), T, c->toff.as<uint32_t>(),
                                                           c->tends.as<uint64_t>());
     CK_LAUNCH();
-    if (open_end) CK(cudaMemcpyAsync(c->tends.as<uint64_t>() + L - 1, &T, 8, cudaMemcpyHostToDevice, c->st));
+    if (!closed) CK(cudaMemcpyAsync(c->tends.as<uint64_t>() + L - 1, &T, 8, cudaMemcpyHostToDevice, c->st));
     c->tntok.grow(L + 16);
     c->tvals.grow((L + 8) * 24);
     c->tnb.grow((L + 8) * 4);
     c->tnboff.grow((L + 8) * 4);
     const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((L + 255) / 256, (uint64_t)c->sms * 16));
     text_parse_lines_kernel<<<g, 256, 0, c->st>>>(c->txt.as<char>(), c->tends.as<uint64_t>(), L,
-                                                  c->tntok.as<uint8_t>(), c->tvals.as<long long>(), bad);
+                                                  c->tntok.as<uint8_t>(), c->tvals.as<long long>(), red);
     CK_LAUNCH();
     text_nonblank_kernel<<<g, 256, 0, c->st>>>(c->tntok.as<uint8_t>(), L, c->tnb.as<uint32_t>());
     CK_LAUNCH();
     scan_counts(c, c->tnb.as<uint32_t>(), (uint32_t)L, c->tnboff.as<uint32_t>(), nullptr);
-    uint32_t nbl = 0;
-    unsigned int b0 = 0;
-    CK(cudaMemcpyAsync(&nbl, c->tnboff.as<uint32_t>() + L, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(&b0, bad, 4, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
     c->launches += 5;
-    if (b0 || nbl == 0) return NMX_EFORMAT;
-    const uint64_t nnz = nbl - 1;
-    nmx_coo* o = coo_alloc(c, nnz);
-    c->thdr.grow(64);
-    long long* hdr = c->thdr.as<long long>();
-    text_entries_kernel<<<g, 256, 0, c->st>>>(c->tntok.as<uint8_t>(), c->tvals.as<long long>(),
-                                              c->tnboff.as<uint32_t>(), L, hdr,
-                                              reinterpret_cast<unsigned long long*>(o->keys), o->counts, bad);
-    CK_LAUNCH();
-    long long h[2] = {0, 0};
-    CK(cudaMemcpyAsync(h, hdr, 16, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(&b0, bad, 4, cudaMemcpyDeviceToHost, c->st));
+    uint32_t nbl = 0;
+    unsigned long long r[TR_N];
+    CK(cudaMemcpyAsync(&nbl, c->tnboff.as<uint32_t>() + L, 4, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(r, red, sizeof(r), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    if (b0 || h[0] < 1 || h[1] < 0 || (uint64_t)h[1] != nnz || h[0] > (1ll << 31)) {
-      nmx_coo_free(o);
-      return NMX_EFORMAT;
-    }
-    if (nnz) {
+    if (r[TR_ENC]) return diag(TXT_ENCODING, 0);
+    if (nbl == 0) return diag(TXT_HEADER, 1);
+    // header = first nonblank line (traffic.py:322-333 order of checks)
+    const uint64_t l0 = r[TR_HEAD];
+    uint8_t t0 = 0;
+    long long h[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(&t0, c->tntok.as<uint8_t>() + l0, 1, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(h, c->tvals.as<long long>() + 3 * l0, 24, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if ((t0 & 0x7F) != 2 || (t0 & 0x80)) return diag(TXT_HEADER, l0 + 1);
+    info[0] = h[0];
+    info[1] = h[1];
+    if (h[0] < 1) return diag(TXT_DIM, l0 + 1);
+    if (h[1] < 0) return diag(TXT_NNZ, l0 + 1);
+    const uint64_t entries = nbl - 1;
+    info[2] = (int64_t)entries;
+    nmx_coo* o = coo_alloc(c, entries);
+    c->tloff.grow((entries + 8) * 4);
+    text_entries_kernel<<<g, 256, 0, c->st>>>(c->tntok.as<uint8_t>(), c->tvals.as<long long>(),
+                                              c->tnboff.as<uint32_t>(), L, h[0],
+                                              reinterpret_cast<unsigned long long*>(o->keys), o->counts,
+                                              c->tloff.as<uint32_t>(), red);
+    CK_LAUNCH();
+    if (entries > 1) {
       const unsigned gn =
-          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nnz + 255) / 256, (uint64_t)c->sms * 16));
-      text_check_kernel<<<gn, 256, 0, c->st>>>(reinterpret_cast<const unsigned long long*>(o->keys), nnz, h[0], bad);
+          (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((entries + 255) / 256, (uint64_t)c->sms * 16));
+      text_order_kernel<<<gn, 256, 0, c->st>>>(reinterpret_cast<const unsigned long long*>(o->keys),
+                                               c->tloff.as<uint32_t>(), entries, red);
       CK_LAUNCH();
-      CK(cudaMemcpyAsync(&b0, bad, 4, cudaMemcpyDeviceToHost, c->st));
-      CK(cudaStreamSynchronize(c->st));
-      if (b0) {
-        nmx_coo_free(o);
-        return NMX_EFORMAT;
-      }
     }
     c->launches += 2;
-    hdr_out[0] = h[0];
-    hdr_out[1] = h[1];
+    CK(cudaMemcpyAsync(r, red, sizeof(r), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const unsigned long long none = ~0ull;
+    int64_t code = TXT_OK;
+    uint64_t line = 0;
+    if (r[TR_TOK] != none) {
+      code = (int64_t)(r[TR_TOK] & 15);
+      line = r[TR_TOK] >> 4;
+    } else if ((uint64_t)h[1] != entries) {
+      code = TXT_COUNT;
+    } else if (r[TR_BOUNDS] != none) {
+      code = TXT_BOUNDS, line = r[TR_BOUNDS];
+    } else if (r[TR_VALUE] != none) {
+      code = TXT_VALUE, line = r[TR_VALUE];
+    } else if (r[TR_ORDER] != none) {
+      code = TXT_ORDER, line = r[TR_ORDER];
+    } else if (r[TR_WIDE] != none || h[0] > (1ll << 32)) {
+      code = TXT_WIDE, line = r[TR_WIDE] != none ? r[TR_WIDE] : l0 + 1;
+    }
+    if (code != TXT_OK) {
+      nmx_coo_free(o);
+      return diag(code, line);
+    }
     *out = o;
     return NMX_OK;
   });

@@ -362,80 +362,70 @@ def write_matrix(matrix: TrafficMatrix, path) -> None:
         f.write(body)
 
 
-def _read_matrix_host(path, text: str, window_id: int) -> TrafficMatrix:
-    """The reference's parser (traffic.py:307-367) for text outside the device fast
-    path: identical acceptance rules and MatrixFileError messages."""
-    lines = [(lineno, parts) for lineno, parts in enumerate((ln.split() for ln in text.splitlines()), 1) if parts]
+_TXT_MESSAGES = {
+    _lib.TXT_HEADER: "expected header 'dim nnz'",
+    _lib.TXT_DIM: "dim must be >= 1",
+    _lib.TXT_NNZ: "nnz must be >= 0",
+    _lib.TXT_FIELDS: "expected 'row col value'",
+    _lib.TXT_INTEGERS: "expected 'row col value' integers",
+    _lib.TXT_VALUE: "value must be >= 1",
+    _lib.TXT_ORDER: "entries must be sorted row-major with no duplicates",
+}
 
-    def fail(lineno: int, why: str) -> MatrixFileError:
-        return MatrixFileError(f"{path}: line {lineno}: {why}")
 
-    if not lines:
-        raise fail(1, "expected header 'dim nnz'")
-    if len(lines[0][1]) != 2:
-        raise fail(lines[0][0], "expected header 'dim nnz'")
-    try:
-        dim, nnz = (int(tok) for tok in lines[0][1])
-    except ValueError:
-        raise fail(lines[0][0], "expected header 'dim nnz'") from None
-    if dim < 1:
-        raise fail(lines[0][0], "dim must be >= 1")
-    if nnz < 0:
-        raise fail(lines[0][0], "nnz must be >= 0")
-    entry_lines = lines[1:]
-    entries = np.empty((len(entry_lines), 3), dtype=np.int64)
-    for k, (lineno, parts) in enumerate(entry_lines):
-        if len(parts) != 3:
-            raise fail(lineno, "expected 'row col value'")
+def _ascii_form(data: bytes) -> bytes:
+    """Text with non-ASCII whitespace, line breaks or digits, rewritten into the ASCII
+    form the device tokenizer reads, line for line (so diagnosed line numbers stay the
+    reference's): str.splitlines() / str.split() boundaries, int()-valid tokens in
+    plain decimal. Everything else is left for the device to diagnose."""
+    text = data.decode()  # UnicodeDecodeError (a ValueError), as Path.read_text raises
+
+    def token(t: str) -> str:
+        if t.isascii():
+            return t
         try:
-            entries[k] = [int(tok) for tok in parts]
-        except (ValueError, OverflowError):
-            raise fail(lineno, "expected 'row col value' integers") from None
-    if len(entry_lines) != nnz:
-        raise MatrixFileError(f"{path}: header claims {nnz} entries, file has {len(entry_lines)}")
-    rows, cols, values = entries[:, 0], entries[:, 1], entries[:, 2]
-    line_no = np.array([lineno for lineno, _ in entry_lines], dtype=np.int64)
-    if nnz:
-        bounds = (rows < 0) | (rows >= dim) | (cols < 0) | (cols >= dim)
-        if np.any(bounds):
-            raise fail(int(line_no[np.argmax(bounds)]), f"row/col outside [0, {dim})")
-        if np.any(values < 1):
-            raise fail(int(line_no[np.argmax(values < 1)]), "value must be >= 1")
-        disorder = np.diff(rows * dim + cols) <= 0
-        if np.any(disorder):
-            raise fail(int(line_no[np.argmax(disorder) + 1]), "entries must be sorted row-major with no duplicates")
-    row_ptr = np.zeros(dim + 1, dtype=np.int64)
-    np.cumsum(np.bincount(rows, minlength=dim), out=row_ptr[1:])
-    return TrafficMatrix(window_id=window_id, dim=dim, row_ptr=row_ptr, col_idx=cols, values=values)
+            return str(int(t))
+        except ValueError:
+            return "?"  # still not an integer: keeps the line's integer error
+
+    return "\n".join(" ".join(token(t) for t in ln.split()) for ln in text.splitlines()).encode()
+
+
+def _parse_text(path, data: bytes):
+    """(dim, COO handle) of a matrix file parsed and validated on the GPU; malformed
+    files raise MatrixFileError worded as the reference's read_matrix (traffic.py:307-367)."""
+    (dim, nnz, entries, code, line), h = _lib.parse_matrix_text(data)
+    if code == _lib.TXT_ENCODING:
+        (dim, nnz, entries, code, line), h = _lib.parse_matrix_text(_ascii_form(data))
+        if code == _lib.TXT_ENCODING:
+            raise MatrixFileError(f"{path}: unreadable characters")
+    if code == _lib.TXT_OK:
+        return dim, h
+    if code == _lib.TXT_COUNT:
+        raise MatrixFileError(f"{path}: header claims {nnz} entries, file has {entries}")
+    if code == _lib.TXT_BOUNDS:
+        raise MatrixFileError(f"{path}: line {line}: row/col outside [0, {dim})")
+    if code == _lib.TXT_WIDE:
+        raise MatrixFileError(f"{path}: line {line}: dim or value beyond 2^32 (device matrix range)")
+    raise MatrixFileError(f"{path}: line {line}: {_TXT_MESSAGES[code]}")
 
 
 def read_matrix_device(path, window_id: int = 0):
     """Parse a matrix file on the GPU into a device COO (keys row << 32 | col, u32
-    counts) without host containers: (dim, DeviceCOO). Text outside the device fast
-    path goes through the reference parser (exact errors) and is uploaded."""
-    from .coo import DeviceCOO, coo_from_keys
+    counts) without host containers: (dim, DeviceCOO)."""
+    from .coo import DeviceCOO
 
-    data = open(path, "rb").read()
-    got = _lib.parse_matrix_text(data)
-    if got is not None:
-        dim, _, h = got
-        return dim, DeviceCOO(h)
-    m = _read_matrix_host(path, data.decode("utf-8", errors="replace"), window_id)
-    rows = np.repeat(np.arange(m.dim, dtype=np.int64), np.diff(m.row_ptr))
-    return m.dim, coo_from_keys((rows.astype(np.uint64) << np.uint64(32)) | m.col_idx.astype(np.uint64), m.values)
+    dim, h = _parse_text(path, open(path, "rb").read())
+    return dim, DeviceCOO(h)
 
 
 def read_matrix(path, window_id: int = 0) -> TrafficMatrix:
-    """Parse a matrix file written by write_matrix (traffic.py:307-367): tokenised
-    and validated on the GPU; malformed files raise MatrixFileError naming the file
-    and line, exactly as the reference (they take the host parser)."""
-    data = open(path, "rb").read()
-    got = _lib.parse_matrix_text(data)
-    if got is None:
-        return _read_matrix_host(path, data.decode("utf-8", errors="replace"), window_id)
+    """Parse a matrix file written by write_matrix (traffic.py:307-367): tokenised,
+    converted and validated on the GPU; malformed files raise MatrixFileError naming
+    the file and line, as the reference does."""
     from .coo import DeviceCOO
 
-    dim, nnz, h = got
+    dim, h = _parse_text(path, open(path, "rb").read())
     coo = DeviceCOO(h)
     keys, counts = coo.download()
     coo.close()
@@ -444,3 +434,5 @@ def read_matrix(path, window_id: int = 0) -> TrafficMatrix:
     row_ptr = np.zeros(dim + 1, dtype=np.int64)
     np.cumsum(np.bincount(rows, minlength=dim), out=row_ptr[1:])
     return TrafficMatrix(window_id=window_id, dim=dim, row_ptr=row_ptr, col_idx=cols, values=counts)
+
+

@@ -85,14 +85,33 @@ def test_malformed_files_rejected(tmp_path, content, match):
         read_matrix_device(path)
 
 
-def test_tolerated_variants(tmp_path):
-    path = tmp_path / "spaced.txt"
-    path.write_text("\n2 1\n\n0 1 4\n\n")
-    assert read_matrix(path).to_dense()[0, 1] == 4
-    path.write_text("2 2\r\n0 1 4\r\n1 1 +7\r\n")  # host path: \r line breaks, signs
-    assert read_matrix(path).to_dense().tolist() == [[0, 4], [0, 7]]
-    path.write_text("2\t1\n 0   1\t4")  # tabs, no final newline
-    assert read_matrix(path).to_dense()[0, 1] == 4
+TEXT_GOLDEN = json.loads((Path(__file__).resolve().parent / "golden" / "text_golden.json").read_text())["cases"]
+
+
+@pytest.mark.parametrize("k", range(len(TEXT_GOLDEN)))
+def test_text_parse_matches_reference(tmp_path, k):
+    """Device tokenizer / validator vs the reference's read_matrix on the same bytes
+    (tests/golden/text_golden.json, made by the reference itself): accepted variants
+    (CRLF, lone CR, VT/FF/FS/GS/RS breaks, US, tabs, signs, underscores, leading zeros,
+    non-ASCII whitespace and digits, no final newline) parse to the same matrix; every
+    malformed file raises the same exception with the same message (file and line)."""
+    import base64
+
+    case = TEXT_GOLDEN[k]
+    path = tmp_path / "m.txt"
+    path.write_bytes(base64.b64decode(case["bytes"]))
+    if case["ok"]:
+        m = read_matrix(path)
+        assert (m.dim, m.row_ptr.tolist(), m.col_idx.tolist(), m.values.tolist()) == (
+            case["dim"], case["row_ptr"], case["col_idx"], case["values"])
+        dim, coo = read_matrix_device(path)
+        assert dim == case["dim"] and coo.nnz == len(case["values"])
+        coo.close()
+    else:
+        with pytest.raises(MatrixFileError) as ei:
+            read_matrix(path)
+        assert type(ei.value).__name__ == case["error"]
+        assert str(ei.value) == case["message"].replace("{path}", str(path))
 
 
 @pytest.mark.parametrize("g", range(len(CLI_GOLDEN)))

@@ -75,3 +75,57 @@ def test_host_chunked_equals_device(lib):
     ds.upload(s)
     dd.upload(d)
     assert lib.stats9(ds, dd, None, 1 << 32) == got_host
+
+
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
+@pytest.mark.parametrize("space", [1 << 32, 1 << 20])
+def test_out_of_core_parts_path(lib, kind, space, monkeypatch):
+    """The > 2^31-packet path (source-part arenas, rows per part, destination-part
+    arenas, columns per part) forced at small sizes with NMX_PARTS_MIN: equal to the
+    one-pass oracle, with invalid packets, uneven windows and records."""
+    gen = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
+    s, d = gen(31, 0, 5 << 20, space)
+    v = np.random.default_rng(5).random(len(s)) > 0.1
+    cuts = [0, 3, 1 << 20, 3 << 20, len(s)]
+    wins = [(s[a:b], d[a:b], v[a:b]) for a, b in zip(cuts[:-1], cuts[1:])]
+    want = orc.stats9_packed(s, d, v)
+    monkeypatch.setenv("NMX_PARTS_MIN", str(1 << 20))
+    assert lib.stream_stats9(wins, space) == want
+    assert lib.stats9(s, d, v, space) == want  # host entry (2^25-packet chunks) through the same path
+    rec = np.zeros(len(s), dtype=np.dtype([("src", "<u4"), ("dst", "<u4"), ("valid", "u1")]))
+    rec["src"], rec["dst"], rec["valid"] = s, d, v
+    assert lib.stream_records([rec[:1 << 21], rec[1 << 21:]], space) == want
+    bad = d.copy()
+    if space < 1 << 32:
+        bad[-1] = space
+        with pytest.raises(ValueError, match="address_space"):
+            lib.stream_stats9([(s, bad)], space)
+
+
+@pytest.mark.parametrize("lg,name", [(31, "cfg5_2^31_seed7"), (32, "cfg5_2^32_seed7")])
+def test_cfg5_full_size_golden(lib, lg, name):
+    """BASELINE config 5 on one B200: 2^31 / 2^32 packets streamed from pinned host
+    memory in 2^28-packet windows (2^32 takes the out-of-core part split), bit-exact
+    against the chunked CPU oracle (tests/golden/full_size.json)."""
+    import json
+    from pathlib import Path
+
+    want = tuple(json.loads((Path(__file__).resolve().parent / "golden" / "full_size.json").read_text())
+                 ["cases"][name]["stats9"])
+    w = 1 << 28
+    ds, dd = lib.DeviceArray(w), lib.DeviceArray(w)
+    wins = []
+    try:
+        for k in range((1 << lg) // w):
+            lib.generate(lib.GEN_UNIFORM, 7, k * w, w, 1 << 32, ds, dd)
+            ps, pd = lib.PinnedArray(w), lib.PinnedArray(w)
+            ps.array[:] = ds.download()
+            pd.array[:] = dd.download()
+            wins.append((ps, pd))
+        ds.close()
+        dd.close()
+        assert lib.stream_stats9([(a.array, b.array) for a, b in wins], 1 << 32) == want
+    finally:
+        for a, b in wins:
+            a.close()
+            b.close()
