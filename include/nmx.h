@@ -123,14 +123,14 @@ int nmx_anonymize_finish(nmx_ctx* ctx, const uint32_t* perm, uint32_t* d_src_out
 
 /* Text matrix files (traffic.py:295-367): header "dim nnz", then
  * "row col value" lines sorted row-major without duplicates.
- *  - nmx_parse_matrix_text: host text -> device COO (keys row << 32 | col, u32 values),
+ *  - nmx_parse_matrix_text: host text -> device COO (keys row << 32 | col, int64 values),
  *    tokenised, converted and validated on the device with the reference's rules
  *    (str.splitlines / str.split / int(), int64 entries) and its check order. info[8]:
  *    [0] dim, [1] nnz (header), [2] entry lines, [3] NMX_TXT_* diagnosis (0 = parsed,
  *    *out set), [4] the 1-based physical line it names (0 = none). A malformed file is
  *    NMX_OK with info[3] != 0 (the caller words the MatrixFileError); NMX_TXT_ENCODING
  *    asks the caller to normalise non-ASCII text (str.split semantics) and call again;
- *    NMX_TXT_WIDE = values >= 2^32 or dim > 2^32 (beyond the device COO).
+ *    NMX_TXT_WIDE = dim > 2^32 (rows / columns beyond the 32-bit key halves).
  *  - nmx_format_matrix_text: entry columns -> the "row col value\n" lines (without the
  *    header); call with out == NULL (or cap too small) to get *bytes first. */
 #define NMX_TXT_OK 0
@@ -185,19 +185,22 @@ int nmx_flat_fetch(nmx_ctx* ctx, int64_t* edge_src, int64_t* row_ids, int64_t* r
                    int64_t* col_ids, int64_t* col_nnz, int64_t* col_sum);
 
 /* Sorted unique COO matrices on the device and their element-wise sum (SURVEY.md
- * 8(a) a11, the merge-path "K10"): keys are (src<<32)|dst, counts u32. The
+ * 8(a) a11, the merge-path "K10"): keys are (src<<32)|dst, counts u64 in [1, 2^63)
+ * (the reference's int64 matrix values). The
  * summed matrix of several windows is merge_add of their COOs (= the matrix of
  * the concatenated packets, traffic.py:221-242 with one window).
  *  - nmx_coo_from_packets: unique links of device packet columns;
- *  - nmx_coo_merge_add: C = A + B by merge path (counts of shared keys added);
- *  - nmx_coo_stats9: the nine statistics of a COO;
+ *  - nmx_coo_merge_add: C = A + B by merge path (counts of shared keys added; a sum
+ *    beyond 2^63 - 1 is NMX_EINVAL);
+ *  - nmx_coo_stats9: the nine statistics of a COO (counts >= 2^32 take 64-bit hash
+ *    tables, up to 2^28 links);
  *  - nmx_coo_nnz / nmx_coo_download / nmx_coo_free;
  *  - nmx_coo_reserve: keep `bytes` of device memory mapped in the pool COOs are
  *    allocated from (stream-ordered allocations then never grow the pool). */
 int nmx_coo_from_packets(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
                          uint64_t n, nmx_coo** out);
 int nmx_coo_merge_add(nmx_ctx* ctx, const nmx_coo* a, const nmx_coo* b, nmx_coo** out);
-/* host sorted unique keys (src << 32 | dst) + counts in [1, 2^32-1] -> device COO */
+/* host sorted unique keys (src << 32 | dst) + counts >= 1 -> device COO */
 int nmx_coo_upload(nmx_ctx* ctx, const uint64_t* keys, const int64_t* counts, uint64_t nnz, nmx_coo** out);
 int nmx_coo_stats9(nmx_ctx* ctx, const nmx_coo* a, int64_t out[9]);
 int nmx_coo_nnz(const nmx_coo* a, uint64_t* nnz);

@@ -6,7 +6,7 @@ window_size=len(stream)), traffic.py:221-242). Here each window becomes a
 ``DeviceCOO`` (``nmx_coo_from_packets``) and windows are combined with the
 merge-path kernel (``nmx_coo_merge_add``) -- the streaming form used when the
 packets do not fit the device at once (BASELINE config 5). Keys are
-(src << 32) | dst, counts u32.
+(src << 32) | dst, counts u64 (int64 on the host).
 """
 
 from __future__ import annotations

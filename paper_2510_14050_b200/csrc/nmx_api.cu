@@ -209,12 +209,13 @@ struct nmx_ctx {
   }
 };
 
-// device-resident sorted unique COO: keys (src<<32)|dst, u32 counts
+// device-resident sorted unique COO: keys (src<<32)|dst, u64 counts in [1, 2^63)
+// (the reference's int64 matrix values, traffic.py:140-194)
 struct nmx_coo {
   int device = 0;
   uint64_t nnz = 0;
   uint64_t* keys = nullptr;
-  uint32_t* counts = nullptr;
+  uint64_t* counts = nullptr;
 };
 
 extern "C" nmx_coo* coo_alloc(nmx_ctx* c, uint64_t nnz);  // stream-ordered COO storage (below)
@@ -2343,8 +2344,8 @@ int nmx_parse_matrix_text(nmx_ctx* c, const char* text, uint64_t T, int64_t info
       code = TXT_VALUE, line = r[TR_VALUE];
     } else if (r[TR_ORDER] != none) {
       code = TXT_ORDER, line = r[TR_ORDER];
-    } else if (r[TR_WIDE] != none || h[0] > (1ll << 32)) {
-      code = TXT_WIDE, line = r[TR_WIDE] != none ? r[TR_WIDE] : l0 + 1;
+    } else if (h[0] > (1ll << 32)) {  // row / col beyond the 32-bit key halves
+      code = TXT_WIDE, line = l0 + 1;
     }
     if (code != TXT_OK) {
       nmx_coo_free(o);
@@ -2659,7 +2660,7 @@ nmx_coo* coo_alloc(nmx_ctx* c, uint64_t nnz) {
   o->nnz = nnz;
   if (nnz) {
     CK(cudaMallocAsync(reinterpret_cast<void**>(&o->keys), nnz * 8, c->st));
-    CK(cudaMallocAsync(reinterpret_cast<void**>(&o->counts), nnz * 4, c->st));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&o->counts), nnz * 8, c->st));
   }
   return o;
 }
@@ -2711,14 +2712,12 @@ int nmx_coo_from_packets(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_ds
 int nmx_coo_upload(nmx_ctx* c, const uint64_t* keys, const int64_t* counts, uint64_t nnz, nmx_coo** out) {
   if (!out || (nnz && (!keys || !counts))) return fail(NMX_EINVAL, "null argument");
   for (uint64_t i = 0; i < nnz; ++i)
-    if (counts[i] < 1 || counts[i] > 0xFFFFFFFFll) return fail(NMX_EINVAL, "COO counts must lie in [1, 2^32-1]");
+    if (counts[i] < 1) return fail(NMX_EINVAL, "COO counts must be >= 1");
   return guarded(c, [&] {
-    std::vector<uint32_t> cc(nnz);
-    for (uint64_t i = 0; i < nnz; ++i) cc[i] = (uint32_t)counts[i];
     nmx_coo* o = coo_alloc(c, nnz);
     if (nnz) {
       CK(cudaMemcpyAsync(o->keys, keys, nnz * 8, cudaMemcpyHostToDevice, c->st));
-      CK(cudaMemcpyAsync(o->counts, cc.data(), nnz * 4, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(o->counts, counts, nnz * 8, cudaMemcpyHostToDevice, c->st));
     }
     CK(cudaStreamSynchronize(c->st));
     *out = o;
@@ -2751,16 +2750,16 @@ int nmx_coo_merge_add(nmx_ctx* c, const nmx_coo* a, const nmx_coo* b, nmx_coo** 
           c->status.as<uint64_t>(), c->next_epoch(), c->small.as<uint32_t>() + kCounters + 28, o->keys, o->counts,
           ovf, ovf + 1);
       CK_LAUNCH();
-      c->dom_end(12 * n);  // + 12 B per output link, added below
+      c->dom_end(16 * n);  // + 16 B per output link, added below
       c->launches += 2;
       unsigned long long res[2] = {0, 0};
       CK(cudaMemcpyAsync(res, ovf, 16, cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
-      c->dom_bytes += 12 * (uint64_t)res[1];
+      c->dom_bytes += 16 * (uint64_t)res[1];
       o->nnz = res[1];
       if (res[0]) {
         nmx_coo_free(o);
-        return fail(NMX_EINVAL, "merged link count exceeds 2^32-1");
+        return fail(NMX_EINVAL, "merged link count exceeds 2^63-1");
       }
     }
     stage_finish(c, 1);
@@ -2782,20 +2781,45 @@ int nmx_coo_stats9(nmx_ctx* c, const nmx_coo* a, int64_t out[9]) {
       coo_link_stats_kernel<<<grid, 256, 0, c->st>>>(a->counts, u, st);
       CK_LAUNCH();
       CK(cudaMemcpyAsync(st + S_LINKS, &u, 8, cudaMemcpyHostToDevice, c->st));
-      if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
-        CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
-      // rows: segments of equal src over the sorted keys (fan-out = links, packets = counts)
-      col_kernel<uint64_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
-          a->keys, a->counts, (uint32_t)u, 32, 0, c->csstatus.as<CSStatus>(), c->next_epoch(), d_small + kCounters + 27,
-          st, 32, S_SRCS, S_MAXFANOUT, S_MAXSRCPK);
-      CK_LAUNCH();
-      // columns: (dst, count) entries sorted by dst
+      unsigned long long maxc = 0;
+      CK(cudaMemcpyAsync(&maxc, st + S_MAXLINK, 8, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      if (maxc > 0xFFFFFFFFull) {  // a link of >= 2^32 packets: 64-bit tables
+        if (u > (1ull << 28)) throw std::runtime_error("COO with counts >= 2^32 and more than 2^28 links");
+        uint64_t slots = 1;
+        while (slots < 2 * u) slots <<= 1;
+        c->cgk.grow(slots * 24);
+        auto* tk = c->cgk.as<unsigned long long>();
+        for (int side = 0; side < 2; ++side) {
+          CK(cudaMemsetAsync(tk, 0, slots * 24, c->st));
+          wide_table_add_kernel<<<grid, 256, 0, c->st>>>(a->keys, a->counts, u, side ? 0 : 32, tk, tk + slots,
+                                                         tk + 2 * slots, slots - 1);
+          CK_LAUNCH();
+          const unsigned rg = (unsigned)std::min<uint64_t>((slots + 255) / 256, (uint64_t)c->sms * 8);
+          wide_table_reduce_kernel<<<rg, 256, 0, c->st>>>(tk, tk + slots, tk + 2 * slots, slots, st,
+                                                          side ? S_DSTS : S_SRCS, side ? S_MAXFANIN : S_MAXFANOUT,
+                                                          side ? S_MAXDSTPK : S_MAXSRCPK);
+          CK_LAUNCH();
+        }
+        c->launches += 5;
+        stage_finish(c, 1);
+        copy_out9(c->h_stats, out, 1);
+        return NMX_OK;
+      }
+      // columns: (dst, count) entries; their 32-bit counts (key order) also feed the row segments
       c->ckA.grow(u * 4);
       c->cvA.grow(u * 4);
       c->ckB.grow(u * 4);
       c->cvB.grow(u * 4);
       coo_col_entries_kernel<<<grid, 256, 0, c->st>>>(a->keys, a->counts, u, c->ckA.as<uint32_t>(),
                                                       c->cvA.as<uint32_t>());
+      CK_LAUNCH();
+      if (c->csstatus.grow(tiles_of(u, kSegTile) * sizeof(CSStatus)))
+        CK(cudaMemsetAsync(c->csstatus.p, 0, c->csstatus.cap, c->st));
+      // rows: segments of equal src over the sorted keys (fan-out = links, packets = counts)
+      col_kernel<uint64_t, kSegIPT><<<(unsigned)tiles_of(u, kSegTile), 256, 0, c->st>>>(
+          a->keys, c->cvA.as<uint32_t>(), (uint32_t)u, 32, 0, c->csstatus.as<CSStatus>(), c->next_epoch(),
+          d_small + kCounters + 27, st, 32, S_SRCS, S_MAXFANOUT, S_MAXSRCPK);
       CK_LAUNCH();
       const int Dc = std::min(21, std::max(11, (int)ceil_log2(u) - 9));
       if (u >= (1ull << 20)) {  // MSD partition + shared-memory grouping
@@ -2844,11 +2868,9 @@ int nmx_coo_download(nmx_ctx* c, const nmx_coo* a, uint64_t* keys, int64_t* coun
   if (!a) return fail(NMX_EINVAL, "null argument");
   return guarded(c, [&] {
     if (!a->nnz) return NMX_OK;
-    std::vector<uint32_t> tmp(counts ? a->nnz : 0);
     if (keys) CK(cudaMemcpyAsync(keys, a->keys, a->nnz * 8, cudaMemcpyDeviceToHost, c->st));
-    if (counts) CK(cudaMemcpyAsync(tmp.data(), a->counts, a->nnz * 4, cudaMemcpyDeviceToHost, c->st));
+    if (counts) CK(cudaMemcpyAsync(counts, a->counts, a->nnz * 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
-    for (uint64_t i = 0; counts && i < a->nnz; ++i) counts[i] = tmp[i];
     return NMX_OK;
   });
 }

@@ -1,5 +1,5 @@
 // nmx_merge.cuh -- K10: merge-path element-wise addition of two sorted unique COO
-// matrices (keys (src << 32) | dst, u32 counts). C = A + B is the union of the
+// matrices (keys (src << 32) | dst, u64 counts). C = A + B is the union of the
 // keys; a key present in both inputs gets the sum of its counts. The summed
 // matrix of several windows is exactly
 // build_matrices(stream, window_size=len(stream)) (traffic.py:221-242).
@@ -13,7 +13,8 @@
 //                           the sum, also across a tile boundary), tile offsets by
 //                           decoupled lookback, compacted output staged in shared
 //                           memory and written coalesced.
-// Traffic: 12 B read + 12 B written per merged position (keys u64 + counts u32).
+// Traffic: 16 B read + 16 B written per merged position (keys u64 + counts u64);
+// a summed count beyond 2^63 - 1 (the reference's int64 values) is reported.
 #pragma once
 #include "nmx_msd.cuh"
 
@@ -49,22 +50,22 @@ __global__ void merge_partition_kernel(const uint64_t* __restrict__ ak, uint64_t
 
 struct MergeSmem {
   uint64_t key[kMgTile];  // A slice [0, la), B slice [la, la + lb); later the compacted output
-  uint32_t cnt[kMgTile];
+  uint64_t cnt[kMgTile];
   uint64_t mkey[kMgTile];  // merged order
-  uint32_t mcnt[kMgTile];
+  uint64_t mcnt[kMgTile];
   uint8_t mfrom[kMgTile];  // 0 = A, 1 = B
   uint32_t wt[kWarps + 1];
   unsigned long long prefix;
   uint32_t tile;
   uint64_t prev_key, next_key;
-  uint32_t next_cnt;
+  uint64_t next_cnt;
   int prev_valid, next_is_b;
 };
 
 __global__ void __launch_bounds__(kMgThreads) merge_add_kernel(
-    const uint64_t* __restrict__ ak, const uint32_t* __restrict__ ac, uint64_t na, const uint64_t* __restrict__ bk,
-    const uint32_t* __restrict__ bc, uint64_t nb, const uint64_t* __restrict__ split, uint64_t* __restrict__ status,
-    uint32_t epoch, uint32_t* __restrict__ tile_counter, uint64_t* __restrict__ ck, uint32_t* __restrict__ cc,
+    const uint64_t* __restrict__ ak, const uint64_t* __restrict__ ac, uint64_t na, const uint64_t* __restrict__ bk,
+    const uint64_t* __restrict__ bc, uint64_t nb, const uint64_t* __restrict__ split, uint64_t* __restrict__ status,
+    uint32_t epoch, uint32_t* __restrict__ tile_counter, uint64_t* __restrict__ ck, uint64_t* __restrict__ cc,
     unsigned long long* __restrict__ overflow, unsigned long long* __restrict__ total) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MergeSmem& S = *reinterpret_cast<MergeSmem*>(smem_raw);
@@ -158,9 +159,9 @@ __global__ void __launch_bounds__(kMgThreads) merge_add_kernel(
     } else if (S.next_is_b && S.next_key == S.mkey[q]) {
       c += S.next_cnt;
     }
-    if (c > 0xFFFFFFFFull) atomicAdd(overflow, 1ull);
+    if (c > 0x7FFFFFFFFFFFFFFFull) atomicAdd(overflow, 1ull);  // both inputs < 2^63: no u64 wrap
     S.key[at] = S.mkey[q];
-    S.cnt[at] = (uint32_t)c;
+    S.cnt[at] = c;
     ++at;
   }
   __syncthreads();

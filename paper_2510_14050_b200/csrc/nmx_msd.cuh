@@ -1273,18 +1273,18 @@ __global__ void __launch_bounds__(256) unique_heads_kernel(const uint64_t* __res
   }
 }
 __global__ void run_counts_kernel(const uint32_t* __restrict__ ustart, uint64_t u, uint64_t n,
-                                  uint32_t* __restrict__ counts) {
+                                  uint64_t* __restrict__ counts) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < u; j += (uint64_t)gridDim.x * blockDim.x)
-    counts[j] = (uint32_t)((j + 1 < u ? ustart[j + 1] : n) - ustart[j]);
+    counts[j] = (j + 1 < u ? ustart[j + 1] : n) - ustart[j];
 }
 
 // link statistics of a COO (valid, links, max link)
-__global__ void coo_link_stats_kernel(const uint32_t* __restrict__ cnt, uint64_t n,
+__global__ void coo_link_stats_kernel(const uint64_t* __restrict__ cnt, uint64_t n,
                                       unsigned long long* __restrict__ stats) {
   unsigned long long v = 0, mx = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     v += cnt[i];
-    mx = max(mx, (unsigned long long)cnt[i]);
+    mx = max(mx, (unsigned long long)cnt[i]);  // counts < 2^63: unsigned = signed order
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -1298,11 +1298,57 @@ __global__ void coo_link_stats_kernel(const uint32_t* __restrict__ cnt, uint64_t
 }
 
 // destinations of a COO as (dst, count) column entries
-__global__ void coo_col_entries_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ cnt, uint64_t n,
+// (counts narrowed: the caller checked max count <= 2^32 - 1)
+__global__ void coo_col_entries_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ cnt, uint64_t n,
                                        uint32_t* __restrict__ ck, uint32_t* __restrict__ cv) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     ck[i] = (uint32_t)keys[i];
-    cv[i] = cnt[i];
+    cv[i] = (uint32_t)cnt[i];
+  }
+}
+
+// Row / column statistics of a COO whose counts exceed 32 bits (a summed matrix
+// with a link of >= 2^32 packets): one open-addressing table per side keyed by
+// address + 1 (0 = empty), packets and links summed with 64-bit atomics, then a
+// reduction over the slots. The 32-bit grouping kernels pack counts into the low
+// word of their items, so these rare matrices take this path instead.
+__global__ void wide_table_add_kernel(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ cnt, uint64_t n,
+                                      int shift, unsigned long long* __restrict__ tkey,
+                                      unsigned long long* __restrict__ tpk, unsigned long long* __restrict__ tln,
+                                      uint64_t mask) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ((keys[i] >> shift) & 0xFFFFFFFFull) + 1;
+    uint64_t h = ((k * 0x9E3779B97F4A7C15ull) >> 20) & mask;
+    for (;;) {
+      const unsigned long long c0 = atomicCAS(tkey + h, 0ull, k);
+      if (c0 == 0ull || c0 == k) break;
+      h = (h + 1) & mask;
+    }
+    atomicAdd(tpk + h, (unsigned long long)cnt[i]);
+    atomicAdd(tln + h, 1ull);
+  }
+}
+__global__ void wide_table_reduce_kernel(const unsigned long long* __restrict__ tkey,
+                                         const unsigned long long* __restrict__ tpk,
+                                         const unsigned long long* __restrict__ tln, uint64_t slots,
+                                         unsigned long long* __restrict__ stats, int s_cnt, int s_len, int s_sum) {
+  unsigned long long nz = 0, ml = 0, mp = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < slots; i += (uint64_t)gridDim.x * blockDim.x)
+    if (tkey[i]) {
+      ++nz;
+      ml = max(ml, tln[i]);
+      mp = max(mp, tpk[i]);
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    nz += __shfl_xor_sync(FULL, nz, o);
+    ml = max(ml, __shfl_xor_sync(FULL, ml, o));
+    mp = max(mp, __shfl_xor_sync(FULL, mp, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(stats + s_cnt, nz);
+    atomicMax(stats + s_len, ml);
+    atomicMax(stats + s_sum, mp);
   }
 }
 

@@ -147,12 +147,12 @@ __global__ void text_nonblank_kernel(const uint8_t* __restrict__ ntok, uint64_t 
     nb[l] = (ntok[l] & 0x7F) ? 1u : 0u;
 }
 
-// entry lines (nonblank j >= 1) -> COO key (row << 32 | col), u32 count and the line
-// number; the first field / integer error as (line << 4 | code), the first bounds,
-// value and beyond-device-range lines (1-based physical line numbers)
+// entry lines (nonblank j >= 1) -> COO key (row << 32 | col), int64 value and the
+// line number; the first field / integer error as (line << 4 | code), the first
+// bounds and value lines (1-based physical line numbers)
 __global__ void text_entries_kernel(const uint8_t* __restrict__ ntok, const long long* __restrict__ vals,
                                     const uint32_t* __restrict__ nboff, uint64_t L, long long dim,
-                                    unsigned long long* __restrict__ keys, uint32_t* __restrict__ cnt,
+                                    unsigned long long* __restrict__ keys, uint64_t* __restrict__ cnt,
                                     uint32_t* __restrict__ eline, unsigned long long* __restrict__ red) {
   for (uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; l < L; l += (uint64_t)gridDim.x * blockDim.x) {
     const uint8_t t = ntok[l];
@@ -177,9 +177,8 @@ __global__ void text_entries_kernel(const uint8_t* __restrict__ ntok, const long
       continue;
     }
     if (v[2] < 1) atomicMin(red + TR_VALUE, line);
-    if (v[2] > 0xFFFFFFFFll) atomicMin(red + TR_WIDE, line);
     keys[j - 1] = ((unsigned long long)v[0] << 32) | (unsigned long long)v[1];
-    cnt[j - 1] = (uint32_t)v[2];
+    cnt[j - 1] = (uint64_t)v[2];
   }
 }
 

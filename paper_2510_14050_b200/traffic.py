@@ -406,12 +406,12 @@ def _parse_text(path, data: bytes):
     if code == _lib.TXT_BOUNDS:
         raise MatrixFileError(f"{path}: line {line}: row/col outside [0, {dim})")
     if code == _lib.TXT_WIDE:
-        raise MatrixFileError(f"{path}: line {line}: dim or value beyond 2^32 (device matrix range)")
+        raise MatrixFileError(f"{path}: line {line}: dim beyond 2^32 (device matrix range)")
     raise MatrixFileError(f"{path}: line {line}: {_TXT_MESSAGES[code]}")
 
 
 def read_matrix_device(path, window_id: int = 0):
-    """Parse a matrix file on the GPU into a device COO (keys row << 32 | col, u32
+    """Parse a matrix file on the GPU into a device COO (keys row << 32 | col, int64
     counts) without host containers: (dim, DeviceCOO)."""
     from .coo import DeviceCOO
 

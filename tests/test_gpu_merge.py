@@ -103,3 +103,25 @@ def test_merge_add_many_tiles(coo, overlap):
     wk, wc = orc.coo_packed(np.concatenate([s, s2]), np.concatenate([d, d2]))
     assert np.array_equal(keys, wk) and np.array_equal(counts, wc)
     assert m.stats9() == orc.stats9_packed(np.concatenate([s, s2]), np.concatenate([d, d2]))
+
+
+@pytest.mark.parametrize("n", [40, 5000])
+def test_wide_counts_merge_and_stats(coo, n):
+    """u64 counts (the reference's int64 matrix values): merged links beyond 2^32 - 1
+    packets keep their exact sums, and the statistics of such a matrix (the 64-bit
+    hash-table path) equal the oracle's; a sum beyond 2^63 - 1 is rejected."""
+    rng = np.random.default_rng(n)
+    src = rng.integers(0, 1 << 32, n, dtype=np.uint64)
+    dst = rng.integers(0, 50, n, dtype=np.uint64)  # shared destinations: wide column sums
+    keys = np.unique((src << np.uint64(32)) | dst)
+    ca = rng.integers(1, 1 << 40, len(keys), dtype=np.int64)
+    cb = rng.integers(1, 1 << 40, len(keys), dtype=np.int64)
+    a = coo.coo_from_keys(keys, ca)
+    b = coo.coo_from_keys(keys[::2], cb[::2])
+    k, c = coo.merge_add(a, b).download()
+    wk, wc = orc.merge_add_coo(keys, ca, keys[::2], cb[::2])
+    assert np.array_equal(k, wk) and np.array_equal(c, wc) and c.max() > (1 << 32)
+    assert coo.merge_add(a, b).stats9() == orc.stats9_from_coo(wk, wc)
+    big = coo.coo_from_keys(keys[:1], np.array([(1 << 62) + 1], np.int64))
+    with pytest.raises(Exception):
+        coo.merge_add(big, big)
