@@ -648,7 +648,9 @@ def run_nmx(args) -> None:
             ems = float(mt.item())
         e2e = {"value": n_total / (ems / 1e3), "unit": "packets/s", "h2d_bytes_per_step": 8 * n_total,
                "d2h_bytes_per_step": 72 * world, "ms_per_step": ems, "steps": args.e2e_steps,
-               "api": "nmx_stats9_host (include/nmx.h) via paper_2510_14050_b200._lib.stats9, pinned host buffers"}
+               "api": ("nmx_stats9_sharded_host (include/nmx.h, libnmx's NCCL communicator) via "
+                       "paper_2510_14050_b200.distributed.sharded_stats9_host" if world > 1 and backend == "nccl" else
+                       "nmx_stats9_host (include/nmx.h) via paper_2510_14050_b200._lib.stats9") + ", pinned host buffers"}
         hs.close()
         hd.close()
 

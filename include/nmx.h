@@ -252,6 +252,28 @@ int nmx_group_stats9_host(nmx_group* grp, const uint32_t* src, const uint32_t* d
                           uint64_t address_space, uint64_t batch_count, int64_t out[9]);
 int nmx_group_last_exchange(nmx_group* grp, uint64_t* bytes1, uint64_t* bytes2);
 
+/* NCCL communicators: the multi-process form (one process per GPU, the driver's
+ * torchrun launch) of the same sharded pipeline. Rank 0 makes an id with
+ * nmx_comm_unique_id and hands it to every rank out of band (bytes); each rank calls
+ * nmx_comm_init on its context (collective). nmx_stats9_sharded[_host] runs exchange 1
+ * (valid packets to owner(src)), links + rows, exchange 2 ((dst, count) of unique links
+ * to owner(dst)), columns and the SUM / MAX combine inside the library: grouped
+ * ncclSend / ncclRecv on the context stream for both all-to-alls, ncclAllGather for
+ * the part counts, two ncclAllReduce for the statistics. Every rank gets the nine
+ * statistics of the matrix summed over all ranks' packets (bit-identical to one
+ * device). Replaces the reference's make_group_scheduler(G) fan-out
+ * (resources.py:139-159, analytics.py:68-81) across processes. */
+#define NMX_COMM_ID_BYTES 128
+typedef struct nmx_comm nmx_comm;
+int nmx_comm_unique_id(uint8_t* id);
+int nmx_comm_init(nmx_ctx* ctx, const uint8_t* id, int nranks, int rank, nmx_comm** out);
+void nmx_comm_destroy(nmx_comm* comm);
+int nmx_stats9_sharded(nmx_ctx* ctx, nmx_comm* comm, const uint32_t* d_src, const uint32_t* d_dst,
+                       const uint8_t* d_valid, uint64_t n, uint64_t address_space, int64_t out[9]);
+int nmx_stats9_sharded_host(nmx_ctx* ctx, nmx_comm* comm, const uint32_t* src, const uint32_t* dst,
+                            const uint8_t* valid, uint64_t n, uint64_t address_space, int64_t out[9]);
+int nmx_comm_last_exchange(nmx_comm* comm, uint64_t* bytes1, uint64_t* bytes2);
+
 /* Timing hooks used by bench.py: CUDA-event time (ms) of the last hot-path
  * call's whole device section, and of its sort / partition section (the MSD
  * row partition, or the onesweep passes on the LSD path) summed over launches,

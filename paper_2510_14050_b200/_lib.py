@@ -80,6 +80,12 @@ SIGNATURES = {
     "nmx_group_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "nmx_group_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _VP]),
     "nmx_group_last_exchange": (C.c_int, [_VP, C.POINTER(_U64), C.POINTER(_U64)]),
+    "nmx_comm_unique_id": (C.c_int, [_VP]),
+    "nmx_comm_init": (C.c_int, [_VP, _VP, C.c_int, C.c_int, C.POINTER(_VP)]),
+    "nmx_comm_destroy": (None, [_VP]),
+    "nmx_stats9_sharded": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_stats9_sharded_host": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_comm_last_exchange": (C.c_int, [_VP, C.POINTER(_U64), C.POINTER(_U64)]),
     "nmx_last_kernel_class": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_int), C.POINTER(_U64), C.c_char_p,
                                          C.c_int]),
     "nmx_last_stages": (C.c_int, [_VP, C.POINTER(C.c_float), C.c_int]),
@@ -332,6 +338,55 @@ def stats9(src, dst, valid=None, address_space: int = 1 << 32, device: int = 0) 
         check(ctx._lib.nmx_stats9_host(ctx.handle, _ptr(s), _ptr(d), _ptr(v), len(s), int(address_space),
                                        out.ctypes.data))
     return tuple(int(x) for x in out)
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL communicator id (nmx_comm_unique_id) for rank 0 to hand out."""
+    lib = load()
+    buf = (C.c_uint8 * 128)()
+    check(lib.nmx_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Communicator:
+    """libnmx's own NCCL communicator for this process's rank (nmx_comm): the sharded
+    nine statistics run inside the library (grouped ncclSend / ncclRecv exchanges,
+    ncclAllGather of the part counts, ncclAllReduce SUM / MAX) on the context stream."""
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int = 0):
+        if len(uid) != 128:
+            raise ValueError("an NCCL id is 128 bytes")
+        self.ctx = context(device)
+        self.device, self.world, self.rank = device, world, rank
+        self._h = C.c_void_p()
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(self.ctx._lib.nmx_comm_init(self.ctx.handle, idbuf, int(world), int(rank), C.byref(self._h)))
+
+    def stats9(self, src, dst, valid=None, address_space: int = 1 << 32) -> tuple:
+        """This rank's packets (device tensors / DeviceArrays, or host arrays) -> the
+        nine statistics of the matrix summed over every rank's packets."""
+        out = np.zeros(9, dtype=np.int64)
+        if _is_device(src):
+            n = int(src.numel())
+            check(self.ctx._lib.nmx_stats9_sharded(self.ctx.handle, self._h, _ptr(src), _ptr(dst), _ptr(valid), n,
+                                                   int(address_space), out.ctypes.data))
+        else:
+            s, d, v = _u32_host(src), _u32_host(dst), _valid_host(valid)
+            if len(s) != len(d) or (v is not None and len(v) != len(s)):
+                raise ValueError("src, dst and valid must have equal lengths")
+            check(self.ctx._lib.nmx_stats9_sharded_host(self.ctx.handle, self._h, _ptr(s), _ptr(d), _ptr(v), len(s),
+                                                        int(address_space), out.ctypes.data))
+        return tuple(int(x) for x in out)
+
+    def last_exchange(self) -> tuple:
+        a, b = C.c_uint64(), C.c_uint64()
+        check(self.ctx._lib.nmx_comm_last_exchange(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+    def close(self) -> None:
+        if self._h:
+            self.ctx._lib.nmx_comm_destroy(self._h)
+            self._h = C.c_void_p()
 
 
 def stream_stats9(windows, address_space: int = 1 << 32, device: int = 0) -> tuple:

@@ -1,5 +1,6 @@
 // nmx_api.cu -- context, workspace and the C ABI of libnmx.so (include/nmx.h).
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <condition_variable>
@@ -1967,6 +1968,117 @@ int group_run(nmx_group* G, const std::function<void(int)>& body, int64_t* out) 
   return NMX_OK;
 }
 
+// ---- NCCL communicators: one process per GPU -----------------
+// The multi-process form of the sharded pipeline: each rank is a process with its own
+// nmx_ctx and one NCCL communicator. Both all-to-all exchanges are grouped
+// ncclSend / ncclRecv on the context stream (src and dst columns of a part in one
+// group, so NCCL moves them together over NVLink / NVSwitch), the per-part counts an
+// ncclAllGather, and the final combine two ncclAllReduce (SUM, MAX) on int64 -- no
+// host staging, no torch on the data path.
+struct CommBufs {
+  DevBuf ps, pd, rs, rd, cs, cc, qs, qc, hs, hd, hv, cnt, red;
+};
+
+#define NK(x)                                                                                       \
+  do {                                                                                              \
+    ncclResult_t r_ = (x);                                                                          \
+    if (r_ != ncclSuccess) throw std::runtime_error(std::string("NCCL: ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+}  // namespace
+
+struct nmx_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 0, rank = 0, device = 0;
+  CommBufs b;
+  uint64_t last_x1 = 0, last_x2 = 0;
+};
+
+namespace {
+
+// rank r sends part p of (sa, sb) (cnt[p] items, parts back to back) to rank p and
+// receives every rank's part r into (ra, rb) in rank order; returns the items received
+uint64_t comm_exchange(nmx_comm* K, nmx_ctx* c, const uint32_t* sa, const uint32_t* sb, const uint64_t* cnt,
+                       DevBuf& ra, DevBuf& rb) {
+  const int g = K->nranks, r = K->rank;
+  K->b.cnt.grow((size_t)(g + 1) * g * 8);
+  auto* dc = K->b.cnt.as<unsigned long long>();
+  std::vector<unsigned long long> mine(cnt, cnt + g), all((size_t)g * g);
+  CK(cudaMemcpyAsync(dc + (size_t)g * g, mine.data(), g * 8, cudaMemcpyHostToDevice, c->st));
+  NK(ncclAllGather(dc + (size_t)g * g, dc, g, ncclUint64, K->comm, c->st));
+  CK(cudaMemcpyAsync(all.data(), dc, (size_t)g * g * 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  uint64_t tot = 0;
+  for (int q = 0; q < g; ++q) tot += all[(size_t)q * g + r];
+  ra.grow(std::max<uint64_t>(tot, 1) * 4);
+  rb.grow(std::max<uint64_t>(tot, 1) * 4);
+  NK(ncclGroupStart());
+  uint64_t soff = 0, roff = 0;
+  for (int p = 0; p < g; ++p) {
+    const uint64_t sl = cnt[p], rl = all[(size_t)p * g + r];
+    if (sl) {
+      NK(ncclSend(sa + soff, sl, ncclUint32, p, K->comm, c->st));
+      NK(ncclSend(sb + soff, sl, ncclUint32, p, K->comm, c->st));
+    }
+    if (rl) {
+      NK(ncclRecv(ra.as<uint32_t>() + roff, rl, ncclUint32, p, K->comm, c->st));
+      NK(ncclRecv(rb.as<uint32_t>() + roff, rl, ncclUint32, p, K->comm, c->st));
+    }
+    soff += sl;
+    roff += rl;
+  }
+  NK(ncclGroupEnd());
+  return tot;
+}
+
+// this rank's share: exchange 1 (owner(src)), links + rows, exchange 2 (owner(dst)),
+// columns, SUM / MAX all-reduce of the nine statistics
+int comm_run(nmx_comm* K, nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+             uint64_t n, uint64_t space, int64_t* out) {
+  const int g = K->nranks;
+  uint64_t cnt1[kMaxParts] = {0}, cnt2[kMaxParts] = {0};
+  K->b.ps.grow(std::max<uint64_t>(n, 1) * 4);
+  K->b.pd.grow(std::max<uint64_t>(n, 1) * 4);
+  if (n) {
+    if (int rc = check_addresses(c, d_src, d_dst, n, space)) return rc;
+    PacketPart it{d_src, d_dst, d_valid, K->b.ps.as<uint32_t>(), K->b.pd.as<uint32_t>()};
+    partition_items(c, it, n, g, cnt1);
+  }
+  const uint64_t m = comm_exchange(K, c, K->b.ps.as<uint32_t>(), K->b.pd.as<uint32_t>(), cnt1, K->b.rs, K->b.rd);
+  if (m >= (1ull << 32)) throw std::runtime_error("more than 2^32-1 packets routed to one rank");
+  K->b.cs.grow(std::max<uint64_t>(m, 1) * 4);
+  K->b.cc.grow(std::max<uint64_t>(m, 1) * 4);
+  int64_t row9[S_COUNT], col9[S_COUNT];
+  if (int rc = shard_rows_impl(c, K->b.rs.as<uint32_t>(), K->b.rd.as<uint32_t>(), m, space, g,
+                               K->b.cs.as<uint32_t>(), K->b.cc.as<uint32_t>(), cnt2, row9))
+    return rc;
+  const uint64_t u = comm_exchange(K, c, K->b.cs.as<uint32_t>(), K->b.cc.as<uint32_t>(), cnt2, K->b.qs, K->b.qc);
+  if (int rc = shard_cols_impl(c, K->b.qs.as<uint32_t>(), K->b.qc.as<uint32_t>(), u, space, col9)) return rc;
+  static const bool kSum[S_COUNT] = {true, true, false, true, false, false, true, false, false};
+  int64_t sv[2 * S_COUNT];
+  for (int i = 0; i < S_COUNT; ++i) {
+    const int64_t v = i < 6 ? row9[i] : col9[i];
+    sv[i] = kSum[i] ? v : 0;
+    sv[S_COUNT + i] = kSum[i] ? 0 : v;
+  }
+  K->b.red.grow(2 * S_COUNT * 8);
+  auto* dr = K->b.red.as<int64_t>();
+  CK(cudaMemcpyAsync(dr, sv, sizeof(sv), cudaMemcpyHostToDevice, c->st));
+  NK(ncclGroupStart());
+  NK(ncclAllReduce(dr, dr, S_COUNT, ncclInt64, ncclSum, K->comm, c->st));
+  NK(ncclAllReduce(dr + S_COUNT, dr + S_COUNT, S_COUNT, ncclInt64, ncclMax, K->comm, c->st));
+  NK(ncclGroupEnd());
+  CK(cudaMemcpyAsync(sv, dr, sizeof(sv), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  for (int i = 0; i < S_COUNT; ++i) out[i] = kSum[i] ? sv[i] : sv[S_COUNT + i];
+  K->last_x1 = K->last_x2 = 0;
+  for (int p = 0; p < g; ++p) {
+    K->last_x1 += cnt1[p] * 8;
+    K->last_x2 += cnt2[p] * 8;
+  }
+  return NMX_OK;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -3026,6 +3138,81 @@ int nmx_group_stats9_host(nmx_group* G, const uint32_t* src, const uint32_t* dst
                        address_space);
       },
       out);
+}
+
+int nmx_comm_unique_id(uint8_t* id) {
+  if (!id) return fail(NMX_EINVAL, "null id");
+  static_assert(sizeof(ncclUniqueId) == NMX_COMM_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId u;
+  const ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return fail(NMX_ECUDA, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  memcpy(id, &u, sizeof(u));
+  return NMX_OK;
+}
+
+int nmx_comm_init(nmx_ctx* c, const uint8_t* id, int nranks, int rank, nmx_comm** out) {
+  if (!id || !out) return fail(NMX_EINVAL, "null argument");
+  if (nranks < 1 || nranks > kMaxParts || rank < 0 || rank >= nranks)
+    return fail(NMX_EINVAL, "need 1 <= nranks <= %d and 0 <= rank < nranks", kMaxParts);
+  *out = nullptr;
+  return guarded(c, [&] {
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof(u));
+    auto* K = new nmx_comm();
+    K->nranks = nranks;
+    K->rank = rank;
+    K->device = c->device;
+    const ncclResult_t r = ncclCommInitRank(&K->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+      delete K;
+      return fail(NMX_ECUDA, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    *out = K;
+    return NMX_OK;
+  });
+}
+
+void nmx_comm_destroy(nmx_comm* K) {
+  if (!K) return;
+  cudaSetDevice(K->device);
+  if (K->comm) ncclCommDestroy(K->comm);
+  delete K;
+}
+
+int nmx_stats9_sharded(nmx_ctx* c, nmx_comm* K, const uint32_t* d_src, const uint32_t* d_dst,
+                       const uint8_t* d_valid, uint64_t n, uint64_t address_space, int64_t out[9]) {
+  if (!K || !out || (n && (!d_src || !d_dst))) return fail(NMX_EINVAL, "null argument");
+  if (K->device != (c ? c->device : -1)) return fail(NMX_EINVAL, "communicator and context on different devices");
+  int b;
+  if (int r = check_space(address_space, b)) return r;
+  return guarded(c, [&] { return comm_run(K, c, d_src, d_dst, d_valid, n, address_space, out); });
+}
+
+int nmx_stats9_sharded_host(nmx_ctx* c, nmx_comm* K, const uint32_t* src, const uint32_t* dst,
+                            const uint8_t* valid, uint64_t n, uint64_t address_space, int64_t out[9]) {
+  if (!K || !out || (n && (!src || !dst))) return fail(NMX_EINVAL, "null argument");
+  if (K->device != (c ? c->device : -1)) return fail(NMX_EINVAL, "communicator and context on different devices");
+  int b;
+  if (int r = check_space(address_space, b)) return r;
+  return guarded(c, [&] {
+    K->b.hs.grow(std::max<uint64_t>(n, 1) * 4);
+    K->b.hd.grow(std::max<uint64_t>(n, 1) * 4);
+    if (valid) K->b.hv.grow(std::max<uint64_t>(n, 1));
+    if (n) {
+      CK(cudaMemcpyAsync(K->b.hs.p, src, n * 4, cudaMemcpyHostToDevice, c->st));
+      CK(cudaMemcpyAsync(K->b.hd.p, dst, n * 4, cudaMemcpyHostToDevice, c->st));
+      if (valid) CK(cudaMemcpyAsync(K->b.hv.p, valid, n, cudaMemcpyHostToDevice, c->st));
+    }
+    return comm_run(K, c, K->b.hs.as<uint32_t>(), K->b.hd.as<uint32_t>(), valid ? K->b.hv.as<uint8_t>() : nullptr,
+                    n, address_space, out);
+  });
+}
+
+int nmx_comm_last_exchange(nmx_comm* K, uint64_t* bytes1, uint64_t* bytes2) {
+  if (!K) return fail(NMX_EINVAL, "null communicator");
+  if (bytes1) *bytes1 = K->last_x1;
+  if (bytes2) *bytes2 = K->last_x2;
+  return NMX_OK;
 }
 
 int nmx_group_last_exchange(nmx_group* G, uint64_t* bytes1, uint64_t* bytes2) {

@@ -1,5 +1,11 @@
 """Multi-GPU nine statistics: one process per GPU, NCCL all-to-all exchange.
 
+Production (NCCL process group): the whole pipeline below runs inside libnmx.so
+through its own NCCL communicator (``nmx_stats9_sharded``, ``_lib.Communicator``);
+torch.distributed only hands the 128-byte communicator id from rank 0 to the others.
+The Python orchestration in ``sharded_stats9`` is the same pipeline with the
+exchanges in torch.distributed, kept for gloo (CPU tests, several ranks on one GPU).
+
 SURVEY.md 8(e). Each rank holds a contiguous shard of the packet stream
 (partition_even rule, partitioning.py:62-70). The summed matrix's statistics
 need one exchange per axis:
@@ -207,7 +213,35 @@ class _DeviceView:
                                          "strides": None}
 
 
+_COMMS: dict = {}
+
+
+def native_communicator(device: int, group=None):
+    """libnmx's NCCL communicator for this rank of ``group`` (made once: rank 0 draws the
+    id, torch.distributed broadcasts its 128 bytes -- the only use of the process group);
+    None when the group's backend is not NCCL (gloo: CPU tests, several ranks on one GPU)."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) != "nccl":
+        return None
+    key = (device, id(group))
+    comm = _COMMS.get(key)
+    if comm is None:
+        from . import _lib
+
+        box = [_lib.comm_unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        comm = _COMMS[key] = _lib.Communicator(box[0], dist.get_world_size(group), dist.get_rank(group), device)
+    return comm
+
+
 def sharded_stats9_device(src, dst, address_space: int, device: int = 0, valid=None, group=None) -> tuple:
+    """This rank's device shard -> the summed matrix's nine statistics. On NCCL the whole
+    pipeline runs in libnmx (nmx_stats9_sharded); gloo runs the same stages with the
+    exchanges in torch.distributed (host-staged)."""
+    comm = native_communicator(device, group)
+    if comm is not None:
+        return comm.stats9(src, dst, valid, address_space)
     ops = _cuda_ops(device)
     return sharded_stats9(as_i32_tensor(src, device), as_i32_tensor(dst, device), valid, address_space, ops, group)
 
@@ -218,6 +252,9 @@ def sharded_stats9_host(src: np.ndarray, dst: np.ndarray, address_space: int, de
 
     from ._lib import _u32_host
 
+    comm = native_communicator(device, group)
+    if comm is not None:
+        return comm.stats9(src, dst, None, address_space)
     # range-checked u32 first (an int64 column reinterpreted as int32 would be two words per address)
     s = torch.from_numpy(_u32_host(src).view(np.int32)).to(f"cuda:{device}", non_blocking=True)
     d = torch.from_numpy(_u32_host(dst).view(np.int32)).to(f"cuda:{device}", non_blocking=True)

@@ -106,8 +106,39 @@ def test_nccl_world_of_one():
         assert got == orc.stats9_packed(ds.download(), dd.download())
         hs, hd = ds.download(), dd.download()
         assert nd.sharded_stats9_host(hs, hd, 1 << 32) == got
+        # the NCCL group ran libnmx's own communicator, not the torch exchanges
+        comm = nd.native_communicator(0)
+        assert comm is not None and comm.last_exchange() == (8 * n, 8 * got[1])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("lg,space,kind", [(0, 1 << 32, "uniform"), (12, 7, "uniform"), (18, 5000, "powerlaw"),
+                                           (21, 1 << 32, "powerlaw"), (22, 1 << 32, "uniform")])
+def test_native_communicator_world_of_one(lg, space, kind):
+    """nmx_comm without torch.distributed: id -> nmx_comm_init -> nmx_stats9_sharded[_host]
+    (grouped ncclSend / ncclRecv to itself, ncclAllGather, ncclAllReduce) equals the oracle,
+    invalid packets included."""
+    from paper_2510_14050_b200 import _lib
+
+    comm = _lib.Communicator(_lib.comm_unique_id(), 1, 0, device=0)
+    try:
+        n = (1 << lg) if lg else 0
+        g = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
+        s, d = g(21, 0, n, space)
+        v = np.random.default_rng(lg).random(n) >= 0.2
+        want = orc.stats9_packed(s, d, v)
+        assert comm.stats9(s, d, v, space) == want
+        if n:
+            ds, dd = _lib.DeviceArray(n), _lib.DeviceArray(n)
+            ds.upload(s)
+            dd.upload(d)
+            assert comm.stats9(ds, dd, None, space) == orc.stats9_packed(s, d)
+        if n and space < (1 << 32):  # addresses beyond the address space are rejected, not packed
+            with pytest.raises(Exception, match="address"):
+                comm.stats9(s, d + np.uint32(space), None, space)
+    finally:
+        comm.close()
 
 
 def _gpu_worker(rank, world, port, cases, q):
