@@ -452,8 +452,8 @@ def run_cli(args) -> None:
     with tempfile.TemporaryDirectory() as d:
         manifest = cli.cmd_generate(n=n, address_space=space, seed=1, window_size=cli.DEFAULT_WINDOW, out_dir=d)
         for _ in range(args.warmup):
-            cli._timed_run(d, 1, None, 1)
-        runs = [cli._timed_run(d, 1, None, 1) for _ in range(args.steps)]
+            cli.run_cell(d, 1, None, 1)
+        runs = [cli.run_cell(d, 1, None, 1) for _ in range(args.steps)]
         best_e2e = min(r[2].end_to_end_time for r in runs)
         best_an = min(r[2].analysis_time for r in runs)
         totals = runs[0][1]
