@@ -340,8 +340,23 @@ def stats9(src, dst, valid=None, address_space: int = 1 << 32, device: int = 0) 
     return tuple(int(x) for x in out)
 
 
+def _prefer_bundled_nccl() -> None:
+    """libnmx opens NCCL at first use; point it at the nvidia-nccl wheel's library (the
+    one torch loads) so one process never mixes two NCCL versions under one soname."""
+    if os.environ.get("NMX_NCCL_LIB"):
+        return
+    import sys
+
+    for p in sys.path:
+        cand = Path(p) / "nvidia" / "nccl" / "lib" / "libnccl.so.2"
+        if cand.exists():
+            os.environ["NMX_NCCL_LIB"] = str(cand)
+            return
+
+
 def comm_unique_id() -> bytes:
     """A fresh NCCL communicator id (nmx_comm_unique_id) for rank 0 to hand out."""
+    _prefer_bundled_nccl()
     lib = load()
     buf = (C.c_uint8 * 128)()
     check(lib.nmx_comm_unique_id(buf))
@@ -356,6 +371,7 @@ class Communicator:
     def __init__(self, uid: bytes, world: int, rank: int, device: int = 0):
         if len(uid) != 128:
             raise ValueError("an NCCL id is 128 bytes")
+        _prefer_bundled_nccl()
         self.ctx = context(device)
         self.device, self.world, self.rank = device, world, rank
         self._h = C.c_void_p()

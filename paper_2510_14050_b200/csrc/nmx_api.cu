@@ -1,8 +1,10 @@
 // nmx_api.cu -- context, workspace and the C ABI of libnmx.so (include/nmx.h).
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is opened at run time (nccl_api)
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <functional>
 #include <thread>
@@ -29,6 +31,9 @@ using namespace nmx;
 namespace {
 
 thread_local std::string g_err;
+thread_local bool g_capturing = false;  // a CUDA graph capture is open on this thread
+// bumped whenever a device buffer is freed or moved: recorded graphs hold raw pointers
+std::atomic<uint64_t> g_buf_gen{0};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -62,6 +67,9 @@ struct DevBuf {
   // grow (never shrinks); returns true when (re)allocated (contents undefined / zeroed by caller)
   bool grow(size_t bytes) {
     if (bytes <= cap) return false;
+    // a captured node may already point at the old buffer: the capture is abandoned
+    if (g_capturing) throw std::runtime_error("buffer growth during graph capture");
+    ++g_buf_gen;
     if (p) CK(cudaFree(p));
     p = nullptr;
     cap = 0;
@@ -81,7 +89,10 @@ struct DevBuf {
     return reinterpret_cast<T*>(p);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      ++g_buf_gen;
+      cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
   }
@@ -152,6 +163,18 @@ struct nmx_ctx {
   // deferred partition read-back (msd_partition(defer) -> msd_partition_wait)
   cudaEvent_t evw = nullptr;
   bool joint_ready = false;  // streamed windows left the level-2 counts in mhist2
+  int scr_off = 0;            // scr() slots of the pending partition read-back (rows 0, columns 8)
+  // CUDA graphs of whole small calls (run_pipeline_msd_graph), keyed by inputs and size
+  struct CallGraph {
+    const void *s, *d, *v;
+    uint64_t n, space;
+    cudaGraphExec_t exec;
+    uint64_t gen;  // g_buf_gen when recorded
+    int launches;  // kernels in the graph
+  };
+  std::vector<CallGraph> graphs;
+  bool capturing = false;
+  bool had_heavy = false;  // the last call sent buckets through the segmented levels
   uint64_t pend_bytes_per_m = 0;
   int pend_L = 0;
   float last_total_ms = 0, last_sort_ms = 0;
@@ -181,12 +204,15 @@ struct nmx_ctx {
   }
   void grow_hstats(size_t words) {
     if (words <= h_stats_cap) return;
+    ++g_buf_gen;
     if (h_stats) cudaFreeHost(h_stats);
     h_stats = nullptr;
     CK(cudaMallocHost(&h_stats, words * sizeof(unsigned long long)));
     h_stats_cap = words;
   }
-  void mark() { CK(cudaEventRecord(ev[nev++], st)); }
+  void mark() {
+    if (!capturing) CK(cudaEventRecord(ev[nev++], st));
+  }
   // dominant-kernel accounting (event pairs around each launch of the class)
   cudaEvent_t evk[64];
   int nevk = 0;
@@ -197,6 +223,10 @@ struct nmx_ctx {
   bool dom_cur = false;
   // the first kernel class that reports in a call owns the accounting
   void dom_begin(const char* nm) {
+    if (capturing) {
+      dom_cur = false;
+      return;
+    }
     if (!dom_name[0]) dom_name = nm;
     dom_cur = strcmp(dom_name, nm) == 0 && nevk + 2 <= 64;
     if (dom_cur) CK(cudaEventRecord(evk[nevk], st));
@@ -357,6 +387,7 @@ void stage_begin(nmx_ctx* c, uint64_t W) {
   c->launches = 0;
   c->last_sort_launches = 0;
   c->last_sort_ms = 0;
+  c->had_heavy = false;
   c->small.grow(kSmallWords * sizeof(uint32_t));
   if (!c->h_small) CK(cudaMallocHost(&c->h_small, kSmallWords * sizeof(uint32_t)));
   c->stats.grow(W * S_COUNT * sizeof(unsigned long long));
@@ -369,6 +400,7 @@ void stage_begin(nmx_ctx* c, uint64_t W) {
 void stage_finish(nmx_ctx* c, uint64_t W) {
   CK(cudaMemcpyAsync(c->h_stats, c->stats.p, W * S_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      c->st));
+  if (c->capturing) return;  // a graph replay is timed and waited on by its caller
   c->mark();  // end
   CK(cudaStreamSynchronize(c->st));
   CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[c->nev - 1]));
@@ -658,8 +690,12 @@ struct MsdSplit {
 // Waits for a partition's read-back (work queued after it keeps the GPU busy
 // meanwhile): returns m, fills split->t.
 uint64_t msd_partition_wait(nmx_ctx* c, MsdSplit* split) {
+  if (c->capturing) {  // inside a graph: no heavy buckets assumed, checked after the replay
+    if (split) split->t = SegTotals{0, 0, 0};
+    return 1;
+  }
   CK(cudaEventSynchronize(c->evw));
-  const unsigned long long* h = c->scr();
+  const unsigned long long* h = c->scr() + c->scr_off;
   const uint64_t m = h[0];
   if (split) {
     split->t = c->pend_L > 1 ? *reinterpret_cast<const SegTotals*>(h + 1) : SegTotals{};
@@ -780,11 +816,11 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   *res_v = in_v;
   c->msd_levels = L;
   // one round trip for the whole partition: m and (with a split) its totals
-  unsigned long long* h = c->scr();  // [0] m, [1..2] split totals
+  unsigned long long* h = c->scr() + c->scr_off;  // [0] m, [1..2] split totals
   if (split) CK(cudaMemcpyAsync(h + 1, c->stot.p, sizeof(SegTotals), cudaMemcpyDeviceToHost, c->st));
   CK(cudaMemcpyAsync(h, gcount, 8, cudaMemcpyDeviceToHost, c->st));
   if (!c->evw) CK(cudaEventCreateWithFlags(&c->evw, cudaEventDisableTiming));
-  CK(cudaEventRecord(c->evw, c->st));
+  if (!c->capturing) CK(cudaEventRecord(c->evw, c->st));
   c->pend_bytes_per_m = (uint64_t)dom_pending * 2 * kItem;
   c->pend_L = L;
   return defer ? 0 : msd_partition_wait(c, split);
@@ -1079,6 +1115,7 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   c->cgk.grow(need * 8);
   MsdSplit sp;
   sp.hk = c->cgk.p;
+  c->scr_off = 8;  // its read-back beside the row partition's (both live in one graph)
   msd_partition<ColConcatSrc, uint64_t, false>(c, cs, cs.n, b + 32, Dc, c->keysA.as<uint64_t>(), nullptr,
                                                c->keysB.as<uint64_t>(), nullptr, &ce, &unused, prehist, &sp, 0, true);
   c->mark();  // column partition end
@@ -1093,6 +1130,8 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   }
   c->mark();  // local columns end
   const uint64_t u = msd_partition_wait(c, &sp);
+  c->scr_off = 0;
+  if (sp.t.big) c->had_heavy = true;
   if (!u) return;
   if (sp.t.big) {  // heavy destination buckets: segmented MSD levels (nmx_seg.cuh)
     c->cgk2.grow((size_t)sp.t.big * 8);
@@ -1179,6 +1218,8 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   const uint32_t nb = 1u << D;
   const int Dc = std::min(D, b);
   const int cshift = b - msd_first_bits(Dc);
+  if (c->capturing)  // light count unknown while recording: every slot past it must read as a hole
+    CK(cudaMemsetAsync(c->colL_dst.p, 0, n * 8, c->st));
   {
     const uint32_t* ngp = seg_plan_groups_dev(c, nb, pre_m ? pre_m : n, kLocChunk,
                                               b - D < 31 ? kLocDirect >> (b - D) : 0);
@@ -1191,8 +1232,13 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   }
   c->mark();  // 3: local rows end
   const uint64_t m = msd_partition_wait(c, &sp);
+  if (c->capturing) {  // the column partition reads all n slots (holes skipped)
+    cs.n1 = cs.n = n;
+    return cs;
+  }
   if (!m) return cs;
   uint64_t uh = 0;
+  if (sp.t.big) c->had_heavy = true;
   if (sp.t.big) {  // heavy row buckets: segmented MSD levels (nmx_seg.cuh)
     c->keysD.grow((size_t)sp.t.big * 8);
     uh = heavy_rows(c, sp.t.big, sp.t.nbig, b, D, cshift, chist, ccount);
@@ -1212,6 +1258,112 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   // ---- columns: MSD partition of the (dst, count) entries by destination bits ----
   if (cs.n) msd_columns(c, cs, b, std::min(D, b), chist);
   stage_finish(c, 1);
+}
+
+// ---- small calls as one CUDA graph -------------------------------------------
+// A call of n <= 2^24 packets is ~20 short kernels and three host round trips
+// (partition read-backs, result). Its launch sequence depends only on (n, b) as long
+// as no bucket is heavy, so after one ordinary call the sequence is recorded once --
+// address check, row partition, shared-memory groups, column partition, column
+// groups, and the D2H of the statistics and of both partitions' heavy totals -- and
+// later calls on the same inputs replay it with one launch and one wait. A replay
+// whose totals report a heavy bucket (its work is not in the graph) is discarded and
+// the call reruns the ordinary way.
+void launch_max_addr(nmx_ctx* c, const uint32_t* s, const uint32_t* d, uint64_t n);
+constexpr uint64_t kGraphMaxN = 1ull << 24;
+constexpr int kGraphSlots = 8;
+constexpr int kScrMaxAddr = 16;  // scr() slot of the replay's largest address
+
+bool graph_eligible(uint64_t n) {
+  static const bool off = getenv("NMX_NO_GRAPHS") != nullptr;
+  return !off && n >= 1 && n <= kGraphMaxN;
+}
+
+nmx_ctx::CallGraph* graph_find(nmx_ctx* c, const void* s, const void* d, const void* v, uint64_t n, uint64_t space) {
+  const uint64_t gen = g_buf_gen.load();
+  for (size_t i = 0; i < c->graphs.size();) {  // a buffer moved since recording: stale
+    if (c->graphs[i].gen != gen) {
+      cudaGraphExecDestroy(c->graphs[i].exec);
+      c->graphs.erase(c->graphs.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+  for (auto& g : c->graphs)
+    if (g.s == s && g.d == d && g.v == v && g.n == n && g.space == space) return &g;
+  return nullptr;
+}
+
+// replay: 1 = statistics in h_stats, 0 = a heavy bucket (rerun), NMX_EINVAL = bad address
+int graph_replay(nmx_ctx* c, nmx_ctx::CallGraph* g, uint64_t space) {
+  c->nev = c->nevk = 0;
+  c->dom_name = "";
+  c->dom_launches = 0;
+  c->dom_bytes = 0;
+  c->scr()[kScrMaxAddr] = 0;  // the replay writes its low 4 bytes
+  c->mark();
+  CK(cudaGraphLaunch(g->exec, c->st));
+  c->mark();
+  CK(cudaStreamSynchronize(c->st));
+  unsigned long long* h = c->scr();
+  if (space < (1ull << 32) && h[kScrMaxAddr] >= space)
+    return fail(NMX_EINVAL, "addresses must lie in [0, address_space): found %llu >= %llu", h[kScrMaxAddr],
+                (unsigned long long)space);
+  const SegTotals* rt = reinterpret_cast<const SegTotals*>(h + 1);
+  const SegTotals* ct = reinterpret_cast<const SegTotals*>(h + 9);
+  if (rt->big || ct->big) return 0;
+  CK(cudaEventElapsedTime(&c->last_total_ms, c->ev[0], c->ev[1]));
+  c->last_nstage = 1;
+  c->last_stage_ms[0] = c->last_total_ms;
+  c->last_sort_ms = 0;
+  c->last_launches = g->launches;  // the recorded kernels (one graph launch)
+  return 1;
+}
+
+// record the call's launch sequence (after an ordinary call sized every buffer)
+void graph_capture(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
+                   int b, int D, uint64_t space) {
+  // every buffer the recording touches at its recorded size (the ordinary call sized
+  // them for its own, possibly smaller, light totals)
+  c->cgk.grow(n * 8);
+  c->rmax.grow(64);
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  c->capturing = g_capturing = true;
+  bool ok = true;
+  int launched = 0;
+  try {
+    if (space < (1ull << 32)) {
+      CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
+      launch_max_addr(c, d_src, d_dst, n);
+      CK(cudaMemcpyAsync(c->scr() + kScrMaxAddr, c->rmax.p, 4, cudaMemcpyDeviceToHost, c->st));
+    }
+    c->launches = space < (1ull << 32) ? 1 : 0;
+    run_pipeline_msd(c, d_src, d_dst, d_valid, n, b, D);  // stage_begin resets the count
+    launched = c->launches + (space < (1ull << 32) ? 1 : 0);
+  } catch (...) {
+    ok = false;
+  }
+  c->capturing = g_capturing = false;
+  c->scr_off = 0;
+  const cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+  if (!ok || e != cudaSuccess || !graph) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    return;
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  if ((int)c->graphs.size() >= kGraphSlots) {
+    cudaGraphExecDestroy(c->graphs.front().exec);
+    c->graphs.erase(c->graphs.begin());
+  }
+  c->graphs.push_back({d_src, d_dst, d_valid, n, space, exec, g_buf_gen.load(), launched});
 }
 
 // The whole pipeline over packet columns already on the device. Writes W*9
@@ -1327,10 +1479,24 @@ int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   }
   if (!d_src || !d_dst) return fail(NMX_EINVAL, "null packet columns");
   for (DevBuf* d : {&c->parS, &c->parD, &c->pcolD, &c->pcolC}) d->release();  // a previous out-of-core call's arenas
+  const bool whole = window_size == 0 || window_size >= n;
+  const int Dg = whole && graph_eligible(n) ? msd_bits(n, b) : 0;
+  if (Dg) {  // small call: replay its recorded graph (address check included)
+    if (nmx_ctx::CallGraph* g = graph_find(c, d_src, d_dst, d_valid, n, space)) {
+      const int r = graph_replay(c, g, space);
+      if (r < 0) return r;
+      if (r == 1) {
+        copy_out9(c->h_stats, out, 1);
+        return NMX_OK;
+      }
+    }
+  }
   if (int r = check_addresses(c, d_src, d_dst, n, space)) return r;
-  if (window_size == 0 || window_size >= n) {
+  if (whole) {
     run_pipeline(c, d_src, d_dst, d_valid, n, b, 0, 1);
     copy_out9(c->h_stats, out, 1);
+    if (Dg && !c->had_heavy && !graph_find(c, d_src, d_dst, d_valid, n, space))
+      graph_capture(c, d_src, d_dst, d_valid, n, b, Dg, space);
     return NMX_OK;
   }
   const uint64_t W = (n + window_size - 1) / window_size;
@@ -1979,10 +2145,56 @@ struct CommBufs {
   DevBuf ps, pd, rs, rd, cs, cc, qs, qc, hs, hd, hv, cnt, red;
 };
 
-#define NK(x)                                                                                       \
-  do {                                                                                              \
-    ncclResult_t r_ = (x);                                                                          \
-    if (r_ != ncclSuccess) throw std::runtime_error(std::string("NCCL: ") + ncclGetErrorString(r_)); \
+// libnccl is opened on first use instead of linked: a process that also imports
+// torch must share torch's NCCL (same soname, newer symbols), so NMX_NCCL_LIB
+// (set by _lib.Communicator to the bundled nvidia-nccl library when present) wins
+// over the system libnccl.so.2.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+};
+const NcclApi* nccl_api() {
+  static std::once_flag once;
+  static NcclApi api;
+  static bool ok = false;
+  std::call_once(once, [] {
+    const char* want = getenv("NMX_NCCL_LIB");
+    void* h = want && *want ? dlopen(want, RTLD_NOW | RTLD_GLOBAL) : nullptr;
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    bool all = true;
+    auto sym = [&](auto& f, const char* name) {
+      f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+      all = all && f;
+    };
+    sym(api.GetUniqueId, "ncclGetUniqueId");
+    sym(api.CommInitRank, "ncclCommInitRank");
+    sym(api.CommDestroy, "ncclCommDestroy");
+    sym(api.AllGather, "ncclAllGather");
+    sym(api.AllReduce, "ncclAllReduce");
+    sym(api.Send, "ncclSend");
+    sym(api.Recv, "ncclRecv");
+    sym(api.GroupStart, "ncclGroupStart");
+    sym(api.GroupEnd, "ncclGroupEnd");
+    sym(api.GetErrorString, "ncclGetErrorString");
+    ok = all;
+  });
+  if (!ok) throw std::runtime_error("NCCL library not found (libnccl.so.2 / NMX_NCCL_LIB)");
+  return &api;
+}
+
+#define NK(x)                                                                                          \
+  do {                                                                                                 \
+    ncclResult_t r_ = (x);                                                                             \
+    if (r_ != ncclSuccess) throw std::runtime_error(std::string("NCCL: ") + nccl_api()->GetErrorString(r_)); \
   } while (0)
 
 }  // namespace
@@ -2005,29 +2217,29 @@ uint64_t comm_exchange(nmx_comm* K, nmx_ctx* c, const uint32_t* sa, const uint32
   auto* dc = K->b.cnt.as<unsigned long long>();
   std::vector<unsigned long long> mine(cnt, cnt + g), all((size_t)g * g);
   CK(cudaMemcpyAsync(dc + (size_t)g * g, mine.data(), g * 8, cudaMemcpyHostToDevice, c->st));
-  NK(ncclAllGather(dc + (size_t)g * g, dc, g, ncclUint64, K->comm, c->st));
+  NK(nccl_api()->AllGather(dc + (size_t)g * g, dc, g, ncclUint64, K->comm, c->st));
   CK(cudaMemcpyAsync(all.data(), dc, (size_t)g * g * 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   uint64_t tot = 0;
   for (int q = 0; q < g; ++q) tot += all[(size_t)q * g + r];
   ra.grow(std::max<uint64_t>(tot, 1) * 4);
   rb.grow(std::max<uint64_t>(tot, 1) * 4);
-  NK(ncclGroupStart());
+  NK(nccl_api()->GroupStart());
   uint64_t soff = 0, roff = 0;
   for (int p = 0; p < g; ++p) {
     const uint64_t sl = cnt[p], rl = all[(size_t)p * g + r];
     if (sl) {
-      NK(ncclSend(sa + soff, sl, ncclUint32, p, K->comm, c->st));
-      NK(ncclSend(sb + soff, sl, ncclUint32, p, K->comm, c->st));
+      NK(nccl_api()->Send(sa + soff, sl, ncclUint32, p, K->comm, c->st));
+      NK(nccl_api()->Send(sb + soff, sl, ncclUint32, p, K->comm, c->st));
     }
     if (rl) {
-      NK(ncclRecv(ra.as<uint32_t>() + roff, rl, ncclUint32, p, K->comm, c->st));
-      NK(ncclRecv(rb.as<uint32_t>() + roff, rl, ncclUint32, p, K->comm, c->st));
+      NK(nccl_api()->Recv(ra.as<uint32_t>() + roff, rl, ncclUint32, p, K->comm, c->st));
+      NK(nccl_api()->Recv(rb.as<uint32_t>() + roff, rl, ncclUint32, p, K->comm, c->st));
     }
     soff += sl;
     roff += rl;
   }
-  NK(ncclGroupEnd());
+  NK(nccl_api()->GroupEnd());
   return tot;
 }
 
@@ -2064,10 +2276,10 @@ int comm_run(nmx_comm* K, nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_d
   K->b.red.grow(2 * S_COUNT * 8);
   auto* dr = K->b.red.as<int64_t>();
   CK(cudaMemcpyAsync(dr, sv, sizeof(sv), cudaMemcpyHostToDevice, c->st));
-  NK(ncclGroupStart());
-  NK(ncclAllReduce(dr, dr, S_COUNT, ncclInt64, ncclSum, K->comm, c->st));
-  NK(ncclAllReduce(dr + S_COUNT, dr + S_COUNT, S_COUNT, ncclInt64, ncclMax, K->comm, c->st));
-  NK(ncclGroupEnd());
+  NK(nccl_api()->GroupStart());
+  NK(nccl_api()->AllReduce(dr, dr, S_COUNT, ncclInt64, ncclSum, K->comm, c->st));
+  NK(nccl_api()->AllReduce(dr + S_COUNT, dr + S_COUNT, S_COUNT, ncclInt64, ncclMax, K->comm, c->st));
+  NK(nccl_api()->GroupEnd());
   CK(cudaMemcpyAsync(sv, dr, sizeof(sv), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   for (int i = 0; i < S_COUNT; ++i) out[i] = kSum[i] ? sv[i] : sv[S_COUNT + i];
@@ -2142,6 +2354,7 @@ void nmx_destroy(nmx_ctx* c) {
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
     b->release();
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_scr) cudaFreeHost(c->h_scr);
   if (c->evw) cudaEventDestroy(c->evw);
@@ -3144,8 +3357,14 @@ int nmx_comm_unique_id(uint8_t* id) {
   if (!id) return fail(NMX_EINVAL, "null id");
   static_assert(sizeof(ncclUniqueId) == NMX_COMM_ID_BYTES, "ncclUniqueId size");
   ncclUniqueId u;
-  const ncclResult_t r = ncclGetUniqueId(&u);
-  if (r != ncclSuccess) return fail(NMX_ECUDA, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  const NcclApi* api = nullptr;
+  try {
+    api = nccl_api();
+  } catch (const std::exception& e) {
+    return fail(NMX_ENODEV, "%s", e.what());
+  }
+  const ncclResult_t r = api->GetUniqueId(&u);
+  if (r != ncclSuccess) return fail(NMX_ECUDA, "ncclGetUniqueId: %s", api->GetErrorString(r));
   memcpy(id, &u, sizeof(u));
   return NMX_OK;
 }
@@ -3162,10 +3381,10 @@ int nmx_comm_init(nmx_ctx* c, const uint8_t* id, int nranks, int rank, nmx_comm*
     K->nranks = nranks;
     K->rank = rank;
     K->device = c->device;
-    const ncclResult_t r = ncclCommInitRank(&K->comm, nranks, u, rank);
+    const ncclResult_t r = nccl_api()->CommInitRank(&K->comm, nranks, u, rank);
     if (r != ncclSuccess) {
       delete K;
-      return fail(NMX_ECUDA, "ncclCommInitRank: %s", ncclGetErrorString(r));
+      return fail(NMX_ECUDA, "ncclCommInitRank: %s", nccl_api()->GetErrorString(r));
     }
     *out = K;
     return NMX_OK;
@@ -3175,7 +3394,7 @@ int nmx_comm_init(nmx_ctx* c, const uint8_t* id, int nranks, int rank, nmx_comm*
 void nmx_comm_destroy(nmx_comm* K) {
   if (!K) return;
   cudaSetDevice(K->device);
-  if (K->comm) ncclCommDestroy(K->comm);
+  if (K->comm) nccl_api()->CommDestroy(K->comm);  // init succeeded, so the library is open
   delete K;
 }
 

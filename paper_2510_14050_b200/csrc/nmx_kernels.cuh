@@ -52,6 +52,10 @@ struct PacketSrc {
   uint64_t window_size;  // 0 -> single window
   int b;                 // bits per address
   bool quad = false;     // src/dst 16-byte aligned (and valid 4-byte aligned): 128-bit loads allowed
+  // addresses are masked to b bits when packed: an out-of-range address (rejected by
+  // the address check, which a recorded graph runs beside the pipeline) can never
+  // carry key bits that index past a bucket array or a shared-memory slot table
+  __device__ __forceinline__ uint32_t am() const { return b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u); }
   // four consecutive packets [4q, 4q+4) with two 128-bit loads (scalar at the tail)
   __device__ __forceinline__ void load_quad(uint64_t q, uint64_t* key, bool* ok) const {
     const uint64_t i = 4 * q;
@@ -60,10 +64,11 @@ struct PacketSrc {
       const uint4 d4 = __ldg(reinterpret_cast<const uint4*>(dst) + q);
       uint32_t vv = 0x01010101u;
       if (valid) vv = __ldg(reinterpret_cast<const uint32_t*>(valid) + q);
-      key[0] = ((uint64_t)s4.x << b) | d4.x;
-      key[1] = ((uint64_t)s4.y << b) | d4.y;
-      key[2] = ((uint64_t)s4.z << b) | d4.z;
-      key[3] = ((uint64_t)s4.w << b) | d4.w;
+      const uint32_t m = am();
+      key[0] = ((uint64_t)(s4.x & m) << b) | (d4.x & m);
+      key[1] = ((uint64_t)(s4.y & m) << b) | (d4.y & m);
+      key[2] = ((uint64_t)(s4.z & m) << b) | (d4.z & m);
+      key[3] = ((uint64_t)(s4.w & m) << b) | (d4.w & m);
       ok[0] = (vv & 0xFFu) != 0;
       ok[1] = (vv & 0xFF00u) != 0;
       ok[2] = (vv & 0xFF0000u) != 0;
@@ -82,7 +87,7 @@ struct PacketSrc {
     const uint32_t s = __ldg(src + j), d = __ldg(dst + j);
     bool ok = in;
     if (valid) ok = ok && __ldg(valid + j) != 0;
-    uint64_t k = ((uint64_t)s << b) | d;
+    uint64_t k = ((uint64_t)(s & am()) << b) | (d & am());
     if (window_size) k |= (j / window_size) << (2 * b);
     key = k;
     val = 0;
