@@ -827,10 +827,20 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
 }
 
 // ---- segmented MSD levels over heavy buckets (nmx_seg.cuh) ------------------
-// split `bits` into ceil(bits / 7) near-equal level widths
+// split `bits` into ceil(bits / seg_level_bits()) near-equal level widths
+// (NMX_SEG_BITS=7 restores the 7-bit segmented levels, for A/B measurements)
+int seg_level_bits() {
+  static const int v = [] {
+    const char* e = getenv("NMX_SEG_BITS");
+    const int x = e ? atoi(e) : kSegLevelBits;
+    return x >= 4 && x <= kSegLevelBits ? x : kSegLevelBits;
+  }();
+  return v;
+}
 int split_levels(int bits, int* out) {
   if (bits <= 0) return 0;
-  const int L = (bits + kMsdLevelBits - 1) / kMsdLevelBits;
+  const int lb = seg_level_bits();
+  const int L = (bits + lb - 1) / lb;
   for (int l = 0; l < L; ++l) out[l] = bits / L + (l < bits % L ? 1 : 0);
   return L;
 }
@@ -919,7 +929,7 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
   bool part[16];
   int L = 0;
   const int r = b - D;                          // source bits below the dense prefix
-  const int r0 = r > 0 ? std::min(r, (r + 1) / 2 > kMsdLevelBits ? kMsdLevelBits : (r + 1) / 2) : 0;
+  const int r0 = r > 0 ? std::min(r, std::min((r + 1) / 2, seg_level_bits())) : 0;
   if (r0) w[L] = r0, sh[L] = 2 * b - D - r0, part[L] = false, ++L;
   {
     int dw[8];
