@@ -48,18 +48,21 @@ __global__ void merge_partition_kernel(const uint64_t* __restrict__ ak, uint64_t
   }
 }
 
+// Shared-memory slices are padded (pad16): the per-thread serial merges read at a
+// stride of ~4 items and the compacted writes at ~8, which would otherwise put a
+// warp on a few banks.
+constexpr int kMgPad = kMgTile + kMgTile / 16;
 struct MergeSmem {
-  uint64_t key[kMgTile];  // A slice [0, la), B slice [la, la + lb); later the compacted output
-  uint64_t cnt[kMgTile];
-  uint64_t mkey[kMgTile];  // merged order
-  uint64_t mcnt[kMgTile];
-  uint8_t mfrom[kMgTile];  // 0 = A, 1 = B
+  uint64_t key[kMgPad];  // A slice [0, la), B slice [la, la + lb); later the compacted output
+  uint64_t cnt[kMgPad];
+  uint64_t fkey[kMgThreads], fcnt[kMgThreads], lkey[kMgThreads];  // each thread's first / last merged item
+  uint8_t ffromb[kMgThreads];
   uint32_t wt[kWarps + 1];
   unsigned long long prefix;
   uint32_t tile;
   uint64_t prev_key, next_key;
   uint64_t next_cnt;
-  int prev_valid, next_is_b;
+  int prev_valid, next_is_b, next_valid;
 };
 
 __global__ void __launch_bounds__(kMgThreads) merge_add_kernel(
@@ -79,18 +82,19 @@ __global__ void __launch_bounds__(kMgThreads) merge_add_kernel(
   const uint64_t ib = d0 - ia, jb = d1 - ja;
   const uint32_t la = (uint32_t)(ja - ia), lb = (uint32_t)(jb - ib), len = la + lb;
   for (uint32_t i = tid; i < la; i += kMgThreads) {
-    S.key[i] = ak[ia + i];
-    S.cnt[i] = ac[ia + i];
+    S.key[pad16(i)] = ak[ia + i];
+    S.cnt[pad16(i)] = ac[ia + i];
   }
   for (uint32_t i = tid; i < lb; i += kMgThreads) {
-    S.key[la + i] = bk[ib + i];
-    S.cnt[la + i] = bc[ib + i];
+    S.key[pad16(la + i)] = bk[ib + i];
+    S.cnt[pad16(la + i)] = bc[ib + i];
   }
   if (tid == 0) {
     // merged position d0 - 1 (its key decides whether our first B element is a duplicate)
     S.prev_valid = d0 > 0;
     if (d0 > 0) S.prev_key = (ia > 0 && (ib == 0 || ak[ia - 1] >= bk[ib - 1])) ? ak[ia - 1] : bk[ib - 1];
     // merged position d1 (a B duplicate of our last A element adds its count here)
+    S.next_valid = d1 < n;
     S.next_is_b = 0;
     S.next_key = 0;
     S.next_cnt = 0;
@@ -105,35 +109,74 @@ __global__ void __launch_bounds__(kMgThreads) merge_add_kernel(
     }
   }
   __syncthreads();
-  // per-thread merge of positions [q0, q1) of this tile
-  const uint32_t q0 = min((uint32_t)tid * kMgIPT, len), q1 = min(q0 + kMgIPT, len);
+  // per-thread merge of positions [q0, q1) of this tile, kept in registers
+  const uint32_t q0 = min((uint32_t)tid * kMgIPT, len), q1 = min(q0 + kMgIPT, len), nq = q1 - q0;
+  uint64_t k[kMgIPT], c[kMgIPT];
+  uint32_t fromb = 0;  // bit q: position q0 + q comes from B
   {
     uint32_t lo = q0 > lb ? q0 - lb : 0, hi = min(q0, la);
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (S.key[mid] <= S.key[la + q0 - 1 - mid])
+      if (S.key[pad16(mid)] <= S.key[pad16(la + q0 - 1 - mid)])
         lo = mid + 1;
       else
         hi = mid;
     }
     uint32_t i = lo, j = q0 - lo;
-    for (uint32_t q = q0; q < q1; ++q) {
-      const bool takeA = i < la && (j >= lb || S.key[i] <= S.key[la + j]);
-      const uint32_t src = takeA ? i++ : la + j++;
-      S.mkey[q] = S.key[src];
-      S.mcnt[q] = S.cnt[src];
-      S.mfrom[q] = takeA ? 0 : 1;
+    uint64_t ka = i < la ? S.key[pad16(i)] : ~0ull, kb = j < lb ? S.key[pad16(la + j)] : ~0ull;
+#pragma unroll
+    for (int q = 0; q < kMgIPT; ++q) {
+      k[q] = 0;
+      c[q] = 0;
+      if ((uint32_t)q < nq) {
+        const bool takeA = i < la && (j >= lb || ka <= kb);
+        if (takeA) {
+          k[q] = ka;
+          c[q] = S.cnt[pad16(i)];
+          ++i;
+          ka = i < la ? S.key[pad16(i)] : ~0ull;
+        } else {
+          k[q] = kb;
+          c[q] = S.cnt[pad16(la + j)];
+          fromb |= 1u << q;
+          ++j;
+          kb = j < lb ? S.key[pad16(la + j)] : ~0ull;
+        }
+      }
     }
   }
-  __syncthreads();
-  // a B element is dropped iff its merged predecessor has the same key
-  uint32_t keepmask = 0, kept = 0;
-  for (uint32_t q = q0; q < q1; ++q) {
-    const bool dup = S.mfrom[q] == 1 && (q > 0 ? S.mkey[q - 1] == S.mkey[q] : (S.prev_valid && S.prev_key == S.mkey[q]));
-    if (!dup) {
-      keepmask |= 1u << (q - q0);
-      ++kept;
+  if (nq) {
+    S.fkey[tid] = k[0];
+    S.fcnt[tid] = c[0];
+    S.ffromb[tid] = fromb & 1u;
+    S.lkey[tid] = k[nq - 1];
+  }
+  __syncthreads();  // every merge has read the slices: they may be overwritten below
+  // neighbours: the merged position before q0 and the one at q1
+  const bool pv = tid ? true : S.prev_valid != 0;
+  const uint64_t pk = tid ? S.lkey[tid - 1] : S.prev_key;
+  const bool inner = q1 < len;
+  const bool nv = inner || S.next_valid;
+  const uint64_t nk = inner ? S.fkey[tid + 1] : S.next_key;
+  const uint64_t nc = inner ? S.fcnt[tid + 1] : S.next_cnt;
+  const bool nbf = inner ? S.ffromb[tid + 1] != 0 : S.next_is_b != 0;
+  // a B element is dropped iff its merged predecessor has the same key (inputs are
+  // unique, so duplicates are exactly adjacent A, B pairs); the A copy takes the sum
+  uint32_t keep = 0, kept = 0;
+#pragma unroll
+  for (int q = 0; q < kMgIPT; ++q) {
+    if ((uint32_t)q >= nq) continue;
+    const bool isb = (fromb >> q) & 1u;
+    const bool dup = isb && (q ? k[q - 1] == k[q] : (pv && pk == k[q]));
+    if (dup) continue;
+    const bool last = (uint32_t)q + 1 == nq;
+    const bool nxb = last ? (nv && nbf && nk == k[q]) : (((fromb >> (q + 1)) & 1u) && k[q + 1] == k[q]);
+    if (nxb) {
+      c[q] += last ? nc : c[q + 1];
+      if (c[q] > 0x7FFFFFFFFFFFFFFFull) atomicAdd(overflow, 1ull);  // both inputs < 2^63: no u64 wrap
     }
+    keep |= 1u << q;
+    ++kept;
   }
   uint32_t tot;
   uint32_t at = block_excl_scan<uint32_t>(kept, S.wt, &tot);
@@ -150,25 +193,19 @@ __global__ void __launch_bounds__(kMgThreads) merge_add_kernel(
     S.prefix = excl;
     if (d1 == n) *total = excl + tot;
   }
-  // compacted output into the (now free) staging arrays
-  for (uint32_t q = q0; q < q1; ++q) {
-    if (!((keepmask >> (q - q0)) & 1u)) continue;
-    unsigned long long c = S.mcnt[q];
-    if (q + 1 < len) {
-      if (S.mfrom[q + 1] == 1 && S.mkey[q + 1] == S.mkey[q]) c += S.mcnt[q + 1];
-    } else if (S.next_is_b && S.next_key == S.mkey[q]) {
-      c += S.next_cnt;
+  // compacted output staged in the (now free) slices, then written coalesced
+#pragma unroll
+  for (int q = 0; q < kMgIPT; ++q)
+    if ((keep >> q) & 1u) {
+      S.key[pad16(at)] = k[q];
+      S.cnt[pad16(at)] = c[q];
+      ++at;
     }
-    if (c > 0x7FFFFFFFFFFFFFFFull) atomicAdd(overflow, 1ull);  // both inputs < 2^63: no u64 wrap
-    S.key[at] = S.mkey[q];
-    S.cnt[at] = c;
-    ++at;
-  }
   __syncthreads();
   const unsigned long long base = S.prefix;
   for (uint32_t j = tid; j < tot; j += kMgThreads) {
-    ck[base + j] = S.key[j];
-    cc[base + j] = S.cnt[j];
+    ck[base + j] = S.key[pad16(j)];
+    cc[base + j] = S.cnt[pad16(j)];
   }
 }
 
