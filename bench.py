@@ -516,7 +516,7 @@ def _step_traffic(config: str, n_total: int, world: int):
     if t.get("items_per_launch") != n_total or not t.get("calls"):
         return None
     return {"bytes": round(sum(v["dram_bytes"] for v in t["kernels"].values()) / t["calls"]),
-            "source": f"profiles/traffic_{config}.json ({t.get('report', '')}, ncu --set full, {t['calls']} call(s))"}
+            "source": f"profiles/traffic_{config}.json ({t.get('report', '')}, {t['calls']} call(s))"}
 
 
 def run_nmx(args) -> None:
@@ -654,6 +654,34 @@ def run_nmx(args) -> None:
         hs.close()
         hd.close()
 
+    # ---- the drop-in API end to end: analytics.stats9(PacketStream) on the reference's
+    # own int64 columns (host memory, not pinned), the call a netmeter user makes ----
+    dropin = None
+    if not args.no_e2e and world == 1 and args.config in ("cfg3", "cfg4"):
+        import numpy as np
+
+        from paper_2510_14050_b200 import analytics as na
+        from paper_2510_14050_b200.traffic import PacketStream
+
+        stream = PacketStream(src=ds.download().astype(np.int64), dst=dd.download().astype(np.int64),
+                              valid=np.ones(n, dtype=bool), address_space=space)  # outside the timed region
+        got = na.stats9(stream).astuple()
+        assert got == tuple(stats), (got, stats)
+        times = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            na.stats9(stream)
+            times.append(time.perf_counter() - t0)
+        best = min(times)
+        dropin = {"value": n_total / best, "unit": "packets/s", "ms_per_step": best * 1e3, "steps": 2,
+                  "h2d_bytes_per_step": 9 * n_total, "d2h_bytes_per_step": 72,
+                  "api": "paper_2510_14050_b200.analytics.stats9(PacketStream) (int64 src / dst + bool valid in "
+                         "pageable host memory, as traffic.py:43-71 holds them) -> nmx_stats9_host_i64: library "
+                         "threads narrow each 2^24-packet window into pinned slots while the previous window is "
+                         "copied and partitioned",
+                  "timing": "wall clock of the host-synchronous call, best of 2"}
+        del stream
+
     parity = golden_parity(args.config, log2n, gen, stats)
     if rank != 0:
         if dist is not None:
@@ -718,6 +746,7 @@ def run_nmx(args) -> None:
                                   ["hist+plan", "row sort", "link/row", "col sort", "col+d2h"]
                                   if len(stage_ms) == 5 else "stages of the rank's last library call")},
         "e2e": e2e,
+        "e2e_dropin": dropin,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches,

@@ -83,6 +83,12 @@ int nmx_stats9_device(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst
 /* Same, from host columns (copied H2D inside the call; pinned memory is fastest). */
 int nmx_stats9_host(nmx_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t address_space, int64_t out[9]);
+/* Same, from the reference's own PacketStream columns (traffic.py:43-71: int64 src /
+ * dst, bool valid as bytes, any host memory): narrowed to u32 by host threads into
+ * pinned slots window by window, overlapped with the copies and the device work.
+ * Addresses outside [0, address_space) -> NMX_EINVAL. */
+int nmx_stats9_host_i64(nmx_ctx* ctx, const int64_t* src, const int64_t* dst, const uint8_t* valid, uint64_t n,
+                        uint64_t address_space, int64_t out[9]);
 
 /* Streamed windows (BASELINE config 5): nine statistics of the matrix summed over
  * `nwin` windows of HOST packet columns (src[k], dst[k], valid[k] or NULL, lens[k]

@@ -47,6 +47,7 @@ SIGNATURES = {
     "nmx_generate": (C.c_int, [_VP, C.c_int, _U64, _U64, _U64, _U64, _VP, _VP]),
     "nmx_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_stats9_host_i64": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stream_stats9": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stream_records": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_anonymize_begin": (C.c_int, [_VP, _VP, _VP, _U64, _VP]),
@@ -352,6 +353,21 @@ def _prefer_bundled_nccl() -> None:
         if cand.exists():
             os.environ["NMX_NCCL_LIB"] = str(cand)
             return
+
+
+def stats9_i64(src: np.ndarray, dst: np.ndarray, valid=None, address_space: int = 1 << 32, device: int = 0) -> tuple:
+    """nmx_stats9_host_i64: the reference's int64 PacketStream columns (+ bool valid)
+    straight from host memory (narrowed by library threads, pinned staging)."""
+    ctx = context(device)
+    s = np.ascontiguousarray(src, dtype=np.int64)
+    d = np.ascontiguousarray(dst, dtype=np.int64)
+    v = None if valid is None else np.ascontiguousarray(valid, dtype=bool).view(np.uint8)
+    if len(s) != len(d) or (v is not None and len(v) != len(s)):
+        raise ValueError("src, dst and valid must have equal lengths")
+    out = np.zeros(9, dtype=np.int64)
+    check(ctx._lib.nmx_stats9_host_i64(ctx.handle, s.ctypes.data, d.ctypes.data, _ptr(v), len(s), int(address_space),
+                                       out.ctypes.data))
+    return tuple(int(x) for x in out)
 
 
 def comm_unique_id() -> bytes:

@@ -236,9 +236,13 @@ def stats9(stream: PacketStream, device: int = 0, scheduler=None, batch_count: i
         raise ValueError("batch_count must be >= 1")
     if len(stream) == 0:
         return Stats9.zero()
+    g = _group(scheduler)
+    if g is None:  # the stream's own int64 columns, narrowed inside the library (nmx_stats9_host_i64)
+        if stream.address_space > 1 << 32:
+            raise ValueError("address_space above 2^32 does not fit the 32-bit packet format")
+        return Stats9(*_lib.stats9_i64(stream.src, stream.dst, stream.valid, stream.address_space, device=device))
     s, d, v = stream.wire()
     v = None if stream.valid.all() else v
-    g = _group(scheduler)
     if g is not None and (g.resource_count > 1 or batch_count > 1):
         return Stats9(*g.native.stats9_host(s, d, v, stream.address_space, batch_count))
     if g is not None:

@@ -158,6 +158,8 @@ struct nmx_ctx {
   }
   unsigned long long* h_stats = nullptr;
   size_t h_stats_cap = 0;
+  void* h_wide = nullptr;  // pinned u32 / u8 slots of the int64-column entry
+  size_t wide_cap = 0;
   cudaEvent_t ev[40];
   int nev = 0;
   // deferred partition read-back (msd_partition(defer) -> msd_partition_wait)
@@ -1534,7 +1536,21 @@ struct HostWindows {
   const uint8_t* const* rec = nullptr;
   const uint64_t* lens = nullptr;
   uint64_t nwin = 0;
+  // producer mode (the reference's int64 columns): window k is written by fill(k, slot)
+  // into pinned slot k & 1 (whose previous copy must have left first) right before
+  // its copy; src[k] / dst[k] / valid[k] then point at that slot
+  std::function<void(uint64_t, int)> fill;
 };
+
+// pinned staging of the producer mode: the window's previous use of the slot must
+// have been copied out before the producer overwrites it
+void produce_window(nmx_ctx* c, const HostWindows& hw, uint64_t k, bool* pin_used) {
+  if (!hw.fill) return;
+  const int sl = (int)(k & 1);
+  if (pin_used[sl]) CK(cudaEventSynchronize(c->evc[sl]));
+  hw.fill(k, sl);
+  pin_used[sl] = true;
+}
 
 // device records -> columns; the largest address seen is max-reduced into *maxaddr
 void unpack_records(nmx_ctx* c, const uint8_t* rec, uint64_t n, uint32_t* s, uint32_t* d, uint8_t* v,
@@ -1599,6 +1615,10 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
     for (uint64_t k = 0; k < hw.nwin; ++k) {
       const uint64_t L = hw.lens[k];
       if (!L) continue;
+      if (hw.fill) {  // the pinned slot is reused every other window: wait for its last copy
+        CK(cudaStreamSynchronize(c->st));
+        hw.fill(k, (int)(k & 1));
+      }
       if (recs) {  // window by window through one record slot (offsets stay 16-byte aligned only at 0)
         CK(cudaMemcpyAsync(c->wr0.p, hw.rec[k], L * 9, cudaMemcpyHostToDevice, c->st));
         c->ws0.grow(L * 4 + 16);
@@ -1659,8 +1679,10 @@ int stream_impl(nmx_ctx* c, const HostWindows& hw, uint64_t space, int64_t* out)
   CK(cudaEventRecord(c->evs, c->st));
   CK(cudaStreamWaitEvent(c->st2, c->evs, 0));  // copies start after the caller's prior work
   bool used[2] = {false, false};
+  bool pin_used[2] = {false, false};
   auto enqueue_copy = [&](uint64_t k) {
     const int sl = (int)(k & 1);
+    produce_window(c, hw, k, pin_used);
     if (used[sl]) CK(cudaStreamWaitEvent(c->st2, c->evu[sl], 0));
     const uint64_t L = hw.lens[k];
     if (L && recs) {
@@ -1743,6 +1765,83 @@ int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const 
   }
   return stats_device_impl(c, c->in_src.as<uint32_t>(), c->in_dst.as<uint32_t>(),
                            valid ? c->in_valid.as<uint8_t>() : nullptr, n, space, window_size, out);
+}
+
+// The reference's own columns (PacketStream: int64 src / dst, bool valid): narrowed to
+// u32 on the host by a few threads per window, into two pinned slots that alternate,
+// while the previous window is copied and partitioned -- the drop-in analytics.stats9
+// without a pageable int64 -> u32 pass in numpy before the call.
+constexpr uint64_t kWideWindow = 1ull << 24;
+int stats_host_i64_impl(nmx_ctx* c, const int64_t* src, const int64_t* dst, const uint8_t* valid, uint64_t n,
+                        uint64_t space, int64_t* out) {
+  int b;
+  if (int r = check_space(space, b)) return r;
+  if (n && (!src || !dst)) return fail(NMX_EINVAL, "null packet columns");
+  if (!n) {
+    std::fill(out, out + S_COUNT, 0);
+    return NMX_OK;
+  }
+  const uint64_t W = std::min<uint64_t>(kWideWindow, n);
+  const uint64_t nwin = (n + W - 1) / W;
+  // pinned slots: u32 src, u32 dst, u8 valid per packet, two of each
+  const size_t slot = W * 9 + 64;
+  if (c->wide_cap < 2 * slot) {
+    if (c->h_wide) CK(cudaFreeHost(c->h_wide));
+    c->h_wide = nullptr;
+    c->wide_cap = 0;
+    CK(cudaMallocHost(&c->h_wide, 2 * slot));
+    c->wide_cap = 2 * slot;
+  }
+  unsigned char* base = static_cast<unsigned char*>(c->h_wide);
+  uint32_t* ps[2] = {reinterpret_cast<uint32_t*>(base), reinterpret_cast<uint32_t*>(base + slot)};
+  uint32_t* pd[2] = {ps[0] + W, ps[1] + W};
+  uint8_t* pv[2] = {reinterpret_cast<uint8_t*>(pd[0] + W), reinterpret_cast<uint8_t*>(pd[1] + W)};
+  std::vector<const uint32_t*> sp(nwin), dp(nwin);
+  std::vector<const uint8_t*> vp(nwin);
+  std::vector<uint64_t> lens(nwin);
+  for (uint64_t k = 0; k < nwin; ++k) {
+    sp[k] = ps[k & 1];
+    dp[k] = pd[k & 1];
+    vp[k] = valid ? pv[k & 1] : nullptr;
+    lens[k] = std::min(W, n - k * W);
+  }
+  const unsigned hw_threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::atomic<bool> bad{false};
+  HostWindows hw;
+  hw.src = sp.data();
+  hw.dst = dp.data();
+  hw.valid = valid ? vp.data() : nullptr;
+  hw.lens = lens.data();
+  hw.nwin = nwin;
+  hw.fill = [&](uint64_t k, int sl) {
+    const uint64_t lo = k * W, L = lens[k];
+    const unsigned T = (unsigned)std::min<uint64_t>(hw_threads, (L + 65535) / 65536);
+    auto work = [&](unsigned t) {
+      const uint64_t a = L * t / T, z = L * (t + 1) / T;
+      uint64_t orr = 0;  // any address outside [0, space): its bits at or above b (or the sign)
+      const int64_t* s = src + lo;
+      const int64_t* d = dst + lo;
+      for (uint64_t i = a; i < z; ++i) {
+        const uint64_t x = (uint64_t)s[i], y = (uint64_t)d[i];
+        orr |= (x >= space) | (y >= space);
+        ps[sl][i] = (uint32_t)x;
+        pd[sl][i] = (uint32_t)y;
+      }
+      if (valid) memcpy(pv[sl] + a, valid + lo + a, z - a);
+      if (orr) bad = true;
+    };
+    if (T <= 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (unsigned t = 1; t < T; ++t) th.emplace_back(work, t);
+      work(0);
+      for (auto& x : th) x.join();
+    }
+  };
+  const int rc = stream_impl(c, hw, space, out);
+  if (bad) return fail(NMX_EINVAL, "addresses must lie in [0, address_space)");
+  return rc;
 }
 
 // ---- multi-GPU shard stages; callers hold the context lock ----
@@ -1872,8 +1971,10 @@ int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wm
   CK(cudaEventRecord(c->evs, c->st));
   CK(cudaStreamWaitEvent(c->st2, c->evs, 0));
   bool used[2] = {false, false};
+  bool pin_used[2] = {false, false};
   auto enqueue_copy = [&](uint64_t k) {
     const int sl = (int)(k & 1);
+    produce_window(c, hw, k, pin_used);
     if (used[sl]) CK(cudaStreamWaitEvent(c->st2, c->evu[sl], 0));
     const uint64_t L = hw.lens[k];
     if (L && recs) {
@@ -2365,6 +2466,7 @@ void nmx_destroy(nmx_ctx* c) {
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
     b->release();
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->h_wide) cudaFreeHost(c->h_wide);
   if (c->h_small) cudaFreeHost(c->h_small);
   if (c->h_scr) cudaFreeHost(c->h_scr);
   if (c->evw) cudaEventDestroy(c->evw);
@@ -2464,6 +2566,12 @@ int nmx_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
 int nmx_stats9_host(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t address_space, int64_t out[9]) {
   return guarded(c, [&] { return stats_host_impl(c, src, dst, valid, n, address_space, 0, out); });
+}
+
+int nmx_stats9_host_i64(nmx_ctx* c, const int64_t* src, const int64_t* dst, const uint8_t* valid, uint64_t n,
+                        uint64_t address_space, int64_t out[9]) {
+  if (!out) return fail(NMX_EINVAL, "null output");
+  return guarded(c, [&] { return stats_host_i64_impl(c, src, dst, valid, n, address_space, out); });
 }
 
 int nmx_stream_stats9(nmx_ctx* c, const uint32_t* const* src, const uint32_t* const* dst, const uint8_t* const* valid,

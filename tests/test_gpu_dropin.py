@@ -138,3 +138,27 @@ def test_concurrent_analysis_on_one_scheduler():
     for t in ts:
         t.join()
     assert got == expected
+
+
+@pytest.mark.parametrize("n,space,kind", [(1000, 7, "uniform"), (70_000, 1 << 20, "powerlaw"),
+                                          ((1 << 24) + 12345, 1 << 32, "uniform"), ((1 << 25) + 3, 5000, "powerlaw")])
+def test_stats9_of_packet_stream_int64_columns(n, space, kind):
+    """analytics.stats9(PacketStream): the stream's own int64 columns through
+    nmx_stats9_host_i64 (threaded narrowing into pinned slots, several windows when
+    n > 2^24, invalid packets) equal the oracle; out-of-range columns are rejected."""
+    import numpy as np
+
+    from oracle import netmeter_oracle as orc
+    from paper_2510_14050_b200 import _lib
+    from paper_2510_14050_b200.analytics import stats9
+    from paper_2510_14050_b200.traffic import PacketStream
+
+    g = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
+    s, d = g(31, 0, n, space)
+    v = np.random.default_rng(n).random(n) >= 0.15
+    st = PacketStream(src=s.astype(np.int64), dst=d.astype(np.int64), valid=v, address_space=space)
+    assert stats9(st).astuple() == orc.stats9_packed(s, d, v)
+    bad = s.astype(np.int64)
+    bad[n // 2] = space if space < (1 << 32) else -1
+    with pytest.raises(ValueError, match="address"):
+        _lib.stats9_i64(bad, d.astype(np.int64), v, space)
