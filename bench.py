@@ -285,8 +285,8 @@ def run_cfg5(args) -> None:
     from paper_2510_14050_b200 import _lib
     from paper_2510_14050_b200 import coo as nc
 
-    if int(os.environ.get("RANK", "0")) != 0:
-        return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_cfg5_sharded(args)
     log2n, space, gen = CONFIGS["cfg5"]
     if args.log2n:
         log2n = args.log2n
@@ -335,6 +335,83 @@ def run_cfg5(args) -> None:
     for a, b in wins:
         a.close()
         b.close()
+
+
+def run_cfg5_sharded(args) -> None:
+    """cfg5 on N ranks: each rank holds its partition_even share of the 2^32 packets in
+    pinned host memory and calls the sharded host entry (nmx_stats9_sharded_host: H2D,
+    owner(src) / owner(dst) exchanges over libnmx's NCCL communicator, SUM / MAX);
+    timed on the host around the call between barriers, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_14050_b200 import _lib
+    from paper_2510_14050_b200 import distributed as nd
+
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    local = int(os.environ.get("NMX_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    backend = os.environ.get("NMX_DIST_BACKEND", "nccl")
+    torch.cuda.set_device(local)
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    log2n, space, gen = CONFIGS["cfg5"]
+    if args.log2n:
+        log2n = args.log2n
+    n_total = 1 << log2n
+    q, r = divmod(n_total, world)
+    n = q + (1 if rank < r else 0)
+    off = rank * q + min(rank, r)
+    kind = _lib.GEN_UNIFORM if gen == "uniform" else _lib.GEN_POWERLAW
+    hs, hd = _lib.PinnedArray(n), _lib.PinnedArray(n)
+    chunk = 1 << 26
+    ds, dd = _lib.DeviceArray(min(n, chunk), device=local), _lib.DeviceArray(min(n, chunk), device=local)
+    for lo in range(0, n, chunk):  # inputs prepared outside the timed region
+        ln = min(chunk, n - lo)
+        _lib.generate(kind, 7, off + lo, ln, space, ds, dd, device=local)
+        hs.array[lo:lo + ln] = ds.download()[:ln]
+        hd.array[lo:lo + ln] = dd.download()[:ln]
+    ds.close()
+    dd.close()
+
+    def step():
+        return nd.sharded_stats9_host(hs.array, hd.array, space, device=local)
+
+    for _ in range(max(1, min(args.warmup, 1))):
+        stats = step()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            dist.barrier()
+            t0 = time.perf_counter()
+            stats = step()
+            times.append(time.perf_counter() - t0)
+    mt = torch.tensor([min(times)], dtype=torch.float64, device=f"cuda:{local}" if backend == "nccl" else "cpu")
+    dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+    best = float(mt.item())
+    parity = golden_parity("cfg5", log2n, gen, stats)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": n_total / best, "unit": "packets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": f"cfg5: 2^{log2n} packets {gen} over {space} addresses in pinned host memory, "
+                                   f"partition_even shares of {world} ranks, each through nmx_stats9_sharded_host "
+                                   "(H2D, NCCL owner(src) / owner(dst) exchanges, SUM / MAX)",
+                       "packets": n_total, "parallelism": f"shards{world}",
+                       "timing": "host wall clock of the call between barriers, best of steps, max over ranks"},
+            "stats9": list(stats), "parity": parity,
+            "e2e": {"value": n_total / best, "unit": "packets/s", "h2d_bytes_per_step": 8 * n_total,
+                    "d2h_bytes_per_step": 72 * world},
+            "clocks": clk.summary(),
+        }), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    hs.close()
+    hd.close()
 
 
 def run_file(args) -> None:

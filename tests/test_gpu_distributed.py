@@ -220,3 +220,31 @@ def test_bench_spawns_ranks():
     finally:
         ds.close()
         dd.close()
+
+
+def test_bench_cfg5_sharded_ranks():
+    """`bench.py --config cfg5 --gpus 2`: each rank's partition_even share in pinned host
+    memory through the sharded host entry; the statistics equal one device's."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    from paper_2510_14050_b200 import _lib
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, NMX_BENCH_DEVICE="0", NMX_DIST_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--config", "cfg5", "--gpus", "2", "--steps", "1",
+                        "--warmup", "3", "--log2n", "23"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    n = 1 << 23
+    ds, dd = _lib.DeviceArray(n), _lib.DeviceArray(n)
+    try:
+        _lib.generate(_lib.GEN_UNIFORM, 7, 0, n, 1 << 32, ds, dd)
+        assert line["stats9"] == list(_lib.stats9(ds, dd, None, 1 << 32))
+    finally:
+        ds.close()
+        dd.close()
