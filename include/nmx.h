@@ -83,6 +83,15 @@ int nmx_stats9_device(nmx_ctx* ctx, const uint32_t* d_src, const uint32_t* d_dst
 /* Same, from host columns (copied H2D inside the call; pinned memory is fastest). */
 int nmx_stats9_host(nmx_ctx* ctx, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t address_space, int64_t out[9]);
+/* A sequence of independent host batches (src[k], dst[k], valid[k] or NULL, lens[k]
+ * packets each < 2^32; pinned memory streams at full host-link bandwidth): batch k's
+ * nine statistics -> out[9k .. 9k+8], each exactly nmx_stats9_host of that batch.
+ * Batch k+1's H2D copy (second stream, two device slots) overlaps batch k's device
+ * work, so a run of batches is bound by the host link rather than by copy + compute.
+ * The loop the reference writes as repeated analyze_matrix calls over packet windows
+ * (analytics.py:95-130); host buffers are borrowed until the call returns. */
+int nmx_stats9_host_batches(nmx_ctx* ctx, uint64_t nbatch, const uint32_t* const* src, const uint32_t* const* dst,
+                            const uint8_t* const* valid, const uint64_t* lens, uint64_t address_space, int64_t* out);
 /* Same, from the reference's own PacketStream columns (traffic.py:43-71: int64 src /
  * dst, bool valid as bytes, any host memory): narrowed to u32 by host threads into
  * pinned slots window by window, overlapped with the copies and the device work.

@@ -48,6 +48,7 @@ SIGNATURES = {
     "nmx_stats9_device": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stats9_host": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stats9_host_i64": (C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _VP]),
+    "nmx_stats9_host_batches": (C.c_int, [_VP, _U64, _VP, _VP, _VP, _VP, _U64, _VP]),
     "nmx_stream_stats9": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_stream_records": (C.c_int, [_VP, _VP, _VP, _U64, _U64, _VP]),
     "nmx_anonymize_begin": (C.c_int, [_VP, _VP, _VP, _U64, _VP]),
@@ -419,6 +420,33 @@ class Communicator:
         if self._h:
             self.ctx._lib.nmx_comm_destroy(self._h)
             self._h = C.c_void_p()
+
+
+def stats9_batches(batches, address_space: int = 1 << 32, device: int = 0) -> list:
+    """Nine statistics of each of several independent host batches
+    (nmx_stats9_host_batches): ``batches`` = [(src, dst) or (src, dst, valid), ...]
+    host arrays; the result is one 9-tuple per batch, each equal to ``stats9`` of that
+    batch. Batch k+1's H2D copy overlaps batch k's device work (pinned memory streams
+    at full host-link bandwidth)."""
+    ctx = context(device)
+    cols = []
+    for w in batches:
+        s, d = _u32_host(w[0]), _u32_host(w[1])
+        v = _valid_host(w[2]) if len(w) > 2 else None
+        if len(s) != len(d) or (v is not None and len(v) != len(s)):
+            raise ValueError("src, dst and valid must have equal lengths")
+        cols.append((s, d, v))
+    k = len(cols)
+    srcp = (C.c_void_p * max(k, 1))(*[c[0].ctypes.data for c in cols])
+    dstp = (C.c_void_p * max(k, 1))(*[c[1].ctypes.data for c in cols])
+    anyv = any(c[2] is not None for c in cols)
+    valp = (C.c_void_p * max(k, 1))(*[(c[2].ctypes.data if c[2] is not None else None) for c in cols])
+    lens = (C.c_uint64 * max(k, 1))(*[len(c[0]) for c in cols])
+    out = np.zeros(9 * max(k, 1), dtype=np.int64)
+    check(ctx._lib.nmx_stats9_host_batches(ctx.handle, k, srcp, dstp, valp if anyv else None, lens,
+                                           int(address_space), out.ctypes.data))
+    del cols
+    return [tuple(int(x) for x in out[9 * i:9 * i + 9]) for i in range(k)]
 
 
 def stream_stats9(windows, address_space: int = 1 << 32, device: int = 0) -> tuple:

@@ -150,6 +150,9 @@ struct nmx_ctx {
   uint32_t epoch = 0;
   cudaStream_t st2 = nullptr;  // copy stream of the streamed path
   cudaEvent_t evc[2] = {nullptr, nullptr}, evu[2] = {nullptr, nullptr}, evs = nullptr;
+  // nmx_stats9_host_batches: two device input slots, copy-done / slot-free events
+  DevBuf bat_s[2], bat_d[2], bat_v[2];
+  cudaEvent_t evbc[2] = {nullptr, nullptr}, evbu[2] = {nullptr, nullptr};
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
   unsigned long long* h_scr = nullptr;  // pinned scalars read back mid-pipeline (one round trip each)
   unsigned long long* scr() {
@@ -298,6 +301,8 @@ void launch_pass(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32_t
     case 5: NMX_PV(512, 8, RANK_ATOMIC_OR, 2); break;
     case 6: NMX_PV(256, 12, RANK_BALLOT, 2); break;
     case 7: NMX_PV(256, 12, RANK_ATOMIC_OR, 2); break;
+    case 8: NMX_PV(512, 8, RANK_MATCH, 2); break;
+    case 9: NMX_PV(256, 8, RANK_MATCH, 3); break;
     case 0: NMX_PV(256, 16, RANK_BALLOT, 1); break;
     default: NMX_PV(512, 8, RANK_ATOMIC_OR, 2); break;
   }
@@ -1767,6 +1772,67 @@ int stats_host_impl(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const 
                            valid ? c->in_valid.as<uint8_t>() : nullptr, n, space, window_size, out);
 }
 
+// Independent host batches back to back (a stream of analyses, the way a sensor feed
+// arrives): batch k+1's H2D copy runs on the copy stream into the other of two device
+// slots while batch k's device pipeline runs on the context stream, so a sequence of
+// batches is bound by the host link, not by copy + compute. Batch k's nine statistics
+// land in out[9k, 9k + 9). Each batch is one stats_device_impl call (summed matrix of
+// its packets); a failing batch stops the sequence with its error.
+int stats_host_batches_impl(nmx_ctx* c, uint64_t nb, const uint32_t* const* src, const uint32_t* const* dst,
+                            const uint8_t* const* valid, const uint64_t* lens, uint64_t space, int64_t* out) {
+  int b;
+  if (int r = check_space(space, b)) return r;
+  if (nb && (!src || !dst || !lens || !out)) return fail(NMX_EINVAL, "null argument");
+  uint64_t nmax = 0;
+  bool any_valid = false;
+  for (uint64_t k = 0; k < nb; ++k) {
+    if (lens[k] >= (1ull << 32))
+      return fail(NMX_EINVAL, "n must be < 2^32 per batch, got %llu in batch %llu", (unsigned long long)lens[k],
+                  (unsigned long long)k);
+    if (lens[k] && (!src[k] || !dst[k])) return fail(NMX_EINVAL, "null packet columns in batch %llu", (unsigned long long)k);
+    nmax = std::max(nmax, lens[k]);
+    any_valid = any_valid || (valid && valid[k]);
+  }
+  if (!nb) return NMX_OK;
+  if (!c->st2) CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    if (!c->evbc[i]) CK(cudaEventCreateWithFlags(&c->evbc[i], cudaEventDisableTiming));
+    if (!c->evbu[i]) CK(cudaEventCreateWithFlags(&c->evbu[i], cudaEventDisableTiming));
+    c->bat_s[i].grow(std::max<uint64_t>(nmax, 1) * 4 + 16);
+    c->bat_d[i].grow(std::max<uint64_t>(nmax, 1) * 4 + 16);
+    if (any_valid) c->bat_v[i].grow(std::max<uint64_t>(nmax, 1) + 16);
+  }
+  if (!c->evs) CK(cudaEventCreate(&c->evs));
+  CK(cudaEventRecord(c->evs, c->st));
+  CK(cudaStreamWaitEvent(c->st2, c->evs, 0));  // copies start after the caller's prior work
+  bool used[2] = {false, false};
+  auto enqueue_copy = [&](uint64_t k) {
+    const int sl = (int)(k & 1);
+    if (used[sl]) CK(cudaStreamWaitEvent(c->st2, c->evbu[sl], 0));  // batch k-2 is done with the slot
+    const uint64_t L = lens[k];
+    if (L) {
+      CK(cudaMemcpyAsync(c->bat_s[sl].p, src[k], L * 4, cudaMemcpyHostToDevice, c->st2));
+      CK(cudaMemcpyAsync(c->bat_d[sl].p, dst[k], L * 4, cudaMemcpyHostToDevice, c->st2));
+      if (valid && valid[k]) CK(cudaMemcpyAsync(c->bat_v[sl].p, valid[k], L, cudaMemcpyHostToDevice, c->st2));
+    }
+    CK(cudaEventRecord(c->evbc[sl], c->st2));
+  };
+  enqueue_copy(0);
+  int rc = NMX_OK;
+  for (uint64_t k = 0; k < nb && rc == NMX_OK; ++k) {
+    if (k + 1 < nb) enqueue_copy(k + 1);
+    const int sl = (int)(k & 1);
+    CK(cudaStreamWaitEvent(c->st, c->evbc[sl], 0));
+    const uint8_t* v = (valid && valid[k]) ? c->bat_v[sl].as<uint8_t>() : nullptr;
+    rc = stats_device_impl(c, c->bat_s[sl].as<uint32_t>(), c->bat_d[sl].as<uint32_t>(), v, lens[k], space, 0,
+                           out + k * S_COUNT);
+    CK(cudaEventRecord(c->evbu[sl], c->st));
+    used[sl] = true;
+  }
+  CK(cudaStreamSynchronize(c->st2));  // no copy outlives the call (host buffers are borrowed)
+  return rc;
+}
+
 // The reference's own columns (PacketStream: int64 src / dst, bool valid): narrowed to
 // u32 on the host by a few threads per window, into two pinned slots that alternate,
 // while the previous window is copied and partitioned -- the drop-in analytics.stats9
@@ -2463,7 +2529,9 @@ void nmx_destroy(nmx_ctx* c) {
   for (DevBuf* b : {&c->mpcnt, &c->mpoff, &c->mscan, &c->mch, &c->mgh, &c->mplan, &c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->cgk, &c->cgv, &c->cgk2, &c->cgv2, &c->colL_dst, &c->colL_cnt, &c->mcur, &c->moff,
                     &c->mhist2, &c->mgb, &c->mheavy, &c->mdst, &c->ckA, &c->ckB, &c->cvA, &c->cvB, &c->status, &c->lrstatus,
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
-                    &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red})
+                    &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red, &c->ws0, &c->ws1,
+                    &c->wd0, &c->wd1, &c->wv0, &c->wv1, &c->wr0, &c->wr1, &c->bat_s[0], &c->bat_s[1], &c->bat_d[0],
+                    &c->bat_d[1], &c->bat_v[0], &c->bat_v[1]})
     b->release();
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->h_wide) cudaFreeHost(c->h_wide);
@@ -2473,7 +2541,8 @@ void nmx_destroy(nmx_ctx* c) {
   if (c->h_stats) cudaFreeHost(c->h_stats);
   for (auto& e : c->ev) cudaEventDestroy(e);
   for (auto& e : c->evk) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->evc[0], c->evc[1], c->evu[0], c->evu[1], c->evs})
+  for (cudaEvent_t e : {c->evc[0], c->evc[1], c->evu[0], c->evu[1], c->evs, c->evbc[0], c->evbc[1], c->evbu[0],
+                        c->evbu[1]})
     if (e) cudaEventDestroy(e);
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->st) cudaStreamDestroy(c->st);
@@ -2566,6 +2635,11 @@ int nmx_stats9_device(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
 int nmx_stats9_host(nmx_ctx* c, const uint32_t* src, const uint32_t* dst, const uint8_t* valid, uint64_t n,
                     uint64_t address_space, int64_t out[9]) {
   return guarded(c, [&] { return stats_host_impl(c, src, dst, valid, n, address_space, 0, out); });
+}
+
+int nmx_stats9_host_batches(nmx_ctx* c, uint64_t nbatch, const uint32_t* const* src, const uint32_t* const* dst,
+                            const uint8_t* const* valid, const uint64_t* lens, uint64_t address_space, int64_t* out) {
+  return guarded(c, [&] { return stats_host_batches_impl(c, nbatch, src, dst, valid, lens, address_space, out); });
 }
 
 int nmx_stats9_host_i64(nmx_ctx* c, const int64_t* src, const int64_t* dst, const uint8_t* valid, uint64_t n,

@@ -126,16 +126,60 @@ __device__ __forceinline__ uint64_t st_value(uint64_t w) { return w & kValueMask
 
 // Exclusive prefix over predecessors of `tile` for one lane of a lookback
 // (status row stride `stride` words, column `col`). Spins until ready.
+// Four predecessors are loaded per round (independent loads in flight) and consumed
+// in order, so a chain of aggregate-only predecessors costs a quarter of the
+// dependent L2 round trips of a one-word walk.
 __device__ __forceinline__ uint64_t lookback_exclusive(const uint64_t* status, uint32_t tile, int stride, int col,
                                                        uint32_t epoch) {
+  constexpr int V = 4;
   uint64_t excl = 0;
   int64_t p = (int64_t)tile - 1;
   while (p >= 0) {
-    uint64_t w = ld_relaxed(status + (size_t)p * stride + col);
-    if (st_epoch(w) != epoch) continue;  // predecessor not published yet
-    excl += st_value(w);
-    if (st_flag(w) == kFlagInc) break;
-    --p;
+    uint64_t w[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) w[j] = p - j >= 0 ? ld_relaxed(status + (size_t)(p - j) * stride + col) : 0ull;
+    int adv = 0;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (done || adv != j) continue;  // stopped earlier in this round
+      if (p - j < 0) {
+        done = true;
+      } else if (st_epoch(w[j]) == epoch) {
+        excl += st_value(w[j]);
+        adv = j + 1;
+        if (st_flag(w[j]) == kFlagInc) done = true;
+      }  // else: not published yet -- re-poll from p - j
+    }
+    if (done) break;
+    p -= adv;
+  }
+  return excl;
+}
+
+// Warp-cooperative lookback (every lane calls it with the same tile / column): lane
+// l reads predecessor p - l, so one round covers 32 predecessors; the prefix stops at
+// the nearest inclusive word or before the nearest unpublished one.
+__device__ __forceinline__ uint64_t lookback_exclusive_warp(const uint64_t* status, uint32_t tile, int stride, int col,
+                                                            uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t p = (int64_t)tile - 1;
+  while (p >= 0) {
+    const int64_t q = p - lane;
+    const uint64_t w = q >= 0 ? ld_relaxed(status + (size_t)q * stride + col) : st_pack(epoch, kFlagInc, 0);
+    const bool ready = st_epoch(w) == epoch;
+    const uint32_t notready = __ballot_sync(FULL, !ready);
+    const uint32_t inc = __ballot_sync(FULL, ready && st_flag(w) == kFlagInc);
+    const int first_nr = notready ? __ffs(notready) - 1 : 32;
+    const int first_inc = inc ? __ffs(inc) - 1 : 32;
+    const int take = first_inc < first_nr ? first_inc + 1 : first_nr;  // lanes [0, take) are consumed
+    uint64_t v = lane < take ? st_value(w) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    excl += v;
+    if (first_inc < first_nr) break;
+    p -= take;
   }
   return excl;
 }

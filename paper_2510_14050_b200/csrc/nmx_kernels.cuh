@@ -183,12 +183,12 @@ __global__ void __launch_bounds__(256) bin_scan_kernel(const uint32_t* __restric
 // K2: one onesweep LSD pass (8-bit digit at `shift`), stable.
 //   * tile id from an atomic counter (forward progress for the lookback)
 //   * warp-level stable ranking into per-warp smem counters; peers of a digit
-//     found either with 8 ballots (RANK_BALLOT) or one smem atomicOr of the
-//     lane bit (RANK_ATOMIC_OR)
+//     found with 8 ballots (RANK_BALLOT), one smem atomicOr of the lane bit
+//     (RANK_ATOMIC_OR) or one match.any (RANK_MATCH)
 //   * decoupled lookback per digit over epoch-tagged u64 status words
 //   * keys staged in smem in digit order -> near-coalesced scatter
 // ---------------------------------------------------------------------------
-enum { RANK_BALLOT = 0, RANK_ATOMIC_OR = 1 };
+enum { RANK_BALLOT = 0, RANK_ATOMIC_OR = 1, RANK_MATCH = 2 };
 
 template <typename KeyT, bool HAS_VAL, int THREADS, int IPT>
 struct PassSmem {
@@ -265,6 +265,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
     uint32_t peers;
     if (RANK == RANK_BALLOT) {
       peers = warp_digit_peers(d, ok);
+    } else if (RANK == RANK_MATCH) {  // one match instruction, no shared memory
+      peers = __match_any_sync(FULL, ok ? d : 0x100u);
+      if (!ok) peers = 0u;
     } else {
       volatile uint32_t* mp = &s.mm[warp][d];
       if (ok) atomicOr((uint32_t*)mp, lanebit);
@@ -299,24 +302,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
       cnt += c;
     }
   }
-  // publish + decoupled lookback (thread tid owns digit tid)
-  uint64_t excl = 0;
-  if (tid < kRadix) {
-    uint64_t* my = status + (size_t)tile * kRadix + tid;
-    if (tile == 0) {
-      st_relaxed(my, st_pack(epoch, kFlagInc, cnt));
-    } else {
-      st_relaxed(my, st_pack(epoch, kFlagAgg, cnt));
-      excl = lookback_exclusive(status, tile, kRadix, tid, epoch);
-      st_relaxed(my, st_pack(epoch, kFlagInc, excl + cnt));
-    }
-  }
+  // publish the tile's aggregate at once (thread tid owns digit tid); the lookback
+  // waits until the tile is staged, so predecessors have had that long to publish
+  // their inclusive prefixes
+  uint64_t* my = status + (size_t)tile * kRadix + tid;
+  if (tid < kRadix) st_relaxed(my, st_pack(epoch, tile == 0 ? kFlagInc : kFlagAgg, cnt));
   uint32_t total;
   const uint32_t tstart = block_excl_scan_n<THREADS>(cnt, s.wt, &total);
-  if (tid < kRadix) {
-    s.tstart[tid] = tstart;
-    s.gbase[tid] = bin_base[tid] + (uint32_t)excl - tstart;
-  }
+  if (tid < kRadix) s.tstart[tid] = tstart;
   __syncthreads();
 
 #pragma unroll
@@ -328,6 +321,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
       s.keys[lp] = k[i];
       if (HAS_VAL) s.vals[lp] = v[HAS_VAL ? i : 0];
     }
+  }
+  if (tid < kRadix) {
+    uint64_t excl = 0;
+    if (tile != 0) {
+      excl = lookback_exclusive(status, tile, kRadix, tid, epoch);
+      st_relaxed(my, st_pack(epoch, kFlagInc, excl + cnt));
+    }
+    s.gbase[tid] = bin_base[tid] + (uint32_t)excl - tstart;
   }
   __syncthreads();
 #pragma unroll

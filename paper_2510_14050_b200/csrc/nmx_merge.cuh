@@ -180,18 +180,20 @@ __global__ void __launch_bounds__(kMgThreads) merge_add_kernel(
   }
   uint32_t tot;
   uint32_t at = block_excl_scan<uint32_t>(kept, S.wt, &tot);
-  if (tid == 0) {
+  if (tid < 32) {  // warp 0: publish, then a 32-wide lookback
     uint64_t* my = status + t;
     unsigned long long excl = 0;
     if (t == 0) {
-      st_relaxed(my, st_pack(epoch, kFlagInc, tot));
+      if (tid == 0) st_relaxed(my, st_pack(epoch, kFlagInc, tot));
     } else {
-      st_relaxed(my, st_pack(epoch, kFlagAgg, tot));
-      excl = lookback_exclusive(status, t, 1, 0, epoch);
-      st_relaxed(my, st_pack(epoch, kFlagInc, excl + tot));
+      if (tid == 0) st_relaxed(my, st_pack(epoch, kFlagAgg, tot));
+      excl = lookback_exclusive_warp(status, t, 1, 0, epoch);
+      if (tid == 0) st_relaxed(my, st_pack(epoch, kFlagInc, excl + tot));
     }
-    S.prefix = excl;
-    if (d1 == n) *total = excl + tot;
+    if (tid == 0) {
+      S.prefix = excl;
+      if (d1 == n) *total = excl + tot;
+    }
   }
   // compacted output staged in the (now free) slices, then written coalesced
 #pragma unroll
