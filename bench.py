@@ -730,11 +730,12 @@ def run_nmx(args) -> None:
                           else "nmx_stats9_host (include/nmx.h) via paper_2510_14050_b200._lib.stats9") +
                          ", pinned host buffers, one call per step (copy, then device work)"}
         e2e = single
-        if world == 1 and args.e2e_steps > 1:
+        nbatch = max(2, args.steps)
+        if world == 1:
             # a run of K batches through nmx_stats9_host_batches: every step's H2D copy (8 B /
             # packet from pinned memory) and its 72-byte result read-back stay inside the
             # timed region; batch k+1's copy overlaps batch k's device work
-            batches = [(hs.array, hd.array)] * args.e2e_steps
+            batches = [(hs.array, hd.array)] * nbatch
             got = _lib.stats9_batches(batches[:1], space, device=local)
             assert got == [tuple(stats)], (got, stats)
             barrier()
@@ -743,11 +744,11 @@ def run_nmx(args) -> None:
             e1.record(stream)
             barrier()
             assert all(r == tuple(stats) for r in res), res
-            bms = e0.elapsed_time(e1) / args.e2e_steps
+            bms = e0.elapsed_time(e1) / nbatch
             e2e = {"value": n_total / (bms / 1e3), "unit": "packets/s", "h2d_bytes_per_step": 8 * n_total,
-                   "d2h_bytes_per_step": 72, "ms_per_step": bms, "steps": args.e2e_steps,
+                   "d2h_bytes_per_step": 72, "ms_per_step": bms, "steps": nbatch,
                    "api": "nmx_stats9_host_batches (include/nmx.h) via paper_2510_14050_b200._lib.stats9_batches: "
-                          f"{args.e2e_steps} independent 2^{log2n}-packet batches from pinned host buffers in one "
+                          f"{nbatch} independent 2^{log2n}-packet batches (one per timed step) from pinned host buffers in one "
                           "call; batch k+1's H2D copy overlaps batch k's device work",
                    "single_call": single}
         hs.close()
@@ -782,6 +783,11 @@ def run_nmx(args) -> None:
         del stream
 
     parity = golden_parity(args.config, log2n, gen, stats)
+    side = None
+    if world == 1 and args.config == "cfg3" and not args.log2n and not args.no_side:
+        ds.close()
+        dd.close()
+        side = {"cfg4": side_config("cfg4", args, local)}
     if rank != 0:
         if dist is not None:
             dist.barrier()
@@ -846,6 +852,7 @@ def run_nmx(args) -> None:
                                   if len(stage_ms) == 5 else "stages of the rank's last library call")},
         "e2e": e2e,
         "e2e_dropin": dropin,
+        "other_configs": side,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": launches,
@@ -856,6 +863,42 @@ def run_nmx(args) -> None:
         dist.destroy_process_group()
     if parity.get("equal") is False:
         sys.exit(f"bench: stats9 {list(stats)} differ from the golden {parity['want']}")
+
+
+def side_config(name: str, args, local: int) -> dict:
+    """A second BASELINE config timed device-resident in the same run (one GPU): its own
+    input, W warm-up + K timed calls between CUDA events on the library stream, and its
+    statistics against the committed golden."""
+    import torch
+
+    from paper_2510_14050_b200 import _lib
+
+    log2n, space, gen = CONFIGS[name]
+    n = 1 << log2n
+    kind = _lib.GEN_UNIFORM if gen == "uniform" else _lib.GEN_POWERLAW
+    ds, dd = _lib.DeviceArray(n, device=local), _lib.DeviceArray(n, device=local)
+    _lib.generate(kind, 7, 0, n, space, ds, dd, device=local)
+    for _ in range(args.warmup):
+        stats = _lib.stats9(ds, dd, None, space, device=local)
+    ctx = _lib.context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    torch.cuda.synchronize(local)
+    e0.record(stream)
+    for _ in range(args.steps):
+        stats = _lib.stats9(ds, dd, None, space, device=local)
+        launches += ctx.last_timing()["kernel_launches"]
+    e1.record(stream)
+    torch.cuda.synchronize(local)
+    ms = e0.elapsed_time(e1) / args.steps
+    t = ctx.last_timing()
+    ds.close()
+    dd.close()
+    return {"workload": f"{name}: 2^{log2n} packets {gen} over {space} addresses, device-resident",
+            "value": n / (ms / 1e3), "unit": "packets/s", "ms_per_step": ms, "steps": args.steps,
+            "warmup": args.warmup, "stats9": list(stats), "parity": golden_parity(name, log2n, gen, stats),
+            "stages_ms": t.get("stages_ms"), "gpu_launches": launches}
 
 
 def spawn_ranks(n: int) -> int:
@@ -889,6 +932,7 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-side", action="store_true", help="skip the cfg4 side measurement of the default run")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))

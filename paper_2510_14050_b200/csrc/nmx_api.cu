@@ -301,8 +301,6 @@ void launch_pass(nmx_ctx* c, const Src& src, uint64_t items, KeyT* out, uint32_t
     case 5: NMX_PV(512, 8, RANK_ATOMIC_OR, 2); break;
     case 6: NMX_PV(256, 12, RANK_BALLOT, 2); break;
     case 7: NMX_PV(256, 12, RANK_ATOMIC_OR, 2); break;
-    case 8: NMX_PV(512, 8, RANK_MATCH, 2); break;
-    case 9: NMX_PV(256, 8, RANK_MATCH, 3); break;
     case 0: NMX_PV(256, 16, RANK_BALLOT, 1); break;
     default: NMX_PV(512, 8, RANK_ATOMIC_OR, 2); break;
   }

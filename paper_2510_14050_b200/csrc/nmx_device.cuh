@@ -126,6 +126,7 @@ __device__ __forceinline__ uint64_t st_value(uint64_t w) { return w & kValueMask
 
 // Exclusive prefix over predecessors of `tile` for one lane of a lookback
 // (status row stride `stride` words, column `col`). Spins until ready.
+constexpr unsigned kLookbackBackoffNs = 64;
 // Four predecessors are loaded per round (independent loads in flight) and consumed
 // in order, so a chain of aggregate-only predecessors costs a quarter of the
 // dependent L2 round trips of a one-word walk.
@@ -152,6 +153,7 @@ __device__ __forceinline__ uint64_t lookback_exclusive(const uint64_t* status, u
       }  // else: not published yet -- re-poll from p - j
     }
     if (done) break;
+    if (!adv) __nanosleep(kLookbackBackoffNs);  // nothing published yet: yield the issue slots
     p -= adv;
   }
   return excl;
@@ -179,6 +181,7 @@ __device__ __forceinline__ uint64_t lookback_exclusive_warp(const uint64_t* stat
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     excl += v;
     if (first_inc < first_nr) break;
+    if (!take) __nanosleep(kLookbackBackoffNs);
     p -= take;
   }
   return excl;

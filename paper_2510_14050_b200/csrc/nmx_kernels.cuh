@@ -183,12 +183,13 @@ __global__ void __launch_bounds__(256) bin_scan_kernel(const uint32_t* __restric
 // K2: one onesweep LSD pass (8-bit digit at `shift`), stable.
 //   * tile id from an atomic counter (forward progress for the lookback)
 //   * warp-level stable ranking into per-warp smem counters; peers of a digit
-//     found with 8 ballots (RANK_BALLOT), one smem atomicOr of the lane bit
-//     (RANK_ATOMIC_OR) or one match.any (RANK_MATCH)
+//     found either with 8 ballots (RANK_BALLOT) or one smem atomicOr of the
+//     lane bit (RANK_ATOMIC_OR); match.any ranking measured 1.4-1.8x slower
+//     (profiles/r02v_onesweep_variants.txt)
 //   * decoupled lookback per digit over epoch-tagged u64 status words
 //   * keys staged in smem in digit order -> near-coalesced scatter
 // ---------------------------------------------------------------------------
-enum { RANK_BALLOT = 0, RANK_ATOMIC_OR = 1, RANK_MATCH = 2 };
+enum { RANK_BALLOT = 0, RANK_ATOMIC_OR = 1 };
 
 template <typename KeyT, bool HAS_VAL, int THREADS, int IPT>
 struct PassSmem {
@@ -265,9 +266,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
     uint32_t peers;
     if (RANK == RANK_BALLOT) {
       peers = warp_digit_peers(d, ok);
-    } else if (RANK == RANK_MATCH) {  // one match instruction, no shared memory
-      peers = __match_any_sync(FULL, ok ? d : 0x100u);
-      if (!ok) peers = 0u;
     } else {
       volatile uint32_t* mp = &s.mm[warp][d];
       if (ok) atomicOr((uint32_t*)mp, lanebit);

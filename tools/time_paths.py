@@ -21,6 +21,8 @@ print(f"lsd 2^{lg}: total {best['total_ms']:.3f} ms, {best['dom_name']} {best['d
       f"x{best['dom_launches']} ({best['dom_bytes'] / best['dom_launches'] / (best['dom_ms'] / best['dom_launches']) / 1e6:.0f} GB/s) {st}", flush=True)
 del os.environ["NMX_PATH"]
 ds.close(); dd.close()
+if not mg:
+    sys.exit(0)
 m = 1 << mg
 ds, dd = _lib.DeviceArray(m), _lib.DeviceArray(m)
 parts = []
