@@ -430,8 +430,15 @@ struct RowsOut {
 
 // hist -> onesweep row sort -> fused link/row kernel. Link + row statistics
 // accumulate into c->stats; the column entries are left in c->ckA / c->cvA.
-// hist -> onesweep LSD sort of the packed keys; returns the sorted keys (m valid)
-uint64_t* sort_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb, uint64_t* m_out) {
+bool sort_rows_msd(nmx_ctx* c, const PacketSrc& ps, int kb, uint64_t* m_out, uint64_t** keys_out);
+// the packed keys of the valid packets, fully sorted (m valid): the MSD partition +
+// per-group shared-memory sort when the inputs allow it, else the LSD onesweep passes.
+// kb_used: key bits that can be nonzero (default 2b + wb)
+uint64_t* sort_rows(nmx_ctx* c, const PacketSrc& ps, int b, int wb, uint64_t* m_out, int kb_used = 0) {
+  {
+    uint64_t* k = nullptr;
+    if (sort_rows_msd(c, ps, kb_used ? kb_used : 2 * b + wb, m_out, &k)) return k;
+  }
   const uint64_t n = ps.n;
   const int kb = 2 * b + wb;
   const int npass = (kb + 7) / 8;
@@ -1068,7 +1075,7 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
   uint64_t lbase = 0;
   int consumed = Dc;
   set_smem(seg_scatter_kernel<uint64_t, false>, sizeof(SegSmem<uint64_t, false>));
-  set_smem(local_cols_kernel, sizeof(LocColSmem));
+  set_smem(local_cols_kernel<false>, sizeof(LocColSmem));
   for (int l = 0; l < L && m; ++l) {
     const int dbits = w[l];
     consumed += dbits;
@@ -1102,7 +1109,7 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
     if (t.light) {
       const uint32_t ngroups = seg_plan_groups(c, C, t.light, kLocColChunk);
       const unsigned grid = (unsigned)std::min<uint64_t>(ngroups, (uint64_t)c->sms * 4);
-      local_cols_kernel<<<grid, kLocColThreads, sizeof(LocColSmem), c->st>>>(
+      local_cols_kernel<false><<<grid, kLocColThreads, sizeof(LocColSmem), c->st>>>(
           light + lbase, c->mplan.as<uint4>(), ngroups, c->stats.as<unsigned long long>(), kNoDirect);
       CK_LAUNCH();
       ++c->launches;
@@ -1119,7 +1126,11 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
 // whose arrays may alias ckA / cvA (the first level reads them all before the
 // second level writes ckA / cvA): MSD partition by destination bits ->
 // shared-memory grouping -> heavy destinations via LSD + col_kernel.
-void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32_t* prehist) {
+// wb > 0 (windowed): entries are dst' = window << (b - wb) | dst with b = address bits
+// + wb; returns false (nothing more queued) when a heavy destination bucket needs the
+// segmented levels, which keep no per-window statistics -- the caller reruns the call
+// on the LSD path.
+bool msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32_t* prehist, int wb = 0) {
   // the levels move packed u64 items (dst << 32 | count, key bits [32, 32 + b))
   // through the row key buffers, free once the row half is queued
   uint64_t* ce = nullptr;
@@ -1137,9 +1148,15 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   {
     const uint32_t* ngp = seg_plan_groups_dev(c, 1u << Dc, cs.n, kLocColChunk,
                                               b - Dc < 31 ? kLocColDirect >> (b - Dc) : 0);
-    set_smem(local_cols_kernel, sizeof(LocColSmem));
-    local_cols_kernel<<<c->sms * 4, kLocColThreads, sizeof(LocColSmem), c->st>>>(
-        ce, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp);
+    if (wb) {
+      set_smem(local_cols_kernel<true>, sizeof(LocColSmem));
+      local_cols_kernel<true><<<c->sms * 4, kLocColThreads, sizeof(LocColSmem), c->st>>>(
+          ce, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp, Dc - wb, b - wb);
+    } else {
+      set_smem(local_cols_kernel<false>, sizeof(LocColSmem));
+      local_cols_kernel<false><<<c->sms * 4, kLocColThreads, sizeof(LocColSmem), c->st>>>(
+          ce, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp);
+    }
     CK_LAUNCH();
     ++c->launches;
   }
@@ -1147,11 +1164,13 @@ void msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   const uint64_t u = msd_partition_wait(c, &sp);
   c->scr_off = 0;
   if (sp.t.big) c->had_heavy = true;
-  if (!u) return;
+  if (!u) return true;
   if (sp.t.big) {  // heavy destination buckets: segmented MSD levels (nmx_seg.cuh)
+    if (wb) return false;
     c->cgk2.grow((size_t)sp.t.big * 8);
     heavy_cols(c, sp.t.big, sp.t.nbig, b, Dc);
   }
+  return true;
 }
 
 // Level 1 of the dense row partition for one window of packets (streaming):
@@ -1199,9 +1218,14 @@ uint64_t msd_window_level1(nmx_ctx* c, const PacketSrc& ps, int kb, int D, uint6
 // 0) as a ColConcatSrc; *chist_out = their first-level histogram + count.
 // pre_m > 0: keysA already holds the level-1 partition of pre_m valid keys
 // (streamed windows); n bounds the buffers. Empty (n1 = n2 = 0) if no valid packet.
+// window_size > 0 (wb window bits, b + wb <= 32): keys w << 2b | src << b | dst, the
+// top D key bits = wb window bits + D - wb source bits, statistics per window; a heavy
+// row bucket sets *aborted (the caller reruns the call on the LSD path).
 ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
-                      int b, int D, uint64_t pre_m, uint32_t** chist_out) {
-  const int kb = 2 * b;
+                      int b, int D, uint64_t pre_m, uint32_t** chist_out, int wb = 0, uint64_t window_size = 0,
+                      bool* aborted = nullptr) {
+  const int kb = 2 * b + wb;
+  const int bs = b + wb;  // source' = window << b | src
   // every buffer the step needs is sized up front (n bounds m, u and the heavy parts)
   c->keysA.grow(n * 8);
   c->keysB.grow(n * 8);
@@ -1214,7 +1238,7 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   auto* ccount = reinterpret_cast<unsigned long long*>(chist + kMsdMaxBins);
   CK(cudaMemsetAsync(chist, 0, (kMsdMaxBins + 4) * 4, c->st));
 
-  PacketSrc ps{d_src, d_dst, d_valid, n, 0, b};
+  PacketSrc ps{d_src, d_dst, d_valid, n, wb ? window_size : 0, b};
   ps.quad = !(((uintptr_t)d_src | (uintptr_t)d_dst) & 15) && !((uintptr_t)d_valid & 3);
   c->mark();  // 1: row partition start
   uint64_t* keys = nullptr;
@@ -1223,25 +1247,37 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   sp.hk = c->keysC.p;
   // the partition's totals come back while the light groups run (plans and
   // group count derived on the device)
-  msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
-                                            c->keysB.as<uint64_t>(), nullptr, &keys, &dummy, nullptr, &sp, pre_m,
-                                            true);
+  if (wb)
+    msd_partition<PacketSrcWin, uint64_t, false>(c, PacketSrcWin{ps}, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
+                                                 c->keysB.as<uint64_t>(), nullptr, &keys, &dummy, nullptr, &sp, pre_m,
+                                                 true);
+  else
+    msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
+                                              c->keysB.as<uint64_t>(), nullptr, &keys, &dummy, nullptr, &sp, pre_m,
+                                              true);
   c->last_sort_launches = c->msd_levels;
   c->mark();  // 2: row partition end
   ColConcatSrc cs{c->colL_dst.as<uint64_t>(), 0, c->ckA.as<uint64_t>(), 0, 0};
   cs.quad = true;  // context buffers are cudaMalloc-aligned
   const uint32_t nb = 1u << D;
-  const int Dc = std::min(D, b);
-  const int cshift = b - msd_first_bits(Dc);
+  const int Dc = std::min(D, bs);
+  const int cshift = bs - msd_first_bits(Dc);
   if (c->capturing)  // light count unknown while recording: every slot past it must read as a hole
     CK(cudaMemsetAsync(c->colL_dst.p, 0, n * 8, c->st));
   {
     const uint32_t* ngp = seg_plan_groups_dev(c, nb, pre_m ? pre_m : n, kLocChunk,
-                                              b - D < 31 ? kLocDirect >> (b - D) : 0);
-    set_smem(local_rows_kernel<false>, sizeof(LocSmem));
-    local_rows_kernel<false><<<c->sms * 2, kLocThreads, sizeof(LocSmem), c->st>>>(
-        keys, c->mplan.as<uint4>(), 0, b, c->colL_dst.as<uint64_t>(), cshift, chist,
-        ccount, c->stats.as<unsigned long long>(), SrcTable{}, b - D, ngp);
+                                              bs - D < 31 ? kLocDirect >> (bs - D) : 0);
+    if (wb) {
+      set_smem(local_rows_kernel<false, true>, sizeof(LocSmem));
+      local_rows_kernel<false, true><<<c->sms * 2, kLocThreads, sizeof(LocSmem), c->st>>>(
+          keys, c->mplan.as<uint4>(), 0, b, c->colL_dst.as<uint64_t>(), cshift, chist,
+          ccount, c->stats.as<unsigned long long>(), SrcTable{}, bs - D, ngp, D - wb);
+    } else {
+      set_smem(local_rows_kernel<false>, sizeof(LocSmem));
+      local_rows_kernel<false><<<c->sms * 2, kLocThreads, sizeof(LocSmem), c->st>>>(
+          keys, c->mplan.as<uint4>(), 0, b, c->colL_dst.as<uint64_t>(), cshift, chist,
+          ccount, c->stats.as<unsigned long long>(), SrcTable{}, b - D, ngp);
+    }
     CK_LAUNCH();
     ++c->launches;
   }
@@ -1254,6 +1290,10 @@ ColConcatSrc msd_rows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   if (!m) return cs;
   uint64_t uh = 0;
   if (sp.t.big) c->had_heavy = true;
+  if (sp.t.big && wb) {  // heavy buckets keep no per-window statistics: LSD path instead
+    if (aborted) *aborted = true;
+    return cs;
+  }
   if (sp.t.big) {  // heavy row buckets: segmented MSD levels (nmx_seg.cuh)
     c->keysD.grow((size_t)sp.t.big * 8);
     uh = heavy_rows(c, sp.t.big, sp.t.nbig, b, D, cshift, chist, ccount);
@@ -1273,6 +1313,73 @@ void run_pipeline_msd(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   // ---- columns: MSD partition of the (dst, count) entries by destination bits ----
   if (cs.n) msd_columns(c, cs, b, std::min(D, b), chist);
   stage_finish(c, 1);
+}
+
+// Sorted packet keys on the MSD machinery (COO builds): dense partition of the top D
+// key bits, then local_sort_kernel per group of whole light buckets, in place. Returns
+// false (the LSD sort runs instead; nothing the caller sees was written) for small or
+// narrow inputs and when a bucket is heavy (> kSegCap keys).
+bool sort_rows_msd(nmx_ctx* c, const PacketSrc& ps, int kb, uint64_t* m_out, uint64_t** keys_out) {
+  const uint64_t n = ps.n;
+  const int D = msd_bits(n, kb);
+  if (!D) return false;
+  c->keysA.grow(n * 8);
+  c->keysB.grow(n * 8);
+  c->keysC.grow(n * 8);
+  c->mark();  // 1: sort start
+  uint64_t* keys = nullptr;
+  uint32_t* dummy = nullptr;
+  MsdSplit sp;
+  sp.hk = c->keysC.p;
+  // window ids (window_size < 4 keeps the scalar per-packet loads of PacketSrc)
+  const uint64_t m =
+      ps.window_size >= 4
+          ? msd_partition<PacketSrcWin, uint64_t, false>(c, PacketSrcWin{ps}, n, kb, D, c->keysA.as<uint64_t>(),
+                                                         nullptr, c->keysB.as<uint64_t>(), nullptr, &keys, &dummy,
+                                                         nullptr, &sp, 0, false)
+          : msd_partition<PacketSrc, uint64_t, false>(c, ps, n, kb, D, c->keysA.as<uint64_t>(), nullptr,
+                                                      c->keysB.as<uint64_t>(), nullptr, &keys, &dummy, nullptr, &sp,
+                                                      0, false);
+  if (sp.t.big) {  // the LSD sort starts from zeroed histograms and re-marks its stages
+    CK(cudaMemsetAsync(c->small.p, 0, kSmallWords * sizeof(uint32_t), c->st));
+    c->nev = 1;
+    return false;
+  }
+  *m_out = m;
+  *keys_out = m ? keys : nullptr;
+  if (m) {
+    const uint32_t* ngp = seg_plan_groups_dev(c, 1u << D, n, kLocChunk, 0);
+    set_smem(local_sort_kernel, sizeof(SortSmem));
+    local_sort_kernel<<<c->sms * 2, kSortThreads, sizeof(SortSmem), c->st>>>(keys, c->mplan.as<uint4>(), ngp);
+    CK_LAUNCH();
+    ++c->launches;
+  }
+  c->last_sort_launches = c->msd_levels + 1;
+  c->mark();  // 2: sort end
+  return true;
+}
+
+// Per-window statistics on the MSD path (analytics.py:109-130 analyze_dataset of
+// build_matrices(stream, W), traffic.py:221-242): the window id rides above the
+// address bits of the row keys and above the destination of the column entries, so
+// the partitions never mix windows; the grouping kernels add into stats[9 w ..].
+// Needs b + wb <= 32 (anonymized address spaces). Returns false, with nothing
+// reported, when a heavy bucket appears (the caller takes the LSD path).
+constexpr uint64_t kWinMsdMinWindow = 1ull << 12;
+bool run_pipeline_msd_windows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                              uint64_t n, int b, uint64_t window_size, uint64_t W) {
+  const int wb = (int)ceil_log2(W);
+  if (b + wb > 32 || window_size < kWinMsdMinWindow) return false;
+  const int D = msd_bits(n, b + wb);
+  if (!D || D < wb + 4) return false;
+  stage_begin(c, W);
+  uint32_t* chist = nullptr;
+  bool aborted = false;
+  const ColConcatSrc cs = msd_rows(c, d_src, d_dst, d_valid, n, b, D, 0, &chist, wb, window_size, &aborted);
+  if (aborted) return false;
+  if (cs.n && !msd_columns(c, cs, b + wb, std::min(D, b + wb), chist, wb)) return false;
+  stage_finish(c, W);
+  return true;
 }
 
 // ---- small calls as one CUDA graph -------------------------------------------
@@ -1388,6 +1495,8 @@ void run_pipeline(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, cons
   if (W == 1) {
     const int D = msd_bits(n, b);
     if (D) return run_pipeline_msd(c, d_src, d_dst, d_valid, n, b, D);
+  } else if (run_pipeline_msd_windows(c, d_src, d_dst, d_valid, n, b, window_size, W)) {
+    return;
   }
   const int wb = W > 1 ? (int)ceil_log2(W) : 0;
   stage_begin(c, W);
@@ -3190,7 +3299,16 @@ int nmx_coo_from_packets(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_ds
     uint64_t u = 0;
     if (n) {
       PacketSrc ps{d_src, d_dst, d_valid, n, 0, 32};
-      uint64_t* keys = sort_rows(c, ps, 32, 0, &m);
+      // keys (src << 32 | dst) only use 32 + bits(max address) bits: the MSD levels
+      // take their digits from there (a narrow address space would otherwise leave
+      // every key in one bucket)
+      c->rmax.grow(64);
+      CK(cudaMemsetAsync(c->rmax.p, 0, 4, c->st));
+      launch_max_addr(c, d_src, d_dst, n);
+      unsigned int mx = 0;
+      CK(cudaMemcpyAsync(&mx, c->rmax.p, 4, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      uint64_t* keys = sort_rows(c, ps, 32, 0, &m, 32 + (int)ceil_log2((uint64_t)mx + 1));
       if (m) {
         const uint64_t tiles = (m + kUniqTile - 1) / kUniqTile;
         c->mhist2.grow((tiles + 8) * 4);

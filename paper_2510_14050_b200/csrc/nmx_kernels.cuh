@@ -95,6 +95,33 @@ struct PacketSrc {
   }
 };
 
+// PacketSrc with window ids (window_size >= 4): quads keep their 128-bit loads and
+// pay one division each (at most one window edge inside a quad). A separate type so
+// the window-free kernels keep their exact code.
+struct PacketSrcWin : PacketSrc {
+  __device__ __forceinline__ void load_quad(uint64_t q, uint64_t* key, bool* ok) const {
+    const uint64_t i = 4 * q;
+    if (quad && i + 4 <= n) {
+      const uint4 s4 = __ldg(reinterpret_cast<const uint4*>(src) + q);
+      const uint4 d4 = __ldg(reinterpret_cast<const uint4*>(dst) + q);
+      uint32_t vv = 0x01010101u;
+      if (valid) vv = __ldg(reinterpret_cast<const uint32_t*>(valid) + q);
+      const uint32_t m = am();
+      const uint64_t w = i / window_size, edge = (w + 1) * window_size;
+      const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        key[t] = ((i + t < edge ? w : w + 1) << (2 * b)) | ((uint64_t)(sv[t] & m) << b) | (dv[t] & m);
+        ok[t] = ((vv >> (8 * t)) & 0xFFu) != 0;
+      }
+    } else {
+      uint32_t v;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) ok[t] = load(i + t, key[t], v);
+    }
+  }
+};
+
 template <typename KeyT, bool HAS_VAL>
 struct KeySrc {
   const KeyT* keys;

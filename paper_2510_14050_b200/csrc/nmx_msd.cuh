@@ -68,6 +68,10 @@ __device__ __forceinline__ void quad_items(const PacketSrc& s, uint64_t q, uint6
   s.load_quad(q, k, ok);
   v[0] = v[1] = v[2] = v[3] = 0;
 }
+__device__ __forceinline__ void quad_items(const PacketSrcWin& s, uint64_t q, uint64_t* k, uint32_t* v, bool* ok) {
+  s.load_quad(q, k, ok);
+  v[0] = v[1] = v[2] = v[3] = 0;
+}
 template <typename KeyT, bool HAS_VAL>
 __device__ __forceinline__ void quad_items(const KeySrc<KeyT, HAS_VAL>& s, uint64_t q, KeyT* k, uint32_t* v,
                                            bool* ok) {
@@ -634,13 +638,47 @@ static_assert(offsetof(LocSmem, t2key) == offsetof(LocSmem, bms) + 4 * kBmWords 
 // and fan-out are partial; they are summed per warp (all lanes usually share
 // one source), per group in the exact source table, and per source in the
 // global table `gsrc` (one atomic per source and group).
-template <bool PARTIAL>
+// link / row totals of a warp's lanes -> one set of atomics (every lane calls it)
+__device__ __forceinline__ void flush_rows(unsigned long long* __restrict__ st, unsigned long long* __restrict__ ccount,
+                                           uint32_t a_valid, uint32_t a_links, uint32_t a_srcs, uint32_t a_mlink,
+                                           uint32_t a_msrc, uint32_t a_mfan) {
+  if (a_srcs) {  // every counted source has >= 1 packet and >= 1 link
+    a_msrc = max(a_msrc, 1u);
+    a_mfan = max(a_mfan, 1u);
+  }
+  unsigned long long w_valid = a_valid, w_links = a_links, w_srcs = a_srcs;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    w_valid += __shfl_xor_sync(FULL, w_valid, o);
+    w_links += __shfl_xor_sync(FULL, w_links, o);
+    w_srcs += __shfl_xor_sync(FULL, w_srcs, o);
+    a_mlink = max(a_mlink, __shfl_xor_sync(FULL, a_mlink, o));
+    a_msrc = max(a_msrc, __shfl_xor_sync(FULL, a_msrc, o));
+    a_mfan = max(a_mfan, __shfl_xor_sync(FULL, a_mfan, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (w_links) atomicAdd(ccount, w_links);
+    if (w_valid) atomicAdd(st + S_VALID, w_valid);
+    if (w_links) atomicAdd(st + S_LINKS, w_links);
+    if (w_srcs) atomicAdd(st + S_SRCS, w_srcs);
+    if (a_mlink) atomicMax(st + S_MAXLINK, (unsigned long long)a_mlink);
+    if (a_msrc) atomicMax(st + S_MAXSRCPK, (unsigned long long)a_msrc);
+    if (a_mfan) atomicMax(st + S_MAXFANOUT, (unsigned long long)a_mfan);
+  }
+}
+
+// WIN (per-window statistics, analytics.py:109-130): keys carry the window id above
+// the 2b address bits and the statistics go to stats[9 w ..]. A group whose buckets lie
+// in one window (plan .z / .w >> wsh) accumulates in registers and flushes at its end;
+// a group spanning windows (only at window edges) adds per key. Column entries carry
+// the window above the destination (dst' = w << b | dst, b + wb <= 32).
+template <bool PARTIAL, bool WIN = false>
 __global__ void __launch_bounds__(kLocThreads, 2)
     local_rows_kernel(const uint64_t* __restrict__ keys, const uint4* __restrict__ plan, uint32_t ngroups, int b,
                       uint64_t* __restrict__ col, int cshift,
                       uint32_t* __restrict__ chist, unsigned long long* __restrict__ ccount,
                       unsigned long long* __restrict__ stats, SrcTable gsrc, int dsb,
-                      const uint32_t* __restrict__ ngp = nullptr) {
+                      const uint32_t* __restrict__ ngp = nullptr, int wsh = 0) {
   if (ngp) ngroups = *ngp;  // group count on the device (grid sized for the SMs)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocSmem& s = *reinterpret_cast<LocSmem*>(smem_raw);
@@ -699,6 +737,12 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         shi = (uint64_t)((pc.w - 1) >> -dsb) + 1;
       }
       direct = shi - slo <= kLocDirect;
+    }
+    int gwin = 0;  // WIN: the group's window, -1 when its buckets span several
+    if constexpr (WIN) {
+      const uint4 pc = s.plan[cur];
+      const uint32_t w0 = pc.z >> wsh, w1 = (pc.w > pc.z ? pc.w - 1 : pc.z) >> wsh;
+      gwin = w0 == w1 ? (int)w0 : -1;
     }
     // 1. hash counters (the 16-bit counter indices stay in registers for phases 2-3)
     // (source counter indices are recomputed where the hashed source path needs them)
@@ -889,19 +933,39 @@ __global__ void __launch_bounds__(kLocThreads, 2)
           s.t1cnt[hl[r]] = 0;
         }
       }
-      col[pos] = ((key & dmask) << 32) | c;  // packed column slot (dst << 32 | count; 0 = hole)
+      uint64_t ck = key & dmask;
+      if constexpr (WIN) ck |= (key >> (2 * b)) << b;  // dst' = window << b | dst
+      col[pos] = (ck << 32) | c;  // packed column slot (dst << 32 | count; 0 = hole)
+      unsigned long long* sw = WIN ? stats + (size_t)S_COUNT * (key >> (2 * b)) : stats;  // straddling groups
       if (c) {
-        atomicAdd(&s.chist[(uint32_t)(key & dmask) >> cshift], 1u);  // the column partition's first level
-        a_links += 1;
-        a_valid += c;
-        a_mlink = max(a_mlink, c);
+        atomicAdd(&s.chist[(uint32_t)ck >> cshift], 1u);  // the column partition's first level
+        if (WIN && gwin < 0) {
+          atomicAdd(ccount, 1ull);
+          atomicAdd(sw + S_LINKS, 1ull);
+          atomicAdd(sw + S_VALID, (unsigned long long)c);
+          atomicMax(sw + S_MAXLINK, (unsigned long long)c);
+        } else {
+          a_links += 1;
+          a_valid += c;
+          a_mlink = max(a_mlink, c);
+        }
       }
       if (st[r] & 4) {  // single-packet source (its maxima of 1 are folded in at the end)
-        a_srcs += 1;
+        if (WIN && gwin < 0) {
+          atomicAdd(sw + S_SRCS, 1ull);
+          atomicMax(sw + S_MAXSRCPK, 1ull);
+          atomicMax(sw + S_MAXFANOUT, 1ull);
+        } else {
+          a_srcs += 1;
+        }
       } else if (st[r] & 8) {
         const uint32_t pf = direct ? dir[hs[r]] : s.t2pf[hs[r]];
         if (PARTIAL) {
           gsrc.add((uint32_t)(key >> b), ((unsigned long long)(pf >> 16) << 32) | (pf & 0xFFFFu));
+        } else if (WIN && gwin < 0) {
+          atomicAdd(sw + S_SRCS, 1ull);
+          atomicMax(sw + S_MAXSRCPK, (unsigned long long)(pf & 0xFFFFu));
+          atomicMax(sw + S_MAXFANOUT, (unsigned long long)(pf >> 16));
         } else {
           a_srcs += 1;
           a_msrc = max(a_msrc, pf & 0xFFFFu);
@@ -922,10 +986,21 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     if (tid == 0 && s.sp_src_pk) {
       if (PARTIAL) {
         gsrc.add(0xFFFFFFFFu, ((unsigned long long)s.sp_src_fo << 32) | s.sp_src_pk);
+      } else if (WIN && gwin < 0) {  // source' 0xFFFFFFFF: the last window (b + wb = 32)
+        unsigned long long* sw = stats + (size_t)S_COUNT * (0xFFFFFFFFu >> b);
+        atomicAdd(sw + S_SRCS, 1ull);
+        atomicMax(sw + S_MAXSRCPK, (unsigned long long)s.sp_src_pk);
+        atomicMax(sw + S_MAXFANOUT, (unsigned long long)s.sp_src_fo);
       } else {
         a_srcs += 1;
         a_msrc = max(a_msrc, s.sp_src_pk);
         a_mfan = max(a_mfan, s.sp_src_fo);
+      }
+    }
+    if constexpr (WIN) {
+      if (gwin >= 0) {  // one window: this group's totals now
+        flush_rows(stats + (size_t)S_COUNT * gwin, ccount, a_valid, a_links, a_srcs, a_mlink, a_msrc, a_mfan);
+        a_valid = a_links = a_srcs = a_mlink = a_msrc = a_mfan = 0;
       }
     }
     __syncthreads();
@@ -934,29 +1009,7 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     for (int r = 0; r < kLocPerThread; ++r) kr[r] = kn[r];
     nmine = nnext;
   }
-  if (a_srcs) {  // every counted source has >= 1 packet and >= 1 link
-    a_msrc = max(a_msrc, 1u);
-    a_mfan = max(a_mfan, 1u);
-  }
-  unsigned long long w_valid = a_valid, w_links = a_links, w_srcs = a_srcs;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    w_valid += __shfl_xor_sync(FULL, w_valid, o);
-    w_links += __shfl_xor_sync(FULL, w_links, o);
-    w_srcs += __shfl_xor_sync(FULL, w_srcs, o);
-    a_mlink = max(a_mlink, __shfl_xor_sync(FULL, a_mlink, o));
-    a_msrc = max(a_msrc, __shfl_xor_sync(FULL, a_msrc, o));
-    a_mfan = max(a_mfan, __shfl_xor_sync(FULL, a_mfan, o));
-  }
-  if (lane == 0) {
-    if (w_links) atomicAdd(ccount, w_links);
-    if (w_valid) atomicAdd(stats + S_VALID, w_valid);
-    if (w_links) atomicAdd(stats + S_LINKS, w_links);
-    if (w_srcs) atomicAdd(stats + S_SRCS, w_srcs);
-    if (a_mlink) atomicMax(stats + S_MAXLINK, (unsigned long long)a_mlink);
-    if (a_msrc) atomicMax(stats + S_MAXSRCPK, (unsigned long long)a_msrc);
-    if (a_mfan) atomicMax(stats + S_MAXFANOUT, (unsigned long long)a_mfan);
-  }
+  if (!WIN) flush_rows(stats, ccount, a_valid, a_links, a_srcs, a_mlink, a_msrc, a_mfan);
   __syncthreads();
   if (tid < (1 << kMsdMaxLevelBits) && s.chist[tid]) atomicAdd(chist + tid, s.chist[tid]);
 }
@@ -1037,15 +1090,36 @@ static_assert(offsetof(LocColSmem, key) == offsetof(LocColSmem, bm) + 4 * kBmWor
 // destination whose hash counter reads "once" has fan-in 1 and `count` packets.
 // Direct destinations as in local_rows_kernel: groups whose buckets span
 // <= kLocColDirect destinations (bucket << dsb) count in slots dst - lo.
+__device__ __forceinline__ void flush_cols(unsigned long long* __restrict__ st, uint32_t a_cnt, uint32_t a_fanin,
+                                           uint32_t a_pk) {
+  if (a_cnt) a_fanin = max(a_fanin, 1u);
+  unsigned long long w_cnt = a_cnt;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    w_cnt += __shfl_xor_sync(FULL, w_cnt, o);
+    a_fanin = max(a_fanin, __shfl_xor_sync(FULL, a_fanin, o));
+    a_pk = max(a_pk, __shfl_xor_sync(FULL, a_pk, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (w_cnt) atomicAdd(st + S_DSTS, w_cnt);
+    if (a_fanin) atomicMax(st + S_MAXFANIN, (unsigned long long)a_fanin);
+    if (a_pk) atomicMax(st + S_MAXDSTPK, (unsigned long long)a_pk);
+  }
+}
+
+// WIN: entries carry dst' = window << wdb | dst; per-window statistics as in
+// local_rows_kernel (group window = plan .z / .w >> wsh)
+template <bool WIN = false>
 __global__ void __launch_bounds__(kLocColThreads, 4)
     local_cols_kernel(const uint64_t* __restrict__ ce, const uint4* __restrict__ plan, uint32_t ngroups,
-                      unsigned long long* __restrict__ stats, int dsb, const uint32_t* __restrict__ ngp = nullptr) {
+                      unsigned long long* __restrict__ stats, int dsb, const uint32_t* __restrict__ ngp = nullptr,
+                      int wsh = 0, int wdb = 0) {
   if (ngp) ngroups = *ngp;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
   uint32_t* dfan = reinterpret_cast<uint32_t*>(smem_raw + offsetof(LocColSmem, bm));  // bm .. npk contiguous
   uint32_t* dpk = dfan + kLocColDirect;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   for (int i = tid; i < kBmWords; i += kLocColThreads) s.bm[i] = 0;
   for (int i = tid; i < kLocCT; i += kLocColThreads) {
     s.key[i] = 0;
@@ -1087,6 +1161,12 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
       const uint4 pc = s.plan[cur];
       dlo = pc.z << dsb;
       direct = ((uint64_t)pc.w << dsb) - dlo <= kLocColDirect;
+    }
+    int gwin = 0;  // WIN: the group's window, -1 when its buckets span several
+    if constexpr (WIN) {
+      const uint4 pc = s.plan[cur];
+      const uint32_t w0 = pc.z >> wsh, w1 = (pc.w > pc.z ? pc.w - 1 : pc.z) >> wsh;
+      gwin = w0 == w1 ? (int)w0 : -1;
     }
     if (!direct) {
 #pragma unroll
@@ -1157,31 +1237,56 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
 #pragma unroll
     for (int r = 0; r < kLocColPerThread; ++r) {
       if ((uint32_t)r >= nmine) continue;
+      uint32_t fan = 0, pk = 0;  // this destination's totals if this entry reports it
       if (stc & (1u << r)) {  // single-link destination (fan-in 1 folded in at the end)
-        a_cnt += 1;
-        a_pk = max(a_pk, vr[r]);
+        fan = 1;
+        pk = vr[r];
       } else if (stc & (256u << r)) {
-        a_cnt += 1;
         if (direct) {
           const uint32_t f = dfan[hh[r]];
-          a_fanin = max(a_fanin, f >> 20);
-          a_pk = max(a_pk, (f & 0xFFFFFu) + dpk[hh[r]]);
+          fan = f >> 20;
+          pk = (f & 0xFFFFFu) + dpk[hh[r]];
           dfan[hh[r]] = 0;
           dpk[hh[r]] = 0;
         } else {
-          a_fanin = max(a_fanin, s.nfan[hh[r]]);
-          a_pk = max(a_pk, s.npk[hh[r]]);
+          fan = s.nfan[hh[r]];
+          pk = s.npk[hh[r]];
           s.key[hh[r]] = 0;
           s.nfan[hh[r]] = 0;
           s.npk[hh[r]] = 0;
         }
       }
+      if (fan) {
+        if (WIN && gwin < 0) {  // a group at a window edge: straight to the entry's window
+          unsigned long long* sw = stats + (size_t)S_COUNT * (kr[r] >> wdb);
+          atomicAdd(sw + S_DSTS, 1ull);
+          atomicMax(sw + S_MAXFANIN, (unsigned long long)fan);
+          atomicMax(sw + S_MAXDSTPK, (unsigned long long)pk);
+        } else {
+          a_cnt += 1;
+          a_fanin = max(a_fanin, fan);
+          a_pk = max(a_pk, pk);
+        }
+      }
       if (!direct) s.bm[h16u(kr[r]) >> 4] = 0;
     }
     if (tid == 0 && s.spf) {
-      a_cnt += 1;
-      a_fanin = max(a_fanin, s.spf);
-      a_pk = max(a_pk, s.spp);
+      if (WIN && gwin < 0) {
+        unsigned long long* sw = stats + (size_t)S_COUNT * (0xFFFFFFFFu >> wdb);
+        atomicAdd(sw + S_DSTS, 1ull);
+        atomicMax(sw + S_MAXFANIN, (unsigned long long)s.spf);
+        atomicMax(sw + S_MAXDSTPK, (unsigned long long)s.spp);
+      } else {
+        a_cnt += 1;
+        a_fanin = max(a_fanin, s.spf);
+        a_pk = max(a_pk, s.spp);
+      }
+    }
+    if constexpr (WIN) {
+      if (gwin >= 0) {
+        flush_cols(stats + (size_t)S_COUNT * gwin, a_cnt, a_fanin, a_pk);
+        a_cnt = a_fanin = a_pk = 0;
+      }
     }
     __syncthreads();
     if (tid == 0) s.spf = s.spp = 0;
@@ -1192,19 +1297,7 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
     }
     nmine = nnext;
   }
-  if (a_cnt) a_fanin = max(a_fanin, 1u);
-  unsigned long long w_cnt = a_cnt;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    w_cnt += __shfl_xor_sync(FULL, w_cnt, o);
-    a_fanin = max(a_fanin, __shfl_xor_sync(FULL, a_fanin, o));
-    a_pk = max(a_pk, __shfl_xor_sync(FULL, a_pk, o));
-  }
-  if (lane == 0) {
-    if (w_cnt) atomicAdd(stats + S_DSTS, w_cnt);
-    if (a_fanin) atomicMax(stats + S_MAXFANIN, (unsigned long long)a_fanin);
-    if (a_pk) atomicMax(stats + S_MAXDSTPK, (unsigned long long)a_pk);
-  }
+  if (!WIN) flush_cols(stats, a_cnt, a_fanin, a_pk);
 }
 
 }  // namespace nmx
@@ -1368,5 +1461,109 @@ struct ColConcatPart {
     out_cv[pos] = v;
   }
 };
+
+
+// ---------------------------------------------------------------------------
+// Sorted keys on the MSD machinery (COO builds: matrix_from_pairs / build_matrices,
+// traffic.py:197-242, and anything else that needs the fully sorted packet keys):
+// after the dense partition every light bucket is a contiguous range and buckets are
+// in key order, so sorting each group of whole buckets in place sorts the array.
+// Per group (<= kLocMaxKeys keys): striped load into shared memory, 8 keys per thread
+// sorted in registers (19-comparator network), then merge-path rounds through shared
+// memory (runs 8 -> 16 -> ... -> P * 8, P = active threads, a power of two), and a
+// striped store back. Padding slots hold ~0 and sort last.
+// ---------------------------------------------------------------------------
+constexpr int kSortThreads = 512;
+constexpr int kSortIPT = 8;
+constexpr int kSortCap = kSortThreads * kSortIPT;  // 4096 >= kLocMaxKeys
+static_assert(kSortCap >= kLocMaxKeys, "a row group must fit one sort tile");
+struct SortSmem {
+  uint64_t k[kSortCap + kSortCap / 16];  // pad16 layout
+  uint4 plan;
+};
+
+__device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {
+  const uint64_t x = a < b ? a : b, y = a < b ? b : a;
+  a = x;
+  b = y;
+}
+__device__ __forceinline__ void sort8(uint64_t* r) {
+  cmpx(r[0], r[1]); cmpx(r[2], r[3]); cmpx(r[4], r[5]); cmpx(r[6], r[7]);
+  cmpx(r[0], r[2]); cmpx(r[1], r[3]); cmpx(r[4], r[6]); cmpx(r[5], r[7]);
+  cmpx(r[1], r[2]); cmpx(r[5], r[6]);
+  cmpx(r[0], r[4]); cmpx(r[1], r[5]); cmpx(r[2], r[6]); cmpx(r[3], r[7]);
+  cmpx(r[2], r[4]); cmpx(r[3], r[5]);
+  cmpx(r[1], r[2]); cmpx(r[3], r[4]); cmpx(r[5], r[6]);
+}
+
+__global__ void __launch_bounds__(kSortThreads, 2)
+    local_sort_kernel(uint64_t* __restrict__ keys, const uint4* __restrict__ plan, const uint32_t* __restrict__ ngp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+  const uint32_t ngroups = *ngp;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    if (tid == 0) S.plan = plan[g];
+    __syncthreads();
+    const uint4 p = S.plan;
+    const uint32_t cnt = p.y - p.x;
+    const uint32_t T = (cnt + kSortIPT - 1) / kSortIPT;
+    uint32_t P = 1;
+    while (P < T) P <<= 1;
+    const uint32_t N = P * kSortIPT;
+    for (uint32_t i = tid; i < N; i += kSortThreads) S.k[pad16(i)] = i < cnt ? keys[p.x + i] : ~0ull;
+    __syncthreads();
+    const bool act = tid < P;
+    uint64_t r[kSortIPT];
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < kSortIPT; ++j) r[j] = S.k[pad16(tid * kSortIPT + j)];
+      sort8(r);
+    }
+    for (uint32_t L = kSortIPT; L < N; L <<= 1) {
+      __syncthreads();  // every read of the previous round is done
+      if (act) {
+#pragma unroll
+        for (int j = 0; j < kSortIPT; ++j) S.k[pad16(tid * kSortIPT + j)] = r[j];
+      }
+      __syncthreads();
+      if (act) {
+        const uint32_t pos = tid * kSortIPT;
+        const uint32_t a0 = pos & ~(2 * L - 1), b0 = a0 + L;  // runs A = [a0, a0 + L), B = [b0, b0 + L)
+        const uint32_t d = pos - a0;                            // this thread's diagonal
+        uint32_t lo = d > L ? d - L : 0, hi = d < L ? d : L;    // first i with A[i] > B[d - 1 - i]
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (S.k[pad16(a0 + mid)] <= S.k[pad16(b0 + d - 1 - mid)])
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        uint32_t i = lo, j = d - lo;
+        uint64_t ka = i < L ? S.k[pad16(a0 + i)] : 0ull, kb = j < L ? S.k[pad16(b0 + j)] : 0ull;
+#pragma unroll
+        for (int q = 0; q < kSortIPT; ++q) {
+          const bool takeA = i < L && (j >= L || ka <= kb);
+          r[q] = takeA ? ka : kb;
+          if (takeA) {
+            ++i;
+            ka = i < L ? S.k[pad16(a0 + i)] : 0ull;
+          } else {
+            ++j;
+            kb = j < L ? S.k[pad16(b0 + j)] : 0ull;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < kSortIPT; ++j) S.k[pad16(tid * kSortIPT + j)] = r[j];
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < cnt; i += kSortThreads) keys[p.x + i] = S.k[pad16(i)];
+    __syncthreads();  // smem and plan are reused by the next group
+  }
+}
 
 }  // namespace nmx

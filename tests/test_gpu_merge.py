@@ -125,3 +125,37 @@ def test_wide_counts_merge_and_stats(coo, n):
     big = coo.coo_from_keys(keys[:1], np.array([(1 << 62) + 1], np.int64))
     with pytest.raises(Exception):
         coo.merge_add(big, big)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
+@pytest.mark.parametrize("lg,space", [(16, 1 << 32), (19, 1 << 20), (21, 1 << 32), (22, (1 << 28) + 5),
+                                      (23, 1 << 24)])
+def test_coo_sorted_on_msd_path(coo, kind, lg, space):
+    """Unique links + counts from the MSD partition and the per-group shared-memory
+    sort (power-law heavy buckets take the LSD sort) == the packed oracle, keys in
+    order; the same keys through nmx_coo_build (matrix_from_pairs' entry) with a
+    tight address space and through windows (build_matrices)."""
+    n = (1 << lg) + 777
+    s, d = _gen(kind, 41, 0, n, space)
+    v = np.random.default_rng(lg).random(n) > 0.05
+    m = coo.coo_from_packets(s, d, v)
+    keys, counts = m.download()
+    wk, wc = orc.coo_packed(s, d, v)
+    assert np.array_equal(keys, wk) and np.array_equal(counts, wc)
+    assert m.stats9() == orc.stats9_packed(s, d, v)
+    m.close()
+
+
+@pytest.mark.parametrize("space,window", [(1 << 20, 1 << 17), (1 << 16, 100_000), (1 << 24, 1 << 21)])
+def test_build_matrices_on_msd_path(space, window):
+    from paper_2510_14050_b200 import traffic as nm
+
+    n = (1 << 22) + 99
+    s, d = orc.gen_uniform(8, 0, n, space)
+    v = np.random.default_rng(3).random(n) > 0.1
+    st = nm.PacketStream(src=s.astype(np.int64), dst=d.astype(np.int64), valid=v, address_space=space)
+    ours = nm.build_matrices(st, window)
+    ref = orc.ref_build_matrices(st.src, st.dst, st.valid, window, space)
+    assert len(ours) == len(ref)
+    for a, (rp, ci, va) in zip(ours, ref):
+        assert np.array_equal(a.row_ptr, rp) and np.array_equal(a.col_idx, ci) and np.array_equal(a.values, va)

@@ -161,3 +161,30 @@ def test_out_of_range_address_rejected_on_device(n):
     # the context is still usable afterwards
     td[n // 2] = 0
     assert _lib.stats9(ts, td, None, space)[0] == n
+
+
+@pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
+@pytest.mark.parametrize("lg,space,window", [(16, 1 << 20, 4096), (20, 1 << 24, 1 << 14), (21, 1 << 18, 50_000),
+                                             (22, 1 << 26, 1 << 16), (22, (1 << 26) - 3, 65_537),
+                                             (23, 1 << 24, 1 << 17)])
+def test_windows_msd_path(lib, kind, lg, space, window):
+    """Per-window statistics through the windowed MSD path (window id above the
+    address bits, b + wb <= 32; power-law inputs with heavy buckets fall back to the
+    LSD path) against the packed oracle, window by window, with invalid packets and a
+    partial last window."""
+    gen = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
+    n = (1 << lg) + 1234
+    s, d = gen(23, 0, n, space)
+    v = np.random.default_rng(lg).random(n) > 0.1
+    s[-5:] = space - 1  # the all-ones source / destination of the last window
+    d[-3:] = space - 1
+    per, _ = orc.stats9_windows_packed(s, d, v, window)
+    assert lib.window_stats9(s, d, v, space, window).tolist() == [list(r) for r in per]
+    # device-resident columns, no validity mask
+    ds, dd = lib.DeviceArray(n), lib.DeviceArray(n)
+    ds.upload(s)
+    dd.upload(d)
+    per2, _ = orc.stats9_windows_packed(s, d, None, window)
+    assert lib.window_stats9(ds, dd, None, space, window).tolist() == [list(r) for r in per2]
+    ds.close()
+    dd.close()

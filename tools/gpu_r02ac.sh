@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_merge.py tests/test_gpu_dropin.py tests/test_gpu_parity.py tests/test_gpu_anonymize.py tests/test_gpu_cli.py -x -q -m gpu 2>&1 | tail -15 > gpurun_out/ac_pytest.txt
+timeout 300 python tools/time_windows.py > gpurun_out/ac_windows.txt 2>&1
+timeout 300 python tools/quick_bench.py 30 > gpurun_out/ac_quick.txt 2>&1
