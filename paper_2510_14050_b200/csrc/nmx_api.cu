@@ -1350,7 +1350,7 @@ bool sort_rows_msd(nmx_ctx* c, const PacketSrc& ps, int kb, uint64_t* m_out, uin
   if (m) {
     const uint32_t* ngp = seg_plan_groups_dev(c, 1u << D, n, kLocChunk, 0);
     set_smem(local_sort_kernel, sizeof(SortSmem));
-    local_sort_kernel<<<c->sms * 2, kSortThreads, sizeof(SortSmem), c->st>>>(keys, c->mplan.as<uint4>(), ngp);
+    local_sort_kernel<<<c->sms * 2, kSortThreads, sizeof(SortSmem), c->st>>>(keys, c->mplan.as<uint4>(), ngp, kb - D);
     CK_LAUNCH();
     ++c->launches;
   }

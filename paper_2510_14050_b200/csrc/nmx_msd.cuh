@@ -1477,8 +1477,15 @@ constexpr int kSortThreads = 512;
 constexpr int kSortIPT = 8;
 constexpr int kSortCap = kSortThreads * kSortIPT;  // 4096 >= kLocMaxKeys
 static_assert(kSortCap >= kLocMaxKeys, "a row group must fit one sort tile");
+constexpr int kSortBins = 2048;          // counting-sort bins of a group's key range
+constexpr uint32_t kSortSmallBin = 32;   // groups with a larger bin take the merge rounds
+constexpr int kSortKPT = (kLocMaxKeys + kSortThreads - 1) / kSortThreads;  // keys per thread (striped)
 struct SortSmem {
   uint64_t k[kSortCap + kSortCap / 16];  // pad16 layout
+  uint32_t cnt[kSortBins];               // bin counts, then bin cursors (-> bin ends)
+  uint32_t st0[kSortBins];               // bin starts
+  uint32_t wt[kSortThreads / 32 + 1];
+  uint32_t maxbin;
   uint4 plan;
 };
 
@@ -1496,17 +1503,92 @@ __device__ __forceinline__ void sort8(uint64_t* r) {
   cmpx(r[1], r[2]); cmpx(r[3], r[4]); cmpx(r[5], r[6]);
 }
 
+// Fast path: the group's keys lie in [b0 << rb, b1 << rb) (its buckets); a counting sort
+// by the monotone bin (key - lo) >> s into 2048 bins, then each bin (a few keys when the
+// keys spread) insertion-sorted by one thread. A group with a bin above kSortSmallBin keys
+// (clustered keys) takes the merge rounds below instead.
 __global__ void __launch_bounds__(kSortThreads, 2)
-    local_sort_kernel(uint64_t* __restrict__ keys, const uint4* __restrict__ plan, const uint32_t* __restrict__ ngp) {
+    local_sort_kernel(uint64_t* __restrict__ keys, const uint4* __restrict__ plan, const uint32_t* __restrict__ ngp,
+                      int rb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
   const uint32_t ngroups = *ngp;
   const uint32_t tid = threadIdx.x;
   for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    if (tid == 0) S.plan = plan[g];
+    if (tid == 0) {
+      S.plan = plan[g];
+      S.maxbin = 0;
+    }
+    for (int i = tid; i < kSortBins; i += kSortThreads) S.cnt[i] = 0;
     __syncthreads();
     const uint4 p = S.plan;
     const uint32_t cnt = p.y - p.x;
+    if (!cnt) {  // uniform
+      __syncthreads();  // every thread has read the plan before it is overwritten
+      continue;
+    }
+    {
+      const uint64_t lo = (uint64_t)p.z << rb, range = (uint64_t)(p.w - p.z) << rb;
+      const int sh = max(0, 64 - __clzll((long long)(range - 1)) - 11);  // (range - 1) >> sh < 2048
+      uint64_t kr[kSortKPT];
+      uint32_t bn[kSortKPT];
+#pragma unroll
+      for (int r = 0; r < kSortKPT; ++r) {
+        const uint32_t j = tid + r * kSortThreads;
+        if (j < cnt) {
+          kr[r] = keys[p.x + j];
+          bn[r] = (uint32_t)((kr[r] - lo) >> sh);
+          atomicAdd(&S.cnt[bn[r]], 1u);
+        }
+      }
+      __syncthreads();
+      constexpr int PER = kSortBins / kSortThreads;  // 4 bins per thread
+      uint32_t c4[PER], sum = 0, mx = 0;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        c4[q] = S.cnt[tid * PER + q];
+        sum += c4[q];
+        mx = max(mx, c4[q]);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+      if ((tid & 31) == 0) atomicMax(&S.maxbin, mx);
+      uint32_t total;
+      uint32_t ex = block_excl_scan_n<kSortThreads>(sum, S.wt, &total);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        S.st0[tid * PER + q] = ex;
+        S.cnt[tid * PER + q] = ex;
+        ex += c4[q];
+      }
+      __syncthreads();
+      if (S.maxbin <= kSortSmallBin) {
+#pragma unroll
+        for (int r = 0; r < kSortKPT; ++r) {
+          const uint32_t j = tid + r * kSortThreads;
+          if (j < cnt) S.k[pad16(atomicAdd(&S.cnt[bn[r]], 1u))] = kr[r];
+        }
+        __syncthreads();
+        for (int bq = tid; bq < kSortBins; bq += kSortThreads) {
+          const uint32_t b0 = S.st0[bq], b1 = S.cnt[bq];
+          for (uint32_t i = b0 + 1; i < b1; ++i) {
+            const uint64_t x = S.k[pad16(i)];
+            uint32_t j = i;
+            while (j > b0) {
+              const uint64_t y = S.k[pad16(j - 1)];
+              if (y <= x) break;
+              S.k[pad16(j)] = y;
+              --j;
+            }
+            S.k[pad16(j)] = x;
+          }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < cnt; i += kSortThreads) keys[p.x + i] = S.k[pad16(i)];
+        __syncthreads();
+        continue;
+      }
+    }
     const uint32_t T = (cnt + kSortIPT - 1) / kSortIPT;
     uint32_t P = 1;
     while (P < T) P <<= 1;
