@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <chrono>
 #include <mutex>
 #include <new>
 #include <stdexcept>
@@ -2115,10 +2116,14 @@ int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wm
   if (P > kMaxParts) return fail(NMX_EINVAL, "too many packets for one device");
   const uint64_t cap = cap_of(P);
   // the part arenas come first: workspace grown by earlier (larger single-pass) calls is
-  // dropped and regrown at part size
+  // dropped and regrown at part size; part-sized workspace (an earlier out-of-core call's)
+  // is kept -- reallocating tens of GB per call cost ~0.5 s
+  const size_t part_ws = (size_t)cap * 8 + (size_t)cap / 8 * 8 + (512ull << 20);
   for (DevBuf* d : {&c->keysA, &c->keysB, &c->keysC, &c->keysD, &c->colL_dst, &c->ckA, &c->ckB, &c->cvA, &c->cvB,
-                    &c->cgk, &c->cgk2, &c->in_src, &c->in_dst, &c->in_valid, &c->lightK, &c->pcolD, &c->pcolC})
-    if (d->cap > (64ull << 20)) d->release();
+                    &c->cgk, &c->cgk2, &c->in_src, &c->in_dst, &c->in_valid, &c->lightK})
+    if (d->cap > part_ws) d->release();
+  for (DevBuf* d : {&c->pcolD, &c->pcolC})
+    if (d->cap > (size_t)P * cap * 4 + (512ull << 20)) d->release();
   c->parS.grow((size_t)P * cap * 4);
   c->parD.grow((size_t)P * cap * 4);
   if (range) {
@@ -2159,6 +2164,16 @@ int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wm
     }
     CK(cudaEventRecord(c->evc[sl], c->st2));
   };
+  // NMX_DEBUG: wall-clock phase times (each phase end synchronizes the stream)
+  const bool dbg = getenv("NMX_DEBUG") != nullptr;
+  auto t_phase = std::chrono::steady_clock::now();
+  auto phase_done = [&](const char* what) {
+    if (!dbg) return;
+    CK(cudaStreamSynchronize(c->st));
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "stream_parts %s: %.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t_phase).count());
+    t_phase = t;
+  };
   // 1. windows -> source-part arenas (the copy of window k+1 overlaps window k's split)
   uint64_t fill[kMaxParts] = {0}, base[kMaxParts], left[kMaxParts], cnt[kMaxParts];
   if (hw.nwin) enqueue_copy(0);
@@ -2187,6 +2202,7 @@ int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wm
   }
   if (range)
     if (int r = check_maxaddr(c, space)) return r;
+  phase_done("1 copies + owner(src) split");
   // 2. rows per source part; column entries -> destination-part arenas
   c->pcolD.grow((size_t)P * cap * 4);
   c->pcolC.grow((size_t)P * cap * 4);
@@ -2209,6 +2225,7 @@ int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wm
     for (int q = 0; q < P; ++q) cfill[q] += cnt[q];
     fold(row9, 0, 6);
   }
+  phase_done("2 rows per source part");
   // 3. columns per destination part
   for (int q = 0; q < P; ++q) {
     if (!cfill[q]) continue;
@@ -2218,6 +2235,7 @@ int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wm
       return r;
     fold(col9, 6, 9);
   }
+  phase_done("3 columns per destination part");
   std::copy(tot, tot + S_COUNT, out);
   c->last_nstage = 0;
   return NMX_OK;
