@@ -1520,8 +1520,9 @@ void partition_items(nmx_ctx* c, const Item& it, uint64_t n, int nparts, uint64_
   auto* d_counts = c->part.as<unsigned long long>();
   auto* d_cursor = d_counts + kMaxParts;
   CK(cudaMemsetAsync(d_counts, 0, kMaxParts * sizeof(unsigned long long), c->st));
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 4095) / 4096, (uint64_t)c->sms * 4));
-  part_count_kernel<Item><<<grid, 256, 0, c->st>>>(it, n, nparts, d_counts);
+  const uint64_t tiles = (n + kPartTile - 1) / kPartTile;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)c->sms * 8));
+  part_tile_count_kernel<Item><<<grid, 256, 0, c->st>>>(it, n, nparts, d_counts);
   CK_LAUNCH();
   unsigned long long hc[kMaxParts];
   CK(cudaMemcpyAsync(hc, d_counts, sizeof(hc), cudaMemcpyDeviceToHost, c->st));
@@ -1536,8 +1537,7 @@ void partition_items(nmx_ctx* c, const Item& it, uint64_t n, int nparts, uint64_
     counts_host[p] = hc[p];
   }
   CK(cudaMemcpyAsync(d_cursor, base, sizeof(unsigned long long) * nparts, cudaMemcpyHostToDevice, c->st));
-  const uint64_t chunk = (n + grid - 1) / grid;
-  part_scatter_kernel<Item><<<grid, 256, 0, c->st>>>(it, n, chunk, nparts, d_cursor);
+  part_tile_scatter_kernel<Item><<<(unsigned)std::max<uint64_t>(tiles, 1), 256, 0, c->st>>>(it, n, nparts, d_cursor);
   CK_LAUNCH();
   c->launches += 2;
   CK(cudaStreamSynchronize(c->st));
@@ -2224,6 +2224,11 @@ int stream_parts_impl(nmx_ctx* c, const HostWindows& hw, uint64_t N, uint64_t wm
       return r;
     for (int q = 0; q < P; ++q) cfill[q] += cnt[q];
     fold(row9, 0, 6);
+    if (dbg) {
+      fprintf(stderr, "  part %d: %llu packets, device %.2f ms, stages", p, (unsigned long long)fill[p], c->last_total_ms);
+      for (int i = 0; i < c->last_nstage; ++i) fprintf(stderr, " %.2f", c->last_stage_ms[i]);
+      fprintf(stderr, "\n");
+    }
   }
   phase_done("2 rows per source part");
   // 3. columns per destination part

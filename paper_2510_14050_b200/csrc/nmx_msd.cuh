@@ -1450,15 +1450,10 @@ struct ColConcatPart {
   ColConcatSrc s;
   uint32_t* out_ck;
   uint32_t* out_cv;
-  __device__ __forceinline__ bool key(uint64_t i, uint32_t& k) const {
-    uint32_t v;
-    return s.load(i, k, v);
-  }
-  __device__ __forceinline__ void store(uint64_t i, uint64_t pos) const {
-    uint32_t k, v;
-    s.load(i, k, v);
-    out_ck[pos] = k;
-    out_cv[pos] = v;
+  __device__ __forceinline__ bool get(uint64_t i, uint32_t& hi, uint32_t& lo) const { return s.load(i, hi, lo); }
+  __device__ __forceinline__ void put(uint64_t pos, uint32_t hi, uint32_t lo) const {
+    out_ck[pos] = hi;
+    out_cv[pos] = lo;
   }
 };
 
