@@ -8,6 +8,7 @@
 #include <condition_variable>
 #include <functional>
 #include <thread>
+#include <immintrin.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1941,6 +1942,109 @@ int stats_host_batches_impl(nmx_ctx* c, uint64_t nb, const uint32_t* const* src,
   return rc;
 }
 
+// int64 -> u32 narrowing of the reference's columns into pinned slots: returns whether
+// an address lies outside [0, space). With AVX2, 8 packets per step and non-temporal
+// 16-byte stores (the pinned slots are only read back by the DMA engine, so no
+// read-for-ownership of their lines).
+__attribute__((target("avx2"))) static bool narrow_u32_avx2(const int64_t* s, const int64_t* d, uint32_t* os,
+                                                           uint32_t* od, uint64_t n, uint64_t space) {
+  uint64_t i = 0, orr = 0;
+  // scalar head until the outputs are 16-byte aligned
+  for (; i < n && (((uintptr_t)(os + i) | (uintptr_t)(od + i)) & 15); ++i) {
+    const uint64_t x = (uint64_t)s[i], y = (uint64_t)d[i];
+    orr |= (x >= space) | (y >= space);
+    os[i] = (uint32_t)x;
+    od[i] = (uint32_t)y;
+  }
+  const __m256i lim = _mm256_set1_epi64x((long long)(space - 1) ^ (long long)0x8000000000000000ull);
+  const __m256i sgn = _mm256_set1_epi64x((long long)0x8000000000000000ull);
+  const __m256i pick = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+  __m256i bad = _mm256_setzero_si256();
+  for (; i + 4 <= n; i += 4) {
+    const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+    const __m256i y = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(d + i));
+    // unsigned x > space - 1 via the sign-flipped signed compare
+    bad = _mm256_or_si256(bad, _mm256_cmpgt_epi64(_mm256_xor_si256(x, sgn), lim));
+    bad = _mm256_or_si256(bad, _mm256_cmpgt_epi64(_mm256_xor_si256(y, sgn), lim));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(os + i),
+                     _mm256_castsi256_si128(_mm256_permutevar8x32_epi32(x, pick)));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(od + i),
+                     _mm256_castsi256_si128(_mm256_permutevar8x32_epi32(y, pick)));
+  }
+  orr |= !_mm256_testz_si256(bad, bad);
+  for (; i < n; ++i) {
+    const uint64_t x = (uint64_t)s[i], y = (uint64_t)d[i];
+    orr |= (x >= space) | (y >= space);
+    os[i] = (uint32_t)x;
+    od[i] = (uint32_t)y;
+  }
+  _mm_sfence();
+  return orr != 0;
+}
+static bool narrow_u32(const int64_t* s, const int64_t* d, uint32_t* os, uint32_t* od, uint64_t n, uint64_t space) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) return narrow_u32_avx2(s, d, os, od, n, space);
+  uint64_t orr = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t x = (uint64_t)s[i], y = (uint64_t)d[i];
+    orr |= (x >= space) | (y >= space);
+    os[i] = (uint32_t)x;
+    od[i] = (uint32_t)y;
+  }
+  return orr != 0;
+}
+
+// T host threads (the caller is thread 0) reused across jobs: run(f) calls f(t, T) on
+// every thread and returns when all are done
+struct NarrowPool {
+  std::vector<std::thread> th;
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::function<void(unsigned, unsigned)> job;
+  uint64_t gen = 0;
+  unsigned pending = 0, nt;
+  bool stop = false;
+  explicit NarrowPool(unsigned n) : nt(std::max(1u, n)) {
+    for (unsigned t = 1; t < nt; ++t)
+      th.emplace_back([this, t] {
+        uint64_t seen = 0;
+        for (;;) {
+          std::function<void(unsigned, unsigned)> f;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [&] { return stop || gen != seen; });
+            if (stop) return;
+            seen = gen;
+            f = job;
+          }
+          f(t, nt);
+          std::lock_guard<std::mutex> lk(mu);
+          if (--pending == 0) done_cv.notify_one();
+        }
+      });
+  }
+  void run(const std::function<void(unsigned, unsigned)>& f) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      job = f;
+      pending = nt - 1;
+      ++gen;
+    }
+    cv.notify_all();
+    f(0, nt);
+    std::unique_lock<std::mutex> lk(mu);
+    done_cv.wait(lk, [&] { return pending == 0; });
+  }
+  ~NarrowPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& x : th) x.join();
+  }
+};
+
 // The reference's own columns (PacketStream: int64 src / dst, bool valid): narrowed to
 // u32 on the host by a few threads per window, into two pinned slots that alternate,
 // while the previous window is copied and partitioned -- the drop-in analytics.stats9
@@ -1981,6 +2085,10 @@ int stats_host_i64_impl(nmx_ctx* c, const int64_t* src, const int64_t* dst, cons
   }
   const unsigned hw_threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   std::atomic<bool> bad{false};
+  // one pool for the whole call (a window is 2^24 packets: spawning threads per window
+  // cost more than the narrowing of a small one)
+  const unsigned T = (unsigned)std::min<uint64_t>(hw_threads, (W + 65535) / 65536);
+  NarrowPool pool(T);
   HostWindows hw;
   hw.src = sp.data();
   hw.dst = dp.data();
@@ -1989,29 +2097,11 @@ int stats_host_i64_impl(nmx_ctx* c, const int64_t* src, const int64_t* dst, cons
   hw.nwin = nwin;
   hw.fill = [&](uint64_t k, int sl) {
     const uint64_t lo = k * W, L = lens[k];
-    const unsigned T = (unsigned)std::min<uint64_t>(hw_threads, (L + 65535) / 65536);
-    auto work = [&](unsigned t) {
-      const uint64_t a = L * t / T, z = L * (t + 1) / T;
-      uint64_t orr = 0;  // any address outside [0, space): its bits at or above b (or the sign)
-      const int64_t* s = src + lo;
-      const int64_t* d = dst + lo;
-      for (uint64_t i = a; i < z; ++i) {
-        const uint64_t x = (uint64_t)s[i], y = (uint64_t)d[i];
-        orr |= (x >= space) | (y >= space);
-        ps[sl][i] = (uint32_t)x;
-        pd[sl][i] = (uint32_t)y;
-      }
+    pool.run([&](unsigned t, unsigned nt) {
+      const uint64_t a = (L * t / nt) & ~7ull, z = t + 1 == nt ? L : (L * (t + 1) / nt) & ~7ull;
+      if (narrow_u32(src + lo + a, dst + lo + a, ps[sl] + a, pd[sl] + a, z - a, space)) bad = true;
       if (valid) memcpy(pv[sl] + a, valid + lo + a, z - a);
-      if (orr) bad = true;
-    };
-    if (T <= 1) {
-      work(0);
-    } else {
-      std::vector<std::thread> th;
-      for (unsigned t = 1; t < T; ++t) th.emplace_back(work, t);
-      work(0);
-      for (auto& x : th) x.join();
-    }
+    });
   };
   const int rc = stream_impl(c, hw, space, out);
   if (bad) return fail(NMX_EINVAL, "addresses must lie in [0, address_space)");
