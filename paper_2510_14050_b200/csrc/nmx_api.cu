@@ -175,6 +175,7 @@ struct nmx_ctx {
   struct CallGraph {
     const void *s, *d, *v;
     uint64_t n, space;
+    uint64_t window;  // 0: summed matrix; else the per-window statistics of windows of this size
     cudaGraphExec_t exec;
     uint64_t gen;  // g_buf_gen when recorded
     int launches;  // kernels in the graph
@@ -1403,7 +1404,8 @@ bool graph_eligible(uint64_t n) {
   return !off && n >= 1 && n <= kGraphMaxN;
 }
 
-nmx_ctx::CallGraph* graph_find(nmx_ctx* c, const void* s, const void* d, const void* v, uint64_t n, uint64_t space) {
+nmx_ctx::CallGraph* graph_find(nmx_ctx* c, const void* s, const void* d, const void* v, uint64_t n, uint64_t space,
+                               uint64_t window = 0) {
   const uint64_t gen = g_buf_gen.load();
   for (size_t i = 0; i < c->graphs.size();) {  // a buffer moved since recording: stale
     if (c->graphs[i].gen != gen) {
@@ -1414,7 +1416,7 @@ nmx_ctx::CallGraph* graph_find(nmx_ctx* c, const void* s, const void* d, const v
     }
   }
   for (auto& g : c->graphs)
-    if (g.s == s && g.d == d && g.v == v && g.n == n && g.space == space) return &g;
+    if (g.s == s && g.d == d && g.v == v && g.n == n && g.space == space && g.window == window) return &g;
   return nullptr;
 }
 
@@ -1445,8 +1447,11 @@ int graph_replay(nmx_ctx* c, nmx_ctx::CallGraph* g, uint64_t space) {
 }
 
 // record the call's launch sequence (after an ordinary call sized every buffer)
+bool run_pipeline_msd_windows(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid,
+                              uint64_t n, int b, uint64_t window_size, uint64_t W);
+// window > 0: the windowed MSD pipeline (per-window statistics, W windows)
 void graph_capture(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, const uint8_t* d_valid, uint64_t n,
-                   int b, int D, uint64_t space) {
+                   int b, int D, uint64_t space, uint64_t window = 0) {
   // every buffer the recording touches at its recorded size (the ordinary call sized
   // them for its own, possibly smaller, light totals)
   c->cgk.grow(n * 8);
@@ -1463,7 +1468,11 @@ void graph_capture(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, con
       CK(cudaMemcpyAsync(c->scr() + kScrMaxAddr, c->rmax.p, 4, cudaMemcpyDeviceToHost, c->st));
     }
     c->launches = space < (1ull << 32) ? 1 : 0;
-    run_pipeline_msd(c, d_src, d_dst, d_valid, n, b, D);  // stage_begin resets the count
+    if (window) {
+      if (!run_pipeline_msd_windows(c, d_src, d_dst, d_valid, n, b, window, (n + window - 1) / window)) ok = false;
+    } else {
+      run_pipeline_msd(c, d_src, d_dst, d_valid, n, b, D);  // stage_begin resets the count
+    }
     launched = c->launches + (space < (1ull << 32) ? 1 : 0);
   } catch (...) {
     ok = false;
@@ -1487,7 +1496,7 @@ void graph_capture(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, con
     cudaGraphExecDestroy(c->graphs.front().exec);
     c->graphs.erase(c->graphs.begin());
   }
-  c->graphs.push_back({d_src, d_dst, d_valid, n, space, exec, g_buf_gen.load(), launched});
+  c->graphs.push_back({d_src, d_dst, d_valid, n, space, window, exec, g_buf_gen.load(), launched});
 }
 
 // The whole pipeline over packet columns already on the device. Writes W*9
@@ -1617,6 +1626,21 @@ int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
       }
     }
   }
+  // small windowed calls on the MSD path (per-window statistics) replay a recorded graph too
+  const uint64_t Wg = whole ? 1 : (n + window_size - 1) / window_size;
+  const int wbg = Wg > 1 ? (int)ceil_log2(Wg) : 0;
+  const bool gw = !whole && graph_eligible(n) && b + wbg <= 32 && window_size >= kWinMsdMinWindow &&
+                  msd_bits(n, b + wbg) >= wbg + 4;
+  if (gw) {
+    if (nmx_ctx::CallGraph* g = graph_find(c, d_src, d_dst, d_valid, n, space, window_size)) {
+      const int r = graph_replay(c, g, space);
+      if (r < 0) return r;
+      if (r == 1) {
+        copy_out9(c->h_stats, out, Wg);
+        return NMX_OK;
+      }
+    }
+  }
   if (int r = check_addresses(c, d_src, d_dst, n, space)) return r;
   if (whole) {
     run_pipeline(c, d_src, d_dst, d_valid, n, b, 0, 1);
@@ -1630,6 +1654,8 @@ int stats_device_impl(nmx_ctx* c, const uint32_t* d_src, const uint32_t* d_dst, 
   if (2 * b + wb <= 64) {
     run_pipeline(c, d_src, d_dst, d_valid, n, b, window_size, W);
     copy_out9(c->h_stats, out, W);
+    if (gw && !c->had_heavy && !graph_find(c, d_src, d_dst, d_valid, n, space, window_size))
+      graph_capture(c, d_src, d_dst, d_valid, n, b, 0, space, window_size);
     return NMX_OK;
   }
   // keys too wide to carry the window id: one window per pipeline run

@@ -97,3 +97,30 @@ def test_valid_flags_and_power_law_replays():
     want = orc.stats9_packed(s, d, v.astype(bool))
     for _ in range(3):
         assert _lib.stats9(ds, dd, dv, 1 << 32) == want
+
+
+@pytest.mark.parametrize("lg,space,window", [(20, 1 << 20, 1 << 14), (23, 1 << 24, 1 << 17), (22, 5000, 100_000)])
+def test_window_replays_equal_oracle(lg, space, window):
+    """Per-window statistics on the MSD path recorded as one graph: replays on the same
+    buffers with new contents, a replay meeting heavy buckets (power-law: rerun on the
+    LSD path), and a replay seeing an out-of-range address."""
+    from paper_2510_14050_b200 import _lib
+
+    n = (1 << lg) + 5
+    ctx = _lib.context(0)
+    ds, dd = _lib.DeviceArray(n), _lib.DeviceArray(n)
+    for seed, gen in ((3, orc.gen_uniform), (4, orc.gen_uniform), (5, orc.gen_powerlaw), (6, orc.gen_uniform)):
+        s, d = gen(seed, 0, n, space)
+        ds.upload(s)
+        dd.upload(d)
+        per, _ = orc.stats9_windows_packed(s, d, None, window)
+        want = [list(r) for r in per]
+        for _ in range(3):
+            assert _lib.window_stats9(ds, dd, None, space, window).tolist() == want
+    if gen is orc.gen_uniform and space < (1 << 32):
+        bad = d.copy()
+        bad[n // 3] = space
+        dd.upload(bad)
+        with pytest.raises(ValueError, match="address_space"):
+            _lib.window_stats9(ds, dd, None, space, window)
+    assert ctx is not None
