@@ -21,7 +21,10 @@
 namespace nmx {
 
 constexpr int kMgThreads = 256;
-constexpr int kMgIPT = 8;
+#ifndef NMX_MG_IPT
+#define NMX_MG_IPT 8
+#endif
+constexpr int kMgIPT = NMX_MG_IPT;  // positions per thread (A/B builds: -DNMX_MG_IPT=...)
 constexpr int kMgTile = kMgThreads * kMgIPT;
 
 // first i in [max(0, d - nb), min(d, na)] with a[i] > b[d - 1 - i] (ties: A first)
