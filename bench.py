@@ -783,6 +783,9 @@ def run_nmx(args) -> None:
         del stream
 
     parity = golden_parity(args.config, log2n, gen, stats)
+    windows = None
+    if world == 1 and args.config == "cfg2" and not args.log2n:
+        windows = cfg2_windows(ds, dd, space, args, local)
     side = None
     if world == 1 and args.config == "cfg3" and not args.log2n and not args.no_side:
         ds.close()
@@ -852,6 +855,7 @@ def run_nmx(args) -> None:
                                   if len(stage_ms) == 5 else "stages of the rank's last library call")},
         "e2e": e2e,
         "e2e_dropin": dropin,
+        "windows": windows,
         "other_configs": side,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
@@ -863,6 +867,40 @@ def run_nmx(args) -> None:
         dist.destroy_process_group()
     if parity.get("equal") is False:
         sys.exit(f"bench: stats9 {list(stats)} differ from the golden {parity['want']}")
+
+
+def cfg2_windows(ds, dd, space: int, args, local: int) -> dict:
+    """BASELINE config 2's second output: the per-window analyze_dataset reports of the
+    64 windows of 2^17 packets (nmx_window_stats9_device on the same device columns),
+    K calls between CUDA events, checked against the reference-made golden."""
+    import torch
+
+    from paper_2510_14050_b200 import _lib
+
+    window = 1 << 17
+    ctx = _lib.context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    for _ in range(args.warmup):
+        per = _lib.window_stats9(ds, dd, None, space, window, device=local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(local)
+    e0.record(stream)
+    for _ in range(args.steps):
+        per = _lib.window_stats9(ds, dd, None, space, window, device=local)
+    e1.record(stream)
+    torch.cuda.synchronize(local)
+    ms = e0.elapsed_time(e1) / args.steps
+    try:
+        want = json.loads((ROOT / "tests" / "golden" / "golden.json").read_text())["cases"]["cfg2"]["windows9"]
+        equal = per.tolist() == want
+    except (OSError, KeyError, ValueError):
+        equal = None
+    n = int(ds.n)
+    return {"workload": f"cfg2 per-window reports: {per.shape[0]} windows of 2^17 packets (build_matrices(s, 2^17) -> "
+                        "analyze_dataset, analytics.py:109-130), device-resident",
+            "value": n / (ms / 1e3), "unit": "packets/s", "ms_per_step": ms, "steps": args.steps,
+            "parity": {"golden": "tests/golden/golden.json cfg2 windows9 (the reference netmeter package's own output)",
+                       "equal": equal}}
 
 
 def side_config(name: str, args, local: int) -> dict:
