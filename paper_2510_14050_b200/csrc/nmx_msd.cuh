@@ -1475,14 +1475,26 @@ static_assert(kSortCap >= kLocMaxKeys, "a row group must fit one sort tile");
 constexpr int kSortBins = 2048;          // counting-sort bins of a group's key range
 constexpr uint32_t kSortSmallBin = 32;   // groups with a larger bin take the merge rounds
 constexpr int kSortKPT = (kLocMaxKeys + kSortThreads - 1) / kSortThreads;  // keys per thread (striped)
+constexpr int kSortRaw = kLocMaxKeys + 2;  // a group's keys plus 16-byte alignment slack
 struct SortSmem {
+  uint64_t raw[2][kSortRaw];             // TMA-loaded keys of the current / next group
   uint64_t k[kSortCap + kSortCap / 16];  // pad16 layout
   uint32_t cnt[kSortBins];               // bin counts, then bin cursors (-> bin ends)
   uint32_t st0[kSortBins];               // bin starts
   uint32_t wt[kSortThreads / 32 + 1];
   uint32_t maxbin;
-  uint4 plan;
+  uint64_t bar[2];                       // mbarriers of the two raw buffers
+  uint4 pl[2];                           // plans of the current / next group
 };
+static_assert(offsetof(SortSmem, raw) % 16 == 0 && (kSortRaw * 8) % 16 == 0, "bulk-copy destinations 16-byte aligned");
+
+// one thread: bulk-copy group p's keys (16-byte aligned cover of [p.x, p.y)) into raw[b]
+__device__ __forceinline__ void sort_group_load(SortSmem& S, const uint64_t* keys, const uint4& p, int b) {
+  if (p.y == p.x) return;
+  const uint64_t a = (8ull * p.x) & ~15ull, e = (8ull * p.y + 15) & ~15ull;
+  mbar_expect_tx(&S.bar[b], (uint32_t)(e - a));
+  bulk_g2s(S.raw[b], reinterpret_cast<const unsigned char*>(keys) + a, (uint32_t)(e - a), &S.bar[b]);
+}
 
 __device__ __forceinline__ void cmpx(uint64_t& a, uint64_t& b) {
   const uint64_t x = a < b ? a : b, y = a < b ? b : a;
@@ -1509,19 +1521,42 @@ __global__ void __launch_bounds__(kSortThreads, 2)
   SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
   const uint32_t ngroups = *ngp;
   const uint32_t tid = threadIdx.x;
-  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+  // the next group's keys arrive by TMA bulk copy (one thread, mbarrier completion)
+  // while the current group is sorted
+  if (tid == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    mbar_init_fence();
+    if (blockIdx.x < ngroups) {
+      S.pl[0] = plan[blockIdx.x];
+      sort_group_load(S, keys, S.pl[0], 0);
+    }
+  }
+  __syncthreads();
+  uint32_t phase = 0;  // bit b: parity of raw[b]'s next completion
+  uint32_t it = 0;
+  for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
+    const int b = it & 1;
+    const uint4 p = S.pl[b];
     if (tid == 0) {
-      S.plan = plan[g];
       S.maxbin = 0;
+      const uint32_t gn = g + gridDim.x;
+      if (gn < ngroups) {  // raw[b ^ 1] was last read before the previous group's final barrier
+        S.pl[b ^ 1] = plan[gn];
+        fence_proxy_async_smem();
+        sort_group_load(S, keys, S.pl[b ^ 1], b ^ 1);
+      }
     }
     for (int i = tid; i < kSortBins; i += kSortThreads) S.cnt[i] = 0;
-    __syncthreads();
-    const uint4 p = S.plan;
     const uint32_t cnt = p.y - p.x;
-    if (!cnt) {  // uniform
-      __syncthreads();  // every thread has read the plan before it is overwritten
+    if (!cnt) {  // uniform; nothing was loaded for it
+      __syncthreads();
       continue;
     }
+    mbar_wait(&S.bar[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const uint64_t* gk = S.raw[b] + (p.x & 1u);  // the group's keys in shared memory
+    __syncthreads();
     {
       const uint64_t lo = (uint64_t)p.z << rb, range = (uint64_t)(p.w - p.z) << rb;
       const int sh = max(0, 64 - __clzll((long long)(range - 1)) - 11);  // (range - 1) >> sh < 2048
@@ -1531,7 +1566,7 @@ __global__ void __launch_bounds__(kSortThreads, 2)
       for (int r = 0; r < kSortKPT; ++r) {
         const uint32_t j = tid + r * kSortThreads;
         if (j < cnt) {
-          kr[r] = keys[p.x + j];
+          kr[r] = gk[j];
           bn[r] = (uint32_t)((kr[r] - lo) >> sh);
           atomicAdd(&S.cnt[bn[r]], 1u);
         }
@@ -1588,7 +1623,7 @@ __global__ void __launch_bounds__(kSortThreads, 2)
     uint32_t P = 1;
     while (P < T) P <<= 1;
     const uint32_t N = P * kSortIPT;
-    for (uint32_t i = tid; i < N; i += kSortThreads) S.k[pad16(i)] = i < cnt ? keys[p.x + i] : ~0ull;
+    for (uint32_t i = tid; i < N; i += kSortThreads) S.k[pad16(i)] = i < cnt ? gk[i] : ~0ull;
     __syncthreads();
     const bool act = tid < P;
     uint64_t r[kSortIPT];
