@@ -154,6 +154,7 @@ struct nmx_ctx {
   cudaEvent_t evc[2] = {nullptr, nullptr}, evu[2] = {nullptr, nullptr}, evs = nullptr;
   // nmx_stats9_host_batches: two device input slots, copy-done / slot-free events
   DevBuf bat_s[2], bat_d[2], bat_v[2];
+  DevBuf mhist3;  // level-3 counts of msd_count23_kernel
   cudaEvent_t evbc[2] = {nullptr, nullptr}, evbu[2] = {nullptr, nullptr};
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
   unsigned long long* h_scr = nullptr;  // pinned scalars read back mid-pipeline (one round trip each)
@@ -617,6 +618,15 @@ void scan_counts(nmx_ctx* c, const uint32_t* cnt, uint32_t n, uint32_t* off, uin
   c->launches += 3;
 }
 
+// NMX_COUNT23=0 keeps two msd_count2 passes (A/B runs)
+bool count23_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("NMX_COUNT23");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 int msd_first_bits(int D) {
   const int L = (D + kMsdMaxLevelBits - 1) / kMsdMaxLevelBits;
   return D / L + (0 < D % L ? 1 : 0);
@@ -796,11 +806,31 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   uint32_t* in_v = voutA;
   KeyT* out_k = outB;
   uint32_t* out_v = voutB;
+  // three levels without the joint level-1/2 counts (the column partition): levels 2
+  // and 3 counted in one pass over the level-1 output (msd_count23_kernel)
+  const bool joint23 = !joint && !pre_m && !HAS_VAL && L == 3 && dl[1] + dl[2] <= kJointMaxBits && dl[2] >= 2 &&
+                       n >= (1ull << 27) && !c->capturing && count23_enabled();
+  if (joint23) {
+    c->mhist3.grow(((size_t)(1u << cum[2]) + 8) * 4);
+    CK(cudaMemsetAsync(c->mhist3.p, 0, (size_t)4 << cum[2], c->st));
+    auto k = msd_count23_kernel<KeyT>;
+    const int jbits = dl[1] + dl[2];
+    const size_t sm = (size_t)8 << jbits;
+    set_smem(k, sm);
+    constexpr uint64_t kPer = 1ull << 20;
+    k<<<(unsigned)((n + kPer - 1) / kPer), kJointCountThreads, sm, c->st>>>(outA, gcount, kPer, kb - cum[2], jbits,
+                                                                             c->mhist3.as<uint32_t>());
+    CK_LAUNCH();
+    hist_fold_kernel<<<(unsigned)std::max(1u, std::min(((1u << cum[1]) + 255) / 256, (uint32_t)c->sms * 4)), 256, 0,
+                       c->st>>>(c->mhist3.as<uint32_t>(), 1u << cum[1], dl[2], c->mhist2.as<uint32_t>());
+    CK_LAUNCH();
+    c->launches += 2;
+  }
   for (int l = 1; l < L; ++l) {
     const int shift = kb - cum[l], bshift = kb - cum[l - 1];
     const uint32_t nbl = 1u << cum[l];
-    uint32_t* h2 = c->mhist2.as<uint32_t>();
-    if (!(joint && l == 1)) {
+    uint32_t* h2 = joint23 && l == 2 ? c->mhist3.as<uint32_t>() : c->mhist2.as<uint32_t>();
+    if (!(joint && l == 1) && !joint23) {
       CK(cudaMemsetAsync(h2, 0, (size_t)nbl * 4, c->st));
       msd_count2_kernel<KeyT><<<(unsigned)tiles_of(n, kMsdTile * kCount2Tiles), kMsdThreads, 0, c->st>>>(
           in_k, gcount, shift, dl[l], bshift, h2);
@@ -2777,7 +2807,7 @@ void nmx_destroy(nmx_ctx* c) {
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red, &c->ws0, &c->ws1,
                     &c->wd0, &c->wd1, &c->wv0, &c->wv1, &c->wr0, &c->wr1, &c->bat_s[0], &c->bat_s[1], &c->bat_d[0],
-                    &c->bat_d[1], &c->bat_v[0], &c->bat_v[1]})
+                    &c->bat_d[1], &c->bat_v[0], &c->bat_v[1], &c->mhist3})
     b->release();
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->h_wide) cudaFreeHost(c->h_wide);

@@ -406,6 +406,69 @@ __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __r
   }
 }
 
+// Levels 2 and 3 counted in one pass over the level-1 output: each CTA takes a
+// contiguous range of `per_cta` items (at most two level-1 parents for large inputs)
+// and histograms the next jbits = d2 + d3 key bits per parent in shared memory;
+// hist3[top cum3 key bits] receives the counts (a third parent: per-item global
+// atomics). One read of the items instead of two msd_count2 passes.
+constexpr int kJointCountThreads = 1024;
+template <typename KeyT>
+__global__ void __launch_bounds__(kJointCountThreads) msd_count23_kernel(const KeyT* __restrict__ keys,
+                                                                        const unsigned long long* __restrict__ mp,
+                                                                        uint64_t per_cta, int shift3, int jbits,
+                                                                        uint32_t* __restrict__ hist3) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+  __shared__ uint64_t s_p0;
+  const uint64_t m = *mp;
+  const uint64_t lo = (uint64_t)blockIdx.x * per_cta;
+  if (lo >= m) return;
+  const uint64_t hi = m - lo < per_cta ? m : lo + per_cta;
+  const int nb = 2 << jbits;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < nb; i += kJointCountThreads) h[i] = 0;
+  if (tid == 0) s_p0 = ((uint64_t)keys[lo] >> shift3) >> jbits;
+  __syncthreads();
+  const uint64_t p0 = s_p0;
+  const uint32_t jmask = (1u << jbits) - 1;
+  constexpr int U = 8;
+  for (uint64_t base = lo; base < hi; base += (uint64_t)kJointCountThreads * U) {
+    KeyT k[U];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      const uint64_t i = base + (uint64_t)r * kJointCountThreads + tid;
+      k[r] = i < hi ? keys[i] : KeyT(0);
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      const uint64_t i = base + (uint64_t)r * kJointCountThreads + tid;
+      if (i < hi) {
+        const uint64_t x = (uint64_t)k[r] >> shift3;  // parent | d2 | d3
+        const uint64_t rel = (x >> jbits) - p0;
+        if (rel < 2)
+          atomicAdd(&h[((uint32_t)rel << jbits) | ((uint32_t)x & jmask)], 1u);
+        else
+          atomicAdd(hist3 + x, 1u);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nb; i += kJointCountThreads)
+    if (h[i]) atomicAdd(hist3 + (((p0 + (uint64_t)(i >> jbits)) << jbits) | ((uint32_t)i & jmask)), h[i]);
+}
+// level-2 counts as row sums of the level-3 counts (2^d3 children per level-2 bucket)
+__global__ void hist_fold_kernel(const uint32_t* __restrict__ hist3, uint32_t nb2, int d3bits, uint32_t* __restrict__ hist2) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nb2; j += gridDim.x * blockDim.x) {
+    const uint4* row = reinterpret_cast<const uint4*>(hist3 + ((size_t)j << d3bits));
+    uint32_t sum = 0;
+    for (int q = 0; q < (1 << d3bits) / 4; ++q) {
+      const uint4 v = row[q];
+      sum += v.x + v.y + v.z + v.w;
+    }
+    hist2[j] = sum;
+  }
+}
+
 // multi-CTA exclusive scan of n u32 counters (4096 per block, coalesced):
 // scan_block_sums -> scan_top (one CTA over the block sums) -> scan_apply
 constexpr int kScanItems = 4096;
