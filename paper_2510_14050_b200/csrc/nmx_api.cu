@@ -815,11 +815,11 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     CK(cudaMemsetAsync(c->mhist3.p, 0, (size_t)4 << cum[2], c->st));
     auto k = msd_count23_kernel<KeyT>;
     const int jbits = dl[1] + dl[2];
-    const size_t sm = (size_t)8 << jbits;
+    const size_t sm = (size_t)4 << jbits;
     set_smem(k, sm);
     constexpr uint64_t kPer = 1ull << 20;
-    k<<<(unsigned)((n + kPer - 1) / kPer), kJointCountThreads, sm, c->st>>>(outA, gcount, kPer, kb - cum[2], jbits,
-                                                                             c->mhist3.as<uint32_t>());
+    k<<<(unsigned)((n + kPer - 1) / kPer), kJointCountThreads, sm, c->st>>>(
+        outA, gcount, off, 1u << dl[0], kPer, kb - cum[2], jbits, c->mhist3.as<uint32_t>());
     CK_LAUNCH();
     hist_fold_kernel<<<(unsigned)std::max(1u, std::min(((1u << cum[1]) + 255) / 256, (uint32_t)c->sms * 4)), 256, 0,
                        c->st>>>(c->mhist3.as<uint32_t>(), 1u << cum[1], dl[2], c->mhist2.as<uint32_t>());

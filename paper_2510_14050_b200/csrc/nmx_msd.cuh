@@ -407,54 +407,64 @@ __global__ void __launch_bounds__(kMsdThreads) msd_count2_kernel(const KeyT* __r
 }
 
 // Levels 2 and 3 counted in one pass over the level-1 output: each CTA takes a
-// contiguous range of `per_cta` items (at most two level-1 parents for large inputs)
-// and histograms the next jbits = d2 + d3 key bits per parent in shared memory;
-// hist3[top cum3 key bits] receives the counts (a third parent: per-item global
-// atomics). One read of the items instead of two msd_count2 passes.
-constexpr int kJointCountThreads = 1024;
+// contiguous range of `per_cta` items, cut at the level-1 parent boundaries (poff),
+// and histograms the next jbits = d2 + d3 key bits of each parent segment in shared
+// memory (64 KB: three CTAs per SM); hist3[parent << jbits | bin] receives the
+// counts. One read of the items instead of two msd_count2 passes.
+constexpr int kJointCountThreads = 512;
 template <typename KeyT>
 __global__ void __launch_bounds__(kJointCountThreads) msd_count23_kernel(const KeyT* __restrict__ keys,
                                                                         const unsigned long long* __restrict__ mp,
+                                                                        const uint32_t* __restrict__ poff, uint32_t P,
                                                                         uint64_t per_cta, int shift3, int jbits,
                                                                         uint32_t* __restrict__ hist3) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-  __shared__ uint64_t s_p0;
+  __shared__ uint32_t s_p;
   const uint64_t m = *mp;
   const uint64_t lo = (uint64_t)blockIdx.x * per_cta;
   if (lo >= m) return;
   const uint64_t hi = m - lo < per_cta ? m : lo + per_cta;
-  const int nb = 2 << jbits;
+  const int nb = 1 << jbits;
   const int tid = threadIdx.x;
-  for (int i = tid; i < nb; i += kJointCountThreads) h[i] = 0;
-  if (tid == 0) s_p0 = ((uint64_t)keys[lo] >> shift3) >> jbits;
-  __syncthreads();
-  const uint64_t p0 = s_p0;
-  const uint32_t jmask = (1u << jbits) - 1;
-  constexpr int U = 8;
-  for (uint64_t base = lo; base < hi; base += (uint64_t)kJointCountThreads * U) {
-    KeyT k[U];
-#pragma unroll
-    for (int r = 0; r < U; ++r) {
-      const uint64_t i = base + (uint64_t)r * kJointCountThreads + tid;
-      k[r] = i < hi ? keys[i] : KeyT(0);
+  if (tid == 0) {  // last parent starting at or before lo
+    uint32_t a = 0, z = P - 1;
+    while (a < z) {
+      const uint32_t mid = (a + z + 1) >> 1;
+      if (poff[mid] <= lo)
+        a = mid;
+      else
+        z = mid - 1;
     }
-#pragma unroll
-    for (int r = 0; r < U; ++r) {
-      const uint64_t i = base + (uint64_t)r * kJointCountThreads + tid;
-      if (i < hi) {
-        const uint64_t x = (uint64_t)k[r] >> shift3;  // parent | d2 | d3
-        const uint64_t rel = (x >> jbits) - p0;
-        if (rel < 2)
-          atomicAdd(&h[((uint32_t)rel << jbits) | ((uint32_t)x & jmask)], 1u);
-        else
-          atomicAdd(hist3 + x, 1u);
-      }
-    }
+    s_p = a;
   }
   __syncthreads();
-  for (int i = tid; i < nb; i += kJointCountThreads)
-    if (h[i]) atomicAdd(hist3 + (((p0 + (uint64_t)(i >> jbits)) << jbits) | ((uint32_t)i & jmask)), h[i]);
+  const uint32_t jmask = (uint32_t)nb - 1;
+  constexpr int U = 8;
+  uint32_t p = s_p;
+  for (uint64_t a = lo; a < hi; ++p) {  // uniform: one parent segment per round
+    const uint64_t pe = p + 1 < P && (uint64_t)poff[p + 1] < hi ? (uint64_t)poff[p + 1] : hi;
+    if (pe <= a) continue;
+    for (int i = tid; i < nb; i += kJointCountThreads) h[i] = 0;
+    __syncthreads();
+    for (uint64_t base = a; base < pe; base += (uint64_t)kJointCountThreads * U) {
+      KeyT k[U];
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const uint64_t i = base + (uint64_t)r * kJointCountThreads + tid;
+        k[r] = i < pe ? keys[i] : KeyT(0);
+      }
+#pragma unroll
+      for (int r = 0; r < U; ++r)
+        if (base + (uint64_t)r * kJointCountThreads + tid < pe)
+          atomicAdd(&h[(uint32_t)((uint64_t)k[r] >> shift3) & jmask], 1u);
+    }
+    __syncthreads();
+    for (int i = tid; i < nb; i += kJointCountThreads)
+      if (h[i]) atomicAdd(hist3 + (((uint64_t)p << jbits) | (uint32_t)i), h[i]);
+    __syncthreads();
+    a = pe;
+  }
 }
 // level-2 counts as row sums of the level-3 counts (2^d3 children per level-2 bucket)
 __global__ void hist_fold_kernel(const uint32_t* __restrict__ hist3, uint32_t nb2, int d3bits, uint32_t* __restrict__ hist2) {
