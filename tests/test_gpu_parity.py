@@ -90,7 +90,7 @@ def test_device_generator_matches_oracle(lib):
 
 
 @pytest.mark.parametrize("kind", ["uniform", "powerlaw"])
-@pytest.mark.parametrize("lg,space", [(23, 1 << 32), (24, 1 << 20), (25, 1 << 32)])
+@pytest.mark.parametrize("lg,space", [(23, 1 << 32), (24, 1 << 20), (25, 1 << 32), (27, 1 << 20), (27, (1 << 30) + 7)])
 def test_large_vs_packed_oracle(lib, kind, lg, space):
     gen = orc.gen_uniform if kind == "uniform" else orc.gen_powerlaw
     s, d = gen(5, 0, 1 << lg, space)
