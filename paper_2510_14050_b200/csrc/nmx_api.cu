@@ -155,6 +155,8 @@ struct nmx_ctx {
   // nmx_stats9_host_batches: two device input slots, copy-done / slot-free events
   DevBuf bat_s[2], bat_d[2], bat_v[2];
   DevBuf mhist3;  // level-3 counts of msd_count23_kernel
+  DevBuf moff1;   // level-1 offsets kept for the positional levels of narrowed column items
+  DevBuf mtpar;   // per-tile parents of those levels (tile_parents_kernel)
   cudaEvent_t evbc[2] = {nullptr, nullptr}, evbu[2] = {nullptr, nullptr};
   uint32_t* h_small = nullptr;  // pinned mirror of `small`
   unsigned long long* h_scr = nullptr;  // pinned scalars read back mid-pipeline (one round trip each)
@@ -633,19 +635,20 @@ int msd_first_bits(int D) {
 }
 
 // dense scatter launch with the bin capacity of this level's digit width
-template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false>
+template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int NM = NM_NONE>
 void launch_msd_scatter(nmx_ctx* c, int dbits, uint64_t tiles, const Src& src, uint64_t n, KeyT* out, uint32_t* vout,
-                        int shift, int bshift, uint32_t* cursor, KeyT* hout = nullptr, uint32_t* hvout = nullptr) {
+                        int shift, int bshift, uint32_t* cursor, KeyT* hout = nullptr, uint32_t* hvout = nullptr,
+                        const NarrowArgs& nw = NarrowArgs{}) {
   if (dbits > kMsdLevelBits) {
-    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdMaxLevelBits>;
+    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdMaxLevelBits, NM>;
     constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdMaxLevelBits)>);
     set_smem(k, sm);
-    k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout);
+    k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout, nw);
   } else {
-    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdLevelBits>;
+    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdLevelBits, NM>;
     constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdLevelBits)>);
     set_smem(k, sm);
-    k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout);
+    k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout, nw);
   }
 }
 
@@ -869,6 +872,112 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
   c->pend_bytes_per_m = (uint64_t)dom_pending * 2 * kItem;
   c->pend_L = L;
   return defer ? 0 : msd_partition_wait(c, split);
+}
+
+// Column partition with narrowed items (NarrowArgs, nmx_msd.cuh): level 1 reads the
+// u64 (dst << 32 | count) items and writes u32 items (dst bits below the level-1
+// digit | count - 1); levels 2 and 3 are counted in one pass and move 4-byte items
+// with positional parents; heavy destination buckets leave widened back to u64
+// (split->hk) for the segmented levels. Per item: 12 + 4 + 8 + 8 bytes over the
+// levels instead of 16 + 8 + 16 + 16. The caller has checked col_narrow_bits()
+// (three levels, every count <= 2^cb). Deferred like msd_partition (defer = true).
+int col_narrow_bits(int b, int D) {
+  int dl[8], cum[8];
+  if (msd_level_bits(D, dl, cum) != 3 || dl[1] + dl[2] > kJointMaxBits || dl[2] < 2) return 0;
+  const int delta = b - dl[0];
+  return delta >= 8 && delta <= 31 ? 32 - delta : 0;  // count bits
+}
+
+void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, int b, int D, const uint32_t* prehist,
+                               MsdSplit* split, uint32_t* k32A, uint32_t* k32B) {
+  int dl[8], cum[8];
+  msd_level_bits(D, dl, cum);
+  const int kb = b + 32, delta = b - dl[0], cb = 32 - delta;
+  uint32_t* d_small = c->small.as<uint32_t>();
+  auto* gcount = reinterpret_cast<unsigned long long*>(d_small + kGCount);
+  const uint32_t nb = 1u << D;
+  c->mcur.grow(((size_t)nb + 8) * 4);
+  c->moff.grow(((size_t)nb + 8) * 4);
+  c->mhist2.grow(((size_t)nb + 8) * 4);
+  c->moff1.grow(((size_t)(1u << dl[0]) + 8) * 4);
+  c->mhist3.grow(((size_t)(1u << cum[2]) + 8) * 4);
+  uint32_t* cur = c->mcur.as<uint32_t>();
+  uint32_t* off = c->moff.as<uint32_t>();
+  uint32_t* off1 = c->moff1.as<uint32_t>();
+  CK(cudaMemcpyAsync(d_small + kHist, prehist, sizeof(uint32_t) * kMsdMaxBins, cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(gcount, prehist + kMsdMaxBins, 8, cudaMemcpyDeviceToDevice, c->st));
+  NarrowArgs nw;
+  nw.delta = delta;
+  nw.cb = cb;
+  uint64_t bpi = 0;  // dominant-class bytes per valid item
+  // level 1: u64 items -> u32
+  scan_counts(c, d_small + kHist, 1u << dl[0], off1, cur);
+  c->dom_begin("msd_scatter");
+  nw.nout = k32A;
+  launch_msd_scatter<ColConcatSrc, uint64_t, false, 1, false, NM_OUT>(c, dl[0], tiles_of(n, kMsdTile), src, n,
+                                                                      nullptr, nullptr, kb - dl[0], 0, cur, nullptr,
+                                                                      nullptr, nw);
+  CK_LAUNCH();
+  bpi += c->dom_cur ? 12 : 0;
+  c->dom_end(0);
+  // levels 2 + 3 counted jointly over the u32 items (parents = level-1 buckets by position)
+  CK(cudaMemsetAsync(c->mhist3.p, 0, (size_t)4 << cum[2], c->st));
+  {
+    auto k = msd_count23_kernel<uint32_t>;
+    const int jbits = dl[1] + dl[2];
+    const size_t sm = (size_t)4 << jbits;
+    set_smem(k, sm);
+    constexpr uint64_t kPer = 1ull << 20;
+    k<<<(unsigned)((n + kPer - 1) / kPer), kJointCountThreads, sm, c->st>>>(
+        k32A, gcount, off1, 1u << dl[0], kPer, kb - cum[2] - delta, jbits, c->mhist3.as<uint32_t>());
+    CK_LAUNCH();
+    hist_fold_kernel<<<(unsigned)std::max(1u, std::min(((1u << cum[1]) + 255) / 256, (uint32_t)c->sms * 4)), 256, 0,
+                       c->st>>>(c->mhist3.as<uint32_t>(), 1u << cum[1], dl[2], c->mhist2.as<uint32_t>());
+    CK_LAUNCH();
+  }
+  // level 2: u32 -> u32, parents = level-1 buckets
+  const uint64_t ntiles = tiles_of(n, kMsdTile);
+  c->mtpar.grow((size_t)(ntiles + 1) * 16);
+  const unsigned tgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ntiles + 255) / 256, (uint64_t)c->sms * 8));
+  nw.tpar = c->mtpar.as<uint4>();
+  scan_counts(c, c->mhist2.as<uint32_t>(), 1u << cum[1], off, cur);
+  nw.nout = nullptr;
+  nw.poff = off1;
+  nw.npar = 1u << dl[0];
+  tile_parents_kernel<<<tgrid, 256, 0, c->st>>>(off1, nw.npar, gcount, ntiles, c->mtpar.as<uint4>());
+  CK_LAUNCH();
+  c->dom_begin("msd_scatter");
+  launch_msd_scatter<KeySrcD<uint32_t, false>, uint32_t, false, 2, false, NM_POS>(
+      c, dl[1], tiles_of(n, kMsdTile), KeySrcD<uint32_t, false>{k32A, nullptr, gcount}, n, k32B, nullptr,
+      kb - cum[1] - delta, 0, cur, nullptr, nullptr, nw);
+  CK_LAUNCH();
+  bpi += c->dom_cur ? 8 : 0;
+  c->dom_end(0);
+  // level 3 with the light / heavy split: parents = level-2 buckets (their offsets in off)
+  c->spoffA.grow(((size_t)std::min<uint64_t>(1u << cum[2], n / (kSegCap + 1) + 1) + 8) * 4);
+  seg_classify_enqueue(c, c->mhist3.as<uint32_t>(), 1u << cum[2], c->spoffA.as<uint32_t>());
+  nw.poff = off;
+  nw.npar = 1u << cum[1];
+  nw.wout = reinterpret_cast<uint64_t*>(split->hk);
+  nw.dlp = dl[1];
+  tile_parents_kernel<<<tgrid, 256, 0, c->st>>>(off, nw.npar, gcount, ntiles, c->mtpar.as<uint4>());
+  CK_LAUNCH();
+  c->dom_begin("msd_scatter");
+  launch_msd_scatter<KeySrcD<uint32_t, false>, uint32_t, false, 2, true, NM_POS>(
+      c, dl[2], tiles_of(n, kMsdTile), KeySrcD<uint32_t, false>{k32B, nullptr, gcount}, n, k32A, nullptr,
+      kb - cum[2] - delta, 0, c->scur.as<uint32_t>(), nullptr, nullptr, nw);
+  CK_LAUNCH();
+  bpi += c->dom_cur ? 8 : 0;
+  c->dom_end(0);
+  c->launches += 7;  // + the scans and the classification (counted there)
+  c->msd_levels = 3;
+  unsigned long long* h = c->scr() + c->scr_off;  // [0] m, [1..2] split totals
+  CK(cudaMemcpyAsync(h + 1, c->stot.p, sizeof(SegTotals), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(h, gcount, 8, cudaMemcpyDeviceToHost, c->st));
+  if (!c->evw) CK(cudaEventCreateWithFlags(&c->evw, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->evw, c->st));
+  c->pend_bytes_per_m = bpi;
+  c->pend_L = 3;
 }
 
 // ---- segmented MSD levels over heavy buckets (nmx_seg.cuh) ------------------
@@ -1163,6 +1272,15 @@ void heavy_cols(nmx_ctx* c, uint64_t ch, uint32_t nheavy, int b, int Dc) {
 // + wb; returns false (nothing more queued) when a heavy destination bucket needs the
 // segmented levels, which keep no per-window statistics -- the caller reruns the call
 // on the LSD path.
+// NMX_NARROW=0 keeps the u64 column items on every level (A/B runs)
+bool narrow_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("NMX_NARROW");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 bool msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32_t* prehist, int wb = 0) {
   // the levels move packed u64 items (dst << 32 | count, key bits [32, 32 + b))
   // through the row key buffers, free once the row half is queued
@@ -1175,13 +1293,42 @@ bool msd_columns(nmx_ctx* c, const ColConcatSrc& cs, int b, int Dc, const uint32
   MsdSplit sp;
   sp.hk = c->cgk.p;
   c->scr_off = 8;  // its read-back beside the row partition's (both live in one graph)
-  msd_partition<ColConcatSrc, uint64_t, false>(c, cs, cs.n, b + 32, Dc, c->keysA.as<uint64_t>(), nullptr,
-                                               c->keysB.as<uint64_t>(), nullptr, &ce, &unused, prehist, &sp, 0, true);
+  // Narrowed items after level 1 when every count fits cb bits: prehist means the
+  // entries come from this call's row half, whose largest link count (stats field 2)
+  // is on the device once the row kernels are done -- one short host wait.
+  NarrowArgs nw;
+  bool narrow = false;
+  if (prehist && !wb && !c->capturing && cs.n >= (1ull << 27) && narrow_enabled()) {
+    if (const int cb = col_narrow_bits(b, Dc)) {
+      unsigned long long* h = c->scr() + 12;
+      CK(cudaMemcpyAsync(h, c->stats.as<unsigned long long>() + S_MAXLINK, 8, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      narrow = *h >= 1 && *h - 1 < (1ull << cb);
+      if (narrow) {
+        int dl[8], cum[8];
+        msd_level_bits(Dc, dl, cum);
+        nw.delta = b - dl[0];
+        nw.cb = cb;
+        nw.dlp = Dc - dl[0];
+      }
+    }
+  }
+  if (narrow)
+    msd_partition_cols_narrow(c, cs, cs.n, b, Dc, prehist, &sp, c->keysA.as<uint32_t>(), c->keysB.as<uint32_t>());
+  else
+    msd_partition<ColConcatSrc, uint64_t, false>(c, cs, cs.n, b + 32, Dc, c->keysA.as<uint64_t>(), nullptr,
+                                                 c->keysB.as<uint64_t>(), nullptr, &ce, &unused, prehist, &sp, 0, true);
   c->mark();  // column partition end
   {
     const uint32_t* ngp = seg_plan_groups_dev(c, 1u << Dc, cs.n, kLocColChunk,
                                               b - Dc < 31 ? kLocColDirect >> (b - Dc) : 0);
-    if (wb) {
+    if (narrow) {
+      nw.poff = c->sloff.as<uint32_t>();
+      set_smem(local_cols_kernel<false, true>, sizeof(LocColSmem));
+      local_cols_kernel<false, true><<<c->sms * 4, kLocColThreads, sizeof(LocColSmem), c->st>>>(
+          nullptr, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp, 0, 0,
+          c->keysA.as<uint32_t>(), nw);
+    } else if (wb) {
       set_smem(local_cols_kernel<true>, sizeof(LocColSmem));
       local_cols_kernel<true><<<c->sms * 4, kLocColThreads, sizeof(LocColSmem), c->st>>>(
           ce, c->mplan.as<uint4>(), 0, c->stats.as<unsigned long long>(), b - Dc, ngp, Dc - wb, b - wb);
@@ -2807,7 +2954,7 @@ void nmx_destroy(nmx_ctx* c) {
                     &c->csstatus, &c->part, &c->rbstatus, &c->mkeys, &c->mlen, &c->msum, &c->ckeys2, &c->clen2, &c->csum2,
                     &c->frows, &c->small, &c->stats, &c->in_src, &c->in_dst, &c->in_valid, &c->red, &c->ws0, &c->ws1,
                     &c->wd0, &c->wd1, &c->wv0, &c->wv1, &c->wr0, &c->wr1, &c->bat_s[0], &c->bat_s[1], &c->bat_d[0],
-                    &c->bat_d[1], &c->bat_v[0], &c->bat_v[1], &c->mhist3})
+                    &c->bat_d[1], &c->bat_v[0], &c->bat_v[1], &c->mhist3, &c->moff1, &c->mtpar})
     b->release();
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->h_wide) cudaFreeHost(c->h_wide);

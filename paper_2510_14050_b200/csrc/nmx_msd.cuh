@@ -100,19 +100,74 @@ struct MsdSmem {
   uint32_t gbase[NB];
   uint32_t wt[kMsdThreads / 32 + 1];
   uint64_t b1first;
+  uint64_t e1, e2;  // NM_POS: ends of the tile's first two parents
 };
+
+// Narrowed column items (NM_*): after the first column level a u64 item
+// (dst << 32 | count) travels as u32 (dst & (2^delta - 1)) << cb | (count - 1),
+// delta = b - d1 destination bits below the first digit, cb = 32 - delta; the
+// dropped prefix is the item's level-1 bucket, known from its position.
+//   NM_OUT  first level: u64 items in, narrowed u32 items out (nw.nout)
+//   NM_POS  later levels over u32 items: parents by position (nw.poff, nw.npar);
+//           SPLIT heavy items leave widened back to u64 (nw.wout), parent id
+//           >> nw.dlp = the level-1 bucket
+constexpr int NM_NONE = 0, NM_OUT = 1, NM_POS = 2;
+struct NarrowArgs {
+  uint32_t* nout = nullptr;
+  uint64_t* wout = nullptr;
+  const uint32_t* poff = nullptr;
+  uint32_t npar = 0;
+  int delta = 0, cb = 0, dlp = 0;
+  const uint4* tpar = nullptr;  // NM_POS: per tile {first parent, its end, the next parent's end, -}
+};
+__device__ __forceinline__ uint32_t narrow_item(uint64_t e, int delta, int cb) {
+  return ((uint32_t)(e >> 32) & ((1u << delta) - 1u)) << cb | ((uint32_t)e - 1u);
+}
+__device__ __forceinline__ uint64_t widen_item(uint32_t u, uint32_t l1, int delta, int cb) {
+  const uint32_t dst = l1 << delta | u >> cb;
+  return (uint64_t)dst << 32 | ((u & ((1u << cb) - 1u)) + 1u);
+}
+// last parent p in [lo, npar) with poff[p] <= i (poff[npar] = total)
+__device__ __forceinline__ uint32_t find_parent(const uint32_t* poff, uint32_t lo, uint32_t npar, uint64_t i) {
+  uint32_t a = lo, z = npar - 1;
+  while (a < z) {
+    const uint32_t mid = (a + z + 1) >> 1;
+    if ((uint64_t)poff[mid] <= i)
+      a = mid;
+    else
+      z = mid - 1;
+  }
+  return a;
+}
+// NM_POS tile table: one thread per 2048-item tile (a per-tile binary search inside
+// the scatter would put ~log2(npar) dependent loads in front of every tile)
+__global__ void tile_parents_kernel(const uint32_t* __restrict__ poff, uint32_t npar,
+                                    const unsigned long long* __restrict__ mp, uint64_t ntiles,
+                                    uint4* __restrict__ tpar) {
+  const uint64_t m = *mp;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t base = t * kMsdTile;
+    if (base >= m) break;
+    const uint32_t p0 = find_parent(poff, 0, npar, base);
+    tpar[t] = make_uint4(p0, p0 + 1 < npar ? poff[p0 + 1] : 0xFFFFFFFFu, p0 + 2 < npar ? poff[p0 + 2] : 0xFFFFFFFFu, 0);
+  }
+}
 
 // SPLIT (last level): cursor values with kLightBit set address the light
 // output (out, vout), the others the heavy output (hout, hvout) -- buckets too
 // large for a shared-memory group leave the dense levels already compacted.
 constexpr uint32_t kLightBit = 0x80000000u;
 // LB: digit-bit capacity (7, or 8 for the levels that save a whole level)
-template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int LB = kMsdLevelBits>
+template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int LB = kMsdLevelBits,
+          int NM = NM_NONE>
 __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
                                                                    uint32_t* __restrict__ vout, int shift, int dbits,
                                                                    int bshift, uint32_t* __restrict__ cursor,
                                                                    KeyT* __restrict__ hout = nullptr,
-                                                                   uint32_t* __restrict__ hvout = nullptr) {
+                                                                   uint32_t* __restrict__ hvout = nullptr,
+                                                                   NarrowArgs nw = NarrowArgs{}) {
+  static_assert(NM != NM_OUT || (LEVEL == 1 && sizeof(KeyT) == 8 && !HAS_VAL), "NM_OUT: first level of u64 items");
+  static_assert(NM != NM_POS || (LEVEL == 2 && sizeof(KeyT) == 4 && !HAS_VAL), "NM_POS: later levels of u32 items");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NBINS = 2 << LB;
   auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL, NBINS>*>(smem_raw);
@@ -124,18 +179,50 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   }
   for (int i = tid; i < NBINS; i += kMsdThreads) S.cnt[i] = 0;
   if (LEVEL == 2 && tid == 0) {
-    KeyT k0 = 0;
-    uint32_t v;
-    src.load(base, k0, v);
-    S.b1first = (uint64_t)k0 >> bshift;
+    if constexpr (NM == NM_POS) {  // positions < 2^31: 0xFFFFFFFF = no such parent
+      const uint4 tp = nw.tpar[blockIdx.x];
+      S.b1first = tp.x;
+      S.e1 = tp.y;
+      S.e2 = tp.z;
+    } else {
+      KeyT k0 = 0;
+      uint32_t v;
+      src.load(base, k0, v);
+      S.b1first = (uint64_t)k0 >> bshift;
+    }
   }
   // issue every load of the tile before using any (memory-level parallelism);
   // order inside a tile is irrelevant to a non-stable partition
   KeyT k[kMsdIPT];
   uint32_t v[kMsdIPT];
   bool ok[kMsdIPT];
+  uint64_t kidx[NM == NM_POS ? kMsdIPT : 1];  // NM_POS: item positions (parents)
   if constexpr (LEVEL == 1) {
     load_items<Src, KeyT, kMsdIPT / 4>(src, base / 4 + tid, kMsdThreads, k, v, ok);
+  } else if constexpr (NM == NM_POS) {
+    // 16-byte loads: lane takes items 4 lane .. 4 lane + 3 of each 128-item slice
+    const uint64_t wbase = base + (uint64_t)warp * 32 * kMsdIPT;
+    const uint64_t nn = src.size();
+    if (wbase + 32 * kMsdIPT <= nn) {
+      const uint4* p = reinterpret_cast<const uint4*>(src.keys + wbase);
+#pragma unroll
+      for (int i = 0; i < kMsdIPT / 4; ++i) {
+        const uint4 x = p[i * 32 + lane];
+        k[4 * i] = x.x, k[4 * i + 1] = x.y, k[4 * i + 2] = x.z, k[4 * i + 3] = x.w;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          ok[4 * i + t] = true;
+          v[4 * i + t] = 0;
+          kidx[4 * i + t] = wbase + (uint64_t)i * 128 + 4 * lane + t;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kMsdIPT; ++i) {
+        kidx[i] = wbase + (uint64_t)i * 32 + lane;
+        ok[i] = src.load(kidx[i], k[i], v[i]);
+      }
+    }
   } else {
     const uint64_t wbase = base + (uint64_t)warp * 32 * kMsdIPT;
     if constexpr (sizeof(KeyT) == 8 && !HAS_VAL && std::is_same<Src, KeySrcD<KeyT, HAS_VAL>>::value) {
@@ -172,6 +259,19 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
       const uint32_t d = (uint32_t)((uint64_t)k[i] >> shift) & dmask;
       if (LEVEL == 1) {
         bin[i] = (int)d;
+      } else if constexpr (NM == NM_POS) {
+        const uint64_t ix = kidx[i];
+        if (ix < S.e2) {
+          bin[i] = (int)(((ix < S.e1 ? 0u : 1u) << dbits) | d);
+        } else {  // third+ parent inside one tile: direct placement
+          const uint32_t par = find_parent(nw.poff, (uint32_t)b1first + 2, nw.npar, ix);
+          const uint32_t r = atomicAdd(cursor + (par << dbits | d), 1u);
+          if (!SPLIT || (r & kLightBit)) {
+            out[SPLIT ? r & ~kLightBit : r] = k[i];
+          } else {
+            nw.wout[r] = widen_item((uint32_t)k[i], par >> nw.dlp, nw.delta, nw.cb);
+          }
+        }
       } else {
         const uint64_t rel = ((uint64_t)k[i] >> bshift) - b1first;
         if (rel < 2) {
@@ -232,21 +332,34 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   }
   __syncthreads();
   const uint32_t total = S.tstart[nbins - 1] + S.cnt[nbins - 1];
+  // NM_POS: staged items are parent-major, so the second parent's start the same
+  const uint32_t rel1 = NM == NM_POS ? S.tstart[1 << dbits] : 0u;
   for (uint32_t j = tid; j < total; j += kMsdThreads) {
     const KeyT key = S.stage[j];
     int b;
-    if (LEVEL == 1)
+    uint32_t rel = 0;
+    if (LEVEL == 1) {
       b = (int)((uint32_t)((uint64_t)key >> shift) & dmask);
-    else
+    } else if constexpr (NM == NM_POS) {
+      rel = j >= rel1 ? 1u : 0u;
+      b = (int)((rel << dbits) | ((uint32_t)key >> shift & dmask));
+    } else {
       b = (int)(((((uint64_t)key >> bshift) - b1first) << dbits) | (((uint64_t)key >> shift) & dmask));
+    }
     const uint32_t g = S.gbase[b];
     if (!SPLIT || (g & kLightBit)) {
       const uint32_t pos = SPLIT ? (g + j) & ~kLightBit : g + j;
-      out[pos] = key;
+      if constexpr (NM == NM_OUT)
+        nw.nout[pos] = narrow_item((uint64_t)key, nw.delta, nw.cb);
+      else
+        out[pos] = key;
       if (HAS_VAL) vout[pos] = S.vstage[j];
     } else {
       const uint32_t pos = (g + j) & ~kLightBit;  // position arithmetic is modulo 2^31
-      hout[pos] = key;
+      if constexpr (NM == NM_POS)
+        nw.wout[pos] = widen_item((uint32_t)key, ((uint32_t)b1first + rel) >> nw.dlp, nw.delta, nw.cb);
+      else
+        hout[pos] = key;
       if (HAS_VAL) hvout[pos] = S.vstage[j];
     }
   }
@@ -1182,11 +1295,62 @@ __device__ __forceinline__ void flush_cols(unsigned long long* __restrict__ st, 
 
 // WIN: entries carry dst' = window << wdb | dst; per-window statistics as in
 // local_rows_kernel (group window = plan .z / .w >> wsh)
-template <bool WIN = false>
+// NARROW: u32 items (NarrowArgs layout) in ce32; the destination prefix is the
+// group's level-1 bucket (first bucket .z >> nw.dlp); a group whose buckets span
+// level-1 buckets finds each item's by position in the light offsets nw.poff.
+// The raw u32 is loaded with the prefetch and decoded only when the group starts
+// (decoding at load time would wait for the load in the middle of the current group):
+// the group's destination prefix once per group, two operations per item.
+__device__ __forceinline__ void col_load(const uint64_t* ce, const uint32_t* ce32, bool narrow, const uint4& p,
+                                         uint32_t j, uint32_t& d, uint32_t& c) {
+  const uint32_t i = light_index(p, j);
+  if (!narrow) {
+    const uint64_t e = ce[i];
+    d = (uint32_t)(e >> 32);
+    c = (uint32_t)e;
+  } else {
+    d = ce32[i];
+  }
+}
+// prefix (level-1 bucket << delta) of a group inside one level-1 bucket, else 0xFFFFFFFF
+__device__ __forceinline__ uint32_t col_prefix(const NarrowArgs& nw, const uint4& p) {
+  const uint32_t l1 = p.z >> nw.dlp;
+  return p.w > p.z && ((p.w - 1) >> nw.dlp) != l1 ? 0xFFFFFFFFu : l1 << nw.delta;
+}
+// Items of a group inside one level-1 bucket keep only their low destination bits
+// (d = u >> cb: injective there; direct slots are offset by the prefix instead), a
+// group spanning level-1 buckets (rare) rebuilds whole destinations by position.
+template <int PT>
+__device__ __forceinline__ void col_decode_group(const NarrowArgs& nw, uint32_t pre, const uint4& p, uint32_t* d,
+                                                 uint32_t* c) {
+  const uint32_t cm = (1u << nw.cb) - 1u;
+  if (pre != 0xFFFFFFFFu) {
+#pragma unroll
+    for (int r = 0; r < PT; ++r) {
+      const uint32_t u = d[r];
+      c[r] = (u & cm) + 1u;
+      d[r] = u >> nw.cb;
+    }
+    return;
+  }
+  const uint32_t l1last = (p.w - 1) >> nw.dlp;
+#pragma unroll
+  for (int r = 0; r < PT; ++r) {
+    const uint32_t u = d[r];
+    const uint32_t i = light_index(p, threadIdx.x + r * blockDim.x);
+    uint32_t l1 = p.z >> nw.dlp;
+    for (uint32_t q = l1 + 1; q <= l1last && nw.poff[q << nw.dlp] <= i; ++q) l1 = q;
+    c[r] = (u & cm) + 1u;
+    d[r] = l1 << nw.delta | u >> nw.cb;
+  }
+}
+
+template <bool WIN = false, bool NARROW = false>
 __global__ void __launch_bounds__(kLocColThreads, 4)
     local_cols_kernel(const uint64_t* __restrict__ ce, const uint4* __restrict__ plan, uint32_t ngroups,
                       unsigned long long* __restrict__ stats, int dsb, const uint32_t* __restrict__ ngp = nullptr,
-                      int wsh = 0, int wdb = 0) {
+                      int wsh = 0, int wdb = 0, const uint32_t* __restrict__ ce32 = nullptr,
+                      NarrowArgs nw = NarrowArgs{}) {
   if (ngp) ngroups = *ngp;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   LocColSmem& s = *reinterpret_cast<LocColSmem*>(smem_raw);
@@ -1213,16 +1377,16 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
     for (int r = 0; r < kLocColPerThread; ++r) {
       const uint32_t j = tid + r * kLocColThreads;
       if (j < nlight) {
-        const uint64_t e = ce[light_index(p, j)];
-        kr[r] = (uint32_t)(e >> 32);
-        vr[r] = (uint32_t)e;
+        col_load(ce, ce32, NARROW, p, j, kr[r], vr[r]);
         ++nmine;
       }
     }
+    if (NARROW) col_decode_group<kLocColPerThread>(nw, col_prefix(nw, p), p, kr, vr);
   }
   // per-thread totals in 32 bits (fan-in and packets of one destination < 2^32)
   uint32_t a_cnt = 0, a_fanin = 0, a_pk = 0;
   uint32_t it = 0;
+  uint32_t cpre = NARROW && blockIdx.x < ngroups ? col_prefix(nw, s.plan[0]) : 0u;  // current group's prefix
   for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x, ++it) {
     const uint32_t cur = it & 1;
     const uint32_t gn = g + gridDim.x;
@@ -1234,6 +1398,8 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
       const uint4 pc = s.plan[cur];
       dlo = pc.z << dsb;
       direct = ((uint64_t)pc.w << dsb) - dlo <= kLocColDirect;
+      // items of a one-bucket group carry destinations without the prefix
+      if (NARROW && cpre != 0xFFFFFFFFu) dlo -= cpre;
     }
     int gwin = 0;  // WIN: the group's window, -1 when its buckets span several
     if constexpr (WIN) {
@@ -1257,9 +1423,7 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
       for (int r = 0; r < kLocColPerThread; ++r) {
         const uint32_t j = tid + r * kLocColThreads;
         if (j < nl2) {
-          const uint64_t e = ce[light_index(pn, j)];
-          kn[r] = (uint32_t)(e >> 32);
-          vn[r] = (uint32_t)e;
+          col_load(ce, ce32, NARROW, pn, j, kn[r], vn[r]);
           ++nnext;
         }
       }
@@ -1341,7 +1505,11 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
           a_pk = max(a_pk, pk);
         }
       }
-      if (!direct) s.bm[h16u(kr[r]) >> 4] = 0;
+    }
+    if (!direct) {  // a loop of its own: a predicated-off clear per item costs as much as the clear
+#pragma unroll
+      for (int r = 0; r < kLocColPerThread; ++r)
+        if ((uint32_t)r < nmine) s.bm[h16u(kr[r]) >> 4] = 0;
     }
     if (tid == 0 && s.spf) {
       if (WIN && gwin < 0) {
@@ -1367,6 +1535,10 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
     for (int r = 0; r < kLocColPerThread; ++r) {
       kr[r] = kn[r];
       vr[r] = vn[r];
+    }
+    if (NARROW) {
+      cpre = col_prefix(nw, pn);
+      if (nnext) col_decode_group<kLocColPerThread>(nw, cpre, pn, kr, vr);
     }
     nmine = nnext;
   }

@@ -97,6 +97,28 @@ def test_large_vs_packed_oracle(lib, kind, lg, space):
     assert lib.stats9(s, d, None, space) == orc.stats9_packed(s, d)
 
 
+@pytest.mark.parametrize("case", ["hot_dst", "tiny_level1", "count_at_limit", "count_over_limit"])
+def test_narrowed_column_items(lib, case):
+    # 2^27 packets over 2^32: the column partition narrows its items to u32 after
+    # level 1 when every link count fits; heavy destination buckets are widened back,
+    # tiles span several tiny level-1 parents, counts sit at / past the narrow limit
+    n = 1 << 27
+    rng = np.random.default_rng(31)
+    s = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    d = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    if case == "hot_dst":
+        d[: n // 4] = 0xDEADBEEF
+    elif case == "tiny_level1":
+        d[: n - n // 100] = rng.integers(0, 1 << 25, n - n // 100, dtype=np.uint64).astype(np.uint32)
+    else:
+        # a link repeated 2^cb times or once more: 2^27 packets -> D = 18 bits in three
+        # 6-bit levels, 26 destination bits below level 1, cb = 32 - 26 = 6
+        reps = (1 << 6) + (1 if case == "count_over_limit" else 0)
+        s[:reps] = 12345
+        d[:reps] = 67890
+    assert lib.stats9(s, d, None, 1 << 32) == orc.stats9_packed(s, d)
+
+
 def test_small_spaces_and_invalid_mix(lib):
     rng = np.random.default_rng(17)
     for _ in range(60):

@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for v in 1 0; do
+NMX_NARROW=$v timeout 600 ncu --set full --import-source on --clock-control none -k regex:local_cols -c 1 -o gpurun_out/bi_lc_n$v python tools/one_call.py 30 > gpurun_out/bi_ncu_n$v.log 2>&1
+done
