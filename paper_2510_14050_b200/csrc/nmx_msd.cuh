@@ -853,6 +853,147 @@ __device__ __forceinline__ void flush_rows(unsigned long long* __restrict__ st, 
   }
 }
 
+// Phase 2 of local_rows_kernel for one key: its link (counter "once" = unique, else
+// the exact link table) and, unless PARTIAL, its source (DIRECT: one slot per source
+// of the group's range; else counters + exact source table). Returns the st bits
+// (bit0 fast link, bit1 fresh table link, bit2 fast source, bit3 source creator).
+template <bool PARTIAL, bool DIRECT>
+__device__ __forceinline__ uint32_t rows_classify(LocSmem& s, uint32_t* dir, uint64_t key, uint32_t kh, int b,
+                                                  uint64_t slo, uint32_t& hl, uint32_t& hs) {
+  uint32_t st = 0;
+  const uint32_t src = (uint32_t)(key >> b);
+  bool fresh;
+  if (bm_once(s.bml, kh)) {  // unique link (the all-ones key included)
+    fresh = true;
+    st |= 1;
+  } else if (key == ~0ull) {  // key + 1 would wrap: its own counter
+    fresh = atomicAdd(&s.sp_link, 1u) == 0;
+    if (fresh) st |= 2;
+  } else {
+    const unsigned long long kk = key + 1;
+    uint32_t h = hslot(kk, kLocT1);
+    for (;;) {
+      unsigned long long c0 = s.t1key[h];
+      if (c0 == 0) {
+        c0 = atomicCAS(&s.t1key[h], 0ull, kk);
+        if (c0 == 0) {
+          atomicAdd(&s.t1cnt[h], 1u);
+          fresh = true;
+          st |= 2;
+          break;
+        }
+      }
+      if (c0 == kk) {
+        atomicAdd(&s.t1cnt[h], 1u);
+        fresh = false;
+        break;
+      }
+      h = h + 1 == kLocT1 ? 0 : h + 1;
+    }
+    hl = h;
+  }
+  if (PARTIAL) return st;  // sources: warp-aggregated by the caller
+  if (DIRECT) {
+    const uint32_t o = (uint32_t)(src - slo);
+    if (atomicAdd(&dir[o], 1u | (fresh ? 0x10000u : 0u)) == 0) st |= 8;
+    hs = o;
+  } else if (src == 0xFFFFFFFFu) {
+    atomicAdd(&s.sp_src_pk, 1u);
+    if (fresh) atomicAdd(&s.sp_src_fo, 1u);
+  } else if (bm_once(s.bms, h16u(src))) {
+    st |= 4;
+  } else {
+    const uint32_t sk = src + 1;
+    uint32_t h = hslot(sk, kLocT2);
+    for (;;) {
+      uint32_t c0 = s.t2key[h];
+      if (c0 == 0) {
+        c0 = atomicCAS(&s.t2key[h], 0u, sk);
+        if (c0 == 0) {
+          st |= 8;
+          c0 = sk;
+        }
+      }
+      if (c0 == sk) {
+        atomicAdd(&s.t2pf[h], 1u | (fresh ? 0x10000u : 0u));
+        break;
+      }
+      h = h + 1 == kLocT2 ? 0 : h + 1;
+    }
+    hs = h;
+  }
+  return st;
+}
+
+// Phase 3 of local_rows_kernel for one key: its column slot (dst << 32 | count, 0 =
+// hole), link totals, the source report of its creator, and the clears.
+template <bool PARTIAL, bool WIN, bool DIRECT>
+__device__ __forceinline__ void rows_result(LocSmem& s, uint32_t* dir, uint64_t key, uint32_t kh, uint32_t st,
+                                            uint32_t hl, uint32_t hs, uint32_t pos, int b, uint64_t* __restrict__ col,
+                                            int cshift, int gwin, unsigned long long* __restrict__ stats,
+                                            unsigned long long* __restrict__ ccount, const SrcTable& gsrc,
+                                            uint32_t& a_valid, uint32_t& a_links, uint32_t& a_srcs, uint32_t& a_mlink,
+                                            uint32_t& a_msrc, uint32_t& a_mfan) {
+  uint32_t c = 0;
+  if (st & 1) {
+    c = 1;
+  } else if (st & 2) {
+    if (key == ~0ull) {
+      c = s.sp_link;
+    } else {
+      c = s.t1cnt[hl];
+      s.t1key[hl] = 0;
+      s.t1cnt[hl] = 0;
+    }
+  }
+  uint64_t ck = key & ((1ull << b) - 1);
+  if constexpr (WIN) ck |= (key >> (2 * b)) << b;  // dst' = window << b | dst
+  col[pos] = (ck << 32) | c;  // packed column slot (dst << 32 | count; 0 = hole)
+  unsigned long long* sw = WIN ? stats + (size_t)S_COUNT * (key >> (2 * b)) : stats;  // straddling groups
+  if (c) {
+    atomicAdd(&s.chist[(uint32_t)ck >> cshift], 1u);  // the column partition's first level
+    if (WIN && gwin < 0) {
+      atomicAdd(ccount, 1ull);
+      atomicAdd(sw + S_LINKS, 1ull);
+      atomicAdd(sw + S_VALID, (unsigned long long)c);
+      atomicMax(sw + S_MAXLINK, (unsigned long long)c);
+    } else {
+      a_links += 1;
+      a_valid += c;
+      a_mlink = max(a_mlink, c);
+    }
+  }
+  if (!DIRECT && (st & 4)) {  // single-packet source (its maxima of 1 are folded in at the end)
+    if (WIN && gwin < 0) {
+      atomicAdd(sw + S_SRCS, 1ull);
+      atomicMax(sw + S_MAXSRCPK, 1ull);
+      atomicMax(sw + S_MAXFANOUT, 1ull);
+    } else {
+      a_srcs += 1;
+    }
+  } else if (st & 8) {
+    const uint32_t pf = DIRECT ? dir[hs] : s.t2pf[hs];
+    if (PARTIAL) {
+      gsrc.add((uint32_t)(key >> b), ((unsigned long long)(pf >> 16) << 32) | (pf & 0xFFFFu));
+    } else if (WIN && gwin < 0) {
+      atomicAdd(sw + S_SRCS, 1ull);
+      atomicMax(sw + S_MAXSRCPK, (unsigned long long)(pf & 0xFFFFu));
+      atomicMax(sw + S_MAXFANOUT, (unsigned long long)(pf >> 16));
+    } else {
+      a_srcs += 1;
+      a_msrc = max(a_msrc, pf & 0xFFFFu);
+      a_mfan = max(a_mfan, pf >> 16);
+    }
+    if (DIRECT) {
+      dir[hs] = 0;
+    } else {
+      s.t2key[hs] = 0;
+      s.t2pf[hs] = 0;
+    }
+  }
+  s.bml[kh >> 4] = 0;  // benign: every writer stores 0
+}
+
 // WIN (per-window statistics, analytics.py:109-130): keys carry the window id above
 // the 2b address bits and the statistics go to stats[9 w ..]. A group whose buckets lie
 // in one window (plan .z / .w >> wsh) accumulates in registers and flushes at its end;
@@ -886,7 +1027,6 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     if (blockIdx.x < ngroups) s.plan[0] = plan[blockIdx.x];
   }
   __syncthreads();
-  const uint64_t dmask = (1ull << b) - 1;
   uint64_t kr[kLocPerThread];
   uint32_t nmine = 0;
   if (blockIdx.x < ngroups) {
@@ -974,75 +1114,18 @@ __global__ void __launch_bounds__(kLocThreads, 2)
         }
       }
     }
-    // 2. classify; exact tables for colliding keys only
+    // 2. classify; exact tables for colliding keys only (the direct-slot and the
+    // hashed-source bodies are separate loops: one uniform branch per group)
     uint32_t st[kLocPerThread];   // bit0 fast link, bit1 fresh (table creator), bit2 fast source, bit3 source creator
     uint32_t hl[kLocPerThread], hs[kLocPerThread];
+    if (!PARTIAL && direct) {
 #pragma unroll
-    for (int r = 0; r < kLocPerThread; ++r) {
-      st[r] = 0;
-      if ((uint32_t)r >= nmine) continue;
-      const uint64_t key = kr[r];
-      const uint32_t src = (uint32_t)(key >> b);
-      bool fresh;
-      if (bm_once(s.bml, kh[r])) {  // unique link (the all-ones key included)
-        fresh = true;
-        st[r] |= 1;
-      } else if (key == ~0ull) {  // key + 1 would wrap: its own counter
-        fresh = atomicAdd(&s.sp_link, 1u) == 0;
-        if (fresh) st[r] |= 2;
-      } else {
-        const unsigned long long kk = key + 1;
-        uint32_t h = hslot(kk, kLocT1);
-        for (;;) {
-          unsigned long long c0 = s.t1key[h];
-          if (c0 == 0) {
-            c0 = atomicCAS(&s.t1key[h], 0ull, kk);
-            if (c0 == 0) {
-              atomicAdd(&s.t1cnt[h], 1u);
-              fresh = true;
-              st[r] |= 2;
-              break;
-            }
-          }
-          if (c0 == kk) {
-            atomicAdd(&s.t1cnt[h], 1u);
-            fresh = false;
-            break;
-          }
-          h = h + 1 == kLocT1 ? 0 : h + 1;
-        }
-        hl[r] = h;
-      }
-      if (PARTIAL) continue;  // sources: warp-aggregated below
-      if (direct) {
-        const uint32_t o = (uint32_t)(src - slo);
-        if (atomicAdd(&dir[o], 1u | (fresh ? 0x10000u : 0u)) == 0) st[r] |= 8;
-        hs[r] = o;
-      } else if (src == 0xFFFFFFFFu) {
-        atomicAdd(&s.sp_src_pk, 1u);
-        if (fresh) atomicAdd(&s.sp_src_fo, 1u);
-      } else if (bm_once(s.bms, h16u(src))) {
-        st[r] |= 4;
-      } else {
-        const uint32_t sk = src + 1;
-        uint32_t h = hslot(sk, kLocT2);
-        for (;;) {
-          uint32_t c0 = s.t2key[h];
-          if (c0 == 0) {
-            c0 = atomicCAS(&s.t2key[h], 0u, sk);
-            if (c0 == 0) {
-              st[r] |= 8;
-              c0 = sk;
-            }
-          }
-          if (c0 == sk) {
-            atomicAdd(&s.t2pf[h], 1u | (fresh ? 0x10000u : 0u));
-            break;
-          }
-          h = h + 1 == kLocT2 ? 0 : h + 1;
-        }
-        hs[r] = h;
-      }
+      for (int r = 0; r < kLocPerThread; ++r)
+        st[r] = (uint32_t)r < nmine ? rows_classify<PARTIAL, true>(s, dir, kr[r], kh[r], b, slo, hl[r], hs[r]) : 0u;
+    } else {
+#pragma unroll
+      for (int r = 0; r < kLocPerThread; ++r)
+        st[r] = (uint32_t)r < nmine ? rows_classify<PARTIAL, false>(s, dir, kr[r], kh[r], b, slo, hl[r], hs[r]) : 0u;
     }
     if constexpr (PARTIAL) {
       if (single) {  // fresh links of the group's one source: per warp, then one shared add
@@ -1102,70 +1185,25 @@ __global__ void __launch_bounds__(kLocThreads, 2)
     }
     __syncthreads();
     // 3. results: one column slot per key, creators report and clear
+    if (!PARTIAL && direct) {
 #pragma unroll
-    for (int r = 0; r < kLocPerThread; ++r) {
-      if ((uint32_t)r >= nmine) continue;
-      const uint64_t key = kr[r];
-      const uint32_t pos = light_index(p, tid + r * kLocThreads);
-      uint32_t c = 0;
-      if (st[r] & 1) {
-        c = 1;
-      } else if (st[r] & 2) {
-        if (key == ~0ull) {
-          c = s.sp_link;
-        } else {
-          c = s.t1cnt[hl[r]];
-          s.t1key[hl[r]] = 0;
-          s.t1cnt[hl[r]] = 0;
-        }
+      for (int r = 0; r < kLocPerThread; ++r)
+        if ((uint32_t)r < nmine)
+          rows_result<PARTIAL, WIN, true>(s, dir, kr[r], kh[r], st[r], hl[r], hs[r],
+                                          light_index(p, tid + r * kLocThreads), b, col, cshift, gwin, stats, ccount,
+                                          gsrc, a_valid, a_links, a_srcs, a_mlink, a_msrc, a_mfan);
+    } else {
+#pragma unroll
+      for (int r = 0; r < kLocPerThread; ++r)
+        if ((uint32_t)r < nmine)
+          rows_result<PARTIAL, WIN, false>(s, dir, kr[r], kh[r], st[r], hl[r], hs[r],
+                                           light_index(p, tid + r * kLocThreads), b, col, cshift, gwin, stats, ccount,
+                                           gsrc, a_valid, a_links, a_srcs, a_mlink, a_msrc, a_mfan);
+      if (!PARTIAL) {  // source counters of the hashed path (a loop of its own, see local_cols_kernel)
+#pragma unroll
+        for (int r = 0; r < kLocPerThread; ++r)
+          if ((uint32_t)r < nmine) s.bms[h16u((uint32_t)(kr[r] >> b)) >> 4] = 0;
       }
-      uint64_t ck = key & dmask;
-      if constexpr (WIN) ck |= (key >> (2 * b)) << b;  // dst' = window << b | dst
-      col[pos] = (ck << 32) | c;  // packed column slot (dst << 32 | count; 0 = hole)
-      unsigned long long* sw = WIN ? stats + (size_t)S_COUNT * (key >> (2 * b)) : stats;  // straddling groups
-      if (c) {
-        atomicAdd(&s.chist[(uint32_t)ck >> cshift], 1u);  // the column partition's first level
-        if (WIN && gwin < 0) {
-          atomicAdd(ccount, 1ull);
-          atomicAdd(sw + S_LINKS, 1ull);
-          atomicAdd(sw + S_VALID, (unsigned long long)c);
-          atomicMax(sw + S_MAXLINK, (unsigned long long)c);
-        } else {
-          a_links += 1;
-          a_valid += c;
-          a_mlink = max(a_mlink, c);
-        }
-      }
-      if (st[r] & 4) {  // single-packet source (its maxima of 1 are folded in at the end)
-        if (WIN && gwin < 0) {
-          atomicAdd(sw + S_SRCS, 1ull);
-          atomicMax(sw + S_MAXSRCPK, 1ull);
-          atomicMax(sw + S_MAXFANOUT, 1ull);
-        } else {
-          a_srcs += 1;
-        }
-      } else if (st[r] & 8) {
-        const uint32_t pf = direct ? dir[hs[r]] : s.t2pf[hs[r]];
-        if (PARTIAL) {
-          gsrc.add((uint32_t)(key >> b), ((unsigned long long)(pf >> 16) << 32) | (pf & 0xFFFFu));
-        } else if (WIN && gwin < 0) {
-          atomicAdd(sw + S_SRCS, 1ull);
-          atomicMax(sw + S_MAXSRCPK, (unsigned long long)(pf & 0xFFFFu));
-          atomicMax(sw + S_MAXFANOUT, (unsigned long long)(pf >> 16));
-        } else {
-          a_srcs += 1;
-          a_msrc = max(a_msrc, pf & 0xFFFFu);
-          a_mfan = max(a_mfan, pf >> 16);
-        }
-        if (direct) {
-          dir[hs[r]] = 0;
-        } else {
-          s.t2key[hs[r]] = 0;
-          s.t2pf[hs[r]] = 0;
-        }
-      }
-      s.bml[kh[r] >> 4] = 0;  // benign: every writer stores 0
-      if (!PARTIAL && !direct) s.bms[h16u((uint32_t)(key >> b)) >> 4] = 0;
     }
     if (PARTIAL && single && tid == 0 && light_count(p))
       gsrc.add((uint32_t)(keys[light_index(p, 0)] >> b), ((unsigned long long)s.one_fo << 32) | light_count(p));
