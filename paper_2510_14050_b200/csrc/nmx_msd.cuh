@@ -1468,12 +1468,24 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
     }
     uint32_t hh[kLocColPerThread];
     uint32_t stc = 0;  // bit r: fast, bit r+8: table creator
+    // this destination's totals when entry r reports it (WIN edge groups: per entry)
+    auto report = [&](int r, uint32_t fan, uint32_t pk) {
+      if (WIN && gwin < 0) {  // a group at a window edge: straight to the entry's window
+        unsigned long long* sw = stats + (size_t)S_COUNT * (kr[r] >> wdb);
+        atomicAdd(sw + S_DSTS, 1ull);
+        atomicMax(sw + S_MAXFANIN, (unsigned long long)fan);
+        atomicMax(sw + S_MAXDSTPK, (unsigned long long)pk);
+      } else {
+        a_cnt += 1;
+        a_fanin = max(a_fanin, fan);
+        a_pk = max(a_pk, pk);
+      }
+    };
+    if (direct) {  // direct slots: separate loops (one uniform branch per group)
 #pragma unroll
-    for (int r = 0; r < kLocColPerThread; ++r) {
-      if ((uint32_t)r >= nmine) continue;
-      const uint32_t d = kr[r];
-      if (direct) {
-        const uint32_t o = d - dlo;
+      for (int r = 0; r < kLocColPerThread; ++r) {
+        if ((uint32_t)r >= nmine) continue;
+        const uint32_t o = kr[r] - dlo;
         // one atomic: fan-in in bits 20+ (<= 2048 entries) | packets of counts < 512
         // (a group's sum of those stays < 2^20); larger counts add to dpk
         const uint32_t c = vr[r];
@@ -1481,72 +1493,63 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
         if (atomicAdd(&dfan[o], (1u << 20) | small) == 0) stc |= 256u << r;
         if (!small) atomicAdd(&dpk[o], c);
         hh[r] = o;
-      } else if (d == 0xFFFFFFFFu) {
-        atomicAdd(&s.spf, 1u);
-        atomicAdd(&s.spp, vr[r]);
-      } else if (bm_once(s.bm, h16u(d))) {
-        stc |= 1u << r;
-      } else {
-        const uint32_t dk = d + 1;
-        uint32_t h = hslot(dk, kLocCT);
-        for (;;) {
-          uint32_t c0 = s.key[h];
-          if (c0 == 0) {
-            c0 = atomicCAS(&s.key[h], 0u, dk);
-            if (c0 == 0) {
-              stc |= 256u << r;
-              c0 = dk;
-            }
-          }
-          if (c0 == dk) {
-            atomicAdd(&s.nfan[h], 1u);
-            atomicAdd(&s.npk[h], vr[r]);
-            break;
-          }
-          h = h + 1 == kLocCT ? 0 : h + 1;
-        }
-        hh[r] = h;
       }
-    }
-    __syncthreads();
+      __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kLocColPerThread; ++r) {
-      if ((uint32_t)r >= nmine) continue;
-      uint32_t fan = 0, pk = 0;  // this destination's totals if this entry reports it
-      if (stc & (1u << r)) {  // single-link destination (fan-in 1 folded in at the end)
-        fan = 1;
-        pk = vr[r];
-      } else if (stc & (256u << r)) {
-        if (direct) {
-          const uint32_t f = dfan[hh[r]];
-          fan = f >> 20;
-          pk = (f & 0xFFFFFu) + dpk[hh[r]];
-          dfan[hh[r]] = 0;
-          dpk[hh[r]] = 0;
+      for (int r = 0; r < kLocColPerThread; ++r) {
+        if ((uint32_t)r >= nmine || !(stc & (256u << r))) continue;
+        const uint32_t f = dfan[hh[r]];
+        report(r, f >> 20, (f & 0xFFFFFu) + dpk[hh[r]]);
+        dfan[hh[r]] = 0;
+        dpk[hh[r]] = 0;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kLocColPerThread; ++r) {
+        if ((uint32_t)r >= nmine) continue;
+        const uint32_t d = kr[r];
+        if (d == 0xFFFFFFFFu) {
+          atomicAdd(&s.spf, 1u);
+          atomicAdd(&s.spp, vr[r]);
+        } else if (bm_once(s.bm, h16u(d))) {
+          stc |= 1u << r;
         } else {
-          fan = s.nfan[hh[r]];
-          pk = s.npk[hh[r]];
+          const uint32_t dk = d + 1;
+          uint32_t h = hslot(dk, kLocCT);
+          for (;;) {
+            uint32_t c0 = s.key[h];
+            if (c0 == 0) {
+              c0 = atomicCAS(&s.key[h], 0u, dk);
+              if (c0 == 0) {
+                stc |= 256u << r;
+                c0 = dk;
+              }
+            }
+            if (c0 == dk) {
+              atomicAdd(&s.nfan[h], 1u);
+              atomicAdd(&s.npk[h], vr[r]);
+              break;
+            }
+            h = h + 1 == kLocCT ? 0 : h + 1;
+          }
+          hh[r] = h;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kLocColPerThread; ++r) {
+        if ((uint32_t)r >= nmine) continue;
+        if (stc & (1u << r)) {  // single-link destination (fan-in 1 folded in at the end)
+          report(r, 1u, vr[r]);
+        } else if (stc & (256u << r)) {
+          report(r, s.nfan[hh[r]], s.npk[hh[r]]);
           s.key[hh[r]] = 0;
           s.nfan[hh[r]] = 0;
           s.npk[hh[r]] = 0;
         }
       }
-      if (fan) {
-        if (WIN && gwin < 0) {  // a group at a window edge: straight to the entry's window
-          unsigned long long* sw = stats + (size_t)S_COUNT * (kr[r] >> wdb);
-          atomicAdd(sw + S_DSTS, 1ull);
-          atomicMax(sw + S_MAXFANIN, (unsigned long long)fan);
-          atomicMax(sw + S_MAXDSTPK, (unsigned long long)pk);
-        } else {
-          a_cnt += 1;
-          a_fanin = max(a_fanin, fan);
-          a_pk = max(a_pk, pk);
-        }
-      }
-    }
-    if (!direct) {  // a loop of its own: a predicated-off clear per item costs as much as the clear
 #pragma unroll
-      for (int r = 0; r < kLocColPerThread; ++r)
+      for (int r = 0; r < kLocColPerThread; ++r)  // hash counters: a loop of its own
         if ((uint32_t)r < nmine) s.bm[h16u(kr[r]) >> 4] = 0;
     }
     if (tid == 0 && s.spf) {
