@@ -60,10 +60,10 @@ CONFIGS = {
 }
 
 
-def _traffic(kernel: str, bytes_per_launch: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed ncu
-    capture (profiles/traffic_latest.json, tools/ncu_traffic.py), scaled from the
-    captured size to this launch's size by the per-item ratio; None if absent."""
+def _traffic(kernel: str, items_per_launch: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel class, from
+    the committed ncu capture (profiles/traffic_latest.json, tools/ncu_traffic.py), scaled
+    from the captured call's items per launch to this one's; None if absent."""
     try:
         t = json.loads((ROOT / "profiles" / "traffic_latest.json").read_text())
     except Exception:
@@ -72,7 +72,7 @@ def _traffic(kernel: str, bytes_per_launch: int):
     if not ks:
         return None
     per_item = sum(v["dram_bytes"] for v in ks) / sum(v["launches"] for v in ks) / t["items_per_launch"]
-    return round(per_item * bytes_per_launch / 16)
+    return round(per_item * items_per_launch)
 
 
 def _peaks():
@@ -798,19 +798,21 @@ def run_nmx(args) -> None:
         return
 
     peaks, peak_kind = _peaks()
-    # dominant kernel class (MSD partition scatter; onesweep pass on the LSD path):
-    # 8 B in + 8 B out per item per launch, timed by CUDA events around every launch
+    # dominant kernel class (MSD partition scatter; onesweep pass on the LSD path): item
+    # bytes in + out per launch (u64 levels 16 B, the narrowing column level 12 B, the u32
+    # column levels 8 B), timed by CUDA events around every launch
     pass_ms = dom_ms / max(dom_launch, 1)
     bytes_per_launch = dom_bytes // max(dom_launch, 1)
     achieved = bytes_per_launch / (pass_ms / 1e3) / 1e9 if pass_ms else 0.0
     roof = {"bound": "hbm", "kernel": timing_last.get("dom_name", ""), "achieved": round(achieved, 1),
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-            "peak_kind": peak_kind, "traffic": _traffic(timing_last.get("dom_name", ""), bytes_per_launch),
+            "peak_kind": peak_kind, "traffic": _traffic(timing_last.get("dom_name", ""), n_total // max(world, 1)),
             "launches_per_step": dom_launch // max(args.steps, 1),
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(pass_ms, 4),
             "share_of_step": round(dom_ms / ms, 4) if ms else None,
-            "note": "algorithmic bytes = 8 B read + 8 B write per item per launch; traffic per launch from ncu "
-                    "dram__bytes in profiles/"}
+            "note": "algorithmic bytes = item bytes read + written per launch, averaged over the class "
+                    "(16 B per item on the u64 levels, 12 B on the column level that narrows items to u32, "
+                    "8 B on the u32 column levels); traffic per launch from ncu dram__bytes in profiles/"}
     # whole step: DRAM bytes the step actually moves (sum over its kernels of ncu
     # dram__bytes_read + write, profiles/traffic_<config>.json, one captured call of the
     # same configuration) / step time. SURVEY.md 8(d)'s canonical LSD byte count
