@@ -1083,7 +1083,8 @@ uint64_t heavy_rows(nmx_ctx* c, uint64_t mh, uint32_t nheavy, int b, int D, int 
   bool part[16];
   int L = 0;
   const int r = b - D;                          // source bits below the dense prefix
-  const int r0 = r > 0 ? std::min(r, std::min((r + 1) / 2, seg_level_bits())) : 0;
+  int r0 = r > 0 ? std::min(r, std::min((r + 1) / 2, seg_level_bits())) : 0;
+  if (const char* e = getenv("NMX_HEAVY_R0")) r0 = std::max(0, std::min(r, atoi(e)));  // A/B runs
   if (r0) w[L] = r0, sh[L] = 2 * b - D - r0, part[L] = false, ++L;
   {
     int dw[8];
