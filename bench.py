@@ -75,6 +75,21 @@ def _traffic(kernel: str, items_per_launch: int):
     return round(per_item * items_per_launch)
 
 
+def _per_launch(totals, peak_gbs):
+    """The dominant class launch by launch, averaged over the timed steps: CUDA-event
+    ms, algorithmic bytes, GB/s and fraction of the HBM peak (nmx_last_kernel_launches)."""
+    runs = [t.get("dom_per_launch") or [] for t in totals]
+    if not runs or any(len(r) != len(runs[0]) for r in runs):
+        return None
+    out = []
+    for i in range(len(runs[0])):
+        ms = sum(r[i][0] for r in runs) / len(runs)
+        by = runs[0][i][1]
+        gbs = by / (ms / 1e3) / 1e9 if ms else 0.0
+        out.append({"ms": round(ms, 4), "bytes": by, "gbs": round(gbs, 1), "frac": round(gbs / peak_gbs, 4)})
+    return out
+
+
 def _peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
@@ -810,6 +825,7 @@ def run_nmx(args) -> None:
             "launches_per_step": dom_launch // max(args.steps, 1),
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(pass_ms, 4),
             "share_of_step": round(dom_ms / ms, 4) if ms else None,
+            "per_launch": _per_launch(totals, peaks["hbm_gbs"]),
             "note": "algorithmic bytes = item bytes read + written per launch, averaged over the class "
                     "(16 B per item on the u64 levels, 12 B on the column level that narrows items to u32, "
                     "8 B on the u32 column levels); traffic per launch from ncu dram__bytes in profiles/"}

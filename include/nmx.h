@@ -302,8 +302,13 @@ int nmx_last_timing(nmx_ctx* ctx, float* total_ms, float* sort_ms, int* sort_lau
 int nmx_last_stages(nmx_ctx* ctx, float* ms, int cap);
 /* The dominant kernel class of the last hot-path call (the MSD partition scatter,
  * or the onesweep pass on the LSD path): summed CUDA-event time of its launches,
- * launch count, algorithmic bytes (8 B in + 8 B out per item per launch) and name. */
+ * launch count, algorithmic bytes (item bytes in + out per launch: 16 per item on
+ * the u64 levels, 12 on the column level that narrows items to u32, 8 on the u32
+ * levels) and name. */
 int nmx_last_kernel_class(nmx_ctx* ctx, float* ms, int* launches, uint64_t* bytes, char* name, int name_cap);
+/* The same class launch by launch (up to cap): CUDA-event ms and algorithmic bytes
+ * of each; *count = the number of launches recorded (<= 32). */
+int nmx_last_kernel_launches(nmx_ctx* ctx, int cap, float* ms, uint64_t* bytes, int* count);
 
 #ifdef __cplusplus
 }

@@ -90,6 +90,7 @@ SIGNATURES = {
     "nmx_comm_last_exchange": (C.c_int, [_VP, C.POINTER(_U64), C.POINTER(_U64)]),
     "nmx_last_kernel_class": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_int), C.POINTER(_U64), C.c_char_p,
                                          C.c_int]),
+    "nmx_last_kernel_launches": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_float), C.POINTER(_U64), C.POINTER(C.c_int)]),
     "nmx_last_stages": (C.c_int, [_VP, C.POINTER(C.c_float), C.c_int]),
     "nmx_last_timing": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_int),
                                   C.POINTER(C.c_int)]),
@@ -181,9 +182,12 @@ class Context:
         dms, dl, db = C.c_float(), C.c_int(), C.c_uint64()
         name = C.create_string_buffer(64)
         check(self._lib.nmx_last_kernel_class(self._h, C.byref(dms), C.byref(dl), C.byref(db), name, 64))
+        lms, lby, lc = (C.c_float * 32)(), (C.c_uint64 * 32)(), C.c_int()
+        check(self._lib.nmx_last_kernel_launches(self._h, 32, lms, lby, C.byref(lc)))
         return dict(total_ms=t.value, sort_ms=s.value, sort_launches=sl.value, kernel_launches=kl.value,
                     stages_ms=[round(st[i], 4) for i in range(max(k, 0))],
-                    dom_ms=dms.value, dom_launches=dl.value, dom_bytes=db.value, dom_name=name.value.decode())
+                    dom_ms=dms.value, dom_launches=dl.value, dom_bytes=db.value, dom_name=name.value.decode(),
+                    dom_per_launch=[(lms[i], lby[i]) for i in range(min(lc.value, 32))])
 
 
 _contexts: dict[int, Context] = {}

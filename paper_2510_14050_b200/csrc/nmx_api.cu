@@ -242,12 +242,23 @@ struct nmx_ctx {
     dom_cur = strcmp(dom_name, nm) == 0 && nevk + 2 <= 64;
     if (dom_cur) CK(cudaEventRecord(evk[nevk], st));
   }
-  void dom_end(uint64_t bytes) {
+  // per launch: algorithmic bytes (known now, or bytes per valid item `bpi` resolved
+  // when the partition's valid count comes back) and the event-pair time
+  uint64_t dom_lbytes[32] = {};
+  uint32_t dom_lbpi[32] = {};
+  float dom_lms[32] = {};
+  void dom_end(uint64_t bytes, uint32_t bpi = 0) {
     if (!dom_cur) return;
     CK(cudaEventRecord(evk[nevk + 1], st));
+    dom_lbytes[nevk / 2] = bytes;
+    dom_lbpi[nevk / 2] = bpi;
     nevk += 2;
     dom_bytes += bytes;
     ++dom_launches;
+  }
+  void dom_resolve(uint64_t m) {  // launches waiting for their item count
+    for (int k = 0; k < nevk / 2; ++k)
+      if (dom_lbpi[k] && !dom_lbytes[k]) dom_lbytes[k] = (uint64_t)dom_lbpi[k] * m;
   }
 };
 
@@ -425,6 +436,7 @@ void stage_finish(nmx_ctx* c, uint64_t W) {
     float t = 0;
     CK(cudaEventElapsedTime(&t, c->evk[i], c->evk[i + 1]));
     c->dom_ms += t;
+    c->dom_lms[i / 2] = t;
   }
 }
 
@@ -732,6 +744,7 @@ uint64_t msd_partition_wait(nmx_ctx* c, MsdSplit* split) {
               split->t.big, split->t.nbig);
   }
   c->dom_bytes += c->pend_bytes_per_m * m;
+  c->dom_resolve(m);
   return m;
 }
 
@@ -802,7 +815,7 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
                                               cur);
     CK_LAUNCH();
     dom_pending += c->dom_cur;
-    c->dom_end(0);
+    c->dom_end(0, 2 * kItem);
     ++c->launches;
   }
   KeyT* in_k = outA;
@@ -855,7 +868,7 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
     }
     CK_LAUNCH();
     dom_pending += c->dom_cur;
-    c->dom_end(0);
+    c->dom_end(0, 2 * kItem);
     c->launches += 3;
     std::swap(in_k, out_k);
     std::swap(in_v, out_v);
@@ -919,7 +932,7 @@ void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, 
                                                                       nullptr, nw);
   CK_LAUNCH();
   bpi += c->dom_cur ? 12 : 0;
-  c->dom_end(0);
+  c->dom_end(0, 12);
   // levels 2 + 3 counted jointly over the u32 items (parents = level-1 buckets by position)
   CK(cudaMemsetAsync(c->mhist3.p, 0, (size_t)4 << cum[2], c->st));
   {
@@ -952,7 +965,7 @@ void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, 
       kb - cum[1] - delta, 0, cur, nullptr, nullptr, nw);
   CK_LAUNCH();
   bpi += c->dom_cur ? 8 : 0;
-  c->dom_end(0);
+  c->dom_end(0, 8);
   // level 3 with the light / heavy split: parents = level-2 buckets (their offsets in off)
   c->spoffA.grow(((size_t)std::min<uint64_t>(1u << cum[2], n / (kSegCap + 1) + 1) + 8) * 4);
   seg_classify_enqueue(c, c->mhist3.as<uint32_t>(), 1u << cum[2], c->spoffA.as<uint32_t>());
@@ -968,7 +981,7 @@ void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, 
       kb - cum[2] - delta, 0, c->scur.as<uint32_t>(), nullptr, nullptr, nw);
   CK_LAUNCH();
   bpi += c->dom_cur ? 8 : 0;
-  c->dom_end(0);
+  c->dom_end(0, 8);
   c->launches += 7;  // + the scans and the classification (counted there)
   c->msd_levels = 3;
   unsigned long long* h = c->scr() + c->scr_off;  // [0] m, [1..2] split totals
@@ -3706,6 +3719,7 @@ int nmx_coo_merge_add(nmx_ctx* c, const nmx_coo* a, const nmx_coo* b, nmx_coo** 
       CK(cudaMemcpyAsync(res, ovf, 16, cudaMemcpyDeviceToHost, c->st));
       CK(cudaStreamSynchronize(c->st));
       c->dom_bytes += 16 * (uint64_t)res[1];
+      if (c->dom_cur) c->dom_lbytes[c->nevk / 2 - 1] += 16 * (uint64_t)res[1];
       o->nnz = res[1];
       if (res[0]) {
         nmx_coo_free(o);
@@ -3842,6 +3856,17 @@ int nmx_last_kernel_class(nmx_ctx* c, float* ms, int* launches, uint64_t* bytes,
   if (launches) *launches = c->dom_launches;
   if (bytes) *bytes = c->dom_bytes;
   if (name && name_cap > 0) snprintf(name, name_cap, "%s", c->dom_name);
+  return NMX_OK;
+}
+
+int nmx_last_kernel_launches(nmx_ctx* c, int cap, float* ms, uint64_t* bytes, int* count) {
+  if (!c || cap < 0) return fail(NMX_EINVAL, "null context or negative capacity");
+  const int k = std::min(cap, c->nevk / 2);
+  for (int i = 0; i < k; ++i) {
+    if (ms) ms[i] = c->dom_lms[i];
+    if (bytes) bytes[i] = c->dom_lbytes[i];
+  }
+  if (count) *count = c->nevk / 2;
   return NMX_OK;
 }
 
