@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   KeyT k[kMsdIPT];
   uint32_t v[kMsdIPT];
   bool ok[kMsdIPT];
-  uint64_t kidx[NM == NM_POS ? kMsdIPT : 1];  // NM_POS: item positions (parents)
+  uint32_t kidx[NM == NM_POS ? kMsdIPT : 1];  // NM_POS: item positions (< 2^31: n < 2^31 per call)
   if constexpr (LEVEL == 1) {
     load_items<Src, KeyT, kMsdIPT / 4>(src, base / 4 + tid, kMsdThreads, k, v, ok);
   } else if constexpr (NM == NM_POS) {
@@ -213,14 +213,14 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
         for (int t = 0; t < 4; ++t) {
           ok[4 * i + t] = true;
           v[4 * i + t] = 0;
-          kidx[4 * i + t] = wbase + (uint64_t)i * 128 + 4 * lane + t;
+          kidx[4 * i + t] = (uint32_t)wbase + (uint32_t)(i * 128 + 4 * lane + t);
         }
       }
     } else {
 #pragma unroll
       for (int i = 0; i < kMsdIPT; ++i) {
-        kidx[i] = wbase + (uint64_t)i * 32 + lane;
-        ok[i] = src.load(kidx[i], k[i], v[i]);
+        kidx[i] = (uint32_t)wbase + (uint32_t)(i * 32 + lane);
+        ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
       }
     }
   } else {
@@ -249,6 +249,9 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   }
   __syncthreads();
   const uint64_t b1first = S.b1first;
+  // NM_POS parent ends in registers: the stores and global atomics below may alias
+  // shared memory as far as the compiler knows, so S.e1 / S.e2 would be reloaded per key
+  const uint32_t e1 = NM == NM_POS ? (uint32_t)S.e1 : 0u, e2 = NM == NM_POS ? (uint32_t)S.e2 : 0u;
   const uint32_t dmask = (1u << dbits) - 1;
   uint32_t rank[kMsdIPT];
   int bin[kMsdIPT];
@@ -260,9 +263,9 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
       if (LEVEL == 1) {
         bin[i] = (int)d;
       } else if constexpr (NM == NM_POS) {
-        const uint64_t ix = kidx[i];
-        if (ix < S.e2) {
-          bin[i] = (int)(((ix < S.e1 ? 0u : 1u) << dbits) | d);
+        const uint32_t ix = kidx[i];
+        if (ix < e2) {
+          bin[i] = (int)(((ix < e1 ? 0u : 1u) << dbits) | d);
         } else {  // third+ parent inside one tile: direct placement
           const uint32_t par = find_parent(nw.poff, (uint32_t)b1first + 2, nw.npar, ix);
           const uint32_t r = atomicAdd(cursor + (par << dbits | d), 1u);
