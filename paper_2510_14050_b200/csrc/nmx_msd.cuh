@@ -1485,6 +1485,7 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
       }
     };
     if (direct) {  // direct slots: separate loops (one uniform branch per group)
+      bool big = false;
 #pragma unroll
       for (int r = 0; r < kLocColPerThread; ++r) {
         if ((uint32_t)r >= nmine) continue;
@@ -1494,17 +1495,31 @@ __global__ void __launch_bounds__(kLocColThreads, 4)
         const uint32_t c = vr[r];
         const uint32_t small = c < 512u ? c : 0u;
         if (atomicAdd(&dfan[o], (1u << 20) | small) == 0) stc |= 256u << r;
-        if (!small) atomicAdd(&dpk[o], c);
+        if (!small) {
+          atomicAdd(&dpk[o], c);
+          big = true;
+        }
         hh[r] = o;
       }
-      __syncthreads();
+      // dpk is all zero unless some entry of the group added to it: only then do the
+      // creators read and clear it (uniform data: no count >= 512, half the slot traffic)
+      if (__syncthreads_or(big)) {
 #pragma unroll
-      for (int r = 0; r < kLocColPerThread; ++r) {
-        if ((uint32_t)r >= nmine || !(stc & (256u << r))) continue;
-        const uint32_t f = dfan[hh[r]];
-        report(r, f >> 20, (f & 0xFFFFFu) + dpk[hh[r]]);
-        dfan[hh[r]] = 0;
-        dpk[hh[r]] = 0;
+        for (int r = 0; r < kLocColPerThread; ++r) {
+          if ((uint32_t)r >= nmine || !(stc & (256u << r))) continue;
+          const uint32_t f = dfan[hh[r]];
+          report(r, f >> 20, (f & 0xFFFFFu) + dpk[hh[r]]);
+          dfan[hh[r]] = 0;
+          dpk[hh[r]] = 0;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < kLocColPerThread; ++r) {
+          if ((uint32_t)r >= nmine || !(stc & (256u << r))) continue;
+          const uint32_t f = dfan[hh[r]];
+          report(r, f >> 20, f & 0xFFFFFu);
+          dfan[hh[r]] = 0;
+        }
       }
     } else {
 #pragma unroll
