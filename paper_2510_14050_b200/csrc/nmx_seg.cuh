@@ -362,7 +362,6 @@ template <typename KeyT, bool HAS_VAL>
 struct SegSmem {
   KeyT stage[kMsdTile];
   uint32_t vstage[HAS_VAL ? kMsdTile : 1];
-  uint16_t sbin[kMsdTile];
   uint32_t cnt[kSegBins];
   uint32_t tstart[kSegBins];
   uint32_t gbase[kSegBins];
@@ -373,8 +372,9 @@ struct SegSmem {
 // Non-stable partition of each parent by `dbits` key bits at `shift`; light
 // children land in (lout, lvout), big children in (bout, bvout). Ranking, the
 // per-tile reservation atomics and the shared-memory staging follow
-// msd_scatter_kernel; the bin of every staged item is kept (it cannot be
-// recomputed from the key: parents are positional).
+// msd_scatter_kernel. Parents are positional, so a staged item's parent is
+// recovered from its staged position: the tile stages parent-major (bin = rel << dbits
+// | digit), parent q's items start at tstart[q << dbits].
 template <typename KeyT, bool HAS_VAL>
 __global__ void __launch_bounds__(kMsdThreads, 5) seg_scatter_kernel(const KeyT* __restrict__ keys,
                                                                  const uint32_t* __restrict__ vals, uint32_t m,
@@ -466,7 +466,6 @@ __global__ void __launch_bounds__(kMsdThreads, 5) seg_scatter_kernel(const KeyT*
       const uint32_t at = S.tstart[bin[i]] + rank[i];
       S.stage[at] = k[i];
       if (HAS_VAL) S.vstage[at] = v[i];
-      S.sbin[at] = (uint16_t)bin[i];
     }
 #pragma unroll
   for (int q = 0; q < kSegBins / kMsdThreads; ++q) {
@@ -477,14 +476,21 @@ __global__ void __launch_bounds__(kMsdThreads, 5) seg_scatter_kernel(const KeyT*
   }
   __syncthreads();
   const uint32_t total = S.tstart[nbins - 1] + S.cnt[nbins - 1];
+  uint32_t pst[kSegMaxRel - 1];  // staged start of parents 1 .. kSegMaxRel - 1
+#pragma unroll
+  for (int q = 1; q < kSegMaxRel; ++q) pst[q - 1] = S.tstart[q << dbits];
   for (uint32_t j = tid; j < total; j += kMsdThreads) {
-    const uint32_t g = S.gbase[S.sbin[j]];
+    const KeyT key = S.stage[j];
+    uint32_t rel = 0;
+#pragma unroll
+    for (int q = 0; q < kSegMaxRel - 1; ++q) rel += j >= pst[q];
+    const uint32_t g = S.gbase[(rel << dbits) | seg_digit(key, shift, dmask)];
     const uint32_t pos = (g + j) & ~kLightBit;
     if (g & kLightBit) {
-      lout[pos] = S.stage[j];
+      lout[pos] = key;
       if (HAS_VAL) lvout[pos] = S.vstage[j];
     } else {
-      bout[pos] = S.stage[j];
+      bout[pos] = key;
       if (HAS_VAL) bvout[pos] = S.vstage[j];
     }
   }
