@@ -647,18 +647,19 @@ int msd_first_bits(int D) {
 }
 
 // dense scatter launch with the bin capacity of this level's digit width
-template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int NM = NM_NONE>
+template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int NM = NM_NONE,
+          int IPT = kMsdIPT>
 void launch_msd_scatter(nmx_ctx* c, int dbits, uint64_t tiles, const Src& src, uint64_t n, KeyT* out, uint32_t* vout,
                         int shift, int bshift, uint32_t* cursor, KeyT* hout = nullptr, uint32_t* hvout = nullptr,
                         const NarrowArgs& nw = NarrowArgs{}) {
   if (dbits > kMsdLevelBits) {
-    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdMaxLevelBits, NM>;
-    constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdMaxLevelBits)>);
+    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdMaxLevelBits, NM, IPT>;
+    constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdMaxLevelBits), kMsdThreads * IPT>);
     set_smem(k, sm);
     k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout, nw);
   } else {
-    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdLevelBits, NM>;
-    constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdLevelBits)>);
+    auto k = msd_scatter_kernel<Src, KeyT, HAS_VAL, LEVEL, SPLIT, kMsdLevelBits, NM, IPT>;
+    constexpr size_t sm = sizeof(MsdSmem<KeyT, HAS_VAL, (2 << kMsdLevelBits), kMsdThreads * IPT>);
     set_smem(k, sm);
     k<<<(unsigned)tiles, kMsdThreads, sm, c->st>>>(src, n, out, vout, shift, dbits, bshift, cursor, hout, hvout, nw);
   }
@@ -894,6 +895,13 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
 // (split->hk) for the segmented levels. Per item: 12 + 4 + 8 + 8 bytes over the
 // levels instead of 16 + 8 + 16 + 16. The caller has checked col_narrow_bits()
 // (three levels, every count <= 2^cb). Deferred like msd_partition (defer = true).
+// items per thread of the u32 column levels (4-byte items: a 4096-item tile stages in
+// the bytes of a 2048-item u64 tile, digit runs twice as long)
+#ifndef NMX_POS_IPT
+#define NMX_POS_IPT 8
+#endif
+constexpr int kPosIPT = NMX_POS_IPT;
+constexpr int kPosTile = kMsdThreads * kPosIPT;
 int col_narrow_bits(int b, int D) {
   int dl[8], cum[8];
   if (msd_level_bits(D, dl, cum) != 3 || dl[1] + dl[2] > kJointMaxBits || dl[2] < 2) return 0;
@@ -948,8 +956,8 @@ void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, 
                        c->st>>>(c->mhist3.as<uint32_t>(), 1u << cum[1], dl[2], c->mhist2.as<uint32_t>());
     CK_LAUNCH();
   }
-  // level 2: u32 -> u32, parents = level-1 buckets
-  const uint64_t ntiles = tiles_of(n, kMsdTile);
+  // level 2: u32 -> u32, parents = level-1 buckets (tiles of kPosIPT items per thread)
+  const uint64_t ntiles = tiles_of(n, kPosTile);
   c->mtpar.grow((size_t)(ntiles + 1) * 16);
   const unsigned tgrid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ntiles + 255) / 256, (uint64_t)c->sms * 8));
   nw.tpar = c->mtpar.as<uint4>();
@@ -957,11 +965,11 @@ void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, 
   nw.nout = nullptr;
   nw.poff = off1;
   nw.npar = 1u << dl[0];
-  tile_parents_kernel<<<tgrid, 256, 0, c->st>>>(off1, nw.npar, gcount, ntiles, c->mtpar.as<uint4>());
+  tile_parents_kernel<<<tgrid, 256, 0, c->st>>>(off1, nw.npar, gcount, ntiles, c->mtpar.as<uint4>(), kPosTile);
   CK_LAUNCH();
   c->dom_begin("msd_scatter");
-  launch_msd_scatter<KeySrcD<uint32_t, false>, uint32_t, false, 2, false, NM_POS>(
-      c, dl[1], tiles_of(n, kMsdTile), KeySrcD<uint32_t, false>{k32A, nullptr, gcount}, n, k32B, nullptr,
+  launch_msd_scatter<KeySrcD<uint32_t, false>, uint32_t, false, 2, false, NM_POS, kPosIPT>(
+      c, dl[1], ntiles, KeySrcD<uint32_t, false>{k32A, nullptr, gcount}, n, k32B, nullptr,
       kb - cum[1] - delta, 0, cur, nullptr, nullptr, nw);
   CK_LAUNCH();
   bpi += c->dom_cur ? 8 : 0;
@@ -973,11 +981,11 @@ void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, 
   nw.npar = 1u << cum[1];
   nw.wout = reinterpret_cast<uint64_t*>(split->hk);
   nw.dlp = dl[1];
-  tile_parents_kernel<<<tgrid, 256, 0, c->st>>>(off, nw.npar, gcount, ntiles, c->mtpar.as<uint4>());
+  tile_parents_kernel<<<tgrid, 256, 0, c->st>>>(off, nw.npar, gcount, ntiles, c->mtpar.as<uint4>(), kPosTile);
   CK_LAUNCH();
   c->dom_begin("msd_scatter");
-  launch_msd_scatter<KeySrcD<uint32_t, false>, uint32_t, false, 2, true, NM_POS>(
-      c, dl[2], tiles_of(n, kMsdTile), KeySrcD<uint32_t, false>{k32B, nullptr, gcount}, n, k32A, nullptr,
+  launch_msd_scatter<KeySrcD<uint32_t, false>, uint32_t, false, 2, true, NM_POS, kPosIPT>(
+      c, dl[2], ntiles, KeySrcD<uint32_t, false>{k32B, nullptr, gcount}, n, k32A, nullptr,
       kb - cum[2] - delta, 0, c->scur.as<uint32_t>(), nullptr, nullptr, nw);
   CK_LAUNCH();
   bpi += c->dom_cur ? 8 : 0;

@@ -91,10 +91,10 @@ __device__ __forceinline__ void load_items(const Src& s, uint64_t q0, uint64_t q
 // the D-bit bucket id; a tile lies in one or two level-1 buckets, keys of further
 // buckets take a per-key global atomic). KeyT u64 = packed row keys; KeyT u32
 // with a u32 payload = column entries (dst, count).
-template <typename KeyT, bool HAS_VAL, int NB = (2 << kMsdLevelBits)>
+template <typename KeyT, bool HAS_VAL, int NB = (2 << kMsdLevelBits), int TILE = kMsdTile>
 struct MsdSmem {
-  KeyT stage[kMsdTile];
-  uint32_t vstage[HAS_VAL ? kMsdTile : 1];
+  KeyT stage[TILE];
+  uint32_t vstage[HAS_VAL ? TILE : 1];
   uint32_t cnt[NB];
   uint32_t tstart[NB];
   uint32_t gbase[NB];
@@ -143,10 +143,10 @@ __device__ __forceinline__ uint32_t find_parent(const uint32_t* poff, uint32_t l
 // the scatter would put ~log2(npar) dependent loads in front of every tile)
 __global__ void tile_parents_kernel(const uint32_t* __restrict__ poff, uint32_t npar,
                                     const unsigned long long* __restrict__ mp, uint64_t ntiles,
-                                    uint4* __restrict__ tpar) {
+                                    uint4* __restrict__ tpar, uint32_t tile = kMsdTile) {
   const uint64_t m = *mp;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t base = t * kMsdTile;
+    const uint64_t base = t * tile;
     if (base >= m) break;
     const uint32_t p0 = find_parent(poff, 0, npar, base);
     tpar[t] = make_uint4(p0, p0 + 1 < npar ? poff[p0 + 1] : 0xFFFFFFFFu, p0 + 2 < npar ? poff[p0 + 2] : 0xFFFFFFFFu, 0);
@@ -159,8 +159,8 @@ __global__ void tile_parents_kernel(const uint32_t* __restrict__ poff, uint32_t 
 constexpr uint32_t kLightBit = 0x80000000u;
 // LB: digit-bit capacity (7, or 8 for the levels that save a whole level)
 template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int LB = kMsdLevelBits,
-          int NM = NM_NONE>
-__global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
+          int NM = NM_NONE, int IPT = kMsdIPT>
+__global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
                                                                    uint32_t* __restrict__ vout, int shift, int dbits,
                                                                    int bshift, uint32_t* __restrict__ cursor,
                                                                    KeyT* __restrict__ hout = nullptr,
@@ -170,10 +170,11 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   static_assert(NM != NM_POS || (LEVEL == 2 && sizeof(KeyT) == 4 && !HAS_VAL), "NM_POS: later levels of u32 items");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int NBINS = 2 << LB;
-  auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL, NBINS>*>(smem_raw);
+  constexpr int TILE = kMsdThreads * IPT;
+  auto& S = *reinterpret_cast<MsdSmem<KeyT, HAS_VAL, NBINS, TILE>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nbins = LEVEL == 1 ? (1 << dbits) : (2 << dbits);
-  const uint64_t base = (uint64_t)blockIdx.x * kMsdTile;
+  const uint64_t base = (uint64_t)blockIdx.x * TILE;
   if constexpr (LEVEL == 2) {
     if (base >= src.size()) return;  // grid sized by an upper bound (KeySrcD)
   }
@@ -193,20 +194,20 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   }
   // issue every load of the tile before using any (memory-level parallelism);
   // order inside a tile is irrelevant to a non-stable partition
-  KeyT k[kMsdIPT];
-  uint32_t v[kMsdIPT];
-  bool ok[kMsdIPT];
-  uint32_t kidx[NM == NM_POS ? kMsdIPT : 1];  // NM_POS: item positions (< 2^31: n < 2^31 per call)
+  KeyT k[IPT];
+  uint32_t v[IPT];
+  bool ok[IPT];
+  uint32_t kidx[NM == NM_POS ? IPT : 1];  // NM_POS: item positions (< 2^31: n < 2^31 per call)
   if constexpr (LEVEL == 1) {
-    load_items<Src, KeyT, kMsdIPT / 4>(src, base / 4 + tid, kMsdThreads, k, v, ok);
+    load_items<Src, KeyT, IPT / 4>(src, base / 4 + tid, kMsdThreads, k, v, ok);
   } else if constexpr (NM == NM_POS) {
     // 16-byte loads: lane takes items 4 lane .. 4 lane + 3 of each 128-item slice
-    const uint64_t wbase = base + (uint64_t)warp * 32 * kMsdIPT;
+    const uint64_t wbase = base + (uint64_t)warp * 32 * IPT;
     const uint64_t nn = src.size();
-    if (wbase + 32 * kMsdIPT <= nn) {
+    if (wbase + 32 * IPT <= nn) {
       const uint4* p = reinterpret_cast<const uint4*>(src.keys + wbase);
 #pragma unroll
-      for (int i = 0; i < kMsdIPT / 4; ++i) {
+      for (int i = 0; i < IPT / 4; ++i) {
         const uint4 x = p[i * 32 + lane];
         k[4 * i] = x.x, k[4 * i + 1] = x.y, k[4 * i + 2] = x.z, k[4 * i + 3] = x.w;
 #pragma unroll
@@ -218,20 +219,20 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < kMsdIPT; ++i) {
+      for (int i = 0; i < IPT; ++i) {
         kidx[i] = (uint32_t)wbase + (uint32_t)(i * 32 + lane);
         ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
       }
     }
   } else {
-    const uint64_t wbase = base + (uint64_t)warp * 32 * kMsdIPT;
+    const uint64_t wbase = base + (uint64_t)warp * 32 * IPT;
     if constexpr (sizeof(KeyT) == 8 && !HAS_VAL && std::is_same<Src, KeySrcD<KeyT, HAS_VAL>>::value) {
       // 16-byte loads: lane takes keys 2 lane, 2 lane + 1 of each 64-key slice
       const uint64_t nn = src.size();
-      if (wbase + 32 * kMsdIPT <= nn) {
+      if (wbase + 32 * IPT <= nn) {
         const ulonglong2* p = reinterpret_cast<const ulonglong2*>(src.keys + wbase);
 #pragma unroll
-        for (int i = 0; i < kMsdIPT / 2; ++i) {
+        for (int i = 0; i < IPT / 2; ++i) {
           const ulonglong2 x = p[i * 32 + lane];
           k[2 * i] = (KeyT)x.x;
           k[2 * i + 1] = (KeyT)x.y;
@@ -240,11 +241,11 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < kMsdIPT; ++i) ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
+        for (int i = 0; i < IPT; ++i) ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < kMsdIPT; ++i) ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
+      for (int i = 0; i < IPT; ++i) ok[i] = src.load(wbase + (uint64_t)i * 32 + lane, k[i], v[i]);
     }
   }
   __syncthreads();
@@ -253,10 +254,10 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   // shared memory as far as the compiler knows, so S.e1 / S.e2 would be reloaded per key
   const uint32_t e1 = NM == NM_POS ? (uint32_t)S.e1 : 0u, e2 = NM == NM_POS ? (uint32_t)S.e2 : 0u;
   const uint32_t dmask = (1u << dbits) - 1;
-  uint32_t rank[kMsdIPT];
-  int bin[kMsdIPT];
+  uint32_t rank[IPT];
+  int bin[IPT];
 #pragma unroll
-  for (int i = 0; i < kMsdIPT; ++i) {
+  for (int i = 0; i < IPT; ++i) {
     bin[i] = -1;
     if (ok[i]) {
       const uint32_t d = (uint32_t)((uint64_t)k[i] >> shift) & dmask;
@@ -295,10 +296,10 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   }
   if (warp_skewed(bin[0])) {
 #pragma unroll
-    for (int i = 0; i < kMsdIPT; ++i) rank[i] = agg_rank(S.cnt, bin[i]);
+    for (int i = 0; i < IPT; ++i) rank[i] = agg_rank(S.cnt, bin[i]);
   } else {
 #pragma unroll
-    for (int i = 0; i < kMsdIPT; ++i)
+    for (int i = 0; i < IPT; ++i)
       if (bin[i] >= 0) rank[i] = atomicAdd(&S.cnt[bin[i]], 1u);
   }
   __syncthreads();
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kMsdThreads, 5) msd_scatter_kernel(Src src, ui
   }
   smem_excl_scan<NBINS>(S.cnt, S.tstart, S.wt);
 #pragma unroll
-  for (int i = 0; i < kMsdIPT; ++i)
+  for (int i = 0; i < IPT; ++i)
     if (bin[i] >= 0) {
       const uint32_t at = S.tstart[bin[i]] + rank[i];
       S.stage[at] = k[i];
