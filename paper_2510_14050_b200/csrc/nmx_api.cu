@@ -858,9 +858,11 @@ uint64_t msd_partition(nmx_ctx* c, const Src& src, uint64_t n, int kb, int D, Ke
       c->spoffA.grow(((size_t)std::min<uint64_t>(nbl, n / (kSegCap + 1) + 1) + 8) * 4);
       seg_classify_enqueue(c, h2, nbl, c->spoffA.as<uint32_t>());
       c->dom_begin("msd_scatter");
+      NarrowArgs sw;
+      sw.big = c->stot.as<uint32_t>() + 1;  // SegTotals.big of the classification just queued
       launch_msd_scatter<KeySrcD<KeyT, HAS_VAL>, KeyT, HAS_VAL, 2, true>(
           c, dl[l], tiles_of(n, kMsdTile), ks, n, out_k, out_v, shift, bshift, c->scur.as<uint32_t>(),
-          reinterpret_cast<KeyT*>(split->hk), split->hv);
+          reinterpret_cast<KeyT*>(split->hk), split->hv, sw);
     } else {
       scan_counts(c, h2, nbl, off, cur);
       c->dom_begin("msd_scatter");
@@ -981,6 +983,7 @@ void msd_partition_cols_narrow(nmx_ctx* c, const ColConcatSrc& src, uint64_t n, 
   nw.npar = 1u << cum[1];
   nw.wout = reinterpret_cast<uint64_t*>(split->hk);
   nw.dlp = dl[1];
+  nw.big = c->stot.as<uint32_t>() + 1;
   tile_parents_kernel<<<tgrid, 256, 0, c->st>>>(off, nw.npar, gcount, ntiles, c->mtpar.as<uint4>(), kPosTile);
   CK_LAUNCH();
   c->dom_begin("msd_scatter");

@@ -119,6 +119,7 @@ struct NarrowArgs {
   uint32_t npar = 0;
   int delta = 0, cb = 0, dlp = 0;
   const uint4* tpar = nullptr;  // NM_POS: per tile {first parent, its end, the next parent's end, -}
+  const uint32_t* big = nullptr;  // SPLIT: items in heavy buckets (0: every tile takes the light-only loop)
 };
 __device__ __forceinline__ uint32_t narrow_item(uint64_t e, int delta, int cb) {
   return ((uint32_t)(e >> 32) & ((1u << delta) - 1u)) << cb | ((uint32_t)e - 1u);
@@ -178,6 +179,10 @@ __global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_ker
   if constexpr (LEVEL == 2) {
     if (base >= src.size()) return;  // grid sized by an upper bound (KeySrcD)
   }
+  // SPLIT without heavy buckets (the classification ran before this launch): every
+  // cursor carries the light bit and the output loop needs no per-item light / heavy
+  // branch. Loaded first so that its latency hides behind the tile's loads.
+  const bool light_only = SPLIT && nw.big && *nw.big == 0;
   for (int i = tid; i < NBINS; i += kMsdThreads) S.cnt[i] = 0;
   if (LEVEL == 2 && tid == 0) {
     if constexpr (NM == NM_POS) {  // positions < 2^31: 0xFFFFFFFF = no such parent
@@ -338,6 +343,26 @@ __global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_ker
   const uint32_t total = S.tstart[nbins - 1] + S.cnt[nbins - 1];
   // NM_POS: staged items are parent-major, so the second parent's start the same
   const uint32_t rel1 = NM == NM_POS ? S.tstart[1 << dbits] : 0u;
+  if (light_only) {
+    for (uint32_t j = tid; j < total; j += kMsdThreads) {
+      const KeyT key = S.stage[j];
+      int b;
+      if (LEVEL == 1) {
+        b = (int)((uint32_t)((uint64_t)key >> shift) & dmask);
+      } else if constexpr (NM == NM_POS) {
+        b = (int)(((j >= rel1 ? 1u : 0u) << dbits) | ((uint32_t)key >> shift & dmask));
+      } else {
+        b = (int)(((((uint64_t)key >> bshift) - b1first) << dbits) | (((uint64_t)key >> shift) & dmask));
+      }
+      const uint32_t pos = (S.gbase[b] + j) & ~kLightBit;
+      if constexpr (NM == NM_OUT)
+        nw.nout[pos] = narrow_item((uint64_t)key, nw.delta, nw.cb);
+      else
+        out[pos] = key;
+      if (HAS_VAL) vout[pos] = S.vstage[j];
+    }
+    return;
+  }
   for (uint32_t j = tid; j < total; j += kMsdThreads) {
     const KeyT key = S.stage[j];
     int b;
