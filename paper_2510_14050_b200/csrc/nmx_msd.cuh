@@ -160,7 +160,7 @@ __global__ void tile_parents_kernel(const uint32_t* __restrict__ poff, uint32_t 
 constexpr uint32_t kLightBit = 0x80000000u;
 // LB: digit-bit capacity (7, or 8 for the levels that save a whole level)
 template <typename Src, typename KeyT, bool HAS_VAL, int LEVEL, bool SPLIT = false, int LB = kMsdLevelBits,
-          int NM = NM_NONE, int IPT = kMsdIPT>
+          int NM = NM_NONE, int IPT = kMsdIPT, bool HI = false>
 __global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_kernel(Src src, uint64_t n_items, KeyT* __restrict__ out,
                                                                    uint32_t* __restrict__ vout, int shift, int dbits,
                                                                    int bshift, uint32_t* __restrict__ cursor,
@@ -259,13 +259,29 @@ __global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_ker
   // shared memory as far as the compiler knows, so S.e1 / S.e2 would be reloaded per key
   const uint32_t e1 = NM == NM_POS ? (uint32_t)S.e1 : 0u, e2 = NM == NM_POS ? (uint32_t)S.e2 : 0u;
   const uint32_t dmask = (1u << dbits) - 1;
+  // HI: u64 keys whose digit and parent fields lie in the high word (shift, bshift >= 32:
+  // row keys and column items at b = 32) -- 32-bit shifts instead of 64-bit ones
+  const int hs = HI ? shift - 32 : shift, hb = HI ? bshift - 32 : bshift;
+  auto digit = [&](KeyT key) -> uint32_t {
+    if constexpr (HI)
+      return ((uint32_t)((uint64_t)key >> 32) >> hs) & dmask;
+    else
+      return (uint32_t)((uint64_t)key >> shift) & dmask;
+  };
+  // parent relative to the tile's first (< 2 for the binned ones; (key >> bshift) has <= 24 bits)
+  auto parent_rel = [&](KeyT key) -> uint32_t {
+    if constexpr (HI)
+      return ((uint32_t)((uint64_t)key >> 32) >> hb) - (uint32_t)b1first;
+    else
+      return (uint32_t)(((uint64_t)key >> bshift) - b1first);
+  };
   uint32_t rank[IPT];
   int bin[IPT];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     bin[i] = -1;
     if (ok[i]) {
-      const uint32_t d = (uint32_t)((uint64_t)k[i] >> shift) & dmask;
+      const uint32_t d = digit(k[i]);
       if (LEVEL == 1) {
         bin[i] = (int)d;
       } else if constexpr (NM == NM_POS) {
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_ker
           }
         }
       } else {
-        const uint64_t rel = ((uint64_t)k[i] >> bshift) - b1first;
+        const uint32_t rel = parent_rel(k[i]);
         if (rel < 2) {
           bin[i] = (int)((rel << dbits) | d);
         } else {  // third+ level-1 bucket inside one tile: direct placement
@@ -348,11 +364,11 @@ __global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_ker
       const KeyT key = S.stage[j];
       int b;
       if (LEVEL == 1) {
-        b = (int)((uint32_t)((uint64_t)key >> shift) & dmask);
+        b = (int)digit(key);
       } else if constexpr (NM == NM_POS) {
         b = (int)(((j >= rel1 ? 1u : 0u) << dbits) | ((uint32_t)key >> shift & dmask));
       } else {
-        b = (int)(((((uint64_t)key >> bshift) - b1first) << dbits) | (((uint64_t)key >> shift) & dmask));
+        b = (int)((parent_rel(key) << dbits) | digit(key));
       }
       const uint32_t pos = (S.gbase[b] + j) & ~kLightBit;
       if constexpr (NM == NM_OUT)
@@ -368,12 +384,12 @@ __global__ void __launch_bounds__(kMsdThreads, IPT == 8 ? 5 : 3) msd_scatter_ker
     int b;
     uint32_t rel = 0;
     if (LEVEL == 1) {
-      b = (int)((uint32_t)((uint64_t)key >> shift) & dmask);
+      b = (int)digit(key);
     } else if constexpr (NM == NM_POS) {
       rel = j >= rel1 ? 1u : 0u;
       b = (int)((rel << dbits) | ((uint32_t)key >> shift & dmask));
     } else {
-      b = (int)(((((uint64_t)key >> bshift) - b1first) << dbits) | (((uint64_t)key >> shift) & dmask));
+      b = (int)((parent_rel(key) << dbits) | digit(key));
     }
     const uint32_t g = S.gbase[b];
     if (!SPLIT || (g & kLightBit)) {
